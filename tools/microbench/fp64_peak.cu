@@ -1,0 +1,68 @@
+// FP64 throughput probe for B200 (sm_100a): vector DFMA vs DMMA (mma.sync m8n8k4 f64).
+// Gives the FP64 roofline denominator that MEASURED_PEAKS.json does not carry.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void dfma_kernel(double* out, int iters, double a, double b) {
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = fma(x[i], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += x[i];
+    if (s == 12345.678) out[0] = s;
+}
+
+__global__ void dmma_kernel(double* out, int iters) {
+    double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { c[i][0] = 0; c[i][1] = 0; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    if (s == 12345.678) out[0] = s;
+}
+
+int main() {
+    double* d; cudaMalloc(&d, 8);
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int l2; cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, 0);
+    printf("SMs %d L2 %d bytes\n", sms, l2);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int threads : {128, 256, 512, 1024}) {
+        int blocks = sms * (2048 / threads);
+        int iters = 4096;
+        dfma_kernel<<<blocks, threads>>>(d, 16, 1.0000001, 1e-9);
+        cudaEventRecord(e0);
+        dfma_kernel<<<blocks, threads>>>(d, iters, 1.0000001, 1e-9);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        double flops = 2.0 * 16 * iters * (double)blocks * threads;
+        printf("DFMA threads/blk %d: %.2f TFLOP/s (%.3f ms)\n", threads, flops / ms / 1e9, ms);
+    }
+    for (int threads : {128, 256, 512, 1024}) {
+        int blocks = sms * (2048 / threads);
+        int iters = 2048;
+        dmma_kernel<<<blocks, threads>>>(d, 16);
+        cudaEventRecord(e0);
+        dmma_kernel<<<blocks, threads>>>(d, iters);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        double flops = 2.0 * 256 * 8 * iters * (double)blocks * (threads / 32);
+        printf("DMMA threads/blk %d: %.2f TFLOP/s (%.3f ms)\n", threads, flops / ms / 1e9, ms);
+    }
+    printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
