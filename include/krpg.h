@@ -1,0 +1,127 @@
+/* krpg — B200-native exact Khatri-Rao-product leverage-score sampler (C ABI).
+ *
+ * This is the drop-in boundary beneath the reference's C++ KrpSampler API
+ * (/root/reference/proj/include/krplev/krp_sampler.hpp). Every entry point is
+ * plain C: handles, raw pointers and sizes, no torch / C++ types. All state
+ * (factors, segment trees, scratch) lives in HBM on one device; host buffers
+ * passed in or out are row-major fp64 like krplev::Matrix (matrix.hpp:13-48).
+ *
+ * Return codes mirror the reference's exception classes so a C++ wrapper can
+ * rethrow the same types:
+ *   KRPG_OK (0), KRPG_INVALID_ARGUMENT (1) -> std::invalid_argument,
+ *   KRPG_RUNTIME_ERROR (2) -> std::runtime_error, KRPG_CUDA_ERROR (3).
+ * krpg_last_error() returns the thread-local message of the last failure.
+ *
+ * Threading: create / update_* / destroy need exclusive access to a handle;
+ * sample / conditional / *_gram may be called concurrently (each call is
+ * serialised on the handle's stream internally).
+ */
+#ifndef KRPG_H
+#define KRPG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KRPG_OK 0
+#define KRPG_INVALID_ARGUMENT 1
+#define KRPG_RUNTIME_ERROR 2
+#define KRPG_CUDA_ERROR 3
+
+/* SampleBatch::kExcluded, krp_sampler.hpp:28 */
+#define KRPG_EXCLUDED 0xFFFFFFFFu
+
+/* factor storage precision on device (fp64 arithmetic either way) */
+#define KRPG_STORE_F64 0u
+#define KRPG_STORE_F32 1u
+
+/* sampling modes */
+#define KRPG_MODE_TWO_STAGE 0u /* bit-exact to KrpSampler::sample (krp_sampler.cpp:82-151) */
+#define KRPG_MODE_ONE_STAGE 1u /* M = G+ o hh^T o G_{>k} per draw (SURVEY §8(c) chain) */
+
+typedef struct krpg_sampler* krpg_t;
+
+const char* krpg_last_error(void);
+/* 1 if a CUDA device is usable (never falls back to the CPU otherwise). */
+int krpg_device_count(void);
+
+/* Replaces KrpSampler::KrpSampler(std::vector<Matrix>)  (krp_sampler.cpp:41-62).
+ * factors[k] is an I[k] x R row-major fp64 host matrix. storage selects the
+ * device copy precision (KRPG_STORE_F32 rounds each entry to fp32 once). */
+int krpg_create(const double* const* factors, const uint64_t* I, uint32_t N, uint32_t R,
+                uint32_t storage, int device, krpg_t* out);
+/* Same, with factors already resident on `device` (row-major, storage dtype). */
+int krpg_create_device(const void* const* dev_factors, const uint64_t* I, uint32_t N,
+                       uint32_t R, uint32_t storage, int device, krpg_t* out);
+int krpg_destroy(krpg_t h);
+
+int krpg_info(krpg_t h, uint32_t* N, uint32_t* R, uint64_t* I /* N entries, nullable */);
+
+/* Replaces KrpSampler::factor_gram(j) (krp_sampler.hpp:66): R x R, taken from
+ * the segment-tree root (the device sum of all leaf Grams). */
+int krpg_factor_gram(krpg_t h, uint32_t j, double* out);
+/* Copy of factor j as stored on device, up-cast to fp64 (I x R). */
+int krpg_factor(krpg_t h, uint32_t j, double* out);
+
+/* Tree introspection (SegmentTreeSampler test support, segment_tree_sampler.hpp:64-95).
+ * The device stores the reference's compact layout: slot 0 = root, slot s>=1 =
+ * heap node 2s-1 (left children), each a packed upper triangle (hpp:111-115). */
+int krpg_tree_shape(krpg_t h, uint32_t j, uint64_t* leaf_count, uint64_t* node_count);
+/* unpacked R x R Gram of a stored node (root or odd heap id) */
+int krpg_node_gram(krpg_t h, uint32_t j, uint64_t node, double* out);
+/* all L stored packed Grams, slot order (L x R(R+1)/2) */
+int krpg_tree_grams(krpg_t h, uint32_t j, double* out);
+
+/* Replaces KrpSampler::sample(excluded, J, seed) (krp_sampler.cpp:82-151).
+ * excluded < 0 means none. Host outputs (each nullable): idx J x N (excluded
+ * column = KRPG_EXCLUDED), prob J, rows J x R. draw_offset shifts the CounterRng
+ * stream ids (stream = draw_offset + d) so J can be sharded across devices with
+ * results identical to one big call. margin (nullable, J): per draw the smallest
+ * |cutoff - u| over all branch/scan comparisons (boundary-draw accounting). */
+int krpg_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t draw_offset,
+                uint32_t mode, uint32_t* idx, double* prob, double* rows, double* margin);
+/* Same with device output pointers on the handle's device (any nullable);
+ * stream 0 = the handle's own stream. Does not synchronise the host unless an
+ * error check needs it (see krpg_sync). */
+int krpg_sample_device(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed,
+                       uint64_t draw_offset, uint32_t mode, uint32_t* d_idx, double* d_prob,
+                       double* d_rows, double* d_margin);
+int krpg_sync(krpg_t h);
+/* The handle's CUDA stream (cudaStream_t) for event timing by callers. */
+void* krpg_stream(krpg_t h);
+
+/* Replaces KrpSampler::conditional(excluded, k, h) (krp_sampler.cpp:153-196).
+ * probs: I_k, mixture: R. */
+int krpg_conditional(krpg_t h, int64_t excluded, uint32_t k, const double* hist, double* probs,
+                     double* mixture);
+
+/* Replaces KrpSampler::update_factor(j, U) (krp_sampler.cpp:198-205): full device rebuild. */
+int krpg_update_factor(krpg_t h, uint32_t j, const double* U, uint64_t I);
+/* Replaces a sequence of KrpSampler::update_factor_entry(j, r[i], c[i], v[i])
+ * (krp_sampler.cpp:207-228) applied in order: all entries are validated first,
+ * then each touched row's net change u'u'^T - uu^T is patched into every stored
+ * node on its root-leaf path (segment_tree_sampler.cpp:358-409 semantics). */
+int krpg_update_entries(krpg_t h, uint32_t j, const uint64_t* r, const uint32_t* c,
+                        const double* v, uint64_t n);
+
+/* Replaces KrpSampler::validate(tol) (krp_sampler.cpp:230-245), but with a
+ * relative tolerance: root Gram vs a fresh device Gram, entrywise
+ * |a-b| <= tol * sqrt(G_aa G_bb). */
+int krpg_validate(krpg_t h, double tol);
+
+/* STS-CP gather (cp_als.cpp:284-289, sketch.cpp:36-52) on device buffers:
+ * w_d = 1/sqrt(J q_d); SA[d,:] = w_d * rows[d,:]. Fails (invalid argument) if
+ * any q_d <= 0 or non-finite. */
+int krpg_gather_sa_device(krpg_t h, uint64_t J, const double* d_prob, const double* d_rows,
+                          double* d_weights, double* d_sa);
+
+/* Timing of the last tree build (ms, device events) for the bench. */
+int krpg_last_build_ms(krpg_t h, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

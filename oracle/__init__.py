@@ -174,7 +174,7 @@ class OracleKrp:
         self.b.check(self._name("krp_factor_gram", "factor_gram")(self.h, _u32(j), _dptr(out)))
         return out
 
-    def sample(self, excluded, J, seed, one_stage=False, want_margin=False):
+    def sample(self, excluded, J, seed, one_stage=False, want_margin=False, draw_offset=0):
         e = -1 if excluded is None else int(excluded)
         idx = np.empty((J, self.N), dtype=np.uint32)
         prob = np.empty(J)
@@ -183,10 +183,13 @@ class OracleKrp:
                 _dptr(prob), _dptr(rows)]
         margin = None
         if self.b.kind == "port":
+            args.insert(4, _u64(draw_offset))
             margin = np.empty(J)
             args.append(_dptr(margin) if want_margin else None)
             f = self.b.fn("krp_sample_one_stage" if one_stage else "krp_sample")
         else:
+            if draw_offset:
+                raise ValueError("the reference has no draw offset")
             f = self.b.fn("sample_one_stage" if one_stage else "sample")
         self.b.check(f(*args))
         if want_margin:

@@ -591,8 +591,9 @@ static void downstream_gram(const ko_krp* s, const uint32_t* inc, uint32_t ninc,
     for (uint32_t p = pos + 1; p < ninc; ++p) hadamard_into(out, s->G[inc[p]], (size_t)R * R);
 }
 
-int ko_krp_sample(const ko_krp* s, int64_t excluded, uint64_t J, uint64_t seed, uint32_t* idx,
-                  double* prob, double* rows, double* margin) { /* :82-151 */
+int ko_krp_sample(const ko_krp* s, int64_t excluded, uint64_t J, uint64_t seed,
+                  uint64_t draw_offset, uint32_t* idx, double* prob, double* rows,
+                  double* margin) { /* :82-151; stream = draw_offset + d (0 = reference) */
     if (J < 1) return fail(1, "KrpSample: sample count must be positive");
     const uint32_t N = s->N, R = s->R;
     uint32_t inc[64], ninc;
@@ -611,7 +612,7 @@ int ko_krp_sample(const ko_krp* s, int64_t excluded, uint64_t J, uint64_t seed, 
     if (margin)
         for (uint64_t d = 0; d < J; ++d) margin[d] = INFINITY;
     rng_t* rngs = malloc(sizeof(rng_t) * J);
-    for (uint64_t d = 0; d < J; ++d) rng_init(&rngs[d], seed, d);
+    for (uint64_t d = 0; d < J; ++d) rng_init(&rngs[d], seed, draw_offset + d);
 
     double* gk = malloc(sizeof(double) * R * R);
     double* V = malloc(sizeof(double) * R * R);
@@ -672,7 +673,8 @@ int ko_krp_sample(const ko_krp* s, int64_t excluded, uint64_t J, uint64_t seed, 
 }
 
 int ko_krp_sample_one_stage(const ko_krp* s, int64_t excluded, uint64_t J, uint64_t seed,
-                            uint32_t* idx, double* prob, double* rows, double* margin) {
+                            uint64_t draw_offset, uint32_t* idx, double* prob, double* rows,
+                            double* margin) {
     if (J < 1) return fail(1, "KrpSample: sample count must be positive");
     const uint32_t N = s->N, R = s->R;
     uint32_t inc[64], ninc;
@@ -691,7 +693,7 @@ int ko_krp_sample_one_stage(const ko_krp* s, int64_t excluded, uint64_t J, uint6
     if (margin)
         for (uint64_t d = 0; d < J; ++d) margin[d] = INFINITY;
     rng_t* rngs = malloc(sizeof(rng_t) * J);
-    for (uint64_t d = 0; d < J; ++d) rng_init(&rngs[d], seed, d);
+    for (uint64_t d = 0; d < J; ++d) rng_init(&rngs[d], seed, draw_offset + d);
     double* Y = malloc(sizeof(double) * R * R);
     volatile int err = 0;
     for (uint32_t pos = 0; pos < ninc; ++pos) {

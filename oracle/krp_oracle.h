@@ -57,11 +57,12 @@ const double* ko_krp_node_packed(const ko_krp* k, uint32_t j, uint64_t node);
 uint64_t ko_krp_leaf_count(const ko_krp* k, uint32_t j);
 /* two-stage sample, krp_sampler.cpp:82-151. margin (nullable, J): per draw the
  * smallest |cutoff - d| over every branch/scan comparison made. */
-int ko_krp_sample(const ko_krp* k, int64_t excluded, uint64_t J, uint64_t seed, uint32_t* idx,
-                  double* prob, double* rows, double* margin);
+int ko_krp_sample(const ko_krp* k, int64_t excluded, uint64_t J, uint64_t seed,
+                  uint64_t draw_offset, uint32_t* idx, double* prob, double* rows, double* margin);
 /* one-stage chain */
 int ko_krp_sample_one_stage(const ko_krp* k, int64_t excluded, uint64_t J, uint64_t seed,
-                            uint32_t* idx, double* prob, double* rows, double* margin);
+                            uint64_t draw_offset, uint32_t* idx, double* prob, double* rows,
+                            double* margin);
 int ko_krp_conditional(const ko_krp* k, int64_t excluded, uint32_t kk, const double* h,
                        double* probs, double* mixture);
 int ko_krp_update_factor(ko_krp* k, uint32_t j, const double* U, uint64_t I);

@@ -1,0 +1,113 @@
+"""ctypes binding of libkrpg.so (the C ABI declared in include/krpg.h).
+
+The shared library is built in-tree (``lib/libkrpg.so``) by :func:`build`.
+There is no fallback: if the library or a CUDA device is missing, every call
+fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB_PATH = os.path.join(PKG, "lib", "libkrpg.so")
+HEADER = os.path.join(ROOT, "include", "krpg.h")
+
+KRPG_OK = 0
+KRPG_INVALID_ARGUMENT = 1
+KRPG_RUNTIME_ERROR = 2
+KRPG_CUDA_ERROR = 3
+EXCLUDED = 0xFFFFFFFF
+STORE_F64, STORE_F32 = 0, 1
+MODE_TWO_STAGE, MODE_ONE_STAGE = 0, 1
+
+
+class KrpgError(RuntimeError):
+    """std::runtime_error analogue (reference: degenerate draws, zero KRP)."""
+
+
+class KrpgInvalidArgument(KrpgError, ValueError):
+    """std::invalid_argument analogue (bad shapes, indices, values)."""
+
+
+class KrpgCudaError(KrpgError):
+    pass
+
+
+def build(force: bool = False, quiet: bool = True) -> str:
+    """Compile libkrpg.so for sm_100a (nvcc cross-compiles without a GPU)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-C", os.path.join(PKG, "csrc"), "-j8"], check=True,
+                       stdout=subprocess.DEVNULL if quiet else None)
+    else:
+        subprocess.run(["make", "-C", os.path.join(PKG, "csrc"), "-j8"], check=True,
+                       stdout=subprocess.DEVNULL if quiet else None)
+    return LIB_PATH
+
+
+_u32, _u64, _i64, _int = C.c_uint32, C.c_uint64, C.c_int64, C.c_int
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+_SIGS = {
+    "krpg_last_error": ([], C.c_char_p),
+    "krpg_device_count": ([], _int),
+    "krpg_create": ([C.POINTER(_dp), C.POINTER(_u64), _u32, _u32, _u32, _int, C.POINTER(_vp)], _int),
+    "krpg_create_device": ([C.POINTER(_vp), C.POINTER(_u64), _u32, _u32, _u32, _int, C.POINTER(_vp)], _int),
+    "krpg_destroy": ([_vp], _int),
+    "krpg_info": ([_vp, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u64)], _int),
+    "krpg_factor_gram": ([_vp, _u32, _dp], _int),
+    "krpg_factor": ([_vp, _u32, _dp], _int),
+    "krpg_tree_shape": ([_vp, _u32, C.POINTER(_u64), C.POINTER(_u64)], _int),
+    "krpg_node_gram": ([_vp, _u32, _u64, _dp], _int),
+    "krpg_tree_grams": ([_vp, _u32, _dp], _int),
+    "krpg_sample": ([_vp, _i64, _u64, _u64, _u64, _u32, C.POINTER(_u32), _dp, _dp, _dp], _int),
+    "krpg_sample_device": ([_vp, _i64, _u64, _u64, _u64, _u32, _vp, _vp, _vp, _vp], _int),
+    "krpg_sync": ([_vp], _int),
+    "krpg_stream": ([_vp], _vp),
+    "krpg_conditional": ([_vp, _i64, _u32, _dp, _dp, _dp], _int),
+    "krpg_update_factor": ([_vp, _u32, _dp, _u64], _int),
+    "krpg_update_entries": ([_vp, _u32, C.POINTER(_u64), C.POINTER(_u32), _dp, _u64], _int),
+    "krpg_validate": ([_vp, C.c_double], _int),
+    "krpg_gather_sa_device": ([_vp, _u64, _vp, _vp, _vp, _vp], _int),
+    "krpg_last_build_ms": ([_vp, C.POINTER(C.c_float)], _int),
+}
+
+_lib: C.CDLL | None = None
+
+
+def lib() -> C.CDLL:
+    """Load libkrpg.so (raises if it was never built — no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: the CUDA extension is not built "
+                "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
+        l = C.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            f = getattr(l, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = l
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == KRPG_OK:
+        return
+    msg = lib().krpg_last_error().decode()
+    if rc == KRPG_INVALID_ARGUMENT:
+        raise KrpgInvalidArgument(msg)
+    if rc == KRPG_CUDA_ERROR:
+        raise KrpgCudaError(msg)
+    raise KrpgError(msg)
+
+
+def declared_symbols() -> list[str]:
+    """Entry points declared in include/krpg.h (for the ABI export test)."""
+    import re
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(krpg_[a-z_0-9]+)\s*\(", text)))

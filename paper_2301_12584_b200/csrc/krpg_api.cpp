@@ -1,0 +1,672 @@
+// C-ABI layer of the B200 KRP leverage sampler (include/krpg.h).
+//
+// Host orchestration only: argument validation with the reference's error
+// classes and messages (krp_sampler.cpp:13-15, 41-72, 84-95), the R x R setup
+// math per sample call (Hadamard of Grams, pseudo-inverse, eigendecompositions
+// of G_{>k}, krp_sampler.cpp:89-123), device memory ownership, and kernel
+// launches on the handle's stream. There is no CPU execution path for any
+// per-row or per-draw work: without a CUDA device every entry point fails.
+#include "krpg.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <future>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "host_linalg.hpp"
+#include "krpg_device.cuh"
+#include "krpg_kernels.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+    } while (0)
+
+void require(bool c, const char* msg) {
+    if (!c) throw std::invalid_argument(msg);
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return KRPG_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return KRPG_INVALID_ARGUMENT;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return KRPG_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return KRPG_RUNTIME_ERROR;
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* ensure(size_t n) {
+        if (n > bytes) {
+            if (p) CK(cudaFree(p));
+            p = nullptr;
+            bytes = 0;
+            CK(cudaMalloc(&p, n));
+            bytes = n;
+        }
+        return p;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct PinBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* ensure(size_t n) {
+        if (n > bytes) {
+            if (p) CK(cudaFreeHost(p));
+            p = nullptr;
+            bytes = 0;
+            CK(cudaMallocHost(&p, n));
+            bytes = n;
+        }
+        return p;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct Factor {
+    uint64_t I = 0;
+    DevBuf U;     // I x R (storage dtype)
+    DevBuf tree;  // L x P compact
+    std::vector<double> G;  // host copy of the root Gram (R x R)
+};
+
+}  // namespace
+
+struct krpg_sampler {
+    int device = 0;
+    uint32_t N = 0, R = 0, storage = 0;
+    uint64_t P = 0;
+    std::vector<Factor> f;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    float last_build_ms = 0.f;
+    std::mutex mu;
+    DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf;
+    PinBuf up, errh;
+
+    size_t elt() const { return storage == KRPG_STORE_F32 ? 4 : 8; }
+
+    void set_device() const { CK(cudaSetDevice(device)); }
+
+    void build_tree(uint32_t k) {
+        Factor& F = f[k];
+        const krpg::Topo t = krpg::make_topo(F.I, R);
+        F.tree.ensure(sizeof(double) * t.L * P);
+        uint64_t na, nb;
+        krpg::tree_transient_doubles(F.I, R, &na, &nb);
+        double* base = static_cast<double*>(tbuf.ensure(sizeof(double) * (na + nb) + 16));
+        krpg::TreeBuildArgs a{};
+        a.U = F.U.p;
+        a.storage = storage;
+        a.I = F.I;
+        a.R = R;
+        a.compact = F.tree.as<double>();
+        a.tbuf_a = base;
+        a.tbuf_b = base + na;
+        a.stream = stream;
+        a.force_generic = 0;
+        CK(cudaEventRecord(ev0, stream));
+        krpg::launch_tree_build(a);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ev1, stream));
+        std::vector<double> root(P);
+        CK(cudaMemcpyAsync(root.data(), F.tree.p, sizeof(double) * P, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        CK(cudaEventElapsedTime(&last_build_ms, ev0, ev1));
+        F.G.assign(size_t(R) * R, 0.0);
+        krpg::unpack_upper(root.data(), R, F.G.data());
+    }
+
+    void upload_factor(uint32_t k, const double* host, uint64_t I) {
+        Factor& F = f[k];
+        F.I = I;
+        F.U.ensure(elt() * I * R);
+        if (storage == KRPG_STORE_F32) {
+            std::vector<float> tmp(I * R);
+            for (uint64_t e = 0; e < I * R; ++e) tmp[e] = static_cast<float>(host[e]);
+            CK(cudaMemcpyAsync(F.U.p, tmp.data(), 4 * I * R, cudaMemcpyHostToDevice, stream));
+            CK(cudaStreamSynchronize(stream));
+        } else {
+            CK(cudaMemcpyAsync(F.U.p, host, 8 * I * R, cudaMemcpyHostToDevice, stream));
+            CK(cudaStreamSynchronize(stream));
+        }
+    }
+
+    std::vector<uint32_t> included(int64_t excluded) const {  // krp_sampler.cpp:64-72
+        if (excluded >= 0) require(uint64_t(excluded) < N, "KrpSampler: excluded index out of range");
+        std::vector<uint32_t> inc;
+        for (uint32_t k = 0; k < N; ++k)
+            if (excluded < 0 || uint32_t(excluded) != k) inc.push_back(k);
+        require(!inc.empty(), "KrpSampler: no factors left after exclusion");
+        return inc;
+    }
+
+    std::vector<double> hadamard_of(const std::vector<uint32_t>& ks) const {
+        std::vector<double> G(size_t(R) * R, 1.0);
+        for (uint32_t k : ks) krpg::hadamard_into(G, f[k].G.data());
+        return G;
+    }
+
+    void check_zero_krp() const {  // krp_sampler.cpp:55-61
+        std::vector<uint32_t> all(N);
+        for (uint32_t k = 0; k < N; ++k) all[k] = k;
+        const std::vector<double> G = hadamard_of(all);
+        double tr = 0.0;
+        for (uint32_t r = 0; r < R; ++r) tr += G[size_t(r) * R + r];
+        require(tr > 0.0, "KrpSampler: Khatri-Rao product is identically zero");
+    }
+
+    void sample_device(int64_t excluded, uint64_t J, uint64_t seed, uint64_t off, uint32_t mode,
+                       uint32_t* d_idx, double* d_prob, double* d_rows, double* d_margin) {
+        require(J >= 1, "KrpSample: sample count must be positive");
+        require(mode == KRPG_MODE_TWO_STAGE || mode == KRPG_MODE_ONE_STAGE, "krpg_sample: unknown mode");
+        const std::vector<uint32_t> inc = included(excluded);
+        const size_t RR = size_t(R) * R;
+
+        // ---- R x R setup (krp_sampler.cpp:89-96, 115-122) ----
+        const std::vector<double> G = hadamard_of(inc);
+        const krpg::Eig ge = krpg::eigh_psd(G.data(), R);
+        const size_t rank = krpg::numerical_rank(ge);
+        if (rank == 0) throw std::runtime_error("KRPSample: Khatri-Rao product of included factors is zero");
+        const std::vector<double> gp = krpg::pinv_from_eigen(ge);
+
+        const size_t npos = inc.size();
+        std::vector<std::vector<double>> Y(npos);
+        for (size_t p = 0; p < npos; ++p) {  // downstream_gram :74-80
+            Y[p].assign(RR, 1.0);
+            krpg::hadamard_into(Y[p], gp.data());
+            for (size_t q = p + 1; q < npos; ++q) krpg::hadamard_into(Y[p], f[inc[q]].G.data());
+        }
+        std::vector<krpg::Eig> ye(npos);
+        if (mode == KRPG_MODE_TWO_STAGE) {
+            std::vector<std::future<krpg::Eig>> fut;
+            for (size_t p = 0; p < npos; ++p)
+                fut.push_back(std::async(std::launch::async, [&, p] { return krpg::eigh_psd(Y[p].data(), R); }));
+            for (size_t p = 0; p < npos; ++p) ye[p] = fut[p].get();
+        }
+
+        // ---- one upload of the small per-call operands ----
+        const size_t per_pos = mode == KRPG_MODE_TWO_STAGE ? RR + R : P;
+        const size_t nd = P + npos * per_pos;
+        double* up_h = static_cast<double*>(up.ensure(sizeof(double) * nd));
+        {
+            const std::vector<double> gpp = krpg::pack_upper(gp.data(), R);
+            std::memcpy(up_h, gpp.data(), sizeof(double) * P);
+            for (size_t p = 0; p < npos; ++p) {
+                double* dst = up_h + P + p * per_pos;
+                if (mode == KRPG_MODE_TWO_STAGE) {
+                    std::memcpy(dst, ye[p].vectors.data(), sizeof(double) * RR);
+                    std::memcpy(dst + RR, ye[p].values.data(), sizeof(double) * R);
+                } else {
+                    const std::vector<double> yp = krpg::pack_upper(Y[p].data(), R);
+                    std::memcpy(dst, yp.data(), sizeof(double) * P);
+                }
+            }
+        }
+        double* dsmall = static_cast<double*>(small.ensure(sizeof(double) * nd));
+        CK(cudaMemcpyAsync(dsmall, up_h, sizeof(double) * nd, cudaMemcpyHostToDevice, stream));
+
+        double* H = d_rows ? d_rows : static_cast<double*>(sH.ensure(sizeof(double) * J * R));
+        int* derr = static_cast<int*>(err.ensure(sizeof(int)));
+        CK(cudaMemsetAsync(derr, 0, sizeof(int), stream));
+        if (d_idx && excluded >= 0) krpg::launch_set_excluded_column(d_idx, J, N, uint32_t(excluded), stream);
+        double* dQ = mode == KRPG_MODE_TWO_STAGE ? static_cast<double*>(Q.ensure(sizeof(double) * R * P)) : nullptr;
+
+        for (size_t p = 0; p < npos; ++p) {
+            const uint32_t k = inc[p];
+            const double* blk = dsmall + P + p * per_pos;
+            krpg::DrawArgs a{};
+            a.R = R;
+            a.N = N;
+            a.k = k;
+            a.pos = uint32_t(p);
+            a.mode = mode;
+            a.J = J;
+            a.seed = seed;
+            a.draw_offset = off;
+            a.H = H;
+            a.idx = d_idx;
+            a.margin = d_margin;
+            a.Z = f[k].tree.as<double>();
+            a.U = f[k].U.p;
+            a.storage = storage;
+            a.I = f[k].I;
+            a.err = derr;
+            a.stream = stream;
+            if (mode == KRPG_MODE_TWO_STAGE) {
+                krpg::launch_etree_build(blk, blk + RR, f[k].tree.as<double>(), R, dQ, stream);
+                a.Q = dQ;
+                a.V = blk;
+            } else {
+                a.Y = blk;
+            }
+            krpg::launch_draws(a);
+        }
+        if (d_prob) krpg::launch_probabilities(H, dsmall, R, J, double(rank), d_prob, stream);
+        CK(cudaGetLastError());
+        int* eh = static_cast<int*>(errh.ensure(sizeof(int)));
+        CK(cudaMemcpyAsync(eh, derr, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (*eh) throw std::runtime_error("row_sample: degenerate distribution (C <= 0)");
+    }
+};
+
+extern "C" {
+
+const char* krpg_last_error(void) { return g_err.c_str(); }
+
+int krpg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+static void validate_shapes(const uint64_t* I, uint32_t N, uint32_t R, uint32_t storage) {
+    require(N >= 1, "KrpSampler: factor list is empty");
+    require(R >= 1, "KrpSampler: empty factor");
+    for (uint32_t k = 0; k < N; ++k) require(I[k] >= 1, "KrpSampler: empty factor");
+    require(R <= 256, "krpg: rank above 256 is not supported on device");
+    require(storage == KRPG_STORE_F64 || storage == KRPG_STORE_F32, "krpg: unknown storage type");
+}
+
+int krpg_create(const double* const* factors, const uint64_t* I, uint32_t N, uint32_t R, uint32_t storage,
+                int device, krpg_t* out) {
+    return guard([&] {
+        *out = nullptr;
+        validate_shapes(I, N, R, storage);
+        for (uint32_t k = 0; k < N; ++k)
+            for (uint64_t e = 0; e < I[k] * R; ++e)
+                require(std::isfinite(factors[k][e]), "KrpSampler: non-finite factor entries");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, "krpg: no such CUDA device");
+        auto* h = new krpg_sampler();
+        try {
+            h->device = device;
+            h->N = N;
+            h->R = R;
+            h->storage = storage;
+            h->P = uint64_t(R) * (R + 1) / 2;
+            h->set_device();
+            CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            CK(cudaEventCreate(&h->ev0));
+            CK(cudaEventCreate(&h->ev1));
+            h->f.resize(N);
+            for (uint32_t k = 0; k < N; ++k) {
+                h->upload_factor(k, factors[k], I[k]);
+                h->build_tree(k);
+            }
+            h->check_zero_krp();
+        } catch (...) {
+            krpg_destroy(h);
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int krpg_create_device(const void* const* dev_factors, const uint64_t* I, uint32_t N, uint32_t R,
+                       uint32_t storage, int device, krpg_t* out) {
+    return guard([&] {
+        *out = nullptr;
+        validate_shapes(I, N, R, storage);
+        auto* h = new krpg_sampler();
+        try {
+            h->device = device;
+            h->N = N;
+            h->R = R;
+            h->storage = storage;
+            h->P = uint64_t(R) * (R + 1) / 2;
+            h->set_device();
+            CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            CK(cudaEventCreate(&h->ev0));
+            CK(cudaEventCreate(&h->ev1));
+            h->f.resize(N);
+            for (uint32_t k = 0; k < N; ++k) {
+                Factor& F = h->f[k];
+                F.I = I[k];
+                F.U.ensure(h->elt() * I[k] * R);
+                CK(cudaMemcpyAsync(F.U.p, dev_factors[k], h->elt() * I[k] * R, cudaMemcpyDeviceToDevice, h->stream));
+                h->build_tree(k);
+            }
+            for (uint32_t k = 0; k < N; ++k)
+                for (double v : h->f[k].G) require(std::isfinite(v), "KrpSampler: non-finite factor entries");
+            h->check_zero_krp();
+        } catch (...) {
+            krpg_destroy(h);
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int krpg_destroy(krpg_t h) {
+    if (!h) return KRPG_OK;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (Factor& F : h->f) {
+        F.U.release();
+        F.tree.release();
+    }
+    for (DevBuf* b : {&h->tbuf, &h->small, &h->Q, &h->err, &h->sH, &h->sIdx, &h->sProb, &h->sMargin, &h->rowbuf})
+        b->release();
+    h->up.release();
+    h->errh.release();
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return KRPG_OK;
+}
+
+int krpg_info(krpg_t h, uint32_t* N, uint32_t* R, uint64_t* I) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        if (N) *N = h->N;
+        if (R) *R = h->R;
+        if (I)
+            for (uint32_t k = 0; k < h->N; ++k) I[k] = h->f[k].I;
+    });
+}
+
+int krpg_factor_gram(krpg_t h, uint32_t j, double* out) {
+    return guard([&] {
+        require(h && j < h->N, "factor_gram: index out of range");
+        std::memcpy(out, h->f[j].G.data(), sizeof(double) * h->R * h->R);
+    });
+}
+
+int krpg_factor(krpg_t h, uint32_t j, double* out) {
+    return guard([&] {
+        require(h && j < h->N, "factor: index out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        const uint64_t n = h->f[j].I * h->R;
+        if (h->storage == KRPG_STORE_F32) {
+            double* tmp = static_cast<double*>(h->rowbuf.ensure(8 * n));
+            krpg::launch_convert_f32_to_f64(h->f[j].U.as<float>(), tmp, n, h->stream);
+            CK(cudaMemcpyAsync(out, tmp, 8 * n, cudaMemcpyDeviceToHost, h->stream));
+        } else {
+            CK(cudaMemcpyAsync(out, h->f[j].U.p, 8 * n, cudaMemcpyDeviceToHost, h->stream));
+        }
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int krpg_tree_shape(krpg_t h, uint32_t j, uint64_t* leaf_count, uint64_t* node_count) {
+    return guard([&] {
+        require(h && j < h->N, "tree: index out of range");
+        const krpg::Topo t = krpg::make_topo(h->f[j].I, h->R);
+        if (leaf_count) *leaf_count = t.L;
+        if (node_count) *node_count = t.n;
+    });
+}
+
+int krpg_node_gram(krpg_t h, uint32_t j, uint64_t node, double* out) {
+    return guard([&] {
+        require(h && j < h->N, "tree: index out of range");
+        const krpg::Topo t = krpg::make_topo(h->f[j].I, h->R);
+        require(node < t.n, "node_gram: node out of range");
+        require(krpg::stored(node), "node_gram: partial Gram not stored at this node");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        std::vector<double> p(h->P);
+        CK(cudaMemcpyAsync(p.data(), h->f[j].tree.as<double>() + krpg::slot_of(node) * h->P, 8 * h->P,
+                           cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        krpg::unpack_upper(p.data(), h->R, out);
+    });
+}
+
+int krpg_tree_grams(krpg_t h, uint32_t j, double* out) {
+    return guard([&] {
+        require(h && j < h->N, "tree: index out of range");
+        const krpg::Topo t = krpg::make_topo(h->f[j].I, h->R);
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        CK(cudaMemcpyAsync(out, h->f[j].tree.p, 8 * t.L * h->P, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int krpg_sample_device(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t draw_offset,
+                       uint32_t mode, uint32_t* d_idx, double* d_prob, double* d_rows, double* d_margin) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->sample_device(excluded, J, seed, draw_offset, mode, d_idx, d_prob, d_rows, d_margin);
+    });
+}
+
+int krpg_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t draw_offset, uint32_t mode,
+                uint32_t* idx, double* prob, double* rows, double* margin) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        require(J >= 1, "KrpSample: sample count must be positive");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        uint32_t* di = idx ? static_cast<uint32_t*>(h->sIdx.ensure(4 * J * h->N)) : nullptr;
+        double* dp = prob ? static_cast<double*>(h->sProb.ensure(8 * J)) : nullptr;
+        double* dr = static_cast<double*>(h->sH.ensure(8 * J * h->R));
+        double* dm = margin ? static_cast<double*>(h->sMargin.ensure(8 * J)) : nullptr;
+        h->sample_device(excluded, J, seed, draw_offset, mode, di, dp, dr, dm);
+        if (idx) CK(cudaMemcpyAsync(idx, di, 4 * J * h->N, cudaMemcpyDeviceToHost, h->stream));
+        if (prob) CK(cudaMemcpyAsync(prob, dp, 8 * J, cudaMemcpyDeviceToHost, h->stream));
+        if (rows) CK(cudaMemcpyAsync(rows, dr, 8 * J * h->R, cudaMemcpyDeviceToHost, h->stream));
+        if (margin) CK(cudaMemcpyAsync(margin, dm, 8 * J, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int krpg_sync(krpg_t h) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+void* krpg_stream(krpg_t h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int krpg_conditional(krpg_t h, int64_t excluded, uint32_t k, const double* hist, double* probs,
+                     double* mixture) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        const uint32_t R = h->R;
+        const size_t RR = size_t(R) * R;
+        const std::vector<uint32_t> inc = h->included(excluded);
+        size_t pos = inc.size();
+        for (size_t p = 0; p < inc.size(); ++p)
+            if (inc[p] == k) pos = p;
+        require(pos < inc.size(), "conditional: factor k is not included");
+        const std::vector<double> G = h->hadamard_of(inc);
+        const std::vector<double> gp = krpg::pinv_from_eigen(krpg::eigh_psd(G.data(), R));
+        std::vector<double> gk(RR, 1.0);
+        krpg::hadamard_into(gk, gp.data());
+        for (size_t q = pos + 1; q < inc.size(); ++q) krpg::hadamard_into(gk, h->f[inc[q]].G.data());
+        const krpg::Eig eig = krpg::eigh_psd(gk.data(), R);
+        std::vector<double> hc(RR, 1.0);
+        krpg::hadamard_into(hc, h->f[k].G.data());
+        krpg::hadamard_into(hc, gk.data());
+        const double C = krpg::quadratic_form(hist, hc.data(), R, hist);
+        if (!(C > 0.0)) throw std::runtime_error("conditional: zero normalizer");
+        std::vector<double> HT(RR);
+        for (uint32_t u = 0; u < R; ++u)
+            for (uint32_t c = 0; c < R; ++c) HT[size_t(u) * R + c] = hist[c] * eig.vectors[size_t(c) * R + u];
+        double* d = static_cast<double*>(h->small.ensure(sizeof(double) * (RR + 2 * R)));
+        double* dHT = d;
+        double* dN = d + RR;
+        double* dW = dN + R;
+        const uint64_t I = h->f[k].I;
+        double* dP = static_cast<double*>(h->sProb.ensure(8 * I));
+        CK(cudaMemcpyAsync(dHT, HT.data(), 8 * RR, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemsetAsync(dN, 0, 8 * R, h->stream));
+        krpg::launch_conditional_norms(h->f[k].U.p, h->storage, I, R, dHT, dN, h->stream);
+        std::vector<double> norms(R), w(R, 0.0);
+        CK(cudaMemcpyAsync(norms.data(), dN, 8 * R, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        for (uint32_t u = 0; u < R; ++u) {
+            if (eig.values[u] == 0.0 || norms[u] == 0.0) continue;
+            w[u] = eig.values[u] * norms[u] / C;
+        }
+        CK(cudaMemcpyAsync(dW, w.data(), 8 * R, cudaMemcpyHostToDevice, h->stream));
+        krpg::launch_conditional_probs(h->f[k].U.p, h->storage, I, R, dHT, dW, dN, dP, h->stream);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(probs, dP, 8 * I, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        std::memcpy(mixture, w.data(), 8 * R);
+    });
+}
+
+int krpg_update_factor(krpg_t h, uint32_t j, const double* U, uint64_t I) {
+    return guard([&] {
+        require(h && j < h->N, "update_factor: index out of range");
+        require(I >= 1, "update_factor: invalid factor");
+        for (uint64_t e = 0; e < I * h->R; ++e) require(std::isfinite(U[e]), "update_factor: invalid factor");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->upload_factor(j, U, I);
+        h->build_tree(j);
+    });
+}
+
+int krpg_update_entries(krpg_t h, uint32_t j, const uint64_t* r, const uint32_t* c, const double* v, uint64_t n) {
+    return guard([&] {
+        require(h && j < h->N, "update_factor_entry: index out of range");
+        const uint32_t R = h->R;
+        for (uint64_t e = 0; e < n; ++e) {
+            require(r[e] < h->f[j].I && c[e] < R, "update_factor_entry: entry out of range");
+            require(std::isfinite(v[e]), "update_factor_entry: non-finite value");
+        }
+        if (n == 0) return;
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        // distinct rows in first-touch order
+        std::unordered_map<uint64_t, uint64_t> slot;
+        std::vector<uint64_t> rows;
+        for (uint64_t e = 0; e < n; ++e)
+            if (slot.emplace(r[e], rows.size()).second) rows.push_back(r[e]);
+        const uint64_t nr = rows.size();
+        const size_t rb = 8 * nr * R;
+        char* d = static_cast<char*>(h->rowbuf.ensure(8 * nr + 2 * rb + 64));
+        uint64_t* drows = reinterpret_cast<uint64_t*>(d);
+        double* dold = reinterpret_cast<double*>(d + ((8 * nr + 15) / 16) * 16);
+        double* dnew = dold + nr * R;
+        CK(cudaMemcpyAsync(drows, rows.data(), 8 * nr, cudaMemcpyHostToDevice, h->stream));
+        krpg::launch_gather_rows(h->f[j].U.p, h->storage, R, nr, drows, dold, h->stream);
+        std::vector<double> oldh(nr * R);
+        CK(cudaMemcpyAsync(oldh.data(), dold, rb, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        std::vector<double> newh = oldh;
+        for (uint64_t e = 0; e < n; ++e) {  // sequential semantics of update_factor_entry
+            double val = v[e];
+            if (h->storage == KRPG_STORE_F32) val = static_cast<double>(static_cast<float>(val));
+            newh[slot[r[e]] * R + c[e]] = val;
+        }
+        CK(cudaMemcpyAsync(dnew, newh.data(), rb, cudaMemcpyHostToDevice, h->stream));
+        krpg::launch_row_deltas(h->f[j].tree.as<double>(), h->f[j].I, R, nr, drows, dold, dnew, h->stream);
+        krpg::launch_scatter_rows(h->f[j].U.p, h->storage, R, nr, drows, dnew, h->stream);
+        CK(cudaGetLastError());
+        std::vector<double> root(h->P);
+        CK(cudaMemcpyAsync(root.data(), h->f[j].tree.p, 8 * h->P, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        krpg::unpack_upper(root.data(), R, h->f[j].G.data());
+    });
+}
+
+int krpg_validate(krpg_t h, double tol) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        const uint32_t R = h->R;
+        double* d = static_cast<double*>(h->small.ensure(8 * size_t(R) * R));
+        std::vector<double> fresh(size_t(R) * R), root(h->P), G(size_t(R) * R);
+        for (uint32_t j = 0; j < h->N; ++j) {
+            krpg::launch_full_gram(h->f[j].U.p, h->storage, h->f[j].I, R, d, h->stream);
+            CK(cudaMemcpyAsync(fresh.data(), d, 8 * size_t(R) * R, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(root.data(), h->f[j].tree.p, 8 * h->P, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            krpg::unpack_upper(root.data(), R, G.data());
+            for (uint32_t a = 0; a < R; ++a)
+                for (uint32_t b = 0; b < R; ++b) {
+                    const double scale = std::sqrt(std::abs(fresh[a * R + a] * fresh[b * R + b]));
+                    const double lim = tol * std::max(scale, 1e-300);
+                    if (std::abs(fresh[a * R + b] - G[a * R + b]) > lim)
+                        throw std::runtime_error("KrpSampler::validate: tree root Gram drifted");
+                    if (std::abs(fresh[a * R + b] - h->f[j].G[a * R + b]) > lim)
+                        throw std::runtime_error("KrpSampler::validate: cached Gram drifted");
+                }
+        }
+    });
+}
+
+int krpg_gather_sa_device(krpg_t h, uint64_t J, const double* d_prob, const double* d_rows, double* d_weights,
+                          double* d_sa) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        require(J >= 1, "make_sampling_weights: J must be positive");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        int* derr = static_cast<int*>(h->err.ensure(sizeof(int)));
+        CK(cudaMemsetAsync(derr, 0, sizeof(int), h->stream));
+        krpg::launch_gather_sa(d_prob, d_rows, J, h->R, d_weights, d_sa, derr, h->stream);
+        CK(cudaGetLastError());
+        int* eh = static_cast<int*>(h->errh.ensure(sizeof(int)));
+        CK(cudaMemcpyAsync(eh, derr, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (*eh) throw std::invalid_argument("make_sampling_weights: sampled index has zero probability");
+    });
+}
+
+int krpg_last_build_ms(krpg_t h, float* ms) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        *ms = h->last_build_ms;
+    });
+}
+
+}  // extern "C"

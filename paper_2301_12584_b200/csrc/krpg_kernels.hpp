@@ -1,0 +1,87 @@
+// Internal launch interface between the C-ABI host layer (krpg_api.cpp) and
+// the CUDA kernels (tree_build.cu, descent.cu, update.cu).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace krpg {
+
+// ---- tree construction (segment_tree_sampler.cpp:111-191 on device) ----
+struct TreeBuildArgs {
+    const void* U;       // I x R row-major, fp64 or fp32 (storage)
+    uint32_t storage;    // 0 = f64, 1 = f32
+    uint64_t I;
+    uint32_t R;
+    double* compact;     // L x P stored Grams (slot order)
+    double* tbuf_a;      // transient level buffers, see tree_transient_doubles
+    double* tbuf_b;
+    cudaStream_t stream;
+    int force_generic;   // test hook: use the scalar kernel
+};
+// doubles needed for (tbuf_a, tbuf_b)
+void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b);
+void launch_tree_build(const TreeBuildArgs& a);
+
+// ---- E-tree (eigenvector stage) construction, krp_sampler.cpp:118-123 ----
+// Q[slot] = (sum_{u in node} lambda_u V[:,u] V[:,u]^T) o G_k, packed.
+void launch_etree_build(const double* V, const double* lam, const double* gk_packed, uint32_t R,
+                        double* Q, cudaStream_t s);
+
+// ---- batched draws ----
+struct DrawArgs {
+    uint32_t R, N, k, pos, mode;  // mode 0 two-stage, 1 one-stage
+    uint64_t J, seed, draw_offset;
+    double* H;          // J x R running Hadamard history (also the output rows)
+    uint32_t* idx;      // J x N or null
+    double* margin;     // J or null
+    const double* Q;    // E-tree compact (two-stage)
+    const double* V;    // R x R eigenvectors of G_{>k} (two-stage)
+    const double* Y;    // packed G_{>k} (one-stage)
+    const double* Z;    // factor k tree compact
+    const void* U;      // factor k rows
+    uint32_t storage;
+    uint64_t I;         // rows of factor k
+    int* err;           // device error flag
+    cudaStream_t stream;
+};
+void launch_draws(const DrawArgs& a);
+
+// q_d = h_d^T G+ h_d / rank  (krp_sampler.cpp:143-149)
+void launch_probabilities(const double* H, const double* gp_packed, uint32_t R, uint64_t J,
+                          double rank, double* prob, cudaStream_t s);
+void launch_fill(double* p, double v, uint64_t n, cudaStream_t s);
+void launch_fill_u32(uint32_t* p, uint32_t v, uint64_t n, cudaStream_t s);
+void launch_set_excluded_column(uint32_t* idx, uint64_t J, uint32_t N, uint32_t col, cudaStream_t s);
+
+// ---- STS-CP gather (cp_als.cpp:284-289) ----
+void launch_gather_sa(const double* prob, const double* rows, uint64_t J, uint32_t R, double* w,
+                      double* sa, int* err, cudaStream_t s);
+
+// ---- conditional distribution (krp_sampler.cpp:153-196) ----
+// HT[u,:] = h o V[:,u]; norms[u] += sum_t (U[t,:] . HT[u,:])^2 (norms zeroed by caller)
+void launch_conditional_norms(const void* U, uint32_t storage, uint64_t I, uint32_t R,
+                              const double* HT, double* norms, cudaStream_t s);
+// probs[t] = sum_u w[u] * (U[t,:] . HT[u,:])^2 / norms[u]  (w[u]=0 skips)
+void launch_conditional_probs(const void* U, uint32_t storage, uint64_t I, uint32_t R,
+                              const double* HT, const double* w, const double* norms,
+                              double* probs, cudaStream_t s);
+
+// ---- updates (segment_tree_sampler.cpp:358-409) ----
+// for each touched row: patch u'u'^T - uu^T into every stored node on its path
+void launch_row_deltas(double* compact, uint64_t I, uint32_t R, uint64_t nrows,
+                       const uint64_t* rows, const double* old_rows, const double* new_rows,
+                       cudaStream_t s);
+void launch_scatter_rows(void* U, uint32_t storage, uint32_t R, uint64_t nrows,
+                         const uint64_t* rows, const double* new_rows, cudaStream_t s);
+void launch_gather_rows(const void* U, uint32_t storage, uint32_t R, uint64_t nrows,
+                        const uint64_t* rows, double* out, cudaStream_t s);
+void launch_convert_f64_to_f32(const double* in, float* out, uint64_t n, cudaStream_t s);
+void launch_convert_f32_to_f64(const float* in, double* out, uint64_t n, cudaStream_t s);
+
+// fresh Gram of a whole factor (validate): out R x R
+void launch_full_gram(const void* U, uint32_t storage, uint64_t I, uint32_t R, double* out,
+                      cudaStream_t s);
+
+}  // namespace krpg

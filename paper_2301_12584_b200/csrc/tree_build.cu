@@ -1,0 +1,340 @@
+// Segment-tree construction on device: the reference's build_grams
+// (/root/reference/proj/src/segment_tree_sampler.cpp:151-191) for the Z-trees
+// (leaf capacity F = R, krp_sampler.cpp:53), B200-first:
+//
+//  * k_leaf_dmma: leaf Grams on the FP64 tensor cores (mma.sync m8n8k4 ->
+//    DMMA.8x8x4), U rows streamed HBM -> shared memory by 1-D TMA bulk copies
+//    (cp.async.bulk -> UBLKCP) through a per-warp 4-stage mbarrier ring. One
+//    warp owns one "position" (a node on level d-1: a pair of leaves, or a
+//    single leaf of a non-perfect tree) and accumulates its full upper-triangle
+//    tile set in registers: after the left leaf's rows the accumulators are the
+//    left leaf's Gram (stored: it is a left child), after the right leaf's rows
+//    they are the parent's Gram. So the first reduction level costs nothing.
+//  * k_level_reduce: the remaining levels, coalesced packed sums level by level
+//    (parent = left + right, :180-186), writing only the stored nodes (root and
+//    left children, :142) into the compact array.
+//  * k_leaf_generic: scalar fallback for ranks the DMMA path does not cover.
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+
+#include "krpg_device.cuh"
+#include "krpg_kernels.hpp"
+#include "ptx.cuh"
+
+namespace krpg {
+
+namespace {
+
+struct PosGeom {
+    uint64_t I, F, npos, hb, pos_node0, left_slot0;
+    uint32_t R, P;
+};
+
+__host__ __device__ __forceinline__ void pos_rows(const PosGeom& g, uint64_t j, uint64_t& r0,
+                                                  uint64_t& rs, uint64_t& r1) {
+    if (j < g.hb) {  // pair of bottom-level leaves 2j, 2j+1
+        r0 = 2 * j * g.F;
+        rs = r0 + g.F;
+        r1 = r0 + 2 * g.F < g.I ? r0 + 2 * g.F : g.I;
+    } else {  // single leaf one level up
+        r0 = (j + g.hb) * g.F;
+        rs = ~uint64_t{0};
+        r1 = r0 + g.F < g.I ? r0 + g.F : g.I;
+    }
+}
+
+PosGeom make_geom(uint64_t I, uint32_t R) {
+    const Topo t = make_topo(I, R);
+    PosGeom g;
+    g.I = I;
+    g.F = R;
+    g.R = R;
+    g.P = R * (R + 1) / 2;
+    const uint32_t D = t.d ? t.d - 1 : 0;
+    g.npos = uint64_t{1} << D;
+    g.hb = t.bottom / 2;
+    g.pos_node0 = t.d ? (uint64_t{1} << D) - 1 : 0;
+    g.left_slot0 = t.d ? (uint64_t{1} << (t.d - 1)) : 0;  // slot of node 2^d-1+2j is 2^(d-1)+j
+    return g;
+}
+
+template <int NB, typename T>
+struct LeafCfg {
+    static constexpr int R = 8 * NB;
+    static constexpr int NT = NB * (NB + 1) / 2;  // upper-triangle 8x8 tiles
+    static constexpr int CH = 8;                  // rows per TMA chunk (2 k-steps)
+    static constexpr int STAGES = 4;
+    static constexpr int ROWB = R * int(sizeof(T));
+    static constexpr int RS = ROWB + 16;  // padded row stride: conflict-free fragment reads
+    static constexpr int CHB = CH * RS;
+    static constexpr int WPC = 4;  // warps per CTA (independent pipelines)
+    static constexpr int SMEM = WPC * STAGES * CHB + WPC * STAGES * 8;
+};
+
+// Fragment loader: lane reads NB consecutive elements of one staged row.
+template <int NB, typename T>
+__device__ __forceinline__ void load_frag(const unsigned char* rowp, double (&x)[NB]) {
+    const T* p = reinterpret_cast<const T*>(rowp);
+    if constexpr (sizeof(T) == 8 && NB % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < NB; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(p + i);
+            x[i] = v.x;
+            x[i + 1] = v.y;
+        }
+    } else if constexpr (sizeof(T) == 4 && NB % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < NB; i += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(p + i);
+            x[i] = v.x;
+            x[i + 1] = v.y;
+            x[i + 2] = v.z;
+            x[i + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) x[i] = static_cast<double>(p[i]);
+    }
+}
+
+// Scatter the warp's accumulator tiles into packed upper-triangle Gram(s).
+// Lane l holds tile (p,q) elements (m, n) = (l>>2, 2(l&3)+i), i.e. G[a][b]
+// with a = m*NB + p, b = n*NB + q (strided column blocks).
+template <int NB>
+__device__ __forceinline__ void store_tiles(const double (&acc)[NB * (NB + 1) / 2][2], int lane,
+                                            double* dst0, double* dst1) {
+    constexpr int R = 8 * NB;
+    const int m = lane >> 2;
+    int t = 0;
+#pragma unroll
+    for (int p = 0; p < NB; ++p) {
+#pragma unroll
+        for (int q = p; q < NB; ++q, ++t) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int n = 2 * (lane & 3) + i;
+                if (p == q && m > n) continue;
+                const uint32_t a = m * NB + p, b = n * NB + q;
+                const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+                const uint32_t idx = pack_index(R, lo, hi);
+                dst0[idx] = acc[t][i];
+                if (dst1) dst1[idx] = acc[t][i];
+            }
+        }
+    }
+}
+
+template <int NB, typename T>
+__global__ void __launch_bounds__(LeafCfg<NB, T>::WPC * 32)
+    k_leaf_dmma(const T* __restrict__ U, PosGeom g, double* __restrict__ compact,
+                double* __restrict__ tout) {
+    using C = LeafCfg<NB, T>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* ring = smem + warp * (C::STAGES * C::CHB);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::WPC * C::STAGES * C::CHB) + warp * C::STAGES;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    const uint64_t nw = uint64_t(gridDim.x) * C::WPC;
+    const uint64_t gw = uint64_t(blockIdx.x) * C::WPC + warp;
+    if (gw >= g.npos) return;
+    const uint64_t P = g.P;
+
+    // producer cursor (runs STAGES-1 chunks ahead)
+    uint64_t pj = gw, prow, prs, pr1;
+    pos_rows(g, pj, prow, prs, pr1);
+    uint64_t issued = 0;
+    auto produce = [&]() {
+        if (pj >= g.npos) return;
+        const int st = int(issued % C::STAGES);
+        const uint64_t left = pr1 - prow;
+        const uint32_t nrows = left < uint64_t(C::CH) ? uint32_t(left) : uint32_t(C::CH);
+        if (lane == 0) mbar_arrive_expect_tx(&bars[st], nrows * C::ROWB);
+        __syncwarp();
+        if (uint32_t(lane) < nrows)
+            tma_load_1d(ring + st * C::CHB + lane * C::RS, U + (prow + lane) * C::R, C::ROWB, &bars[st]);
+        ++issued;
+        prow += C::CH;
+        if (prow >= pr1) {
+            pj += nw;
+            if (pj < g.npos) pos_rows(g, pj, prow, prs, pr1);
+        }
+    };
+    for (int s = 0; s < C::STAGES - 1; ++s) produce();
+
+    uint64_t cj = gw, crow, crs, cr1;
+    pos_rows(g, cj, crow, crs, cr1);
+    double acc[C::NT][2];
+#pragma unroll
+    for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+
+    const int frow = lane & 3;
+    const int fcol = (lane >> 2) * NB * int(sizeof(T));
+    for (uint64_t i = 0; cj < g.npos; ++i) {
+        produce();
+        const int st = int(i % C::STAGES);
+        mbar_wait(&bars[st], uint32_t((i / C::STAGES) & 1));
+        const uint64_t left = cr1 - crow;
+        const int nvalid = left < uint64_t(C::CH) ? int(left) : C::CH;
+        const unsigned char* buf = ring + st * C::CHB;
+#pragma unroll
+        for (int ks = 0; ks < C::CH / 4; ++ks) {
+            const int row = ks * 4 + frow;
+            double x[NB];
+            if (row < nvalid) {
+                load_frag<NB, T>(buf + row * C::RS + fcol, x);
+            } else {
+#pragma unroll
+                for (int p = 0; p < NB; ++p) x[p] = 0.0;
+            }
+            int t = 0;
+#pragma unroll
+            for (int p = 0; p < NB; ++p)
+#pragma unroll
+                for (int q = p; q < NB; ++q, ++t) dmma_884(acc[t][0], acc[t][1], x[p], x[q]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        crow += C::CH;
+        if (crow == crs) {  // left leaf of a pair complete: it is a left child -> stored
+            store_tiles<NB>(acc, lane, compact + (g.left_slot0 + cj) * P, nullptr);
+        }
+        if (crow >= cr1) {
+            const uint64_t v = g.pos_node0 + cj;
+            double* d0 = tout ? tout + cj * P : nullptr;
+            double* d1 = stored(v) ? compact + slot_of(v) * P : nullptr;
+            if (!d0) {
+                d0 = d1;
+                d1 = nullptr;
+            }
+            if (d0) store_tiles<NB>(acc, lane, d0, d1);
+#pragma unroll
+            for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+            cj += nw;
+            if (cj < g.npos) pos_rows(g, cj, crow, crs, cr1);
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_leaf_generic(const T* __restrict__ U, PosGeom g, double* __restrict__ compact,
+                               double* __restrict__ tout) {
+    const uint32_t R = g.R;
+    const uint64_t P = g.P;
+    for (uint64_t j = blockIdx.x; j < g.npos; j += gridDim.x) {
+        uint64_t r0, rs, r1;
+        pos_rows(g, j, r0, rs, r1);
+        const uint64_t v = g.pos_node0 + j;
+        for (uint32_t k = threadIdx.x; k < P; k += blockDim.x) {
+            uint32_t a, b;
+            unpack_pair(R, k, a, b);
+            double acc = 0.0;
+            for (uint64_t i = r0; i < r1; ++i) {
+                acc += static_cast<double>(U[i * R + a]) * static_cast<double>(U[i * R + b]);
+                if (i + 1 == rs) compact[(g.left_slot0 + j) * P + k] = acc;
+            }
+            if (tout) tout[j * P + k] = acc;
+            if (stored(v)) compact[slot_of(v) * P + k] = acc;
+        }
+    }
+}
+
+__global__ void k_level_reduce(const double* __restrict__ child, double* __restrict__ parent,
+                               double* __restrict__ compact, uint64_t nj, uint64_t P, uint64_t node0) {
+    for (uint64_t j = blockIdx.x; j < nj; j += gridDim.x) {
+        const double* c0 = child + 2 * j * P;
+        const double* c1 = c0 + P;
+        const uint64_t v = node0 + j;
+        double* cp = stored(v) ? compact + slot_of(v) * P : nullptr;
+        double* pp = parent ? parent + j * P : nullptr;
+        for (uint64_t k = threadIdx.x; k < P; k += blockDim.x) {
+            const double s = c0[k] + c1[k];
+            if (pp) pp[k] = s;
+            if (cp) cp[k] = s;
+        }
+    }
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+template <int NB, typename T>
+void launch_dmma(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s) {
+    using C = LeafCfg<NB, T>;
+    auto kern = k_leaf_dmma<NB, T>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        configured = true;
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::WPC * 32, C::SMEM);
+    if (occ < 1) occ = 1;
+    const uint64_t need = (g.npos + C::WPC - 1) / C::WPC;
+    const uint64_t grid = std::min<uint64_t>(need, uint64_t(sm_count()) * occ);
+    kern<<<unsigned(grid), C::WPC * 32, C::SMEM, s>>>(U, g, compact, tout);
+}
+
+template <typename T>
+void launch_leaf(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s,
+                 bool generic) {
+    if (!generic) {
+        switch (g.R) {
+            case 8: return launch_dmma<1, T>(U, g, compact, tout, s);
+            case 16: return launch_dmma<2, T>(U, g, compact, tout, s);
+            case 24: return launch_dmma<3, T>(U, g, compact, tout, s);
+            case 32: return launch_dmma<4, T>(U, g, compact, tout, s);
+            case 40: return launch_dmma<5, T>(U, g, compact, tout, s);
+            case 48: return launch_dmma<6, T>(U, g, compact, tout, s);
+            case 56: return launch_dmma<7, T>(U, g, compact, tout, s);
+            case 64: return launch_dmma<8, T>(U, g, compact, tout, s);
+            default: break;
+        }
+    }
+    const uint64_t grid = std::min<uint64_t>(g.npos, uint64_t(sm_count()) * 16);
+    k_leaf_generic<T><<<unsigned(grid), 256, 0, s>>>(U, g, compact, tout);
+}
+
+}  // namespace
+
+void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b) {
+    const PosGeom g = make_geom(I, R);
+    *a = g.npos > 1 ? g.npos * g.P : 0;
+    *b = g.npos > 2 ? (g.npos / 2) * g.P : 0;
+}
+
+void launch_tree_build(const TreeBuildArgs& a) {
+    const PosGeom g = make_geom(a.I, a.R);
+    double* tout = g.npos > 1 ? a.tbuf_a : nullptr;
+    if (a.storage == 1)
+        launch_leaf<float>(static_cast<const float*>(a.U), g, a.compact, tout, a.stream, a.force_generic);
+    else
+        launch_leaf<double>(static_cast<const double*>(a.U), g, a.compact, tout, a.stream, a.force_generic);
+    // remaining levels D-1 .. 0
+    uint32_t D = 0;
+    while ((uint64_t{1} << D) < g.npos) ++D;
+    double* cur = a.tbuf_a;
+    double* nxt = a.tbuf_b;
+    for (int l = int(D) - 1; l >= 0; --l) {
+        const uint64_t nj = uint64_t{1} << l;
+        double* parent = l > 0 ? nxt : nullptr;
+        const unsigned grid = unsigned(std::min<uint64_t>(nj, uint64_t(sm_count()) * 8));
+        k_level_reduce<<<grid, 256, 0, a.stream>>>(cur, parent, a.compact, nj, g.P, nj - 1);
+        std::swap(cur, nxt);
+    }
+}
+
+}  // namespace krpg

@@ -1,0 +1,273 @@
+"""Python mirror of the reference's C++ sampler API over the krpg C ABI.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/krplev/krp_sampler.hpp:17-101 so parity tests
+read like the reference's own tests (test_krp_sampler.cpp). All work runs on
+the GPU through libkrpg.so; there is no CPU execution path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import (EXCLUDED, MODE_ONE_STAGE, MODE_TWO_STAGE, STORE_F32, STORE_F64, check,
+                   KrpgError, KrpgInvalidArgument)
+
+_dp = C.POINTER(C.c_double)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+class RowOrder(enum.Enum):
+    """krp_sampler.hpp:17-25."""
+    Ascending = 0  # first factor varies slowest
+    Reversed = 1   # first factor varies fastest (mode-j matricization order)
+
+
+@dataclass
+class SampleBatch:
+    """krp_sampler.hpp:27-48: J draws with exact probabilities and KRP rows."""
+    excluded: Optional[int]
+    count: int
+    factor_count: int
+    dims: np.ndarray                 # per-factor rows, excluded slot = 0
+    indices: np.ndarray              # J x N uint32, excluded column = kExcluded
+    probabilities: np.ndarray        # J
+    rows: np.ndarray                 # J x R
+    margin: Optional[np.ndarray] = field(default=None)  # J (boundary accounting)
+
+    kExcluded = EXCLUDED
+
+    def index(self, draw: int, factor: int) -> int:
+        return int(self.indices[draw, factor])
+
+    def flat_indices(self, order: RowOrder = RowOrder.Ascending) -> np.ndarray:
+        """Mixed-radix KRP row ids (krp_sampler.cpp:19-39)."""
+        ks = [k for k in range(self.factor_count) if self.excluded is None or k != self.excluded]
+        if order == RowOrder.Reversed:
+            ks = ks[::-1]
+        flat = np.zeros(self.count, dtype=np.uint64)
+        for k in ks:
+            flat = flat * np.uint64(self.dims[k]) + self.indices[:, k].astype(np.uint64)
+        return flat
+
+    def flat_index(self, draw: int, order: RowOrder = RowOrder.Ascending) -> int:
+        ks = [k for k in range(self.factor_count) if self.excluded is None or k != self.excluded]
+        if order == RowOrder.Reversed:
+            ks = ks[::-1]
+        flat = 0
+        for k in ks:
+            flat = flat * int(self.dims[k]) + int(self.indices[draw, k])
+        return flat
+
+
+@dataclass
+class ConditionalDistribution:
+    """krp_sampler.hpp:50-55."""
+    probabilities: np.ndarray
+    mixture_weights: np.ndarray
+
+
+class KrpSampler:
+    """Exact leverage-score sampler for the KRP U_1 o ... o U_N (krp_sampler.hpp:57-101).
+
+    Holds one segment tree per factor in HBM (leaf capacity R, compact
+    layout). ``sample`` reproduces the reference's two-stage draws bit-exactly
+    (up to counted boundary draws); ``mode="one_stage"`` draws from the
+    north-star's per-draw M = G+ o hh^T o G_{>k} directly.
+    """
+
+    def __init__(self, factors: Sequence[np.ndarray], storage: str = "f64", device: int = 0):
+        L = _lib.lib()
+        fs = [_f64(f) for f in factors]
+        N = len(fs)
+        if N == 0:
+            raise KrpgInvalidArgument("KrpSampler: factor list is empty")
+        for f in fs:
+            if f.ndim != 2:
+                raise KrpgInvalidArgument("KrpSampler: factors must be 2-D")
+        R = fs[0].shape[1]
+        if any(f.shape[1] != R for f in fs):
+            raise KrpgInvalidArgument("KrpSampler: inconsistent column counts")
+        I = (C.c_uint64 * N)(*[f.shape[0] for f in fs])
+        ptrs = (_dp * N)(*[_ptr(f) for f in fs])
+        h = C.c_void_p()
+        st = STORE_F32 if storage == "f32" else STORE_F64
+        check(L.krpg_create(ptrs, I, N, R, st, device, C.byref(h)))
+        self._h = h
+        self._N, self._R = N, R
+        self._dims = [f.shape[0] for f in fs]
+        self._storage = st
+
+    @classmethod
+    def from_device(cls, factors, storage: str = "f64", device: int = 0) -> "KrpSampler":
+        """Build from torch CUDA tensors (row-major, float64 or float32)."""
+        L = _lib.lib()
+        N = len(factors)
+        R = int(factors[0].shape[1])
+        I = (C.c_uint64 * N)(*[int(f.shape[0]) for f in factors])
+        ptrs = (C.c_void_p * N)(*[C.c_void_p(f.data_ptr()) for f in factors])
+        h = C.c_void_p()
+        st = STORE_F32 if storage == "f32" else STORE_F64
+        check(L.krpg_create_device(ptrs, I, N, R, st, device, C.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        self._N, self._R = N, R
+        self._dims = [int(f.shape[0]) for f in factors]
+        self._storage = st
+        return self
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.lib().krpg_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- accessors (krp_sampler.hpp:63-68) ----
+    def factor_count(self) -> int:
+        return self._N
+
+    def rank(self) -> int:
+        return self._R
+
+    def factor(self, j: int) -> np.ndarray:
+        if not 0 <= j < self._N:
+            raise KrpgInvalidArgument("factor: index out of range")
+        out = np.empty((self._dims[j], self._R))
+        check(_lib.lib().krpg_factor(self._h, j, _ptr(out)))
+        return out
+
+    def factor_gram(self, j: int) -> np.ndarray:
+        if not 0 <= j < self._N:
+            raise KrpgInvalidArgument("factor_gram: index out of range")
+        out = np.empty((self._R, self._R))
+        check(_lib.lib().krpg_factor_gram(self._h, j, _ptr(out)))
+        return out
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ---- tree introspection (segment_tree_sampler.hpp:64-95) ----
+    def tree_shape(self, j: int):
+        lc, nc = C.c_uint64(), C.c_uint64()
+        check(_lib.lib().krpg_tree_shape(self._h, j, C.byref(lc), C.byref(nc)))
+        return int(lc.value), int(nc.value)
+
+    def node_gram(self, j: int, node: int) -> np.ndarray:
+        out = np.empty((self._R, self._R))
+        check(_lib.lib().krpg_node_gram(self._h, j, node, _ptr(out)))
+        return out
+
+    def tree_grams(self, j: int) -> np.ndarray:
+        L, _ = self.tree_shape(j)
+        P = self._R * (self._R + 1) // 2
+        out = np.empty((L, P))
+        check(_lib.lib().krpg_tree_grams(self._h, j, _ptr(out)))
+        return out
+
+    # ---- sampling (krp_sampler.cpp:82-151) ----
+    def sample(self, excluded: Optional[int], J: int, seed: int, *, mode: str = "two_stage",
+               draw_offset: int = 0, margin: bool = False) -> SampleBatch:
+        if J < 1:
+            raise KrpgInvalidArgument("KrpSample: sample count must be positive")
+        e = -1 if excluded is None else int(excluded)
+        if e < -1:
+            raise KrpgInvalidArgument("KrpSampler: excluded index out of range")
+        N, R = self._N, self._R
+        idx = np.empty((J, N), dtype=np.uint32)
+        prob = np.empty(J)
+        rows = np.empty((J, R))
+        mg = np.empty(J) if margin else None
+        m = MODE_ONE_STAGE if mode == "one_stage" else MODE_TWO_STAGE
+        check(_lib.lib().krpg_sample(self._h, e, J, seed, draw_offset, m,
+                                     idx.ctypes.data_as(C.POINTER(C.c_uint32)), _ptr(prob), _ptr(rows),
+                                     _ptr(mg) if mg is not None else None))
+        dims = np.array([0 if (excluded is not None and k == excluded) else self._dims[k]
+                         for k in range(N)], dtype=np.uint64)
+        return SampleBatch(excluded, J, N, dims, idx, prob, rows, mg)
+
+    def sample_device(self, excluded: Optional[int], J: int, seed: int, idx=None, prob=None,
+                      rows=None, margin=None, *, mode: str = "two_stage", draw_offset: int = 0) -> None:
+        """Device-resident outputs (torch CUDA tensors or None)."""
+        e = -1 if excluded is None else int(excluded)
+        m = MODE_ONE_STAGE if mode == "one_stage" else MODE_TWO_STAGE
+
+        def p(t):
+            return C.c_void_p(t.data_ptr()) if t is not None else None
+
+        check(_lib.lib().krpg_sample_device(self._h, e, J, seed, draw_offset, m, p(idx), p(prob),
+                                            p(rows), p(margin)))
+
+    def gather_sa_device(self, J: int, prob, rows, weights, sa) -> None:
+        check(_lib.lib().krpg_gather_sa_device(self._h, J, C.c_void_p(prob.data_ptr()),
+                                               C.c_void_p(rows.data_ptr()),
+                                               C.c_void_p(weights.data_ptr()) if weights is not None else None,
+                                               C.c_void_p(sa.data_ptr())))
+
+    def stream(self) -> int:
+        return int(_lib.lib().krpg_stream(self._h) or 0)
+
+    def last_build_ms(self) -> float:
+        v = C.c_float()
+        check(_lib.lib().krpg_last_build_ms(self._h, C.byref(v)))
+        return float(v.value)
+
+    # ---- conditional (krp_sampler.cpp:153-196) ----
+    def conditional(self, excluded: Optional[int], k: int, h) -> ConditionalDistribution:
+        h = _f64(h)
+        if h.size != self._R:
+            raise KrpgInvalidArgument("conditional: history vector has wrong length")
+        if not 0 <= k < self._N:
+            raise KrpgInvalidArgument("conditional: factor k is not included")
+        e = -1 if excluded is None else int(excluded)
+        probs = np.empty(self._dims[k])
+        mix = np.empty(self._R)
+        check(_lib.lib().krpg_conditional(self._h, e, k, _ptr(h), _ptr(probs), _ptr(mix)))
+        return ConditionalDistribution(probs, mix)
+
+    # ---- updates (krp_sampler.cpp:198-228) ----
+    def update_factor(self, j: int, U) -> None:
+        U = _f64(U)
+        if not 0 <= j < self._N:
+            raise KrpgInvalidArgument("update_factor: index out of range")
+        if U.ndim != 2 or U.shape[1] != self._R:
+            raise KrpgInvalidArgument("update_factor: column count mismatch")
+        check(_lib.lib().krpg_update_factor(self._h, j, _ptr(U), U.shape[0]))
+        self._dims[j] = U.shape[0]
+
+    def update_factor_entry(self, j: int, r: int, c: int, value: float) -> None:
+        self.update_factor_entries(j, [r], [c], [value])
+
+    def update_factor_entries(self, j: int, r, c, v) -> None:
+        r = np.ascontiguousarray(r, dtype=np.uint64)
+        c = np.ascontiguousarray(c, dtype=np.uint32)
+        v = _f64(v)
+        if not (r.size == c.size == v.size):
+            raise KrpgInvalidArgument("update_factor_entry: length mismatch")
+        check(_lib.lib().krpg_update_entries(self._h, j, r.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                             c.ctypes.data_as(C.POINTER(C.c_uint32)), _ptr(v), v.size))
+
+    def validate(self, tol: float = 1e-10) -> None:
+        check(_lib.lib().krpg_validate(self._h, tol))
+
+
+def device_count() -> int:
+    return int(_lib.lib().krpg_device_count())

@@ -1,0 +1,59 @@
+"""Shared parity helpers: compare the device sampler with a CPU oracle.
+
+Indices must be bit-exact except for *boundary draws*: draws whose uniform lies
+within ``tol`` (1e-10, north_star) of a branch / leaf-scan threshold in either
+implementation. Such draws are counted, and any mismatch outside that margin
+is a failure.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+BOUNDARY_TOL = 1e-10
+
+
+def rel_err_matrix(A: np.ndarray, B: np.ndarray) -> float:
+    """max |A-B| / sqrt(diag(A)_a diag(A)_b): Gram-scale relative error."""
+    d = np.sqrt(np.abs(np.outer(np.diag(B), np.diag(B))))
+    d = np.maximum(d, np.finfo(float).tiny)
+    return float(np.max(np.abs(A - B) / d))
+
+
+def compare_draws(gpu_idx, gpu_margin, ref_idx, ref_margin=None, tol=BOUNDARY_TOL):
+    """Returns (n_mismatch, n_boundary_mismatch, n_unexplained)."""
+    mism = np.any(gpu_idx != ref_idx, axis=1)
+    n = int(mism.sum())
+    m = gpu_margin[mism]
+    if ref_margin is not None:
+        m = np.minimum(m, ref_margin[mism])
+    boundary = m <= tol
+    return n, int(boundary.sum()), int((~boundary).sum())
+
+
+def rel_err_vec(a, b):
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))) if a.size else 0.0
+
+
+def rows_rel_err(a, b):
+    """max over draws of |a-b|_inf / |b|_inf (rows are Hadamard products)."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    scale = np.maximum(np.max(np.abs(b), axis=1, keepdims=True), 1e-300)
+    return float(np.max(np.abs(a - b) / scale)) if a.size else 0.0
+
+
+def pareto_factors(shapes, seed, frac=1.0, alpha=1.5):
+    """Config-1/2 inputs: N(0,1) entries, rows scaled by a Pareto(alpha) weight
+    w = (1-u)^(-1/alpha); frac < 1 scales only that fraction of rows."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for (I, R) in shapes:
+        U = rng.standard_normal((I, R))
+        u = rng.random(I)
+        w = (1.0 - rng.random(I)) ** (-1.0 / alpha)
+        if frac < 1.0:
+            w = np.where(u < frac, w, 1.0)
+        out.append(U * w[:, None])
+    return out
