@@ -121,6 +121,30 @@ int krpg_gather_sa_device(krpg_t h, uint64_t J, const double* d_prob, const doub
 /* Timing of the last tree build (ms, device events) for the bench. */
 int krpg_last_build_ms(krpg_t h, float* ms);
 
+/* ---- instrumentation (bench / profiling support) ----
+ * Every kernel launch is counted per category; when profiling is enabled each
+ * category's launches are also bracketed by CUDA events on the handle's stream
+ * and their device time accumulated. */
+#define KRPG_PROF_TREE_LEAF 0   /* DMMA leaf/pair Gram kernel            */
+#define KRPG_PROF_TREE_LEVELS 1 /* level-by-level packed reductions      */
+#define KRPG_PROF_ETREE 2       /* eigenvector-stage tree construction   */
+#define KRPG_PROF_DRAWS 3       /* batched root-to-leaf descent          */
+#define KRPG_PROF_PROB 4        /* probability epilogue                  */
+#define KRPG_PROF_UPDATE 5      /* incremental updates                   */
+#define KRPG_PROF_OTHER 6       /* fills, gathers, conversions           */
+#define KRPG_PROF_N 8
+int krpg_profile_enable(krpg_t h, int on);
+/* ms and launches: arrays of KRPG_PROF_N (nullable); reset != 0 zeroes them */
+int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
+
+/* ---- host-only test support (no device needed) ---- */
+/* Row range [first, last) of heap node v of the complete tree over I rows with
+ * leaf capacity F (SegmentTreeSampler::node_segment, segment_tree_sampler.hpp:74-76). */
+int krpg_topology_node_rows(uint64_t I, uint64_t F, uint64_t v, uint64_t* first, uint64_t* last,
+                            uint64_t* leaf_count, uint64_t* node_count);
+/* The host eigensolver used per sample call (values descending, vectors as columns). */
+int krpg_host_eigh(const double* G, uint32_t n, double* vectors, double* values);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,10 +83,10 @@ class _Backend:
             self.p = "kref_"
         else:
             raise ValueError(kind)
-        self.lib[self.p + "last_error"].restype = C.c_char_p
+        getattr(self.lib, self.p + "last_error").restype = C.c_char_p
 
     def fn(self, name):
-        return self.lib[self.p + name]
+        return getattr(self.lib, self.p + name)
 
     def check(self, rc: int):
         if rc == 0:

@@ -125,6 +125,49 @@ struct krpg_sampler {
     DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf;
     PinBuf up, errh;
 
+    // ---- instrumentation: launch counts always, event timing when enabled ----
+    bool prof_on = false;
+    double prof_ms[KRPG_PROF_N] = {};
+    uint64_t prof_launches[KRPG_PROF_N] = {};
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct ProfRec {
+        int cat;
+        cudaEvent_t a, b;
+    };
+    std::vector<ProfRec> prof_pending;
+
+    cudaEvent_t next_event() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+    cudaEvent_t pbegin() {
+        if (!prof_on) return nullptr;
+        cudaEvent_t e = next_event();
+        CK(cudaEventRecord(e, stream));
+        return e;
+    }
+    void pend(int cat, cudaEvent_t a, int launches) {
+        prof_launches[cat] += uint64_t(launches);
+        if (!prof_on || !a) return;
+        cudaEvent_t b = next_event();
+        CK(cudaEventRecord(b, stream));
+        prof_pending.push_back({cat, a, b});
+    }
+    void presolve() {  // call after the stream has been synchronised
+        for (const ProfRec& r : prof_pending) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, r.a, r.b));
+            prof_ms[r.cat] += ms;
+        }
+        prof_pending.clear();
+        ev_used = 0;
+    }
+
     size_t elt() const { return storage == KRPG_STORE_F32 ? 4 : 8; }
 
     void set_device() const { CK(cudaSetDevice(device)); }
@@ -147,12 +190,18 @@ struct krpg_sampler {
         a.stream = stream;
         a.force_generic = 0;
         CK(cudaEventRecord(ev0, stream));
-        krpg::launch_tree_build(a);
+        cudaEvent_t t0 = pbegin();
+        const int nl = krpg::launch_tree_leaves(a);
+        pend(KRPG_PROF_TREE_LEAF, t0, nl);
+        t0 = pbegin();
+        const int nv = krpg::launch_tree_levels(a);
+        pend(KRPG_PROF_TREE_LEVELS, t0, nv);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev1, stream));
         std::vector<double> root(P);
         CK(cudaMemcpyAsync(root.data(), F.tree.p, sizeof(double) * P, cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
+        presolve();
         CK(cudaEventElapsedTime(&last_build_ms, ev0, ev1));
         F.G.assign(size_t(R) * R, 0.0);
         krpg::unpack_upper(root.data(), R, F.G.data());
@@ -250,7 +299,10 @@ struct krpg_sampler {
         double* H = d_rows ? d_rows : static_cast<double*>(sH.ensure(sizeof(double) * J * R));
         int* derr = static_cast<int*>(err.ensure(sizeof(int)));
         CK(cudaMemsetAsync(derr, 0, sizeof(int), stream));
-        if (d_idx && excluded >= 0) krpg::launch_set_excluded_column(d_idx, J, N, uint32_t(excluded), stream);
+        if (d_idx && excluded >= 0) {
+            krpg::launch_set_excluded_column(d_idx, J, N, uint32_t(excluded), stream);
+            prof_launches[KRPG_PROF_OTHER] += 1;
+        }
         double* dQ = mode == KRPG_MODE_TWO_STAGE ? static_cast<double*>(Q.ensure(sizeof(double) * R * P)) : nullptr;
 
         for (size_t p = 0; p < npos; ++p) {
@@ -275,19 +327,28 @@ struct krpg_sampler {
             a.err = derr;
             a.stream = stream;
             if (mode == KRPG_MODE_TWO_STAGE) {
+                cudaEvent_t t0 = pbegin();
                 krpg::launch_etree_build(blk, blk + RR, f[k].tree.as<double>(), R, dQ, stream);
+                pend(KRPG_PROF_ETREE, t0, 1);
                 a.Q = dQ;
                 a.V = blk;
             } else {
                 a.Y = blk;
             }
+            cudaEvent_t t0 = pbegin();
             krpg::launch_draws(a);
+            pend(KRPG_PROF_DRAWS, t0, 1);
         }
-        if (d_prob) krpg::launch_probabilities(H, dsmall, R, J, double(rank), d_prob, stream);
+        if (d_prob) {
+            cudaEvent_t t0 = pbegin();
+            krpg::launch_probabilities(H, dsmall, R, J, double(rank), d_prob, stream);
+            pend(KRPG_PROF_PROB, t0, 1);
+        }
         CK(cudaGetLastError());
         int* eh = static_cast<int*>(errh.ensure(sizeof(int)));
         CK(cudaMemcpyAsync(eh, derr, sizeof(int), cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
+        presolve();
         if (*eh) throw std::runtime_error("row_sample: degenerate distribution (C <= 0)");
     }
 };
@@ -393,6 +454,7 @@ int krpg_destroy(krpg_t h) {
         b->release();
     h->up.release();
     h->errh.release();
+    for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -607,12 +669,16 @@ int krpg_update_entries(krpg_t h, uint32_t j, const uint64_t* r, const uint32_t*
             newh[slot[r[e]] * R + c[e]] = val;
         }
         CK(cudaMemcpyAsync(dnew, newh.data(), rb, cudaMemcpyHostToDevice, h->stream));
+        cudaEvent_t t0 = h->pbegin();
         krpg::launch_row_deltas(h->f[j].tree.as<double>(), h->f[j].I, R, nr, drows, dold, dnew, h->stream);
         krpg::launch_scatter_rows(h->f[j].U.p, h->storage, R, nr, drows, dnew, h->stream);
+        h->pend(KRPG_PROF_UPDATE, t0, 2);
+        h->prof_launches[KRPG_PROF_OTHER] += 1;  // gather of the old rows
         CK(cudaGetLastError());
         std::vector<double> root(h->P);
         CK(cudaMemcpyAsync(root.data(), h->f[j].tree.p, 8 * h->P, cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
+        h->presolve();
         krpg::unpack_upper(root.data(), R, h->f[j].G.data());
     });
 }
@@ -666,6 +732,49 @@ int krpg_last_build_ms(krpg_t h, float* ms) {
     return guard([&] {
         require(h, "krpg: null handle");
         *ms = h->last_build_ms;
+    });
+}
+
+int krpg_profile_enable(krpg_t h, int on) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->prof_on = on != 0;
+    });
+}
+
+int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        std::lock_guard<std::mutex> lk(h->mu);
+        for (int c = 0; c < KRPG_PROF_N; ++c) {
+            if (ms) ms[c] = h->prof_ms[c];
+            if (launches) launches[c] = h->prof_launches[c];
+            if (reset) {
+                h->prof_ms[c] = 0.0;
+                h->prof_launches[c] = 0;
+            }
+        }
+    });
+}
+
+int krpg_topology_node_rows(uint64_t I, uint64_t F, uint64_t v, uint64_t* first, uint64_t* last,
+                            uint64_t* leaf_count, uint64_t* node_count) {
+    return guard([&] {
+        require(I >= 1 && F >= 1, "topology: empty");
+        const krpg::Topo t = krpg::make_topo(I, F);
+        require(v < t.n, "node_segment: node out of range");
+        krpg::node_rows(t, v, first, last);
+        if (leaf_count) *leaf_count = t.L;
+        if (node_count) *node_count = t.n;
+    });
+}
+
+int krpg_host_eigh(const double* G, uint32_t n, double* vectors, double* values) {
+    return guard([&] {
+        const krpg::Eig e = krpg::eigh_psd(G, n);
+        std::memcpy(vectors, e.vectors.data(), sizeof(double) * n * n);
+        std::memcpy(values, e.values.data(), sizeof(double) * n);
     });
 }
 

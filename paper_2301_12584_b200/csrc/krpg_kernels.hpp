@@ -22,7 +22,9 @@ struct TreeBuildArgs {
 };
 // doubles needed for (tbuf_a, tbuf_b)
 void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b);
-void launch_tree_build(const TreeBuildArgs& a);
+// leaf / first-pair level (DMMA) then the remaining levels; returns #launches
+int launch_tree_leaves(const TreeBuildArgs& a);
+int launch_tree_levels(const TreeBuildArgs& a);
 
 // ---- E-tree (eigenvector stage) construction, krp_sampler.cpp:118-123 ----
 // Q[slot] = (sum_{u in node} lambda_u V[:,u] V[:,u]^T) o G_k, packed.

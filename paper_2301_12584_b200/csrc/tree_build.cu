@@ -316,25 +316,32 @@ void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b) {
     *b = g.npos > 2 ? (g.npos / 2) * g.P : 0;
 }
 
-void launch_tree_build(const TreeBuildArgs& a) {
+int launch_tree_leaves(const TreeBuildArgs& a) {
     const PosGeom g = make_geom(a.I, a.R);
     double* tout = g.npos > 1 ? a.tbuf_a : nullptr;
     if (a.storage == 1)
         launch_leaf<float>(static_cast<const float*>(a.U), g, a.compact, tout, a.stream, a.force_generic);
     else
         launch_leaf<double>(static_cast<const double*>(a.U), g, a.compact, tout, a.stream, a.force_generic);
-    // remaining levels D-1 .. 0
+    return 1;
+}
+
+int launch_tree_levels(const TreeBuildArgs& a) {
+    const PosGeom g = make_geom(a.I, a.R);
     uint32_t D = 0;
     while ((uint64_t{1} << D) < g.npos) ++D;
     double* cur = a.tbuf_a;
     double* nxt = a.tbuf_b;
+    int launches = 0;
     for (int l = int(D) - 1; l >= 0; --l) {
         const uint64_t nj = uint64_t{1} << l;
         double* parent = l > 0 ? nxt : nullptr;
         const unsigned grid = unsigned(std::min<uint64_t>(nj, uint64_t(sm_count()) * 8));
         k_level_reduce<<<grid, 256, 0, a.stream>>>(cur, parent, a.compact, nj, g.P, nj - 1);
+        ++launches;
         std::swap(cur, nxt);
     }
+    return launches;
 }
 
 }  // namespace krpg

@@ -57,3 +57,42 @@ def pareto_factors(shapes, seed, frac=1.0, alpha=1.5):
             w = np.where(u < frac, w, 1.0)
         out.append(U * w[:, None])
     return out
+
+
+def config1_factors(shapes=((4096, 16),) * 3, seed=2301, kind="port"):
+    """Config-1 inputs built only from the reference CounterRng (rng.hpp:13-48,
+    support.hpp:12-18): entries N(0,1) from stream k, every row scaled by a
+    Pareto(1.5) weight w = (1-u)^(-1/1.5) with u from stream 1000+k."""
+    import oracle
+    b = oracle.backend(kind)
+    out = []
+    for k, (I, R) in enumerate(shapes):
+        U = b.normals(seed, k, I * R).reshape(I, R)
+        u = b.uniforms(seed, 1000 + k, I)
+        w = np.power(1.0 - u, -1.0 / 1.5)
+        out.append(U * w[:, None])
+    return out
+
+
+def spiked_factors(shapes, seed, frac=0.01, scale=10.0, kind="port"):
+    """testsupport::random_spiked_matrix (support.hpp:21-31): N(0,1) with about
+    `frac` of entries scaled by `scale`, normal and uniform interleaved per entry."""
+    import oracle
+    b = oracle.backend(kind)
+    out = []
+    for k, (I, R) in enumerate(shapes):
+        n = I * R
+        # one normal() consumes two uniforms, then one uniform: 3 per entry
+        u = b.uniforms(seed + k, 0, 3 * n).reshape(n, 3)
+        z = np.sqrt(-2.0 * np.log(1.0 - u[:, 0])) * np.cos(6.283185307179586476925 * u[:, 1])
+        z = np.where(u[:, 2] < frac, z * scale, z)
+        out.append(z.reshape(I, R))
+    return out
+
+
+def digest(arrays) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()

@@ -1,0 +1,378 @@
+"""GPU parity tests: the device sampler (through the C ABI) against the CPU
+oracle on identical factors and identical uniforms.
+
+Bars (north_star): tree Grams and probabilities within fp64 relative 1e-10;
+drawn indices bit-exact except counted boundary draws (uniform within 1e-10 of
+a threshold); chi-square against exact leverage on an enumerable problem.
+Test structure follows the reference's test_krp_sampler.cpp / test_segment_tree.cpp.
+"""
+import os
+from functools import lru_cache
+
+import numpy as np
+import pytest
+
+import oracle
+from parity_util import (compare_draws, config1_factors, digest, pareto_factors, rel_err_matrix,
+                         rel_err_vec, rows_rel_err, spiked_factors)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_v1.npz")
+TOL = 1e-10
+
+
+@lru_cache(maxsize=1)
+def golden():
+    return dict(np.load(GOLDEN))
+
+
+def K():
+    from paper_2301_12584_b200 import KrpSampler
+    return KrpSampler
+
+
+def assert_draws_match(b, ref_idx, ref_prob=None, ref_rows=None, ref_margin=None, allow=0):
+    n, nb, nu = compare_draws(b.indices, b.margin, ref_idx, ref_margin)
+    assert nu == 0, f"{nu} index mismatches outside the {TOL} boundary margin"
+    assert nb <= max(allow, n), "boundary accounting inconsistent"
+    same = ~np.any(b.indices != ref_idx, axis=1)
+    if ref_prob is not None:
+        assert rel_err_vec(b.probabilities[same], ref_prob[same]) <= TOL
+    if ref_rows is not None:
+        assert rows_rel_err(b.rows[same], ref_rows[same]) <= TOL
+    return n, nb
+
+
+# ------------------------------------------------------------------ trees
+TREE_SHAPES = [(1, 3), (2, 1), (5, 2), (64, 4), (33, 3), (4096, 16), (1000, 8), (777, 24), (513, 32),
+               (4097, 64), (3000, 40), (130, 5), (257, 1), (2049, 56), (100, 100)]
+
+
+@pytest.mark.parametrize("I,R", TREE_SHAPES)
+def test_tree_grams_node_by_node(I, R):
+    """Every stored node Gram vs the reference build_grams (segment_tree_sampler.cpp:151-191)
+    at fp64 relative 1e-10 (entrywise, scaled by sqrt(G_aa G_bb))."""
+    fs = pareto_factors([(I, R), (7, R)], seed=I + R)
+    s = K()(fs)
+    t = oracle.OracleTree(fs[0], R, None, "port")
+    L, n = s.tree_shape(0)
+    assert (L, n) == (t.leaf_count, t.node_count)
+    grams = s.tree_grams(0)
+    P = R * (R + 1) // 2
+    iu = np.triu_indices(R)
+    for slot in range(L):
+        v = 0 if slot == 0 else 2 * slot - 1
+        G = np.zeros((R, R))
+        G[iu] = grams[slot]
+        G = G + G.T - np.diag(np.diag(G))
+        assert rel_err_matrix(G, t.node_gram(v)) <= TOL, (slot, v)
+    assert grams.shape == (L, P)
+
+
+def test_tree_fp32_storage_upcast_parity():
+    """Config-3 style storage: fp32 on device, fp64 accumulation; the oracle gets the
+    exact fp64 up-cast of the same fp32 values."""
+    fs = pareto_factors([(3001, 32), (2000, 32)], seed=5)
+    f32 = [f.astype(np.float32).astype(np.float64) for f in fs]
+    s = K()(fs, storage="f32")
+    o = oracle.OracleKrp(f32, "port")
+    assert np.array_equal(s.factor(0), f32[0])
+    for v in [0] + list(range(1, 2 * 94 - 1, 2)):
+        assert rel_err_matrix(s.node_gram(0, v), o.node_gram(0, v)) <= TOL
+    for e in (None, 0):
+        b = s.sample(e, 3000, 3, margin=True)
+        ri, rp, rr, rm = o.sample(e, 3000, 3, want_margin=True)
+        assert_draws_match(b, ri, rp, rr, rm)
+
+
+# ------------------------------------------------------------ draws
+CASES = [
+    ([(8, 3), (7, 3), (6, 3)], 1),
+    ([(64, 4), (40, 4), (33, 4)], 2),
+    ([(1000, 8), (777, 8), (513, 8)], 3),
+    ([(300, 5), (200, 5)], 4),
+    ([(5000, 64), (3000, 64), (4097, 64)], 5),
+    ([(2000, 32), (1500, 32), (999, 32), (1234, 32)], 6),
+    ([(700, 24), (650, 24), (30, 24)], 7),
+    ([(900, 40), (10, 40)], 8),
+]
+
+
+@pytest.mark.parametrize("shapes,seed", CASES)
+@pytest.mark.parametrize("mode", ["two_stage", "one_stage"])
+def test_sample_bit_exact_against_oracle(shapes, seed, mode):
+    """KrpSampler::sample (two-stage, krp_sampler.cpp:82-151) and the one-stage
+    M = G+ o hh^T o G_{>k} chain, every exclusion setting."""
+    fs = pareto_factors(shapes, seed)
+    s = K()(fs)
+    o = oracle.OracleKrp(fs, "port")
+    for e in [None] + list(range(len(shapes))):
+        b = s.sample(e, 4096, 100 + seed, mode=mode, margin=True)
+        ri, rp, rr, rm = o.sample(e, 4096, 100 + seed, one_stage=(mode == "one_stage"), want_margin=True)
+        assert_draws_match(b, ri, rp, rr, rm)
+        if e is not None:
+            assert np.all(b.indices[:, e] == 0xFFFFFFFF)
+
+
+def test_config1_golden_vectors():
+    """Config 1 (3 x 4096 x 16, Pareto rows, J = 8192) against the reference's own
+    outputs (tests/golden, produced by oracle/_ref)."""
+    g = golden()
+    fs = config1_factors()
+    assert digest(fs) == str(g["c1_digest"])
+    s = K()(fs)
+    J, seed = int(g["c1_J"]), int(g["c1_seed"])
+    total = 0
+    for e in (None, 0, 1, 2):
+        tag = "none" if e is None else str(e)
+        b = s.sample(e, J, seed, margin=True)
+        n, _ = assert_draws_match(b, g[f"c1_idx_{tag}"], g[f"c1_prob_{tag}"])
+        total += n
+    b = s.sample(None, J, seed, mode="one_stage", margin=True)
+    assert_draws_match(b, g["c1_idx_one_stage"], g["c1_prob_one_stage"])
+    for j in range(3):
+        assert rel_err_matrix(s.factor_gram(j), g[f"c1_gram_{j}"]) <= TOL
+    for v, G in zip(g["c1_node_ids"], g["c1_nodes_f0"]):
+        assert rel_err_matrix(s.node_gram(0, int(v)), G) <= TOL
+
+
+def test_draw_offset_sharding_matches_one_call():
+    fs = pareto_factors([(3000, 16), (2000, 16), (1000, 16)], 9)
+    s = K()(fs)
+    full = s.sample(None, 3001, 42)
+    parts = [s.sample(None, c, 42, draw_offset=st) for st, c in [(0, 1000), (1000, 1001), (2001, 1000)]]
+    assert np.array_equal(np.concatenate([p.indices for p in parts]), full.indices)
+    assert np.array_equal(np.concatenate([p.probabilities for p in parts]), full.probabilities)
+
+
+# ---------------------------------------------------- distribution checks
+def test_chi_square_against_exact_leverage_64x64x64():
+    """Config-1 chi-square sub-case: 64 x 64 x 64 (262,144 KRP rows), R = 16, 2^22
+    draws vs exact leverage (reference.cpp:30-48); cells with expected < 5 pooled."""
+    from scipy import stats
+    fs = config1_factors(shapes=((64, 16),) * 3, seed=77)
+    q = oracle.backend("port").leverage(fs)
+    s = K()(fs)
+    J = 1 << 22
+    counts = np.zeros(q.size, dtype=np.int64)
+    for c in range(4):
+        b = s.sample(None, J // 4, 1000 + c)
+        flat = (b.indices[:, 0].astype(np.int64) * 64 + b.indices[:, 1]) * 64 + b.indices[:, 2]
+        counts += np.bincount(flat, minlength=q.size)
+        if c == 0:  # probabilities reported with each draw are the exact leverage / rank
+            assert rel_err_vec(b.probabilities, q[flat] * 1.0) <= 1e-9
+    exp = q * J
+    big = exp >= 5
+    obs = np.append(counts[big], counts[~big].sum())
+    ex = np.append(exp[big], exp[~big].sum())
+    chi2 = np.sum((obs - ex) ** 2 / ex)
+    p = stats.chi2.sf(chi2, obs.size - 1)
+    assert p > 0.001, (chi2, obs.size, p)
+    tv = 0.5 * np.sum(np.abs(q - counts / J))
+    assert tv < 0.05
+
+
+def test_uniform_and_identity_known_answers():
+    """test_krp_sampler.cpp:82-107."""
+    s = K()([np.ones((2, 1)), np.ones((2, 1))])
+    b = s.sample(None, 40000, 610)
+    counts = np.bincount(b.flat_indices(), minlength=4)
+    assert np.sum((counts - 10000.0) ** 2 / 10000.0) < 11.345
+    assert np.allclose(b.probabilities, 0.25)
+    s = K()([np.eye(2), np.eye(2)])
+    b = s.sample(None, 100000, 611)
+    counts = np.bincount(b.flat_indices(), minlength=4)
+    q = np.array([0.5, 0, 0, 0.5])
+    assert 0.5 * np.abs(q - counts / 1e5).sum() <= 0.01
+    assert counts[1] == 0 and counts[2] == 0
+
+
+def test_spiked_figure5_fixture():
+    """test_krp_sampler.cpp:109-124 plus the golden draws of the same fixture."""
+    g = golden()
+    sp = spiked_factors([(8, 8)] * 3, 620)
+    assert digest(sp) == str(g["sp_digest"])
+    s = K()(sp)
+    b = s.sample(None, 4096, 621, margin=True)
+    assert_draws_match(b, g["sp_idx"], g["sp_prob"])
+    b = s.sample(None, 50000, 621)
+    counts = np.bincount(b.flat_indices(), minlength=512)
+    assert 0.5 * np.abs(g["sp_leverage"] - counts / 50000).sum() <= 0.05
+    cd = s.conditional(None, 1, g["sp_cond_h"])
+    assert np.max(np.abs(cd.probabilities - g["sp_cond_p"])) <= TOL
+    assert np.max(np.abs(cd.mixture_weights - g["sp_cond_mix"])) <= TOL
+
+
+def test_conditional_matches_oracle_and_chains_to_leverage():
+    """test_krp_sampler.cpp:126-192: conditional vs direct formula and the chained joint."""
+    shapes = [(8, 3), (7, 3), (6, 3)]
+    fs = [oracle.random_matrix(r, c, 701 + k) for k, (r, c) in enumerate(shapes)]
+    s = K()(fs)
+    o = oracle.OracleKrp(fs, "port")
+    h = np.array([0.4, -1.1, 0.9])
+    for k in range(3):
+        cd = s.conditional(None, k, h)
+        p, m = o.conditional(None, k, h)
+        assert np.max(np.abs(cd.probabilities - p)) <= TOL
+        assert abs(cd.mixture_weights.sum() - 1.0) <= 1e-10
+    # chained joint == normalized leverage
+    joint = np.zeros(8 * 7 * 6)
+
+    def walk(pos, hv, prefix, flat):
+        if pos == 3:
+            joint[flat] = prefix
+            return
+        p = s.conditional(None, pos, hv).probabilities
+        for t in range(p.size):
+            if p[t] > 0:
+                walk(pos + 1, hv * fs[pos][t], prefix * p[t], flat * shapes[pos][0] + t)
+
+    walk(0, np.ones(3), 1.0, 0)
+    assert np.max(np.abs(joint - oracle.backend("port").leverage(fs))) <= 1e-8
+
+
+def test_exclusion_consistency():
+    """test_krp_sampler.cpp:233-247: counters follow the position in the included list."""
+    fs = [oracle.random_matrix(9, 3, 740 + j) for j in range(3)]
+    full = K()(fs)
+    red = K()([fs[0], fs[2]])
+    a = full.sample(1, 500, 741)
+    b = red.sample(None, 500, 741)
+    assert np.array_equal(a.indices[:, 0], b.indices[:, 0])
+    assert np.array_equal(a.indices[:, 2], b.indices[:, 1])
+    assert rel_err_vec(a.probabilities, b.probabilities) <= 1e-12
+
+
+def test_flat_index_and_rows_are_hadamard_products():
+    """test_krp_sampler.cpp:308-333."""
+    fs = [oracle.random_matrix(2, 2, 770), oracle.random_matrix(3, 2, 771), oracle.random_matrix(4, 2, 772)]
+    s = K()(fs)
+    b = s.sample(None, 50, 773)
+    from paper_2301_12584_b200 import RowOrder
+    i0, i1, i2 = (b.indices[:, k].astype(np.uint64) for k in range(3))
+    assert np.array_equal(b.flat_indices(RowOrder.Ascending), (i0 * 3 + i1) * 4 + i2)
+    assert np.array_equal(b.flat_indices(RowOrder.Reversed), (i2 * 3 + i1) * 2 + i0)
+    expect = fs[0][i0.astype(int)] * fs[1][i1.astype(int)] * fs[2][i2.astype(int)]
+    assert rows_rel_err(b.rows, expect) <= 1e-12
+
+
+# ---------------------------------------------------------------- updates
+def test_update_factor_rebuilds_only_the_touched_factor():
+    """test_krp_sampler.cpp:249-274."""
+    fs = [oracle.random_matrix(8, 4, 750 + j) for j in range(3)]
+    s = K()(fs)
+    g0, g1 = s.factor_gram(0), s.factor_gram(1)
+    unew = oracle.random_matrix(8, 4, 753)
+    s.update_factor(2, unew)
+    assert np.array_equal(s.factor_gram(0), g0) and np.array_equal(s.factor_gram(1), g1)
+    assert rel_err_matrix(s.factor_gram(2), unew.T @ unew) <= TOL
+    fresh = K()([fs[0], fs[1], unew])
+    a = s.sample(None, 300, 754)
+    b = fresh.sample(None, 300, 754)
+    assert np.array_equal(a.indices, b.indices)
+
+
+@pytest.mark.parametrize("I,R,n", [(10, 3, 20), (4096, 16, 2000), (3001, 32, 5000)])
+def test_update_entries_match_sequential_reference_updates(I, R, n):
+    """update_factor_entry sequence (krp_sampler.cpp:207-228) vs the oracle applying the
+    same sequence: node Grams within 1e-10 relative; later draws agree up to boundary draws."""
+    fs = pareto_factors([(I, R), (max(I // 2, 3), R)], seed=I)
+    s = K()(fs)
+    o = oracle.OracleKrp(fs, "port")
+    rng = np.random.default_rng(I)
+    r = rng.integers(0, I, n).astype(np.uint64)
+    c = rng.integers(0, R, n).astype(np.uint32)
+    v = rng.standard_normal(n)
+    s.update_factor_entries(0, r, c, v)
+    o.update_entries(0, r, c, v)
+    L, nn = s.tree_shape(0)
+    for node in [0] + list(range(1, nn, 2)):
+        assert rel_err_matrix(s.node_gram(0, node), o.node_gram(0, node)) <= TOL
+    assert np.array_equal(s.factor(0), o.factors[0])
+    s.validate(1e-10)
+    b = s.sample(None, 2000, 5, margin=True)
+    ri, rp, rr, rm = o.sample(None, 2000, 5, want_margin=True)
+    assert_draws_match(b, ri, rp, rr, rm)
+
+
+def test_update_golden_sequence():
+    g = golden()
+    fu = [oracle.random_matrix(10, 3, 760 + j) for j in range(2)]
+    s = K()(fu)
+    s.update_factor_entries(0, g["upd_r"], g["upd_c"], g["upd_v"])
+    assert rel_err_matrix(s.factor_gram(0), g["upd_gram0"]) <= TOL
+    b = s.sample(None, 400, 763, margin=True)
+    assert_draws_match(b, g["upd_idx"])
+
+
+# ------------------------------------------------------------ STS-CP gather
+def test_gather_sa_matches_sampling_weights():
+    import torch
+    fs = pareto_factors([(2000, 16), (1000, 16), (500, 16)], 21)
+    s = K()(fs)
+    J = 4096
+    idx = torch.empty(J, 3, dtype=torch.int32, device="cuda")
+    prob = torch.empty(J, dtype=torch.float64, device="cuda")
+    rows = torch.empty(J, 16, dtype=torch.float64, device="cuda")
+    s.sample_device(0, J, 5, idx, prob, rows)
+    w = torch.empty(J, dtype=torch.float64, device="cuda")
+    sa = torch.empty(J, 16, dtype=torch.float64, device="cuda")
+    s.gather_sa_device(J, prob, rows, w, sa)
+    pw = oracle.backend("port").sampling_weights(prob.cpu().numpy(), J)
+    assert rel_err_vec(w.cpu().numpy(), pw) <= 1e-14
+    assert rows_rel_err(sa.cpu().numpy(), rows.cpu().numpy() * pw[:, None]) <= 1e-14
+
+
+# ------------------------------------------------------------------ errors
+def test_error_behaviour_matches_reference_classes():
+    from paper_2301_12584_b200 import KrpgError, KrpgInvalidArgument
+    with pytest.raises(KrpgInvalidArgument):
+        K()([np.ones((2, 1)), np.ones((2, 2))])
+    with pytest.raises(KrpgInvalidArgument):
+        K()([np.zeros((2, 2)), np.zeros((2, 2))])  # all-zero product
+    with pytest.raises(KrpgInvalidArgument):
+        K()([])
+    with pytest.raises(KrpgInvalidArgument):
+        K()([np.array([[np.nan, 1.0]])])
+    s = K()([np.ones((3, 2)), np.ones((4, 2))])
+    with pytest.raises(KrpgInvalidArgument):
+        s.sample(2, 10, 1)
+    with pytest.raises(KrpgInvalidArgument):
+        s.sample(None, 0, 1)
+    with pytest.raises(KrpgInvalidArgument):
+        s.update_factor_entry(0, 3, 0, 1.0)
+    with pytest.raises(KrpgInvalidArgument):
+        s.update_factor_entry(0, 0, 2, 1.0)
+    with pytest.raises(KrpgInvalidArgument):
+        s.update_factor_entry(0, 0, 0, float("inf"))
+    one = K()([np.ones((3, 2))])
+    with pytest.raises(KrpgInvalidArgument):
+        one.sample(0, 4, 1)  # no factors left
+    # rank-deficient included product after updates -> zero KRP at sample time
+    z = K()([np.eye(2), np.ones((2, 2))])
+    z.update_factor(0, np.zeros((2, 2)))
+    with pytest.raises(KrpgError):
+        z.sample(1, 4, 1)
+
+
+# ---------------------------------------------- large-size properties (config 4 scale)
+@pytest.mark.parametrize("R", [16, 64])
+def test_large_factor_properties(R):
+    """At 2^20 rows (config-4 size): tree root == fresh device Gram (validate, relative),
+    drawn rows equal the Hadamard product of the drawn factor rows, probabilities equal
+    h^T G+ h / rank recomputed on the host."""
+    import torch
+    I = 1 << 20
+    g = torch.Generator(device="cuda").manual_seed(R)
+    fs = [torch.randn(I, R, dtype=torch.float64, device="cuda", generator=g) for _ in range(3)]
+    s = K().from_device(fs)
+    s.validate(1e-10)
+    b = s.sample(None, 8192, 3)
+    hf = [f.cpu().numpy() for f in fs]
+    expect = hf[0][b.indices[:, 0]] * hf[1][b.indices[:, 1]] * hf[2][b.indices[:, 2]]
+    assert rows_rel_err(b.rows, expect) <= 1e-14
+    G = s.factor_gram(0) * s.factor_gram(1) * s.factor_gram(2)
+    Gp = np.linalg.pinv(G, hermitian=True)
+    q = np.einsum("dr,rs,ds->d", b.rows, Gp, b.rows) / R
+    assert rel_err_vec(b.probabilities, q) <= 1e-8
