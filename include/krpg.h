@@ -100,6 +100,11 @@ int krpg_conditional(krpg_t h, int64_t excluded, uint32_t k, const double* hist,
 
 /* Replaces KrpSampler::update_factor(j, U) (krp_sampler.cpp:198-205): full device rebuild. */
 int krpg_update_factor(krpg_t h, uint32_t j, const double* U, uint64_t I);
+/* Same with the new factor already on the handle's device (storage dtype), e.g.
+ * produced by a device-side STS-CP solve (cp_als.cpp:293-313). */
+int krpg_update_factor_device(krpg_t h, uint32_t j, const void* dU, uint64_t I);
+/* Rebuild factor j's tree from its current device rows (timing / recovery). */
+int krpg_rebuild(krpg_t h, uint32_t j);
 /* Replaces a sequence of KrpSampler::update_factor_entry(j, r[i], c[i], v[i])
  * (krp_sampler.cpp:207-228) applied in order: all entries are validated first,
  * then each touched row's net change u'u'^T - uu^T is patched into every stored

@@ -73,7 +73,16 @@ _SIGS = {
     "krpg_validate": ([_vp, C.c_double], _int),
     "krpg_gather_sa_device": ([_vp, _u64, _vp, _vp, _vp, _vp], _int),
     "krpg_last_build_ms": ([_vp, C.POINTER(C.c_float)], _int),
+    "krpg_update_factor_device": ([_vp, _u32, _vp, _u64], _int),
+    "krpg_rebuild": ([_vp, _u32], _int),
+    "krpg_profile_enable": ([_vp, _int], _int),
+    "krpg_profile_read": ([_vp, _dp, C.POINTER(_u64), _int], _int),
+    "krpg_topology_node_rows": ([_u64, _u64, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64),
+                                 C.POINTER(_u64)], _int),
+    "krpg_host_eigh": ([_dp, _u32, _dp, _dp], _int),
 }
+
+PROF_NAMES = ["tree_leaf", "tree_levels", "etree", "draws", "prob", "update", "other", "spare"]
 
 _lib: C.CDLL | None = None
 

@@ -635,6 +635,30 @@ int krpg_update_factor(krpg_t h, uint32_t j, const double* U, uint64_t I) {
     });
 }
 
+int krpg_update_factor_device(krpg_t h, uint32_t j, const void* dU, uint64_t I) {
+    return guard([&] {
+        require(h && j < h->N, "update_factor: index out of range");
+        require(I >= 1 && dU, "update_factor: invalid factor");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        Factor& F = h->f[j];
+        F.I = I;
+        F.U.ensure(h->elt() * I * h->R);
+        CK(cudaMemcpyAsync(F.U.p, dU, h->elt() * I * h->R, cudaMemcpyDeviceToDevice, h->stream));
+        h->build_tree(j);
+        for (double x : F.G) require(std::isfinite(x), "update_factor: invalid factor");
+    });
+}
+
+int krpg_rebuild(krpg_t h, uint32_t j) {
+    return guard([&] {
+        require(h && j < h->N, "rebuild: index out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->build_tree(j);
+    });
+}
+
 int krpg_update_entries(krpg_t h, uint32_t j, const uint64_t* r, const uint32_t* c, const double* v, uint64_t n) {
     return guard([&] {
         require(h && j < h->N, "update_factor_entry: index out of range");

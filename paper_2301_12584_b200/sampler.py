@@ -222,6 +222,24 @@ class KrpSampler:
                                                C.c_void_p(weights.data_ptr()) if weights is not None else None,
                                                C.c_void_p(sa.data_ptr())))
 
+    def update_factor_device(self, j: int, U) -> None:
+        """New factor j from a torch CUDA tensor (storage dtype), full device rebuild."""
+        check(_lib.lib().krpg_update_factor_device(self._h, j, C.c_void_p(U.data_ptr()), int(U.shape[0])))
+        self._dims[j] = int(U.shape[0])
+
+    def rebuild(self, j: int) -> None:
+        check(_lib.lib().krpg_rebuild(self._h, j))
+
+    def profile_enable(self, on: bool = True) -> None:
+        check(_lib.lib().krpg_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        ms = np.zeros(8)
+        n = np.zeros(8, dtype=np.uint64)
+        check(_lib.lib().krpg_profile_read(self._h, _ptr(ms), n.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                           1 if reset else 0))
+        return {name: {"ms": float(ms[i]), "launches": int(n[i])} for i, name in enumerate(_lib.PROF_NAMES)}
+
     def stream(self) -> int:
         return int(_lib.lib().krpg_stream(self._h) or 0)
 
