@@ -142,6 +142,13 @@ int krpg_profile_enable(krpg_t h, int on);
 /* ms and launches: arrays of KRPG_PROF_N (nullable); reset != 0 zeroes them */
 int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
 
+/* ---- options ----
+ * KRPG_OPT_GROUPED_DESCENT (default 1): use the level-synchronous, node-grouped
+ * DMMA descent (R = 8..64, multiple of 8, two-stage mode); 0 forces the
+ * per-draw-warp descent (the path used for every other rank / mode). */
+#define KRPG_OPT_GROUPED_DESCENT 1
+int krpg_set_option(krpg_t h, int option, int64_t value);
+
 /* ---- host-only test support (no device needed) ---- */
 /* Row range [first, last) of heap node v of the complete tree over I rows with
  * leaf capacity F (SegmentTreeSampler::node_segment, segment_tree_sampler.hpp:74-76). */

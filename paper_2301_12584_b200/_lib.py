@@ -80,7 +80,9 @@ _SIGS = {
     "krpg_topology_node_rows": ([_u64, _u64, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64),
                                  C.POINTER(_u64)], _int),
     "krpg_host_eigh": ([_dp, _u32, _dp, _dp], _int),
+    "krpg_set_option": ([_vp, _int, _i64], _int),
 }
+OPT_GROUPED_DESCENT = 1
 
 PROF_NAMES = ["tree_leaf", "tree_levels", "etree", "draws", "prob", "update", "other", "spare"]
 

@@ -33,20 +33,35 @@ __device__ __forceinline__ double packed_qf(const double* __restrict__ G, const 
     double acc[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) acc[s] = 0.0;
-    uint32_t off = 0;
-    for (uint32_t a = 0; a < R; ++a) {
-        const double xa = xs[a];
-        const double xa2 = xa + xa;
+    // Rows are processed in batches of RB with all loads issued before any use,
+    // so each lane keeps RB*S independent loads in flight (memory-level parallelism).
+    constexpr int RB = 8;
+    for (uint32_t a0 = 0; a0 < R; a0 += RB) {
+        double g[RB][S];
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const uint32_t b = uint32_t(lane) + 32u * s;
-            if (b >= a && b < R) {
-                double g = __ldg(G + off + (b - a));
-                if (WEIGHTED) g *= __ldg(W + off + (b - a));
-                acc[s] = fma(g, b == a ? xa : xa2, acc[s]);
+        for (int j = 0; j < RB; ++j) {
+            const uint32_t a = a0 + j;
+            const uint32_t off = a * R - (a * (a - 1)) / 2;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const uint32_t b = uint32_t(lane) + 32u * s;
+                const bool ok = a < R && b >= a && b < R;
+                double v = ok ? __ldg(G + off + (b - a)) : 0.0;
+                if (WEIGHTED) v *= ok ? __ldg(W + off + (b - a)) : 0.0;
+                g[j][s] = v;
             }
         }
-        off += R - a;
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            const uint32_t a = a0 + j;
+            const double xa = a < R ? xs[a] : 0.0;
+            const double xa2 = xa + xa;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const uint32_t b = uint32_t(lane) + 32u * s;
+                acc[s] = fma(g[j][s], b == a ? xa : xa2, acc[s]);
+            }
+        }
     }
     double t = 0.0;
 #pragma unroll
@@ -156,18 +171,41 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
     }
     double cum = low;
     uint64_t pick = ~uint64_t{0}, last_nz = ~uint64_t{0};
-    for (uint64_t i = first; i < last; ++i) {
-        double mass;
-        if (MODE == 0) {
-            double part = 0.0;
+    if (MODE == 0) {
+        // rank-1 leaf masses (U[i,:] . z)^2, 8 rows per batch: loads of the whole
+        // batch are in flight together, then the sequential scan (:284-291).
+        constexpr int LB = 8;
+        for (uint64_t i0 = first; i0 < last && pick == ~uint64_t{0}; i0 += LB) {
+            double part[LB];
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const uint32_t b = lane + 32u * s;
-                if (b < R) part = fma(static_cast<double>(U[i * R + b]), zr[s], part);
+            for (int j = 0; j < LB; ++j) {
+                const uint64_t i = i0 + j;
+                double p = 0.0;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const uint32_t b = lane + 32u * s;
+                    const double u_ib = (i < last && b < R) ? static_cast<double>(U[i * R + b]) : 0.0;
+                    p = fma(u_ib, zr[s], p);
+                }
+                part[j] = p;
             }
-            const double dot = warp_sum(part);
-            mass = dot * dot;
-        } else {
+#pragma unroll
+            for (int j = 0; j < LB; ++j) part[j] = warp_sum(part[j]);
+#pragma unroll
+            for (int j = 0; j < LB; ++j) {
+                const uint64_t i = i0 + j;
+                if (i >= last || pick != ~uint64_t{0}) continue;
+                const double m = inv_c * (part[j] * part[j]);
+                if (m > 0.0) last_nz = i;
+                cum += m;
+                margin = fmin(margin, fabs(cum - u));
+                if (cum >= u) pick = i;
+            }
+        }
+    }
+    for (uint64_t i = first; MODE == 1 && i < last; ++i) {
+        double mass;
+        {
             // general leaf mass: (h o r)^T G_{>k} (h o r), packed
             double xr[S];
             __syncwarp();

@@ -122,8 +122,9 @@ struct krpg_sampler {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_build_ms = 0.f;
     std::mutex mu;
-    DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf;
+    DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf, gstate, zbuf;
     PinBuf up, errh;
+    bool use_grouped = true;  // level-synchronous DMMA descent where supported
 
     // ---- instrumentation: launch counts always, event timing when enabled ----
     bool prof_on = false;
@@ -305,6 +306,73 @@ struct krpg_sampler {
         }
         double* dQ = mode == KRPG_MODE_TWO_STAGE ? static_cast<double*>(Q.ensure(sizeof(double) * R * P)) : nullptr;
 
+        if (use_grouped && krpg::grouped_supported(R, mode)) {
+            // ---- level-synchronous grouped descent (descent_v2.cu) ----
+            uint64_t nmax = 2ull * R;
+            for (uint32_t k : inc) nmax = std::max<uint64_t>(nmax, krpg::make_topo(f[k].I, R).n);
+            const size_t Ju = size_t(J);
+            char* st = static_cast<char*>(gstate.ensure(Ju * (4 * 4 + 8 * 3) + nmax * 4 * 3 + 256));
+            auto carve = [&](size_t bytes) {
+                char* p = st;
+                st += (bytes + 127) / 128 * 128;
+                return p;
+            };
+            krpg::GroupedArgs g{};
+            g.perm_a = reinterpret_cast<uint32_t*>(carve(4 * Ju));
+            g.perm_b = reinterpret_cast<uint32_t*>(carve(4 * Ju));
+            g.node = reinterpret_cast<uint32_t*>(carve(4 * Ju));
+            g.rank = reinterpret_cast<uint32_t*>(carve(4 * Ju));
+            g.low = reinterpret_cast<double*>(carve(8 * Ju));
+            g.invc = reinterpret_cast<double*>(carve(8 * Ju));
+            g.ud = reinterpret_cast<double*>(carve(8 * Ju));
+            g.gstart = reinterpret_cast<uint32_t*>(carve(4 * nmax));
+            g.cntL = reinterpret_cast<uint32_t*>(carve(4 * nmax));
+            g.cntR = reinterpret_cast<uint32_t*>(carve(4 * nmax));
+            g.Zb = static_cast<double*>(zbuf.ensure(sizeof(double) * J * R));
+            g.R = R;
+            g.N = N;
+            g.storage = storage;
+            g.J = J;
+            g.seed = seed;
+            g.draw_offset = off;
+            g.H = H;
+            g.idx = d_idx;
+            g.margin = d_margin;
+            g.err = derr;
+            g.stream = stream;
+            krpg::launch_fill(H, 1.0, J * R, stream);
+            prof_launches[KRPG_PROF_OTHER] += 1;
+            for (size_t p = 0; p < npos; ++p) {
+                const uint32_t k = inc[p];
+                const double* blk = dsmall + P + p * per_pos;
+                cudaEvent_t t0 = pbegin();
+                krpg::launch_etree_build(blk, blk + RR, f[k].tree.as<double>(), R, dQ, stream);
+                pend(KRPG_PROF_ETREE, t0, 1);
+                g.k = k;
+                g.pos = uint32_t(p);
+                g.I = f[k].I;
+                g.Q = dQ;
+                g.V = blk;
+                g.Z = f[k].tree.as<double>();
+                g.U = f[k].U.p;
+                t0 = pbegin();
+                const int nl = krpg::launch_position_grouped(g);
+                pend(KRPG_PROF_DRAWS, t0, nl);
+            }
+            if (d_prob) {
+                cudaEvent_t t0 = pbegin();
+                krpg::launch_probabilities_grouped(H, dsmall, R, J, double(rank), d_prob, stream);
+                pend(KRPG_PROF_PROB, t0, 1);
+            }
+            CK(cudaGetLastError());
+            int* eh = static_cast<int*>(errh.ensure(sizeof(int)));
+            CK(cudaMemcpyAsync(eh, derr, sizeof(int), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            presolve();
+            if (*eh) throw std::runtime_error("row_sample: degenerate distribution (C <= 0)");
+            return;
+        }
+
         for (size_t p = 0; p < npos; ++p) {
             const uint32_t k = inc[p];
             const double* blk = dsmall + P + p * per_pos;
@@ -450,7 +518,8 @@ int krpg_destroy(krpg_t h) {
         F.U.release();
         F.tree.release();
     }
-    for (DevBuf* b : {&h->tbuf, &h->small, &h->Q, &h->err, &h->sH, &h->sIdx, &h->sProb, &h->sMargin, &h->rowbuf})
+    for (DevBuf* b : {&h->tbuf, &h->small, &h->Q, &h->err, &h->sH, &h->sIdx, &h->sProb, &h->sMargin, &h->rowbuf,
+                      &h->gstate, &h->zbuf})
         b->release();
     h->up.release();
     h->errh.release();
@@ -779,6 +848,17 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset) {
                 h->prof_launches[c] = 0;
             }
         }
+    });
+}
+
+int krpg_set_option(krpg_t h, int option, int64_t value) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        std::lock_guard<std::mutex> lk(h->mu);
+        if (option == KRPG_OPT_GROUPED_DESCENT)
+            h->use_grouped = value != 0;
+        else
+            throw std::invalid_argument("krpg_set_option: unknown option");
     });
 }
 

@@ -50,6 +50,28 @@ struct DrawArgs {
 };
 void launch_draws(const DrawArgs& a);
 
+// ---- grouped (level-synchronous, DMMA) two-stage descent, descent_v2.cu ----
+struct GroupedArgs {
+    uint32_t R, N, k, pos, storage;
+    uint64_t J, seed, draw_offset, I;
+    double* H;           // J x R history / output rows
+    double* Zb;          // J x R scratch (z = h o V[:,u])
+    uint32_t* idx;       // J x N or null
+    double* margin;      // J or null
+    const double* Q;     // E-tree compact
+    const double* V;     // eigenvectors of G_{>k}
+    const double* Z;     // factor tree compact
+    const void* U;       // factor rows
+    uint32_t *perm_a, *perm_b, *node, *rank, *gstart, *cntL, *cntR;
+    double *low, *invc, *ud;
+    int* err;
+    cudaStream_t stream;
+};
+bool grouped_supported(uint32_t R, uint32_t mode);
+int launch_position_grouped(const GroupedArgs& g);
+void launch_probabilities_grouped(const double* H, const double* gp_packed, uint32_t R, uint64_t J,
+                                  double rank, double* prob, cudaStream_t s);
+
 // q_d = h_d^T G+ h_d / rank  (krp_sampler.cpp:143-149)
 void launch_probabilities(const double* H, const double* gp_packed, uint32_t R, uint64_t J,
                           double rank, double* prob, cudaStream_t s);

@@ -227,6 +227,10 @@ class KrpSampler:
         check(_lib.lib().krpg_update_factor_device(self._h, j, C.c_void_p(U.data_ptr()), int(U.shape[0])))
         self._dims[j] = int(U.shape[0])
 
+    def set_grouped_descent(self, on: bool) -> None:
+        """Choose the level-synchronous grouped DMMA descent (default) or the per-draw kernel."""
+        check(_lib.lib().krpg_set_option(self._h, _lib.OPT_GROUPED_DESCENT, 1 if on else 0))
+
     def rebuild(self, j: int) -> None:
         check(_lib.lib().krpg_rebuild(self._h, j))
 
