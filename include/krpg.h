@@ -137,7 +137,15 @@ int krpg_last_build_ms(krpg_t h, float* ms);
 #define KRPG_PROF_PROB 4        /* probability epilogue                  */
 #define KRPG_PROF_UPDATE 5      /* incremental updates                   */
 #define KRPG_PROF_OTHER 6       /* fills, gathers, conversions           */
-#define KRPG_PROF_N 8
+/* finer split of KRPG_PROF_DRAWS for the grouped descent (only timed when
+ * KRPG_OPT_PROFILE_DETAIL is set; their launches are counted under DRAWS) */
+#define KRPG_PROF_D_ROOT 8       /* normaliser passes (root of E / Z trees) */
+#define KRPG_PROF_D_LEVEL_CTA 9  /* shallow levels, cooperative CTA kernel */
+#define KRPG_PROF_D_LEVEL_WARP 10 /* deep levels, per-warp kernel          */
+#define KRPG_PROF_D_REGROUP 11   /* child-run scatter                      */
+#define KRPG_PROF_D_LEAF 12      /* leaf scan + h update                   */
+#define KRPG_PROF_D_MISC 13      /* stage init, z formation                */
+#define KRPG_PROF_N 16
 int krpg_profile_enable(krpg_t h, int on);
 /* ms and launches: arrays of KRPG_PROF_N (nullable); reset != 0 zeroes them */
 int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
@@ -147,6 +155,9 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
  * DMMA descent (R = 8..64, multiple of 8, two-stage mode); 0 forces the
  * per-draw-warp descent (the path used for every other rank / mode). */
 #define KRPG_OPT_GROUPED_DESCENT 1
+#define KRPG_OPT_PROFILE_DETAIL 2 /* per-kernel-type event timing inside the descent */
+#define KRPG_OPT_FUSED_DEEP 3     /* default 1: deep levels + leaf scan in one warp-local pass;
+                                     0: per-level global regrouping down to the leaves */
 int krpg_set_option(krpg_t h, int option, int64_t value);
 
 /* ---- host-only test support (no device needed) ---- */

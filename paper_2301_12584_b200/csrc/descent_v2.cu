@@ -49,7 +49,7 @@ struct Tiles {
 // upper triangle, segment_tree_sampler.hpp:111-115): bf[t(p,q)][s] holds
 // c_pq * G[8p + 4s + (lane&3)][8q + (lane>>2)], c = 2 off the diagonal tile.
 template <int NB>
-__device__ __forceinline__ void load_gfrag(const double* __restrict__ G, int lane,
+[[maybe_unused]] __device__ __forceinline__ void load_gfrag(const double* __restrict__ G, int lane,
                                            double (&bf)[Tiles<NB>::NT][2]) {
     constexpr int R = 8 * NB;
     const int r4 = lane & 3, cq = lane >> 2;
@@ -126,39 +126,161 @@ struct EvalArgs {
     double rank_div;        // EV_PROB: numerical rank
 };
 
-template <int NB, int MODE>
-__global__ void __launch_bounds__(WPB * 32) k_eval(EvalArgs a) {
-    constexpr int R = 8 * NB;
-    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
-    const int lane = threadIdx.x & 31;
-    const uint64_t base = (uint64_t(blockIdx.x) * WPB + (threadIdx.x >> 5)) * CHUNK;
-    if (base >= a.J) return;
-    const int cnt = a.J - base < uint64_t(CHUNK) ? int(a.J - base) : CHUNK;
-    const bool live = lane < cnt;
-    const uint32_t dl = live ? (a.perm ? a.perm[base + lane] : uint32_t(base + lane)) : 0u;
-    uint32_t vl = 0;
-    if (MODE == EV_LEVEL) vl = live ? a.node[dl] : 0xFFFFFFFFu;
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, vl, 1);
-    uint32_t starts = __ballot_sync(0xffffffffu, live && (lane == 0 || vl != prev));
+// Per-lane B-fragment addressing into a packed symmetric Gram (same for every
+// node): rowoff[p][s] = pack_index(row, 0) - row for row = 8p + 4s + (lane&3);
+// diag[p][s] = packed index of the diagonal-tile element (mirrored below the diagonal).
+template <int NB>
+struct FragAddr {
+    int rowoff[NB][2];
+    int diag[NB][2];
+    __device__ __forceinline__ explicit FragAddr(int lane) {
+        constexpr int R = 8 * NB;
+        const int r4 = lane & 3, cq = lane >> 2;
+#pragma unroll
+        for (int p = 0; p < NB; ++p)
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const int row = 8 * p + 4 * s + r4;
+                const int col = 8 * p + cq;
+                rowoff[p][s] = row * R - (row * (row - 1)) / 2 - row;
+                diag[p][s] = row <= col ? rowoff[p][s] + col : col * R - (col * (col - 1)) / 2 - col + row;
+            }
+    }
+};
 
-    double bf[Tiles<NB>::NT][2];
-    while (starts) {
-        const int rs = __ffs(starts) - 1;
-        starts &= starts - 1;
-        const int re = starts ? __ffs(starts) - 1 : cnt;
-        const uint32_t v = __shfl_sync(0xffffffffu, vl, rs);
-        const double* G = a.tree;
-        if (MODE == EV_LEVEL) {
-            if (is_leaf(a.topo, v)) continue;  // reached a leaf one level up (non-perfect tree)
-            G = a.tree + slot_of(2ull * v + 1) * P;
+// mass of the 8 X rows of a block against a packed Gram G (shared or global
+// memory; B fragments are gathered per block, nothing persists in registers).
+template <int NB>
+__device__ __forceinline__ double block_qf_packed(const double* G, const FragAddr<NB>& fa, const double* xr,
+                                                  int lane) {
+    const int r4 = lane & 3, cq = lane >> 2;
+    double av[NB][2];
+#pragma unroll
+    for (int p = 0; p < NB; ++p)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) av[p][s] = xr ? xr[8 * p + 4 * s + r4] : 0.0;
+    double y[NB][2];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) y[q][0] = y[q][1] = 0.0;
+#pragma unroll
+    for (int p = 0; p < NB; ++p) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const double gd = G[fa.diag[p][s]];
+            dmma_884(y[p][0], y[p][1], av[p][s], gd);
+#pragma unroll
+            for (int q = p + 1; q < NB; ++q) {
+                const double g = G[fa.rowoff[p][s] + 8 * q + cq];
+                dmma_884(y[q][0], y[q][1], av[p][s], g + g);
+            }
         }
-        load_gfrag<NB>(G, lane, bf);
-        for (int b0 = rs; b0 < re; b0 += 8) {
+    }
+    double part = 0.0;
+    if (xr) {
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const double2 xv = *reinterpret_cast<const double2*>(xr + 8 * q + 2 * r4);
+            part = fma(xv.x, y[q][0], part);
+            part = fma(xv.y, y[q][1], part);
+        }
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    return part;
+}
+
+constexpr int CB = WPB * 32;  // positions per CTA in the cooperative variant
+
+// Cooperative variant for shallow levels / single-matrix passes: the CTA's 128
+// sorted positions form few runs; each run's Gram is staged once into shared
+// memory by a 1-D TMA bulk copy (double-buffered: the next run's copy is in
+// flight while this run computes) and the run's 8-draw blocks are spread over
+// the CTA's warps. Child slots come from shared-memory counters, folded into
+// the global per-node counters with one atomic per run per side.
+template <int NB, int MODE>
+__global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
+    constexpr int R = 8 * NB;
+    constexpr uint32_t P = uint32_t(R) * (R + 1) / 2;
+    extern __shared__ __align__(128) double sG[];  // [2][P]
+    __shared__ uint32_t s_d[CB], s_v[CB];
+    __shared__ int s_rs[CB + 1];
+    __shared__ int s_nruns;
+    __shared__ uint32_t s_cnt[2], s_base[2];
+    __shared__ __align__(8) uint64_t bar[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t base = uint64_t(blockIdx.x) * CB;
+    const int cnt = a.J - base < uint64_t(CB) ? int(a.J - base) : CB;
+    if (tid < cnt) {
+        const uint32_t d = a.perm ? a.perm[base + tid] : uint32_t(base + tid);
+        s_d[tid] = d;
+        s_v[tid] = MODE == EV_LEVEL ? a.node[d] : 0u;
+    }
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    {  // run boundaries -> compact list s_rs
+        const bool flag = tid < cnt && (tid == 0 || s_v[tid] != s_v[tid - 1]);
+        const unsigned bal = __ballot_sync(0xffffffffu, flag);
+        __shared__ int wcount[WPB];
+        if (lane == 0) wcount[warp] = __popc(bal);
+        __syncthreads();
+        int off = 0;
+        for (int w = 0; w < warp; ++w) off += wcount[w];
+        if (flag) s_rs[off + __popc(bal & ((1u << lane) - 1u))] = tid;
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < WPB; ++w) tot += wcount[w];
+            s_nruns = tot;
+            s_rs[tot] = cnt;
+        }
+        __syncthreads();
+    }
+    const int nruns = s_nruns;
+    auto gsrc = [&](int r) -> const double* {
+        if (MODE != EV_LEVEL) return a.tree;
+        const uint32_t v = s_v[s_rs[r]];
+        if (is_leaf(a.topo, v)) return nullptr;
+        return a.tree + slot_of(2ull * v + 1) * uint64_t(P);
+    };
+    if (tid == 0 && nruns > 0) {
+        const double* g0 = gsrc(0);
+        if (g0) {
+            mbar_arrive_expect_tx(&bar[0], P * 8);
+            tma_load_1d(sG, g0, P * 8, &bar[0]);
+        }
+    }
+    const FragAddr<NB> fa(lane);
+    uint32_t phase[2] = {0u, 0u};
+    for (int r = 0; r < nruns; ++r) {
+        const int buf = r & 1;
+        if (tid == 0 && r + 1 < nruns) {  // prefetch the next run's Gram into the other buffer
+            const double* g1 = gsrc(r + 1);
+            if (g1) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&bar[buf ^ 1], P * 8);
+                tma_load_1d(sG + (buf ^ 1) * P, g1, P * 8, &bar[buf ^ 1]);
+            }
+        }
+        const double* gr = gsrc(r);
+        if (!gr) continue;  // draws parked at a leaf one level up
+        mbar_wait(&bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        const int rs = s_rs[r], re = s_rs[r + 1];
+        const uint32_t v = s_v[rs];
+        if (tid < 2) s_cnt[tid] = 0;
+        __syncthreads();
+        const double* G = sG + buf * P;
+        const int nblk = (re - rs + 7) >> 3;
+        for (int b = warp; b < nblk; b += WPB) {
+            const int b0 = rs + 8 * b;
             const int n = min(8, re - b0);
             const int m = lane >> 2;
             const bool valid = m < n;
-            const uint32_t dd = __shfl_sync(0xffffffffu, dl, (b0 + m) & 31);
-            const double mass = block_qf<NB>(bf, valid ? a.X + uint64_t(dd) * R : nullptr, lane);
+            const uint32_t dd = valid ? s_d[b0 + m] : 0u;
+            const double mass = block_qf_packed<NB>(G, fa, valid ? a.X + uint64_t(dd) * R : nullptr, lane);
             const bool owner = valid && (lane & 3) == 0;
             if (MODE == EV_ROOT) {
                 if (owner) {
@@ -169,11 +291,10 @@ __global__ void __launch_bounds__(WPB * 32) k_eval(EvalArgs a) {
                 if (owner) a.prob[dd] = mass / a.rank_div;
             } else {
                 bool left = false;
-                double lo = 0.0, u = 0.0, cutoff = 0.0;
+                double cutoff = 0.0;
                 if (owner) {
-                    lo = a.low[dd];
-                    u = a.ud[dd];
-                    cutoff = lo + a.invc[dd] * mass;
+                    const double u = a.ud[dd];
+                    cutoff = a.low[dd] + a.invc[dd] * mass;
                     left = cutoff >= u;
                     if (a.margin) a.margin[dd] = fmin(a.margin[dd], fabs(cutoff - u));
                 }
@@ -181,8 +302,8 @@ __global__ void __launch_bounds__(WPB * 32) k_eval(EvalArgs a) {
                 const unsigned rm = __ballot_sync(0xffffffffu, owner && !left);
                 uint32_t bl = 0, br = 0;
                 if (lane == 0) {
-                    if (lm) bl = atomicAdd(a.cntL + v, uint32_t(__popc(lm)));
-                    if (rm) br = atomicAdd(a.cntR + v, uint32_t(__popc(rm)));
+                    if (lm) bl = atomicAdd(&s_cnt[0], uint32_t(__popc(lm)));
+                    if (rm) br = atomicAdd(&s_cnt[1], uint32_t(__popc(rm)));
                 }
                 bl = __shfl_sync(0xffffffffu, bl, 0);
                 br = __shfl_sync(0xffffffffu, br, 0);
@@ -199,6 +320,99 @@ __global__ void __launch_bounds__(WPB * 32) k_eval(EvalArgs a) {
                 }
             }
         }
+        __syncthreads();
+        if (MODE == EV_LEVEL) {
+            if (tid == 0) {
+                s_base[0] = s_cnt[0] ? atomicAdd(a.cntL + v, s_cnt[0]) : 0u;
+                s_base[1] = s_cnt[1] ? atomicAdd(a.cntR + v, s_cnt[1]) : 0u;
+            }
+            __syncthreads();
+            for (int t = rs + tid; t < re; t += CB) {
+                const uint32_t d = s_d[t];
+                a.rank[d] += (a.node[d] & 1u) ? s_base[0] : s_base[1];
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Per-warp variant for deep levels (runs of a few draws, Grams read once from
+// HBM): B fragments gathered straight from global memory per block, the next
+// run's Gram prefetched into L2 while this run computes, and all runs' child
+// slots claimed with one warp-wide round of atomics at the end.
+template <int NB>
+__global__ void __launch_bounds__(WPB * 32) k_eval_warp(EvalArgs a) {
+    constexpr int R = 8 * NB;
+    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
+    const int lane = threadIdx.x & 31;
+    const uint64_t base = (uint64_t(blockIdx.x) * WPB + (threadIdx.x >> 5)) * CHUNK;
+    if (base >= a.J) return;
+    const int cnt = a.J - base < uint64_t(CHUNK) ? int(a.J - base) : CHUNK;
+    const bool live = lane < cnt;
+    const uint32_t dl = live ? a.perm[base + lane] : 0u;
+    const uint32_t vl = live ? a.node[dl] : 0xFFFFFFFFu;
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, vl, 1);
+    const uint32_t starts0 = __ballot_sync(0xffffffffu, live && (lane == 0 || vl != prev));
+    const FragAddr<NB> fa(lane);
+    uint32_t leftm = 0, movedm = 0;
+    uint32_t starts = starts0;
+    while (starts) {
+        const int rs = __ffs(starts) - 1;
+        starts &= starts - 1;
+        const int re = starts ? __ffs(starts) - 1 : cnt;
+        const uint32_t v = __shfl_sync(0xffffffffu, vl, rs);
+        if (is_leaf(a.topo, v)) continue;
+        if (starts) {  // warm L2 with the next run's Gram (prefetch.global.L2)
+            const uint32_t vn = __shfl_sync(0xffffffffu, vl, __ffs(starts) - 1);
+            if (!is_leaf(a.topo, vn)) {
+                const char* gn = reinterpret_cast<const char*>(a.tree + slot_of(2ull * vn + 1) * P);
+                for (uint32_t o = lane * 128; o < P * 8; o += 32 * 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(gn + o));
+            }
+        }
+        const double* G = a.tree + slot_of(2ull * v + 1) * P;
+        for (int b0 = rs; b0 < re; b0 += 8) {
+            const int n = min(8, re - b0);
+            const int m = lane >> 2;
+            const bool valid = m < n;
+            const uint32_t dd = __shfl_sync(0xffffffffu, dl, (b0 + m) & 31);
+            const double mass = block_qf_packed<NB>(G, fa, valid ? a.X + uint64_t(dd) * R : nullptr, lane);
+            const bool owner = valid && (lane & 3) == 0;
+            bool left = false;
+            if (owner) {
+                const double u = a.ud[dd];
+                const double cutoff = a.low[dd] + a.invc[dd] * mass;
+                left = cutoff >= u;
+                if (a.margin) a.margin[dd] = fmin(a.margin[dd], fabs(cutoff - u));
+                a.node[dd] = left ? 2 * v + 1 : 2 * v + 2;
+                if (!left) a.low[dd] = cutoff;
+            }
+            const unsigned lm = __ballot_sync(0xffffffffu, owner && left);
+#pragma unroll
+            for (int mm = 0; mm < 8; ++mm)
+                if (mm < n) leftm |= ((lm >> (4 * mm)) & 1u) << (b0 + mm);
+            movedm |= (n == 32 ? 0xffffffffu : ((1u << n) - 1u)) << b0;
+        }
+    }
+    // one round of atomics for every run of the warp, then slots
+    if (live && ((movedm >> lane) & 1u)) {
+        const uint32_t le = starts0 & ((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
+        const int rs = 31 - __clz(le);
+        const uint32_t gt = starts0 & ~((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
+        const int re = gt ? __ffs(gt) - 1 : cnt;
+        const uint32_t runm = (re == 32 ? 0xffffffffu : ((1u << re) - 1u)) & ~((1u << rs) - 1u);
+        const bool left = (leftm >> lane) & 1u;
+        const uint32_t side = (left ? leftm : (movedm & ~leftm)) & runm;
+        uint32_t bl = 0, br = 0;
+        if (lane == rs) {
+            const uint32_t nl = __popc(leftm & runm), nr = __popc(movedm & ~leftm & runm);
+            if (nl) bl = atomicAdd(a.cntL + vl, nl);
+            if (nr) br = atomicAdd(a.cntR + vl, nr);
+        }
+        const unsigned mv = __activemask();
+        bl = __shfl_sync(mv, bl, rs);
+        br = __shfl_sync(mv, br, rs);
+        a.rank[dl] = (left ? bl : br) + __popc(side & ((1u << lane) - 1u));
     }
 }
 
@@ -356,46 +570,848 @@ __global__ void __launch_bounds__(WPB * 32) k_leaf(LeafArgs a) {
     }
 }
 
+// Leaf scan, streaming version: each warp streams the rows of its runs' leaves
+// HBM -> shared memory through a 3-stage 1-D TMA ring (16 rows per stage, rows
+// padded for conflict-light fragment reads), computes the 16 x 8 mass tile of
+// every 8-draw block on DMMA, and lets each draw's lane continue its sequential
+// cumulative scan (segment_tree_sampler.cpp:284-292) over those 16 rows. Scan
+// state (cum, pick, last nonzero, margin) lives in the lane that owns the draw's
+// sorted position, so no per-leaf mass buffer is needed.
+template <int NB, typename T>
+struct LeafCfg2 {
+    static constexpr int R = 8 * NB;
+    static constexpr int CH = 16;
+    static constexpr int STAGES = 3;
+    static constexpr int ROWB = R * int(sizeof(T));
+    static constexpr int RS = ROWB;  // unpadded: one bulk copy per chunk
+    static constexpr int CHB = CH * RS;
+    static constexpr int WARP_BYTES = (STAGES * CHB + CH * 8 * 8 + STAGES * 8 + 127) / 128 * 128;
+    static constexpr int SMEM = WPB * WARP_BYTES;
+};
+
+template <int NB, typename T>
+__global__ void __launch_bounds__(WPB * 32) k_leaf2(LeafArgs a) {
+    using C = LeafCfg2<NB, T>;
+    constexpr int R = 8 * NB;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char* ring = smem_raw + warp * C::WARP_BYTES;
+    double* msm = reinterpret_cast<double*>(ring + C::STAGES * C::CHB);  // [CH][8]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + C::STAGES * C::CHB + C::CH * 8 * 8);
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const uint64_t base = (uint64_t(blockIdx.x) * WPB + warp) * CHUNK;
+    if (base >= a.J) return;
+    const int cnt = a.J - base < uint64_t(CHUNK) ? int(a.J - base) : CHUNK;
+    const bool live = lane < cnt;
+    const uint32_t dl = live ? a.perm[base + lane] : 0u;
+    const uint32_t vl = live ? a.node[dl] : 0xFFFFFFFFu;
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, vl, 1);
+    const uint32_t starts0 = __ballot_sync(0xffffffffu, live && (lane == 0 || vl != prev));
+    // lane-owned scan state of the draw at sorted position base + lane
+    double cum = 0.0, ic = 0.0, u = 0.0, mg = 0.0;
+    if (live) {
+        cum = a.low[dl];
+        ic = a.invc[dl];
+        u = a.ud[dl];
+        mg = a.margin ? a.margin[dl] : 0.0;
+    }
+    uint64_t pick = ~uint64_t{0}, last_nz = ~uint64_t{0};
+    const T* U = static_cast<const T*>(a.U);
+
+    auto run_rows = [&](uint32_t v, uint64_t& first, uint64_t& last) {
+        const uint64_t l = leaf_index(a.topo, v);
+        first = l * a.topo.F;
+        last = first + a.topo.F < a.topo.I ? first + a.topo.F : a.topo.I;
+    };
+    // producer cursor: current run (bit set of remaining run starts) and row
+    uint32_t pstarts = starts0;
+    uint64_t prow = 0, plast = 0;
+    bool pmore = pstarts != 0;
+    if (pmore) {
+        const int rs = __ffs(pstarts) - 1;
+        pstarts &= pstarts - 1;
+        run_rows(__shfl_sync(0xffffffffu, vl, rs), prow, plast);
+    }
+    uint32_t issued = 0;
+    auto produce = [&]() {
+        if (!pmore) return;
+        const int st = int(issued % C::STAGES);
+        const uint64_t left = plast - prow;
+        const uint32_t nrows = left < uint64_t(C::CH) ? uint32_t(left) : uint32_t(C::CH);
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&bars[st], nrows * C::ROWB);
+            if (C::RS == C::ROWB)  // one contiguous bulk copy per chunk
+                tma_load_1d(ring + st * C::CHB, U + prow * R, nrows * C::ROWB, &bars[st]);
+        }
+        __syncwarp();
+        if (C::RS != C::ROWB && uint32_t(lane) < nrows)
+            tma_load_1d(ring + st * C::CHB + lane * C::RS, U + (prow + lane) * R, C::ROWB, &bars[st]);
+        ++issued;
+        prow += C::CH;
+        if (prow >= plast) {
+            if (pstarts) {
+                const int rs = __ffs(pstarts) - 1;
+                pstarts &= pstarts - 1;
+                run_rows(__shfl_sync(0xffffffffu, vl, rs), prow, plast);
+            } else {
+                pmore = false;
+            }
+        }
+    };
+    for (int s = 0; s < C::STAGES - 1; ++s) produce();
+
+    const int r4 = lane & 3, m8 = lane >> 2;
+    uint32_t cstarts = starts0;
+    uint32_t chunk_i = 0;
+    while (cstarts) {
+        const int rs = __ffs(cstarts) - 1;
+        cstarts &= cstarts - 1;
+        const int re = cstarts ? __ffs(cstarts) - 1 : cnt;
+        uint64_t first, last;
+        run_rows(__shfl_sync(0xffffffffu, vl, rs), first, last);
+        for (uint64_t r0 = first; r0 < last; r0 += C::CH, ++chunk_i) {
+            produce();
+            const int st = int(chunk_i % C::STAGES);
+            mbar_wait(&bars[st], (chunk_i / C::STAGES) & 1u);
+            const int nr = last - r0 < uint64_t(C::CH) ? int(last - r0) : C::CH;
+            const unsigned char* buf = ring + st * C::CHB;
+            for (int b0 = rs; b0 < re; b0 += 8) {
+                const int n = min(8, re - b0);
+                const bool valid = m8 < n;
+                const uint32_t dd = __shfl_sync(0xffffffffu, dl, (b0 + m8) & 31);
+                double zb[2 * NB];
+#pragma unroll
+                for (int s = 0; s < 2 * NB; ++s) zb[s] = valid ? a.Z[uint64_t(dd) * R + 4 * s + r4] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const int row = 8 * mt + m8;
+                    const bool rv = row < nr;
+                    const T* up = reinterpret_cast<const T*>(buf + (rv ? row : 0) * C::RS) + r4;
+                    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                    for (int s = 0; s < 2 * NB; ++s) dmma_884(acc0, acc1, rv ? static_cast<double>(up[4 * s]) : 0.0, zb[s]);
+                    msm[(8 * mt + m8) * 8 + 2 * r4] = acc0 * acc0;
+                    msm[(8 * mt + m8) * 8 + 2 * r4 + 1] = acc1 * acc1;
+                }
+                __syncwarp();
+                if (lane >= b0 && lane < b0 + n && pick == ~uint64_t{0}) {
+                    const int col = lane - b0;
+                    for (int i = 0; i < nr; ++i) {
+                        const double mm = ic * msm[i * 8 + col];
+                        if (mm > 0.0) last_nz = r0 + i;
+                        cum += mm;
+                        mg = fmin(mg, fabs(cum - u));
+                        if (cum >= u) {
+                            pick = r0 + i;
+                            break;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            fence_proxy_async();
+            __syncwarp();
+        }
+        // finalize the run's draws (fallback :292), index, margin
+        const bool mine = lane >= rs && lane < re;
+        if (mine) {
+            if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : last - 1;
+            if (a.margin) a.margin[dl] = mg;
+            if (a.idx) a.idx[uint64_t(dl) * a.N + a.k] = uint32_t(pick);
+        }
+        // h *= U[pick]  (krp_sampler.cpp:137-138)
+        for (int t = rs; t < re; ++t) {
+            const uint32_t dt = __shfl_sync(0xffffffffu, dl, t);
+            const uint64_t pt = __shfl_sync(0xffffffffu, pick, t);
+            for (int c = lane; c < R; c += 32) a.H[uint64_t(dt) * R + c] *= static_cast<double>(U[pt * R + c]);
+        }
+    }
+}
+
+struct DeepArgs {
+    uint64_t J;
+    uint32_t N, k, level0;
+    const uint32_t* perm;
+    const uint32_t* node;
+    const double* low;
+    const double* invc;
+    const double* ud;
+    double* margin;
+    const double* X;   // z rows (J x R)
+    double* H;         // history rows (updated with the drawn row)
+    uint32_t* idx;
+    uint32_t* pick;    // per draw picked row (for the h update pass)
+    const void* U;
+    const double* tree;
+    Topo topo;
+};
+
+// Mass x^T G x of up to 3 draws of one run on the CUDA cores (a run of 1-3
+// draws would waste 5/8+ of every DMMA): lane b owns x_b, rows of the packed
+// Gram are streamed 8 at a time (16 coalesced loads in flight per lane), x_a is
+// a shared-memory broadcast.
+template <int S>
+__device__ __forceinline__ void small_run_qf(const double* __restrict__ G, const double (&xr)[3][S],
+                                             const double* xs /*[3][R]*/, int n, uint32_t R, int lane,
+                                             double (&mass)[3]) {
+    double acc[3][S];
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[t][s] = 0.0;
+    constexpr int RB = 8;
+    for (uint32_t a0 = 0; a0 < R; a0 += RB) {
+        double g[RB][S];
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            const uint32_t ar = a0 + j;
+            const uint32_t off = ar * R - (ar * (ar - 1)) / 2;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const uint32_t b = uint32_t(lane) + 32u * s;
+                g[j][s] = (ar < R && b >= ar && b < R) ? __ldg(G + off + (b - ar)) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            const uint32_t ar = a0 + j;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                if (t >= n) break;
+                const double xa = ar < R ? xs[t * R + ar] : 0.0;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const uint32_t b = uint32_t(lane) + 32u * s;
+                    acc[t][s] = fma(g[j][s], b == ar ? xa : xa + xa, acc[t][s]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        double p = 0.0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) p = fma(acc[t][s], xr[t][s], p);
+        mass[t] = warp_sum(p);
+    }
+}
+
+// Deep levels + leaf scan, fused: each warp carries the 32 draws at its sorted
+// positions from level `level0` to the leaves with warp-local regrouping (a run
+// splits into its left then right draws: a stable partition done with ballots
+// and one shuffle permutation per level), so no global scatter, counters or
+// extra launches are needed where runs hold only a handful of draws. Runs of
+// >= 4 draws use the DMMA block kernel, smaller ones the CUDA-core path. The
+// leaf scan walks the leaf 8 rows at a time (DMMA U_rows x Z^T) and stops as
+// soon as every draw of the block has picked its row.
+template <int NB, typename T>
+__global__ void __launch_bounds__(WPB * 32) k_deep(DeepArgs a) {
+    constexpr int R = 8 * NB;
+    constexpr int S = (R + 31) / 32;
+    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
+    __shared__ double xsm[WPB][3 * R];
+    __shared__ uint32_t perm_sm[WPB][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t base = (uint64_t(blockIdx.x) * WPB + warp) * 32;
+    if (base >= a.J) return;
+    const int cnt = a.J - base < 32ull ? int(a.J - base) : 32;
+    const bool live = lane < cnt;
+    uint32_t d = live ? a.perm[base + lane] : 0u;
+    uint32_t v = live ? a.node[d] : 0xFFFFFFFFu;
+    double lo = 0.0, ic = 0.0, uu = 0.0, mg = 0.0;
+    if (live) {
+        lo = a.low[d];
+        ic = a.invc[d];
+        uu = a.ud[d];
+        mg = a.margin ? a.margin[d] : 0.0;
+    }
+    const FragAddr<NB> fa(lane);
+    const unsigned below = (1u << lane) - 1u;
+    double* xs = xsm[warp];
+
+    for (uint32_t lev = a.level0; lev < a.topo.d; ++lev) {
+        const uint32_t prevv = __shfl_up_sync(0xffffffffu, v, 1);
+        const uint32_t starts = __ballot_sync(0xffffffffu, live && (lane == 0 || v != prevv));
+        double mine = 0.0;
+        uint32_t st = starts;
+        while (st) {
+            const int rs = __ffs(st) - 1;
+            st &= st - 1;
+            const int re = st ? __ffs(st) - 1 : cnt;
+            const uint32_t vr = __shfl_sync(0xffffffffu, v, rs);
+            if (is_leaf(a.topo, vr)) continue;
+            const double* G = a.tree + slot_of(2ull * vr + 1) * P;
+            if (st) {  // warm L2 with the next run's Gram
+                const uint32_t vn = __shfl_sync(0xffffffffu, v, __ffs(st) - 1);
+                if (!is_leaf(a.topo, vn)) {
+                    const char* gn = reinterpret_cast<const char*>(a.tree + slot_of(2ull * vn + 1) * P);
+                    for (uint32_t o = lane * 128; o < P * 8; o += 32 * 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(gn + o));
+                }
+            }
+            const int n = re - rs;
+            if (n >= 4) {
+                for (int b0 = rs; b0 < re; b0 += 8) {
+                    const int nb = min(8, re - b0);
+                    const int m = lane >> 2;
+                    const uint32_t dd = __shfl_sync(0xffffffffu, d, (b0 + m) & 31);
+                    const double mass = block_qf_packed<NB>(G, fa, m < nb ? a.X + uint64_t(dd) * R : nullptr, lane);
+                    const double mj = __shfl_sync(0xffffffffu, mass, (4 * (lane - b0)) & 31);
+                    if (lane >= b0 && lane < b0 + nb) mine = mj;
+                }
+            } else {
+                double xr[3][S];
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    const uint32_t dt = __shfl_sync(0xffffffffu, d, (rs + t) & 31);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const uint32_t b = lane + 32u * s;
+                        const double x = (t < n && b < uint32_t(R)) ? a.X[uint64_t(dt) * R + b] : 0.0;
+                        xr[t][s] = x;
+                        if (b < uint32_t(R)) xs[t * R + b] = x;
+                    }
+                }
+                __syncwarp();
+                double ms[3];
+                small_run_qf<S>(G, xr, xs, n, R, lane, ms);
+                __syncwarp();
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+                    if (lane == rs + t && t < n) mine = ms[t];
+            }
+        }
+        // branch decisions (row_sample :269-277) and the warp-local stable split
+        const bool moved = live && !is_leaf(a.topo, v);
+        bool left = false;
+        if (moved) {
+            const double cutoff = lo + ic * mine;
+            left = cutoff >= uu;
+            mg = fmin(mg, fabs(cutoff - uu));
+            if (!left) lo = cutoff;
+        }
+        const uint32_t leftm = __ballot_sync(0xffffffffu, moved && left);
+        const uint32_t movedm = __ballot_sync(0xffffffffu, moved);
+        int newpos = lane;
+        if (moved) {
+            const uint32_t le = starts & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
+            const int rs = 31 - __clz(le);
+            const uint32_t gt = starts & ~(lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
+            const int re = gt ? __ffs(gt) - 1 : cnt;
+            const uint32_t runm = (re == 32 ? 0xffffffffu : ((1u << re) - 1u)) & ~((1u << rs) - 1u);
+            const int nl = __popc(leftm & runm);
+            newpos = left ? rs + __popc(leftm & runm & below) : rs + nl + __popc(movedm & ~leftm & runm & below);
+            v = left ? 2 * v + 1 : 2 * v + 2;
+        }
+        perm_sm[warp][newpos] = uint32_t(lane);
+        __syncwarp();
+        const int src = live ? int(perm_sm[warp][lane]) : lane;
+        __syncwarp();
+        d = __shfl_sync(0xffffffffu, d, src);
+        v = __shfl_sync(0xffffffffu, v, src);
+        lo = __shfl_sync(0xffffffffu, lo, src);
+        ic = __shfl_sync(0xffffffffu, ic, src);
+        uu = __shfl_sync(0xffffffffu, uu, src);
+        mg = __shfl_sync(0xffffffffu, mg, src);
+    }
+
+    // ---------------- leaf scan (segment_tree_sampler.cpp:281-292) ----------------
+    const T* U = static_cast<const T*>(a.U);
+    const int r4 = lane & 3, m8 = lane >> 2;
+    const uint32_t prevv = __shfl_up_sync(0xffffffffu, v, 1);
+    uint32_t st = __ballot_sync(0xffffffffu, live && (lane == 0 || v != prevv));
+    uint64_t pick = ~uint64_t{0}, last_nz = ~uint64_t{0};
+    double cum = lo;
+    while (st) {
+        const int rs = __ffs(st) - 1;
+        st &= st - 1;
+        const int re = st ? __ffs(st) - 1 : cnt;
+        const uint32_t vr = __shfl_sync(0xffffffffu, v, rs);
+        const uint64_t l = leaf_index(a.topo, vr);
+        const uint64_t first = l * a.topo.F;
+        const uint64_t last = first + a.topo.F < a.topo.I ? first + a.topo.F : a.topo.I;
+        if (st) {  // warm L2 with the first half of the next run's leaf rows
+            const uint32_t vn = __shfl_sync(0xffffffffu, v, __ffs(st) - 1);
+            const uint64_t fn = leaf_index(a.topo, vn) * a.topo.F;
+            const uint64_t ln = fn + a.topo.F < a.topo.I ? fn + a.topo.F : a.topo.I;
+            const uint64_t bytes = ((ln - fn + 1) / 2) * R * sizeof(T);
+            const char* p = reinterpret_cast<const char*>(U + fn * R);
+            for (uint64_t o = uint64_t(lane) * 128; o < bytes; o += 32 * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+        }
+        for (int b0 = rs; b0 < re; b0 += 8) {
+            const int nb = min(8, re - b0);
+            const bool mine_lane = lane >= b0 && lane < b0 + nb;
+            const int jj = (lane - b0) & 7;
+            const uint32_t dd = __shfl_sync(0xffffffffu, d, (b0 + m8) & 31);
+            double zb[2 * NB];
+#pragma unroll
+            for (int s = 0; s < 2 * NB; ++s) zb[s] = m8 < nb ? a.X[uint64_t(dd) * R + 4 * s + r4] : 0.0;
+            for (uint64_t r0 = first; r0 < last; r0 += 16) {
+                if (!__any_sync(0xffffffffu, mine_lane && pick == ~uint64_t{0})) break;  // all picked: stop reading
+                double av[2][2 * NB];  // two 8-row tiles in flight
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const uint64_t row = r0 + 8 * h2 + m8;
+                    const bool rv = row < last;
+                    const T* up = U + (rv ? row : first) * R + r4;
+#pragma unroll
+                    for (int s = 0; s < 2 * NB; ++s) av[h2][s] = rv ? static_cast<double>(__ldg(up + 4 * s)) : 0.0;
+                }
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                    for (int s = 0; s < 2 * NB; ++s) dmma_884(acc0, acc1, av[h2][s], zb[s]);
+                    const double q0 = acc0 * acc0, q1 = acc1 * acc1;
+                    const uint64_t rb = r0 + 8 * h2;
+#pragma unroll
+                    for (int rr = 0; rr < 8; ++rr) {
+                        const double w0 = __shfl_sync(0xffffffffu, q0, rr * 4 + (jj >> 1));
+                        const double w1 = __shfl_sync(0xffffffffu, q1, rr * 4 + (jj >> 1));
+                        if (mine_lane && pick == ~uint64_t{0} && rb + rr < last) {
+                            const double mm = ic * ((jj & 1) ? w1 : w0);
+                            if (mm > 0.0) last_nz = rb + rr;
+                            cum += mm;
+                            mg = fmin(mg, fabs(cum - uu));
+                            if (cum >= uu) pick = rb + rr;
+                        }
+                    }
+                }
+            }
+            if (mine_lane) {
+                if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : last - 1;
+                if (a.margin) a.margin[d] = mg;
+                if (a.idx) a.idx[uint64_t(d) * a.N + a.k] = uint32_t(pick);
+                a.pick[d] = uint32_t(pick);  // h *= U[pick] runs as its own parallel pass
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_deep2: the fused deep-levels + leaf pass with every run's operand staged
+// into a per-warp shared-memory buffer by cp.async in ONE round trip (a Gram:
+// P doubles; a leaf: 32 padded rows per chunk) while the next run's operand is
+// pulled into L2. All arithmetic then runs out of shared memory.
+// ---------------------------------------------------------------------------
+template <int NB, typename T>
+struct DeepCfg {
+    static constexpr int R = 8 * NB;
+    static constexpr int P = R * (R + 1) / 2;
+    static constexpr int GB = (P * 8 + 15) / 16 * 16;
+    static constexpr int LROWS = 32;
+    static constexpr int ROWB = R * int(sizeof(T));
+    static constexpr int RSP = ROWB + 16;  // padded leaf row stride (conflict-light fragments)
+    static constexpr int LB = LROWS * RSP;
+    static constexpr int BUF = ((GB > LB ? GB : LB) + 127) / 128 * 128;
+    static constexpr int XS = 3 * R * 8;
+    static constexpr int WARP_BYTES = BUF + XS + 128;
+    static constexpr int SMEM = WPB * WARP_BYTES;
+};
+
+// small runs (<= 3 draws) from a shared-memory Gram: lane b owns x_b
+template <int S>
+__device__ __forceinline__ void small_run_qf_sm(const double* Gs, const double (&xr)[3][S], const double* xs, int n,
+                                                uint32_t R, int lane, double (&mass)[3]) {
+    double acc[3][S];
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[t][s] = 0.0;
+    uint32_t off = 0;
+    for (uint32_t ar = 0; ar < R; ++ar) {
+        double g[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const uint32_t b = uint32_t(lane) + 32u * s;
+            g[s] = (b >= ar && b < R) ? Gs[off + (b - ar)] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            if (t >= n) break;
+            const double xa = xs[t * R + ar];
+            const double xa2 = xa + xa;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const uint32_t b = uint32_t(lane) + 32u * s;
+                acc[t][s] = fma(g[s], b == ar ? xa : xa2, acc[t][s]);
+            }
+        }
+        off += R - ar;
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        double p = 0.0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) p = fma(acc[t][s], xr[t][s], p);
+        mass[t] = warp_sum(p);
+    }
+}
+
+// Same quadratic forms for exactly ND draws: acc_b = sum_{a<=b} G_ab (2 x_a)
+// (x2s holds 2x), then mass = sum_b x_b (acc_b - G_bb x_b). The row loop is
+// split at 32-column boundaries so only one register slot needs a predicate.
+template <int NB, int ND>
+__device__ __forceinline__ void small_qf(const double* Gs, const double* x2s, const double (&xr)[3][(8 * NB + 31) / 32],
+                                         int lane, double (&mass)[3]) {
+    constexpr int R = 8 * NB;
+    constexpr int S = (R + 31) / 32;
+    double acc[ND][S];
+#pragma unroll
+    for (int t = 0; t < ND; ++t)
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[t][s] = 0.0;
+    int off = 0;
+#pragma unroll
+    for (int kb = 0; kb < S; ++kb) {
+        const int a_end = R < 32 * (kb + 1) ? R : 32 * (kb + 1);
+#pragma unroll 4
+        for (int ar = 32 * kb; ar < a_end; ++ar) {
+            double g[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int b = lane + 32 * s;
+                if (s < kb) {
+                    g[s] = 0.0;
+                } else if (s == kb) {
+                    g[s] = (b >= ar && b < R) ? Gs[off + b - ar] : 0.0;
+                } else {
+                    g[s] = b < R ? Gs[off + b - ar] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < ND; ++t) {
+                const double xa2 = x2s[t * R + ar];
+#pragma unroll
+                for (int s = kb; s < S; ++s) acc[t][s] = fma(g[s], xa2, acc[t][s]);
+            }
+            off += R - ar;
+        }
+    }
+    double gbb[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int b = lane + 32 * s;
+        gbb[s] = b < R ? Gs[b * R - (b * (b - 1)) / 2] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < ND; ++t) {
+        double p = 0.0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) p = fma(xr[t][s], acc[t][s] - gbb[s] * xr[t][s], p);
+        mass[t] = warp_sum(p);
+    }
+}
+
+template <int NB, typename T>
+__global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
+    using C = DeepCfg<NB, T>;
+    constexpr int R = 8 * NB;
+    constexpr int S = (R + 31) / 32;
+    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char* wbase = smem_raw + warp * C::WARP_BYTES;
+    unsigned char* buf = wbase;
+    double* xs = reinterpret_cast<double*>(wbase + C::BUF);
+    uint32_t* perm_sm = reinterpret_cast<uint32_t*>(wbase + C::BUF + C::XS);
+    const uint64_t base = (uint64_t(blockIdx.x) * WPB + warp) * 32;
+    if (base >= a.J) return;
+    const int cnt = a.J - base < 32ull ? int(a.J - base) : 32;
+    const bool live = lane < cnt;
+    uint32_t d = live ? a.perm[base + lane] : 0u;
+    uint32_t v = live ? a.node[d] : 0xFFFFFFFFu;
+    double lo = 0.0, ic = 0.0, uu = 0.0, mg = 0.0;
+    if (live) {
+        lo = a.low[d];
+        ic = a.invc[d];
+        uu = a.ud[d];
+        mg = a.margin ? a.margin[d] : 0.0;
+    }
+    const FragAddr<NB> fa(lane);
+    const unsigned below = (1u << lane) - 1u;
+    const double* Gs = reinterpret_cast<const double*>(buf);
+
+    for (uint32_t lev = a.level0; lev < a.topo.d; ++lev) {
+        const uint32_t prevv = __shfl_up_sync(0xffffffffu, v, 1);
+        const uint32_t starts = __ballot_sync(0xffffffffu, live && (lane == 0 || v != prevv));
+        double mine = 0.0;
+        uint32_t st = starts;
+        while (st) {
+            const int rs = __ffs(st) - 1;
+            st &= st - 1;
+            const int re = st ? __ffs(st) - 1 : cnt;
+            const uint32_t vr = __shfl_sync(0xffffffffu, v, rs);
+            if (is_leaf(a.topo, vr)) continue;
+            {  // stage this run's Gram, warm L2 with the next one
+                const char* g = reinterpret_cast<const char*>(a.tree + slot_of(2ull * vr + 1) * P);
+                for (int o = lane * 16; o < C::GB; o += 32 * 16) cp_async16(buf + o, g + o);
+                cp_async_commit();
+                if (st) {
+                    const uint32_t vn = __shfl_sync(0xffffffffu, v, __ffs(st) - 1);
+                    if (!is_leaf(a.topo, vn)) {
+                        const char* gn = reinterpret_cast<const char*>(a.tree + slot_of(2ull * vn + 1) * P);
+                        for (int o = lane * 128; o < C::GB; o += 32 * 128)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(gn + o));
+                    }
+                }
+            }
+            const int n = re - rs;
+            if (n >= 4) {
+                cp_async_wait_all();
+                __syncwarp();
+                for (int b0 = rs; b0 < re; b0 += 8) {
+                    const int nb = min(8, re - b0);
+                    const int m = lane >> 2;
+                    const uint32_t dd = __shfl_sync(0xffffffffu, d, (b0 + m) & 31);
+                    const double mass = block_qf_packed<NB>(Gs, fa, m < nb ? a.X + uint64_t(dd) * R : nullptr, lane);
+                    const double mj = __shfl_sync(0xffffffffu, mass, (4 * (lane - b0)) & 31);
+                    if (lane >= b0 && lane < b0 + nb) mine = mj;
+                }
+            } else {
+                double xr[3][S];
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    const uint32_t dt = __shfl_sync(0xffffffffu, d, (rs + t) & 31);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const uint32_t b = lane + 32u * s;
+                        const double x = (t < n && b < uint32_t(R)) ? a.X[uint64_t(dt) * R + b] : 0.0;
+                        xr[t][s] = x;
+                        if (b < uint32_t(R)) xs[t * R + b] = x + x;
+                    }
+                }
+                cp_async_wait_all();
+                __syncwarp();
+                double ms[3] = {0.0, 0.0, 0.0};
+                if (n == 1)
+                    small_qf<NB, 1>(Gs, xs, xr, lane, ms);
+                else if (n == 2)
+                    small_qf<NB, 2>(Gs, xs, xr, lane, ms);
+                else
+                    small_qf<NB, 3>(Gs, xs, xr, lane, ms);
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+                    if (lane == rs + t && t < n) mine = ms[t];
+            }
+            __syncwarp();
+        }
+        const bool moved = live && !is_leaf(a.topo, v);
+        bool left = false;
+        if (moved) {
+            const double cutoff = lo + ic * mine;
+            left = cutoff >= uu;
+            mg = fmin(mg, fabs(cutoff - uu));
+            if (!left) lo = cutoff;
+        }
+        const uint32_t leftm = __ballot_sync(0xffffffffu, moved && left);
+        const uint32_t movedm = __ballot_sync(0xffffffffu, moved);
+        int newpos = lane;
+        if (moved) {
+            const uint32_t le = starts & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
+            const int rs = 31 - __clz(le);
+            const uint32_t gt = starts & ~(lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
+            const int re = gt ? __ffs(gt) - 1 : cnt;
+            const uint32_t runm = (re == 32 ? 0xffffffffu : ((1u << re) - 1u)) & ~((1u << rs) - 1u);
+            const int nl = __popc(leftm & runm);
+            newpos = left ? rs + __popc(leftm & runm & below) : rs + nl + __popc(movedm & ~leftm & runm & below);
+            v = left ? 2 * v + 1 : 2 * v + 2;
+        }
+        perm_sm[newpos] = uint32_t(lane);
+        __syncwarp();
+        const int src = live ? int(perm_sm[lane]) : lane;
+        __syncwarp();
+        d = __shfl_sync(0xffffffffu, d, src);
+        v = __shfl_sync(0xffffffffu, v, src);
+        lo = __shfl_sync(0xffffffffu, lo, src);
+        ic = __shfl_sync(0xffffffffu, ic, src);
+        uu = __shfl_sync(0xffffffffu, uu, src);
+        mg = __shfl_sync(0xffffffffu, mg, src);
+    }
+
+    // ---------------- leaf scan (segment_tree_sampler.cpp:281-292) ----------------
+    const T* U = static_cast<const T*>(a.U);
+    const int r4 = lane & 3, m8 = lane >> 2;
+    const uint32_t prevv = __shfl_up_sync(0xffffffffu, v, 1);
+    uint32_t st = __ballot_sync(0xffffffffu, live && (lane == 0 || v != prevv));
+    uint64_t pick = ~uint64_t{0}, last_nz = ~uint64_t{0};
+    double cum = lo;
+    constexpr int PIECES = C::ROWB / 16;  // 16-byte pieces per row
+    while (st) {
+        const int rs = __ffs(st) - 1;
+        st &= st - 1;
+        const int re = st ? __ffs(st) - 1 : cnt;
+        const uint32_t vr = __shfl_sync(0xffffffffu, v, rs);
+        const uint64_t l = leaf_index(a.topo, vr);
+        const uint64_t first = l * a.topo.F;
+        const uint64_t last = first + a.topo.F < a.topo.I ? first + a.topo.F : a.topo.I;
+        const bool in_run = lane >= rs && lane < re;
+        for (uint64_t c0 = first; c0 < last; c0 += C::LROWS) {
+            if (!__any_sync(0xffffffffu, in_run && pick == ~uint64_t{0})) break;  // every draw picked
+            const int nrow = last - c0 < uint64_t(C::LROWS) ? int(last - c0) : C::LROWS;
+            const char* src = reinterpret_cast<const char*>(U + c0 * R);
+            for (int p = lane; p < nrow * PIECES; p += 32) {
+                const int row = p / PIECES, pc = p - row * PIECES;
+                cp_async16(buf + row * C::RSP + pc * 16, src + uint64_t(row) * C::ROWB + pc * 16);
+            }
+            cp_async_commit();
+            if (c0 == first && st) {  // warm L2 with the first chunk of the next run's leaf
+                const uint32_t vn = __shfl_sync(0xffffffffu, v, __ffs(st) - 1);
+                const uint64_t fn = leaf_index(a.topo, vn) * a.topo.F;
+                const uint64_t ln = fn + a.topo.F < a.topo.I ? fn + a.topo.F : a.topo.I;
+                const uint64_t bytes = (ln - fn < uint64_t(C::LROWS) ? ln - fn : uint64_t(C::LROWS)) * C::ROWB;
+                const char* pn = reinterpret_cast<const char*>(U + fn * R);
+                for (uint64_t o = uint64_t(lane) * 128; o < bytes; o += 32 * 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + o));
+            }
+            cp_async_wait_all();
+            __syncwarp();
+            for (int b0 = rs; b0 < re; b0 += 8) {
+                const int nb = min(8, re - b0);
+                const bool mine_lane = lane >= b0 && lane < b0 + nb;
+                const int jj = (lane - b0) & 7;
+                const uint32_t dd = __shfl_sync(0xffffffffu, d, (b0 + m8) & 31);
+                double zb[2 * NB];
+#pragma unroll
+                for (int s = 0; s < 2 * NB; ++s) zb[s] = m8 < nb ? a.X[uint64_t(dd) * R + 4 * s + r4] : 0.0;
+#pragma unroll
+                for (int tt = 0; tt < C::LROWS / 8; ++tt) {
+                    if (8 * tt >= nrow) break;
+                    const int row = 8 * tt + m8;
+                    const bool rv = row < nrow;
+                    const T* up = reinterpret_cast<const T*>(buf + (rv ? row : 0) * C::RSP) + r4;
+                    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                    for (int s = 0; s < 2 * NB; ++s) dmma_884(acc0, acc1, rv ? static_cast<double>(up[4 * s]) : 0.0, zb[s]);
+                    const double q0 = acc0 * acc0, q1 = acc1 * acc1;
+                    const uint64_t rb = c0 + 8 * tt;
+#pragma unroll
+                    for (int rr = 0; rr < 8; ++rr) {
+                        const double w0 = __shfl_sync(0xffffffffu, q0, rr * 4 + (jj >> 1));
+                        const double w1 = __shfl_sync(0xffffffffu, q1, rr * 4 + (jj >> 1));
+                        if (mine_lane && pick == ~uint64_t{0} && rb + rr < last) {
+                            const double mm = ic * ((jj & 1) ? w1 : w0);
+                            if (mm > 0.0) last_nz = rb + rr;
+                            cum += mm;
+                            mg = fmin(mg, fabs(cum - uu));
+                            if (cum >= uu) pick = rb + rr;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (in_run) {
+            if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : last - 1;
+            if (a.margin) a.margin[d] = mg;
+            if (a.idx) a.idx[uint64_t(d) * a.N + a.k] = uint32_t(pick);
+            a.pick[d] = uint32_t(pick);
+        }
+    }
+}
+
+// h_d *= U_k[pick_d] for every draw (krp_sampler.cpp:137-138): one thread per
+// (draw, column pair), fully coalesced, every load independent.
+template <typename T>
+__global__ void k_apply_pick(double* __restrict__ H, const T* __restrict__ U, const uint32_t* __restrict__ pick,
+                             uint64_t J, uint32_t R) {
+    const uint64_t total = J * R;
+    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t d = e / R;
+        const uint32_t c = uint32_t(e - d * R);
+        H[e] *= static_cast<double>(U[uint64_t(pick[d]) * R + c]);
+    }
+}
+
 unsigned grid_for(uint64_t n, unsigned block) {
     return unsigned(std::min<uint64_t>((n + block - 1) / block, 148ull * 64));
 }
 
+// mode EV_LEVEL with warp_variant selects the per-warp deep-level kernel.
 template <int NB>
-void launch_eval(int mode, const EvalArgs& a, cudaStream_t s) {
-    const unsigned grid = unsigned((a.J + uint64_t(CHUNK) * WPB - 1) / (uint64_t(CHUNK) * WPB));
+void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
+    constexpr size_t smem = 2 * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
+    const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
     if (mode == EV_ROOT)
-        k_eval<NB, EV_ROOT><<<grid, WPB * 32, 0, s>>>(a);
+        k_eval_cta<NB, EV_ROOT><<<grid, CB, smem, s>>>(a);
     else if (mode == EV_PROB)
-        k_eval<NB, EV_PROB><<<grid, WPB * 32, 0, s>>>(a);
+        k_eval_cta<NB, EV_PROB><<<grid, CB, smem, s>>>(a);
+    else if (warp_variant)
+        k_eval_warp<NB><<<unsigned((a.J + uint64_t(CHUNK) * WPB - 1) / (uint64_t(CHUNK) * WPB)), WPB * 32, 0, s>>>(a);
     else
-        k_eval<NB, EV_LEVEL><<<grid, WPB * 32, 0, s>>>(a);
+        k_eval_cta<NB, EV_LEVEL><<<grid, CB, smem, s>>>(a);
 }
 
-void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s) {
+void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
     switch (R / 8) {
-        case 1: return launch_eval<1>(mode, a, s);
-        case 2: return launch_eval<2>(mode, a, s);
-        case 3: return launch_eval<3>(mode, a, s);
-        case 4: return launch_eval<4>(mode, a, s);
-        case 5: return launch_eval<5>(mode, a, s);
-        case 6: return launch_eval<6>(mode, a, s);
-        case 7: return launch_eval<7>(mode, a, s);
-        default: return launch_eval<8>(mode, a, s);
+        case 1: return launch_eval<1>(mode, a, s, warp_variant);
+        case 2: return launch_eval<2>(mode, a, s, warp_variant);
+        case 3: return launch_eval<3>(mode, a, s, warp_variant);
+        case 4: return launch_eval<4>(mode, a, s, warp_variant);
+        case 5: return launch_eval<5>(mode, a, s, warp_variant);
+        case 6: return launch_eval<6>(mode, a, s, warp_variant);
+        case 7: return launch_eval<7>(mode, a, s, warp_variant);
+        default: return launch_eval<8>(mode, a, s, warp_variant);
     }
+}
+
+// shallow levels (many draws per node) -> cooperative CTA kernel; deep -> per-warp
+inline bool deep_level(uint64_t J, uint32_t level) { return (J >> level) < 64; }
+
+template <int NB, typename T>
+void launch_deep2(const DeepArgs& a, unsigned grid, cudaStream_t s) {
+    using C = DeepCfg<NB, T>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_deep2<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        configured = true;
+    }
+    k_deep2<NB, T><<<grid, WPB * 32, C::SMEM, s>>>(a);
+}
+
+template <typename T>
+void dispatch_deep(uint32_t R, const DeepArgs& a, unsigned grid, cudaStream_t s) {
+    switch (R / 8) {
+        case 1: return launch_deep2<1, T>(a, grid, s);
+        case 2: return launch_deep2<2, T>(a, grid, s);
+        case 3: return launch_deep2<3, T>(a, grid, s);
+        case 4: return launch_deep2<4, T>(a, grid, s);
+        case 5: return launch_deep2<5, T>(a, grid, s);
+        case 6: return launch_deep2<6, T>(a, grid, s);
+        case 7: return launch_deep2<7, T>(a, grid, s);
+        default: return launch_deep2<8, T>(a, grid, s);
+    }
+}
+
+template <int NB, typename T>
+void launch_leaf2(const LeafArgs& a, cudaStream_t s) {
+    using C = LeafCfg2<NB, T>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_leaf2<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        configured = true;
+    }
+    const unsigned grid = unsigned((a.J + uint64_t(CHUNK) * WPB - 1) / (uint64_t(CHUNK) * WPB));
+    k_leaf2<NB, T><<<grid, WPB * 32, C::SMEM, s>>>(a);
 }
 
 template <typename T>
 void dispatch_leaf(uint32_t R, const LeafArgs& a, cudaStream_t s) {
-    const unsigned grid = unsigned((a.J + uint64_t(CHUNK) * WPB - 1) / (uint64_t(CHUNK) * WPB));
     switch (R / 8) {
-        case 1: return k_leaf<1, T><<<grid, WPB * 32, 0, s>>>(a), void();
-        case 2: return k_leaf<2, T><<<grid, WPB * 32, 0, s>>>(a), void();
-        case 3: return k_leaf<3, T><<<grid, WPB * 32, 0, s>>>(a), void();
-        case 4: return k_leaf<4, T><<<grid, WPB * 32, 0, s>>>(a), void();
-        case 5: return k_leaf<5, T><<<grid, WPB * 32, 0, s>>>(a), void();
-        case 6: return k_leaf<6, T><<<grid, WPB * 32, 0, s>>>(a), void();
-        case 7: return k_leaf<7, T><<<grid, WPB * 32, 0, s>>>(a), void();
-        default: return k_leaf<8, T><<<grid, WPB * 32, 0, s>>>(a), void();
+        case 1: return launch_leaf2<1, T>(a, s);
+        case 2: return launch_leaf2<2, T>(a, s);
+        case 3: return launch_leaf2<3, T>(a, s);
+        case 4: return launch_leaf2<4, T>(a, s);
+        case 5: return launch_leaf2<5, T>(a, s);
+        case 6: return launch_leaf2<6, T>(a, s);
+        case 7: return launch_leaf2<7, T>(a, s);
+        default: return launch_leaf2<8, T>(a, s);
     }
 }
 
@@ -410,6 +1426,10 @@ int launch_position_grouped(const GroupedArgs& g) {
     const uint64_t J = g.J;
     int launches = 0;
     const unsigned gs = grid_for(J, 256);
+    auto mark = [&](int cat) {
+        if (g.mark) g.mark(g.mark_ctx, cat);
+    };
+    mark(-1);
     EvalArgs e{};
     e.J = J;
     e.node = g.node;
@@ -429,23 +1449,28 @@ int launch_position_grouped(const GroupedArgs& g) {
     cudaMemsetAsync(g.cntL, 0, sizeof(uint32_t) * te.n, g.stream);
     cudaMemsetAsync(g.cntR, 0, sizeof(uint32_t) * te.n, g.stream);
     ++launches;
+    mark(13);
     e.X = g.H;
     e.tree = g.Q;
     e.topo = te;
     e.perm = nullptr;
     dispatch_eval(R, EV_ROOT, e, g.stream);
     ++launches;
+    mark(8);
     uint32_t* pin = g.perm_a;
     uint32_t* pout = g.perm_b;
     for (uint32_t l = 0; l < te.d; ++l) {
         e.perm = pin;
-        dispatch_eval(R, EV_LEVEL, e, g.stream);
+        dispatch_eval(R, EV_LEVEL, e, g.stream, deep_level(J, l));
+        mark(deep_level(J, l) ? 10 : 9);
         k_scatter<<<gs, 256, 0, g.stream>>>(pin, pout, g.node, g.rank, g.gstart, g.cntL, J, (2u << l) - 1);
+        mark(11);
         launches += 2;
         std::swap(pin, pout);
     }
     k_make_z<<<grid_for(J * R, 256), 256, 0, g.stream>>>(g.H, g.V, g.node, te, R, J, g.Zb);
     ++launches;
+    mark(13);
 
     // ---------------- stage 2: factor tree, rank-1 M = z z^T ----------------
     const Topo tz = make_topo(g.I, R);
@@ -454,18 +1479,67 @@ int launch_position_grouped(const GroupedArgs& g) {
     cudaMemsetAsync(g.cntL, 0, sizeof(uint32_t) * tz.n, g.stream);
     cudaMemsetAsync(g.cntR, 0, sizeof(uint32_t) * tz.n, g.stream);
     ++launches;
+    mark(13);
     e.X = g.Zb;
     e.tree = g.Z;
     e.topo = tz;
     e.perm = nullptr;
     dispatch_eval(R, EV_ROOT, e, g.stream);
     ++launches;
+    mark(8);
     pin = g.perm_a;
     pout = g.perm_b;
-    for (uint32_t l = 0; l < tz.d; ++l) {
+    // shallow levels: global regrouping; deep levels + leaf scan: one fused pass
+    uint32_t l0 = 0;
+    while (l0 < tz.d && !deep_level(J, l0)) ++l0;
+    for (uint32_t l = 0; l < l0; ++l) {
         e.perm = pin;
-        dispatch_eval(R, EV_LEVEL, e, g.stream);
+        dispatch_eval(R, EV_LEVEL, e, g.stream, false);
+        mark(9);
         k_scatter<<<gs, 256, 0, g.stream>>>(pin, pout, g.node, g.rank, g.gstart, g.cntL, J, (2u << l) - 1);
+        mark(11);
+        launches += 2;
+        std::swap(pin, pout);
+    }
+    if (g.fused_deep) {
+        DeepArgs da{};
+        da.J = J;
+        da.N = g.N;
+        da.k = g.k;
+        da.level0 = l0;
+        da.perm = pin;
+        da.node = g.node;
+        da.low = g.low;
+        da.invc = g.invc;
+        da.ud = g.ud;
+        da.margin = g.margin;
+        da.X = g.Zb;
+        da.H = g.H;
+        da.idx = g.idx;
+        da.pick = g.rank;  // rank[] is free after the last regroup
+        da.U = g.U;
+        da.tree = g.Z;
+        da.topo = tz;
+        const unsigned grid = unsigned((J + 32ull * WPB - 1) / (32ull * WPB));
+        if (g.storage == 1)
+            dispatch_deep<float>(R, da, grid, g.stream);
+        else
+            dispatch_deep<double>(R, da, grid, g.stream);
+        mark(12);
+        if (g.storage == 1)
+            k_apply_pick<float><<<grid_for(J * R, 256), 256, 0, g.stream>>>(g.H, static_cast<const float*>(g.U), g.rank, J, R);
+        else
+            k_apply_pick<double><<<grid_for(J * R, 256), 256, 0, g.stream>>>(g.H, static_cast<const double*>(g.U), g.rank, J, R);
+        launches += 2;
+        mark(13);
+        return launches;
+    }
+    for (uint32_t l = l0; l < tz.d; ++l) {
+        e.perm = pin;
+        dispatch_eval(R, EV_LEVEL, e, g.stream, true);
+        mark(10);
+        k_scatter<<<gs, 256, 0, g.stream>>>(pin, pout, g.node, g.rank, g.gstart, g.cntL, J, (2u << l) - 1);
+        mark(11);
         launches += 2;
         std::swap(pin, pout);
     }
@@ -489,6 +1563,7 @@ int launch_position_grouped(const GroupedArgs& g) {
     else
         dispatch_leaf<double>(R, la, g.stream);
     ++launches;
+    mark(12);
     return launches;
 }
 

@@ -125,6 +125,19 @@ struct krpg_sampler {
     DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf, gstate, zbuf;
     PinBuf up, errh;
     bool use_grouped = true;  // level-synchronous DMMA descent where supported
+    bool prof_detail = false;  // per-kernel-type timing marks inside the descent
+    bool fused_deep = true;    // deep levels + leaf scan fused (descent_v2.cu k_deep)
+    cudaEvent_t mark_prev = nullptr;
+
+    // timing hook for the grouped descent: attributes the device time since the
+    // previous mark to category `cat` (cat < 0 only sets the reference point)
+    static void mark_cb(void* ctx, int cat) {
+        auto* self = static_cast<krpg_sampler*>(ctx);
+        cudaEvent_t e = self->next_event();
+        CK(cudaEventRecord(e, self->stream));
+        if (cat >= 0 && self->mark_prev) self->prof_pending.push_back({cat, self->mark_prev, e});
+        self->mark_prev = e;
+    }
 
     // ---- instrumentation: launch counts always, event timing when enabled ----
     bool prof_on = false;
@@ -340,6 +353,11 @@ struct krpg_sampler {
             g.margin = d_margin;
             g.err = derr;
             g.stream = stream;
+            g.fused_deep = fused_deep ? 1 : 0;
+            if (prof_on && prof_detail) {
+                g.mark = &krpg_sampler::mark_cb;
+                g.mark_ctx = this;
+            }
             krpg::launch_fill(H, 1.0, J * R, stream);
             prof_launches[KRPG_PROF_OTHER] += 1;
             for (size_t p = 0; p < npos; ++p) {
@@ -857,6 +875,10 @@ int krpg_set_option(krpg_t h, int option, int64_t value) {
         std::lock_guard<std::mutex> lk(h->mu);
         if (option == KRPG_OPT_GROUPED_DESCENT)
             h->use_grouped = value != 0;
+        else if (option == KRPG_OPT_PROFILE_DETAIL)
+            h->prof_detail = value != 0;
+        else if (option == KRPG_OPT_FUSED_DEEP)
+            h->fused_deep = value != 0;
         else
             throw std::invalid_argument("krpg_set_option: unknown option");
     });

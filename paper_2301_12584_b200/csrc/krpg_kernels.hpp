@@ -66,6 +66,9 @@ struct GroupedArgs {
     double *low, *invc, *ud;
     int* err;
     cudaStream_t stream;
+    void (*mark)(void* ctx, int cat);  // optional per-launch timing hook
+    void* mark_ctx;
+    int fused_deep;                    // deep levels + leaf in one warp-local pass
 };
 bool grouped_supported(uint32_t R, uint32_t mode);
 int launch_position_grouped(const GroupedArgs& g);

@@ -46,6 +46,13 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, ui
         : "memory");
 }
 
+// per-thread 16-byte async global -> shared copies (LDGSTS), grouped
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // D(8x8) += A(8x4) * B(4x8), fp64 tensor core (DMMA.8x8x4)
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"

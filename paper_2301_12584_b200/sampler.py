@@ -231,15 +231,20 @@ class KrpSampler:
         """Choose the level-synchronous grouped DMMA descent (default) or the per-draw kernel."""
         check(_lib.lib().krpg_set_option(self._h, _lib.OPT_GROUPED_DESCENT, 1 if on else 0))
 
+    def set_fused_deep(self, on: bool) -> None:
+        """Fused warp-local deep levels + leaf scan (default) or per-level global regrouping."""
+        check(_lib.lib().krpg_set_option(self._h, _lib.OPT_FUSED_DEEP, 1 if on else 0))
+
     def rebuild(self, j: int) -> None:
         check(_lib.lib().krpg_rebuild(self._h, j))
 
-    def profile_enable(self, on: bool = True) -> None:
+    def profile_enable(self, on: bool = True, detail: bool = False) -> None:
         check(_lib.lib().krpg_profile_enable(self._h, 1 if on else 0))
+        check(_lib.lib().krpg_set_option(self._h, _lib.OPT_PROFILE_DETAIL, 1 if detail else 0))
 
     def profile_read(self, reset: bool = True) -> dict:
-        ms = np.zeros(8)
-        n = np.zeros(8, dtype=np.uint64)
+        ms = np.zeros(16)
+        n = np.zeros(16, dtype=np.uint64)
         check(_lib.lib().krpg_profile_read(self._h, _ptr(ms), n.ctypes.data_as(C.POINTER(C.c_uint64)),
                                            1 if reset else 0))
         return {name: {"ms": float(ms[i]), "launches": int(n[i])} for i, name in enumerate(_lib.PROF_NAMES)}

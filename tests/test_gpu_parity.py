@@ -100,15 +100,16 @@ CASES = [
 
 
 @pytest.mark.parametrize("shapes,seed", CASES)
-@pytest.mark.parametrize("mode,descent", [("two_stage", "grouped"), ("two_stage", "per_draw"),
-                                          ("one_stage", "per_draw")])
+@pytest.mark.parametrize("mode,descent", [("two_stage", "grouped"), ("two_stage", "grouped_unfused"),
+                                          ("two_stage", "per_draw"), ("one_stage", "per_draw")])
 def test_sample_bit_exact_against_oracle(shapes, seed, mode, descent):
     """KrpSampler::sample (two-stage, krp_sampler.cpp:82-151) and the one-stage
     M = G+ o hh^T o G_{>k} chain, every exclusion setting, through both descent
     kernels (level-synchronous grouped DMMA and per-draw warps)."""
     fs = pareto_factors(shapes, seed)
     s = K()(fs)
-    s.set_grouped_descent(descent == "grouped")
+    s.set_grouped_descent(descent.startswith("grouped"))
+    s.set_fused_deep(descent != "grouped_unfused")
     o = oracle.OracleKrp(fs, "port")
     for e in [None] + list(range(len(shapes))):
         b = s.sample(e, 4096, 100 + seed, mode=mode, margin=True)

@@ -9,3 +9,4 @@ print("value %.3e samples/s  ms/step %.3f  e2e %.3e  draws frac %.3f  kernels %s
     d["value"], d["ms_per_step"], d["e2e"]["value"], d["roofline"]["frac"], d["kernel_ms_per_step"],
     d["tree_build"]["ms_per_factor"], d["tree_build"]["achieved_gbs"]))
 PY
+python tools/prof_detail.py
