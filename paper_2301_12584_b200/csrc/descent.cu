@@ -304,6 +304,29 @@ __global__ void k_etree(const double* __restrict__ V, const double* __restrict__
     }
 }
 
+// Same Q, one thread per (stored node, packed entry): grid (ceil(P/128), R), so
+// every entry's sum over the node's eigenvectors runs in parallel.
+__global__ void __launch_bounds__(128) k_etree2(const double* __restrict__ V, const double* __restrict__ lam,
+                                                const double* __restrict__ gk, uint32_t R, double* __restrict__ Q) {
+    const uint32_t P = R * (R + 1) / 2;
+    const uint32_t k = blockIdx.x * 128 + threadIdx.x;
+    if (k >= P) return;
+    const uint64_t s = blockIdx.y;
+    const Topo te = make_topo(R, 1);
+    const uint64_t v = s == 0 ? 0 : 2 * s - 1;
+    uint64_t u0, u1;
+    node_rows(te, v, &u0, &u1);
+    uint32_t a, b;
+    unpack_pair(R, k, a, b);
+    const double g = __ldg(gk + k);
+    const double* va = V + uint64_t(a) * R;
+    const double* vb = V + uint64_t(b) * R;
+    double acc = 0.0;
+#pragma unroll 8
+    for (uint64_t u = u0; u < u1; ++u) acc = fma(__ldg(lam + u) * __ldg(va + u), __ldg(vb + u), acc);
+    Q[s * P + k] = acc * g;
+}
+
 template <int S>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     k_probabilities(const double* __restrict__ H, const double* __restrict__ gp, uint32_t R, uint64_t J,
@@ -409,7 +432,8 @@ void launch_draws(const DrawArgs& a) {
 
 void launch_etree_build(const double* V, const double* lam, const double* gk_packed, uint32_t R, double* Q,
                         cudaStream_t s) {
-    k_etree<<<R, 256, 48 * 1024, s>>>(V, lam, gk_packed, R, Q);
+    const uint32_t P = R * (R + 1) / 2;
+    k_etree2<<<dim3((P + 127) / 128, R), 128, 0, s>>>(V, lam, gk_packed, R, Q);
 }
 
 void launch_probabilities(const double* H, const double* gp_packed, uint32_t R, uint64_t J, double rank,

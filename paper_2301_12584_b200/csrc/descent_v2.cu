@@ -36,7 +36,7 @@ namespace v2 {
 constexpr int CHUNK = 32;  // sorted positions per warp
 constexpr int WPB = 4;     // warps per block
 
-enum { EV_ROOT = 0, EV_LEVEL = 1, EV_PROB = 2 };
+enum { EV_ROOT = 0, EV_LEVEL = 1, EV_PROB = 2, EV_LEVEL0 = 3 };
 
 template <int NB>
 struct Tiles {
@@ -124,6 +124,9 @@ struct EvalArgs {
     int* err;
     double* prob;           // EV_PROB output
     double rank_div;        // EV_PROB: numerical rank
+    uint32_t* perm_out;     // level passes: next level's sorted order
+    uint32_t* GS;           // per node position range [GS, GE) at its level
+    uint32_t* GE;
 };
 
 // Per-lane B-fragment addressing into a packed symmetric Gram (same for every
@@ -191,22 +194,85 @@ __device__ __forceinline__ double block_qf_packed(const double* G, const FragAdd
 
 constexpr int CB = WPB * 32;  // positions per CTA in the cooperative variant
 
-// Cooperative variant for shallow levels / single-matrix passes: the CTA's 128
-// sorted positions form few runs; each run's Gram is staged once into shared
-// memory by a 1-D TMA bulk copy (double-buffered: the next run's copy is in
-// flight while this run computes) and the run's 8-draw blocks are spread over
-// the CTA's warps. Child slots come from shared-memory counters, folded into
-// the global per-node counters with one atomic per run per side.
+// Same block quadratic form with the Gram already folded in shared memory
+// (off-diagonal 8x8 tiles pre-doubled) and the X block in shared memory with
+// row stride XS doubles.
+template <int NB>
+__device__ __forceinline__ double block_qf_folded(const double* G, const FragAddr<NB>& fa, const double* xr,
+                                                  int lane) {
+    const int r4 = lane & 3, cq = lane >> 2;
+    double av[NB][2];
+#pragma unroll
+    for (int p = 0; p < NB; ++p)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) av[p][s] = xr[8 * p + 4 * s + r4];
+    double y[NB][2];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) y[q][0] = y[q][1] = 0.0;
+#pragma unroll
+    for (int p = 0; p < NB; ++p) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            dmma_884(y[p][0], y[p][1], av[p][s], G[fa.diag[p][s]]);
+#pragma unroll
+            for (int q = p + 1; q < NB; ++q) dmma_884(y[q][0], y[q][1], av[p][s], G[fa.rowoff[p][s] + 8 * q + cq]);
+        }
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const double2 xv = *reinterpret_cast<const double2*>(xr + 8 * q + 2 * r4);
+        part = fma(xv.x, y[q][0], part);
+        part = fma(xv.y, y[q][1], part);
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    return part;
+}
+
+// double the entries of off-diagonal 8x8 tiles of a packed Gram in place
+template <int NB>
+__device__ __forceinline__ void fold_offdiag(double* G, int tid, int nthreads) {
+    constexpr int R = 8 * NB;
+    constexpr int P = R * (R + 1) / 2;
+    for (int k = tid; k < P; k += nthreads) {
+        uint32_t a, b;
+        unpack_pair(R, uint32_t(k), a, b);
+        if ((a >> 3) != (b >> 3)) G[k] += G[k];
+    }
+}
+
+// Cooperative shallow-level kernel, v3: everything a block needs is in shared
+// memory before the DMMAs start — the CTA's 128 X rows (cp.async, padded
+// stride), its per-draw scalars, and each run's Gram (TMA, double-buffered,
+// folded once per run).
+template <int NB>
+struct CtaCfg {
+    static constexpr int R = 8 * NB;
+    static constexpr int P = R * (R + 1) / 2;
+    static constexpr int GD = (P + 15) / 16 * 16;  // doubles per Gram buffer (16-double aligned)
+    static constexpr int XS = R + 2;               // padded X row stride (doubles): 16 B aligned rows
+    static constexpr size_t SMEM = sizeof(double) * (2 * GD + size_t(CB) * XS + 4 * CB);
+};
+
 template <int NB, int MODE>
-__global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
+__global__ void __launch_bounds__(CB) k_eval_cta3(EvalArgs a) {
+    using C = CtaCfg<NB>;
     constexpr int R = 8 * NB;
     constexpr uint32_t P = uint32_t(R) * (R + 1) / 2;
-    extern __shared__ __align__(128) double sG[];  // [2][P]
+    extern __shared__ __align__(128) double dsm[];
+    double* sG = dsm;                          // [2][GD]
+    double* sX = dsm + 2 * C::GD;              // [CB][XS]
+    double* s_low = sX + CB * C::XS;           // [CB]
+    double* s_ic = s_low + CB;
+    double* s_u = s_ic + CB;
+    double* s_mg = s_u + CB;
     __shared__ uint32_t s_d[CB], s_v[CB];
     __shared__ int s_rs[CB + 1];
     __shared__ int s_nruns;
     __shared__ uint32_t s_cnt[2], s_base[2];
     __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int wcount[WPB];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t base = uint64_t(blockIdx.x) * CB;
     const int cnt = a.J - base < uint64_t(CB) ? int(a.J - base) : CB;
@@ -214,6 +280,176 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
         const uint32_t d = a.perm ? a.perm[base + tid] : uint32_t(base + tid);
         s_d[tid] = d;
         s_v[tid] = MODE == EV_LEVEL ? a.node[d] : 0u;
+        if (MODE == EV_LEVEL) {
+            s_low[tid] = a.low[d];
+            s_ic[tid] = a.invc[d];
+            s_u[tid] = a.ud[d];
+            s_mg[tid] = a.margin ? a.margin[d] : 0.0;
+        }
+    }
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    // X rows of the CTA's draws -> shared (16-byte cp.async pieces, padded rows)
+    {
+        constexpr int PCS = R / 2;  // 16-byte pieces per row
+        for (int p = tid; p < cnt * PCS; p += CB) {
+            const int row = p / PCS, pc = p - row * PCS;
+            cp_async16(sX + row * C::XS + 2 * pc, a.X + uint64_t(s_d[row]) * R + 2 * pc);
+        }
+        cp_async_commit();
+    }
+    {  // run boundaries -> compact list s_rs
+        const bool flag = tid < cnt && (tid == 0 || s_v[tid] != s_v[tid - 1]);
+        const unsigned bal = __ballot_sync(0xffffffffu, flag);
+        if (lane == 0) wcount[warp] = __popc(bal);
+        __syncthreads();
+        int off = 0;
+        for (int w = 0; w < warp; ++w) off += wcount[w];
+        if (flag) s_rs[off + __popc(bal & ((1u << lane) - 1u))] = tid;
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < WPB; ++w) tot += wcount[w];
+            s_nruns = tot;
+            s_rs[tot] = cnt;
+        }
+        __syncthreads();
+    }
+    const int nruns = s_nruns;
+    auto gsrc = [&](int r) -> const double* {
+        if (MODE != EV_LEVEL) return a.tree;
+        const uint32_t v = s_v[s_rs[r]];
+        if (is_leaf(a.topo, v)) return nullptr;
+        return a.tree + slot_of(2ull * v + 1) * uint64_t(P);
+    };
+    if (tid == 0 && nruns > 0) {
+        const double* g0 = gsrc(0);
+        if (g0) {
+            mbar_arrive_expect_tx(&bar[0], P * 8);
+            tma_load_1d(sG, g0, P * 8, &bar[0]);
+        }
+    }
+    const FragAddr<NB> fa(lane);
+    uint32_t phase[2] = {0u, 0u};
+    cp_async_wait_all();
+    for (int r = 0; r < nruns; ++r) {
+        const int buf = r & 1;
+        if (tid == 0 && r + 1 < nruns) {
+            const double* g1 = gsrc(r + 1);
+            if (g1) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&bar[buf ^ 1], P * 8);
+                tma_load_1d(sG + (buf ^ 1) * C::GD, g1, P * 8, &bar[buf ^ 1]);
+            }
+        }
+        const double* gr = gsrc(r);
+        if (!gr) continue;
+        mbar_wait(&bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        const int rs = s_rs[r], re = s_rs[r + 1];
+        const uint32_t v = s_v[rs];
+        double* G = sG + buf * C::GD;
+        if (tid < 2) s_cnt[tid] = 0;
+        fold_offdiag<NB>(G, tid, CB);
+        __syncthreads();  // folded Gram + X rows (cp.async) visible to all warps
+        const int nblk = (re - rs + 7) >> 3;
+        for (int b = warp; b < nblk; b += WPB) {
+            const int b0 = rs + 8 * b;
+            const int n = min(8, re - b0);
+            const int m = lane >> 2;
+            const bool valid = m < n;
+            const int slot = b0 + (valid ? m : 0);
+            const double mass = block_qf_folded<NB>(G, fa, sX + slot * C::XS, lane);
+            const bool owner = valid && (lane & 3) == 0;
+            const uint32_t dd = s_d[slot];
+            if (MODE == EV_ROOT) {
+                if (owner) {
+                    if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
+                    a.invc[dd] = 1.0 / mass;
+                }
+            } else if (MODE == EV_PROB) {
+                if (owner) a.prob[dd] = mass / a.rank_div;
+            } else {
+                bool left = false;
+                double cutoff = 0.0;
+                if (owner) {
+                    const double u = s_u[slot];
+                    cutoff = s_low[slot] + s_ic[slot] * mass;
+                    left = cutoff >= u;
+                    if (a.margin) a.margin[dd] = fmin(s_mg[slot], fabs(cutoff - u));
+                }
+                const unsigned lm = __ballot_sync(0xffffffffu, owner && left);
+                const unsigned rm = __ballot_sync(0xffffffffu, owner && !left);
+                uint32_t bl = 0, br = 0;
+                if (lane == 0) {
+                    if (lm) bl = atomicAdd(&s_cnt[0], uint32_t(__popc(lm)));
+                    if (rm) br = atomicAdd(&s_cnt[1], uint32_t(__popc(rm)));
+                }
+                bl = __shfl_sync(0xffffffffu, bl, 0);
+                br = __shfl_sync(0xffffffffu, br, 0);
+                if (owner) {
+                    const unsigned below = (1u << lane) - 1u;
+                    if (left) {
+                        a.node[dd] = 2 * v + 1;
+                        a.rank[dd] = bl + __popc(lm & below);
+                    } else {
+                        a.node[dd] = 2 * v + 2;
+                        a.rank[dd] = br + __popc(rm & below);
+                        a.low[dd] = cutoff;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (MODE == EV_LEVEL) {
+            if (tid == 0) {
+                s_base[0] = s_cnt[0] ? atomicAdd(a.cntL + v, s_cnt[0]) : 0u;
+                s_base[1] = s_cnt[1] ? atomicAdd(a.cntR + v, s_cnt[1]) : 0u;
+            }
+            __syncthreads();
+            for (int t = rs + tid; t < re; t += CB) {
+                const uint32_t d = s_d[t];
+                a.rank[d] += (a.node[d] & 1u) ? s_base[0] : s_base[1];
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Cooperative variant for shallow levels / single-matrix passes: the CTA's 128
+// sorted positions form few runs; each run's Gram is staged once into shared
+// memory by a 1-D TMA bulk copy (double-buffered: the next run's copy is in
+// flight while this run computes) and the run's 8-draw blocks are spread over
+// the CTA's warps. Child slots come from shared-memory counters, folded into
+// the global per-node counters with one atomic per run per side.
+//
+// Level passes write the next level's sorted order directly: a run's left
+// draws fill its node's position range [GS, GE) from the front and its right
+// draws from the back, so the child ranges need no second pass (the left
+// child's extent GS + cntL is only read by the next level). With ROOT0 the
+// level-0 pass also evaluates the root normaliser C (root Gram in the second
+// shared buffer), replacing a separate normaliser pass.
+template <int NB, int MODE, bool ROOT0 = false>
+__global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
+    constexpr int R = 8 * NB;
+    constexpr uint32_t P = uint32_t(R) * (R + 1) / 2;
+    extern __shared__ __align__(128) double sG[];  // [2][P]
+    __shared__ uint32_t s_d[CB], s_v[CB], s_rank[CB];
+    __shared__ uint8_t s_left[CB];
+    __shared__ int s_rs[CB + 1];
+    __shared__ int s_nruns;
+    __shared__ uint32_t s_cnt[2], s_base[2], s_gs, s_ge;
+    __shared__ __align__(8) uint64_t bar[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t base = uint64_t(blockIdx.x) * CB;
+    const int cnt = a.J - base < uint64_t(CB) ? int(a.J - base) : CB;
+    if (tid < cnt) {
+        const uint32_t d = a.perm ? a.perm[base + tid] : uint32_t(base + tid);
+        s_d[tid] = d;
+        s_v[tid] = (MODE == EV_LEVEL && !ROOT0) ? a.node[d] : 0u;
     }
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -251,12 +487,16 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
             mbar_arrive_expect_tx(&bar[0], P * 8);
             tma_load_1d(sG, g0, P * 8, &bar[0]);
         }
+        if (ROOT0) {  // root Gram (slot 0) for the normaliser, second buffer
+            mbar_arrive_expect_tx(&bar[1], P * 8);
+            tma_load_1d(sG + P, a.tree, P * 8, &bar[1]);
+        }
     }
     const FragAddr<NB> fa(lane);
     uint32_t phase[2] = {0u, 0u};
     for (int r = 0; r < nruns; ++r) {
         const int buf = r & 1;
-        if (tid == 0 && r + 1 < nruns) {  // prefetch the next run's Gram into the other buffer
+        if (!ROOT0 && tid == 0 && r + 1 < nruns) {  // prefetch the next run's Gram into the other buffer
             const double* g1 = gsrc(r + 1);
             if (g1) {
                 fence_proxy_async();
@@ -264,13 +504,31 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
                 tma_load_1d(sG + (buf ^ 1) * P, g1, P * 8, &bar[buf ^ 1]);
             }
         }
+        const int rs = s_rs[r], re = s_rs[r + 1];
         const double* gr = gsrc(r);
-        if (!gr) continue;  // draws parked at a leaf one level up
+        if (!gr) {  // draws parked at a leaf one level up keep their positions
+            if (MODE == EV_LEVEL)
+                for (int t = rs + tid; t < re; t += CB) a.perm_out[base + t] = s_d[t];
+            continue;
+        }
         mbar_wait(&bar[buf], phase[buf]);
         phase[buf] ^= 1u;
-        const int rs = s_rs[r], re = s_rs[r + 1];
+        if (ROOT0) mbar_wait(&bar[1], 0u);
         const uint32_t v = s_v[rs];
         if (tid < 2) s_cnt[tid] = 0;
+        if (MODE == EV_LEVEL && tid == 0) {  // this node's position range, from its parent's
+            uint32_t gs = 0, ge = uint32_t(a.J);
+            if (v != 0) {
+                const uint32_t p = (v - 1) >> 1;
+                const uint32_t gl = a.GS[p] + a.cntL[p];
+                gs = (v & 1u) ? a.GS[p] : gl;
+                ge = (v & 1u) ? gl : a.GE[p];
+            }
+            s_gs = gs;
+            s_ge = ge;
+            a.GS[v] = gs;
+            a.GE[v] = ge;
+        }
         __syncthreads();
         const double* G = sG + buf * P;
         const int nblk = (re - rs + 7) >> 3;
@@ -280,7 +538,8 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
             const int m = lane >> 2;
             const bool valid = m < n;
             const uint32_t dd = valid ? s_d[b0 + m] : 0u;
-            const double mass = block_qf_packed<NB>(G, fa, valid ? a.X + uint64_t(dd) * R : nullptr, lane);
+            const double* xrow = valid ? a.X + uint64_t(dd) * R : nullptr;
+            const double mass = block_qf_packed<NB>(G, fa, xrow, lane);
             const bool owner = valid && (lane & 3) == 0;
             if (MODE == EV_ROOT) {
                 if (owner) {
@@ -290,11 +549,22 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
             } else if (MODE == EV_PROB) {
                 if (owner) a.prob[dd] = mass / a.rank_div;
             } else {
+                double croot = 0.0;
+                if (ROOT0) croot = block_qf_packed<NB>(sG + P, fa, xrow, lane);
                 bool left = false;
                 double cutoff = 0.0;
                 if (owner) {
                     const double u = a.ud[dd];
-                    cutoff = a.low[dd] + a.invc[dd] * mass;
+                    double ic;
+                    if (ROOT0) {
+                        if (!isfinite(croot) || croot <= 0.0) atomicExch(a.err, 1);
+                        ic = 1.0 / croot;
+                        a.invc[dd] = ic;
+                        cutoff = 0.0 + ic * mass;
+                    } else {
+                        ic = a.invc[dd];
+                        cutoff = a.low[dd] + ic * mass;
+                    }
                     left = cutoff >= u;
                     if (a.margin) a.margin[dd] = fmin(a.margin[dd], fabs(cutoff - u));
                 }
@@ -309,12 +579,14 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
                 br = __shfl_sync(0xffffffffu, br, 0);
                 if (owner) {
                     const unsigned below = (1u << lane) - 1u;
+                    const int slot = b0 + m;
+                    s_left[slot] = left ? 1 : 0;
                     if (left) {
                         a.node[dd] = 2 * v + 1;
-                        a.rank[dd] = bl + __popc(lm & below);
+                        s_rank[slot] = bl + __popc(lm & below);
                     } else {
                         a.node[dd] = 2 * v + 2;
-                        a.rank[dd] = br + __popc(rm & below);
+                        s_rank[slot] = br + __popc(rm & below);
                         a.low[dd] = cutoff;
                     }
                 }
@@ -328,8 +600,8 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
             }
             __syncthreads();
             for (int t = rs + tid; t < re; t += CB) {
-                const uint32_t d = s_d[t];
-                a.rank[d] += (a.node[d] & 1u) ? s_base[0] : s_base[1];
+                const uint32_t pos = s_left[t] ? s_gs + s_base[0] + s_rank[t] : s_ge - 1u - (s_base[1] + s_rank[t]);
+                a.perm_out[pos] = s_d[t];
             }
             __syncthreads();
         }
@@ -1334,14 +1606,27 @@ unsigned grid_for(uint64_t n, unsigned block) {
 }
 
 // mode EV_LEVEL with warp_variant selects the per-warp deep-level kernel.
+template <int NB, int MODE>
+void launch_cta3(const EvalArgs& a, unsigned grid, cudaStream_t s) {
+    constexpr size_t smem = CtaCfg<NB>::SMEM;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_eval_cta3<NB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        configured = true;
+    }
+    k_eval_cta3<NB, MODE><<<grid, CB, smem, s>>>(a);
+}
+
 template <int NB>
 void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
-    constexpr size_t smem = 2 * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
     const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
+    constexpr size_t smem = 2 * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
     if (mode == EV_ROOT)
         k_eval_cta<NB, EV_ROOT><<<grid, CB, smem, s>>>(a);
     else if (mode == EV_PROB)
         k_eval_cta<NB, EV_PROB><<<grid, CB, smem, s>>>(a);
+    else if (mode == EV_LEVEL0)
+        k_eval_cta<NB, EV_LEVEL, true><<<grid, CB, smem, s>>>(a);
     else if (warp_variant)
         k_eval_warp<NB><<<unsigned((a.J + uint64_t(CHUNK) * WPB - 1) / (uint64_t(CHUNK) * WPB)), WPB * 32, 0, s>>>(a);
     else
@@ -1450,24 +1735,35 @@ int launch_position_grouped(const GroupedArgs& g) {
     cudaMemsetAsync(g.cntR, 0, sizeof(uint32_t) * te.n, g.stream);
     ++launches;
     mark(13);
+    e.GS = g.gstart;
+    e.GE = g.gend;
+    uint32_t* pin = g.perm_a;
+    uint32_t* pout = g.perm_b;
+    // CTA-cooperative levels [0, lcta) with direct next-level scatter; level 0
+    // also computes the normaliser (a separate pass only when lcta == 0)
+    auto cta_levels = [&](uint32_t lcta) {
+        pin = g.perm_a;
+        pout = g.perm_b;
+        if (lcta == 0) {
+            e.perm = nullptr;
+            dispatch_eval(R, EV_ROOT, e, g.stream);
+            ++launches;
+            mark(8);
+            return;
+        }
+        for (uint32_t l = 0; l < lcta; ++l) {
+            e.perm = l == 0 ? nullptr : pin;
+            e.perm_out = pout;
+            dispatch_eval(R, l == 0 ? EV_LEVEL0 : EV_LEVEL, e, g.stream, false);
+            ++launches;
+            mark(9);
+            std::swap(pin, pout);
+        }
+    };
     e.X = g.H;
     e.tree = g.Q;
     e.topo = te;
-    e.perm = nullptr;
-    dispatch_eval(R, EV_ROOT, e, g.stream);
-    ++launches;
-    mark(8);
-    uint32_t* pin = g.perm_a;
-    uint32_t* pout = g.perm_b;
-    for (uint32_t l = 0; l < te.d; ++l) {
-        e.perm = pin;
-        dispatch_eval(R, EV_LEVEL, e, g.stream, deep_level(J, l));
-        mark(deep_level(J, l) ? 10 : 9);
-        k_scatter<<<gs, 256, 0, g.stream>>>(pin, pout, g.node, g.rank, g.gstart, g.cntL, J, (2u << l) - 1);
-        mark(11);
-        launches += 2;
-        std::swap(pin, pout);
-    }
+    cta_levels(te.d);
     k_make_z<<<grid_for(J * R, 256), 256, 0, g.stream>>>(g.H, g.V, g.node, te, R, J, g.Zb);
     ++launches;
     mark(13);
@@ -1483,24 +1779,10 @@ int launch_position_grouped(const GroupedArgs& g) {
     e.X = g.Zb;
     e.tree = g.Z;
     e.topo = tz;
-    e.perm = nullptr;
-    dispatch_eval(R, EV_ROOT, e, g.stream);
-    ++launches;
-    mark(8);
-    pin = g.perm_a;
-    pout = g.perm_b;
     // shallow levels: global regrouping; deep levels + leaf scan: one fused pass
     uint32_t l0 = 0;
     while (l0 < tz.d && !deep_level(J, l0)) ++l0;
-    for (uint32_t l = 0; l < l0; ++l) {
-        e.perm = pin;
-        dispatch_eval(R, EV_LEVEL, e, g.stream, false);
-        mark(9);
-        k_scatter<<<gs, 256, 0, g.stream>>>(pin, pout, g.node, g.rank, g.gstart, g.cntL, J, (2u << l) - 1);
-        mark(11);
-        launches += 2;
-        std::swap(pin, pout);
-    }
+    cta_levels(l0);
     if (g.fused_deep) {
         DeepArgs da{};
         da.J = J;

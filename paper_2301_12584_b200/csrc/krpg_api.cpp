@@ -324,7 +324,7 @@ struct krpg_sampler {
             uint64_t nmax = 2ull * R;
             for (uint32_t k : inc) nmax = std::max<uint64_t>(nmax, krpg::make_topo(f[k].I, R).n);
             const size_t Ju = size_t(J);
-            char* st = static_cast<char*>(gstate.ensure(Ju * (4 * 4 + 8 * 3) + nmax * 4 * 3 + 256));
+            char* st = static_cast<char*>(gstate.ensure(Ju * (4 * 4 + 8 * 3) + nmax * 4 * 4 + 1024));
             auto carve = [&](size_t bytes) {
                 char* p = st;
                 st += (bytes + 127) / 128 * 128;
@@ -339,6 +339,7 @@ struct krpg_sampler {
             g.invc = reinterpret_cast<double*>(carve(8 * Ju));
             g.ud = reinterpret_cast<double*>(carve(8 * Ju));
             g.gstart = reinterpret_cast<uint32_t*>(carve(4 * nmax));
+            g.gend = reinterpret_cast<uint32_t*>(carve(4 * nmax));
             g.cntL = reinterpret_cast<uint32_t*>(carve(4 * nmax));
             g.cntR = reinterpret_cast<uint32_t*>(carve(4 * nmax));
             g.Zb = static_cast<double*>(zbuf.ensure(sizeof(double) * J * R));

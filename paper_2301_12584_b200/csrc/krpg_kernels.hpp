@@ -62,7 +62,7 @@ struct GroupedArgs {
     const double* V;     // eigenvectors of G_{>k}
     const double* Z;     // factor tree compact
     const void* U;       // factor rows
-    uint32_t *perm_a, *perm_b, *node, *rank, *gstart, *cntL, *cntR;
+    uint32_t *perm_a, *perm_b, *node, *rank, *gstart, *gend, *cntL, *cntR;
     double *low, *invc, *ud;
     int* err;
     cudaStream_t stream;
