@@ -72,6 +72,72 @@ void tridiagonalize(std::vector<double>& a, std::size_t n, std::vector<double>& 
     }
 }
 
+// Householder tridiagonalisation of the full symmetric matrix a (n x n,
+// row-major, both triangles kept): all updates are row-contiguous (symv +
+// rank-2), so they vectorise. Reflector k (acting on coordinates k+1..n-1) is
+// I - beta_k v_k v_k^T; v_k is stored in row k of `refl` at columns k+1..n-1.
+// On return d/e hold the tridiagonal (e[i] couples i-1 and i, e[0] = 0).
+void tridiagonalize_rowmajor(std::vector<double>& a, std::size_t n, std::vector<double>& d,
+                             std::vector<double>& e, std::vector<double>& refl, std::vector<double>& beta) {
+    std::vector<double> p(n), w(n);
+    refl.assign(n * n, 0.0);
+    beta.assign(n, 0.0);
+    e.assign(n, 0.0);
+    for (std::size_t k = 0; k + 2 < n; ++k) {
+        double* ak = a.data() + k * n;
+        const std::size_t m0 = k + 1;
+        double sig = 0.0;
+        for (std::size_t j = m0 + 1; j < n; ++j) sig += ak[j] * ak[j];
+        const double x0 = ak[m0];
+        d[k] = ak[k];
+        if (sig == 0.0) {  // already tridiagonal in this column
+            e[k + 1] = x0;
+            continue;
+        }
+        const double nrm = std::sqrt(x0 * x0 + sig);
+        const double alpha = x0 >= 0.0 ? -nrm : nrm;
+        double* v = refl.data() + k * n;
+        v[m0] = x0 - alpha;
+        for (std::size_t j = m0 + 1; j < n; ++j) v[j] = ak[j];
+        const double vtv = v[m0] * v[m0] + sig;
+        const double b = 2.0 / vtv;
+        beta[k] = b;
+        e[k + 1] = alpha;
+        // p = b * A22 v
+        double pv = 0.0;
+        for (std::size_t i = m0; i < n; ++i) {
+            const double* ai = a.data() + i * n;
+            double s = 0.0;
+            for (std::size_t j = m0; j < n; ++j) s += ai[j] * v[j];
+            p[i] = b * s;
+            pv += p[i] * v[i];
+        }
+        const double K = 0.5 * b * pv;
+        for (std::size_t i = m0; i < n; ++i) w[i] = p[i] - K * v[i];
+        for (std::size_t i = m0; i < n; ++i) {
+            double* ai = a.data() + i * n;
+            const double vi = v[i], wi = w[i];
+            for (std::size_t j = m0; j < n; ++j) ai[j] -= vi * w[j] + wi * v[j];
+        }
+    }
+    if (n >= 2) {
+        d[n - 2] = a[(n - 2) * n + (n - 2)];
+        d[n - 1] = a[(n - 1) * n + (n - 1)];
+        e[n - 1] = a[(n - 2) * n + (n - 1)];
+    } else {
+        d[0] = a[0];
+    }
+}
+
+// Givens rotation of two contiguous rows (vectorised: the rows never alias)
+inline void rotate_rows(double* __restrict__ zi, double* __restrict__ zi1, std::size_t n, double c, double s) {
+    for (std::size_t k = 0; k < n; ++k) {
+        const double a0 = zi[k], a1 = zi1[k];
+        zi1[k] = s * a0 + c * a1;
+        zi[k] = c * a0 - s * a1;
+    }
+}
+
 // Implicit-shift QL on the tridiagonal (d, e); zt holds Q^T (rows = vectors)
 // and is rotated alongside so its rows become the eigenvectors.
 void tridiagonal_ql(std::vector<double>& d, std::vector<double>& e, std::vector<double>& zt,
@@ -90,14 +156,14 @@ void tridiagonal_ql(std::vector<double>& d, std::vector<double>& e, std::vector<
             if (m != l) {
                 if (++iter > 60) throw std::runtime_error("eigh_psd: QL iteration did not converge");
                 double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-                double r = std::hypot(g, 1.0);
+                double r = std::sqrt(g * g + 1.0);
                 g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? std::abs(r) : -std::abs(r)));
                 double s = 1.0, c = 1.0, p = 0.0;
                 bool deflated = false;
                 for (std::size_t i = m; i-- > l;) {
                     double f = s * e[i];
                     const double b = c * e[i];
-                    r = std::hypot(f, g);
+                    r = std::sqrt(f * f + g * g);
                     e[i + 1] = r;
                     if (r == 0.0) {
                         d[i + 1] -= p;
@@ -112,13 +178,7 @@ void tridiagonal_ql(std::vector<double>& d, std::vector<double>& e, std::vector<
                     p = s * r;
                     d[i + 1] = g + p;
                     g = c * r - b;
-                    double* zi = zt.data() + i * n;
-                    double* zi1 = zt.data() + (i + 1) * n;
-                    for (std::size_t k = 0; k < n; ++k) {
-                        f = zi1[k];
-                        zi1[k] = s * zi[k] + c * f;
-                        zi[k] = c * zi[k] - s * f;
-                    }
+                    rotate_rows(zt.data() + i * n, zt.data() + (i + 1) * n, n, c, s);
                 }
                 if (deflated) continue;
                 d[l] -= p;
@@ -147,16 +207,41 @@ Eig eigh_psd(const double* G, std::size_t n) {
     std::vector<double> a(n * n), d(n), e(n);
     for (std::size_t i = 0; i < n; ++i)
         for (std::size_t j = 0; j < n; ++j) a[i * n + j] = 0.5 * (G[i * n + j] + G[j * n + i]);
+    std::vector<double> zt(n * n, 0.0);  // rows = eigenvectors
     if (n == 1) {
         d[0] = a[0];
-        a[0] = 1.0;
+        zt[0] = 1.0;
     } else {
-        tridiagonalize(a, n, d, e);
+        std::vector<double> refl, beta;
+        tridiagonalize_rowmajor(a, n, d, e, refl, beta);
+        for (std::size_t i = 0; i < n; ++i) zt[i * n + i] = 1.0;
+        tridiagonal_ql(d, e, zt, n);  // zt rows: eigenvectors of the tridiagonal
+        // back-transform all vectors at once, z <- H_0 H_1 ... H_{n-3} z, on the
+        // coordinate-major copy zc[j][r] so every update is a contiguous axpy
+        std::vector<double> zc(n * n), s(n);
+        for (std::size_t r = 0; r < n; ++r)
+            for (std::size_t j = 0; j < n; ++j) zc[j * n + r] = zt[r * n + j];
+        for (std::size_t k = n - 2; k-- > 0;) {
+            if (beta[k] == 0.0) continue;
+            const double* v = refl.data() + k * n;
+            std::fill(s.begin(), s.end(), 0.0);
+            for (std::size_t j = k + 1; j < n; ++j) {
+                const double vj = v[j];
+                const double* __restrict__ zj = zc.data() + j * n;
+                double* __restrict__ sp = s.data();
+                for (std::size_t r = 0; r < n; ++r) sp[r] += vj * zj[r];
+            }
+            for (std::size_t r = 0; r < n; ++r) s[r] *= beta[k];
+            for (std::size_t j = k + 1; j < n; ++j) {
+                const double vj = v[j];
+                double* __restrict__ zj = zc.data() + j * n;
+                const double* __restrict__ sp = s.data();
+                for (std::size_t r = 0; r < n; ++r) zj[r] -= vj * sp[r];
+            }
+        }
+        for (std::size_t r = 0; r < n; ++r)
+            for (std::size_t j = 0; j < n; ++j) zt[r * n + j] = zc[j * n + r];
     }
-    std::vector<double> zt(n * n);  // rows = Q columns
-    for (std::size_t i = 0; i < n; ++i)
-        for (std::size_t j = 0; j < n; ++j) zt[j * n + i] = a[i * n + j];
-    if (n > 1) tridiagonal_ql(d, e, zt, n);
 
     std::vector<std::size_t> order(n);
     std::iota(order.begin(), order.end(), 0);

@@ -281,34 +281,48 @@ struct krpg_sampler {
             krpg::hadamard_into(Y[p], gp.data());
             for (size_t q = p + 1; q < npos; ++q) krpg::hadamard_into(Y[p], f[inc[q]].G.data());
         }
+        // Eigendecompositions of G_{>k} (two-stage): position 0 on this thread,
+        // the others concurrently; each position's operands are uploaded just
+        // before its kernels, so the device starts on position 0 while later
+        // eigensolves are still running on the host.
         std::vector<krpg::Eig> ye(npos);
+        std::vector<std::future<krpg::Eig>> fut(npos);
         if (mode == KRPG_MODE_TWO_STAGE) {
-            std::vector<std::future<krpg::Eig>> fut;
-            for (size_t p = 0; p < npos; ++p)
-                fut.push_back(std::async(std::launch::async, [&, p] { return krpg::eigh_psd(Y[p].data(), R); }));
-            for (size_t p = 0; p < npos; ++p) ye[p] = fut[p].get();
+            for (size_t p = 1; p < npos; ++p)
+                fut[p] = std::async(std::launch::async, [&, p] { return krpg::eigh_psd(Y[p].data(), R); });
+            ye[0] = krpg::eigh_psd(Y[0].data(), R);
         }
 
-        // ---- one upload of the small per-call operands ----
         const size_t per_pos = mode == KRPG_MODE_TWO_STAGE ? RR + R : P;
         const size_t nd = P + npos * per_pos;
         double* up_h = static_cast<double*>(up.ensure(sizeof(double) * nd));
+        double* dsmall = static_cast<double*>(small.ensure(sizeof(double) * nd));
+        auto stage_pos = [&](size_t p) {  // fill + upload position p's operands
+            double* dst = up_h + P + p * per_pos;
+            if (mode == KRPG_MODE_TWO_STAGE) {
+                if (p > 0) ye[p] = fut[p].get();
+                std::memcpy(dst, ye[p].vectors.data(), sizeof(double) * RR);
+                std::memcpy(dst + RR, ye[p].values.data(), sizeof(double) * R);
+            } else {
+                const std::vector<double> yp = krpg::pack_upper(Y[p].data(), R);
+                std::memcpy(dst, yp.data(), sizeof(double) * P);
+            }
+            CK(cudaMemcpyAsync(dsmall + P + p * per_pos, dst, sizeof(double) * per_pos, cudaMemcpyHostToDevice,
+                               stream));
+        };
         {
             const std::vector<double> gpp = krpg::pack_upper(gp.data(), R);
             std::memcpy(up_h, gpp.data(), sizeof(double) * P);
-            for (size_t p = 0; p < npos; ++p) {
-                double* dst = up_h + P + p * per_pos;
-                if (mode == KRPG_MODE_TWO_STAGE) {
-                    std::memcpy(dst, ye[p].vectors.data(), sizeof(double) * RR);
-                    std::memcpy(dst + RR, ye[p].values.data(), sizeof(double) * R);
-                } else {
-                    const std::vector<double> yp = krpg::pack_upper(Y[p].data(), R);
-                    std::memcpy(dst, yp.data(), sizeof(double) * P);
-                }
-            }
+            CK(cudaMemcpyAsync(dsmall, up_h, sizeof(double) * P, cudaMemcpyHostToDevice, stream));
         }
-        double* dsmall = static_cast<double*>(small.ensure(sizeof(double) * nd));
-        CK(cudaMemcpyAsync(dsmall, up_h, sizeof(double) * nd, cudaMemcpyHostToDevice, stream));
+        stage_pos(0);
+        struct JoinAll {  // never leave eigensolver threads behind on an exception
+            std::vector<std::future<krpg::Eig>>& f;
+            ~JoinAll() {
+                for (auto& x : f)
+                    if (x.valid()) x.wait();
+            }
+        } join_all{fut};
 
         double* H = d_rows ? d_rows : static_cast<double*>(sH.ensure(sizeof(double) * J * R));
         int* derr = static_cast<int*>(err.ensure(sizeof(int)));
@@ -364,6 +378,7 @@ struct krpg_sampler {
             for (size_t p = 0; p < npos; ++p) {
                 const uint32_t k = inc[p];
                 const double* blk = dsmall + P + p * per_pos;
+                if (p > 0) stage_pos(p);
                 cudaEvent_t t0 = pbegin();
                 krpg::launch_etree_build(blk, blk + RR, f[k].tree.as<double>(), R, dQ, stream);
                 pend(KRPG_PROF_ETREE, t0, 1);
@@ -395,6 +410,7 @@ struct krpg_sampler {
         for (size_t p = 0; p < npos; ++p) {
             const uint32_t k = inc[p];
             const double* blk = dsmall + P + p * per_pos;
+            if (p > 0) stage_pos(p);
             krpg::DrawArgs a{};
             a.R = R;
             a.N = N;
