@@ -25,6 +25,23 @@ def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+_TORCH_DT = {np.dtype(np.uint32): "int32", np.dtype(np.float64): "float64"}
+
+
+def _host_array(shape, dtype) -> np.ndarray:
+    """Output buffer in page-locked host memory (torch's caching pinned
+    allocator, so repeated calls reuse blocks) so device->host copies run at
+    link speed; plain numpy memory when torch/CUDA is unavailable."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            t = torch.empty(shape, dtype=getattr(torch, _TORCH_DT[np.dtype(dtype)]), pin_memory=True)
+            return t.numpy().view(dtype)
+    except Exception:
+        pass
+    return np.empty(shape, dtype=dtype)
+
+
 def _ptr(a: np.ndarray):
     return a.ctypes.data_as(_dp)
 
@@ -192,10 +209,10 @@ class KrpSampler:
         if e < -1:
             raise KrpgInvalidArgument("KrpSampler: excluded index out of range")
         N, R = self._N, self._R
-        idx = np.empty((J, N), dtype=np.uint32)
-        prob = np.empty(J)
-        rows = np.empty((J, R))
-        mg = np.empty(J) if margin else None
+        idx = _host_array((J, N), np.uint32)
+        prob = _host_array((J,), np.float64)
+        rows = _host_array((J, R), np.float64)
+        mg = _host_array((J,), np.float64) if margin else None
         m = MODE_ONE_STAGE if mode == "one_stage" else MODE_TWO_STAGE
         check(_lib.lib().krpg_sample(self._h, e, J, seed, draw_offset, m,
                                      idx.ctypes.data_as(C.POINTER(C.c_uint32)), _ptr(prob), _ptr(rows),
