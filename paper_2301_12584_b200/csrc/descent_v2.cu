@@ -25,6 +25,7 @@
 // per-draw kernel (descent.cu).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "krpg_device.cuh"
 #include "krpg_kernels.hpp"
@@ -1272,6 +1273,12 @@ __global__ void __launch_bounds__(WPB * 32) k_deep(DeepArgs a) {
 // P doubles; a leaf: 32 padded rows per chunk) while the next run's operand is
 // pulled into L2. All arithmetic then runs out of shared memory.
 // ---------------------------------------------------------------------------
+// runs of at least this many draws use the DMMA block path in k_deep2
+#ifndef KRPG_DEEP_DMMA_MIN
+#define KRPG_DEEP_DMMA_MIN 4
+#endif
+constexpr int kDeepDmmaMin = KRPG_DEEP_DMMA_MIN;
+
 template <int NB, typename T>
 struct DeepCfg {
     static constexpr int R = 8 * NB;
@@ -1334,38 +1341,51 @@ __device__ __forceinline__ void small_qf(const double* Gs, const double* x2s, co
                                          int lane, double (&mass)[3]) {
     constexpr int R = 8 * NB;
     constexpr int S = (R + 31) / 32;
-    double acc[ND][S];
+    // two partial accumulators (even / odd rows) halve the dependent DFMA chains
+    double acc[ND][S], acc1[ND][S];
 #pragma unroll
     for (int t = 0; t < ND; ++t)
 #pragma unroll
-        for (int s = 0; s < S; ++s) acc[t][s] = 0.0;
+        for (int s = 0; s < S; ++s) acc[t][s] = acc1[t][s] = 0.0;
     int off = 0;
 #pragma unroll
     for (int kb = 0; kb < S; ++kb) {
-        const int a_end = R < 32 * (kb + 1) ? R : 32 * (kb + 1);
-#pragma unroll 4
-        for (int ar = 32 * kb; ar < a_end; ++ar) {
-            double g[S];
+        const int a_end = R < 32 * (kb + 1) ? R : 32 * (kb + 1);  // even: R is a multiple of 8
+#pragma unroll 2
+        for (int ar = 32 * kb; ar < a_end; ar += 2) {
+            const int off1 = off + R - ar;  // row ar + 1
+            double g[S], h[S];
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const int b = lane + 32 * s;
                 if (s < kb) {
                     g[s] = 0.0;
+                    h[s] = 0.0;
                 } else if (s == kb) {
                     g[s] = (b >= ar && b < R) ? Gs[off + b - ar] : 0.0;
+                    h[s] = (b >= ar + 1 && b < R) ? Gs[off1 + b - ar - 1] : 0.0;
                 } else {
                     g[s] = b < R ? Gs[off + b - ar] : 0.0;
+                    h[s] = b < R ? Gs[off1 + b - ar - 1] : 0.0;
                 }
             }
 #pragma unroll
             for (int t = 0; t < ND; ++t) {
                 const double xa2 = x2s[t * R + ar];
+                const double xb2 = x2s[t * R + ar + 1];
 #pragma unroll
-                for (int s = kb; s < S; ++s) acc[t][s] = fma(g[s], xa2, acc[t][s]);
+                for (int s = kb; s < S; ++s) {
+                    acc[t][s] = fma(g[s], xa2, acc[t][s]);
+                    acc1[t][s] = fma(h[s], xb2, acc1[t][s]);
+                }
             }
-            off += R - ar;
+            off = off1 + R - ar - 1;
         }
     }
+#pragma unroll
+    for (int t = 0; t < ND; ++t)
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[t][s] += acc1[t][s];
     double gbb[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -1435,7 +1455,7 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
                 }
             }
             const int n = re - rs;
-            if (n >= 4) {
+            if (n >= kDeepDmmaMin) {
                 cp_async_wait_all();
                 __syncwarp();
                 for (int b0 = rs; b0 < re; b0 += 8) {
@@ -1524,6 +1544,14 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
         const uint64_t first = l * a.topo.F;
         const uint64_t last = first + a.topo.F < a.topo.I ? first + a.topo.F : a.topo.I;
         const bool in_run = lane >= rs && lane < re;
+        // z fragments of the run's first 8-draw block, loaded once for all its chunks
+        double zfirst[2 * NB];
+        {
+            const int nb0 = min(8, re - rs);
+            const uint32_t dd0 = __shfl_sync(0xffffffffu, d, (rs + m8) & 31);
+#pragma unroll
+            for (int s = 0; s < 2 * NB; ++s) zfirst[s] = m8 < nb0 ? a.X[uint64_t(dd0) * R + 4 * s + r4] : 0.0;
+        }
         for (uint64_t c0 = first; c0 < last; c0 += C::LROWS) {
             if (!__any_sync(0xffffffffu, in_run && pick == ~uint64_t{0})) break;  // every draw picked
             const int nrow = last - c0 < uint64_t(C::LROWS) ? int(last - c0) : C::LROWS;
@@ -1551,17 +1579,30 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
                 const uint32_t dd = __shfl_sync(0xffffffffu, d, (b0 + m8) & 31);
                 double zb[2 * NB];
 #pragma unroll
-                for (int s = 0; s < 2 * NB; ++s) zb[s] = m8 < nb ? a.X[uint64_t(dd) * R + 4 * s + r4] : 0.0;
+                for (int s = 0; s < 2 * NB; ++s)
+                    zb[s] = b0 == rs ? zfirst[s] : (m8 < nb ? a.X[uint64_t(dd) * R + 4 * s + r4] : 0.0);
+                // all tiles of the chunk first: 2 x NTL independent DMMA chains (even / odd k)
+                constexpr int NTL = C::LROWS / 8;
+                double qa[NTL][2];
 #pragma unroll
-                for (int tt = 0; tt < C::LROWS / 8; ++tt) {
-                    if (8 * tt >= nrow) break;
+                for (int tt = 0; tt < NTL; ++tt) {
                     const int row = 8 * tt + m8;
                     const bool rv = row < nrow;
                     const T* up = reinterpret_cast<const T*>(buf + (rv ? row : 0) * C::RSP) + r4;
-                    double acc0 = 0.0, acc1 = 0.0;
+                    double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
 #pragma unroll
-                    for (int s = 0; s < 2 * NB; ++s) dmma_884(acc0, acc1, rv ? static_cast<double>(up[4 * s]) : 0.0, zb[s]);
-                    const double q0 = acc0 * acc0, q1 = acc1 * acc1;
+                    for (int s = 0; s < 2 * NB; s += 2) {
+                        dmma_884(e0, e1, rv ? static_cast<double>(up[4 * s]) : 0.0, zb[s]);
+                        if (s + 1 < 2 * NB) dmma_884(o0, o1, rv ? static_cast<double>(up[4 * s + 4]) : 0.0, zb[s + 1]);
+                    }
+                    const double acc0 = e0 + o0, acc1 = e1 + o1;
+                    qa[tt][0] = acc0 * acc0;
+                    qa[tt][1] = acc1 * acc1;
+                }
+#pragma unroll
+                for (int tt = 0; tt < NTL; ++tt) {
+                    if (8 * tt >= nrow) break;
+                    const double q0 = qa[tt][0], q1 = qa[tt][1];
                     const uint64_t rb = c0 + 8 * tt;
 #pragma unroll
                     for (int rr = 0; rr < 8; ++rr) {
