@@ -193,7 +193,8 @@ __device__ __forceinline__ double block_qf_packed(const double* G, const FragAdd
     return part;
 }
 
-constexpr int CB = WPB * 32;  // positions per CTA in the cooperative variant
+constexpr int CWARPS = 4;        // warps per CTA in the cooperative variant (8 measured slower)
+constexpr int CB = CWARPS * 32;  // positions per CTA in the cooperative variant
 
 // Same block quadratic form with the Gram already folded in shared memory
 // (off-diagonal 8x8 tiles pre-doubled) and the X block in shared memory with
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
     {  // run boundaries -> compact list s_rs
         const bool flag = tid < cnt && (tid == 0 || s_v[tid] != s_v[tid - 1]);
         const unsigned bal = __ballot_sync(0xffffffffu, flag);
-        __shared__ int wcount[WPB];
+        __shared__ int wcount[CWARPS];
         if (lane == 0) wcount[warp] = __popc(bal);
         __syncthreads();
         int off = 0;
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
         if (flag) s_rs[off + __popc(bal & ((1u << lane) - 1u))] = tid;
         if (tid == 0) {
             int tot = 0;
-            for (int w = 0; w < WPB; ++w) tot += wcount[w];
+            for (int w = 0; w < CWARPS; ++w) tot += wcount[w];
             s_nruns = tot;
             s_rs[tot] = cnt;
         }
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
         __syncthreads();
         const double* G = sG + buf * P;
         const int nblk = (re - rs + 7) >> 3;
-        for (int b = warp; b < nblk; b += WPB) {
+        for (int b = warp; b < nblk; b += CWARPS) {
             const int b0 = rs + 8 * b;
             const int n = min(8, re - b0);
             const int m = lane >> 2;
