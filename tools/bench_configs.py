@@ -1,0 +1,122 @@
+"""Secondary BASELINE.json configurations (the headline config 2 is bench.py):
+
+  --config 3 : N=4 factors 1.5e7 x 32, uniform[-1,1], fp32-stored / fp64-accumulated;
+               tree build, 2^20 two-stage draws, 10^5 random single-entry updates.
+  --config 4 : rank sweep, N=3 factors 2^20 x R (R in 16..256), N(0,1); J = 65536.
+
+One JSON line per measurement. Device times by CUDA events on the sampler's stream.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import torch  # noqa: E402
+
+from bench import descent_bytes, load_peaks  # noqa: E402
+from paper_2301_12584_b200 import KrpSampler  # noqa: E402
+
+
+def timed(fn, stream, reps):
+    evs = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def measure(s, N, I, R, J, storage, label, reps=5, extra=None):
+    dev = torch.device("cuda")
+    stream = torch.cuda.ExternalStream(s.stream(), device=dev)
+    peak, _ = load_peaks()
+    # tree build (device time of the leaf + level kernels)
+    s.profile_enable(True)
+    s.profile_read(reset=True)
+    for j in range(N):
+        s.rebuild(j)
+    pb = s.profile_read(reset=True)
+    build_ms = (pb["tree_leaf"]["ms"] + pb["tree_levels"]["ms"]) / N
+    P = R * (R + 1) // 2
+    L = (I + R - 1) // R
+    elt = 4 if storage == "f32" else 8
+    build_bytes = I * R * elt + L * P * 8
+    idx = torch.empty(J, N, dtype=torch.int32, device=dev)
+    prob = torch.empty(J, dtype=torch.float64, device=dev)
+    rows = torch.empty(J, R, dtype=torch.float64, device=dev)
+    for i in range(2):
+        s.sample_device(None, J, 7 + i, idx, prob, rows)
+    s.profile_read(reset=True)
+    ts = timed(lambda: s.sample_device(None, J, 100, idx, prob, rows), stream, reps)
+    prof = s.profile_read(reset=True)
+    ms = float(np.median(ts))
+    bytes_step, _ = descent_bytes(idx.cpu().numpy().view(np.uint32), [I] * N, R, elt=elt)
+    draws_ms = prof["draws"]["ms"] / reps
+    line = {"config": label, "N": N, "I": I, "R": R, "J": J, "storage": storage,
+            "samples_per_s": J / (ms / 1e3), "ms_per_sample_call": ms,
+            "descent": {"alg_bytes": bytes_step, "kernel_ms": draws_ms,
+                        "achieved_gbs": bytes_step / (draws_ms / 1e3) / 1e9,
+                        "frac_of_hbm": bytes_step / (draws_ms / 1e3) / 1e9 / peak},
+            "tree_build": {"ms_per_factor": build_ms, "alg_bytes": build_bytes,
+                           "achieved_gbs": build_bytes / (build_ms / 1e3) / 1e9,
+                           "gflops": I * R * (R + 1) / (build_ms / 1e3) / 1e9},
+            "descent_path": "grouped-dmma" if (R % 8 == 0 and R <= 64) else "per-draw"}
+    if extra:
+        line.update(extra)
+    print(json.dumps(line), flush=True)
+
+
+def config3(args):
+    N, I, R, J = 4, 15_000_000, 32, 1 << 20
+    g = torch.Generator(device="cuda").manual_seed(3)
+    fs = [torch.rand(I, R, dtype=torch.float32, device="cuda", generator=g) * 2 - 1 for _ in range(N)]
+    s = KrpSampler.from_device(fs, storage="f32")
+    del fs
+    torch.cuda.empty_cache()
+    # 10^5 random single-entry updates on factor 0 (one batched call, wall time incl. transfers)
+    rng = np.random.default_rng(5)
+    n = 100_000
+    r = rng.integers(0, I, n).astype(np.uint64)
+    c = rng.integers(0, R, n).astype(np.uint32)
+    v = rng.uniform(-1, 1, n)
+    s.update_factor_entries(0, r[:10], c[:10], v[:10])  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s.update_factor_entries(0, r, c, v)
+    torch.cuda.synchronize()
+    upd_s = time.perf_counter() - t0
+    measure(s, N, I, R, J, "f32", "config3", reps=3,
+            extra={"updates": {"count": n, "seconds": upd_s, "updates_per_s": n / upd_s}})
+
+
+def config4(args):
+    for R in args.ranks:
+        N, I, J = 3, 1 << 20, 65536
+        g = torch.Generator(device="cuda").manual_seed(R)
+        fs = [torch.randn(I, R, dtype=torch.float64, device="cuda", generator=g) for _ in range(N)]
+        s = KrpSampler.from_device(fs)
+        del fs
+        measure(s, N, I, R, J, "f64", f"config4_R{R}", reps=3)
+        s.close()
+        torch.cuda.empty_cache()
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", type=int, choices=[3, 4], required=True)
+    p.add_argument("--ranks", type=int, nargs="+", default=[16, 32, 64, 128, 256])
+    args = p.parse_args()
+    torch.cuda.init()
+    (config3 if args.config == 3 else config4)(args)
+
+
+if __name__ == "__main__":
+    main()
