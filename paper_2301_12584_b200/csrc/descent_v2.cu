@@ -46,68 +46,6 @@ struct Tiles {
     __host__ __device__ static constexpr int t(int p, int q) { return p * NB - (p * (p - 1)) / 2 + (q - p); }
 };
 
-// Gather the DMMA B fragments of a packed symmetric matrix (reference packed
-// upper triangle, segment_tree_sampler.hpp:111-115): bf[t(p,q)][s] holds
-// c_pq * G[8p + 4s + (lane&3)][8q + (lane>>2)], c = 2 off the diagonal tile.
-template <int NB>
-[[maybe_unused]] __device__ __forceinline__ void load_gfrag(const double* __restrict__ G, int lane,
-                                           double (&bf)[Tiles<NB>::NT][2]) {
-    constexpr int R = 8 * NB;
-    const int r4 = lane & 3, cq = lane >> 2;
-#pragma unroll
-    for (int p = 0; p < NB; ++p) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const int row = 8 * p + 4 * s + r4;
-            const int rowoff = row * R - (row * (row - 1)) / 2 - row;  // pack_index(row, col) = rowoff + col
-#pragma unroll
-            for (int q = p; q < NB; ++q) {
-                const int col = 8 * q + cq;
-                int idx;
-                if (q > p) {
-                    idx = rowoff + col;
-                } else {
-                    idx = row <= col ? rowoff + col : col * R - (col * (col - 1)) / 2 - col + row;
-                }
-                const double g = __ldg(G + idx);
-                bf[Tiles<NB>::t(p, q)][s] = q > p ? g + g : g;
-            }
-        }
-    }
-}
-
-// mass_m = x_m^T G x_m for the 8 rows m = lane>>2 of an X block (row pointer xr,
-// nullptr = masked row); all 4 lanes of a row end with the same value.
-template <int NB>
-__device__ __forceinline__ double block_qf(const double (&bf)[Tiles<NB>::NT][2], const double* __restrict__ xr,
-                                           int lane) {
-    const int r4 = lane & 3;
-    double y[NB][2];
-#pragma unroll
-    for (int q = 0; q < NB; ++q) y[q][0] = y[q][1] = 0.0;
-#pragma unroll
-    for (int p = 0; p < NB; ++p) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const double a = xr ? xr[8 * p + 4 * s + r4] : 0.0;
-#pragma unroll
-            for (int q = p; q < NB; ++q) dmma_884(y[q][0], y[q][1], a, bf[Tiles<NB>::t(p, q)][s]);
-        }
-    }
-    double part = 0.0;
-    if (xr) {
-#pragma unroll
-        for (int q = 0; q < NB; ++q) {
-            const double2 xv = *reinterpret_cast<const double2*>(xr + 8 * q + 2 * r4);
-            part = fma(xv.x, y[q][0], part);
-            part = fma(xv.y, y[q][1], part);
-        }
-    }
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    return part;
-}
-
 struct EvalArgs {
     uint64_t J;
     const uint32_t* perm;   // sorted position -> draw (nullptr: identity)
@@ -196,244 +134,6 @@ __device__ __forceinline__ double block_qf_packed(const double* G, const FragAdd
 constexpr int CWARPS = 4;        // warps per CTA in the cooperative variant (8 measured slower)
 constexpr int CB = CWARPS * 32;  // positions per CTA in the cooperative variant
 
-// Same block quadratic form with the Gram already folded in shared memory
-// (off-diagonal 8x8 tiles pre-doubled) and the X block in shared memory with
-// row stride XS doubles.
-template <int NB>
-__device__ __forceinline__ double block_qf_folded(const double* G, const FragAddr<NB>& fa, const double* xr,
-                                                  int lane) {
-    const int r4 = lane & 3, cq = lane >> 2;
-    double av[NB][2];
-#pragma unroll
-    for (int p = 0; p < NB; ++p)
-#pragma unroll
-        for (int s = 0; s < 2; ++s) av[p][s] = xr[8 * p + 4 * s + r4];
-    double y[NB][2];
-#pragma unroll
-    for (int q = 0; q < NB; ++q) y[q][0] = y[q][1] = 0.0;
-#pragma unroll
-    for (int p = 0; p < NB; ++p) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            dmma_884(y[p][0], y[p][1], av[p][s], G[fa.diag[p][s]]);
-#pragma unroll
-            for (int q = p + 1; q < NB; ++q) dmma_884(y[q][0], y[q][1], av[p][s], G[fa.rowoff[p][s] + 8 * q + cq]);
-        }
-    }
-    double part = 0.0;
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-        const double2 xv = *reinterpret_cast<const double2*>(xr + 8 * q + 2 * r4);
-        part = fma(xv.x, y[q][0], part);
-        part = fma(xv.y, y[q][1], part);
-    }
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    return part;
-}
-
-// double the entries of off-diagonal 8x8 tiles of a packed Gram in place
-template <int NB>
-__device__ __forceinline__ void fold_offdiag(double* G, int tid, int nthreads) {
-    constexpr int R = 8 * NB;
-    constexpr int P = R * (R + 1) / 2;
-    for (int k = tid; k < P; k += nthreads) {
-        uint32_t a, b;
-        unpack_pair(R, uint32_t(k), a, b);
-        if ((a >> 3) != (b >> 3)) G[k] += G[k];
-    }
-}
-
-// Cooperative shallow-level kernel, v3: everything a block needs is in shared
-// memory before the DMMAs start — the CTA's 128 X rows (cp.async, padded
-// stride), its per-draw scalars, and each run's Gram (TMA, double-buffered,
-// folded once per run).
-template <int NB>
-struct CtaCfg {
-    static constexpr int R = 8 * NB;
-    static constexpr int P = R * (R + 1) / 2;
-    static constexpr int GD = (P + 15) / 16 * 16;  // doubles per Gram buffer (16-double aligned)
-    static constexpr int XS = R + 2;               // padded X row stride (doubles): 16 B aligned rows
-    static constexpr size_t SMEM = sizeof(double) * (2 * GD + size_t(CB) * XS + 4 * CB);
-};
-
-template <int NB, int MODE>
-__global__ void __launch_bounds__(CB) k_eval_cta3(EvalArgs a) {
-    using C = CtaCfg<NB>;
-    constexpr int R = 8 * NB;
-    constexpr uint32_t P = uint32_t(R) * (R + 1) / 2;
-    extern __shared__ __align__(128) double dsm[];
-    double* sG = dsm;                          // [2][GD]
-    double* sX = dsm + 2 * C::GD;              // [CB][XS]
-    double* s_low = sX + CB * C::XS;           // [CB]
-    double* s_ic = s_low + CB;
-    double* s_u = s_ic + CB;
-    double* s_mg = s_u + CB;
-    __shared__ uint32_t s_d[CB], s_v[CB];
-    __shared__ int s_rs[CB + 1];
-    __shared__ int s_nruns;
-    __shared__ uint32_t s_cnt[2], s_base[2];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ int wcount[WPB];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t base = uint64_t(blockIdx.x) * CB;
-    const int cnt = a.J - base < uint64_t(CB) ? int(a.J - base) : CB;
-    if (tid < cnt) {
-        const uint32_t d = a.perm ? a.perm[base + tid] : uint32_t(base + tid);
-        s_d[tid] = d;
-        s_v[tid] = MODE == EV_LEVEL ? a.node[d] : 0u;
-        if (MODE == EV_LEVEL) {
-            s_low[tid] = a.low[d];
-            s_ic[tid] = a.invc[d];
-            s_u[tid] = a.ud[d];
-            s_mg[tid] = a.margin ? a.margin[d] : 0.0;
-        }
-    }
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    // X rows of the CTA's draws -> shared (16-byte cp.async pieces, padded rows)
-    {
-        constexpr int PCS = R / 2;  // 16-byte pieces per row
-        for (int p = tid; p < cnt * PCS; p += CB) {
-            const int row = p / PCS, pc = p - row * PCS;
-            cp_async16(sX + row * C::XS + 2 * pc, a.X + uint64_t(s_d[row]) * R + 2 * pc);
-        }
-        cp_async_commit();
-    }
-    {  // run boundaries -> compact list s_rs
-        const bool flag = tid < cnt && (tid == 0 || s_v[tid] != s_v[tid - 1]);
-        const unsigned bal = __ballot_sync(0xffffffffu, flag);
-        if (lane == 0) wcount[warp] = __popc(bal);
-        __syncthreads();
-        int off = 0;
-        for (int w = 0; w < warp; ++w) off += wcount[w];
-        if (flag) s_rs[off + __popc(bal & ((1u << lane) - 1u))] = tid;
-        if (tid == 0) {
-            int tot = 0;
-            for (int w = 0; w < WPB; ++w) tot += wcount[w];
-            s_nruns = tot;
-            s_rs[tot] = cnt;
-        }
-        __syncthreads();
-    }
-    const int nruns = s_nruns;
-    auto gsrc = [&](int r) -> const double* {
-        if (MODE != EV_LEVEL) return a.tree;
-        const uint32_t v = s_v[s_rs[r]];
-        if (is_leaf(a.topo, v)) return nullptr;
-        return a.tree + slot_of(2ull * v + 1) * uint64_t(P);
-    };
-    if (tid == 0 && nruns > 0) {
-        const double* g0 = gsrc(0);
-        if (g0) {
-            mbar_arrive_expect_tx(&bar[0], P * 8);
-            tma_load_1d(sG, g0, P * 8, &bar[0]);
-        }
-    }
-    const FragAddr<NB> fa(lane);
-    uint32_t phase[2] = {0u, 0u};
-    cp_async_wait_all();
-    for (int r = 0; r < nruns; ++r) {
-        const int buf = r & 1;
-        if (tid == 0 && r + 1 < nruns) {
-            const double* g1 = gsrc(r + 1);
-            if (g1) {
-                fence_proxy_async();
-                mbar_arrive_expect_tx(&bar[buf ^ 1], P * 8);
-                tma_load_1d(sG + (buf ^ 1) * C::GD, g1, P * 8, &bar[buf ^ 1]);
-            }
-        }
-        const double* gr = gsrc(r);
-        if (!gr) continue;
-        mbar_wait(&bar[buf], phase[buf]);
-        phase[buf] ^= 1u;
-        const int rs = s_rs[r], re = s_rs[r + 1];
-        const uint32_t v = s_v[rs];
-        double* G = sG + buf * C::GD;
-        if (tid < 2) s_cnt[tid] = 0;
-        fold_offdiag<NB>(G, tid, CB);
-        __syncthreads();  // folded Gram + X rows (cp.async) visible to all warps
-        const int nblk = (re - rs + 7) >> 3;
-        for (int b = warp; b < nblk; b += WPB) {
-            const int b0 = rs + 8 * b;
-            const int n = min(8, re - b0);
-            const int m = lane >> 2;
-            const bool valid = m < n;
-            const int slot = b0 + (valid ? m : 0);
-            const double mass = block_qf_folded<NB>(G, fa, sX + slot * C::XS, lane);
-            const bool owner = valid && (lane & 3) == 0;
-            const uint32_t dd = s_d[slot];
-            if (MODE == EV_ROOT) {
-                if (owner) {
-                    if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
-                    a.invc[dd] = 1.0 / mass;
-                }
-            } else if (MODE == EV_PROB) {
-                if (owner) a.prob[dd] = mass / a.rank_div;
-            } else {
-                bool left = false;
-                double cutoff = 0.0;
-                if (owner) {
-                    const double u = s_u[slot];
-                    cutoff = s_low[slot] + s_ic[slot] * mass;
-                    left = cutoff >= u;
-                    if (a.margin) a.margin[dd] = fmin(s_mg[slot], fabs(cutoff - u));
-                }
-                const unsigned lm = __ballot_sync(0xffffffffu, owner && left);
-                const unsigned rm = __ballot_sync(0xffffffffu, owner && !left);
-                uint32_t bl = 0, br = 0;
-                if (lane == 0) {
-                    if (lm) bl = atomicAdd(&s_cnt[0], uint32_t(__popc(lm)));
-                    if (rm) br = atomicAdd(&s_cnt[1], uint32_t(__popc(rm)));
-                }
-                bl = __shfl_sync(0xffffffffu, bl, 0);
-                br = __shfl_sync(0xffffffffu, br, 0);
-                if (owner) {
-                    const unsigned below = (1u << lane) - 1u;
-                    if (left) {
-                        a.node[dd] = 2 * v + 1;
-                        a.rank[dd] = bl + __popc(lm & below);
-                    } else {
-                        a.node[dd] = 2 * v + 2;
-                        a.rank[dd] = br + __popc(rm & below);
-                        a.low[dd] = cutoff;
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        if (MODE == EV_LEVEL) {
-            if (tid == 0) {
-                s_base[0] = s_cnt[0] ? atomicAdd(a.cntL + v, s_cnt[0]) : 0u;
-                s_base[1] = s_cnt[1] ? atomicAdd(a.cntR + v, s_cnt[1]) : 0u;
-            }
-            __syncthreads();
-            for (int t = rs + tid; t < re; t += CB) {
-                const uint32_t d = s_d[t];
-                a.rank[d] += (a.node[d] & 1u) ? s_base[0] : s_base[1];
-            }
-            __syncthreads();
-        }
-    }
-}
-
-// Cooperative variant for shallow levels / single-matrix passes: the CTA's 128
-// sorted positions form few runs; each run's Gram is staged once into shared
-// memory by a 1-D TMA bulk copy (double-buffered: the next run's copy is in
-// flight while this run computes) and the run's 8-draw blocks are spread over
-// the CTA's warps. Child slots come from shared-memory counters, folded into
-// the global per-node counters with one atomic per run per side.
-//
-// Level passes write the next level's sorted order directly: a run's left
-// draws fill its node's position range [GS, GE) from the front and its right
-// draws from the back, so the child ranges need no second pass (the left
-// child's extent GS + cntL is only read by the next level). With ROOT0 the
-// level-0 pass also evaluates the root normaliser C (root Gram in the second
-// shared buffer), replacing a separate normaliser pass.
 template <int NB, int MODE, bool ROOT0 = false>
 __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
     constexpr int R = 8 * NB;
@@ -754,96 +454,6 @@ struct LeafArgs {
     Topo topo;          // Z topology (F = R)
 };
 
-// Leaf scan for runs of draws sharing a leaf: S = U_leaf * Z^T on DMMA, masses
-// S^2, per-draw sequential scan (segment_tree_sampler.cpp:281-292), then
-// h *= U[t] and the index write (krp_sampler.cpp:136-138).
-template <int NB, typename T>
-__global__ void __launch_bounds__(WPB * 32) k_leaf(LeafArgs a) {
-    constexpr int R = 8 * NB;
-    __shared__ double sm[WPB][R][9];  // masses [row][draw], padded
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t base = (uint64_t(blockIdx.x) * WPB + warp) * CHUNK;
-    if (base >= a.J) return;
-    const int cnt = a.J - base < uint64_t(CHUNK) ? int(a.J - base) : CHUNK;
-    const bool live = lane < cnt;
-    const uint32_t dl = live ? a.perm[base + lane] : 0u;
-    const uint32_t vl = live ? a.node[dl] : 0xFFFFFFFFu;
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, vl, 1);
-    uint32_t starts = __ballot_sync(0xffffffffu, live && (lane == 0 || vl != prev));
-    const T* U = static_cast<const T*>(a.U);
-    const int r4 = lane & 3, m8 = lane >> 2;
-    while (starts) {
-        const int rs = __ffs(starts) - 1;
-        starts &= starts - 1;
-        const int re = starts ? __ffs(starts) - 1 : cnt;
-        const uint32_t v = __shfl_sync(0xffffffffu, vl, rs);
-        const uint64_t l = leaf_index(a.topo, v);
-        const uint64_t first = l * a.topo.F;
-        const uint64_t last = first + a.topo.F < a.topo.I ? first + a.topo.F : a.topo.I;
-        const int nrows = int(last - first);
-        for (int b0 = rs; b0 < re; b0 += 8) {
-            const int n = min(8, re - b0);
-            const bool valid = m8 < n;
-            const uint32_t dd = __shfl_sync(0xffffffffu, dl, (b0 + m8) & 31);
-            // B fragments: Z[draw = lane>>2][4s + (lane&3)]
-            double zb[2 * NB];
-#pragma unroll
-            for (int s = 0; s < 2 * NB; ++s) zb[s] = valid ? a.Z[uint64_t(dd) * R + 4 * s + r4] : 0.0;
-            double acc[NB][2];
-#pragma unroll
-            for (int mt = 0; mt < NB; ++mt) {
-                acc[mt][0] = acc[mt][1] = 0.0;
-                const int row = 8 * mt + m8;
-                const bool rv = row < nrows;
-                const T* up = U + (first + (rv ? row : 0)) * R + r4;
-#pragma unroll
-                for (int s = 0; s < 2 * NB; ++s) {
-                    const double av = rv ? static_cast<double>(up[4 * s]) : 0.0;
-                    dmma_884(acc[mt][0], acc[mt][1], av, zb[s]);
-                }
-            }
-            __syncwarp();
-#pragma unroll
-            for (int mt = 0; mt < NB; ++mt) {
-                sm[warp][8 * mt + m8][2 * r4] = acc[mt][0] * acc[mt][0];
-                sm[warp][8 * mt + m8][2 * r4 + 1] = acc[mt][1] * acc[mt][1];
-            }
-            __syncwarp();
-            uint64_t pick = 0;
-            const uint32_t dme = __shfl_sync(0xffffffffu, dl, (b0 + (lane & 7)) & 31);
-            if (lane < n) {
-                const double ic = a.invc[dme];
-                const double u = a.ud[dme];
-                double cum = a.low[dme];
-                double mg = a.margin ? a.margin[dme] : 0.0;
-                uint64_t last_nz = ~uint64_t{0};
-                pick = ~uint64_t{0};
-                for (int i = 0; i < nrows; ++i) {
-                    const double mm = ic * sm[warp][i][lane];
-                    if (mm > 0.0) last_nz = first + i;
-                    cum += mm;
-                    mg = fmin(mg, fabs(cum - u));
-                    if (cum >= u) {
-                        pick = first + i;
-                        break;
-                    }
-                }
-                if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : last - 1;
-                if (a.margin) a.margin[dme] = mg;
-                if (a.idx) a.idx[uint64_t(dme) * a.N + a.k] = uint32_t(pick);
-            }
-            // h *= U[pick] for the block's draws
-            for (int t = 0; t < n; ++t) {
-                const uint32_t dt = __shfl_sync(0xffffffffu, dme, t);
-                const uint64_t pt = __shfl_sync(0xffffffffu, pick, t);
-                for (int c = lane; c < R; c += 32)
-                    a.H[uint64_t(dt) * R + c] *= static_cast<double>(U[pt * R + c]);
-            }
-            __syncwarp();
-        }
-    }
-}
-
 // Leaf scan, streaming version: each warp streams the rows of its runs' leaves
 // HBM -> shared memory through a 3-stage 1-D TMA ring (16 rows per stage, rows
 // padded for conflict-light fragment reads), computes the 16 x 8 mass tile of
@@ -854,7 +464,7 @@ __global__ void __launch_bounds__(WPB * 32) k_leaf(LeafArgs a) {
 template <int NB, typename T>
 struct LeafCfg2 {
     static constexpr int R = 8 * NB;
-    static constexpr int CH = 16;
+    static constexpr int CH = NB <= 8 ? 16 : 8;  // rows per stage (smem: 4 warps x 3 stages)
     static constexpr int STAGES = 3;
     static constexpr int ROWB = R * int(sizeof(T));
     static constexpr int RS = ROWB;  // unpadded: one bulk copy per chunk
@@ -962,7 +572,7 @@ __global__ void __launch_bounds__(WPB * 32) k_leaf2(LeafArgs a) {
 #pragma unroll
                 for (int s = 0; s < 2 * NB; ++s) zb[s] = valid ? a.Z[uint64_t(dd) * R + 4 * s + r4] : 0.0;
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
+                for (int mt = 0; mt < C::CH / 8; ++mt) {
                     const int row = 8 * mt + m8;
                     const bool rv = row < nr;
                     const T* up = reinterpret_cast<const T*>(buf + (rv ? row : 0) * C::RS) + r4;
@@ -1025,256 +635,7 @@ struct DeepArgs {
     Topo topo;
 };
 
-// Mass x^T G x of up to 3 draws of one run on the CUDA cores (a run of 1-3
-// draws would waste 5/8+ of every DMMA): lane b owns x_b, rows of the packed
-// Gram are streamed 8 at a time (16 coalesced loads in flight per lane), x_a is
-// a shared-memory broadcast.
-template <int S>
-__device__ __forceinline__ void small_run_qf(const double* __restrict__ G, const double (&xr)[3][S],
-                                             const double* xs /*[3][R]*/, int n, uint32_t R, int lane,
-                                             double (&mass)[3]) {
-    double acc[3][S];
-#pragma unroll
-    for (int t = 0; t < 3; ++t)
-#pragma unroll
-        for (int s = 0; s < S; ++s) acc[t][s] = 0.0;
-    constexpr int RB = 8;
-    for (uint32_t a0 = 0; a0 < R; a0 += RB) {
-        double g[RB][S];
-#pragma unroll
-        for (int j = 0; j < RB; ++j) {
-            const uint32_t ar = a0 + j;
-            const uint32_t off = ar * R - (ar * (ar - 1)) / 2;
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const uint32_t b = uint32_t(lane) + 32u * s;
-                g[j][s] = (ar < R && b >= ar && b < R) ? __ldg(G + off + (b - ar)) : 0.0;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < RB; ++j) {
-            const uint32_t ar = a0 + j;
-#pragma unroll
-            for (int t = 0; t < 3; ++t) {
-                if (t >= n) break;
-                const double xa = ar < R ? xs[t * R + ar] : 0.0;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    const uint32_t b = uint32_t(lane) + 32u * s;
-                    acc[t][s] = fma(g[j][s], b == ar ? xa : xa + xa, acc[t][s]);
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-        double p = 0.0;
-#pragma unroll
-        for (int s = 0; s < S; ++s) p = fma(acc[t][s], xr[t][s], p);
-        mass[t] = warp_sum(p);
-    }
-}
-
-// Deep levels + leaf scan, fused: each warp carries the 32 draws at its sorted
-// positions from level `level0` to the leaves with warp-local regrouping (a run
-// splits into its left then right draws: a stable partition done with ballots
-// and one shuffle permutation per level), so no global scatter, counters or
-// extra launches are needed where runs hold only a handful of draws. Runs of
-// >= 4 draws use the DMMA block kernel, smaller ones the CUDA-core path. The
-// leaf scan walks the leaf 8 rows at a time (DMMA U_rows x Z^T) and stops as
-// soon as every draw of the block has picked its row.
-template <int NB, typename T>
-__global__ void __launch_bounds__(WPB * 32) k_deep(DeepArgs a) {
-    constexpr int R = 8 * NB;
-    constexpr int S = (R + 31) / 32;
-    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
-    __shared__ double xsm[WPB][3 * R];
-    __shared__ uint32_t perm_sm[WPB][32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t base = (uint64_t(blockIdx.x) * WPB + warp) * 32;
-    if (base >= a.J) return;
-    const int cnt = a.J - base < 32ull ? int(a.J - base) : 32;
-    const bool live = lane < cnt;
-    uint32_t d = live ? a.perm[base + lane] : 0u;
-    uint32_t v = live ? a.node[d] : 0xFFFFFFFFu;
-    double lo = 0.0, ic = 0.0, uu = 0.0, mg = 0.0;
-    if (live) {
-        lo = a.low[d];
-        ic = a.invc[d];
-        uu = a.ud[d];
-        mg = a.margin ? a.margin[d] : 0.0;
-    }
-    const FragAddr<NB> fa(lane);
-    const unsigned below = (1u << lane) - 1u;
-    double* xs = xsm[warp];
-
-    for (uint32_t lev = a.level0; lev < a.topo.d; ++lev) {
-        const uint32_t prevv = __shfl_up_sync(0xffffffffu, v, 1);
-        const uint32_t starts = __ballot_sync(0xffffffffu, live && (lane == 0 || v != prevv));
-        double mine = 0.0;
-        uint32_t st = starts;
-        while (st) {
-            const int rs = __ffs(st) - 1;
-            st &= st - 1;
-            const int re = st ? __ffs(st) - 1 : cnt;
-            const uint32_t vr = __shfl_sync(0xffffffffu, v, rs);
-            if (is_leaf(a.topo, vr)) continue;
-            const double* G = a.tree + slot_of(2ull * vr + 1) * P;
-            if (st) {  // warm L2 with the next run's Gram
-                const uint32_t vn = __shfl_sync(0xffffffffu, v, __ffs(st) - 1);
-                if (!is_leaf(a.topo, vn)) {
-                    const char* gn = reinterpret_cast<const char*>(a.tree + slot_of(2ull * vn + 1) * P);
-                    for (uint32_t o = lane * 128; o < P * 8; o += 32 * 128)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(gn + o));
-                }
-            }
-            const int n = re - rs;
-            if (n >= 4) {
-                for (int b0 = rs; b0 < re; b0 += 8) {
-                    const int nb = min(8, re - b0);
-                    const int m = lane >> 2;
-                    const uint32_t dd = __shfl_sync(0xffffffffu, d, (b0 + m) & 31);
-                    const double mass = block_qf_packed<NB>(G, fa, m < nb ? a.X + uint64_t(dd) * R : nullptr, lane);
-                    const double mj = __shfl_sync(0xffffffffu, mass, (4 * (lane - b0)) & 31);
-                    if (lane >= b0 && lane < b0 + nb) mine = mj;
-                }
-            } else {
-                double xr[3][S];
-#pragma unroll
-                for (int t = 0; t < 3; ++t) {
-                    const uint32_t dt = __shfl_sync(0xffffffffu, d, (rs + t) & 31);
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const uint32_t b = lane + 32u * s;
-                        const double x = (t < n && b < uint32_t(R)) ? a.X[uint64_t(dt) * R + b] : 0.0;
-                        xr[t][s] = x;
-                        if (b < uint32_t(R)) xs[t * R + b] = x;
-                    }
-                }
-                __syncwarp();
-                double ms[3];
-                small_run_qf<S>(G, xr, xs, n, R, lane, ms);
-                __syncwarp();
-#pragma unroll
-                for (int t = 0; t < 3; ++t)
-                    if (lane == rs + t && t < n) mine = ms[t];
-            }
-        }
-        // branch decisions (row_sample :269-277) and the warp-local stable split
-        const bool moved = live && !is_leaf(a.topo, v);
-        bool left = false;
-        if (moved) {
-            const double cutoff = lo + ic * mine;
-            left = cutoff >= uu;
-            mg = fmin(mg, fabs(cutoff - uu));
-            if (!left) lo = cutoff;
-        }
-        const uint32_t leftm = __ballot_sync(0xffffffffu, moved && left);
-        const uint32_t movedm = __ballot_sync(0xffffffffu, moved);
-        int newpos = lane;
-        if (moved) {
-            const uint32_t le = starts & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
-            const int rs = 31 - __clz(le);
-            const uint32_t gt = starts & ~(lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
-            const int re = gt ? __ffs(gt) - 1 : cnt;
-            const uint32_t runm = (re == 32 ? 0xffffffffu : ((1u << re) - 1u)) & ~((1u << rs) - 1u);
-            const int nl = __popc(leftm & runm);
-            newpos = left ? rs + __popc(leftm & runm & below) : rs + nl + __popc(movedm & ~leftm & runm & below);
-            v = left ? 2 * v + 1 : 2 * v + 2;
-        }
-        perm_sm[warp][newpos] = uint32_t(lane);
-        __syncwarp();
-        const int src = live ? int(perm_sm[warp][lane]) : lane;
-        __syncwarp();
-        d = __shfl_sync(0xffffffffu, d, src);
-        v = __shfl_sync(0xffffffffu, v, src);
-        lo = __shfl_sync(0xffffffffu, lo, src);
-        ic = __shfl_sync(0xffffffffu, ic, src);
-        uu = __shfl_sync(0xffffffffu, uu, src);
-        mg = __shfl_sync(0xffffffffu, mg, src);
-    }
-
-    // ---------------- leaf scan (segment_tree_sampler.cpp:281-292) ----------------
-    const T* U = static_cast<const T*>(a.U);
-    const int r4 = lane & 3, m8 = lane >> 2;
-    const uint32_t prevv = __shfl_up_sync(0xffffffffu, v, 1);
-    uint32_t st = __ballot_sync(0xffffffffu, live && (lane == 0 || v != prevv));
-    uint64_t pick = ~uint64_t{0}, last_nz = ~uint64_t{0};
-    double cum = lo;
-    while (st) {
-        const int rs = __ffs(st) - 1;
-        st &= st - 1;
-        const int re = st ? __ffs(st) - 1 : cnt;
-        const uint32_t vr = __shfl_sync(0xffffffffu, v, rs);
-        const uint64_t l = leaf_index(a.topo, vr);
-        const uint64_t first = l * a.topo.F;
-        const uint64_t last = first + a.topo.F < a.topo.I ? first + a.topo.F : a.topo.I;
-        if (st) {  // warm L2 with the first half of the next run's leaf rows
-            const uint32_t vn = __shfl_sync(0xffffffffu, v, __ffs(st) - 1);
-            const uint64_t fn = leaf_index(a.topo, vn) * a.topo.F;
-            const uint64_t ln = fn + a.topo.F < a.topo.I ? fn + a.topo.F : a.topo.I;
-            const uint64_t bytes = ((ln - fn + 1) / 2) * R * sizeof(T);
-            const char* p = reinterpret_cast<const char*>(U + fn * R);
-            for (uint64_t o = uint64_t(lane) * 128; o < bytes; o += 32 * 128)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
-        }
-        for (int b0 = rs; b0 < re; b0 += 8) {
-            const int nb = min(8, re - b0);
-            const bool mine_lane = lane >= b0 && lane < b0 + nb;
-            const int jj = (lane - b0) & 7;
-            const uint32_t dd = __shfl_sync(0xffffffffu, d, (b0 + m8) & 31);
-            double zb[2 * NB];
-#pragma unroll
-            for (int s = 0; s < 2 * NB; ++s) zb[s] = m8 < nb ? a.X[uint64_t(dd) * R + 4 * s + r4] : 0.0;
-            for (uint64_t r0 = first; r0 < last; r0 += 16) {
-                if (!__any_sync(0xffffffffu, mine_lane && pick == ~uint64_t{0})) break;  // all picked: stop reading
-                double av[2][2 * NB];  // two 8-row tiles in flight
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    const uint64_t row = r0 + 8 * h2 + m8;
-                    const bool rv = row < last;
-                    const T* up = U + (rv ? row : first) * R + r4;
-#pragma unroll
-                    for (int s = 0; s < 2 * NB; ++s) av[h2][s] = rv ? static_cast<double>(__ldg(up + 4 * s)) : 0.0;
-                }
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-                    for (int s = 0; s < 2 * NB; ++s) dmma_884(acc0, acc1, av[h2][s], zb[s]);
-                    const double q0 = acc0 * acc0, q1 = acc1 * acc1;
-                    const uint64_t rb = r0 + 8 * h2;
-#pragma unroll
-                    for (int rr = 0; rr < 8; ++rr) {
-                        const double w0 = __shfl_sync(0xffffffffu, q0, rr * 4 + (jj >> 1));
-                        const double w1 = __shfl_sync(0xffffffffu, q1, rr * 4 + (jj >> 1));
-                        if (mine_lane && pick == ~uint64_t{0} && rb + rr < last) {
-                            const double mm = ic * ((jj & 1) ? w1 : w0);
-                            if (mm > 0.0) last_nz = rb + rr;
-                            cum += mm;
-                            mg = fmin(mg, fabs(cum - uu));
-                            if (cum >= uu) pick = rb + rr;
-                        }
-                    }
-                }
-            }
-            if (mine_lane) {
-                if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : last - 1;
-                if (a.margin) a.margin[d] = mg;
-                if (a.idx) a.idx[uint64_t(d) * a.N + a.k] = uint32_t(pick);
-                a.pick[d] = uint32_t(pick);  // h *= U[pick] runs as its own parallel pass
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// k_deep2: the fused deep-levels + leaf pass with every run's operand staged
-// into a per-warp shared-memory buffer by cp.async in ONE round trip (a Gram:
-// P doubles; a leaf: 32 padded rows per chunk) while the next run's operand is
-// pulled into L2. All arithmetic then runs out of shared memory.
-// ---------------------------------------------------------------------------
-// runs of at least this many draws use the DMMA block path in k_deep2
+// runs with fewer draws than this use the CUDA-core quadratic form (small_qf)
 #ifndef KRPG_DEEP_DMMA_MIN
 #define KRPG_DEEP_DMMA_MIN 4
 #endif
@@ -1296,47 +657,6 @@ struct DeepCfg {
 };
 
 // small runs (<= 3 draws) from a shared-memory Gram: lane b owns x_b
-template <int S>
-__device__ __forceinline__ void small_run_qf_sm(const double* Gs, const double (&xr)[3][S], const double* xs, int n,
-                                                uint32_t R, int lane, double (&mass)[3]) {
-    double acc[3][S];
-#pragma unroll
-    for (int t = 0; t < 3; ++t)
-#pragma unroll
-        for (int s = 0; s < S; ++s) acc[t][s] = 0.0;
-    uint32_t off = 0;
-    for (uint32_t ar = 0; ar < R; ++ar) {
-        double g[S];
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const uint32_t b = uint32_t(lane) + 32u * s;
-            g[s] = (b >= ar && b < R) ? Gs[off + (b - ar)] : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-            if (t >= n) break;
-            const double xa = xs[t * R + ar];
-            const double xa2 = xa + xa;
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const uint32_t b = uint32_t(lane) + 32u * s;
-                acc[t][s] = fma(g[s], b == ar ? xa : xa2, acc[t][s]);
-            }
-        }
-        off += R - ar;
-    }
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-        double p = 0.0;
-#pragma unroll
-        for (int s = 0; s < S; ++s) p = fma(acc[t][s], xr[t][s], p);
-        mass[t] = warp_sum(p);
-    }
-}
-
-// Same quadratic forms for exactly ND draws: acc_b = sum_{a<=b} G_ab (2 x_a)
-// (x2s holds 2x), then mass = sum_b x_b (acc_b - G_bb x_b). The row loop is
-// split at 32-column boundaries so only one register slot needs a predicate.
 template <int NB, int ND>
 __device__ __forceinline__ void small_qf(const double* Gs, const double* x2s, const double (&xr)[3][(8 * NB + 31) / 32],
                                          int lane, double (&mass)[3]) {
@@ -1647,32 +967,34 @@ unsigned grid_for(uint64_t n, unsigned block) {
     return unsigned(std::min<uint64_t>((n + block - 1) / block, 148ull * 64));
 }
 
-// mode EV_LEVEL with warp_variant selects the per-warp deep-level kernel.
-template <int NB, int MODE>
-void launch_cta3(const EvalArgs& a, unsigned grid, cudaStream_t s) {
-    constexpr size_t smem = CtaCfg<NB>::SMEM;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_eval_cta3<NB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured = true;
+template <int NB, int MODE, bool ROOT0>
+void launch_cta(const EvalArgs& a, unsigned grid, cudaStream_t s) {
+    constexpr size_t smem = 2 * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
+    if constexpr (smem > 48 * 1024) {
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(k_eval_cta<NB, MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            configured = true;
+        }
     }
-    k_eval_cta3<NB, MODE><<<grid, CB, smem, s>>>(a);
+    k_eval_cta<NB, MODE, ROOT0><<<grid, CB, smem, s>>>(a);
 }
 
+// mode EV_LEVEL with warp_variant selects the per-warp deep-level kernel (R <= 64).
 template <int NB>
 void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
     const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
-    constexpr size_t smem = 2 * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
     if (mode == EV_ROOT)
-        k_eval_cta<NB, EV_ROOT><<<grid, CB, smem, s>>>(a);
+        launch_cta<NB, EV_ROOT, false>(a, grid, s);
     else if (mode == EV_PROB)
-        k_eval_cta<NB, EV_PROB><<<grid, CB, smem, s>>>(a);
+        launch_cta<NB, EV_PROB, false>(a, grid, s);
     else if (mode == EV_LEVEL0)
-        k_eval_cta<NB, EV_LEVEL, true><<<grid, CB, smem, s>>>(a);
-    else if (warp_variant)
-        k_eval_warp<NB><<<unsigned((a.J + uint64_t(CHUNK) * WPB - 1) / (uint64_t(CHUNK) * WPB)), WPB * 32, 0, s>>>(a);
-    else
-        k_eval_cta<NB, EV_LEVEL><<<grid, CB, smem, s>>>(a);
+        launch_cta<NB, EV_LEVEL, true>(a, grid, s);
+    else if (warp_variant) {
+        if constexpr (NB <= 8)
+            k_eval_warp<NB><<<unsigned((a.J + uint64_t(CHUNK) * WPB - 1) / (uint64_t(CHUNK) * WPB)), WPB * 32, 0, s>>>(a);
+    } else
+        launch_cta<NB, EV_LEVEL, false>(a, grid, s);
 }
 
 void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
@@ -1684,7 +1006,19 @@ void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, bool
         case 5: return launch_eval<5>(mode, a, s, warp_variant);
         case 6: return launch_eval<6>(mode, a, s, warp_variant);
         case 7: return launch_eval<7>(mode, a, s, warp_variant);
-        default: return launch_eval<8>(mode, a, s, warp_variant);
+        case 8: return launch_eval<8>(mode, a, s, warp_variant);
+        case 9: return launch_eval<9>(mode, a, s);
+        case 10: return launch_eval<10>(mode, a, s);
+        case 11: return launch_eval<11>(mode, a, s);
+        case 12: return launch_eval<12>(mode, a, s);
+        case 13: return launch_eval<13>(mode, a, s);
+        case 14: return launch_eval<14>(mode, a, s);
+        case 15: return launch_eval<15>(mode, a, s);
+        case 16: return launch_eval<16>(mode, a, s);
+        case 17: return launch_eval<17>(mode, a, s);
+        case 18: return launch_eval<18>(mode, a, s);
+        case 19: return launch_eval<19>(mode, a, s);
+        default: return launch_eval<20>(mode, a, s);
     }
 }
 
@@ -1738,13 +1072,27 @@ void dispatch_leaf(uint32_t R, const LeafArgs& a, cudaStream_t s) {
         case 5: return launch_leaf2<5, T>(a, s);
         case 6: return launch_leaf2<6, T>(a, s);
         case 7: return launch_leaf2<7, T>(a, s);
-        default: return launch_leaf2<8, T>(a, s);
+        case 8: return launch_leaf2<8, T>(a, s);
+        case 9: return launch_leaf2<9, T>(a, s);
+        case 10: return launch_leaf2<10, T>(a, s);
+        case 11: return launch_leaf2<11, T>(a, s);
+        case 12: return launch_leaf2<12, T>(a, s);
+        case 13: return launch_leaf2<13, T>(a, s);
+        case 14: return launch_leaf2<14, T>(a, s);
+        case 15: return launch_leaf2<15, T>(a, s);
+        case 16: return launch_leaf2<16, T>(a, s);
+        case 17: return launch_leaf2<17, T>(a, s);
+        case 18: return launch_leaf2<18, T>(a, s);
+        case 19: return launch_leaf2<19, T>(a, s);
+        default: return launch_leaf2<20, T>(a, s);
     }
 }
 
 }  // namespace v2
 
-bool grouped_supported(uint32_t R, uint32_t mode) { return mode == 0 && R % 8 == 0 && R >= 8 && R <= 64; }
+// R <= 64: CTA levels + fused deep/leaf kernel; 64 < R <= 160: CTA kernel on every
+// level (both Gram buffers of a run fit in shared memory) + streaming leaf scan.
+bool grouped_supported(uint32_t R, uint32_t mode) { return mode == 0 && R % 8 == 0 && R >= 8 && R <= 160; }
 
 // One factor position of the two-stage draw, grouped version. Returns #launches.
 int launch_position_grouped(const GroupedArgs& g) {
@@ -1823,9 +1171,9 @@ int launch_position_grouped(const GroupedArgs& g) {
     e.topo = tz;
     // shallow levels: global regrouping; deep levels + leaf scan: one fused pass
     uint32_t l0 = 0;
-    while (l0 < tz.d && !deep_level(J, l0)) ++l0;
+    while (l0 < tz.d && (R > 64 || !deep_level(J, l0))) ++l0;
     cta_levels(l0);
-    if (g.fused_deep) {
+    if (g.fused_deep && R <= 64) {
         DeepArgs da{};
         da.J = J;
         da.N = g.N;

@@ -222,6 +222,188 @@ __global__ void __launch_bounds__(LeafCfg<NB, T>::WPC * 32)
     }
 }
 
+// ---- large ranks (R = 96 .. 256, R % 32 == 0): one CTA per position ------
+// The upper-triangle 8x8 tile set no longer fits one warp's registers, so it
+// is split into 4x4-tile super-blocks (32 columns x 32 columns); warp w owns
+// super-blocks w and w + NW (at most 32 tiles = 64 accumulator registers).
+// Rows are staged once per CTA by TMA (warp 0 issues one bulk copy per row
+// through a 4-stage ring) and read by every warp. Columns use the contiguous
+// fragment layout (block p = columns 8p .. 8p+7, lane m -> column 8p+m) with
+// rows padded by 8 elements, so each fragment load is bank-conflict free.
+template <int R_, typename T>
+struct BigCfg {
+    static constexpr int R = R_;
+    static constexpr int NB = R / 8;
+    static constexpr int NBS = NB / 4;                // super-blocks per dimension
+    static constexpr int S = NBS * (NBS + 1) / 2;     // upper-triangle super-blocks
+    // Register budget: one SM cannot hold R=256's 528 tiles (67k accumulator
+    // registers), so from R=192 the super-blocks are split over SPLIT CTAs
+    // (gridDim.y) that read the same rows (the repeat reads are L2 hits when
+    // the group runs concurrently; these ranks are FP64-pipe bound anyway).
+    static constexpr int SPLIT = R >= 256 ? 3 : (R >= 192 ? 2 : 1);
+    static constexpr int SBW = R >= 192 ? 1 : 2;      // super-blocks per warp
+    static constexpr int SS = (S + SPLIT - 1) / SPLIT;  // super-blocks per CTA
+    static constexpr int NW = (SS + SBW - 1) / SBW;     // warps per CTA
+    static constexpr int CH = 8;                      // rows per chunk (2 k-steps)
+    static constexpr int STAGES = 4;
+    static constexpr int ROWB = R * int(sizeof(T));
+    static constexpr int RS = ROWB + 8 * int(sizeof(T));
+    static constexpr int CHB = CH * RS;
+    static constexpr int SMEM = STAGES * CHB + STAGES * 8;
+    static_assert(R % 32 == 0, "large-rank leaf kernel needs R % 32 == 0");
+};
+
+template <int R>
+__device__ __forceinline__ void store_superblock(const double (&acc)[16][2], int P0, int Q0, int lane,
+                                                 double* dst0, double* dst1) {
+    const int m = lane >> 2;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int p = 4 * P0 + i, q = 4 * Q0 + j;
+            if (q < p) continue;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t a = 8 * p + m, b = 8 * q + 2 * (lane & 3) + e;
+                if (a > b) continue;
+                const uint32_t idx = pack_index(R, a, b);
+                dst0[idx] = acc[4 * i + j][e];
+                if (dst1) dst1[idx] = acc[4 * i + j][e];
+            }
+        }
+}
+
+template <int R_, typename T>
+__global__ void __launch_bounds__(BigCfg<R_, T>::NW * 32, 1)
+    k_leaf_cta(const T* __restrict__ U, PosGeom g, double* __restrict__ compact, double* __restrict__ tout) {
+    using C = BigCfg<R_, T>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::CHB);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    int sp[C::SBW], sq[C::SBW];
+    bool has[C::SBW];
+#pragma unroll
+    for (int k = 0; k < C::SBW; ++k) {
+        const int sl = warp + k * C::NW;
+        const int s = int(blockIdx.y) * C::SS + sl;
+        has[k] = sl < C::SS && s < C::S;
+        if (s < C::NBS) {
+            sp[k] = sq[k] = s;
+        } else {
+            int o = s - C::NBS, p = 0, len = C::NBS - 1;
+            while (len > 0 && o >= len) {
+                o -= len;
+                ++p;
+                --len;
+            }
+            sp[k] = p;
+            sq[k] = p + 1 + o;
+        }
+    }
+
+    const uint64_t P = g.P;
+    if (blockIdx.x >= g.npos) return;
+    // producer cursor: warp 0 only (runs STAGES-1 chunks ahead of the consumers)
+    uint64_t pj = blockIdx.x, prow = 0, prs, pr1 = 0, issued = 0;
+    if (warp == 0) pos_rows(g, pj, prow, prs, pr1);
+    auto produce = [&]() {
+        if (warp != 0 || pj >= g.npos) return;
+        const int st = int(issued % C::STAGES);
+        const uint64_t left = pr1 - prow;
+        const uint32_t nrows = left < uint64_t(C::CH) ? uint32_t(left) : uint32_t(C::CH);
+        if (lane == 0) mbar_arrive_expect_tx(&bars[st], nrows * C::ROWB);
+        __syncwarp();
+        if (uint32_t(lane) < nrows)
+            tma_load_1d(smem + st * C::CHB + lane * C::RS, U + (prow + lane) * C::R, C::ROWB, &bars[st]);
+        ++issued;
+        prow += C::CH;
+        if (prow >= pr1) {
+            pj += gridDim.x;
+            if (pj < g.npos) pos_rows(g, pj, prow, prs, pr1);
+        }
+    };
+    for (int s = 0; s < C::STAGES - 1; ++s) produce();
+
+    uint64_t cj = blockIdx.x, crow, crs, cr1;
+    pos_rows(g, cj, crow, crs, cr1);
+    double acc[C::SBW][16][2];
+#pragma unroll
+    for (int k = 0; k < C::SBW; ++k)
+#pragma unroll
+        for (int t = 0; t < 16; ++t) acc[k][t][0] = acc[k][t][1] = 0.0;
+
+    const int m = lane >> 2;
+    for (uint32_t i = 0; cj < g.npos; ++i) {
+        produce();
+        const int st = int(i % C::STAGES);
+        mbar_wait(&bars[st], (i / C::STAGES) & 1);
+        const uint64_t left = cr1 - crow;
+        const int nvalid = left < uint64_t(C::CH) ? int(left) : C::CH;
+        const T* buf = reinterpret_cast<const T*>(smem + st * C::CHB);
+#pragma unroll
+        for (int ks = 0; ks < C::CH / 4; ++ks) {
+            const int row = ks * 4 + (lane & 3);
+            const bool valid = row < nvalid;
+            const T* rp = buf + row * (C::RS / int(sizeof(T))) + m;
+#pragma unroll
+            for (int k = 0; k < C::SBW; ++k) {
+                if (!has[k]) continue;
+                double xa[4], xb[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    xa[u] = valid ? static_cast<double>(rp[8 * (4 * sp[k] + u)]) : 0.0;
+                    xb[u] = valid ? static_cast<double>(rp[8 * (4 * sq[k] + u)]) : 0.0;
+                }
+                if (sp[k] == sq[k]) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = u; v < 4; ++v) dmma_884(acc[k][4 * u + v][0], acc[k][4 * u + v][1], xa[u], xb[v]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) dmma_884(acc[k][4 * u + v][0], acc[k][4 * u + v][1], xa[u], xb[v]);
+                }
+            }
+        }
+        fence_proxy_async();
+        __syncthreads();
+        crow += C::CH;
+        if (crow == crs) {  // left leaf of a pair complete: it is a left child -> stored
+            double* dst = compact + (g.left_slot0 + cj) * P;
+#pragma unroll
+            for (int k = 0; k < C::SBW; ++k)
+                if (has[k]) store_superblock<C::R>(acc[k], sp[k], sq[k], lane, dst, nullptr);
+        }
+        if (crow >= cr1) {
+            const uint64_t v = g.pos_node0 + cj;
+            double* d0 = tout ? tout + cj * P : nullptr;
+            double* d1 = stored(v) ? compact + slot_of(v) * P : nullptr;
+            if (!d0) {
+                d0 = d1;
+                d1 = nullptr;
+            }
+#pragma unroll
+            for (int k = 0; k < C::SBW; ++k) {
+                if (has[k] && d0) store_superblock<C::R>(acc[k], sp[k], sq[k], lane, d0, d1);
+#pragma unroll
+                for (int t = 0; t < 16; ++t) acc[k][t][0] = acc[k][t][1] = 0.0;
+            }
+            cj += gridDim.x;
+            if (cj < g.npos) pos_rows(g, cj, crow, crs, cr1);
+        }
+    }
+}
+
 template <typename T>
 __global__ void k_leaf_generic(const T* __restrict__ U, PosGeom g, double* __restrict__ compact,
                                double* __restrict__ tout) {
@@ -288,11 +470,33 @@ void launch_dmma(const T* U, const PosGeom& g, double* compact, double* tout, cu
     kern<<<unsigned(grid), C::WPC * 32, C::SMEM, s>>>(U, g, compact, tout);
 }
 
+template <int R_, typename T>
+void launch_big(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s) {
+    using C = BigCfg<R_, T>;
+    auto kern = k_leaf_cta<R_, T>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        configured = true;
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NW * 32, C::SMEM);
+    if (occ < 1) occ = 1;
+    const uint64_t grid = std::min<uint64_t>(g.npos, std::max<uint64_t>(1, uint64_t(sm_count()) * occ / C::SPLIT));
+    kern<<<dim3(unsigned(grid), C::SPLIT), C::NW * 32, C::SMEM, s>>>(U, g, compact, tout);
+}
+
 template <typename T>
 void launch_leaf(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s,
                  bool generic) {
     if (!generic) {
         switch (g.R) {
+            case 96: return launch_big<96, T>(U, g, compact, tout, s);
+            case 128: return launch_big<128, T>(U, g, compact, tout, s);
+            case 160: return launch_big<160, T>(U, g, compact, tout, s);
+            case 192: return launch_big<192, T>(U, g, compact, tout, s);
+            case 224: return launch_big<224, T>(U, g, compact, tout, s);
+            case 256: return launch_big<256, T>(U, g, compact, tout, s);
             case 8: return launch_dmma<1, T>(U, g, compact, tout, s);
             case 16: return launch_dmma<2, T>(U, g, compact, tout, s);
             case 24: return launch_dmma<3, T>(U, g, compact, tout, s);

@@ -46,7 +46,9 @@ def assert_draws_match(b, ref_idx, ref_prob=None, ref_rows=None, ref_margin=None
 
 # ------------------------------------------------------------------ trees
 TREE_SHAPES = [(1, 3), (2, 1), (5, 2), (64, 4), (33, 3), (4096, 16), (1000, 8), (777, 24), (513, 32),
-               (4097, 64), (3000, 40), (130, 5), (257, 1), (2049, 56), (100, 100)]
+               (4097, 64), (3000, 40), (130, 5), (257, 1), (2049, 56), (100, 100),
+               # large ranks: CTA-per-position DMMA kernel (split super-blocks from R = 192)
+               (1500, 96), (3000, 128), (1000, 160), (2500, 192), (700, 224), (2049, 256), (600, 136)]
 
 
 @pytest.mark.parametrize("I,R", TREE_SHAPES)
@@ -70,15 +72,17 @@ def test_tree_grams_node_by_node(I, R):
     assert grams.shape == (L, P)
 
 
-def test_tree_fp32_storage_upcast_parity():
+@pytest.mark.parametrize("R", [32, 128])
+def test_tree_fp32_storage_upcast_parity(R):
     """Config-3 style storage: fp32 on device, fp64 accumulation; the oracle gets the
     exact fp64 up-cast of the same fp32 values."""
-    fs = pareto_factors([(3001, 32), (2000, 32)], seed=5)
+    fs = pareto_factors([(3001, R), (2000, R)], seed=5)
     f32 = [f.astype(np.float32).astype(np.float64) for f in fs]
     s = K()(fs, storage="f32")
     o = oracle.OracleKrp(f32, "port")
     assert np.array_equal(s.factor(0), f32[0])
-    for v in [0] + list(range(1, 2 * 94 - 1, 2)):
+    L = (3001 + R - 1) // R
+    for v in [0] + list(range(1, 2 * L - 1, 2)):
         assert rel_err_matrix(s.node_gram(0, v), o.node_gram(0, v)) <= TOL
     for e in (None, 0):
         b = s.sample(e, 3000, 3, margin=True)
@@ -96,6 +100,9 @@ CASES = [
     ([(2000, 32), (1500, 32), (999, 32), (1234, 32)], 6),
     ([(700, 24), (650, 24), (30, 24)], 7),
     ([(900, 40), (10, 40)], 8),
+    ([(1500, 128), (900, 128)], 9),
+    ([(1200, 160), (800, 160), (333, 160)], 10),
+    ([(2000, 72), (1000, 72)], 11),
 ]
 
 
