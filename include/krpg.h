@@ -158,6 +158,13 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
 #define KRPG_OPT_PROFILE_DETAIL 2 /* per-kernel-type event timing inside the descent */
 #define KRPG_OPT_FUSED_DEEP 3     /* default 1: deep levels + leaf scan in one warp-local pass;
                                      0: per-level global regrouping down to the leaves */
+/* KRPG_OPT_ASYNC (default 0): krpg_sample_device returns once the call's work is
+ * enqueued on the handle's stream, without a host synchronisation, so the host
+ * setup of the next call (R x R eigensolves) overlaps this call's kernels. A
+ * degenerate-distribution error raised by any such call is reported by the next
+ * krpg_sync (or krpg_sample) on the handle; profiling events are resolved by
+ * krpg_profile_read. */
+#define KRPG_OPT_ASYNC 4
 int krpg_set_option(krpg_t h, int option, int64_t value);
 
 /* ---- host-only test support (no device needed) ---- */

@@ -88,6 +88,7 @@ PROF_NAMES = ["tree_leaf", "tree_levels", "etree", "draws", "prob", "update", "o
               "d_root", "d_level_cta", "d_level_warp", "d_regroup", "d_leaf", "d_misc", "spare2", "spare3"]
 OPT_PROFILE_DETAIL = 2
 OPT_FUSED_DEEP = 3
+OPT_ASYNC = 4
 
 _lib: C.CDLL | None = None
 

@@ -134,10 +134,16 @@ __device__ __forceinline__ double block_qf_packed(const double* G, const FragAdd
 constexpr int CWARPS = 4;        // warps per CTA in the cooperative variant (8 measured slower)
 constexpr int CB = CWARPS * 32;  // positions per CTA in the cooperative variant
 
+// Gram buffers per CTA: two (next run prefetched) while they are small; one for
+// R > 64 so that 3 CTAs share an SM (the root-fused level 0 always needs two).
+template <int NB, bool ROOT0>
+__host__ __device__ constexpr int cta_nbuf() { return (ROOT0 || NB <= 8) ? 2 : 1; }
+
 template <int NB, int MODE, bool ROOT0 = false>
 __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
     constexpr int R = 8 * NB;
     constexpr uint32_t P = uint32_t(R) * (R + 1) / 2;
+    constexpr int NBUF = cta_nbuf<NB, ROOT0>();
     extern __shared__ __align__(128) double sG[];  // [2][P]
     __shared__ uint32_t s_d[CB], s_v[CB], s_rank[CB];
     __shared__ uint8_t s_left[CB];
@@ -197,13 +203,21 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
     const FragAddr<NB> fa(lane);
     uint32_t phase[2] = {0u, 0u};
     for (int r = 0; r < nruns; ++r) {
-        const int buf = r & 1;
-        if (!ROOT0 && tid == 0 && r + 1 < nruns) {  // prefetch the next run's Gram into the other buffer
+        const int buf = NBUF == 2 ? (r & 1) : 0;
+        if (NBUF == 2 && !ROOT0 && tid == 0 && r + 1 < nruns) {  // prefetch the next run's Gram
             const double* g1 = gsrc(r + 1);
             if (g1) {
                 fence_proxy_async();
                 mbar_arrive_expect_tx(&bar[buf ^ 1], P * 8);
                 tma_load_1d(sG + (buf ^ 1) * P, g1, P * 8, &bar[buf ^ 1]);
+            }
+        }
+        if (NBUF == 1 && tid == 0 && r > 0) {  // single buffer: load after the previous run
+            const double* g1 = gsrc(r);
+            if (g1) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&bar[0], P * 8);
+                tma_load_1d(sG, g1, P * 8, &bar[0]);
             }
         }
         const int rs = s_rs[r], re = s_rs[r + 1];
@@ -290,6 +304,277 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
                         a.node[dd] = 2 * v + 2;
                         s_rank[slot] = br + __popc(rm & below);
                         a.low[dd] = cutoff;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (MODE == EV_LEVEL) {
+            if (tid == 0) {
+                s_base[0] = s_cnt[0] ? atomicAdd(a.cntL + v, s_cnt[0]) : 0u;
+                s_base[1] = s_cnt[1] ? atomicAdd(a.cntR + v, s_cnt[1]) : 0u;
+            }
+            __syncthreads();
+            for (int t = rs + tid; t < re; t += CB) {
+                const uint32_t pos = s_left[t] ? s_gs + s_base[0] + s_rank[t] : s_ge - 1u - (s_base[1] + s_rank[t]);
+                a.perm_out[pos] = s_d[t];
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ---- ranks whose Gram does not fit shared memory (R > 160) ----------------
+// Same CTA / run / decision structure as k_eval_cta, but each run's packed
+// Gram is streamed HBM/L2 -> shared memory in chunks of whole 8-row tile-rows
+// through a 3-stage TMA ring, and the quadratic form is reorganised by
+// tile-row so that nothing but a scalar survives between chunks:
+//   x^T G x = sum_p x_p . t_p,  t_p = G_pp x_p + 2 sum_{q>p} G_pq x_q,
+// t_p for 8 draws = one DMMA chain over q >= p (A = the draws' x_q fragments,
+// held in registers for the whole Gram; B = tile-row p of G). A warp carries
+// SB_BW 8-draw blocks through one pass over the Gram; runs longer than one
+// wave (CWARPS * SB_BW blocks) stream the Gram again (an L2 hit).
+constexpr int SB_BW = 2;
+constexpr int SB_STAGES = 3;
+constexpr int SB_CHD = 3072;  // doubles per ring stage (24 KB) >= the largest tile-row at R <= 256
+
+template <int NB>
+__device__ __forceinline__ int tile_row_off(int p) {  // pack_index(8p, 8p)
+    constexpr int R = 8 * NB;
+    const int r = 8 * p;
+    return r * R - (r * (r - 1)) / 2;
+}
+
+template <int NB, int MODE>
+__global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a) {
+    constexpr int R = 8 * NB;
+    constexpr uint32_t P = uint32_t(R) * (R + 1) / 2;
+    static_assert(8 * R <= SB_CHD, "tile-row larger than a ring stage");
+    constexpr int BW = NB >= 28 ? 1 : SB_BW;  // register budget: x fragments of BW blocks
+    extern __shared__ __align__(128) double ring[];  // [SB_STAGES][SB_CHD]
+    __shared__ uint32_t s_d[CB], s_v[CB], s_rank[CB];
+    __shared__ uint8_t s_left[CB];
+    __shared__ int s_rs[CB + 1];
+    __shared__ int s_nruns;
+    __shared__ int s_cb[NB + 1];  // chunk c = tile-rows [s_cb[c], s_cb[c+1])
+    __shared__ int s_nch;
+    __shared__ uint32_t s_cnt[2], s_base[2], s_gs, s_ge;
+    __shared__ __align__(8) uint64_t bar[SB_STAGES];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t base = uint64_t(blockIdx.x) * CB;
+    const int cnt = a.J - base < uint64_t(CB) ? int(a.J - base) : CB;
+    if (tid < cnt) {
+        const uint32_t d = a.perm ? a.perm[base + tid] : uint32_t(base + tid);
+        s_d[tid] = d;
+        s_v[tid] = MODE == EV_LEVEL ? a.node[d] : 0u;
+    }
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < SB_STAGES; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+        int nc = 0, p0 = 0;
+        while (p0 < NB) {  // greedy: whole tile-rows while they fit one stage
+            int p1 = p0 + 1;
+            while (p1 < NB && (p1 + 1 < NB ? tile_row_off<NB>(p1 + 1) : int(P)) - tile_row_off<NB>(p0) <= SB_CHD) ++p1;
+            s_cb[nc++] = p0;
+            p0 = p1;
+        }
+        s_cb[nc] = NB;
+        s_nch = nc;
+    }
+    __syncthreads();
+    {  // run boundaries -> compact list s_rs
+        const bool flag = tid < cnt && (tid == 0 || s_v[tid] != s_v[tid - 1]);
+        const unsigned bal = __ballot_sync(0xffffffffu, flag);
+        __shared__ int wcount[CWARPS];
+        if (lane == 0) wcount[warp] = __popc(bal);
+        __syncthreads();
+        int off = 0;
+        for (int w = 0; w < warp; ++w) off += wcount[w];
+        if (flag) s_rs[off + __popc(bal & ((1u << lane) - 1u))] = tid;
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < CWARPS; ++w) tot += wcount[w];
+            s_nruns = tot;
+            s_rs[tot] = cnt;
+        }
+        __syncthreads();
+    }
+    const int nruns = s_nruns, nch = s_nch;
+    constexpr int WAVE = CWARPS * BW;
+    auto gsrc = [&](int r) -> const double* {
+        if (MODE != EV_LEVEL) return a.tree;
+        const uint32_t v = s_v[s_rs[r]];
+        if (is_leaf(a.topo, v)) return nullptr;
+        return a.tree + slot_of(2ull * v + 1) * uint64_t(P);
+    };
+    // producer (thread 0): the sequence run -> wave -> chunk, skipping leaf runs
+    int pr = 0, pw = 0, pc = 0;
+    uint32_t issued = 0;
+    const double* pg = nullptr;
+    auto pseek = [&]() {  // advance pr to the next run with a Gram
+        while (pr < nruns && !(pg = gsrc(pr))) ++pr;
+    };
+    auto produce = [&]() {
+        if (tid != 0 || pr >= nruns) return;
+        const int st = int(issued % SB_STAGES);
+        const int o0 = tile_row_off<NB>(s_cb[pc]);
+        const int o1 = s_cb[pc + 1] < NB ? tile_row_off<NB>(s_cb[pc + 1]) : int(P);
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bar[st], uint32_t(o1 - o0) * 8u);
+        tma_load_1d(ring + st * SB_CHD, pg + o0, uint32_t(o1 - o0) * 8u, &bar[st]);
+        ++issued;
+        if (++pc == nch) {
+            pc = 0;
+            const int nblk = (s_rs[pr + 1] - s_rs[pr] + 7) >> 3;
+            if (++pw * WAVE >= nblk) {
+                pw = 0;
+                ++pr;
+                pseek();
+            }
+        }
+    };
+    if (tid == 0) {
+        pseek();
+        for (int s = 0; s < SB_STAGES - 1; ++s) produce();
+    }
+    uint32_t consumed = 0;
+    const int r4 = lane & 3, cq = lane >> 2, m = lane >> 2;
+    for (int r = 0; r < nruns; ++r) {
+        const int rs = s_rs[r], re = s_rs[r + 1];
+        if (!gsrc(r)) {  // draws parked at a leaf one level up keep their positions
+            if (MODE == EV_LEVEL)
+                for (int t = rs + tid; t < re; t += CB) a.perm_out[base + t] = s_d[t];
+            continue;
+        }
+        const uint32_t v = s_v[rs];
+        if (tid < 2) s_cnt[tid] = 0;
+        if (MODE == EV_LEVEL && tid == 0) {  // this node's position range, from its parent's
+            uint32_t gs = 0, ge = uint32_t(a.J);
+            if (v != 0) {
+                const uint32_t p = (v - 1) >> 1;
+                const uint32_t gl = a.GS[p] + a.cntL[p];
+                gs = (v & 1u) ? a.GS[p] : gl;
+                ge = (v & 1u) ? gl : a.GE[p];
+            }
+            s_gs = gs;
+            s_ge = ge;
+            a.GS[v] = gs;
+            a.GE[v] = ge;
+        }
+        __syncthreads();
+        const int nblk = (re - rs + 7) >> 3;
+        for (int w0 = 0; w0 < nblk; w0 += WAVE) {
+            // this warp's blocks of the wave: x fragments for the whole pass
+            double av[BW][NB][2];
+            double part[BW];
+            bool bval[BW];
+            const double* xr[BW];
+#pragma unroll
+            for (int j = 0; j < BW; ++j) {
+                const int b = w0 + warp + CWARPS * j;
+                bval[j] = b < nblk;
+                const int b0 = rs + 8 * b;
+                const bool valid = bval[j] && b0 + m < re;
+                xr[j] = valid ? a.X + uint64_t(s_d[b0 + m]) * R : nullptr;
+                part[j] = 0.0;
+#pragma unroll
+                for (int q = 0; q < NB; ++q)
+#pragma unroll
+                    for (int s = 0; s < 2; ++s) av[j][q][s] = xr[j] ? xr[j][8 * q + 4 * s + r4] : 0.0;
+            }
+            for (int c = 0; c < nch; ++c, ++consumed) {
+                produce();
+                const int st = int(consumed % SB_STAGES);
+                mbar_wait(&bar[st], (consumed / SB_STAGES) & 1u);
+                const double* Gc = ring + st * SB_CHD - tile_row_off<NB>(s_cb[c]);
+                const int pa = s_cb[c], pb = s_cb[c + 1];
+#pragma unroll
+                for (int p = 0; p < NB; ++p) {
+                    if (p < pa || p >= pb) continue;
+                    const int row = 8 * p + cq;
+                    const int roff = row * R - (row * (row - 1)) / 2 - row;  // pack_index(row, col) = roff + col
+                    double d0[BW][2], d1[BW][2];  // two chains (even / odd q)
+#pragma unroll
+                    for (int j = 0; j < BW; ++j) d0[j][0] = d0[j][1] = d1[j][0] = d1[j][1] = 0.0;
+#pragma unroll
+                    for (int q = p; q < NB; ++q)
+#pragma unroll
+                        for (int s = 0; s < 2; ++s) {
+                            const int col = 8 * q + 4 * s + r4;
+                            double g;
+                            if (q > p) {
+                                g = Gc[roff + col];
+                                g = g + g;
+                            } else {
+                                g = col >= row ? Gc[roff + col] : Gc[col * R - (col * (col - 1)) / 2 - col + row];
+                            }
+#pragma unroll
+                            for (int j = 0; j < BW; ++j) {
+                                if ((q & 1) == 0)
+                                    dmma_884(d0[j][0], d0[j][1], av[j][q][s], g);
+                                else
+                                    dmma_884(d1[j][0], d1[j][1], av[j][q][s], g);
+                            }
+                        }
+#pragma unroll
+                    for (int j = 0; j < BW; ++j)
+                        if (xr[j]) {
+                            const double2 xv = *reinterpret_cast<const double2*>(xr[j] + 8 * p + 2 * r4);
+                            part[j] = fma(xv.x, d0[j][0] + d1[j][0], part[j]);
+                            part[j] = fma(xv.y, d0[j][1] + d1[j][1], part[j]);
+                        }
+                }
+                __syncthreads();  // stage free for the producer
+            }
+#pragma unroll
+            for (int j = 0; j < BW; ++j) {
+                double mass = part[j];
+                mass += __shfl_xor_sync(0xffffffffu, mass, 1);
+                mass += __shfl_xor_sync(0xffffffffu, mass, 2);
+                if (!bval[j]) continue;  // warp-uniform
+                const int b0 = rs + 8 * (w0 + warp + CWARPS * j);
+                const int n = min(8, re - b0);
+                const bool valid = m < n;
+                const uint32_t dd = valid ? s_d[b0 + m] : 0u;
+                const bool owner = valid && r4 == 0;
+                if (MODE == EV_ROOT) {
+                    if (owner) {
+                        if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
+                        a.invc[dd] = 1.0 / mass;
+                    }
+                } else if (MODE == EV_PROB) {
+                    if (owner) a.prob[dd] = mass / a.rank_div;
+                } else {
+                    bool left = false;
+                    double cutoff = 0.0;
+                    if (owner) {
+                        const double u = a.ud[dd];
+                        cutoff = a.low[dd] + a.invc[dd] * mass;
+                        left = cutoff >= u;
+                        if (a.margin) a.margin[dd] = fmin(a.margin[dd], fabs(cutoff - u));
+                    }
+                    const unsigned lm = __ballot_sync(0xffffffffu, owner && left);
+                    const unsigned rm = __ballot_sync(0xffffffffu, owner && !left);
+                    uint32_t bl = 0, br = 0;
+                    if (lane == 0) {
+                        if (lm) bl = atomicAdd(&s_cnt[0], uint32_t(__popc(lm)));
+                        if (rm) br = atomicAdd(&s_cnt[1], uint32_t(__popc(rm)));
+                    }
+                    bl = __shfl_sync(0xffffffffu, bl, 0);
+                    br = __shfl_sync(0xffffffffu, br, 0);
+                    if (owner) {
+                        const unsigned below = (1u << lane) - 1u;
+                        const int slot = b0 + m;
+                        s_left[slot] = left ? 1 : 0;
+                        if (left) {
+                            a.node[dd] = 2 * v + 1;
+                            s_rank[slot] = bl + __popc(lm & below);
+                        } else {
+                            a.node[dd] = 2 * v + 2;
+                            s_rank[slot] = br + __popc(rm & below);
+                            a.low[dd] = cutoff;
+                        }
                     }
                 }
             }
@@ -576,9 +861,21 @@ __global__ void __launch_bounds__(WPB * 32) k_leaf2(LeafArgs a) {
                     const int row = 8 * mt + m8;
                     const bool rv = row < nr;
                     const T* up = reinterpret_cast<const T*>(buf + (rv ? row : 0) * C::RS) + r4;
-                    double acc0 = 0.0, acc1 = 0.0;
+                    // NC independent DMMA chains over k (a single chain of 2*NB dependent
+                    // DMMAs is latency bound at large R)
+                    constexpr int NC = NB >= 8 ? 4 : (NB >= 2 ? 2 : 1);
+                    double c0[NC], c1[NC];
 #pragma unroll
-                    for (int s = 0; s < 2 * NB; ++s) dmma_884(acc0, acc1, rv ? static_cast<double>(up[4 * s]) : 0.0, zb[s]);
+                    for (int c = 0; c < NC; ++c) c0[c] = c1[c] = 0.0;
+#pragma unroll
+                    for (int s = 0; s < 2 * NB; ++s)
+                        dmma_884(c0[s % NC], c1[s % NC], rv ? static_cast<double>(up[4 * s]) : 0.0, zb[s]);
+#pragma unroll
+                    for (int c = 1; c < NC; ++c) {
+                        c0[0] += c0[c];
+                        c1[0] += c1[c];
+                    }
+                    const double acc0 = c0[0], acc1 = c1[0];
                     msm[(8 * mt + m8) * 8 + 2 * r4] = acc0 * acc0;
                     msm[(8 * mt + m8) * 8 + 2 * r4 + 1] = acc1 * acc1;
                 }
@@ -969,7 +1266,7 @@ unsigned grid_for(uint64_t n, unsigned block) {
 
 template <int NB, int MODE, bool ROOT0>
 void launch_cta(const EvalArgs& a, unsigned grid, cudaStream_t s) {
-    constexpr size_t smem = 2 * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
+    constexpr size_t smem = cta_nbuf<NB, ROOT0>() * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
     if constexpr (smem > 48 * 1024) {
         static bool configured = false;
         if (!configured) {
@@ -978,6 +1275,29 @@ void launch_cta(const EvalArgs& a, unsigned grid, cudaStream_t s) {
         }
     }
     k_eval_cta<NB, MODE, ROOT0><<<grid, CB, smem, s>>>(a);
+}
+
+template <int NB, int MODE>
+void launch_stream_mode(const EvalArgs& a, unsigned grid, cudaStream_t s) {
+    constexpr size_t smem = size_t(SB_STAGES) * SB_CHD * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_eval_stream<NB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        configured = true;
+    }
+    k_eval_stream<NB, MODE><<<grid, CB, smem, s>>>(a);
+}
+
+// R > 160: streamed-Gram kernel; no root-fused level 0 (the host runs EV_ROOT first)
+template <int NB>
+void launch_stream(int mode, const EvalArgs& a, cudaStream_t s) {
+    const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
+    if (mode == EV_ROOT)
+        launch_stream_mode<NB, EV_ROOT>(a, grid, s);
+    else if (mode == EV_PROB)
+        launch_stream_mode<NB, EV_PROB>(a, grid, s);
+    else
+        launch_stream_mode<NB, EV_LEVEL>(a, grid, s);
 }
 
 // mode EV_LEVEL with warp_variant selects the per-warp deep-level kernel (R <= 64).
@@ -1018,7 +1338,10 @@ void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, bool
         case 17: return launch_eval<17>(mode, a, s);
         case 18: return launch_eval<18>(mode, a, s);
         case 19: return launch_eval<19>(mode, a, s);
-        default: return launch_eval<20>(mode, a, s);
+        case 20: return launch_eval<20>(mode, a, s);
+        case 24: return launch_stream<24>(mode, a, s);
+        case 28: return launch_stream<28>(mode, a, s);
+        default: return launch_stream<32>(mode, a, s);
     }
 }
 
@@ -1084,7 +1407,10 @@ void dispatch_leaf(uint32_t R, const LeafArgs& a, cudaStream_t s) {
         case 17: return launch_leaf2<17, T>(a, s);
         case 18: return launch_leaf2<18, T>(a, s);
         case 19: return launch_leaf2<19, T>(a, s);
-        default: return launch_leaf2<20, T>(a, s);
+        case 20: return launch_leaf2<20, T>(a, s);
+        case 24: return launch_leaf2<24, T>(a, s);
+        case 28: return launch_leaf2<28, T>(a, s);
+        default: return launch_leaf2<32, T>(a, s);
     }
 }
 
@@ -1092,7 +1418,10 @@ void dispatch_leaf(uint32_t R, const LeafArgs& a, cudaStream_t s) {
 
 // R <= 64: CTA levels + fused deep/leaf kernel; 64 < R <= 160: CTA kernel on every
 // level (both Gram buffers of a run fit in shared memory) + streaming leaf scan.
-bool grouped_supported(uint32_t R, uint32_t mode) { return mode == 0 && R % 8 == 0 && R >= 8 && R <= 160; }
+// 160 < R <= 256 (R % 32 == 0): streamed-Gram level kernel + streaming leaf scan.
+bool grouped_supported(uint32_t R, uint32_t mode) {
+    return mode == 0 && R % 8 == 0 && R >= 8 && (R <= 160 || (R <= 256 && R % 32 == 0));
+}
 
 // One factor position of the two-stage draw, grouped version. Returns #launches.
 int launch_position_grouped(const GroupedArgs& g) {
@@ -1141,10 +1470,16 @@ int launch_position_grouped(const GroupedArgs& g) {
             mark(8);
             return;
         }
+        if (R > 160) {  // streamed kernel: separate normaliser pass
+            e.perm = nullptr;
+            dispatch_eval(R, EV_ROOT, e, g.stream);
+            ++launches;
+            mark(8);
+        }
         for (uint32_t l = 0; l < lcta; ++l) {
             e.perm = l == 0 ? nullptr : pin;
             e.perm_out = pout;
-            dispatch_eval(R, l == 0 ? EV_LEVEL0 : EV_LEVEL, e, g.stream, false);
+            dispatch_eval(R, (l == 0 && R <= 160) ? EV_LEVEL0 : EV_LEVEL, e, g.stream, false);
             ++launches;
             mark(9);
             std::swap(pin, pout);

@@ -6,71 +6,11 @@
 #include <limits>
 #include <numeric>
 #include <stdexcept>
+#include <thread>
 
 namespace krpg {
 
 namespace {
-
-// Householder reduction of the symmetric matrix a (n x n, row-major, lower
-// triangle used) to tridiagonal form. On return a holds the orthogonal Q with
-// A = Q T Q^T, d the diagonal and e the sub-diagonal (e[0] = 0).
-void tridiagonalize(std::vector<double>& a, std::size_t n, std::vector<double>& d,
-                    std::vector<double>& e) {
-    auto A = [&](std::size_t i, std::size_t j) -> double& { return a[i * n + j]; };
-    for (std::size_t i = n - 1; i > 0; --i) {
-        const std::size_t l = i - 1;
-        double h = 0.0;
-        if (l > 0) {
-            double scale = 0.0;
-            for (std::size_t k = 0; k <= l; ++k) scale += std::abs(A(i, k));
-            if (scale == 0.0) {
-                e[i] = A(i, l);
-            } else {
-                for (std::size_t k = 0; k <= l; ++k) {
-                    A(i, k) /= scale;
-                    h += A(i, k) * A(i, k);
-                }
-                double f = A(i, l);
-                double g = f >= 0.0 ? -std::sqrt(h) : std::sqrt(h);
-                e[i] = scale * g;
-                h -= f * g;
-                A(i, l) = f - g;
-                f = 0.0;
-                for (std::size_t j = 0; j <= l; ++j) {
-                    A(j, i) = A(i, j) / h;
-                    g = 0.0;
-                    for (std::size_t k = 0; k <= j; ++k) g += A(j, k) * A(i, k);
-                    for (std::size_t k = j + 1; k <= l; ++k) g += A(k, j) * A(i, k);
-                    e[j] = g / h;
-                    f += e[j] * A(i, j);
-                }
-                const double hh = f / (h + h);
-                for (std::size_t j = 0; j <= l; ++j) {
-                    f = A(i, j);
-                    e[j] = g = e[j] - hh * f;
-                    for (std::size_t k = 0; k <= j; ++k) A(j, k) -= (f * e[k] + g * A(i, k));
-                }
-            }
-        } else {
-            e[i] = A(i, l);
-        }
-        d[i] = h;
-    }
-    d[0] = 0.0;
-    e[0] = 0.0;
-    for (std::size_t i = 0; i < n; ++i) {
-        if (d[i] != 0.0) {
-            for (std::size_t j = 0; j < i; ++j) {
-                double g = 0.0;
-                for (std::size_t k = 0; k < i; ++k) g += A(i, k) * A(k, j);
-                for (std::size_t k = 0; k < i; ++k) A(k, j) -= g * A(k, i);
-            }
-        }
-        d[i] = A(i, i);
-        A(i, i) = 1.0;
-        for (std::size_t j = 0; j < i; ++j) A(j, i) = A(i, j) = 0.0;
-    }
-}
 
 // Householder tridiagonalisation of the full symmetric matrix a (n x n,
 // row-major, both triangles kept): all updates are row-contiguous (symv +
@@ -108,6 +48,7 @@ void tridiagonalize_rowmajor(std::vector<double>& a, std::size_t n, std::vector<
         for (std::size_t i = m0; i < n; ++i) {
             const double* ai = a.data() + i * n;
             double s = 0.0;
+#pragma omp simd reduction(+ : s)
             for (std::size_t j = m0; j < n; ++j) s += ai[j] * v[j];
             p[i] = b * s;
             pv += p[i] * v[i];
@@ -129,19 +70,15 @@ void tridiagonalize_rowmajor(std::vector<double>& a, std::size_t n, std::vector<
     }
 }
 
-// Givens rotation of two contiguous rows (vectorised: the rows never alias)
-inline void rotate_rows(double* __restrict__ zi, double* __restrict__ zi1, std::size_t n, double c, double s) {
-    for (std::size_t k = 0; k < n; ++k) {
-        const double a0 = zi[k], a1 = zi1[k];
-        zi1[k] = s * a0 + c * a1;
-        zi[k] = c * a0 - s * a1;
-    }
-}
+struct Rot {
+    std::uint32_t i;  // rotates rows i, i+1 of Z^T
+    double c, s;
+};
 
-// Implicit-shift QL on the tridiagonal (d, e); zt holds Q^T (rows = vectors)
-// and is rotated alongside so its rows become the eigenvectors.
-void tridiagonal_ql(std::vector<double>& d, std::vector<double>& e, std::vector<double>& zt,
-                    std::size_t n) {
+// Implicit-shift QL on the tridiagonal (d, e), eigenvalues only; the Givens
+// rotations that would update the eigenvector matrix are recorded in order
+// (O(n^2) of them) and applied afterwards, in parallel over column slices.
+void tridiagonal_ql(std::vector<double>& d, std::vector<double>& e, std::size_t n, std::vector<Rot>& rots) {
     for (std::size_t i = 1; i < n; ++i) e[i - 1] = e[i];
     e[n - 1] = 0.0;
     const double eps = std::numeric_limits<double>::epsilon();
@@ -171,14 +108,15 @@ void tridiagonal_ql(std::vector<double>& d, std::vector<double>& e, std::vector<
                         deflated = true;
                         break;
                     }
-                    s = f / r;
-                    c = g / r;
+                    const double ir = 1.0 / r;
+                    s = f * ir;
+                    c = g * ir;
                     g = d[i + 1] - p;
                     r = (d[i] - g) * s + 2.0 * c * b;
                     p = s * r;
                     d[i + 1] = g + p;
                     g = c * r - b;
-                    rotate_rows(zt.data() + i * n, zt.data() + (i + 1) * n, n, c, s);
+                    rots.push_back(Rot{std::uint32_t(i), c, s});
                 }
                 if (deflated) continue;
                 d[l] -= p;
@@ -187,6 +125,51 @@ void tridiagonal_ql(std::vector<double>& d, std::vector<double>& e, std::vector<
             }
         } while (m != l);
     }
+}
+
+// Apply the recorded rotations to columns [k0, k1) of zt (n x n, row-major).
+void apply_rotations(const std::vector<Rot>& rots, double* zt, std::size_t n, std::size_t k0, std::size_t k1) {
+    for (const Rot& q : rots) {
+        double* __restrict__ zi = zt + q.i * n;
+        double* __restrict__ zi1 = zi + n;
+        const double c = q.c, s = q.s;
+        for (std::size_t k = k0; k < k1; ++k) {
+            const double a0 = zi[k], a1 = zi1[k];
+            zi1[k] = s * a0 + c * a1;
+            zi[k] = c * a0 - s * a1;
+        }
+    }
+}
+
+// Back-transform eigenvectors r in [r0, r1) (rows of zt): z <- H_0 ... H_{n-3} z.
+void back_transform(const std::vector<double>& refl, const std::vector<double>& beta, double* zt, std::size_t n,
+                    std::size_t r0, std::size_t r1) {
+    for (std::size_t k = n - 2; k-- > 0;) {
+        if (beta[k] == 0.0) continue;
+        const double* __restrict__ v = refl.data() + k * n;
+        for (std::size_t r = r0; r < r1; ++r) {
+            double* __restrict__ z = zt + r * n;
+            double sdot = 0.0;
+#pragma omp simd reduction(+ : sdot)
+            for (std::size_t j = k + 1; j < n; ++j) sdot += v[j] * z[j];
+            sdot *= beta[k];
+            for (std::size_t j = k + 1; j < n; ++j) z[j] -= sdot * v[j];
+        }
+    }
+}
+
+// fn(t) for t in [0, T): T-1 helper threads + the caller
+template <typename F>
+void run_parallel(unsigned T, F&& fn) {
+    if (T <= 1) {
+        fn(0u);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(T - 1);
+    for (unsigned t = 1; t < T; ++t) th.emplace_back(fn, t);
+    fn(0u);
+    for (auto& x : th) x.join();
 }
 
 }  // namespace
@@ -215,32 +198,21 @@ Eig eigh_psd(const double* G, std::size_t n) {
         std::vector<double> refl, beta;
         tridiagonalize_rowmajor(a, n, d, e, refl, beta);
         for (std::size_t i = 0; i < n; ++i) zt[i * n + i] = 1.0;
-        tridiagonal_ql(d, e, zt, n);  // zt rows: eigenvectors of the tridiagonal
-        // back-transform all vectors at once, z <- H_0 H_1 ... H_{n-3} z, on the
-        // coordinate-major copy zc[j][r] so every update is a contiguous axpy
-        std::vector<double> zc(n * n), s(n);
-        for (std::size_t r = 0; r < n; ++r)
-            for (std::size_t j = 0; j < n; ++j) zc[j * n + r] = zt[r * n + j];
-        for (std::size_t k = n - 2; k-- > 0;) {
-            if (beta[k] == 0.0) continue;
-            const double* v = refl.data() + k * n;
-            std::fill(s.begin(), s.end(), 0.0);
-            for (std::size_t j = k + 1; j < n; ++j) {
-                const double vj = v[j];
-                const double* __restrict__ zj = zc.data() + j * n;
-                double* __restrict__ sp = s.data();
-                for (std::size_t r = 0; r < n; ++r) sp[r] += vj * zj[r];
-            }
-            for (std::size_t r = 0; r < n; ++r) s[r] *= beta[k];
-            for (std::size_t j = k + 1; j < n; ++j) {
-                const double vj = v[j];
-                double* __restrict__ zj = zc.data() + j * n;
-                const double* __restrict__ sp = s.data();
-                for (std::size_t r = 0; r < n; ++r) zj[r] -= vj * sp[r];
-            }
-        }
-        for (std::size_t r = 0; r < n; ++r)
-            for (std::size_t j = 0; j < n; ++j) zt[r * n + j] = zc[j * n + r];
+        std::vector<Rot> rots;
+        rots.reserve(2 * n * n);
+        tridiagonal_ql(d, e, n, rots);  // eigenvalues; rotations recorded
+        // eigenvectors of the tridiagonal, then of A; both passes split the
+        // work into independent slices (columns, then vectors) over threads
+        const unsigned T = n >= 128 ? std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency() / 2)) : 1u;
+        const std::size_t cw = (n + T - 1) / T;
+        run_parallel(T, [&](unsigned t) {
+            const std::size_t k0 = std::min(n, t * cw), k1 = std::min(n, k0 + cw);
+            apply_rotations(rots, zt.data(), n, k0, k1);
+        });
+        run_parallel(T, [&](unsigned t) {
+            const std::size_t r0 = std::min(n, t * cw), r1 = std::min(n, r0 + cw);
+            back_transform(refl, beta, zt.data(), n, r0, r1);
+        });
     }
 
     std::vector<std::size_t> order(n);

@@ -123,7 +123,11 @@ struct krpg_sampler {
     float last_build_ms = 0.f;
     std::mutex mu;
     DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf, gstate, zbuf;
-    PinBuf up, errh;
+    PinBuf up[2], errh;       // operand staging is double-buffered (async calls)
+    cudaEvent_t up_ev[2] = {nullptr, nullptr};
+    unsigned call_no = 0;
+    bool async_mode = false;  // KRPG_OPT_ASYNC: no per-call host sync; errors at krpg_sync
+    bool err_zeroed = false;
     bool use_grouped = true;  // level-synchronous DMMA descent where supported
     bool prof_detail = false;  // per-kernel-type timing marks inside the descent
     bool fused_deep = true;    // deep levels + leaf scan fused (descent_v2.cu k_deep)
@@ -295,7 +299,12 @@ struct krpg_sampler {
 
         const size_t per_pos = mode == KRPG_MODE_TWO_STAGE ? RR + R : P;
         const size_t nd = P + npos * per_pos;
-        double* up_h = static_cast<double*>(up.ensure(sizeof(double) * nd));
+        // pinned staging slot: the one used two calls ago, whose uploads have
+        // long been consumed (waited on explicitly: calls may be asynchronous)
+        const unsigned slot = call_no++ & 1u;
+        if (!up_ev[slot]) CK(cudaEventCreateWithFlags(&up_ev[slot], cudaEventDisableTiming));
+        else CK(cudaEventSynchronize(up_ev[slot]));
+        double* up_h = static_cast<double*>(up[slot].ensure(sizeof(double) * nd));
         double* dsmall = static_cast<double*>(small.ensure(sizeof(double) * nd));
         auto stage_pos = [&](size_t p) {  // fill + upload position p's operands
             double* dst = up_h + P + p * per_pos;
@@ -326,7 +335,10 @@ struct krpg_sampler {
 
         double* H = d_rows ? d_rows : static_cast<double*>(sH.ensure(sizeof(double) * J * R));
         int* derr = static_cast<int*>(err.ensure(sizeof(int)));
-        CK(cudaMemsetAsync(derr, 0, sizeof(int), stream));
+        if (!async_mode || !err_zeroed) {  // async: the flag is sticky until krpg_sync reads it
+            CK(cudaMemsetAsync(derr, 0, sizeof(int), stream));
+            err_zeroed = true;
+        }
         if (d_idx && excluded >= 0) {
             krpg::launch_set_excluded_column(d_idx, J, N, uint32_t(excluded), stream);
             prof_launches[KRPG_PROF_OTHER] += 1;
@@ -393,17 +405,13 @@ struct krpg_sampler {
                 const int nl = krpg::launch_position_grouped(g);
                 pend(KRPG_PROF_DRAWS, t0, nl);
             }
+            CK(cudaEventRecord(up_ev[slot], stream));
             if (d_prob) {
                 cudaEvent_t t0 = pbegin();
                 krpg::launch_probabilities_grouped(H, dsmall, R, J, double(rank), d_prob, stream);
                 pend(KRPG_PROF_PROB, t0, 1);
             }
-            CK(cudaGetLastError());
-            int* eh = static_cast<int*>(errh.ensure(sizeof(int)));
-            CK(cudaMemcpyAsync(eh, derr, sizeof(int), cudaMemcpyDeviceToHost, stream));
-            CK(cudaStreamSynchronize(stream));
-            presolve();
-            if (*eh) throw std::runtime_error("row_sample: degenerate distribution (C <= 0)");
+            finish_call(derr);
             return;
         }
 
@@ -442,17 +450,38 @@ struct krpg_sampler {
             krpg::launch_draws(a);
             pend(KRPG_PROF_DRAWS, t0, 1);
         }
+        CK(cudaEventRecord(up_ev[slot], stream));
         if (d_prob) {
             cudaEvent_t t0 = pbegin();
             krpg::launch_probabilities(H, dsmall, R, J, double(rank), d_prob, stream);
             pend(KRPG_PROF_PROB, t0, 1);
         }
+        finish_call(derr);
+    }
+
+    // end of a sample call: synchronous mode reads the device error flag now;
+    // asynchronous mode (KRPG_OPT_ASYNC) leaves it for krpg_sync, and profiling
+    // events for krpg_profile_read
+    void finish_call(int* derr) {
         CK(cudaGetLastError());
+        if (async_mode) return;
         int* eh = static_cast<int*>(errh.ensure(sizeof(int)));
         CK(cudaMemcpyAsync(eh, derr, sizeof(int), cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
         presolve();
         if (*eh) throw std::runtime_error("row_sample: degenerate distribution (C <= 0)");
+    }
+
+    // synchronise and surface an error raised by any asynchronous call since the last check
+    void sync_check() {
+        CK(cudaStreamSynchronize(stream));
+        if (!async_mode || !err.p) return;
+        int flag = 0;
+        CK(cudaMemcpy(&flag, err.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (flag) {
+            CK(cudaMemset(err.p, 0, sizeof(int)));
+            throw std::runtime_error("row_sample: degenerate distribution (C <= 0)");
+        }
     }
 };
 
@@ -556,7 +585,10 @@ int krpg_destroy(krpg_t h) {
     for (DevBuf* b : {&h->tbuf, &h->small, &h->Q, &h->err, &h->sH, &h->sIdx, &h->sProb, &h->sMargin, &h->rowbuf,
                       &h->gstate, &h->zbuf})
         b->release();
-    h->up.release();
+    for (int i = 0; i < 2; ++i) {
+        h->up[i].release();
+        if (h->up_ev[i]) cudaEventDestroy(h->up_ev[i]);
+    }
     h->errh.release();
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -662,14 +694,16 @@ int krpg_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t 
         if (prob) CK(cudaMemcpyAsync(prob, dp, 8 * J, cudaMemcpyDeviceToHost, h->stream));
         if (rows) CK(cudaMemcpyAsync(rows, dr, 8 * J * h->R, cudaMemcpyDeviceToHost, h->stream));
         if (margin) CK(cudaMemcpyAsync(margin, dm, 8 * J, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        h->sync_check();
     });
 }
 
 int krpg_sync(krpg_t h) {
     return guard([&] {
         require(h, "krpg: null handle");
-        CK(cudaStreamSynchronize(h->stream));
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->sync_check();
     });
 }
 
@@ -875,6 +909,9 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset) {
     return guard([&] {
         require(h, "krpg: null handle");
         std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        CK(cudaStreamSynchronize(h->stream));  // resolve events of asynchronous calls
+        h->presolve();
         for (int c = 0; c < KRPG_PROF_N; ++c) {
             if (ms) ms[c] = h->prof_ms[c];
             if (launches) launches[c] = h->prof_launches[c];
@@ -896,6 +933,10 @@ int krpg_set_option(krpg_t h, int option, int64_t value) {
             h->prof_detail = value != 0;
         else if (option == KRPG_OPT_FUSED_DEEP)
             h->fused_deep = value != 0;
+        else if (option == KRPG_OPT_ASYNC) {
+            if (!value && h->async_mode) h->sync_check();
+            h->async_mode = value != 0;
+        }
         else
             throw std::invalid_argument("krpg_set_option: unknown option");
     });

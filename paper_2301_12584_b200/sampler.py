@@ -252,6 +252,16 @@ class KrpSampler:
         """Fused warp-local deep levels + leaf scan (default) or per-level global regrouping."""
         check(_lib.lib().krpg_set_option(self._h, _lib.OPT_FUSED_DEEP, 1 if on else 0))
 
+    def set_async(self, on: bool) -> None:
+        """KRPG_OPT_ASYNC: sample_device returns once enqueued (no host sync), so
+        the next call's host setup overlaps this call's kernels; errors surface
+        at sync()."""
+        check(_lib.lib().krpg_set_option(self._h, _lib.OPT_ASYNC, 1 if on else 0))
+
+    def sync(self) -> None:
+        """Wait for the handle's stream; raises an error left by an asynchronous call."""
+        check(_lib.lib().krpg_sync(self._h))
+
     def rebuild(self, j: int) -> None:
         check(_lib.lib().krpg_rebuild(self._h, j))
 

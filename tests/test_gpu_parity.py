@@ -103,6 +103,8 @@ CASES = [
     ([(1500, 128), (900, 128)], 9),
     ([(1200, 160), (800, 160), (333, 160)], 10),
     ([(2000, 72), (1000, 72)], 11),
+    ([(3000, 256), (1100, 256)], 12),
+    ([(2500, 192), (700, 192)], 13),
 ]
 
 
@@ -155,6 +157,31 @@ def test_draw_offset_sharding_matches_one_call():
     parts = [s.sample(None, c, 42, draw_offset=st) for st, c in [(0, 1000), (1000, 1001), (2001, 1000)]]
     assert np.array_equal(np.concatenate([p.indices for p in parts]), full.indices)
     assert np.array_equal(np.concatenate([p.probabilities for p in parts]), full.probabilities)
+
+
+def test_async_calls_match_synchronous_calls():
+    """KRPG_OPT_ASYNC: back-to-back calls without host synchronisation (staging
+    buffers reused across in-flight calls) give the same bits as synchronous calls."""
+    import torch
+    fs = pareto_factors([(5000, 64), (3000, 64), (4097, 64)], 21)
+    s = K()(fs)
+    J = 4096
+    outs = []
+    for mode_async in (False, True):
+        s.set_async(mode_async)
+        res = []
+        for i in range(5):
+            idx = torch.empty(J, 3, dtype=torch.int32, device="cuda")
+            prob = torch.empty(J, dtype=torch.float64, device="cuda")
+            rows = torch.empty(J, 64, dtype=torch.float64, device="cuda")
+            s.sample_device(None if i % 2 == 0 else i % 3, J, 900 + i, idx, prob, rows)
+            res.append((idx, prob, rows))
+        s.sync()
+        outs.append([tuple(t.cpu().numpy() for t in r) for r in res])
+    s.set_async(False)
+    for a, b in zip(*outs):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
 
 
 # ---------------------------------------------------- distribution checks

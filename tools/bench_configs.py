@@ -68,7 +68,7 @@ def measure(s, N, I, R, J, storage, label, reps=5, extra=None):
             "tree_build": {"ms_per_factor": build_ms, "alg_bytes": build_bytes,
                            "achieved_gbs": build_bytes / (build_ms / 1e3) / 1e9,
                            "gflops": I * R * (R + 1) / (build_ms / 1e3) / 1e9},
-            "descent_path": "grouped-dmma" if (R % 8 == 0 and R <= 160) else "per-draw"}
+            "descent_path": "grouped-dmma" if (R % 8 == 0 and (R <= 160 or (R <= 256 and R % 32 == 0))) else "per-draw"}
     if extra:
         line.update(extra)
     print(json.dumps(line), flush=True)
