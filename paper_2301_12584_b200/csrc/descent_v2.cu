@@ -110,10 +110,13 @@ __device__ __forceinline__ double block_qf_packed(const double* G, const FragAdd
         for (int s = 0; s < 2; ++s) {
             const double gd = G[fa.diag[p][s]];
             dmma_884(y[p][0], y[p][1], av[p][s], gd);
+            // off-diagonal tiles count twice (folded weights): (2a) g == a (2g)
+            // exactly, so the doubling is applied once to the A fragment
+            const double a2 = av[p][s] + av[p][s];
 #pragma unroll
             for (int q = p + 1; q < NB; ++q) {
                 const double g = G[fa.rowoff[p][s] + 8 * q + cq];
-                dmma_884(y[q][0], y[q][1], av[p][s], g + g);
+                dmma_884(y[q][0], y[q][1], a2, g);
             }
         }
     }
@@ -502,19 +505,16 @@ __global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a) {
 #pragma unroll
                         for (int s = 0; s < 2; ++s) {
                             const int col = 8 * q + 4 * s + r4;
-                            double g;
-                            if (q > p) {
-                                g = Gc[roff + col];
-                                g = g + g;
-                            } else {
-                                g = col >= row ? Gc[roff + col] : Gc[col * R - (col * (col - 1)) / 2 - col + row];
-                            }
+                            // off-diagonal tiles count twice: (2a) g == a (2g) exactly
+                            const double g = (q > p || col >= row) ? Gc[roff + col]
+                                                                   : Gc[col * R - (col * (col - 1)) / 2 - col + row];
 #pragma unroll
                             for (int j = 0; j < BW; ++j) {
+                                const double x = q > p ? av[j][q][s] + av[j][q][s] : av[j][q][s];
                                 if ((q & 1) == 0)
-                                    dmma_884(d0[j][0], d0[j][1], av[j][q][s], g);
+                                    dmma_884(d0[j][0], d0[j][1], x, g);
                                 else
-                                    dmma_884(d1[j][0], d1[j][1], av[j][q][s], g);
+                                    dmma_884(d1[j][0], d1[j][1], x, g);
                             }
                         }
 #pragma unroll
