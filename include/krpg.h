@@ -167,6 +167,23 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
 #define KRPG_OPT_ASYNC 4
 int krpg_set_option(krpg_t h, int option, int64_t value);
 
+/* ---- row-partitioned construction (multi-GPU) ----
+ * The tree over I rows splits into parts = 2^g subtrees (the nodes of level g);
+ * subtree `part` covers the contiguous rows krpg_partition_rows(...). A rank that
+ * holds (at least) those rows of U_j in its handle builds the subtree's stored
+ * nodes with krpg_build_partition, which also returns the subtree root Gram
+ * (P doubles, device). After the stored slots (per tree level, each partition's
+ * range is contiguous, see sharding.partition_slots) and the subtree roots are
+ * exchanged (e.g. NCCL all-gather), krpg_finish_partitions computes levels
+ * g-1 .. 0 identically on every rank. Replaces the single-process build_grams
+ * (segment_tree_sampler.cpp:151-191); results are bit-identical to it. */
+int krpg_tree_device(krpg_t h, uint32_t j, double** d_tree, uint64_t* slots);
+int krpg_factor_device(krpg_t h, uint32_t j, void** d_U);
+int krpg_build_partition(krpg_t h, uint32_t j, uint32_t parts, uint32_t part, double* d_subroot);
+int krpg_finish_partitions(krpg_t h, uint32_t j, uint32_t parts, const double* d_subroots);
+int krpg_partition_rows(uint64_t I, uint32_t R, uint32_t parts, uint32_t part, uint64_t* first,
+                        uint64_t* last);
+
 /* ---- host-only test support (no device needed) ---- */
 /* Row range [first, last) of heap node v of the complete tree over I rows with
  * leaf capacity F (SegmentTreeSampler::node_segment, segment_tree_sampler.hpp:74-76). */

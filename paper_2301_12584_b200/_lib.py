@@ -81,6 +81,11 @@ _SIGS = {
                                  C.POINTER(_u64)], _int),
     "krpg_host_eigh": ([_dp, _u32, _dp, _dp], _int),
     "krpg_set_option": ([_vp, _int, _i64], _int),
+    "krpg_tree_device": ([_vp, _u32, C.POINTER(_vp), C.POINTER(_u64)], _int),
+    "krpg_factor_device": ([_vp, _u32, C.POINTER(_vp)], _int),
+    "krpg_build_partition": ([_vp, _u32, _u32, _u32, _vp], _int),
+    "krpg_finish_partitions": ([_vp, _u32, _u32, _vp], _int),
+    "krpg_partition_rows": ([_u64, _u32, _u32, _u32, C.POINTER(_u64), C.POINTER(_u64)], _int),
 }
 OPT_GROUPED_DESCENT = 1
 

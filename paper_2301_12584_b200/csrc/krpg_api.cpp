@@ -225,6 +225,69 @@ struct krpg_sampler {
         krpg::unpack_upper(root.data(), R, F.G.data());
     }
 
+    // ---- row-partitioned construction ----
+    krpg::TreeBuildArgs tree_args(uint32_t k) {
+        Factor& F = f[k];
+        const krpg::Topo t = krpg::make_topo(F.I, R);
+        F.tree.ensure(sizeof(double) * t.L * P);
+        uint64_t na, nb;
+        krpg::tree_transient_doubles(F.I, R, &na, &nb);
+        double* base = static_cast<double*>(tbuf.ensure(sizeof(double) * (na + nb) + 16));
+        krpg::TreeBuildArgs a{};
+        a.U = F.U.p;
+        a.storage = storage;
+        a.I = F.I;
+        a.R = R;
+        a.compact = F.tree.as<double>();
+        a.tbuf_a = base;
+        a.tbuf_b = base + na;
+        a.stream = stream;
+        return a;
+    }
+    void check_parts(uint32_t k, uint32_t parts) const {
+        require(parts >= 2 && (parts & (parts - 1)) == 0, "krpg_build_partition: parts must be a power of two >= 2");
+        require(parts <= krpg::tree_positions(f[k].I, R), "krpg_build_partition: more parts than tree positions");
+    }
+    // stored nodes of subtree `part` on levels >= log2(parts), from U_k's rows of that subtree
+    void build_partition(uint32_t k, uint32_t parts, uint32_t part, double* d_subroot) {
+        check_parts(k, parts);
+        require(part < parts, "krpg_build_partition: part out of range");
+        krpg::TreeBuildArgs a = tree_args(k);
+        a.parts = parts;
+        a.part = part;
+        a.subroot = d_subroot;
+        cudaEvent_t t0 = pbegin();
+        const int nl = krpg::launch_tree_leaves(a);
+        pend(KRPG_PROF_TREE_LEAF, t0, nl);
+        t0 = pbegin();
+        const int nv = krpg::launch_tree_levels(a);
+        if (nv < 0) throw CudaError("krpg_build_partition: device copy failed");
+        pend(KRPG_PROF_TREE_LEVELS, t0, nv);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(stream));
+    }
+    // levels above the parts subtree roots; refreshes the cached root Gram
+    void finish_partitions(uint32_t k, uint32_t parts, const double* d_subroots) {
+        check_parts(k, parts);
+        krpg::TreeBuildArgs a = tree_args(k);
+        a.parts = parts;
+        cudaEvent_t t0 = pbegin();
+        const int nv = krpg::launch_tree_top(a, d_subroots);
+        if (nv < 0) throw CudaError("krpg_finish_partitions: device copy failed");
+        pend(KRPG_PROF_TREE_LEVELS, t0, nv);
+        CK(cudaGetLastError());
+        refresh_root(k);
+    }
+    void refresh_root(uint32_t k) {
+        Factor& F = f[k];
+        std::vector<double> root(P);
+        CK(cudaMemcpyAsync(root.data(), F.tree.p, sizeof(double) * P, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        presolve();
+        F.G.assign(size_t(R) * R, 0.0);
+        krpg::unpack_upper(root.data(), R, F.G.data());
+    }
+
     void upload_factor(uint32_t k, const double* host, uint64_t I) {
         Factor& F = f[k];
         F.I = I;
@@ -794,6 +857,50 @@ int krpg_rebuild(krpg_t h, uint32_t j) {
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
         h->build_tree(j);
+    });
+}
+
+int krpg_tree_device(krpg_t h, uint32_t j, double** d_tree, uint64_t* slots) {
+    return guard([&] {
+        require(h && j < h->N, "krpg_tree_device: index out of range");
+        *d_tree = h->f[j].tree.as<double>();
+        *slots = krpg::make_topo(h->f[j].I, h->R).L;
+    });
+}
+
+int krpg_factor_device(krpg_t h, uint32_t j, void** d_U) {
+    return guard([&] {
+        require(h && j < h->N, "krpg_factor_device: index out of range");
+        *d_U = h->f[j].U.p;
+    });
+}
+
+int krpg_build_partition(krpg_t h, uint32_t j, uint32_t parts, uint32_t part, double* d_subroot) {
+    return guard([&] {
+        require(h && j < h->N, "krpg_build_partition: index out of range");
+        require(d_subroot, "krpg_build_partition: null subroot buffer");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->build_partition(j, parts, part, d_subroot);
+    });
+}
+
+int krpg_finish_partitions(krpg_t h, uint32_t j, uint32_t parts, const double* d_subroots) {
+    return guard([&] {
+        require(h && j < h->N, "krpg_finish_partitions: index out of range");
+        require(d_subroots, "krpg_finish_partitions: null subroot buffer");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->finish_partitions(j, parts, d_subroots);
+    });
+}
+
+int krpg_partition_rows(uint64_t I, uint32_t R, uint32_t parts, uint32_t part, uint64_t* first, uint64_t* last) {
+    return guard([&] {
+        require(I >= 1 && R >= 1, "krpg_partition_rows: empty factor");
+        require(parts >= 1 && (parts & (parts - 1)) == 0 && part < parts, "krpg_partition_rows: bad partition");
+        require(parts <= krpg::tree_positions(I, R), "krpg_partition_rows: more parts than tree positions");
+        krpg::tree_partition_rows(I, R, parts, part, first, last);
     });
 }
 

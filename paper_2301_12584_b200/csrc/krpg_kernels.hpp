@@ -19,12 +19,21 @@ struct TreeBuildArgs {
     double* tbuf_b;
     cudaStream_t stream;
     int force_generic;   // test hook: use the scalar kernel
+    uint32_t parts = 1;  // > 1: build only subtree `part` of `parts` (a power of two)
+    uint32_t part = 0;
+    double* subroot = nullptr;  // partitioned build: receives the subtree root Gram (P)
 };
 // doubles needed for (tbuf_a, tbuf_b)
 void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b);
-// leaf / first-pair level (DMMA) then the remaining levels; returns #launches
+// leaf / first-pair level (DMMA) then the remaining levels; returns #launches (< 0: CUDA error)
 int launch_tree_leaves(const TreeBuildArgs& a);
 int launch_tree_levels(const TreeBuildArgs& a);
+// partitioned build: levels above the parts subtree roots (parts x P on device)
+int launch_tree_top(const TreeBuildArgs& a, const double* subroots);
+// positions (level d-1 nodes) of the tree over I rows with leaf capacity R
+uint64_t tree_positions(uint64_t I, uint32_t R);
+// rows [first, last) under subtree `part` of `parts`
+void tree_partition_rows(uint64_t I, uint32_t R, uint32_t parts, uint32_t part, uint64_t* first, uint64_t* last);
 
 // ---- E-tree (eigenvector stage) construction, krp_sampler.cpp:118-123 ----
 // Q[slot] = (sum_{u in node} lambda_u V[:,u] V[:,u]^T) o G_k, packed.

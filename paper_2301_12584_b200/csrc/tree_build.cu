@@ -28,6 +28,7 @@ namespace {
 
 struct PosGeom {
     uint64_t I, F, npos, hb, pos_node0, left_slot0;
+    uint64_t p0, p1;  // positions processed by this launch: [p0, p1) (a partition's subtree)
     uint32_t R, P;
 };
 
@@ -56,6 +57,8 @@ PosGeom make_geom(uint64_t I, uint32_t R) {
     g.hb = t.bottom / 2;
     g.pos_node0 = t.d ? (uint64_t{1} << D) - 1 : 0;
     g.left_slot0 = t.d ? (uint64_t{1} << (t.d - 1)) : 0;  // slot of node 2^d-1+2j is 2^(d-1)+j
+    g.p0 = 0;
+    g.p1 = g.npos;
     return g;
 }
 
@@ -142,8 +145,8 @@ __global__ void __launch_bounds__(LeafCfg<NB, T>::WPC * 32)
     __syncwarp();
 
     const uint64_t nw = uint64_t(gridDim.x) * C::WPC;
-    const uint64_t gw = uint64_t(blockIdx.x) * C::WPC + warp;
-    if (gw >= g.npos) return;
+    const uint64_t gw = g.p0 + uint64_t(blockIdx.x) * C::WPC + warp;
+    if (gw >= g.p1) return;
     const uint64_t P = g.P;
 
     // producer cursor (runs STAGES-1 chunks ahead)
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(LeafCfg<NB, T>::WPC * 32)
     pos_rows(g, pj, prow, prs, pr1);
     uint64_t issued = 0;
     auto produce = [&]() {
-        if (pj >= g.npos) return;
+        if (pj >= g.p1) return;
         const int st = int(issued % C::STAGES);
         const uint64_t left = pr1 - prow;
         const uint32_t nrows = left < uint64_t(C::CH) ? uint32_t(left) : uint32_t(C::CH);
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(LeafCfg<NB, T>::WPC * 32)
         prow += C::CH;
         if (prow >= pr1) {
             pj += nw;
-            if (pj < g.npos) pos_rows(g, pj, prow, prs, pr1);
+            if (pj < g.p1) pos_rows(g, pj, prow, prs, pr1);
         }
     };
     for (int s = 0; s < C::STAGES - 1; ++s) produce();
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(LeafCfg<NB, T>::WPC * 32)
 
     const int frow = lane & 3;
     const int fcol = (lane >> 2) * NB * int(sizeof(T));
-    for (uint64_t i = 0; cj < g.npos; ++i) {
+    for (uint64_t i = 0; cj < g.p1; ++i) {
         produce();
         const int st = int(i % C::STAGES);
         mbar_wait(&bars[st], uint32_t((i / C::STAGES) & 1));
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(LeafCfg<NB, T>::WPC * 32)
 #pragma unroll
             for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
             cj += nw;
-            if (cj < g.npos) pos_rows(g, cj, crow, crs, cr1);
+            if (cj < g.p1) pos_rows(g, cj, crow, crs, cr1);
         }
     }
 }
@@ -310,12 +313,12 @@ __global__ void __launch_bounds__(BigCfg<R_, T>::NW * 32, 1)
     }
 
     const uint64_t P = g.P;
-    if (blockIdx.x >= g.npos) return;
+    if (g.p0 + blockIdx.x >= g.p1) return;
     // producer cursor: warp 0 only (runs STAGES-1 chunks ahead of the consumers)
-    uint64_t pj = blockIdx.x, prow = 0, prs, pr1 = 0, issued = 0;
+    uint64_t pj = g.p0 + blockIdx.x, prow = 0, prs, pr1 = 0, issued = 0;
     if (warp == 0) pos_rows(g, pj, prow, prs, pr1);
     auto produce = [&]() {
-        if (warp != 0 || pj >= g.npos) return;
+        if (warp != 0 || pj >= g.p1) return;
         const int st = int(issued % C::STAGES);
         const uint64_t left = pr1 - prow;
         const uint32_t nrows = left < uint64_t(C::CH) ? uint32_t(left) : uint32_t(C::CH);
@@ -327,12 +330,12 @@ __global__ void __launch_bounds__(BigCfg<R_, T>::NW * 32, 1)
         prow += C::CH;
         if (prow >= pr1) {
             pj += gridDim.x;
-            if (pj < g.npos) pos_rows(g, pj, prow, prs, pr1);
+            if (pj < g.p1) pos_rows(g, pj, prow, prs, pr1);
         }
     };
     for (int s = 0; s < C::STAGES - 1; ++s) produce();
 
-    uint64_t cj = blockIdx.x, crow, crs, cr1;
+    uint64_t cj = g.p0 + blockIdx.x, crow, crs, cr1;
     pos_rows(g, cj, crow, crs, cr1);
     double acc[C::SBW][16][2];
 #pragma unroll
@@ -341,7 +344,7 @@ __global__ void __launch_bounds__(BigCfg<R_, T>::NW * 32, 1)
         for (int t = 0; t < 16; ++t) acc[k][t][0] = acc[k][t][1] = 0.0;
 
     const int m = lane >> 2;
-    for (uint32_t i = 0; cj < g.npos; ++i) {
+    for (uint32_t i = 0; cj < g.p1; ++i) {
         produce();
         const int st = int(i % C::STAGES);
         mbar_wait(&bars[st], (i / C::STAGES) & 1);
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(BigCfg<R_, T>::NW * 32, 1)
                 for (int t = 0; t < 16; ++t) acc[k][t][0] = acc[k][t][1] = 0.0;
             }
             cj += gridDim.x;
-            if (cj < g.npos) pos_rows(g, cj, crow, crs, cr1);
+            if (cj < g.p1) pos_rows(g, cj, crow, crs, cr1);
         }
     }
 }
@@ -409,7 +412,7 @@ __global__ void k_leaf_generic(const T* __restrict__ U, PosGeom g, double* __res
                                double* __restrict__ tout) {
     const uint32_t R = g.R;
     const uint64_t P = g.P;
-    for (uint64_t j = blockIdx.x; j < g.npos; j += gridDim.x) {
+    for (uint64_t j = g.p0 + blockIdx.x; j < g.p1; j += gridDim.x) {
         uint64_t r0, rs, r1;
         pos_rows(g, j, r0, rs, r1);
         const uint64_t v = g.pos_node0 + j;
@@ -428,8 +431,8 @@ __global__ void k_leaf_generic(const T* __restrict__ U, PosGeom g, double* __res
 }
 
 __global__ void k_level_reduce(const double* __restrict__ child, double* __restrict__ parent,
-                               double* __restrict__ compact, uint64_t nj, uint64_t P, uint64_t node0) {
-    for (uint64_t j = blockIdx.x; j < nj; j += gridDim.x) {
+                               double* __restrict__ compact, uint64_t j0, uint64_t nj, uint64_t P, uint64_t node0) {
+    for (uint64_t j = j0 + blockIdx.x; j < nj; j += gridDim.x) {
         const double* c0 = child + 2 * j * P;
         const double* c1 = c0 + P;
         const uint64_t v = node0 + j;
@@ -465,7 +468,7 @@ void launch_dmma(const T* U, const PosGeom& g, double* compact, double* tout, cu
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::WPC * 32, C::SMEM);
     if (occ < 1) occ = 1;
-    const uint64_t need = (g.npos + C::WPC - 1) / C::WPC;
+    const uint64_t need = (g.p1 - g.p0 + C::WPC - 1) / C::WPC;
     const uint64_t grid = std::min<uint64_t>(need, uint64_t(sm_count()) * occ);
     kern<<<unsigned(grid), C::WPC * 32, C::SMEM, s>>>(U, g, compact, tout);
 }
@@ -482,7 +485,7 @@ void launch_big(const T* U, const PosGeom& g, double* compact, double* tout, cud
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NW * 32, C::SMEM);
     if (occ < 1) occ = 1;
-    const uint64_t grid = std::min<uint64_t>(g.npos, std::max<uint64_t>(1, uint64_t(sm_count()) * occ / C::SPLIT));
+    const uint64_t grid = std::min<uint64_t>(g.p1 - g.p0, std::max<uint64_t>(1, uint64_t(sm_count()) * occ / C::SPLIT));
     kern<<<dim3(unsigned(grid), C::SPLIT), C::NW * 32, C::SMEM, s>>>(U, g, compact, tout);
 }
 
@@ -508,11 +511,23 @@ void launch_leaf(const T* U, const PosGeom& g, double* compact, double* tout, cu
             default: break;
         }
     }
-    const uint64_t grid = std::min<uint64_t>(g.npos, uint64_t(sm_count()) * 16);
+    const uint64_t grid = std::min<uint64_t>(g.p1 - g.p0, uint64_t(sm_count()) * 16);
     k_leaf_generic<T><<<unsigned(grid), 256, 0, s>>>(U, g, compact, tout);
 }
 
 }  // namespace
+
+uint64_t tree_positions(uint64_t I, uint32_t R) { return make_geom(I, R).npos; }
+
+void tree_partition_rows(uint64_t I, uint32_t R, uint32_t parts, uint32_t part, uint64_t* first, uint64_t* last) {
+    const PosGeom g = make_geom(I, R);
+    const uint64_t span = g.npos / parts;
+    uint64_t r0, rs, r1;
+    pos_rows(g, uint64_t(part) * span, r0, rs, r1);
+    *first = r0;
+    pos_rows(g, uint64_t(part + 1) * span - 1, r0, rs, r1);
+    *last = r1;
+}
 
 void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b) {
     const PosGeom g = make_geom(I, R);
@@ -521,7 +536,12 @@ void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b) {
 }
 
 int launch_tree_leaves(const TreeBuildArgs& a) {
-    const PosGeom g = make_geom(a.I, a.R);
+    PosGeom g = make_geom(a.I, a.R);
+    if (a.parts > 1) {  // one partition's subtree: positions [part, part+1) * npos / parts
+        const uint64_t span = g.npos / a.parts;
+        g.p0 = uint64_t(a.part) * span;
+        g.p1 = g.p0 + span;
+    }
     double* tout = g.npos > 1 ? a.tbuf_a : nullptr;
     if (a.storage == 1)
         launch_leaf<float>(static_cast<const float*>(a.U), g, a.compact, tout, a.stream, a.force_generic);
@@ -530,20 +550,60 @@ int launch_tree_leaves(const TreeBuildArgs& a) {
     return 1;
 }
 
+// Levels above the positions, bottom-up (:180-186). Whole tree: down to the
+// root. One partition (parts = 2^gl > 1): only the partition's own nodes on
+// levels D-1 .. gl, and its subtree root Gram (level gl) is copied to a.subroot.
 int launch_tree_levels(const TreeBuildArgs& a) {
     const PosGeom g = make_geom(a.I, a.R);
     uint32_t D = 0;
     while ((uint64_t{1} << D) < g.npos) ++D;
+    uint32_t gl = 0;
+    while ((1u << gl) < a.parts) ++gl;
     double* cur = a.tbuf_a;
     double* nxt = a.tbuf_b;
     int launches = 0;
-    for (int l = int(D) - 1; l >= 0; --l) {
+    for (int l = int(D) - 1; l >= int(gl); --l) {
         const uint64_t nj = uint64_t{1} << l;
-        double* parent = l > 0 ? nxt : nullptr;
-        const unsigned grid = unsigned(std::min<uint64_t>(nj, uint64_t(sm_count()) * 8));
-        k_level_reduce<<<grid, 256, 0, a.stream>>>(cur, parent, a.compact, nj, g.P, nj - 1);
+        const uint64_t span = nj >> gl;  // nodes of this level per partition
+        const uint64_t j0 = a.parts > 1 ? uint64_t(a.part) * span : 0;
+        const uint64_t j1 = a.parts > 1 ? j0 + span : nj;
+        double* parent = (l > 0) ? nxt : nullptr;
+        const unsigned grid = unsigned(std::min<uint64_t>(j1 - j0, uint64_t(sm_count()) * 8));
+        k_level_reduce<<<grid, 256, 0, a.stream>>>(cur, parent, a.compact, j0, j1, g.P, nj - 1);
         ++launches;
         std::swap(cur, nxt);
+    }
+    if (a.parts > 1 && a.subroot) {  // cur holds level gl
+        if (cudaMemcpyAsync(a.subroot, cur + uint64_t(a.part) * g.P, sizeof(double) * g.P,
+                            cudaMemcpyDeviceToDevice, a.stream) != cudaSuccess)
+            return -1;
+    }
+    return launches;
+}
+
+// Top of a partitioned build: the parts = 2^gl subtree roots (parts x P, in
+// subtree order) are level gl; stores the stored ones and reduces to the root.
+int launch_tree_top(const TreeBuildArgs& a, const double* subroots) {
+    const PosGeom g = make_geom(a.I, a.R);
+    uint32_t gl = 0;
+    while ((1u << gl) < a.parts) ++gl;
+    int launches = 0;
+    for (uint32_t i = 0; i < a.parts; i += 2) {  // even i = left children (odd heap ids) -> stored
+        const uint64_t v = (uint64_t{1} << gl) - 1 + i;
+        if (cudaMemcpyAsync(a.compact + slot_of(v) * g.P, subroots + uint64_t(i) * g.P,
+                            sizeof(double) * g.P, cudaMemcpyDeviceToDevice, a.stream) != cudaSuccess)
+            return -1;
+    }
+    const double* cur = subroots;
+    double* bufs[2] = {a.tbuf_a, a.tbuf_b};
+    int which = 0;
+    for (int l = int(gl) - 1; l >= 0; --l) {
+        const uint64_t nj = uint64_t{1} << l;
+        double* parent = l > 0 ? bufs[which] : nullptr;
+        k_level_reduce<<<unsigned(nj), 256, 0, a.stream>>>(cur, parent, a.compact, 0, nj, g.P, nj - 1);
+        ++launches;
+        cur = parent;
+        which ^= 1;
     }
     return launches;
 }

@@ -265,6 +265,25 @@ class KrpSampler:
     def rebuild(self, j: int) -> None:
         check(_lib.lib().krpg_rebuild(self._h, j))
 
+    # ---- row-partitioned construction (multi-GPU, see sharding.build_partitioned) ----
+    def tree_device(self, j: int):
+        """Zero-copy torch view (L*P doubles) of factor j's compact tree in HBM."""
+        import torch
+
+        from .sharding import _DeviceArray
+        ptr, slots = C.c_void_p(), C.c_uint64()
+        check(_lib.lib().krpg_tree_device(self._h, j, C.byref(ptr), C.byref(slots)))
+        P = self._R * (self._R + 1) // 2
+        return torch.as_tensor(_DeviceArray(ptr.value, slots.value * P), device="cuda")
+
+    def build_partition(self, j: int, parts: int, part: int, subroot) -> None:
+        """Stored nodes of subtree `part` of `parts`; subtree root Gram -> `subroot` (P doubles, CUDA)."""
+        check(_lib.lib().krpg_build_partition(self._h, j, parts, part, C.c_void_p(subroot.data_ptr())))
+
+    def finish_partitions(self, j: int, parts: int, subroots) -> None:
+        """Top levels from all subtree roots (parts x P doubles, CUDA, subtree order)."""
+        check(_lib.lib().krpg_finish_partitions(self._h, j, parts, C.c_void_p(subroots.data_ptr())))
+
     def profile_enable(self, on: bool = True, detail: bool = False) -> None:
         check(_lib.lib().krpg_profile_enable(self._h, 1 if on else 0))
         check(_lib.lib().krpg_set_option(self._h, _lib.OPT_PROFILE_DETAIL, 1 if detail else 0))

@@ -414,3 +414,36 @@ def test_large_factor_properties(R):
     Gp = np.linalg.pinv(G, hermitian=True)
     q = np.einsum("dr,rs,ds->d", b.rows, Gp, b.rows) / R
     assert rel_err_vec(b.probabilities, q) <= 1e-8
+
+
+# ------------------------------------------------ partitioned construction (8(e))
+@pytest.mark.parametrize("shape,storage", [((4096, 16), "f64"), ((777, 24), "f64"), ((3001, 64), "f64"),
+                                           ((2049, 56), "f32"), ((5000, 128), "f64"), ((2600, 256), "f64")])
+def test_partitioned_build_bit_identical_to_single_build(shape, storage):
+    """Each subtree built on its own (krpg_build_partition, as one rank would) and
+    the top levels reduced from the subtree roots (krpg_finish_partitions) give
+    the single-process tree bit for bit. Ranks run one after another on this
+    one GPU (no inter-kernel waiting); the exchange itself is the gloo test."""
+    import torch
+    from paper_2301_12584_b200.sharding import tree_geometry
+    I, R = shape
+    fs = pareto_factors([shape, (50, R)], seed=I + R)
+    s = K()(fs, storage=storage)
+    full = s.tree_grams(0).copy()
+    G0 = s.factor_gram(0).copy()
+    P = R * (R + 1) // 2
+    npos = tree_geometry(I, R)["npos"]
+    parts = 2
+    while parts <= min(npos, 8):
+        s.tree_device(0).fill_(float("nan"))
+        roots = torch.empty(parts, P, dtype=torch.float64, device="cuda")
+        for part in range(parts):
+            s.build_partition(0, parts, part, roots[part])
+        s.finish_partitions(0, parts, roots.view(-1))
+        assert np.array_equal(s.tree_grams(0), full), parts
+        assert np.array_equal(s.factor_gram(0), G0)
+        parts *= 2
+    b = s.sample(None, 2000, 5, margin=True)
+    o = oracle.OracleKrp([f.astype(np.float32).astype(np.float64) if storage == "f32" else f for f in fs], "port")
+    ri, rp, rr, rm = o.sample(None, 2000, 5, want_margin=True)
+    assert_draws_match(b, ri, rp, rr, rm)
