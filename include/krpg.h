@@ -167,6 +167,26 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
 #define KRPG_OPT_ASYNC 4
 int krpg_set_option(krpg_t h, int option, int64_t value);
 
+/* ---- STS-CP solve slice ----
+ * A device-resident sparse tensor: SparseTensorCoo::from_entries (tensor.cpp:34-75)
+ * semantics -- coordinates validated, duplicates summed, entries sorted
+ * lexicographically; fiber indexes (SparseTensorCoo::fiber_index, tensor.cpp:104-129)
+ * are built on the device on first use. Requires prod(dims) <= 2^64, nnz < 2^32, N <= 8. */
+typedef struct krpg_tensor* krpg_tensor_t;
+int krpg_tensor_create(const uint64_t* dims, uint32_t N, const uint32_t* coords, const double* values,
+                       uint64_t nnz, int device, krpg_tensor_t* out);
+int krpg_tensor_destroy(krpg_tensor_t t);
+int krpg_tensor_info(krpg_tensor_t t, uint64_t* nnz, double* norm_sq);
+/* deduplicated, sorted entries (host): coords nnz x N, values nnz (each nullable) */
+int krpg_tensor_entries(krpg_tensor_t t, uint32_t* coords, double* values);
+/* One STS-CP factor update of mode j, the StsCp branch of cp_als.cpp:279-313:
+ * batch = sample(j, J, seed); w = 1/sqrt(J q) (make_sampling_weights, sketch.cpp:36-52);
+ * SA = w o rows; SB = w o sampled_rhs_rows(T, j, batch) (cp_als.cpp:122-145, formed as a
+ * sparse scatter, never the dense J x I_j block); U_j = (pinv_psd(gram(SA)) gram_cross(SA, SB))^T;
+ * normalize_columns (cp_als.cpp:39-52) -> sigma (R, host, nullable); update_factor(j, U_j).
+ * The factor of the handle is replaced and its tree rebuilt on the device. */
+int krpg_sts_solve(krpg_t h, krpg_tensor_t T, uint32_t j, uint64_t J, uint64_t seed, double* sigma);
+
 /* ---- row-partitioned construction (multi-GPU) ----
  * The tree over I rows splits into parts = 2^g subtrees (the nodes of level g);
  * subtree `part` covers the contiguous rows krpg_partition_rows(...). A rank that

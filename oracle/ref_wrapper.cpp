@@ -13,6 +13,10 @@
 //   materialize_krp / leverage_scores              reference/reference.hpp:28-32
 //   CounterRng                                     rng.hpp:13-48
 //   make_sampling_weights                          sketch.hpp:37-39
+//   SparseTensorCoo::from_entries, sampled_rhs_rows,
+//   gram / gram_cross / pinv_psd / matmul          tensor.hpp:23, cp_als.hpp:52, dense_kernels.hpp
+//   (one STS-CP factor update, the StsCp branch of cp_als.cpp:279-313)
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -21,11 +25,13 @@
 #include <string>
 #include <vector>
 
+#include "krplev/cp_als.hpp"
 #include "krplev/dense_kernels.hpp"
 #include "krplev/krp_sampler.hpp"
 #include "krplev/rng.hpp"
 #include "krplev/segment_tree_sampler.hpp"
 #include "krplev/sketch.hpp"
+#include "krplev/tensor.hpp"
 #include "reference.hpp"
 
 using namespace krplev;  // == krplev_ref via -D
@@ -293,6 +299,62 @@ int kref_sampling_weights(const double* prob, uint64_t n, uint64_t J, double* w)
         std::vector<uint64_t> ids(n, 0);
         RowSampleWeights rw = make_sampling_weights(ids, std::span<const double>(prob, n), J);
         std::memcpy(w, rw.weights.data(), sizeof(double) * n);
+    });
+}
+
+// Deduplicated, sorted entries of SparseTensorCoo::from_entries (tensor.cpp:34-75).
+// Call with coords_out == nullptr to get the count.
+int kref_tensor_entries(const uint64_t* dims, uint32_t N, const uint32_t* coords, const double* values, uint64_t nnz,
+                        uint32_t* coords_out, double* values_out, uint64_t* nnz_out) {
+    return guard([&] {
+        SparseTensorCoo T = SparseTensorCoo::from_entries(std::vector<uint64_t>(dims, dims + N),
+                                                          std::vector<uint32_t>(coords, coords + nnz * N),
+                                                          std::vector<double>(values, values + nnz));
+        *nnz_out = T.nnz();
+        if (coords_out)
+            for (std::size_t e = 0; e < T.nnz(); ++e)
+                for (uint32_t k = 0; k < N; ++k) coords_out[e * N + k] = T.coords(e)[k];
+        if (values_out) std::memcpy(values_out, T.values().data(), sizeof(double) * T.nnz());
+    });
+}
+
+// One STS-CP factor update of mode j (cp_als.cpp:279-313, solver StsCp) through the
+// reference's public functions; the column renormalisation of cp_als.cpp:39-52 is
+// internal to that file and is restated here (norms into sigma, zero column ->
+// unit basis vector c % I).
+int kref_sts_step(const double* const* factors, const uint64_t* I, uint32_t N, uint32_t R, const uint32_t* coords,
+                  const double* values, uint64_t nnz, uint32_t j, uint64_t J, uint64_t seed, double* unew,
+                  double* sigma) {
+    return guard([&] {
+        std::vector<Matrix> fs;
+        std::vector<uint64_t> dims(I, I + N);
+        for (uint32_t k = 0; k < N; ++k) fs.push_back(to_matrix(factors[k], I[k], R));
+        KrpSampler sampler(fs);
+        SparseTensorCoo T = SparseTensorCoo::from_entries(dims, std::vector<uint32_t>(coords, coords + nnz * N),
+                                                          std::vector<double>(values, values + nnz));
+        SampleBatch batch = sampler.sample(j, J, seed);
+        const RowSampleWeights w =
+            make_sampling_weights(batch.flat_indices(RowOrder::Reversed), batch.probabilities, batch.count);
+        Matrix sa = std::move(batch.rows);
+        for (std::size_t d = 0; d < sa.rows; ++d)
+            for (std::size_t c = 0; c < R; ++c) sa(d, c) *= w.weights[d];
+        Matrix sb = sampled_rhs_rows(T, j, batch);
+        for (std::size_t d = 0; d < sb.rows; ++d)
+            for (std::size_t c = 0; c < sb.cols; ++c) sb(d, c) *= w.weights[d];
+        const Matrix gs = gram(sa);
+        Matrix u = transpose(matmul(pinv_psd(gs), gram_cross(sa, sb)));
+        for (std::size_t c = 0; c < u.cols; ++c) {
+            double nrm = 0.0;
+            for (std::size_t i = 0; i < u.rows; ++i) nrm += u(i, c) * u(i, c);
+            nrm = std::sqrt(nrm);
+            sigma[c] = nrm;
+            if (nrm > 0.0) {
+                for (std::size_t i = 0; i < u.rows; ++i) u(i, c) /= nrm;
+            } else {
+                u(c % u.rows, c) = 1.0;
+            }
+        }
+        std::memcpy(unew, u.data.data(), sizeof(double) * u.rows * u.cols);
     });
 }
 

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <future>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -112,6 +113,54 @@ struct Factor {
 };
 
 }  // namespace
+
+// Device-resident sparse tensor (SparseTensorCoo, tensor.hpp:18-70): deduplicated,
+// lexicographically sorted COO + per-mode fiber indexes built on first use.
+struct krpg_tensor {
+    int device = 0;
+    uint32_t N = 0;
+    std::vector<uint64_t> dims;
+    uint64_t nnz = 0;
+    double norm_sq = 0.0;
+    DevBuf coords, values;
+    struct Fiber {
+        bool built = false;
+        uint64_t G = 0;
+        DevBuf keys, ptr, fcoord, fval;
+    };
+    std::vector<Fiber> fib;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+
+    const Fiber& fiber(uint32_t j) {
+        Fiber& F = fib[j];
+        if (!F.built) {
+            uint64_t* k = nullptr;
+            uint64_t* p = nullptr;
+            uint32_t* c = nullptr;
+            double* v = nullptr;
+            F.G = krpg::fiber_index_build(coords.as<uint32_t>(), values.as<double>(), nnz, N, dims.data(), j, &k,
+                                          &p, &c, &v, stream);
+            F.keys.p = k;
+            F.ptr.p = p;
+            F.fcoord.p = c;
+            F.fval.p = v;
+            F.built = true;
+        }
+        return F;
+    }
+    ~krpg_tensor() {
+        coords.release();
+        values.release();
+        for (Fiber& F : fib) {
+            F.keys.release();
+            F.ptr.release();
+            F.fcoord.release();
+            F.fval.release();
+        }
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
 
 struct krpg_sampler {
     int device = 0;
@@ -224,6 +273,9 @@ struct krpg_sampler {
         F.G.assign(size_t(R) * R, 0.0);
         krpg::unpack_upper(root.data(), R, F.G.data());
     }
+
+    // ---- STS-CP factor update (cp_als.cpp:282-313, solver StsCp) ----
+    void sts_solve(krpg_tensor& T, uint32_t j, uint64_t J, uint64_t seed, double* sigma_out);
 
     // ---- row-partitioned construction ----
     krpg::TreeBuildArgs tree_args(uint32_t k) {
@@ -548,9 +600,147 @@ struct krpg_sampler {
     }
 };
 
+void krpg_sampler::sts_solve(krpg_tensor& T, uint32_t j, uint64_t J, uint64_t seed, double* sigma_out) {
+    require(T.N == N, "sts_solve: tensor order differs from the factor count");
+    for (uint32_t k = 0; k < N; ++k) require(T.dims[k] == f[k].I, "sts_solve: tensor dims differ from the factors");
+    require(T.device == device, "sts_solve: tensor and sampler on different devices");
+    const uint64_t Ij = f[j].I;
+    // 1) sampler->sample(j, J, seed) (:279-282)
+    uint32_t* di = static_cast<uint32_t*>(sIdx.ensure(4 * J * N));
+    double* dp = static_cast<double*>(sProb.ensure(8 * J));
+    double* dr = static_cast<double*>(sH.ensure(8 * J * R));
+    sample_device(int64_t(j), J, seed, 0, KRPG_MODE_TWO_STAGE, di, dp, dr, nullptr);
+    sync_check();  // an asynchronous-mode sample reports its error here
+    // 2) weights + SA = w o rows (:283-287, make_sampling_weights sketch.cpp:36-52); gram(sa)
+    char* base = static_cast<char*>(rowbuf.ensure(8 * (J * R + J + R * R + R * R + R) + 8 * Ij * R * 2 + 1024));
+    double* sa = reinterpret_cast<double*>(base);
+    double* w = sa + J * R;
+    double* gs = w + J;
+    double* pinv = gs + size_t(R) * R;
+    double* nrm = pinv + size_t(R) * R;
+    double* M = nrm + R;
+    double* Unew = M + Ij * R;
+    int* derr = static_cast<int*>(err.ensure(sizeof(int)));
+    CK(cudaMemsetAsync(derr, 0, sizeof(int), stream));
+    krpg::launch_gather_sa(dp, dr, J, R, w, sa, derr, stream);
+    CK(cudaMemsetAsync(gs, 0, 8 * size_t(R) * R, stream));
+    krpg::launch_full_gram(sa, KRPG_STORE_F64, J, R, gs, stream);
+    // 3) sampled_rhs_rows + gram_cross(sa, sb), as a sparse scatter into M = (SA^T SB)^T
+    CK(cudaStreamSynchronize(T.stream));
+    const krpg_tensor::Fiber& F = T.fiber(j);
+    CK(cudaMemsetAsync(M, 0, 8 * Ij * R, stream));
+    krpg::launch_sampled_rhs(di, J, N, j, T.dims.data(), dp, dr, R, F.keys.as<uint64_t>(), F.G,
+                             F.ptr.as<uint64_t>(), F.fcoord.as<uint32_t>(), F.fval.as<double>(), M, derr, stream);
+    // 4) pinv_psd(gram(sa)) on the host (dense_kernels.cpp:207)
+    std::vector<double> gh(size_t(R) * R);
+    int eh = 0;
+    CK(cudaMemcpyAsync(gh.data(), gs, 8 * gh.size(), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(&eh, derr, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (eh) throw std::invalid_argument("make_sampling_weights: sampled index has zero probability");
+    for (double x : gh) require(std::isfinite(x), "gram: non-finite entries");
+    const std::vector<double> ph = krpg::pinv_from_eigen(krpg::eigh_psd(gh.data(), R));
+    CK(cudaMemcpyAsync(pinv, ph.data(), 8 * ph.size(), cudaMemcpyHostToDevice, stream));
+    // 5) unew = transpose(matmul(pinv, gram_cross)) ; normalize_columns (:295, :309)
+    krpg::launch_solve_rows(M, Ij, R, pinv, Unew, stream);
+    krpg::launch_normalize_columns(Unew, Ij, R, nrm, stream);
+    std::vector<double> sg(R);
+    CK(cudaMemcpyAsync(sg.data(), nrm, 8 * R, cudaMemcpyDeviceToHost, stream));
+    // 6) sampler->update_factor(j, unew) (:312-313): device copy in the storage type + rebuild
+    Factor& Fj = f[j];
+    if (storage == KRPG_STORE_F32)
+        krpg::launch_convert_f64_to_f32(Unew, Fj.U.as<float>(), Ij * R, stream);
+    else
+        CK(cudaMemcpyAsync(Fj.U.p, Unew, 8 * Ij * R, cudaMemcpyDeviceToDevice, stream));
+    build_tree(j);
+    if (sigma_out) std::copy(sg.begin(), sg.end(), sigma_out);
+}
+
 extern "C" {
 
 const char* krpg_last_error(void) { return g_err.c_str(); }
+
+int krpg_tensor_create(const uint64_t* dims, uint32_t N, const uint32_t* coords, const double* values, uint64_t nnz,
+                       int device, krpg_tensor_t* out) {
+    return guard([&] {
+        *out = nullptr;
+        require(N >= 1, "SparseTensorCoo: no dimensions");
+        require(N <= 8, "krpg_tensor_create: at most 8 modes on device");
+        for (uint32_t k = 0; k < N; ++k) require(dims[k] >= 1, "SparseTensorCoo: empty mode");
+        for (uint64_t e = 0; e < nnz; ++e)
+            for (uint32_t k = 0; k < N; ++k)
+                require(coords[e * N + k] < dims[k], "SparseTensorCoo: coordinate out of range");
+        unsigned __int128 prod = 1;
+        for (uint32_t k = 0; k < N; ++k) prod *= dims[k];
+        require(prod <= (unsigned __int128)(~uint64_t{0}), "krpg_tensor_create: tensor index space exceeds 2^64");
+        require(nnz < (uint64_t{1} << 32), "krpg_tensor_create: more than 2^32 entries");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, "krpg: no such CUDA device");
+        auto t = std::make_unique<krpg_tensor>();
+        t->device = device;
+        t->N = N;
+        t->dims.assign(dims, dims + N);
+        t->fib.resize(N);
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+        if (nnz) {
+            DevBuf c_in, v_in;
+            CK(cudaMemcpyAsync(c_in.ensure(4 * nnz * N), coords, 4 * nnz * N, cudaMemcpyHostToDevice, t->stream));
+            CK(cudaMemcpyAsync(v_in.ensure(8 * nnz), values, 8 * nnz, cudaMemcpyHostToDevice, t->stream));
+            uint32_t* co = nullptr;
+            double* vo = nullptr;
+            t->nnz = krpg::tensor_ingest(c_in.as<uint32_t>(), v_in.as<double>(), nnz, N, dims, &co, &vo, t->stream);
+            t->coords.p = co;
+            t->values.p = vo;
+            c_in.release();
+            v_in.release();
+            std::vector<double> vh(t->nnz);
+            CK(cudaMemcpy(vh.data(), vo, 8 * t->nnz, cudaMemcpyDeviceToHost));
+            double sq = 0.0;
+            for (double x : vh) sq += x * x;
+            t->norm_sq = sq;
+        }
+        *out = t.release();
+    });
+}
+
+int krpg_tensor_destroy(krpg_tensor_t t) {
+    return guard([&] {
+        if (!t) return;
+        cudaSetDevice(t->device);
+        delete t;
+    });
+}
+
+int krpg_tensor_info(krpg_tensor_t t, uint64_t* nnz, double* norm_sq) {
+    return guard([&] {
+        require(t, "krpg: null tensor");
+        if (nnz) *nnz = t->nnz;
+        if (norm_sq) *norm_sq = t->norm_sq;
+    });
+}
+
+int krpg_tensor_entries(krpg_tensor_t t, uint32_t* coords, double* values) {
+    return guard([&] {
+        require(t, "krpg: null tensor");
+        CK(cudaSetDevice(t->device));
+        if (coords && t->nnz) CK(cudaMemcpy(coords, t->coords.p, 4 * t->nnz * t->N, cudaMemcpyDeviceToHost));
+        if (values && t->nnz) CK(cudaMemcpy(values, t->values.p, 8 * t->nnz, cudaMemcpyDeviceToHost));
+    });
+}
+
+int krpg_sts_solve(krpg_t h, krpg_tensor_t T, uint32_t j, uint64_t J, uint64_t seed, double* sigma) {
+    return guard([&] {
+        require(h && T, "krpg: null handle");
+        require(j < h->N, "sts_solve: mode out of range");
+        require(J >= 1, "KrpSample: sample count must be positive");
+        std::lock_guard<std::mutex> lk(h->mu);
+        std::lock_guard<std::mutex> lt(T->mu);
+        h->set_device();
+        h->sts_solve(*T, j, J, seed, sigma);
+    });
+}
 
 int krpg_device_count(void) {
     int n = 0;

@@ -120,4 +120,22 @@ void launch_convert_f32_to_f64(const float* in, double* out, uint64_t n, cudaStr
 void launch_full_gram(const void* U, uint32_t storage, uint64_t I, uint32_t R, double* out,
                       cudaStream_t s);
 
+// ---- STS-CP solve slice (sts.cu; cp_als.cpp:282-313) ----
+// dedup + lexicographic sort of COO entries (tensor.cpp:34-75); returns nnz after
+// dedup, *_out allocated with cudaMalloc (caller frees)
+uint64_t tensor_ingest(const uint32_t* d_coords, const double* d_vals, uint64_t nnz, uint32_t N, const uint64_t* dims,
+                       uint32_t** d_coords_out, double** d_vals_out, cudaStream_t s);
+// fiber index of mode j (tensor.cpp:104-129); returns #fibers G; outputs cudaMalloc'ed
+uint64_t fiber_index_build(const uint32_t* d_coords, const double* d_vals, uint64_t nnz, uint32_t N,
+                           const uint64_t* dims, uint32_t j, uint64_t** d_keys, uint64_t** d_ptr,
+                           uint32_t** d_fcoord, double** d_fval, cudaStream_t s);
+// M (I_j x R, zeroed by the caller) += scatter of the sampled fibers (gram_cross(sa, sb)^T)
+void launch_sampled_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, const uint64_t* dims,
+                        const double* prob, const double* rows, uint32_t R, const uint64_t* keys, uint64_t G,
+                        const uint64_t* ptr, const uint32_t* fcoord, const double* fval, double* M, int* err,
+                        cudaStream_t s);
+void launch_solve_rows(const double* M, uint64_t I, uint32_t R, const double* pinv, double* U, cudaStream_t s);
+// column norms -> nrm (R), columns scaled to unit norm (cp_als.cpp:39-52)
+void launch_normalize_columns(double* U, uint64_t I, uint32_t R, double* nrm, cudaStream_t s);
+
 }  // namespace krpg

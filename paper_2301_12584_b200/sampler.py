@@ -265,6 +265,14 @@ class KrpSampler:
     def rebuild(self, j: int) -> None:
         check(_lib.lib().krpg_rebuild(self._h, j))
 
+    def sts_solve(self, T, j: int, J: int, seed: int) -> np.ndarray:
+        """One STS-CP factor update of mode j against the sparse tensor T (cp_als.cpp:279-313,
+        solver StsCp): factor j is replaced by the normalised solve and its tree rebuilt;
+        returns the column norms sigma (normalize_columns, cp_als.cpp:39-52)."""
+        sigma = np.empty(self._R)
+        check(_lib.lib().krpg_sts_solve(self._h, T._h, j, J, seed, sigma.ctypes.data_as(C.POINTER(C.c_double))))
+        return sigma
+
     # ---- row-partitioned construction (multi-GPU, see sharding.build_partitioned) ----
     def tree_device(self, j: int):
         """Zero-copy torch view (L*P doubles) of factor j's compact tree in HBM."""

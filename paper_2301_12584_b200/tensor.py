@@ -1,0 +1,69 @@
+"""Device-resident sparse tensor for the STS-CP solve slice.
+
+Mirrors the reference's SparseTensorCoo (tensor.hpp:18-70): ``from_entries``
+validates coordinates, sums duplicates and sorts entries lexicographically --
+here on the device (krpg_tensor_create). ``KrpSampler.sts_solve`` then runs one
+STS-CP factor update (the StsCp branch of cp_als.cpp:279-313) against it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+
+
+class SparseTensor:
+    def __init__(self, dims: Sequence[int], coords, values, device: int = 0):
+        self.dims = [int(d) for d in dims]
+        N = len(self.dims)
+        coords = np.ascontiguousarray(np.asarray(coords, dtype=np.uint32).reshape(-1, N))
+        values = np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(-1))
+        if coords.shape[0] != values.shape[0]:
+            from ._lib import KrpgInvalidArgument
+            raise KrpgInvalidArgument("SparseTensorCoo: coords/values mismatch")
+        self._h = C.c_void_p()
+        dims_c = (C.c_uint64 * N)(*self.dims)
+        check(_lib.lib().krpg_tensor_create(dims_c, N, coords.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                            values.ctypes.data_as(C.POINTER(C.c_double)), values.shape[0],
+                                            device, C.byref(self._h)))
+
+    @classmethod
+    def from_entries(cls, dims, coords, values, device: int = 0) -> "SparseTensor":
+        return cls(dims, coords, values, device)
+
+    def ndim(self) -> int:
+        return len(self.dims)
+
+    def nnz(self) -> int:
+        n = C.c_uint64()
+        check(_lib.lib().krpg_tensor_info(self._h, C.byref(n), None))
+        return int(n.value)
+
+    def norm_squared(self) -> float:
+        x = C.c_double()
+        check(_lib.lib().krpg_tensor_info(self._h, None, C.byref(x)))
+        return float(x.value)
+
+    def entries(self):
+        """(coords nnz x N, values nnz): deduplicated, lexicographically sorted."""
+        n = self.nnz()
+        c = np.empty((n, self.ndim()), dtype=np.uint32)
+        v = np.empty(n)
+        check(_lib.lib().krpg_tensor_entries(self._h, c.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                             v.ctypes.data_as(C.POINTER(C.c_double))))
+        return c, v
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.lib().krpg_tensor_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

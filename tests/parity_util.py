@@ -96,3 +96,19 @@ def digest(arrays) -> str:
     for a in arrays:
         h.update(np.ascontiguousarray(a).tobytes())
     return h.hexdigest()
+
+
+def sparse_tensor(dims, nnz, seed, s=1.1):
+    """Synthetic COO in the config-5 style: per-mode Zipf(s)-skewed
+    coordinates (so fibers repeat and duplicates occur), lognormal(0,1) values.
+    Raw entries, duplicates not yet summed."""
+    rng = np.random.default_rng(seed)
+    coords = np.empty((nnz, len(dims)), dtype=np.uint32)
+    for k, d in enumerate(dims):
+        ranks = np.arange(1, d + 1, dtype=float)
+        p = ranks ** (-s)
+        p /= p.sum()
+        perm = rng.permutation(d)  # popular indices scattered over the mode
+        coords[:, k] = perm[rng.choice(d, size=nnz, p=p)]
+    values = rng.lognormal(0.0, 1.0, size=nnz)
+    return coords, values

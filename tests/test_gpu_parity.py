@@ -447,3 +447,56 @@ def test_partitioned_build_bit_identical_to_single_build(shape, storage):
     o = oracle.OracleKrp([f.astype(np.float32).astype(np.float64) if storage == "f32" else f for f in fs], "port")
     ri, rp, rr, rm = o.sample(None, 2000, 5, want_margin=True)
     assert_draws_match(b, ri, rp, rr, rm)
+
+
+# ------------------------------------------------ STS-CP solve slice (8(f) rank 1)
+def test_sparse_tensor_ingestion_matches_from_entries():
+    """Device dedup + lexicographic sort vs SparseTensorCoo::from_entries (tensor.cpp:34-75)."""
+    from oracle import sts_cp
+    from paper_2301_12584_b200 import SparseTensor
+    from parity_util import sparse_tensor
+    dims = (300, 200, 150)
+    coords, values = sparse_tensor(dims, 20000, seed=4)
+    T = SparseTensor(dims, coords, values)
+    oc, ov = sts_cp.from_entries(dims, coords, values)
+    c, v = T.entries()
+    assert np.array_equal(c, oc)
+    assert np.allclose(v, ov, rtol=1e-14, atol=0)
+    assert T.nnz() == len(ov) < len(values)
+    assert abs(T.norm_squared() - float(np.sum(ov * ov))) <= 1e-12 * float(np.sum(ov * ov))
+
+
+@pytest.mark.parametrize("dims,R,storage", [((300, 200, 150), 16, "f64"), ((120, 90, 70, 40), 8, "f64"),
+                                            ((500, 400, 300), 64, "f32")])
+def test_sts_solve_matches_restatement(dims, R, storage):
+    """krpg_sts_solve vs the restatement (pinned bit-for-bit to the reference's StsCp
+    step, tests/test_sts_oracle.py) on the same batch; fp64 tolerance 1e-9 relative
+    (device sums run in other orders: fp64 atomics, blocked Gram, another eigensolver).
+    Afterwards the rebuilt tree samples the new factor exactly."""
+    from oracle import sts_cp
+    from paper_2301_12584_b200 import SparseTensor
+    from parity_util import sparse_tensor
+    coords, values = sparse_tensor(dims, 30000, seed=len(dims) + R)
+    fs = pareto_factors([(d, R) for d in dims], seed=R)
+    s = K()(fs, storage=storage)
+    T = SparseTensor(dims, coords, values)
+    oc, ov = T.entries()
+    port = oracle.backend("port")
+    J, seed = 4096, 31
+    for j in range(len(dims)):
+        b = s.sample(j, J, seed)  # the batch sts_solve draws internally
+        U_ref, sg_ref = sts_cp.sts_step(dims, oc, ov, j, b.indices, b.probabilities, b.rows,
+                                        lambda G: port.pinv(G)[0])
+        sg = s.sts_solve(T, j, J, seed)
+        assert np.max(np.abs(sg - sg_ref) / sg_ref) <= 1e-9
+        U = s.factor(j)
+        if storage == "f32":
+            assert np.max(np.abs(U - U_ref)) <= 1e-6 * np.max(np.abs(U_ref))
+        else:
+            assert np.max(np.abs(U - U_ref)) <= 1e-9 * np.max(np.abs(U_ref))
+        fs[j] = U
+    s.validate()
+    o = oracle.OracleKrp(fs, "port")
+    bb = s.sample(None, 3000, 7, margin=True)
+    ri, rp, rr, rm = o.sample(None, 3000, 7, want_margin=True)
+    assert_draws_match(bb, ri, rp, rr, rm)
