@@ -137,6 +137,7 @@ int krpg_last_build_ms(krpg_t h, float* ms);
 #define KRPG_PROF_PROB 4        /* probability epilogue                  */
 #define KRPG_PROF_UPDATE 5      /* incremental updates                   */
 #define KRPG_PROF_OTHER 6       /* fills, gathers, conversions           */
+#define KRPG_PROF_STS 7         /* STS-CP solve: weights, Grams, fiber scatter, row solve, normalise */
 /* finer split of KRPG_PROF_DRAWS for the grouped descent (only timed when
  * KRPG_OPT_PROFILE_DETAIL is set; their launches are counted under DRAWS) */
 #define KRPG_PROF_D_ROOT 8       /* normaliser passes (root of E / Z trees) */
@@ -145,6 +146,7 @@ int krpg_last_build_ms(krpg_t h, float* ms);
 #define KRPG_PROF_D_REGROUP 11   /* child-run scatter                      */
 #define KRPG_PROF_D_LEAF 12      /* leaf scan + h update                   */
 #define KRPG_PROF_D_MISC 13      /* stage init, z formation                */
+#define KRPG_PROF_STS_SCATTER 14 /* STS-CP: fiber lookup + scatter of the sampled right-hand side */
 #define KRPG_PROF_N 16
 int krpg_profile_enable(krpg_t h, int on);
 /* ms and launches: arrays of KRPG_PROF_N (nullable); reset != 0 zeroes them */
@@ -186,6 +188,9 @@ int krpg_tensor_entries(krpg_tensor_t t, uint32_t* coords, double* values);
  * normalize_columns (cp_als.cpp:39-52) -> sigma (R, host, nullable); update_factor(j, U_j).
  * The factor of the handle is replaced and its tree rebuilt on the device. */
 int krpg_sts_solve(krpg_t h, krpg_tensor_t T, uint32_t j, uint64_t J, uint64_t seed, double* sigma);
+/* statistics of the last krpg_sts_solve (3 values): draws whose fiber holds a nonzero,
+ * distinct sampled fibers, tensor entries visited by the scatter */
+int krpg_sts_last_stats(krpg_t h, uint64_t* stats);
 
 /* ---- row-partitioned construction (multi-GPU) ----
  * The tree over I rows splits into parts = 2^g subtrees (the nodes of level g);

@@ -91,11 +91,12 @@ _SIGS = {
     "krpg_tensor_info": ([_vp, C.POINTER(_u64), C.POINTER(C.c_double)], _int),
     "krpg_tensor_entries": ([_vp, C.POINTER(_u32), _dp], _int),
     "krpg_sts_solve": ([_vp, _vp, _u32, _u64, _u64, _dp], _int),
+    "krpg_sts_last_stats": ([_vp, C.POINTER(_u64)], _int),
 }
 OPT_GROUPED_DESCENT = 1
 
-PROF_NAMES = ["tree_leaf", "tree_levels", "etree", "draws", "prob", "update", "other", "spare",
-              "d_root", "d_level_cta", "d_level_warp", "d_regroup", "d_leaf", "d_misc", "spare2", "spare3"]
+PROF_NAMES = ["tree_leaf", "tree_levels", "etree", "draws", "prob", "update", "other", "sts",
+              "d_root", "d_level_cta", "d_level_warp", "d_regroup", "d_leaf", "d_misc", "sts_scatter", "spare3"]
 OPT_PROFILE_DETAIL = 2
 OPT_FUSED_DEEP = 3
 OPT_ASYNC = 4

@@ -123,41 +123,23 @@ struct krpg_tensor {
     uint64_t nnz = 0;
     double norm_sq = 0.0;
     DevBuf coords, values;
-    struct Fiber {
-        bool built = false;
-        uint64_t G = 0;
-        DevBuf keys, ptr, fcoord, fval;
-    };
-    std::vector<Fiber> fib;
+    std::vector<krpg::FiberIndexDev> fib;
+    std::vector<bool> fib_built;
     cudaStream_t stream = nullptr;
     std::mutex mu;
 
-    const Fiber& fiber(uint32_t j) {
-        Fiber& F = fib[j];
-        if (!F.built) {
-            uint64_t* k = nullptr;
-            uint64_t* p = nullptr;
-            uint32_t* c = nullptr;
-            double* v = nullptr;
-            F.G = krpg::fiber_index_build(coords.as<uint32_t>(), values.as<double>(), nnz, N, dims.data(), j, &k,
-                                          &p, &c, &v, stream);
-            F.keys.p = k;
-            F.ptr.p = p;
-            F.fcoord.p = c;
-            F.fval.p = v;
-            F.built = true;
+    const krpg::FiberIndexDev& fiber(uint32_t j) {
+        if (!fib_built[j]) {
+            krpg::fiber_index_build(coords.as<uint32_t>(), values.as<double>(), nnz, N, dims.data(), j, &fib[j],
+                                    stream);
+            fib_built[j] = true;
         }
-        return F;
+        return fib[j];
     }
     ~krpg_tensor() {
         coords.release();
         values.release();
-        for (Fiber& F : fib) {
-            F.keys.release();
-            F.ptr.release();
-            F.fcoord.release();
-            F.fval.release();
-        }
+        for (krpg::FiberIndexDev& F : fib) krpg::fiber_index_free(F);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -171,7 +153,8 @@ struct krpg_sampler {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_build_ms = 0.f;
     std::mutex mu;
-    DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf, gstate, zbuf;
+    DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf, gstate, zbuf, stswork;
+    uint64_t sts_stats[4] = {0, 0, 0, 0};  // last STS step: draws hitting a nonzero fiber, fibers, entries
     PinBuf up[2], errh;       // operand staging is double-buffered (async calls)
     cudaEvent_t up_ev[2] = {nullptr, nullptr};
     unsigned call_no = 0;
@@ -612,7 +595,7 @@ void krpg_sampler::sts_solve(krpg_tensor& T, uint32_t j, uint64_t J, uint64_t se
     sample_device(int64_t(j), J, seed, 0, KRPG_MODE_TWO_STAGE, di, dp, dr, nullptr);
     sync_check();  // an asynchronous-mode sample reports its error here
     // 2) weights + SA = w o rows (:283-287, make_sampling_weights sketch.cpp:36-52); gram(sa)
-    char* base = static_cast<char*>(rowbuf.ensure(8 * (J * R + J + R * R + R * R + R) + 8 * Ij * R * 2 + 1024));
+    char* base = static_cast<char*>(rowbuf.ensure(8 * (J * R + J + 2 * size_t(R) * R + R + 2 * Ij * R) + 1024));
     double* sa = reinterpret_cast<double*>(base);
     double* w = sa + J * R;
     double* gs = w + J;
@@ -620,38 +603,39 @@ void krpg_sampler::sts_solve(krpg_tensor& T, uint32_t j, uint64_t J, uint64_t se
     double* nrm = pinv + size_t(R) * R;
     double* M = nrm + R;
     double* Unew = M + Ij * R;
+    void* work = stswork.ensure(krpg::sts_work_bytes(J, R));
     int* derr = static_cast<int*>(err.ensure(sizeof(int)));
     CK(cudaMemsetAsync(derr, 0, sizeof(int), stream));
+    cudaEvent_t t_sts = pbegin();
     krpg::launch_gather_sa(dp, dr, J, R, w, sa, derr, stream);
     CK(cudaMemsetAsync(gs, 0, 8 * size_t(R) * R, stream));
     krpg::launch_full_gram(sa, KRPG_STORE_F64, J, R, gs, stream);
-    // 3) sampled_rhs_rows + gram_cross(sa, sb), as a sparse scatter into M = (SA^T SB)^T
+    pend(KRPG_PROF_STS, t_sts, 3);
+    // 3) sampled_rhs_rows + gram_cross(sa, sb), sparse (overlaps the host pinv below)
     CK(cudaStreamSynchronize(T.stream));
-    const krpg_tensor::Fiber& F = T.fiber(j);
-    CK(cudaMemsetAsync(M, 0, 8 * Ij * R, stream));
-    krpg::launch_sampled_rhs(di, J, N, j, T.dims.data(), dp, dr, R, F.keys.as<uint64_t>(), F.G,
-                             F.ptr.as<uint64_t>(), F.fcoord.as<uint32_t>(), F.fval.as<double>(), M, derr, stream);
+    const krpg::FiberIndexDev& F = T.fiber(j);
+    t_sts = pbegin();
+    krpg::launch_sts_rhs(di, J, N, j, T.dims.data(), dp, dr, R, F, work, M, derr, stream);
+    pend(KRPG_PROF_STS_SCATTER, t_sts, 9);
     // 4) pinv_psd(gram(sa)) on the host (dense_kernels.cpp:207)
     std::vector<double> gh(size_t(R) * R);
     int eh = 0;
     CK(cudaMemcpyAsync(gh.data(), gs, 8 * gh.size(), cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(&eh, derr, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(sts_stats, krpg::sts_stats_ptr(work, J, R), 32, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     if (eh) throw std::invalid_argument("make_sampling_weights: sampled index has zero probability");
     for (double x : gh) require(std::isfinite(x), "gram: non-finite entries");
     const std::vector<double> ph = krpg::pinv_from_eigen(krpg::eigh_psd(gh.data(), R));
     CK(cudaMemcpyAsync(pinv, ph.data(), 8 * ph.size(), cudaMemcpyHostToDevice, stream));
-    // 5) unew = transpose(matmul(pinv, gram_cross)) ; normalize_columns (:295, :309)
-    krpg::launch_solve_rows(M, Ij, R, pinv, Unew, stream);
-    krpg::launch_normalize_columns(Unew, Ij, R, nrm, stream);
+    // 5) unew = transpose(matmul(pinv, gram_cross)) (:295), normalize_columns (:309)
+    // stored straight into U_j (sampler->update_factor(j, unew), :312-313), rebuild
+    Factor& Fj = f[j];
+    t_sts = pbegin();
+    krpg::launch_solve_normalize(M, Ij, R, pinv, Unew, nrm, Fj.U.p, storage, stream);
+    pend(KRPG_PROF_STS, t_sts, 4);
     std::vector<double> sg(R);
     CK(cudaMemcpyAsync(sg.data(), nrm, 8 * R, cudaMemcpyDeviceToHost, stream));
-    // 6) sampler->update_factor(j, unew) (:312-313): device copy in the storage type + rebuild
-    Factor& Fj = f[j];
-    if (storage == KRPG_STORE_F32)
-        krpg::launch_convert_f64_to_f32(Unew, Fj.U.as<float>(), Ij * R, stream);
-    else
-        CK(cudaMemcpyAsync(Fj.U.p, Unew, 8 * Ij * R, cudaMemcpyDeviceToDevice, stream));
     build_tree(j);
     if (sigma_out) std::copy(sg.begin(), sg.end(), sigma_out);
 }
@@ -682,6 +666,7 @@ int krpg_tensor_create(const uint64_t* dims, uint32_t N, const uint32_t* coords,
         t->N = N;
         t->dims.assign(dims, dims + N);
         t->fib.resize(N);
+        t->fib_built.assign(N, false);
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
         if (nnz) {
@@ -727,6 +712,13 @@ int krpg_tensor_entries(krpg_tensor_t t, uint32_t* coords, double* values) {
         CK(cudaSetDevice(t->device));
         if (coords && t->nnz) CK(cudaMemcpy(coords, t->coords.p, 4 * t->nnz * t->N, cudaMemcpyDeviceToHost));
         if (values && t->nnz) CK(cudaMemcpy(values, t->values.p, 8 * t->nnz, cudaMemcpyDeviceToHost));
+    });
+}
+
+int krpg_sts_last_stats(krpg_t h, uint64_t* stats) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        for (int i = 0; i < 3; ++i) stats[i] = h->sts_stats[i];
     });
 }
 
@@ -835,7 +827,7 @@ int krpg_destroy(krpg_t h) {
         F.U.release();
         F.tree.release();
     }
-    for (DevBuf* b : {&h->tbuf, &h->small, &h->Q, &h->err, &h->sH, &h->sIdx, &h->sProb, &h->sMargin, &h->rowbuf,
+    for (DevBuf* b : {&h->tbuf, &h->small, &h->Q, &h->err, &h->sH, &h->sIdx, &h->sProb, &h->sMargin, &h->rowbuf, &h->stswork,
                       &h->gstate, &h->zbuf})
         b->release();
     for (int i = 0; i < 2; ++i) {

@@ -125,17 +125,30 @@ void launch_full_gram(const void* U, uint32_t storage, uint64_t I, uint32_t R, d
 // dedup, *_out allocated with cudaMalloc (caller frees)
 uint64_t tensor_ingest(const uint32_t* d_coords, const double* d_vals, uint64_t nnz, uint32_t N, const uint64_t* dims,
                        uint32_t** d_coords_out, double** d_vals_out, cudaStream_t s);
-// fiber index of mode j (tensor.cpp:104-129); returns #fibers G; outputs cudaMalloc'ed
-uint64_t fiber_index_build(const uint32_t* d_coords, const double* d_vals, uint64_t nnz, uint32_t N,
-                           const uint64_t* dims, uint32_t j, uint64_t** d_keys, uint64_t** d_ptr,
-                           uint32_t** d_fcoord, double** d_fval, cudaStream_t s);
-// M (I_j x R, zeroed by the caller) += scatter of the sampled fibers (gram_cross(sa, sb)^T)
-void launch_sampled_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, const uint64_t* dims,
-                        const double* prob, const double* rows, uint32_t R, const uint64_t* keys, uint64_t G,
-                        const uint64_t* ptr, const uint32_t* fcoord, const double* fval, double* M, int* err,
-                        cudaStream_t s);
-void launch_solve_rows(const double* M, uint64_t I, uint32_t R, const double* pinv, double* U, cudaStream_t s);
-// column norms -> nrm (R), columns scaled to unit norm (cp_als.cpp:39-52)
-void launch_normalize_columns(double* U, uint64_t I, uint32_t R, double* nrm, cudaStream_t s);
+// fiber index of mode j (tensor.cpp:104-129): distinct keys, CSR offsets, and the
+// (coordinate j, value) of every entry in fiber order
+struct FiberIndexDev {
+    uint64_t G = 0, nnz = 0, I = 0;
+    uint64_t* keys = nullptr;    // G distinct matricization columns, ascending
+    uint64_t* fptr = nullptr;    // G + 1
+    uint32_t* fcoord = nullptr;  // nnz
+    double* fval = nullptr;      // nnz
+};
+void fiber_index_build(const uint32_t* d_coords, const double* d_vals, uint64_t nnz, uint32_t N, const uint64_t* dims,
+                       uint32_t j, FiberIndexDev* out, cudaStream_t s);
+void fiber_index_free(FiberIndexDev& f);
+// device scratch for one step, and where its statistics live (4 u64: draws with a
+// nonzero fiber, distinct sampled fibers, entries visited, unused)
+size_t sts_work_bytes(uint64_t J, uint32_t R);
+const void* sts_stats_ptr(void* work, uint64_t J, uint32_t R);
+// M (I_j x R) = (SA^T SB)^T from the batch: draws -> fibers, per distinct fiber
+// S = sum w^2 rows, entries scattered v S (M zeroed here)
+void launch_sts_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, const uint64_t* dims, const double* prob,
+                    const double* rows, uint32_t R, const FiberIndexDev& F, void* work, double* M, int* err,
+                    cudaStream_t s);
+// U = (pinv M^T)^T row by row into Utmp, column norms -> nrm (R), then the
+// normalised columns (cp_als.cpp:39-52) stored into Uout (storage 0 f64, 1 f32)
+void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const double* pinv, double* Utmp, double* nrm,
+                            void* Uout, uint32_t storage, cudaStream_t s);
 
 }  // namespace krpg

@@ -8,13 +8,17 @@
 //  * fiber index of mode j (SparseTensorCoo::fiber_index, tensor.cpp:104-129):
 //    entries sorted by their mode-j matricization column (lowest mode
 //    fastest), distinct keys + CSR offsets; the fiber's (coordinate j, value)
-//    pairs are stored contiguously in key order for the scatter;
+//    pairs are stored contiguously in key order;
 //  * sampled right-hand side (sampled_rhs_rows, cp_als.cpp:122-145) without
-//    the dense J x I_j block: each draw's fiber is found by binary search and
-//    its nonzeros scattered straight into M = (SA^T SB)^T (I_j x R):
-//    M[i, :] += (w_d rows_d) (w_d v), the products gram_cross forms;
-//  * the solve U_j = (pinv(SA^T SA) (SA^T SB))^T row by row, then
-//    normalize_columns (cp_als.cpp:39-52).
+//    the dense J x I_j block: each draw's fiber is found by binary search,
+//    draws are sorted by fiber, and every distinct sampled fiber g gets
+//    S_g = sum_{d -> g} w_d^2 rows_d (a deterministic segmented sum), so a
+//    fiber drawn many times is visited once; its nonzeros then add v_e S_g
+//    into row coord_j(e) of M = (SA^T SB)^T, in fixed-size chunks of entries
+//    per warp (load-balanced across huge Zipf fibers);
+//  * the solve U_j[i] = pinv(SA^T SA) M[i] row by row (gram_cross + matmul +
+//    transpose, dense_kernels.cpp:44-56, 209-223), column norms on the way,
+//    then normalize_columns (cp_als.cpp:39-52) fused with the store into U_j.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -24,14 +28,15 @@
 
 #include "krpg_device.cuh"
 #include "krpg_kernels.hpp"
+#include "ptx.cuh"
 
 namespace krpg {
 
 namespace {
 
-#define STS_CK(call)                                                                          \
-    do {                                                                                      \
-        cudaError_t e_ = (call);                                                              \
+#define STS_CK(call)                                                                                       \
+    do {                                                                                                   \
+        cudaError_t e_ = (call);                                                                           \
         if (e_ != cudaSuccess) throw std::runtime_error(std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
@@ -53,9 +58,16 @@ struct Scratch {  // CUB temporary storage
 };
 
 struct Radix {  // mixed-radix strides, up to 8 modes
-    uint64_t dim[8], stride[8];
+    uint64_t stride[8];
     uint32_t N;
 };
+
+constexpr uint32_t SCHUNK = 128;  // entries per scatter work item
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+
+unsigned grid_of(uint64_t n) { return unsigned(std::min<uint64_t>((n + 255) / 256, 148ull * 32)); }
+
+int bits_for(uint64_t top) { return top ? 64 - __builtin_clzll(top) : 1; }
 
 __global__ void k_linear_keys(const uint32_t* __restrict__ coords, uint64_t nnz, Radix rx, uint64_t* __restrict__ key,
                               uint64_t* __restrict__ id) {
@@ -87,93 +99,278 @@ __global__ void k_gather_fiber(const uint64_t* __restrict__ order, const uint32_
     }
 }
 
-unsigned grid_of(uint64_t n) { return unsigned(std::min<uint64_t>((n + 255) / 256, 148ull * 32)); }
-
-// one warp per draw: fiber lookup (lane 0 binary search), then the fiber's
-// nonzeros scattered into M with the products of gram_cross(sa, sb)
-__global__ void k_sampled_rhs_scatter(const uint32_t* __restrict__ idx, uint64_t J, uint32_t N, Radix colrx,
-                                      const double* __restrict__ prob, const double* __restrict__ rows, uint32_t R,
-                                      const uint64_t* __restrict__ keys, uint64_t G, const uint64_t* __restrict__ ptr,
-                                      const uint32_t* __restrict__ fcoord, const double* __restrict__ fval,
-                                      double* __restrict__ M, int* err) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t d = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); d < J; d += warps) {
+// per draw: the fiber (index into the sorted distinct keys) its drawn
+// coordinates select, NONE if that fiber has no nonzero; checks q > 0
+__global__ void k_draw_fibers(const uint32_t* __restrict__ idx, uint64_t J, uint32_t N, Radix colrx,
+                              const double* __restrict__ prob, const uint64_t* __restrict__ keys, uint64_t G,
+                              uint32_t* __restrict__ gdraw, uint32_t* __restrict__ did, int* err) {
+    for (uint64_t d = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; d < J; d += uint64_t(gridDim.x) * blockDim.x) {
         const double q = prob[d];
-        if (!(q > 0.0) || !isfinite(q)) {  // make_sampling_weights (sketch.cpp:44-47)
-            if (lane == 0) atomicExch(err, 1);
+        if (!(q > 0.0) || !isfinite(q)) atomicExch(err, 1);  // make_sampling_weights (sketch.cpp:44-47)
+        // flat index, RowOrder::Reversed (first included factor fastest) = the
+        // mode-j matricization column of the drawn coordinates (tensor.cpp:20-32)
+        uint64_t u = 0;
+        for (uint32_t k = 0; k < N; ++k) u += uint64_t(idx[d * N + k]) * colrx.stride[k];
+        uint64_t lo = 0, hi = G;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < u)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        gdraw[d] = (lo < G && keys[lo] == u) ? uint32_t(lo) : NONE;
+        did[d] = uint32_t(d);
+    }
+}
+
+// one warp per sampled fiber (segment of the fiber-sorted draws):
+// S[sg] = sum_d (w_d rows_d) w_d in draw order; chunk count of its entries
+__global__ void k_fiber_sums(const uint32_t* __restrict__ ug, const uint32_t* __restrict__ cnt,
+                             const uint32_t* __restrict__ start, const uint32_t* __restrict__ nseg,
+                             const uint32_t* __restrict__ dsorted, const double* __restrict__ prob,
+                             const double* __restrict__ rows, uint64_t J, uint32_t R,
+                             const uint64_t* __restrict__ fptr, double* __restrict__ S, uint32_t* __restrict__ wcnt) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t n = *nseg;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t sg = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); sg < J; sg += warps) {
+        if (sg >= n) {  // unused segment slots take no scatter work
+            if (lane == 0) wcnt[sg] = 0;
             continue;
         }
-        const double w = 1.0 / sqrt(static_cast<double>(J) * q);
-        int64_t g = -1;
-        if (lane == 0) {
-            // flat index, RowOrder::Reversed (first included factor fastest) = the
-            // mode-j matricization column of the drawn coordinates
-            uint64_t u = 0;
-            for (uint32_t k = 0; k < N; ++k) u += uint64_t(idx[d * N + k]) * colrx.stride[k];
-            uint64_t lo = 0, hi = G;
-            while (lo < hi) {
-                const uint64_t mid = (lo + hi) >> 1;
-                if (keys[mid] < u) lo = mid + 1; else hi = mid;
-            }
-            if (lo < G && keys[lo] == u) g = int64_t(lo);
+        const uint32_t g = ug[sg];
+        if (g == NONE) {  // draws whose fiber holds no nonzero (all-zero SB row)
+            if (lane == 0) wcnt[sg] = 0;
+            continue;
         }
-        g = __shfl_sync(0xffffffffu, g, 0);
-        if (g < 0) continue;  // all-zero fiber
-        for (uint64_t p = ptr[g]; p < ptr[g + 1]; ++p) {
-            const uint64_t i = fcoord[p];
-            const double sb = w * fval[p];
-            for (uint32_t c = lane; c < R; c += 32) atomicAdd(M + i * R + c, (w * rows[d * R + c]) * sb);
+        if (lane == 0) wcnt[sg] = uint32_t((fptr[g + 1] - fptr[g] + SCHUNK - 1) / SCHUNK);
+        for (uint32_t c = lane; c < R; c += 32) {
+            double acc = 0.0;
+            for (uint32_t t = start[sg]; t < start[sg] + cnt[sg]; ++t) {
+                const uint32_t d = dsorted[t];
+                const double w = 1.0 / sqrt(static_cast<double>(J) * prob[d]);
+                acc += (w * rows[uint64_t(d) * R + c]) * w;
+            }
+            S[sg * R + c] = acc;
         }
     }
 }
 
-// U[i, a] = sum_k pinv[a, k] M[i, k] (matmul(pinv, gram_cross) transposed, dense_kernels.cpp:209-223)
+// step statistics: draws with a nonzero fiber, distinct sampled fibers, entries visited
+__global__ void k_sts_stats(const uint32_t* __restrict__ ug, const uint32_t* __restrict__ cnt,
+                            const uint32_t* __restrict__ nseg, const uint64_t* __restrict__ fptr,
+                            unsigned long long* __restrict__ stats) {
+    const uint32_t n = *nseg;
+    unsigned long long a = 0, b = 0, c = 0;
+    for (uint32_t sg = blockIdx.x * blockDim.x + threadIdx.x; sg < n; sg += gridDim.x * blockDim.x) {
+        const uint32_t g = ug[sg];
+        if (g == NONE) continue;
+        a += cnt[sg];
+        b += 1;
+        c += fptr[g + 1] - fptr[g];
+    }
+    atomicAdd(stats + 0, a);
+    atomicAdd(stats + 1, b);
+    atomicAdd(stats + 2, c);
+}
+
+// one warp per work item (SCHUNK entries of one sampled fiber):
+// M[coord_j(e), :] += v_e S[sg] (the products of gram_cross(sa, sb), regrouped)
+__global__ void k_fiber_scatter(const uint32_t* __restrict__ ug, const uint32_t* __restrict__ wstart,
+                                const uint32_t* __restrict__ nseg, uint64_t J, const uint64_t* __restrict__ fptr,
+                                const uint32_t* __restrict__ fcoord, const double* __restrict__ fval,
+                                const double* __restrict__ S, uint32_t R, double* __restrict__ M) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t n = *nseg;
+    if (n == 0) return;
+    const uint64_t total = wstart[J];  // exclusive scan over J slots, J + 1 entries
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t it = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); it < total; it += warps) {
+        uint32_t lo = 0, hi = n;  // last segment with wstart <= it (it has work, so it is a fiber)
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (wstart[mid] <= it)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const uint32_t sg = lo, g = ug[sg];
+        const uint64_t p0 = fptr[g] + (it - wstart[sg]) * SCHUNK;
+        const uint64_t p1 = p0 + SCHUNK < fptr[g + 1] ? p0 + SCHUNK : fptr[g + 1];
+        const double* Sg = S + uint64_t(sg) * R;
+        double sv[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) sv[t] = (lane + 32 * t < int(R)) ? Sg[lane + 32 * t] : 0.0;
+        for (uint64_t p = p0; p < p1; ++p) {
+            const uint64_t i = fcoord[p];
+            const double v = fval[p];
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (lane + 32 * t < int(R)) atomicAdd(M + i * R + lane + 32 * t, v * sv[t]);
+        }
+    }
+}
+
+// U[i, a] = sum_k pinv[a, k] M[i, k] (matmul(pinv, gram_cross) transposed,
+// dense_kernels.cpp:209-223), one warp per row; pinv staged transposed in shared
+// memory so lanes (= output columns) read consecutive words. The column sums of
+// squares for normalize_columns are accumulated on the way (colsq, R).
 __global__ void k_solve_rows(const double* __restrict__ M, uint64_t I, uint32_t R, const double* __restrict__ pinv,
-                             double* __restrict__ U, int staged) {
-    extern __shared__ double smem_p[];  // R x R when it fits shared memory
+                             double* __restrict__ U, double* __restrict__ colsq, int staged) {
+    extern __shared__ double smem_p[];  // pinv^T, R x R, when it fits shared memory
+    __shared__ double s_sq[256];
+    for (uint32_t e = threadIdx.x; e < R; e += blockDim.x) s_sq[e] = 0.0;
     if (staged)
-        for (uint32_t e = threadIdx.x; e < R * R; e += blockDim.x) smem_p[e] = pinv[e];
+        for (uint32_t e = threadIdx.x; e < R * R; e += blockDim.x) smem_p[(e % R) * R + e / R] = pinv[e];
     __syncthreads();
-    const double* sp = staged ? smem_p : pinv;
     const int lane = threadIdx.x & 31;
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    double sq[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // R <= 256: lane owns columns lane + 32 t
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < I; i += warps) {
         const double* m = M + i * R;
-        for (uint32_t a = lane; a < R; a += 32) {
-            double acc = 0.0;
-            for (uint32_t k = 0; k < R; ++k) acc += sp[a * R + k] * m[k];
-            U[i * R + a] = acc;
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        bool nz = false;  // rows no sampled fiber touched are zero: skip the product
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (lane + 32 * t < int(R)) nz |= m[lane + 32 * t] != 0.0;
+        if (__any_sync(0xffffffffu, nz))
+        for (uint32_t k = 0; k < R; ++k) {
+            const double mk = m[k];
+            if (mk == 0.0) continue;  // untouched rows / zero entries (matmul skips them too)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const uint32_t a = lane + 32 * t;
+                if (a < R) acc[t] = fma(staged ? smem_p[k * R + a] : pinv[a * R + k], mk, acc[t]);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const uint32_t a = lane + 32 * t;
+            if (a < R) {
+                U[i * R + a] = acc[t];
+                sq[t] = fma(acc[t], acc[t], sq[t]);
+            }
         }
     }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const uint32_t a = lane + 32 * t;
+        if (a < R) atomicAdd(&s_sq[a], sq[t]);
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < R; e += blockDim.x) atomicAdd(colsq + e, s_sq[e]);
 }
 
-__global__ void k_col_sumsq(const double* __restrict__ U, uint64_t I, uint32_t R, uint64_t rows_per_block,
-                            double* __restrict__ out) {
-    const uint64_t r0 = blockIdx.x * rows_per_block;
-    const uint64_t r1 = r0 + rows_per_block < I ? r0 + rows_per_block : I;
-    for (uint32_t c = threadIdx.x; c < R; c += blockDim.x) {
-        double acc = 0.0;
-        for (uint64_t i = r0; i < r1; ++i) acc += U[i * R + c] * U[i * R + c];
-        atomicAdd(out + c, acc);
+// Same solve on the FP64 tensor cores: a warp takes 8 rows, D (8 rows x 8 cols of
+// U) = sum over k-steps of M[rows, 4s..4s+3] (A) x pinv^T[4s..4s+3, 8q..8q+7] (B);
+// pinv staged in shared memory with rows padded to R + 4 doubles (conflict-free
+// B fragments). All-zero 8-row blocks (rows no sampled fiber touched) skip the MMA.
+template <int NB>
+__global__ void __launch_bounds__(256) k_solve_rows_dmma(const double* __restrict__ M, uint64_t I,
+                                                         const double* __restrict__ pinv, double* __restrict__ U,
+                                                         double* __restrict__ colsq) {
+    constexpr int R = 8 * NB, KS = R / 4, LD = R + 4;
+    extern __shared__ double sp[];  // R x LD
+    __shared__ double s_sq[R];
+    for (int e = threadIdx.x; e < R; e += blockDim.x) s_sq[e] = 0.0;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) sp[(e / R) * LD + e % R] = pinv[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, m = lane >> 2, kq = lane & 3;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    double sq[NB][2];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) sq[q][0] = sq[q][1] = 0.0;
+    const uint64_t nblk = (I + 7) / 8;
+    for (uint64_t b = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); b < nblk; b += warps) {
+        const uint64_t row = 8 * b + m;
+        const bool rv = row < I;
+        double a[KS];
+        bool nz = false;
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+            a[t] = rv ? M[row * R + 4 * t + kq] : 0.0;
+            nz |= a[t] != 0.0;
+        }
+        double d[NB][2];
+#pragma unroll
+        for (int q = 0; q < NB; ++q) d[q][0] = d[q][1] = 0.0;
+        if (__any_sync(0xffffffffu, nz)) {
+#pragma unroll
+            for (int t = 0; t < KS; ++t)
+#pragma unroll
+                for (int q = 0; q < NB; ++q) dmma_884(d[q][0], d[q][1], a[t], sp[(8 * q + m) * LD + 4 * t + kq]);
+        }
+        if (rv) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                *reinterpret_cast<double2*>(U + row * R + 8 * q + 2 * kq) = make_double2(d[q][0], d[q][1]);
+                sq[q][0] = fma(d[q][0], d[q][0], sq[q][0]);
+                sq[q][1] = fma(d[q][1], d[q][1], sq[q][1]);
+            }
+        }
     }
+    // reduce over the 8 row-lanes sharing (lane & 3), then per block, then global
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double v = sq[q][e];
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            if (m == 0) atomicAdd(&s_sq[8 * q + 2 * kq + e], v);
+        }
+    __syncthreads();
+    for (int e = threadIdx.x; e < R; e += blockDim.x) atomicAdd(colsq + e, s_sq[e]);
 }
 
 __global__ void k_sqrt_inplace(double* x, uint32_t n) {
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = sqrt(x[i]);
 }
 
-__global__ void k_normalize(double* __restrict__ U, uint64_t I, uint32_t R, const double* __restrict__ nrm) {
+// normalize_columns (cp_als.cpp:39-52) fused with the store into the factor's
+// storage type
+template <typename T>
+__global__ void k_normalize_store(const double* __restrict__ U, uint64_t I, uint32_t R, const double* __restrict__ nrm,
+                                  T* __restrict__ out) {
     const uint64_t total = I * R;
     for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t c = uint32_t(e % R);
         const double n = nrm[c];
+        double x = U[e];
         if (n > 0.0)
-            U[e] /= n;
-        else if (e / R == c % I)  // zero column: deterministic unit basis vector (cp_als.cpp:48-50)
-            U[e] = 1.0;
+            x /= n;
+        else if (e / R == c % I)  // zero column: deterministic unit basis vector
+            x = 1.0;
+        out[e] = static_cast<T>(x);
     }
 }
+
+struct StsWork {  // views into the per-step scratch (sts_work_bytes)
+    double* S;
+    unsigned long long* stats;
+    uint32_t *gdraw, *gsort, *did, *dsort, *ug, *cnt, *wcnt, *start, *wstart, *nseg;
+    void* cub;
+    StsWork(void* work, uint64_t J, uint32_t R) {
+        char* w = static_cast<char*>(work);
+        S = reinterpret_cast<double*>(w);
+        stats = reinterpret_cast<unsigned long long*>(w + 8 * J * R);
+        gdraw = reinterpret_cast<uint32_t*>(stats + 4);
+        gsort = gdraw + J;
+        did = gsort + J;
+        dsort = did + J;
+        ug = dsort + J;
+        cnt = ug + J;
+        wcnt = cnt + J;  // J + 1 (the last slot stays 0)
+        start = wcnt + J + 1;
+        wstart = start + J + 1;
+        nseg = wstart + J + 1;
+        cub = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(nseg + 1) + 255) & ~uintptr_t(255));
+    }
+};
+
+constexpr size_t kCubBytes = size_t(1) << 20;
 
 }  // namespace
 
@@ -183,14 +380,12 @@ uint64_t tensor_ingest(const uint32_t* d_coords, const double* d_vals, uint64_t 
     Radix rx{};
     rx.N = N;
     uint64_t st = 1;
-    for (int m = int(N) - 1; m >= 0; --m) {
-        rx.dim[m] = dims[m];
+    for (int m = int(N) - 1; m >= 0; --m) {  // mode 0 slowest: lexicographic order
         rx.stride[m] = st;
         st *= dims[m];
     }
-    uint64_t *key = nullptr, *key2 = nullptr, *ukey = nullptr;
+    uint64_t *key = nullptr, *key2 = nullptr, *ukey = nullptr, *nrun = nullptr;
     double *val2 = nullptr, *uval = nullptr;
-    uint64_t* nrun = nullptr;
     STS_CK(cudaMallocAsync(&key, 8 * nnz, s));
     STS_CK(cudaMallocAsync(&key2, 8 * nnz, s));
     STS_CK(cudaMallocAsync(&val2, 8 * nnz, s));
@@ -200,11 +395,7 @@ uint64_t tensor_ingest(const uint32_t* d_coords, const double* d_vals, uint64_t 
     k_linear_keys<<<grid_of(nnz), 256, 0, s>>>(d_coords, nnz, rx, key, nullptr);
     Scratch tmp;
     size_t need = 0;
-    int bits = 64;
-    {
-        uint64_t top = st - 1;
-        bits = top ? 64 - __builtin_clzll(top) : 1;
-    }
+    const int bits = bits_for(st - 1);
     STS_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, d_vals, val2, nnz, 0, bits, s));
     STS_CK(cub::DeviceRadixSort::SortPairs(tmp.get(need), need, key, key2, d_vals, val2, nnz, 0, bits, s));
     need = 0;
@@ -213,8 +404,8 @@ uint64_t tensor_ingest(const uint32_t* d_coords, const double* d_vals, uint64_t 
     uint64_t n = 0;
     STS_CK(cudaMemcpyAsync(&n, nrun, 8, cudaMemcpyDeviceToHost, s));
     STS_CK(cudaStreamSynchronize(s));
-    STS_CK(cudaMalloc(d_coords_out, 4 * n * N));
-    STS_CK(cudaMalloc(d_vals_out, 8 * n));
+    STS_CK(cudaMalloc(d_coords_out, 4 * std::max<uint64_t>(n, 1) * N));
+    STS_CK(cudaMalloc(d_vals_out, 8 * std::max<uint64_t>(n, 1)));
     k_decode<<<grid_of(n), 256, 0, s>>>(ukey, n, rx, *d_coords_out);
     STS_CK(cudaMemcpyAsync(*d_vals_out, uval, 8 * n, cudaMemcpyDeviceToDevice, s));
     for (void* p : {static_cast<void*>(key), static_cast<void*>(key2), static_cast<void*>(val2),
@@ -225,64 +416,71 @@ uint64_t tensor_ingest(const uint32_t* d_coords, const double* d_vals, uint64_t 
 }
 
 // ---- fiber index of mode j ----
-uint64_t fiber_index_build(const uint32_t* d_coords, const double* d_vals, uint64_t nnz, uint32_t N,
-                           const uint64_t* dims, uint32_t j, uint64_t** d_keys, uint64_t** d_ptr,
-                           uint32_t** d_fcoord, double** d_fval, cudaStream_t s) {
+void fiber_index_build(const uint32_t* d_coords, const double* d_vals, uint64_t nnz, uint32_t N, const uint64_t* dims,
+                       uint32_t j, FiberIndexDev* out, cudaStream_t s) {
     Radix rx{};
     rx.N = N;
     uint64_t st = 1;
     for (uint32_t m = 0; m < N; ++m) {  // lowest mode fastest, mode j skipped (tensor.cpp:20-32)
-        rx.dim[m] = dims[m];
         rx.stride[m] = m == j ? 0 : st;
         if (m != j) st *= dims[m];
     }
+    const uint64_t n1 = std::max<uint64_t>(nnz, 1);
     uint64_t *key = nullptr, *key2 = nullptr, *id = nullptr, *id2 = nullptr, *cnt = nullptr, *nrun = nullptr;
-    STS_CK(cudaMallocAsync(&key, 8 * nnz, s));
-    STS_CK(cudaMallocAsync(&key2, 8 * nnz, s));
-    STS_CK(cudaMallocAsync(&id, 8 * nnz, s));
-    STS_CK(cudaMallocAsync(&id2, 8 * nnz, s));
-    STS_CK(cudaMallocAsync(&cnt, 8 * (nnz + 1), s));
+    STS_CK(cudaMallocAsync(&key, 8 * n1, s));
+    STS_CK(cudaMallocAsync(&key2, 8 * n1, s));
+    STS_CK(cudaMallocAsync(&id, 8 * n1, s));
+    STS_CK(cudaMallocAsync(&id2, 8 * n1, s));
+    STS_CK(cudaMallocAsync(&cnt, 8 * (n1 + 1), s));
     STS_CK(cudaMallocAsync(&nrun, 8, s));
     k_linear_keys<<<grid_of(nnz), 256, 0, s>>>(d_coords, nnz, rx, key, id);
-    int bits = 1;
-    {
-        const uint64_t top = st - 1;
-        bits = top ? 64 - __builtin_clzll(top) : 1;
-    }
+    const int bits = bits_for(st - 1);
     Scratch tmp;
     size_t need = 0;
     STS_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, id, id2, nnz, 0, bits, s));
     STS_CK(cub::DeviceRadixSort::SortPairs(tmp.get(need), need, key, key2, id, id2, nnz, 0, bits, s));
-    uint64_t* ukeys = key;  // reuse
     need = 0;
-    STS_CK(cub::DeviceRunLengthEncode::Encode(nullptr, need, key2, ukeys, cnt, nrun, nnz, s));
-    STS_CK(cub::DeviceRunLengthEncode::Encode(tmp.get(need), need, key2, ukeys, cnt, nrun, nnz, s));
+    STS_CK(cub::DeviceRunLengthEncode::Encode(nullptr, need, key2, key, cnt, nrun, nnz, s));
+    STS_CK(cub::DeviceRunLengthEncode::Encode(tmp.get(need), need, key2, key, cnt, nrun, nnz, s));
     uint64_t G = 0;
     STS_CK(cudaMemcpyAsync(&G, nrun, 8, cudaMemcpyDeviceToHost, s));
     STS_CK(cudaStreamSynchronize(s));
-    STS_CK(cudaMalloc(d_keys, 8 * std::max<uint64_t>(G, 1)));
-    STS_CK(cudaMalloc(d_ptr, 8 * (G + 1)));
-    STS_CK(cudaMalloc(d_fcoord, 4 * std::max<uint64_t>(nnz, 1)));
-    STS_CK(cudaMalloc(d_fval, 8 * std::max<uint64_t>(nnz, 1)));
-    STS_CK(cudaMemcpyAsync(*d_keys, ukeys, 8 * G, cudaMemcpyDeviceToDevice, s));
+    out->G = G;
+    out->nnz = nnz;
+    out->I = dims[j];
+    STS_CK(cudaMalloc(&out->keys, 8 * std::max<uint64_t>(G, 1)));
+    STS_CK(cudaMalloc(&out->fptr, 8 * (G + 1)));
+    STS_CK(cudaMalloc(&out->fcoord, 4 * n1));
+    STS_CK(cudaMalloc(&out->fval, 8 * n1));
+    STS_CK(cudaMemcpyAsync(out->keys, key, 8 * G, cudaMemcpyDeviceToDevice, s));
     STS_CK(cudaMemsetAsync(cnt + G, 0, 8, s));
     need = 0;
-    STS_CK(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, *d_ptr, G + 1, s));
-    STS_CK(cub::DeviceScan::ExclusiveSum(tmp.get(need), need, cnt, *d_ptr, G + 1, s));
-    // the fiber-ordered (coordinate j, value) pairs, from the sorted entry ids
-    k_gather_fiber<<<grid_of(nnz), 256, 0, s>>>(id2, d_coords, d_vals, nnz, N, j, *d_fcoord, *d_fval);
+    STS_CK(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, out->fptr, G + 1, s));
+    STS_CK(cub::DeviceScan::ExclusiveSum(tmp.get(need), need, cnt, out->fptr, G + 1, s));
+    k_gather_fiber<<<grid_of(nnz), 256, 0, s>>>(id2, d_coords, d_vals, nnz, N, j, out->fcoord, out->fval);
     for (void* p : {static_cast<void*>(key), static_cast<void*>(key2), static_cast<void*>(id), static_cast<void*>(id2),
                     static_cast<void*>(cnt), static_cast<void*>(nrun)})
         STS_CK(cudaFreeAsync(p, s));
     STS_CK(cudaStreamSynchronize(s));
-    return G;
+}
+
+void fiber_index_free(FiberIndexDev& f) {
+    for (void* p : {static_cast<void*>(f.keys), static_cast<void*>(f.fptr), static_cast<void*>(f.fcoord),
+                    static_cast<void*>(f.fval)})
+        if (p) cudaFree(p);
+    f = FiberIndexDev{};
 }
 
 // ---- one STS-CP step's device work ----
-void launch_sampled_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, const uint64_t* dims,
-                        const double* prob, const double* rows, uint32_t R, const uint64_t* keys, uint64_t G,
-                        const uint64_t* ptr, const uint32_t* fcoord, const double* fval, double* M, int* err,
-                        cudaStream_t s) {
+// layout: S (J x R doubles) | stats (4 u64) | gdraw gsort did dsort ug cnt (J u32 each)
+//         | wcnt start wstart (J+1 each) | nseg | CUB scratch (256-aligned)
+size_t sts_work_bytes(uint64_t J, uint32_t R) { return 8 * J * R + 32 + 4 * (9 * J + 4) + 512 + kCubBytes; }
+
+const void* sts_stats_ptr(void* work, uint64_t J, uint32_t R) { return StsWork(work, J, R).stats; }
+
+void launch_sts_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, const uint64_t* dims, const double* prob,
+                    const double* rows, uint32_t R, const FiberIndexDev& F, void* work, double* M, int* err,
+                    cudaStream_t s) {
     Radix colrx{};
     colrx.N = N;
     uint64_t st = 1;
@@ -290,11 +488,38 @@ void launch_sampled_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j,
         colrx.stride[m] = m == j ? 0 : st;
         if (m != j) st *= dims[m];
     }
-    const unsigned grid = unsigned(std::min<uint64_t>((J + 7) / 8, 148ull * 16));
-    k_sampled_rhs_scatter<<<grid, 256, 0, s>>>(idx, J, N, colrx, prob, rows, R, keys, G, ptr, fcoord, fval, M, err);
+    StsWork W(work, J, R);
+    auto cub_check = [&](size_t need) {
+        if (need > kCubBytes) throw std::runtime_error("sts: CUB scratch too small");
+    };
+    k_draw_fibers<<<grid_of(J), 256, 0, s>>>(idx, J, N, colrx, prob, F.keys, F.G, W.gdraw, W.did, err);
+    size_t need = 0;
+    STS_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, W.gdraw, W.gsort, W.did, W.dsort, J, 0, 32, s));
+    cub_check(need);
+    STS_CK(cub::DeviceRadixSort::SortPairs(W.cub, need, W.gdraw, W.gsort, W.did, W.dsort, J, 0, 32, s));
+    need = 0;
+    STS_CK(cub::DeviceRunLengthEncode::Encode(nullptr, need, W.gsort, W.ug, W.cnt, W.nseg, J, s));
+    cub_check(need);
+    STS_CK(cub::DeviceRunLengthEncode::Encode(W.cub, need, W.gsort, W.ug, W.cnt, W.nseg, J, s));
+    need = 0;
+    STS_CK(cub::DeviceScan::ExclusiveSum(nullptr, need, W.cnt, W.start, J, s));
+    cub_check(need);
+    STS_CK(cub::DeviceScan::ExclusiveSum(W.cub, need, W.cnt, W.start, J, s));
+    const unsigned wgrid = unsigned(std::min<uint64_t>((J + 7) / 8, 148ull * 16));
+    k_fiber_sums<<<wgrid, 256, 0, s>>>(W.ug, W.cnt, W.start, W.nseg, W.dsort, prob, rows, J, R, F.fptr, W.S, W.wcnt);
+    STS_CK(cudaMemsetAsync(W.wcnt + J, 0, 4, s));  // wstart[J] = total work items
+    need = 0;
+    STS_CK(cub::DeviceScan::ExclusiveSum(nullptr, need, W.wcnt, W.wstart, J + 1, s));
+    cub_check(need);
+    STS_CK(cub::DeviceScan::ExclusiveSum(W.cub, need, W.wcnt, W.wstart, J + 1, s));
+    STS_CK(cudaMemsetAsync(W.stats, 0, 32, s));
+    k_sts_stats<<<64, 256, 0, s>>>(W.ug, W.cnt, W.nseg, F.fptr, W.stats);
+    STS_CK(cudaMemsetAsync(M, 0, 8 * F.I * R, s));
+    k_fiber_scatter<<<148 * 16, 256, 0, s>>>(W.ug, W.wstart, W.nseg, J, F.fptr, F.fcoord, F.fval, W.S, R, M);
 }
 
-void launch_solve_rows(const double* M, uint64_t I, uint32_t R, const double* pinv, double* U, cudaStream_t s) {
+void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const double* pinv, double* Utmp, double* nrm,
+                            void* Uout, uint32_t storage, cudaStream_t s) {
     const size_t need = sizeof(double) * R * R;
     const bool staged = need <= 160 * 1024;  // R <= 144; larger pinv is read through L1/L2
     const size_t smem = staged ? need : 0;
@@ -303,17 +528,43 @@ void launch_solve_rows(const double* M, uint64_t I, uint32_t R, const double* pi
         cudaFuncSetAttribute(k_solve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         configured_for = smem;
     }
-    const unsigned grid = unsigned(std::min<uint64_t>((I + 7) / 8, 148ull * 8));
-    k_solve_rows<<<grid, 256, smem, s>>>(M, I, R, pinv, U, staged ? 1 : 0);
-}
-
-void launch_normalize_columns(double* U, uint64_t I, uint32_t R, double* nrm, cudaStream_t s) {
-    const uint64_t rpb = 256;
-    const unsigned grid = unsigned((I + rpb - 1) / rpb);
     cudaMemsetAsync(nrm, 0, sizeof(double) * R, s);
-    k_col_sumsq<<<grid, 64, 0, s>>>(U, I, R, rpb, nrm);
+    if (R % 8 == 0 && R <= 128) {  // FP64 tensor-core path (padded pinv fits shared memory)
+        const size_t dsm = sizeof(double) * R * (R + 4);
+        const unsigned grid = unsigned(std::min<uint64_t>((I + 63) / 64, 148ull * 8));
+        auto launch = [&](auto kern) {
+            static size_t conf = 0;
+            if (dsm > 48 * 1024 && conf < dsm) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));
+                conf = dsm;
+            }
+            kern<<<grid, 256, dsm, s>>>(M, I, pinv, Utmp, nrm);
+        };
+        switch (R / 8) {
+            case 1: launch(k_solve_rows_dmma<1>); break;
+            case 2: launch(k_solve_rows_dmma<2>); break;
+            case 3: launch(k_solve_rows_dmma<3>); break;
+            case 4: launch(k_solve_rows_dmma<4>); break;
+            case 5: launch(k_solve_rows_dmma<5>); break;
+            case 6: launch(k_solve_rows_dmma<6>); break;
+            case 7: launch(k_solve_rows_dmma<7>); break;
+            case 8: launch(k_solve_rows_dmma<8>); break;
+            case 12: launch(k_solve_rows_dmma<12>); break;
+            case 16: launch(k_solve_rows_dmma<16>); break;
+            default: {
+                const unsigned g2 = unsigned(std::min<uint64_t>((I + 7) / 8, 148ull * 8));
+                k_solve_rows<<<g2, 256, smem, s>>>(M, I, R, pinv, Utmp, nrm, staged ? 1 : 0);
+            }
+        }
+    } else {
+        const unsigned grid = unsigned(std::min<uint64_t>((I + 7) / 8, 148ull * 8));
+        k_solve_rows<<<grid, 256, smem, s>>>(M, I, R, pinv, Utmp, nrm, staged ? 1 : 0);
+    }
     k_sqrt_inplace<<<1, 256, 0, s>>>(nrm, R);
-    k_normalize<<<grid_of(I * R), 256, 0, s>>>(U, I, R, nrm);
+    if (storage == 1)
+        k_normalize_store<float><<<grid_of(I * R), 256, 0, s>>>(Utmp, I, R, nrm, static_cast<float*>(Uout));
+    else
+        k_normalize_store<double><<<grid_of(I * R), 256, 0, s>>>(Utmp, I, R, nrm, static_cast<double*>(Uout));
 }
 
 }  // namespace krpg

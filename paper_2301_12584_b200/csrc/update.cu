@@ -133,7 +133,8 @@ void launch_convert_f32_to_f64(const float* in, double* out, uint64_t n, cudaStr
 }
 
 void launch_full_gram(const void* U, uint32_t storage, uint64_t I, uint32_t R, double* out, cudaStream_t s) {
-    const uint64_t rpb = 4096;
+    // ~4 blocks per SM whatever I is (each block: one partial Gram, then atomics)
+    const uint64_t rpb = std::max<uint64_t>(64, (I + 148 * 4 - 1) / (148 * 4));
     const unsigned grid = unsigned((I + rpb - 1) / rpb);
     cudaMemsetAsync(out, 0, sizeof(double) * R * R, s);
     if (storage == 1)

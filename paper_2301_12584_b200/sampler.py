@@ -273,6 +273,12 @@ class KrpSampler:
         check(_lib.lib().krpg_sts_solve(self._h, T._h, j, J, seed, sigma.ctypes.data_as(C.POINTER(C.c_double))))
         return sigma
 
+    def sts_last_stats(self) -> dict:
+        st = (C.c_uint64 * 3)()
+        check(_lib.lib().krpg_sts_last_stats(self._h, st))
+        return {"draws_hitting_nonzero_fibers": int(st[0]), "distinct_fibers": int(st[1]),
+                "entries_visited": int(st[2])}
+
     # ---- row-partitioned construction (multi-GPU, see sharding.build_partitioned) ----
     def tree_device(self, j: int):
         """Zero-copy torch view (L*P doubles) of factor j's compact tree in HBM."""

@@ -3,6 +3,10 @@
   --config 3 : N=4 factors 1.5e7 x 32, uniform[-1,1], fp32-stored / fp64-accumulated;
                tree build, 2^20 two-stage draws, 10^5 random single-entry updates.
   --config 4 : rank sweep, N=3 factors 2^20 x R (R in 16..256), N(0,1); J = 65536.
+  --config 5 : STS-CP factor updates (krpg_sts_solve) on a synthetic COO tensor with the
+               Amazon-Reviews shape 4.8e6 x 1.8e6 x 1.8e6, Zipf(1.1) coordinates per mode,
+               lognormal(0,1) values, duplicates summed; R = 64, J = 65536. The raw
+               nonzero count is scaled down (--nnz, default 2e8 vs 1.7e9) and said so.
 
 One JSON line per measurement. Device times by CUDA events on the sampler's stream.
 """
@@ -109,13 +113,68 @@ def config4(args):
         torch.cuda.empty_cache()
 
 
+def zipf_coords(d, n, s, gen):
+    """Bounded continuous power law x^-s on [1, d+1) by inverse CDF, floored to a
+    rank, then mapped through a random permutation of the mode (GPU)."""
+    u = torch.rand(n, dtype=torch.float64, device="cuda", generator=gen)
+    a = 1.0 - s
+    x = (1.0 + u * ((d + 1.0) ** a - 1.0)) ** (1.0 / a)
+    r = torch.clamp(x.floor().to(torch.int64) - 1, 0, d - 1)
+    perm = torch.randperm(d, device="cuda", generator=gen)
+    return perm[r].to(torch.int32)
+
+
+def config5(args):
+    dims = (4_800_000, 1_800_000, 1_800_000)
+    R, J, nnz = 64, 65536, int(args.nnz)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    coords = torch.stack([zipf_coords(d, nnz, 1.1, gen) for d in dims], dim=1)
+    values = torch.randn(nnz, dtype=torch.float64, device="cuda", generator=gen).exp()
+    from paper_2301_12584_b200 import SparseTensor
+    t0 = time.perf_counter()
+    T = SparseTensor(dims, coords.cpu().numpy().view(np.uint32), values.cpu().numpy())
+    ingest_s = time.perf_counter() - t0
+    del coords, values
+    torch.cuda.empty_cache()
+    fs = [torch.randn(d, R, dtype=torch.float64, device="cuda", generator=gen) for d in dims]
+    s = KrpSampler.from_device(fs)
+    del fs
+    torch.cuda.empty_cache()
+    for j in range(3):  # warm: fiber indexes + buffers
+        s.sts_solve(T, j, J, 100 + j)
+    s.profile_enable(True)
+    res = []
+    for rnd in range(args.rounds):
+        for j in range(3):
+            s.profile_read(reset=True)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s.sts_solve(T, j, J, 1000 * rnd + j)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+            pr = s.profile_read(reset=True)
+            res.append({"mode": j, "I_j": dims[j], "wall_ms": wall * 1e3, "stats": s.sts_last_stats(),
+                        "device_ms": {k: round(v["ms"], 4) for k, v in pr.items() if v["launches"]}})
+    for j in range(3):
+        walls = [r["wall_ms"] for r in res if r["mode"] == j]
+        last = [r for r in res if r["mode"] == j][-1]
+        print(json.dumps({"config": "config5", "workload": "STS-CP factor update (krpg_sts_solve)",
+                          "dims": dims, "R": R, "J": J, "raw_nnz": nnz, "nnz": T.nnz(),
+                          "scaled": f"raw nonzeros {nnz:.3g} instead of 1.7e9 (synthetic Zipf(1.1) tensor)",
+                          "mode": j, "ms_per_update_median": float(np.median(walls)),
+                          "device_ms_breakdown_last": last["device_ms"], "step_stats_last": last["stats"],
+                          "ingest_s": ingest_s}), flush=True)
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--config", type=int, choices=[3, 4], required=True)
+    p.add_argument("--config", type=int, choices=[3, 4, 5], required=True)
+    p.add_argument("--nnz", type=float, default=2e8)
+    p.add_argument("--rounds", type=int, default=3)
     p.add_argument("--ranks", type=int, nargs="+", default=[16, 32, 64, 128, 256])
     args = p.parse_args()
     torch.cuda.init()
-    (config3 if args.config == 3 else config4)(args)
+    {3: config3, 4: config4, 5: config5}[args.config](args)
 
 
 if __name__ == "__main__":
