@@ -167,6 +167,10 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
  * krpg_sync (or krpg_sample) on the handle; profiling events are resolved by
  * krpg_profile_read. */
 #define KRPG_OPT_ASYNC 4
+/* KRPG_OPT_SLICES (default 1, 1..8): the grouped descent splits the J draws into this
+ * many slices run on concurrent streams (results are identical for any value; on
+ * config 2 one slice measured fastest). */
+#define KRPG_OPT_SLICES 5
 int krpg_set_option(krpg_t h, int option, int64_t value);
 
 /* ---- STS-CP solve slice ----

@@ -100,6 +100,7 @@ PROF_NAMES = ["tree_leaf", "tree_levels", "etree", "draws", "prob", "update", "o
 OPT_PROFILE_DETAIL = 2
 OPT_FUSED_DEEP = 3
 OPT_ASYNC = 4
+OPT_SLICES = 5
 
 _lib: C.CDLL | None = None
 

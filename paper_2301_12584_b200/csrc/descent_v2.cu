@@ -64,6 +64,8 @@ struct EvalArgs {
     double* prob;           // EV_PROB output
     double rank_div;        // EV_PROB: numerical rank
     uint32_t* perm_out;     // level passes: next level's sorted order
+    const uint32_t* nsort_in;  // node of each sorted position (nullable: read node[perm[i]])
+    uint32_t* nsort_out;       // node of each position of perm_out
     uint32_t* GS;           // per node position range [GS, GE) at its level
     uint32_t* GE;
 };
@@ -155,12 +157,16 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
     __shared__ uint32_t s_cnt[2], s_base[2], s_gs, s_ge;
     __shared__ __align__(8) uint64_t bar[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // PDL: the next level's grid may launch now; this grid waits for the previous
+    // one (its perm / node / counters) before touching global state
+    griddep_launch_dependents();
+    griddep_wait();
     const uint64_t base = uint64_t(blockIdx.x) * CB;
     const int cnt = a.J - base < uint64_t(CB) ? int(a.J - base) : CB;
     if (tid < cnt) {
         const uint32_t d = a.perm ? a.perm[base + tid] : uint32_t(base + tid);
         s_d[tid] = d;
-        s_v[tid] = (MODE == EV_LEVEL && !ROOT0) ? a.node[d] : 0u;
+        s_v[tid] = (MODE == EV_LEVEL && !ROOT0) ? (a.nsort_in ? a.nsort_in[base + tid] : a.node[d]) : 0u;
     }
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -227,7 +233,10 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
         const double* gr = gsrc(r);
         if (!gr) {  // draws parked at a leaf one level up keep their positions
             if (MODE == EV_LEVEL)
-                for (int t = rs + tid; t < re; t += CB) a.perm_out[base + t] = s_d[t];
+                for (int t = rs + tid; t < re; t += CB) {
+                    a.perm_out[base + t] = s_d[t];
+                    if (a.nsort_out) a.nsort_out[base + t] = s_v[t];
+                }
             continue;
         }
         mbar_wait(&bar[buf], phase[buf]);
@@ -258,8 +267,17 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
             const bool valid = m < n;
             const uint32_t dd = valid ? s_d[b0 + m] : 0u;
             const double* xrow = valid ? a.X + uint64_t(dd) * R : nullptr;
-            const double mass = block_qf_packed<NB>(G, fa, xrow, lane);
             const bool owner = valid && (lane & 3) == 0;
+            // decision inputs requested before the DMMA chain (independent loads in flight)
+            double u_pre = 0.0, ic_pre = 0.0, low_pre = 0.0;
+            if (MODE == EV_LEVEL && owner) {
+                u_pre = a.ud[dd];
+                if (!ROOT0) {
+                    ic_pre = a.invc[dd];
+                    low_pre = a.low[dd];
+                }
+            }
+            const double mass = block_qf_packed<NB>(G, fa, xrow, lane);
             if (MODE == EV_ROOT) {
                 if (owner) {
                     if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
@@ -273,7 +291,7 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
                 bool left = false;
                 double cutoff = 0.0;
                 if (owner) {
-                    const double u = a.ud[dd];
+                    const double u = u_pre;
                     double ic;
                     if (ROOT0) {
                         if (!isfinite(croot) || croot <= 0.0) atomicExch(a.err, 1);
@@ -281,8 +299,8 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
                         a.invc[dd] = ic;
                         cutoff = 0.0 + ic * mass;
                     } else {
-                        ic = a.invc[dd];
-                        cutoff = a.low[dd] + ic * mass;
+                        ic = ic_pre;
+                        cutoff = low_pre + ic * mass;
                     }
                     left = cutoff >= u;
                     if (a.margin) a.margin[dd] = fmin(a.margin[dd], fabs(cutoff - u));
@@ -321,6 +339,7 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
             for (int t = rs + tid; t < re; t += CB) {
                 const uint32_t pos = s_left[t] ? s_gs + s_base[0] + s_rank[t] : s_ge - 1u - (s_base[1] + s_rank[t]);
                 a.perm_out[pos] = s_d[t];
+                if (a.nsort_out) a.nsort_out[pos] = 2 * v + (s_left[t] ? 1u : 2u);
             }
             __syncthreads();
         }
@@ -369,7 +388,7 @@ __global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a) {
     if (tid < cnt) {
         const uint32_t d = a.perm ? a.perm[base + tid] : uint32_t(base + tid);
         s_d[tid] = d;
-        s_v[tid] = MODE == EV_LEVEL ? a.node[d] : 0u;
+        s_v[tid] = MODE == EV_LEVEL ? (a.nsort_in ? a.nsort_in[base + tid] : a.node[d]) : 0u;
     }
     if (tid == 0) {
 #pragma unroll
@@ -447,7 +466,10 @@ __global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a) {
         const int rs = s_rs[r], re = s_rs[r + 1];
         if (!gsrc(r)) {  // draws parked at a leaf one level up keep their positions
             if (MODE == EV_LEVEL)
-                for (int t = rs + tid; t < re; t += CB) a.perm_out[base + t] = s_d[t];
+                for (int t = rs + tid; t < re; t += CB) {
+                    a.perm_out[base + t] = s_d[t];
+                    if (a.nsort_out) a.nsort_out[base + t] = s_v[t];
+                }
             continue;
         }
         const uint32_t v = s_v[rs];
@@ -589,6 +611,7 @@ __global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a) {
             for (int t = rs + tid; t < re; t += CB) {
                 const uint32_t pos = s_left[t] ? s_gs + s_base[0] + s_rank[t] : s_ge - 1u - (s_base[1] + s_rank[t]);
                 a.perm_out[pos] = s_d[t];
+                if (a.nsort_out) a.nsort_out[pos] = 2 * v + (s_left[t] ? 1u : 2u);
             }
             __syncthreads();
         }
@@ -700,7 +723,13 @@ __global__ void k_scatter(const uint32_t* __restrict__ perm_in, uint32_t* __rest
 // stage init: identity order, everyone at the root, this stage's uniform
 __global__ void k_stage_init(uint32_t* perm, uint32_t* node, double* low, double* ud, uint32_t* gstart,
                              uint64_t J, uint64_t seed, uint64_t off, uint64_t counter, double* margin,
-                             int reset_margin) {
+                             int reset_margin, uint32_t* cntL, uint32_t* cntR, uint64_t nnodes) {
+    griddep_launch_dependents();
+    griddep_wait();
+    for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nnodes; v += uint64_t(gridDim.x) * blockDim.x) {
+        cntL[v] = 0;
+        cntR[v] = 0;
+    }
     for (uint64_t d = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; d < J; d += uint64_t(gridDim.x) * blockDim.x) {
         perm[d] = uint32_t(d);
         node[d] = 0;
@@ -714,6 +743,8 @@ __global__ void k_stage_init(uint32_t* perm, uint32_t* node, double* low, double
 // z_d = h_d o V[:, u_d], u_d = the E-tree leaf reached (F = 1 -> row = leaf index)
 __global__ void k_make_z(const double* __restrict__ H, const double* __restrict__ V, const uint32_t* __restrict__ node,
                          Topo te, uint32_t R, uint64_t J, double* __restrict__ Z) {
+    griddep_launch_dependents();
+    griddep_wait();
     const uint64_t total = J * R;
     for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t d = e / R;
@@ -1027,6 +1058,8 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
     constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    griddep_launch_dependents();
+    griddep_wait();
     unsigned char* wbase = smem_raw + warp * C::WARP_BYTES;
     unsigned char* buf = wbase;
     double* xs = reinterpret_cast<double*>(wbase + C::BUF);
@@ -1252,6 +1285,8 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
 template <typename T>
 __global__ void k_apply_pick(double* __restrict__ H, const T* __restrict__ U, const uint32_t* __restrict__ pick,
                              uint64_t J, uint32_t R) {
+    griddep_launch_dependents();
+    griddep_wait();
     const uint64_t total = J * R;
     for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t d = e / R;
@@ -1264,6 +1299,24 @@ unsigned grid_for(uint64_t n, unsigned block) {
     return unsigned(std::min<uint64_t>((n + block - 1) / block, 148ull * 64));
 }
 
+// launch with programmatic stream serialization (PDL): the kernel may start
+// while the previous one drains; every kernel launched this way executes
+// griddep_wait() before it touches data the previous kernel produces
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int NB, int MODE, bool ROOT0>
 void launch_cta(const EvalArgs& a, unsigned grid, cudaStream_t s) {
     constexpr size_t smem = cta_nbuf<NB, ROOT0>() * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
@@ -1274,7 +1327,19 @@ void launch_cta(const EvalArgs& a, unsigned grid, cudaStream_t s) {
             configured = true;
         }
     }
-    k_eval_cta<NB, MODE, ROOT0><<<grid, CB, smem, s>>>(a);
+    // launched with programmatic stream serialization: overlaps the previous
+    // kernel's tail (k_eval_cta waits on griddepcontrol before reading its inputs)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(CB);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_eval_cta<NB, MODE, ROOT0>, a);
 }
 
 template <int NB, int MODE>
@@ -1356,7 +1421,7 @@ void launch_deep2(const DeepArgs& a, unsigned grid, cudaStream_t s) {
         cudaFuncSetAttribute(k_deep2<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         configured = true;
     }
-    k_deep2<NB, T><<<grid, WPB * 32, C::SMEM, s>>>(a);
+    launch_pdl(k_deep2<NB, T>, dim3(grid), dim3(WPB * 32), C::SMEM, s, a);
 }
 
 template <typename T>
@@ -1448,10 +1513,8 @@ int launch_position_grouped(const GroupedArgs& g) {
 
     // ---------------- stage 1: eigenvector tree (F = 1, Y = G_k) ----------------
     const Topo te = make_topo(R, 1);
-    k_stage_init<<<gs, 256, 0, g.stream>>>(g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed, g.draw_offset,
-                                            2ull * g.pos + 1, g.margin, g.pos == 0);
-    cudaMemsetAsync(g.cntL, 0, sizeof(uint32_t) * te.n, g.stream);
-    cudaMemsetAsync(g.cntR, 0, sizeof(uint32_t) * te.n, g.stream);
+    launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
+               g.draw_offset, 2ull * g.pos + 1, g.margin, int(g.pos == 0), g.cntL, g.cntR, uint64_t(te.n));
     ++launches;
     mark(13);
     e.GS = g.gstart;
@@ -1476,29 +1539,35 @@ int launch_position_grouped(const GroupedArgs& g) {
             ++launches;
             mark(8);
         }
+        uint32_t* nin = g.nsort_a;
+        uint32_t* nout = g.nsort_b;
         for (uint32_t l = 0; l < lcta; ++l) {
             e.perm = l == 0 ? nullptr : pin;
             e.perm_out = pout;
+            e.nsort_in = (l == 0 || !nin) ? nullptr : nin;
+            e.nsort_out = nout;
             dispatch_eval(R, (l == 0 && R <= 160) ? EV_LEVEL0 : EV_LEVEL, e, g.stream, false);
             ++launches;
             mark(9);
             std::swap(pin, pout);
+            std::swap(nin, nout);
         }
+        e.nsort_in = nullptr;
+        e.nsort_out = nullptr;
     };
     e.X = g.H;
     e.tree = g.Q;
     e.topo = te;
     cta_levels(te.d);
-    k_make_z<<<grid_for(J * R, 256), 256, 0, g.stream>>>(g.H, g.V, g.node, te, R, J, g.Zb);
+    launch_pdl(k_make_z, dim3(grid_for(J * R, 256)), dim3(256), 0, g.stream, (const double*)g.H, g.V,
+               (const uint32_t*)g.node, te, R, J, g.Zb);
     ++launches;
     mark(13);
 
     // ---------------- stage 2: factor tree, rank-1 M = z z^T ----------------
     const Topo tz = make_topo(g.I, R);
-    k_stage_init<<<gs, 256, 0, g.stream>>>(g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed, g.draw_offset,
-                                            2ull * g.pos + 2, g.margin, 0);
-    cudaMemsetAsync(g.cntL, 0, sizeof(uint32_t) * tz.n, g.stream);
-    cudaMemsetAsync(g.cntR, 0, sizeof(uint32_t) * tz.n, g.stream);
+    launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
+               g.draw_offset, 2ull * g.pos + 2, g.margin, 0, g.cntL, g.cntR, uint64_t(tz.n));
     ++launches;
     mark(13);
     e.X = g.Zb;
@@ -1534,9 +1603,11 @@ int launch_position_grouped(const GroupedArgs& g) {
             dispatch_deep<double>(R, da, grid, g.stream);
         mark(12);
         if (g.storage == 1)
-            k_apply_pick<float><<<grid_for(J * R, 256), 256, 0, g.stream>>>(g.H, static_cast<const float*>(g.U), g.rank, J, R);
+            launch_pdl(k_apply_pick<float>, dim3(grid_for(J * R, 256)), dim3(256), 0, g.stream, g.H,
+                       static_cast<const float*>(g.U), (const uint32_t*)g.rank, J, R);
         else
-            k_apply_pick<double><<<grid_for(J * R, 256), 256, 0, g.stream>>>(g.H, static_cast<const double*>(g.U), g.rank, J, R);
+            launch_pdl(k_apply_pick<double>, dim3(grid_for(J * R, 256)), dim3(256), 0, g.stream, g.H,
+                       static_cast<const double*>(g.U), (const uint32_t*)g.rank, J, R);
         launches += 2;
         mark(13);
         return launches;

@@ -163,6 +163,27 @@ struct krpg_sampler {
     bool use_grouped = true;  // level-synchronous DMMA descent where supported
     bool prof_detail = false;  // per-kernel-type timing marks inside the descent
     bool fused_deep = true;    // deep levels + leaf scan fused (descent_v2.cu k_deep)
+    uint32_t nslices = 1;      // KRPG_OPT_SLICES: concurrent draw slices of the grouped descent
+    std::vector<cudaStream_t> sstreams;
+    std::vector<cudaEvent_t> sevents;  // [0] fork, [s] join of slice s
+    cudaStream_t slice_stream(int sl) {
+        while (int(sstreams.size()) < sl) {
+            cudaStream_t x;
+            CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            sstreams.push_back(x);
+        }
+        return sstreams[sl - 1];
+    }
+    cudaEvent_t slice_event(int i) {
+        while (int(sevents.size()) <= i) {
+            cudaEvent_t x;
+            CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+            sevents.push_back(x);
+        }
+        return sevents[i];
+    }
+    cudaEvent_t fork_ev() { return slice_event(0); }
+    cudaEvent_t join_ev(int sl) { return slice_event(sl); }
     cudaEvent_t mark_prev = nullptr;
 
     // timing hook for the grouped descent: attributes the device time since the
@@ -448,7 +469,10 @@ struct krpg_sampler {
             uint64_t nmax = 2ull * R;
             for (uint32_t k : inc) nmax = std::max<uint64_t>(nmax, krpg::make_topo(f[k].I, R).n);
             const size_t Ju = size_t(J);
-            char* st = static_cast<char*>(gstate.ensure(Ju * (4 * 4 + 8 * 3) + nmax * 4 * 4 + 1024));
+            // draw slices on concurrent streams: the level kernels of one slice are
+            // latency bound, so a second independent slice fills the SMs' idle phases
+            const int S = (prof_on && prof_detail) ? 1 : int(std::max<uint64_t>(1, std::min<uint64_t>(nslices, J / 8192)));
+            char* st = static_cast<char*>(gstate.ensure(Ju * (4 * 6 + 8 * 3) + S * nmax * 4 * 4 + 1024 * (S + 3)));
             auto carve = [&](size_t bytes) {
                 char* p = st;
                 st += (bytes + 127) / 128 * 128;
@@ -459,13 +483,15 @@ struct krpg_sampler {
             g.perm_b = reinterpret_cast<uint32_t*>(carve(4 * Ju));
             g.node = reinterpret_cast<uint32_t*>(carve(4 * Ju));
             g.rank = reinterpret_cast<uint32_t*>(carve(4 * Ju));
+            g.nsort_a = reinterpret_cast<uint32_t*>(carve(4 * Ju));
+            g.nsort_b = reinterpret_cast<uint32_t*>(carve(4 * Ju));
             g.low = reinterpret_cast<double*>(carve(8 * Ju));
             g.invc = reinterpret_cast<double*>(carve(8 * Ju));
             g.ud = reinterpret_cast<double*>(carve(8 * Ju));
-            g.gstart = reinterpret_cast<uint32_t*>(carve(4 * nmax));
-            g.gend = reinterpret_cast<uint32_t*>(carve(4 * nmax));
-            g.cntL = reinterpret_cast<uint32_t*>(carve(4 * nmax));
-            g.cntR = reinterpret_cast<uint32_t*>(carve(4 * nmax));
+            g.gstart = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
+            g.gend = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
+            g.cntL = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
+            g.cntR = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
             g.Zb = static_cast<double*>(zbuf.ensure(sizeof(double) * J * R));
             g.R = R;
             g.N = N;
@@ -500,7 +526,38 @@ struct krpg_sampler {
                 g.Z = f[k].tree.as<double>();
                 g.U = f[k].U.p;
                 t0 = pbegin();
-                const int nl = krpg::launch_position_grouped(g);
+                int nl = 0;
+                if (S > 1) CK(cudaEventRecord(fork_ev(), stream));
+                for (int sl = 0; sl < S; ++sl) {
+                    const uint64_t s0 = J * uint64_t(sl) / S, s1 = J * uint64_t(sl + 1) / S;
+                    krpg::GroupedArgs gs = g;
+                    gs.J = s1 - s0;
+                    gs.draw_offset = off + s0;
+                    gs.H = H + s0 * R;
+                    gs.Zb = g.Zb + s0 * R;
+                    gs.idx = d_idx ? d_idx + s0 * N : nullptr;
+                    gs.margin = d_margin ? d_margin + s0 : nullptr;
+                    gs.perm_a = g.perm_a + s0;
+                    gs.perm_b = g.perm_b + s0;
+                    gs.node = g.node + s0;
+                    gs.rank = g.rank + s0;
+                    gs.nsort_a = g.nsort_a + s0;
+                    gs.nsort_b = g.nsort_b + s0;
+                    gs.low = g.low + s0;
+                    gs.invc = g.invc + s0;
+                    gs.ud = g.ud + s0;
+                    gs.gstart = g.gstart + sl * nmax;
+                    gs.gend = g.gend + sl * nmax;
+                    gs.cntL = g.cntL + sl * nmax;
+                    gs.cntR = g.cntR + sl * nmax;
+                    gs.stream = sl == 0 ? stream : slice_stream(sl);
+                    if (sl > 0) CK(cudaStreamWaitEvent(gs.stream, fork_ev(), 0));
+                    nl += krpg::launch_position_grouped(gs);
+                    if (sl > 0) {
+                        CK(cudaEventRecord(join_ev(sl), gs.stream));
+                        CK(cudaStreamWaitEvent(stream, join_ev(sl), 0));
+                    }
+                }
                 pend(KRPG_PROF_DRAWS, t0, nl);
             }
             CK(cudaEventRecord(up_ev[slot], stream));
@@ -838,6 +895,8 @@ int krpg_destroy(krpg_t h) {
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
+    for (cudaStream_t x : h->sstreams) cudaStreamDestroy(x);
+    for (cudaEvent_t x : h->sevents) cudaEventDestroy(x);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
     return KRPG_OK;
@@ -1222,7 +1281,10 @@ int krpg_set_option(krpg_t h, int option, int64_t value) {
             h->prof_detail = value != 0;
         else if (option == KRPG_OPT_FUSED_DEEP)
             h->fused_deep = value != 0;
-        else if (option == KRPG_OPT_ASYNC) {
+        else if (option == KRPG_OPT_SLICES) {
+            require(value >= 1 && value <= 8, "krpg_set_option: slices must be in [1, 8]");
+            h->nslices = uint32_t(value);
+        } else if (option == KRPG_OPT_ASYNC) {
             if (!value && h->async_mode) h->sync_check();
             h->async_mode = value != 0;
         }

@@ -72,6 +72,7 @@ struct GroupedArgs {
     const double* Z;     // factor tree compact
     const void* U;       // factor rows
     uint32_t *perm_a, *perm_b, *node, *rank, *gstart, *gend, *cntL, *cntR;
+    uint32_t *nsort_a, *nsort_b;  // node per sorted position (level kernels), nullable
     double *low, *invc, *ud;
     int* err;
     cudaStream_t stream;

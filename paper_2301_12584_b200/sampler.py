@@ -252,6 +252,10 @@ class KrpSampler:
         """Fused warp-local deep levels + leaf scan (default) or per-level global regrouping."""
         check(_lib.lib().krpg_set_option(self._h, _lib.OPT_FUSED_DEEP, 1 if on else 0))
 
+    def set_slices(self, n: int) -> None:
+        """Concurrent draw slices of the grouped descent (KRPG_OPT_SLICES, default 1)."""
+        check(_lib.lib().krpg_set_option(self._h, _lib.OPT_SLICES, int(n)))
+
     def set_async(self, on: bool) -> None:
         """KRPG_OPT_ASYNC: sample_device returns once enqueued (no host sync), so
         the next call's host setup overlaps this call's kernels; errors surface

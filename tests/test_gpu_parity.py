@@ -500,3 +500,19 @@ def test_sts_solve_matches_restatement(dims, R, storage):
     bb = s.sample(None, 3000, 7, margin=True)
     ri, rp, rr, rm = o.sample(None, 3000, 7, want_margin=True)
     assert_draws_match(bb, ri, rp, rr, rm)
+
+
+def test_descent_slices_give_identical_draws():
+    """KRPG_OPT_SLICES: the J draws split into slices on concurrent streams give the
+    same bits as one slice (the per-draw RNG stream is the global draw index)."""
+    fs = pareto_factors([(5000, 64), (3000, 64), (4097, 64)], 23)
+    s = K()(fs)
+    out = []
+    for n in (1, 2, 3):
+        s.set_slices(n)
+        b = s.sample(1, 30000, 77, margin=True)
+        out.append((b.indices, b.probabilities, b.rows))
+    s.set_slices(1)
+    for o in out[1:]:
+        for x, y in zip(o, out[0]):
+            assert np.array_equal(x, y)
