@@ -196,6 +196,27 @@ int krpg_sts_solve(krpg_t h, krpg_tensor_t T, uint32_t j, uint64_t J, uint64_t s
  * distinct sampled fibers, tensor entries visited by the scatter */
 int krpg_sts_last_stats(krpg_t h, uint64_t* stats);
 
+/* ---- standalone segment tree (SegmentTreeSampler, segment_tree_sampler.hpp:26-139) ----
+ * The tree over U (I x R, host, row-major) with leaf capacity F and a fixed PSD Y,
+ * rank-1 (y, R) or general (Y, R x R): give exactly one. Device build identical to
+ * the sampler's (compact layout). */
+typedef struct krpg_segtree* krpg_segtree_t;
+int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, const double* Y,
+                        const double* y, int device, krpg_segtree_t* out);
+int krpg_segtree_destroy(krpg_segtree_t t);
+int krpg_segtree_shape(krpg_segtree_t t, uint64_t* leaf_count, uint64_t* node_count);
+/* node_gram(node) (:79): stored nodes (root, left children) only */
+int krpg_segtree_node_gram(krpg_segtree_t t, uint64_t node, double* out /* R x R */);
+/* Batched row_sample (:258-293): draw d walks with history H[d] (J x R, host) and the
+ * uniform CounterRng(seed, stream0 + d) at `counter` (a fresh CounterRng's first
+ * uniform is counter 1). out: J row indices; margin (nullable): boundary margins. */
+int krpg_segtree_sample(krpg_segtree_t t, const double* H, uint64_t J, uint64_t seed, uint64_t stream0,
+                        uint64_t counter, uint64_t* out, double* margin);
+/* analytic_probabilities(h) (:310-323): q_{h,U,Y} for every row (out: I) */
+int krpg_segtree_probabilities(krpg_segtree_t t, const double* h, double* out);
+/* update_entry(r, c, value) (:358-409) */
+int krpg_segtree_update_entry(krpg_segtree_t t, uint64_t r, uint32_t c, double value);
+
 /* ---- row-partitioned construction (multi-GPU) ----
  * The tree over I rows splits into parts = 2^g subtrees (the nodes of level g);
  * subtree `part` covers the contiguous rows krpg_partition_rows(...). A rank that

@@ -7,10 +7,11 @@ mirror of the reference's KrpSampler API for tests and benchmarks.
 """
 from ._lib import (EXCLUDED, KrpgCudaError, KrpgError, KrpgInvalidArgument, build, lib)
 from .sampler import ConditionalDistribution, KrpSampler, RowOrder, SampleBatch, device_count
+from .segtree import SegmentTreeSampler
 from .tensor import SparseTensor
 
 __all__ = [
     "EXCLUDED", "KrpgCudaError", "KrpgError", "KrpgInvalidArgument", "build", "lib",
     "ConditionalDistribution", "KrpSampler", "RowOrder", "SampleBatch", "device_count",
-    "SparseTensor",
+    "SparseTensor", "SegmentTreeSampler",
 ]

@@ -92,6 +92,13 @@ _SIGS = {
     "krpg_tensor_entries": ([_vp, C.POINTER(_u32), _dp], _int),
     "krpg_sts_solve": ([_vp, _vp, _u32, _u64, _u64, _dp], _int),
     "krpg_sts_last_stats": ([_vp, C.POINTER(_u64)], _int),
+    "krpg_segtree_create": ([_dp, _u64, _u32, _u64, _dp, _dp, _int, C.POINTER(_vp)], _int),
+    "krpg_segtree_destroy": ([_vp], _int),
+    "krpg_segtree_shape": ([_vp, C.POINTER(_u64), C.POINTER(_u64)], _int),
+    "krpg_segtree_node_gram": ([_vp, _u64, _dp], _int),
+    "krpg_segtree_sample": ([_vp, _dp, _u64, _u64, _u64, _u64, C.POINTER(_u64), _dp], _int),
+    "krpg_segtree_probabilities": ([_vp, _dp, _dp], _int),
+    "krpg_segtree_update_entry": ([_vp, _u64, _u32, C.c_double], _int),
 }
 OPT_GROUPED_DESCENT = 1
 

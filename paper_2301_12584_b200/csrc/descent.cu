@@ -107,14 +107,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
     const T* U = static_cast<const T*>(a.U);
     const uint64_t key = rng_key(a.seed, a.draw_offset + d);
 
+    constexpr bool STANDALONE = MODE >= 2;  // SegmentTreeSampler::row_sample on a single tree
     double hr[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         const uint32_t b = lane + 32u * s;
-        hr[s] = b < R ? (a.pos == 0 ? 1.0 : a.H[d * R + b]) : 0.0;
+        hr[s] = b < R ? ((a.pos == 0 && !STANDALONE) ? 1.0 : a.H[d * R + b]) : 0.0;
     }
-    double margin = (a.pos == 0 || !a.margin) ? HUGE_VAL : a.margin[d];
-    const Topo tz = make_topo(a.I, R);
+    double margin = (a.pos == 0 || STANDALONE || !a.margin) ? HUGE_VAL : a.margin[d];
+    const Topo tz = make_topo(a.I, a.F ? a.F : R);
 
     double zr[S];
     double inv_c, low, u;
@@ -149,6 +150,31 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
             if (lane == 0) atomicExch(a.err, 1);
             return;
         }
+    } else if (MODE == 2) {
+        // ---- rank-1 Y = y y^T: z = h o y, M = z z^T (fold_weights :197-204) ----
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const uint32_t b = lane + 32u * s;
+            zr[s] = b < R ? hr[s] * __ldg(a.yv + b) : 0.0;
+            if (b < R) xs[b] = zr[s];
+        }
+        __syncwarp();
+        u = rng_uniform(key, a.counter);
+        if (!walk<S, false>(a.Z, nullptr, tz, P, xs, zr, R, lane, u, inv_c, low, node, margin)) {
+            if (lane == 0) atomicExch(a.err, 1);
+            return;
+        }
+    } else if (MODE == 3) {
+        // ---- general Y: M = hh^T o Y ----
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (lane + 32 * s < int(R)) xs[lane + 32 * s] = hr[s];
+        __syncwarp();
+        u = rng_uniform(key, a.counter);
+        if (!walk<S, true>(a.Z, a.Y, tz, P, xs, hr, R, lane, u, inv_c, low, node, margin)) {
+            if (lane == 0) atomicExch(a.err, 1);
+            return;
+        }
     } else {
         // ---- one-stage: M = hh^T o G_{>k} on the factor tree directly ----
 #pragma unroll
@@ -171,7 +197,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
     }
     double cum = low;
     uint64_t pick = ~uint64_t{0}, last_nz = ~uint64_t{0};
-    if (MODE == 0) {
+    if (MODE == 0 || MODE == 2) {
         // rank-1 leaf masses (U[i,:] . z)^2, 8 rows per batch: loads of the whole
         // batch are in flight together, then the sequential scan (:284-291).
         constexpr int LB = 8;
@@ -203,7 +229,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
             }
         }
     }
-    for (uint64_t i = first; MODE == 1 && i < last; ++i) {
+    for (uint64_t i = first; (MODE == 1 || MODE == 3) && i < last; ++i) {
         double mass;
         {
             // general leaf mass: (h o r)^T G_{>k} (h o r), packed
@@ -229,6 +255,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
     }
     if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : last - 1;
 
+    if (STANDALONE) {
+        if (lane == 0) {
+            a.idx64[d] = pick;
+            if (a.margin) a.margin[d] = margin;
+        }
+        return;
+    }
     // ---- outputs: index, h *= U_k[pick] (:136-138) ----
     if (a.idx && lane == 0) a.idx[d * a.N + a.k] = static_cast<uint32_t>(pick);
 #pragma unroll
@@ -239,14 +272,80 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
     if (a.margin && lane == 0) a.margin[d] = margin;
 }
 
+// q_{h,U,Y}[i] numerators for every row (SegmentTreeSampler::analytic_probabilities,
+// segment_tree_sampler.cpp:310-323): one warp per row; rank-1 (U_i . (h o y))^2, or
+// (h o U_i)^T Y (h o U_i) for general Y (packed); row 0 of `out` ... I-1, and
+// out[I] = the normaliser C (root Gram).
+template <int S>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_segtree_masses(const double* __restrict__ U, uint64_t I, uint32_t R, const double* __restrict__ h,
+                     const double* __restrict__ yv, const double* __restrict__ Y, const double* __restrict__ root,
+                     double* __restrict__ out) {
+    extern __shared__ double xs_all[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* xs = xs_all + warp * R;
+    const uint64_t nw = uint64_t(gridDim.x) * kWarpsPerBlock;
+    for (uint64_t i = uint64_t(blockIdx.x) * kWarpsPerBlock + warp; i <= I; i += nw) {
+        double xr[S];
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const uint32_t b = lane + 32u * s;
+            double x = 0.0;
+            if (b < R) {
+                if (i == I)
+                    x = yv ? h[b] * yv[b] : h[b];  // normaliser: x = z (rank-1) or h (general)
+                else
+                    x = yv ? U[i * R + b] * h[b] * yv[b] : h[b] * U[i * R + b];
+            }
+            xr[s] = x;
+            if (b < R) xs[b] = x;
+        }
+        __syncwarp();
+        double m;
+        if (i == I) {
+            m = yv ? packed_qf<S, false>(root, nullptr, xs, xr, R, lane) : packed_qf<S, true>(root, Y, xs, xr, R, lane);
+        } else if (yv) {
+            double p = 0.0;
+#pragma unroll
+            for (int s = 0; s < S; ++s) p += xr[s];
+            p = warp_sum(p);
+            m = p * p;
+        } else {
+            m = packed_qf<S, false>(Y, nullptr, xs, xr, R, lane);
+        }
+        if (lane == 0) out[i] = m;
+    }
+}
+
+void launch_segtree_masses_s(const double* U, uint64_t I, uint32_t R, const double* h, const double* yv,
+                             const double* Y, const double* root, double* out, cudaStream_t s) {
+    const unsigned grid = unsigned(std::min<uint64_t>((I + 1 + kWarpsPerBlock - 1) / kWarpsPerBlock, 148ull * 16));
+    const size_t smem = size_t(kWarpsPerBlock) * R * sizeof(double);
+    switch ((R + 31) / 32) {
+        case 1: k_segtree_masses<1><<<grid, kWarpsPerBlock * 32, smem, s>>>(U, I, R, h, yv, Y, root, out); break;
+        case 2: k_segtree_masses<2><<<grid, kWarpsPerBlock * 32, smem, s>>>(U, I, R, h, yv, Y, root, out); break;
+        case 3: k_segtree_masses<3><<<grid, kWarpsPerBlock * 32, smem, s>>>(U, I, R, h, yv, Y, root, out); break;
+        case 4: k_segtree_masses<4><<<grid, kWarpsPerBlock * 32, smem, s>>>(U, I, R, h, yv, Y, root, out); break;
+        case 5: k_segtree_masses<5><<<grid, kWarpsPerBlock * 32, smem, s>>>(U, I, R, h, yv, Y, root, out); break;
+        case 6: k_segtree_masses<6><<<grid, kWarpsPerBlock * 32, smem, s>>>(U, I, R, h, yv, Y, root, out); break;
+        case 7: k_segtree_masses<7><<<grid, kWarpsPerBlock * 32, smem, s>>>(U, I, R, h, yv, Y, root, out); break;
+        default: k_segtree_masses<8><<<grid, kWarpsPerBlock * 32, smem, s>>>(U, I, R, h, yv, Y, root, out); break;
+    }
+}
+
 template <int S, typename T>
 void launch_draws_t(const DrawArgs& a) {
     const unsigned grid = unsigned((a.J + kWarpsPerBlock - 1) / kWarpsPerBlock);
     const size_t smem = size_t(kWarpsPerBlock) * a.R * sizeof(double);
     if (a.mode == 0)
         k_draws<S, T, 0><<<grid, kWarpsPerBlock * 32, smem, a.stream>>>(a);
-    else
+    else if (a.mode == 1)
         k_draws<S, T, 1><<<grid, kWarpsPerBlock * 32, smem, a.stream>>>(a);
+    else if (a.mode == 2)
+        k_draws<S, T, 2><<<grid, kWarpsPerBlock * 32, smem, a.stream>>>(a);
+    else
+        k_draws<S, T, 3><<<grid, kWarpsPerBlock * 32, smem, a.stream>>>(a);
 }
 
 template <typename T>
@@ -422,6 +521,11 @@ unsigned grid_for(uint64_t n, unsigned block) {
 }
 
 }  // namespace
+
+void launch_segtree_masses(const double* U, uint64_t I, uint32_t R, const double* h, const double* yv,
+                           const double* Y, const double* root, double* out, cudaStream_t s) {
+    launch_segtree_masses_s(U, I, R, h, yv, Y, root, out, s);
+}
 
 void launch_draws(const DrawArgs& a) {
     if (a.storage == 1)

@@ -697,9 +697,210 @@ void krpg_sampler::sts_solve(krpg_tensor& T, uint32_t j, uint64_t J, uint64_t se
     if (sigma_out) std::copy(sg.begin(), sg.end(), sigma_out);
 }
 
+// Device SegmentTreeSampler (segment_tree_sampler.hpp:26-139): a standalone tree over
+// U (I x R) with leaf capacity F and a fixed PSD Y (rank-1 y y^T or general).
+struct krpg_segtree {
+    int device = 0;
+    uint64_t I = 0, F = 0;
+    uint32_t R = 0;
+    bool rank1 = true;
+    DevBuf U, tree, tbuf, yv, Yp, err, scratch;
+    std::vector<double> y_host, Y_host;  // as given (validation / introspection)
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    uint64_t P() const { return uint64_t(R) * (R + 1) / 2; }
+    void build() {
+        const krpg::Topo t = krpg::make_topo(I, F);
+        tree.ensure(sizeof(double) * t.L * P());
+        uint64_t na, nb;
+        krpg::tree_transient_doubles(I, R, &na, &nb, F);
+        double* base = static_cast<double*>(tbuf.ensure(sizeof(double) * (na + nb) + 16));
+        krpg::TreeBuildArgs a{};
+        a.U = U.p;
+        a.storage = KRPG_STORE_F64;
+        a.I = I;
+        a.R = R;
+        a.F = F;
+        a.compact = tree.as<double>();
+        a.tbuf_a = base;
+        a.tbuf_b = base + na;
+        a.stream = stream;
+        krpg::launch_tree_leaves(a);
+        if (krpg::launch_tree_levels(a) < 0) throw CudaError("segment tree: level build failed");
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(stream));
+    }
+    ~krpg_segtree() {
+        for (DevBuf* b : {&U, &tree, &tbuf, &yv, &Yp, &err, &scratch}) b->release();
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
 extern "C" {
 
 const char* krpg_last_error(void) { return g_err.c_str(); }
+
+int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, const double* Y, const double* y,
+                        int device, krpg_segtree_t* out) {
+    return guard([&] {
+        *out = nullptr;
+        require(I >= 1 && R >= 1, "SegmentTreeSampler: empty matrix");
+        require(F >= 1, "SegmentTreeSampler: leaf capacity must be positive");
+        require(R <= 256, "krpg: rank above 256 is not supported on device");
+        require((Y != nullptr) != (y != nullptr), "SegmentTreeSampler: give exactly one of Y (R x R) or y (R)");
+        for (uint64_t e = 0; e < I * R; ++e) require(std::isfinite(U[e]), "SegmentTreeSampler: non-finite entries");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, "krpg: no such CUDA device");
+        auto t = std::make_unique<krpg_segtree>();
+        t->device = device;
+        t->I = I;
+        t->R = R;
+        t->F = F;
+        t->rank1 = y != nullptr;
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+        CK(cudaMemcpyAsync(t->U.ensure(8 * I * R), U, 8 * I * R, cudaMemcpyHostToDevice, t->stream));
+        if (y) {
+            t->y_host.assign(y, y + R);
+            for (double v : t->y_host) require(std::isfinite(v), "SegmentTreeSampler: non-finite y");
+            CK(cudaMemcpyAsync(t->yv.ensure(8 * R), t->y_host.data(), 8 * R, cudaMemcpyHostToDevice, t->stream));
+        } else {
+            t->Y_host.assign(Y, Y + size_t(R) * R);
+            for (double v : t->Y_host) require(std::isfinite(v), "SegmentTreeSampler: non-finite Y");
+            const std::vector<double> yp = krpg::pack_upper(Y, R);
+            CK(cudaMemcpyAsync(t->Yp.ensure(8 * yp.size()), yp.data(), 8 * yp.size(), cudaMemcpyHostToDevice,
+                               t->stream));
+            CK(cudaStreamSynchronize(t->stream));
+        }
+        t->build();
+        *out = t.release();
+    });
+}
+
+int krpg_segtree_destroy(krpg_segtree_t t) {
+    return guard([&] {
+        if (!t) return;
+        cudaSetDevice(t->device);
+        delete t;
+    });
+}
+
+int krpg_segtree_shape(krpg_segtree_t t, uint64_t* leaf_count, uint64_t* node_count) {
+    return guard([&] {
+        require(t, "krpg: null tree");
+        const krpg::Topo tp = krpg::make_topo(t->I, t->F);
+        *leaf_count = tp.L;
+        *node_count = tp.n;
+    });
+}
+
+int krpg_segtree_node_gram(krpg_segtree_t t, uint64_t node, double* out) {
+    return guard([&] {
+        require(t, "krpg: null tree");
+        const krpg::Topo tp = krpg::make_topo(t->I, t->F);
+        require(node < tp.n, "node_gram: node out of range");
+        require(node == 0 || (node & 1), "node_gram: Gram of this node is not stored (compact layout)");
+        std::lock_guard<std::mutex> lk(t->mu);
+        CK(cudaSetDevice(t->device));
+        const uint64_t slot = node == 0 ? 0 : (node + 1) / 2;
+        std::vector<double> g(t->P());
+        CK(cudaMemcpy(g.data(), t->tree.as<double>() + slot * t->P(), 8 * t->P(), cudaMemcpyDeviceToHost));
+        krpg::unpack_upper(g.data(), t->R, out);
+    });
+}
+
+int krpg_segtree_sample(krpg_segtree_t t, const double* H, uint64_t J, uint64_t seed, uint64_t stream0,
+                        uint64_t counter, uint64_t* out, double* margin) {
+    return guard([&] {
+        require(t, "krpg: null tree");
+        require(J >= 1, "row_sample: count must be positive");
+        for (uint64_t e = 0; e < J * t->R; ++e) require(std::isfinite(H[e]), "row_sample: non-finite h");
+        std::lock_guard<std::mutex> lk(t->mu);
+        CK(cudaSetDevice(t->device));
+        char* w = static_cast<char*>(t->scratch.ensure(8 * J * t->R + 8 * J + 8 * J + 256));
+        double* dH = reinterpret_cast<double*>(w);
+        uint64_t* dout = reinterpret_cast<uint64_t*>(w + 8 * J * t->R);
+        double* dm = reinterpret_cast<double*>(w + 8 * J * t->R + 8 * J);
+        int* derr = static_cast<int*>(t->err.ensure(sizeof(int)));
+        CK(cudaMemsetAsync(derr, 0, sizeof(int), t->stream));
+        CK(cudaMemcpyAsync(dH, H, 8 * J * t->R, cudaMemcpyHostToDevice, t->stream));
+        krpg::DrawArgs a{};
+        a.R = t->R;
+        a.N = 1;
+        a.mode = t->rank1 ? 2 : 3;
+        a.J = J;
+        a.seed = seed;
+        a.draw_offset = stream0;
+        a.H = dH;
+        a.margin = margin ? dm : nullptr;
+        a.Y = t->rank1 ? nullptr : t->Yp.as<double>();
+        a.yv = t->rank1 ? t->yv.as<double>() : nullptr;
+        a.Z = t->tree.as<double>();
+        a.U = t->U.p;
+        a.storage = KRPG_STORE_F64;
+        a.I = t->I;
+        a.F = t->F;
+        a.counter = counter;
+        a.idx64 = dout;
+        a.err = derr;
+        a.stream = t->stream;
+        krpg::launch_draws(a);
+        CK(cudaGetLastError());
+        int eh = 0;
+        CK(cudaMemcpyAsync(out, dout, 8 * J, cudaMemcpyDeviceToHost, t->stream));
+        if (margin) CK(cudaMemcpyAsync(margin, dm, 8 * J, cudaMemcpyDeviceToHost, t->stream));
+        CK(cudaMemcpyAsync(&eh, derr, sizeof(int), cudaMemcpyDeviceToHost, t->stream));
+        CK(cudaStreamSynchronize(t->stream));
+        if (eh) throw std::runtime_error("row_sample: degenerate distribution (C <= 0)");
+    });
+}
+
+int krpg_segtree_probabilities(krpg_segtree_t t, const double* h, double* out) {
+    return guard([&] {
+        require(t, "krpg: null tree");
+        std::lock_guard<std::mutex> lk(t->mu);
+        CK(cudaSetDevice(t->device));
+        char* w = static_cast<char*>(t->scratch.ensure(8 * t->R + 8 * (t->I + 1) + 256));
+        double* dh = reinterpret_cast<double*>(w);
+        double* dout = dh + t->R;
+        CK(cudaMemcpyAsync(dh, h, 8 * t->R, cudaMemcpyHostToDevice, t->stream));
+        krpg::launch_segtree_masses(t->U.as<double>(), t->I, t->R, dh, t->rank1 ? t->yv.as<double>() : nullptr,
+                                    t->rank1 ? nullptr : t->Yp.as<double>(), t->tree.as<double>(), dout, t->stream);
+        std::vector<double> m(t->I + 1);
+        CK(cudaMemcpyAsync(m.data(), dout, 8 * m.size(), cudaMemcpyDeviceToHost, t->stream));
+        CK(cudaStreamSynchronize(t->stream));
+        const double C = m[t->I];
+        if (!std::isfinite(C) || C <= 0.0) throw std::runtime_error("row_sample: degenerate distribution (C <= 0)");
+        for (uint64_t i = 0; i < t->I; ++i) out[i] = m[i] / C;
+    });
+}
+
+int krpg_segtree_update_entry(krpg_segtree_t t, uint64_t r, uint32_t c, double value) {
+    return guard([&] {
+        require(t, "krpg: null tree");
+        require(r < t->I && c < t->R, "update_entry: entry out of range");
+        require(std::isfinite(value), "update_entry: non-finite value");
+        std::lock_guard<std::mutex> lk(t->mu);
+        CK(cudaSetDevice(t->device));
+        const uint32_t R = t->R;
+        std::vector<double> oldr(R), newr;
+        CK(cudaMemcpy(oldr.data(), t->U.as<double>() + r * R, 8 * R, cudaMemcpyDeviceToHost));
+        newr = oldr;
+        newr[c] = value;
+        char* w = static_cast<char*>(t->scratch.ensure(8 * 2 * R + 64));
+        double* d_old = reinterpret_cast<double*>(w);
+        double* d_new = d_old + R;
+        uint64_t* d_row = reinterpret_cast<uint64_t*>(d_new + R);
+        CK(cudaMemcpyAsync(d_old, oldr.data(), 8 * R, cudaMemcpyHostToDevice, t->stream));
+        CK(cudaMemcpyAsync(d_new, newr.data(), 8 * R, cudaMemcpyHostToDevice, t->stream));
+        CK(cudaMemcpyAsync(d_row, &r, 8, cudaMemcpyHostToDevice, t->stream));
+        krpg::launch_row_deltas(t->tree.as<double>(), t->I, R, t->F, 1, d_row, d_old, d_new, t->stream);
+        CK(cudaMemcpyAsync(t->U.as<double>() + r * R + c, &value, 8, cudaMemcpyHostToDevice, t->stream));
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(t->stream));
+    });
+}
 
 int krpg_tensor_create(const uint64_t* dims, uint32_t N, const uint32_t* coords, const double* values, uint64_t nnz,
                        int device, krpg_tensor_t* out) {
@@ -1180,7 +1381,7 @@ int krpg_update_entries(krpg_t h, uint32_t j, const uint64_t* r, const uint32_t*
         }
         CK(cudaMemcpyAsync(dnew, newh.data(), rb, cudaMemcpyHostToDevice, h->stream));
         cudaEvent_t t0 = h->pbegin();
-        krpg::launch_row_deltas(h->f[j].tree.as<double>(), h->f[j].I, R, nr, drows, dold, dnew, h->stream);
+        krpg::launch_row_deltas(h->f[j].tree.as<double>(), h->f[j].I, R, 0, nr, drows, dold, dnew, h->stream);
         krpg::launch_scatter_rows(h->f[j].U.p, h->storage, R, nr, drows, dnew, h->stream);
         h->pend(KRPG_PROF_UPDATE, t0, 2);
         h->prof_launches[KRPG_PROF_OTHER] += 1;  // gather of the old rows

@@ -19,12 +19,13 @@ struct TreeBuildArgs {
     double* tbuf_b;
     cudaStream_t stream;
     int force_generic;   // test hook: use the scalar kernel
+    uint64_t F = 0;      // leaf capacity (0: F = R, the KrpSampler trees)
     uint32_t parts = 1;  // > 1: build only subtree `part` of `parts` (a power of two)
     uint32_t part = 0;
     double* subroot = nullptr;  // partitioned build: receives the subtree root Gram (P)
 };
 // doubles needed for (tbuf_a, tbuf_b)
-void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b);
+void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b, uint64_t F = 0);
 // leaf / first-pair level (DMMA) then the remaining levels; returns #launches (< 0: CUDA error)
 int launch_tree_leaves(const TreeBuildArgs& a);
 int launch_tree_levels(const TreeBuildArgs& a);
@@ -42,7 +43,8 @@ void launch_etree_build(const double* V, const double* lam, const double* gk_pac
 
 // ---- batched draws ----
 struct DrawArgs {
-    uint32_t R, N, k, pos, mode;  // mode 0 two-stage, 1 one-stage
+    uint32_t R, N, k, pos, mode;  // mode 0 two-stage, 1 one-stage; standalone segment tree
+                                  // (SegmentTreeSampler::row_sample): 2 rank-1 y, 3 general Y
     uint64_t J, seed, draw_offset;
     double* H;          // J x R running Hadamard history (also the output rows)
     uint32_t* idx;      // J x N or null
@@ -56,8 +58,16 @@ struct DrawArgs {
     uint64_t I;         // rows of factor k
     int* err;           // device error flag
     cudaStream_t stream;
+    // modes 2 / 3: leaf capacity, the uniform's counter, rank-1 y, index output
+    uint64_t F = 0;
+    uint64_t counter = 1;
+    const double* yv = nullptr;
+    uint64_t* idx64 = nullptr;
 };
 void launch_draws(const DrawArgs& a);
+// SegmentTreeSampler::analytic_probabilities numerators (out[0..I)) and normaliser (out[I])
+void launch_segtree_masses(const double* U, uint64_t I, uint32_t R, const double* h, const double* yv,
+                           const double* Y, const double* root, double* out, cudaStream_t s);
 
 // ---- grouped (level-synchronous, DMMA) two-stage descent, descent_v2.cu ----
 struct GroupedArgs {
@@ -107,7 +117,7 @@ void launch_conditional_probs(const void* U, uint32_t storage, uint64_t I, uint3
 
 // ---- updates (segment_tree_sampler.cpp:358-409) ----
 // for each touched row: patch u'u'^T - uu^T into every stored node on its path
-void launch_row_deltas(double* compact, uint64_t I, uint32_t R, uint64_t nrows,
+void launch_row_deltas(double* compact, uint64_t I, uint32_t R, uint64_t F, uint64_t nrows,
                        const uint64_t* rows, const double* old_rows, const double* new_rows,
                        cudaStream_t s);
 void launch_scatter_rows(void* U, uint32_t storage, uint32_t R, uint64_t nrows,

@@ -45,11 +45,12 @@ __host__ __device__ __forceinline__ void pos_rows(const PosGeom& g, uint64_t j, 
     }
 }
 
-PosGeom make_geom(uint64_t I, uint32_t R) {
-    const Topo t = make_topo(I, R);
+PosGeom make_geom(uint64_t I, uint32_t R, uint64_t F = 0) {
+    if (!F) F = R;
+    const Topo t = make_topo(I, F);
     PosGeom g;
     g.I = I;
-    g.F = R;
+    g.F = F;
     g.R = R;
     g.P = R * (R + 1) / 2;
     const uint32_t D = t.d ? t.d - 1 : 0;
@@ -492,6 +493,7 @@ void launch_big(const T* U, const PosGeom& g, double* compact, double* tout, cud
 template <typename T>
 void launch_leaf(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s,
                  bool generic) {
+    if (g.F % 8 != 0) generic = true;  // the DMMA kernels stream leaves in 8-row chunks
     if (!generic) {
         switch (g.R) {
             case 96: return launch_big<96, T>(U, g, compact, tout, s);
@@ -529,14 +531,14 @@ void tree_partition_rows(uint64_t I, uint32_t R, uint32_t parts, uint32_t part, 
     *last = r1;
 }
 
-void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b) {
-    const PosGeom g = make_geom(I, R);
+void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b, uint64_t F) {
+    const PosGeom g = make_geom(I, R, F);
     *a = g.npos > 1 ? g.npos * g.P : 0;
     *b = g.npos > 2 ? (g.npos / 2) * g.P : 0;
 }
 
 int launch_tree_leaves(const TreeBuildArgs& a) {
-    PosGeom g = make_geom(a.I, a.R);
+    PosGeom g = make_geom(a.I, a.R, a.F);
     if (a.parts > 1) {  // one partition's subtree: positions [part, part+1) * npos / parts
         const uint64_t span = g.npos / a.parts;
         g.p0 = uint64_t(a.part) * span;
@@ -554,7 +556,7 @@ int launch_tree_leaves(const TreeBuildArgs& a) {
 // root. One partition (parts = 2^gl > 1): only the partition's own nodes on
 // levels D-1 .. gl, and its subtree root Gram (level gl) is copied to a.subroot.
 int launch_tree_levels(const TreeBuildArgs& a) {
-    const PosGeom g = make_geom(a.I, a.R);
+    const PosGeom g = make_geom(a.I, a.R, a.F);
     uint32_t D = 0;
     while ((uint64_t{1} << D) < g.npos) ++D;
     uint32_t gl = 0;
@@ -584,7 +586,7 @@ int launch_tree_levels(const TreeBuildArgs& a) {
 // Top of a partitioned build: the parts = 2^gl subtree roots (parts x P, in
 // subtree order) are level gl; stores the stored ones and reduces to the root.
 int launch_tree_top(const TreeBuildArgs& a, const double* subroots) {
-    const PosGeom g = make_geom(a.I, a.R);
+    const PosGeom g = make_geom(a.I, a.R, a.F);
     uint32_t gl = 0;
     while ((1u << gl) < a.parts) ++gl;
     int launches = 0;
