@@ -212,6 +212,10 @@ int krpg_segtree_node_gram(krpg_segtree_t t, uint64_t node, double* out /* R x R
  * uniform is counter 1). out: J row indices; margin (nullable): boundary margins. */
 int krpg_segtree_sample(krpg_segtree_t t, const double* H, uint64_t J, uint64_t seed, uint64_t stream0,
                         uint64_t counter, uint64_t* out, double* margin);
+/* Same with a CounterRng key and counter per draw (keys = the generator's mixed
+ * stream key, rng.hpp:16-18) -- what the C++ drop-in's row_sample(h, rng) uses. */
+int krpg_segtree_sample_keyed(krpg_segtree_t t, const double* H, uint64_t J, const uint64_t* keys,
+                              const uint64_t* counters, uint64_t* out, double* margin);
 /* analytic_probabilities(h) (:310-323): q_{h,U,Y} for every row (out: I) */
 int krpg_segtree_probabilities(krpg_segtree_t t, const double* h, double* out);
 /* update_entry(r, c, value) (:358-409) */

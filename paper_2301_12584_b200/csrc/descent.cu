@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
     const uint64_t P = uint64_t(R) * (R + 1) / 2;
     double* xs = xs_all + warp * R;
     const T* U = static_cast<const T*>(a.U);
-    const uint64_t key = rng_key(a.seed, a.draw_offset + d);
+    const uint64_t key = a.keys ? a.keys[d] : rng_key(a.seed, a.draw_offset + d);
 
     constexpr bool STANDALONE = MODE >= 2;  // SegmentTreeSampler::row_sample on a single tree
     double hr[S];
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
             if (b < R) xs[b] = zr[s];
         }
         __syncwarp();
-        u = rng_uniform(key, a.counter);
+        u = rng_uniform(key, a.counters ? a.counters[d] : a.counter);
         if (!walk<S, false>(a.Z, nullptr, tz, P, xs, zr, R, lane, u, inv_c, low, node, margin)) {
             if (lane == 0) atomicExch(a.err, 1);
             return;
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
         for (int s = 0; s < S; ++s)
             if (lane + 32 * s < int(R)) xs[lane + 32 * s] = hr[s];
         __syncwarp();
-        u = rng_uniform(key, a.counter);
+        u = rng_uniform(key, a.counters ? a.counters[d] : a.counter);
         if (!walk<S, true>(a.Z, a.Y, tz, P, xs, hr, R, lane, u, inv_c, low, node, margin)) {
             if (lane == 0) atomicExch(a.err, 1);
             return;

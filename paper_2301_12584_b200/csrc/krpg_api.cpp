@@ -810,18 +810,42 @@ int krpg_segtree_node_gram(krpg_segtree_t t, uint64_t node, double* out) {
     });
 }
 
+static void segtree_sample_impl(krpg_segtree_t t, const double* H, uint64_t J, uint64_t seed, uint64_t stream0,
+                                uint64_t counter, const uint64_t* keys, const uint64_t* counters, uint64_t* out,
+                                double* margin);
+
 int krpg_segtree_sample(krpg_segtree_t t, const double* H, uint64_t J, uint64_t seed, uint64_t stream0,
                         uint64_t counter, uint64_t* out, double* margin) {
+    return guard([&] { segtree_sample_impl(t, H, J, seed, stream0, counter, nullptr, nullptr, out, margin); });
+}
+
+int krpg_segtree_sample_keyed(krpg_segtree_t t, const double* H, uint64_t J, const uint64_t* keys,
+                              const uint64_t* counters, uint64_t* out, double* margin) {
     return guard([&] {
+        require(keys && counters, "row_sample: null keys / counters");
+        segtree_sample_impl(t, H, J, 0, 0, 0, keys, counters, out, margin);
+    });
+}
+
+static void segtree_sample_impl(krpg_segtree_t t, const double* H, uint64_t J, uint64_t seed, uint64_t stream0,
+                                uint64_t counter, const uint64_t* keys, const uint64_t* counters, uint64_t* out,
+                                double* margin) {
+    {
         require(t, "krpg: null tree");
         require(J >= 1, "row_sample: count must be positive");
         for (uint64_t e = 0; e < J * t->R; ++e) require(std::isfinite(H[e]), "row_sample: non-finite h");
         std::lock_guard<std::mutex> lk(t->mu);
         CK(cudaSetDevice(t->device));
-        char* w = static_cast<char*>(t->scratch.ensure(8 * J * t->R + 8 * J + 8 * J + 256));
+        char* w = static_cast<char*>(t->scratch.ensure(8 * J * t->R + 8 * J * 4 + 256));
         double* dH = reinterpret_cast<double*>(w);
         uint64_t* dout = reinterpret_cast<uint64_t*>(w + 8 * J * t->R);
         double* dm = reinterpret_cast<double*>(w + 8 * J * t->R + 8 * J);
+        uint64_t* dkeys = reinterpret_cast<uint64_t*>(w + 8 * J * t->R + 16 * J);
+        uint64_t* dctr = dkeys + J;
+        if (keys) {
+            CK(cudaMemcpyAsync(dkeys, keys, 8 * J, cudaMemcpyHostToDevice, t->stream));
+            CK(cudaMemcpyAsync(dctr, counters, 8 * J, cudaMemcpyHostToDevice, t->stream));
+        }
         int* derr = static_cast<int*>(t->err.ensure(sizeof(int)));
         CK(cudaMemsetAsync(derr, 0, sizeof(int), t->stream));
         CK(cudaMemcpyAsync(dH, H, 8 * J * t->R, cudaMemcpyHostToDevice, t->stream));
@@ -842,6 +866,8 @@ int krpg_segtree_sample(krpg_segtree_t t, const double* H, uint64_t J, uint64_t 
         a.I = t->I;
         a.F = t->F;
         a.counter = counter;
+        a.keys = keys ? dkeys : nullptr;
+        a.counters = keys ? dctr : nullptr;
         a.idx64 = dout;
         a.err = derr;
         a.stream = t->stream;
@@ -853,7 +879,7 @@ int krpg_segtree_sample(krpg_segtree_t t, const double* H, uint64_t J, uint64_t 
         CK(cudaMemcpyAsync(&eh, derr, sizeof(int), cudaMemcpyDeviceToHost, t->stream));
         CK(cudaStreamSynchronize(t->stream));
         if (eh) throw std::runtime_error("row_sample: degenerate distribution (C <= 0)");
-    });
+    }
 }
 
 int krpg_segtree_probabilities(krpg_segtree_t t, const double* h, double* out) {

@@ -63,6 +63,8 @@ struct DrawArgs {
     uint64_t counter = 1;
     const double* yv = nullptr;
     uint64_t* idx64 = nullptr;
+    const uint64_t* keys = nullptr;      // per-draw CounterRng keys (nullable: derive from seed)
+    const uint64_t* counters = nullptr;  // per-draw counters (nullable: `counter`)
 };
 void launch_draws(const DrawArgs& a);
 // SegmentTreeSampler::analytic_probabilities numerators (out[0..I)) and normaliser (out[I])

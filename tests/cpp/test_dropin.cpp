@@ -11,6 +11,7 @@
 
 #include "krp_oracle.h"
 #include "krplev/krp_sampler.hpp"
+#include "krplev/segment_tree_sampler.hpp"
 
 using namespace krplev;
 
@@ -145,6 +146,68 @@ int main() {
             }
         }
         CHECK(ok);
+    }
+    // SegmentTreeSampler drop-in (test_segment_tree.cpp's checks on the device tree)
+    {
+        // identity rows, y = ones, h = ones: every row has mass 1 -> uniform (known answer)
+        Matrix eye(4, 4);
+        for (std::size_t i = 0; i < 4; ++i) eye(i, i) = 1.0;
+        const SegmentTreeSampler t(eye, 1, std::vector<double>(4, 1.0));
+        const std::vector<double> h(4, 1.0);
+        const std::vector<double> q = t.analytic_probabilities(h);
+        bool uni = true;
+        for (double v : q) uni &= std::abs(v - 0.25) < 1e-15;
+        CHECK(uni);
+        CounterRng rng(5, 0);
+        const std::size_t r = t.row_sample(h, rng);
+        CHECK(r < 4);
+        CHECK(rng.draws() == 1);  // exactly one uniform consumed
+        CHECK(std::abs(t.normalizer(h) - 4.0) < 1e-12);
+        CHECK_THROWS_AS(SegmentTreeSampler(eye, 0, std::vector<double>(4, 1.0)), std::invalid_argument);
+        CHECK_THROWS_AS(t.row_sample(std::vector<double>(3, 1.0), rng), std::invalid_argument);
+        CHECK_THROWS_AS(t.row_sample(std::vector<double>(4, 0.0), rng), std::runtime_error);
+    }
+    {
+        const Matrix U = random_matrix(777, 8, 780);
+        Matrix Y(8, 8);
+        const Matrix A = random_matrix(11, 8, 781);
+        for (std::size_t a = 0; a < 8; ++a)
+            for (std::size_t b = 0; b < 8; ++b) {
+                double s = 0.0;
+                for (std::size_t k = 0; k < 11; ++k) s += A(k, a) * A(k, b);
+                Y(a, b) = s / 8.0;
+            }
+        const SegmentTreeSampler t(U, 5, Y, SegmentTreeSampler::Layout::Full);
+        // children-sum invariant (segment_tree_sampler.cpp:180-186)
+        bool sums = true;
+        for (std::size_t v = 0; v < t.node_count(); ++v) {
+            if (t.is_leaf(v)) continue;
+            const Matrix p = t.node_gram(v), l = t.node_gram(t.left_child(v)), rr = t.node_gram(t.right_child(v));
+            for (std::size_t e = 0; e < p.data.size(); ++e)
+                sums &= std::abs(p.data[e] - l.data[e] - rr.data[e]) <= 1e-10 * (1.0 + std::abs(p.data[e]));
+        }
+        CHECK(sums);
+        // draws vs the oracle restatement of the reference tree, same streams
+        ko_tree* o = nullptr;
+        CHECK(ko_tree_create(U.data.data(), U.rows, 8, 5, Y.data.data(), &o) == 0);
+        std::vector<double> h(8);
+        int same = 0;
+        for (int d = 0; d < 300; ++d) {
+            CounterRng hr(900 + d, 1);
+            for (double& v : h) v = hr.normal();
+            CounterRng rng(31, d);
+            const std::size_t got = t.row_sample(h, rng);
+            std::uint64_t ref = 0;
+            CHECK(ko_tree_row_sample(o, h.data(), 31, uint64_t(d), 1, &ref) == 0);
+            same += got == ref;
+        }
+        CHECK(same == 300);
+        double tot = 0.0;
+        for (double v : t.analytic_probabilities(h)) tot += v;
+        CHECK(std::abs(tot - 1.0) < 1e-12);
+        const auto seg = t.leaf_segment(3);
+        CHECK(t.leaf_probabilities(h, 3).size() == seg.second - seg.first);
+        ko_tree_destroy(o);
     }
     std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
     return g_fail ? 1 : 0;
