@@ -97,6 +97,7 @@ _SIGS = {
     "krpg_segtree_shape": ([_vp, C.POINTER(_u64), C.POINTER(_u64)], _int),
     "krpg_segtree_node_gram": ([_vp, _u64, _dp], _int),
     "krpg_segtree_sample": ([_vp, _dp, _u64, _u64, _u64, _u64, C.POINTER(_u64), _dp], _int),
+    "krpg_segtree_sample_keyed": ([_vp, _dp, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), _dp], _int),
     "krpg_segtree_probabilities": ([_vp, _dp, _dp], _int),
     "krpg_segtree_update_entry": ([_vp, _u64, _u32, C.c_double], _int),
 }
