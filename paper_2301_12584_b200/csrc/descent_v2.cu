@@ -1203,26 +1203,41 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
 #pragma unroll
             for (int s = 0; s < 2 * NB; ++s) zfirst[s] = m8 < nb0 ? a.X[uint64_t(dd0) * R + 4 * s + r4] : 0.0;
         }
-        for (uint64_t c0 = first; c0 < last; c0 += C::LROWS) {
-            if (!__any_sync(0xffffffffu, in_run && pick == ~uint64_t{0})) break;  // every draw picked
-            const int nrow = last - c0 < uint64_t(C::LROWS) ? int(last - c0) : C::LROWS;
+        // rows stream through two half-buffers of PR rows: piece k+1 is in flight
+        // while piece k is scanned
+        constexpr int PR = C::LROWS / 2;
+        auto issue = [&](uint64_t c0, int slot) {
+            const int nrow = last - c0 < uint64_t(PR) ? int(last - c0) : PR;
             const char* src = reinterpret_cast<const char*>(U + c0 * R);
+            unsigned char* dst = buf + slot * PR * C::RSP;
             for (int p = lane; p < nrow * PIECES; p += 32) {
                 const int row = p / PIECES, pc = p - row * PIECES;
-                cp_async16(buf + row * C::RSP + pc * 16, src + uint64_t(row) * C::ROWB + pc * 16);
+                cp_async16(dst + row * C::RSP + pc * 16, src + uint64_t(row) * C::ROWB + pc * 16);
             }
             cp_async_commit();
-            if (c0 == first && st) {  // warm L2 with the first chunk of the next run's leaf
-                const uint32_t vn = __shfl_sync(0xffffffffu, v, __ffs(st) - 1);
-                const uint64_t fn = leaf_index(a.topo, vn) * a.topo.F;
-                const uint64_t ln = fn + a.topo.F < a.topo.I ? fn + a.topo.F : a.topo.I;
-                const uint64_t bytes = (ln - fn < uint64_t(C::LROWS) ? ln - fn : uint64_t(C::LROWS)) * C::ROWB;
-                const char* pn = reinterpret_cast<const char*>(U + fn * R);
-                for (uint64_t o = uint64_t(lane) * 128; o < bytes; o += 32 * 128)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + o));
+        };
+        issue(first, 0);
+        if (st) {  // warm L2 with the first rows of the next run's leaf
+            const uint32_t vn = __shfl_sync(0xffffffffu, v, __ffs(st) - 1);
+            const uint64_t fn = leaf_index(a.topo, vn) * a.topo.F;
+            const uint64_t ln = fn + a.topo.F < a.topo.I ? fn + a.topo.F : a.topo.I;
+            const uint64_t bytes = (ln - fn < uint64_t(C::LROWS) ? ln - fn : uint64_t(C::LROWS)) * C::ROWB;
+            const char* pn = reinterpret_cast<const char*>(U + fn * R);
+            for (uint64_t o = uint64_t(lane) * 128; o < bytes; o += 32 * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + o));
+        }
+        int slot = 0;
+        for (uint64_t c0 = first; c0 < last; c0 += PR, slot ^= 1) {
+            if (!__any_sync(0xffffffffu, in_run && pick == ~uint64_t{0})) break;  // every draw picked
+            const int nrow = last - c0 < uint64_t(PR) ? int(last - c0) : PR;
+            if (c0 + PR < last) {
+                issue(c0 + PR, slot ^ 1);
+                cp_async_wait_one();
+            } else {
+                cp_async_wait_all();
             }
-            cp_async_wait_all();
             __syncwarp();
+            const unsigned char* pbuf = buf + slot * PR * C::RSP;
             for (int b0 = rs; b0 < re; b0 += 8) {
                 const int nb = min(8, re - b0);
                 const bool mine_lane = lane >= b0 && lane < b0 + nb;
@@ -1232,14 +1247,14 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
 #pragma unroll
                 for (int s = 0; s < 2 * NB; ++s)
                     zb[s] = b0 == rs ? zfirst[s] : (m8 < nb ? a.X[uint64_t(dd) * R + 4 * s + r4] : 0.0);
-                // all tiles of the chunk first: 2 x NTL independent DMMA chains (even / odd k)
-                constexpr int NTL = C::LROWS / 8;
+                // all tiles of the piece first: 2 x NTL independent DMMA chains (even / odd k)
+                constexpr int NTL = PR / 8;
                 double qa[NTL][2];
 #pragma unroll
                 for (int tt = 0; tt < NTL; ++tt) {
                     const int row = 8 * tt + m8;
                     const bool rv = row < nrow;
-                    const T* up = reinterpret_cast<const T*>(buf + (rv ? row : 0) * C::RSP) + r4;
+                    const T* up = reinterpret_cast<const T*>(pbuf + (rv ? row : 0) * C::RSP) + r4;
                     double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
 #pragma unroll
                     for (int s = 0; s < 2 * NB; s += 2) {
@@ -1271,6 +1286,8 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
             }
             __syncwarp();
         }
+        cp_async_wait_all();  // drain a piece issued before an early exit
+        __syncwarp();
         if (in_run) {
             if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : last - 1;
             if (a.margin) a.margin[d] = mg;
