@@ -56,12 +56,23 @@ def measure(s, N, I, R, J, storage, label, reps=5, extra=None):
     idx = torch.empty(J, N, dtype=torch.int32, device=dev)
     prob = torch.empty(J, dtype=torch.float64, device=dev)
     rows = torch.empty(J, R, dtype=torch.float64, device=dev)
+    # asynchronous issue as in bench.py: a call's host setup overlaps the previous call's kernels
+    s.set_async(True)
     for i in range(2):
         s.sample_device(None, J, 7 + i, idx, prob, rows)
+    s.sync()
     s.profile_read(reset=True)
-    ts = timed(lambda: s.sample_device(None, J, 100, idx, prob, rows), stream, reps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(reps):
+        s.sample_device(None, J, 100 + i, idx, prob, rows)
+    e1.record(stream)
+    s.sync()
+    torch.cuda.synchronize()
+    s.set_async(False)
     prof = s.profile_read(reset=True)
-    ms = float(np.median(ts))
+    ms = e0.elapsed_time(e1) / reps
     bytes_step, _ = descent_bytes(idx.cpu().numpy().view(np.uint32), [I] * N, R, elt=elt)
     draws_ms = prof["draws"]["ms"] / reps
     line = {"config": label, "N": N, "I": I, "R": R, "J": J, "storage": storage,
