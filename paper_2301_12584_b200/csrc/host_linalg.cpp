@@ -252,17 +252,50 @@ std::size_t numerical_rank(const Eig& e) {
 std::vector<double> pinv_from_eigen(const Eig& e) {
     const std::size_t n = e.values.size();
     const double tau = rank_cutoff(e);
+    // P = W V^T over the kept eigenpairs, W = V diag(1/lambda): row-by-row dot
+    // products of contiguous rows (u runs along a row of `vectors`), upper triangle
+    // then mirrored
+    std::vector<double> inv(n, 0.0);
+    for (std::size_t u = 0; u < n; ++u)
+        if (e.values[u] > tau) inv[u] = 1.0 / e.values[u];
+    std::vector<double> W(n * n);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t u = 0; u < n; ++u) W[i * n + u] = e.vectors[i * n + u] * inv[u];
     std::vector<double> P(n * n, 0.0);
-    for (std::size_t u = 0; u < n; ++u) {
-        if (e.values[u] <= tau) continue;
-        const double inv = 1.0 / e.values[u];
-        for (std::size_t i = 0; i < n; ++i) {
-            const double vi = e.vectors[i * n + u] * inv;
-            double* row = P.data() + i * n;
-            for (std::size_t j = 0; j < n; ++j) row[j] += vi * e.vectors[j * n + u];
+    for (std::size_t i = 0; i < n; ++i) {
+        const double* wi = W.data() + i * n;
+        for (std::size_t j = i; j < n; ++j) {
+            const double* vj = e.vectors.data() + j * n;
+            double acc = 0.0;
+#pragma omp simd reduction(+ : acc)
+            for (std::size_t u = 0; u < n; ++u) acc += wi[u] * vj[u];
+            P[i * n + j] = acc;
+            P[j * n + i] = acc;
         }
     }
     return P;
+}
+
+Eig eig_of_pinv(const Eig& e) {
+    const std::size_t n = e.values.size();
+    const double tau = rank_cutoff(e);
+    Eig out;
+    out.values.assign(n, 0.0);
+    out.vectors.assign(n * n, 0.0);
+    std::size_t k = 0;
+    // 1/lambda descending = lambda ascending over the kept eigenpairs, then the null space
+    for (std::size_t u = n; u-- > 0;) {
+        if (e.values[u] <= tau) continue;
+        out.values[k] = 1.0 / e.values[u];
+        for (std::size_t i = 0; i < n; ++i) out.vectors[i * n + k] = e.vectors[i * n + u];
+        ++k;
+    }
+    for (std::size_t u = 0; u < n; ++u) {
+        if (e.values[u] > tau) continue;
+        for (std::size_t i = 0; i < n; ++i) out.vectors[i * n + k] = e.vectors[i * n + u];
+        ++k;
+    }
+    return out;
 }
 
 void hadamard_into(std::vector<double>& out, const double* m) {

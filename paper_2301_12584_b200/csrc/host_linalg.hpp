@@ -24,6 +24,9 @@ Eig eigh_psd(const double* G, std::size_t n);
 double rank_cutoff(const Eig& e);                 // n * eps * lambda_max (:178-182)
 std::size_t numerical_rank(const Eig& e);         // #{lambda > cutoff}  (:184-190)
 std::vector<double> pinv_from_eigen(const Eig& e);  // sum_{lambda>cutoff} v v^T / lambda (:192-205)
+// eigendecomposition of pinv_from_eigen(e) read off e (values 1/lambda descending, then
+// the null space): equals eigh_psd(G+) up to rounding, without a second eigensolve
+Eig eig_of_pinv(const Eig& e);
 
 // out = ones o m_0 o m_1 ... (dense_kernels.cpp:82-91)
 void hadamard_into(std::vector<double>& out, const double* m);

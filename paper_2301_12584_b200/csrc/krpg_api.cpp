@@ -411,9 +411,13 @@ struct krpg_sampler {
         std::vector<krpg::Eig> ye(npos);
         std::vector<std::future<krpg::Eig>> fut(npos);
         if (mode == KRPG_MODE_TWO_STAGE) {
-            for (size_t p = 1; p < npos; ++p)
+            // the last position's Y is G+ itself (no later factor): its eigenpairs are
+            // those of G, inverted and reordered, no eigensolve needed
+            const size_t last = npos - 1;
+            for (size_t p = 1; p < last; ++p)
                 fut[p] = std::async(std::launch::async, [&, p] { return krpg::eigh_psd(Y[p].data(), R); });
-            ye[0] = krpg::eigh_psd(Y[0].data(), R);
+            if (last > 0) fut[last] = std::async(std::launch::deferred, [&] { return krpg::eig_of_pinv(ge); });
+            ye[0] = last == 0 ? krpg::eig_of_pinv(ge) : krpg::eigh_psd(Y[0].data(), R);
         }
 
         const size_t per_pos = mode == KRPG_MODE_TWO_STAGE ? RR + R : P;
