@@ -308,6 +308,10 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # profiling events only inside the timed region above (kernel time for the roofline);
+    # the rest measures the API as a user calls it
+    s.profile_enable(False)
+
     # ---- exclude-one rates (device-timed, not part of the headline) ----
     excl = {}
     for k in range(N):
@@ -321,8 +325,9 @@ def run_ours(args):
 
     # ---- e2e: the public host API (host outputs, copies inside the region) ----
     e2e_t = []
-    for i in range(2):  # untimed: first-call pinned output buffers
-        s.sample(None, J, args.seed + 700 + i, mode=args.mode, draw_offset=rank * J)
+    b = None
+    for i in range(3):  # untimed: the pinned output buffers of two live batches are cached
+        b = s.sample(None, J, args.seed + 700 + i, mode=args.mode, draw_offset=rank * J)
     for i in range(args.e2e_steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
