@@ -366,44 +366,7 @@ void launch_draws_s(const DrawArgs& a) {
 // ---------------------------------------------------------------------------
 // E-tree: Q[slot] = (sum_{u in node} lambda_u V[:,u] V[:,u]^T) o G_k (packed)
 // ---------------------------------------------------------------------------
-// One block per stored E-node; the node's eigenvector columns V[:, u0:u1] and
-// eigenvalues are staged in shared memory first, so the per-entry sums
-// sum_u lam_u V[a,u] V[b,u] run out of shared memory instead of dependent loads.
-__global__ void k_etree(const double* __restrict__ V, const double* __restrict__ lam,
-                        const double* __restrict__ gk, uint32_t R, double* __restrict__ Q) {
-    extern __shared__ double sv[];  // [R][uc] column chunk of the node, then lam[uc]
-    const Topo te = make_topo(R, 1);
-    const uint32_t P = R * (R + 1) / 2;
-    const uint64_t s = blockIdx.x;  // slot
-    const uint64_t v = s == 0 ? 0 : 2 * s - 1;
-    uint64_t u0, u1;
-    node_rows(te, v, &u0, &u1);
-    const uint32_t nu = uint32_t(u1 - u0);
-    const uint32_t UC = (48u * 1024u / 8u) / (R + 1u);  // columns per chunk (48 KB of smem)
-    for (uint32_t j0 = 0; j0 < nu; j0 += UC) {
-        const uint32_t uc = nu - j0 < UC ? nu - j0 : UC;
-        double* sl = sv + uint64_t(R) * uc;
-        __syncthreads();
-        for (uint32_t e = threadIdx.x; e < R * uc; e += blockDim.x) {
-            const uint32_t c = e / uc, j = e % uc;
-            sv[e] = V[uint64_t(c) * R + u0 + j0 + j];
-        }
-        for (uint32_t j = threadIdx.x; j < uc; j += blockDim.x) sl[j] = lam[u0 + j0 + j];
-        __syncthreads();
-        const bool last_chunk = j0 + uc >= nu;
-        for (uint32_t k = threadIdx.x; k < P; k += blockDim.x) {
-            uint32_t a, b;
-            unpack_pair(R, k, a, b);
-            const double* va = sv + uint64_t(a) * uc;
-            const double* vb = sv + uint64_t(b) * uc;
-            double acc = j0 ? Q[s * P + k] : 0.0;
-            for (uint32_t j = 0; j < uc; ++j) acc = fma(sl[j] * va[j], vb[j], acc);
-            Q[s * P + k] = last_chunk ? acc * gk[k] : acc;
-        }
-    }
-}
-
-// Same Q, one thread per (stored node, packed entry): grid (ceil(P/128), R), so
+// One thread per (stored node, packed entry): grid (ceil(P/128), R), so
 // every entry's sum over the node's eigenvectors runs in parallel.
 __global__ void __launch_bounds__(128) k_etree2(const double* __restrict__ V, const double* __restrict__ lam,
                                                 const double* __restrict__ gk, uint32_t R, double* __restrict__ Q) {
