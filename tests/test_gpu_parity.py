@@ -516,3 +516,34 @@ def test_descent_slices_give_identical_draws():
     for o in out[1:]:
         for x, y in zip(o, out[0]):
             assert np.array_equal(x, y)
+
+
+# ------------------------------------------------ full headline size (config 2)
+def test_config2_full_size_draws_match_lazy_reference():
+    """3 x 2^22 x 64 fp64 (the headline problem, 1% Pareto rows): a window of draws
+    of a large call (global draw ids 1,000,003 ...) checked one by one against the
+    lazy restatement of the reference sampler (oracle/lazy.py: node Grams formed on
+    demand, pinned to the C oracle): indices bit-exact up to counted boundary draws,
+    probabilities within 1e-10."""
+    import os
+    import sys
+
+    import torch
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import make_factors
+    from oracle.lazy import LazyKrp
+
+    class A:
+        N, I, R, seed = 3, 1 << 22, 64, 2301
+
+    fs = make_factors(A(), "cuda")
+    s = K().from_device(fs)
+    host = [f.cpu().numpy() for f in fs]
+    del fs
+    torch.cuda.empty_cache()
+    lz = LazyKrp(host)
+    d0, n = 1_000_003, 256
+    for e in (None, 1):
+        b = s.sample(e, n, 42, draw_offset=d0, margin=True)
+        li, lp, lr, lm = lz.sample(e, np.arange(d0, d0 + n), 42)
+        assert_draws_match(b, li, lp, lr, lm)
