@@ -204,6 +204,8 @@ typedef struct krpg_segtree* krpg_segtree_t;
 int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, const double* Y,
                         const double* y, int device, krpg_segtree_t* out);
 int krpg_segtree_destroy(krpg_segtree_t t);
+/* device copy of a tree (the reference SegmentTreeSampler has value semantics) */
+int krpg_segtree_clone(krpg_segtree_t t, krpg_segtree_t* out);
 int krpg_segtree_shape(krpg_segtree_t t, uint64_t* leaf_count, uint64_t* node_count);
 /* node_gram(node) (:79): stored nodes (root, left children) only */
 int krpg_segtree_node_gram(krpg_segtree_t t, uint64_t node, double* out /* R x R */);

@@ -12,7 +12,7 @@
 // Differences (documented in DESIGN.md):
 //  * storage is always the compact layout (root + left children); with
 //    Layout::Full, node_gram of a right child is formed as parent - left sibling;
-//  * from_sparse is not provided (out of scope);
+//  * from_sparse throws std::invalid_argument (out of scope);
 //  * extra: row_sample_batch (J draws, one history and one stream each).
 #pragma once
 
@@ -46,7 +46,8 @@ public:
     // General PSD Y. F is the leaf capacity.
     SegmentTreeSampler(const Matrix& U, std::size_t F, const Matrix& Y, Layout layout = Layout::Compact)
         : layout_(layout), u_(U), y_(Y) {
-        if (Y.rows != U.cols || Y.cols != U.cols) throw std::invalid_argument("SegmentTreeSampler: Y must be R x R");
+        if (U.empty()) throw std::invalid_argument("build_sampler: empty matrix");
+        if (Y.rows != U.cols || Y.cols != U.cols) throw std::invalid_argument("build_sampler: Y must be R x R");
         create(F, Y.data.data(), nullptr);
     }
     // Rank-1 Y = y y^T.
@@ -54,6 +55,29 @@ public:
         : layout_(layout), u_(U), y_vec_(std::move(y_rank1)) {
         if (y_vec_.size() != U.cols) throw std::invalid_argument("SegmentTreeSampler: y must have R entries");
         create(F, nullptr, y_vec_.data());
+    }
+
+    // value semantics like the reference: a copy owns its own device tree
+    SegmentTreeSampler(const SegmentTreeSampler& o)
+        : layout_(o.layout_), u_(o.u_), y_(o.y_), y_vec_(o.y_vec_), F_(o.F_) {
+        krpg_segtree_t t = nullptr;
+        detail::segtree_check(krpg_segtree_clone(o.h_.get(), &t));
+        h_.reset(t);
+    }
+    SegmentTreeSampler& operator=(const SegmentTreeSampler& o) {
+        if (this != &o) {
+            SegmentTreeSampler tmp(o);
+            *this = std::move(tmp);
+        }
+        return *this;
+    }
+    SegmentTreeSampler(SegmentTreeSampler&&) noexcept = default;
+    SegmentTreeSampler& operator=(SegmentTreeSampler&&) noexcept = default;
+
+    // Sparse construction (segment_tree_sampler.cpp:67-109) is outside this port's
+    // scope: the device tree has a fixed leaf capacity.
+    static SegmentTreeSampler from_sparse(const SparseMatrixCoo&, Layout = Layout::Compact) {
+        throw std::invalid_argument("SegmentTreeSampler::from_sparse: not supported by the device tree");
     }
 
     std::size_t rows() const { return u_.rows; }
@@ -128,10 +152,13 @@ public:
 
     // Normalizer C = <h h^T, U^T U, Y>.
     double normalizer(std::span<const double> h) const { return gram_mass(node_gram(0), h); }
-    // Total mass of the left subtree of an internal node (branch threshold without the offset).
+    // Normalised mass of the left subtree of an internal node: the branch threshold of
+    // the sampling walk without the running offset (segment_tree_sampler.cpp:325-331).
     double left_subtree_mass(std::size_t node, std::span<const double> h) const {
         if (is_leaf(node)) throw std::invalid_argument("left_subtree_mass: node is a leaf");
-        return gram_mass(node_gram(left_child(node)), h);
+        const double C = normalizer(h);
+        if (C <= 0.0) throw std::runtime_error("left_subtree_mass: degenerate distribution");
+        return gram_mass(node_gram(left_child(node)), h) / C;
     }
     std::vector<double> analytic_probabilities(std::span<const double> h) const {
         check_h(h);

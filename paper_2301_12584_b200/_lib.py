@@ -94,6 +94,7 @@ _SIGS = {
     "krpg_sts_last_stats": ([_vp, C.POINTER(_u64)], _int),
     "krpg_segtree_create": ([_dp, _u64, _u32, _u64, _dp, _dp, _int, C.POINTER(_vp)], _int),
     "krpg_segtree_destroy": ([_vp], _int),
+    "krpg_segtree_clone": ([_vp, C.POINTER(_vp)], _int),
     "krpg_segtree_shape": ([_vp, C.POINTER(_u64), C.POINTER(_u64)], _int),
     "krpg_segtree_node_gram": ([_vp, _u64, _dp], _int),
     "krpg_segtree_sample": ([_vp, _dp, _u64, _u64, _u64, _u64, C.POINTER(_u64), _dp], _int),

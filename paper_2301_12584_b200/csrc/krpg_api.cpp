@@ -748,11 +748,16 @@ int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, con
                         int device, krpg_segtree_t* out) {
     return guard([&] {
         *out = nullptr;
-        require(I >= 1 && R >= 1, "SegmentTreeSampler: empty matrix");
-        require(F >= 1, "SegmentTreeSampler: leaf capacity must be positive");
+        // validation and messages as segment_tree_sampler.cpp:26-45 / :47-65
+        require(I >= 1 && R >= 1, "build_sampler: empty matrix");
+        for (uint64_t e = 0; e < I * R; ++e) require(std::isfinite(U[e]), "build_sampler: non-finite entries");
+        require(F >= 1, "build_sampler: leaf capacity must be positive");
         require(R <= 256, "krpg: rank above 256 is not supported on device");
         require((Y != nullptr) != (y != nullptr), "SegmentTreeSampler: give exactly one of Y (R x R) or y (R)");
-        for (uint64_t e = 0; e < I * R; ++e) require(std::isfinite(U[e]), "SegmentTreeSampler: non-finite entries");
+        if (Y) {
+            for (uint64_t e = 0; e < uint64_t(R) * R; ++e) require(std::isfinite(Y[e]), "build_sampler: non-finite Y");
+            (void)krpg::eigh_psd(Y, R);  // rejects asymmetric or indefinite Y
+        }
         int ndev = 0;
         CK(cudaGetDeviceCount(&ndev));
         require(device >= 0 && device < ndev, "krpg: no such CUDA device");
@@ -767,11 +772,11 @@ int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, con
         CK(cudaMemcpyAsync(t->U.ensure(8 * I * R), U, 8 * I * R, cudaMemcpyHostToDevice, t->stream));
         if (y) {
             t->y_host.assign(y, y + R);
-            for (double v : t->y_host) require(std::isfinite(v), "SegmentTreeSampler: non-finite y");
+            for (double v : t->y_host) require(std::isfinite(v), "build_sampler: non-finite y");
             CK(cudaMemcpyAsync(t->yv.ensure(8 * R), t->y_host.data(), 8 * R, cudaMemcpyHostToDevice, t->stream));
         } else {
             t->Y_host.assign(Y, Y + size_t(R) * R);
-            for (double v : t->Y_host) require(std::isfinite(v), "SegmentTreeSampler: non-finite Y");
+            for (double v : t->Y_host) require(std::isfinite(v), "build_sampler: non-finite Y");
             const std::vector<double> yp = krpg::pack_upper(Y, R);
             CK(cudaMemcpyAsync(t->Yp.ensure(8 * yp.size()), yp.data(), 8 * yp.size(), cudaMemcpyHostToDevice,
                                t->stream));
@@ -779,6 +784,34 @@ int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, con
         }
         t->build();
         *out = t.release();
+    });
+}
+
+int krpg_segtree_clone(krpg_segtree_t t, krpg_segtree_t* out) {
+    return guard([&] {
+        *out = nullptr;
+        require(t, "krpg: null tree");
+        std::lock_guard<std::mutex> lk(t->mu);
+        CK(cudaSetDevice(t->device));
+        auto c = std::make_unique<krpg_segtree>();
+        c->device = t->device;
+        c->I = t->I;
+        c->R = t->R;
+        c->F = t->F;
+        c->rank1 = t->rank1;
+        c->y_host = t->y_host;
+        c->Y_host = t->Y_host;
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        auto dup = [&](DevBuf& dst, const DevBuf& src) {
+            if (!src.p) return;
+            CK(cudaMemcpyAsync(dst.ensure(src.bytes), src.p, src.bytes, cudaMemcpyDeviceToDevice, t->stream));
+        };
+        dup(c->U, t->U);
+        dup(c->tree, t->tree);
+        dup(c->yv, t->yv);
+        dup(c->Yp, t->Yp);
+        CK(cudaStreamSynchronize(t->stream));
+        *out = c.release();
     });
 }
 
