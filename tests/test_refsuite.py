@@ -1,5 +1,5 @@
 """The reference's OWN unit tests (test_krp_sampler.cpp, test_segment_tree.cpp,
-test_rng.cpp), compiled unmodified against the B200 drop-in headers and libkrpg.so
+test_rng.cpp, test_sketch.cpp), compiled unmodified against the B200 drop-in headers and libkrpg.so
 (oracle/Makefile target `_ref/refsuite`, built where /root/reference exists), run
 on the device. The five sparse-construction cases exercise
 SegmentTreeSampler::from_sparse, which is out of this port's scope (SURVEY 8(f)
