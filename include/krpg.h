@@ -203,6 +203,16 @@ int krpg_sts_last_stats(krpg_t h, uint64_t* stats);
 typedef struct krpg_segtree* krpg_segtree_t;
 int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, const double* Y,
                         const double* y, int device, krpg_segtree_t* out);
+/* The same tree over an explicit row partition: leaf l (in order) holds rows
+ * [leaf_offsets[l], leaf_offsets[l+1]), L leaves, offsets[0] = 0, offsets[L] = I,
+ * strictly ascending (init_tree's leaf_segments, segment_tree_sampler.cpp:111-149).
+ * from_sparse (:67-109) builds its greedy nnz partition on the host and calls this. */
+int krpg_segtree_create_segments(const double* U, uint64_t I, uint32_t R, const uint64_t* leaf_offsets,
+                                 uint64_t L, const double* Y, const double* y, int device,
+                                 krpg_segtree_t* out);
+/* leaf offsets of a tree (leaf_count + 1 values) and the rows of heap node v (node_segment) */
+int krpg_segtree_leaf_offsets(krpg_segtree_t t, uint64_t* offsets);
+int krpg_segtree_node_rows(krpg_segtree_t t, uint64_t v, uint64_t* first, uint64_t* last);
 int krpg_segtree_destroy(krpg_segtree_t t);
 /* device copy of a tree (the reference SegmentTreeSampler has value semantics) */
 int krpg_segtree_clone(krpg_segtree_t t, krpg_segtree_t* out);

@@ -12,10 +12,14 @@
 // Differences (documented in DESIGN.md):
 //  * storage is always the compact layout (root + left children); with
 //    Layout::Full, node_gram of a right child is formed as parent - left sibling;
-//  * from_sparse throws std::invalid_argument (out of scope);
+//  * from_sparse keeps the reference's validation, Y = ones and greedy R^2-nonzero
+//    leaf partition, but the device holds the densified rows (variable leaf segments
+//    via krpg_segtree_create_segments); draws equal the reference's sparse tree's;
 //  * extra: row_sample_batch (J draws, one history and one stream each).
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <span>
@@ -59,7 +63,8 @@ public:
 
     // value semantics like the reference: a copy owns its own device tree
     SegmentTreeSampler(const SegmentTreeSampler& o)
-        : layout_(o.layout_), u_(o.u_), y_(o.y_), y_vec_(o.y_vec_), F_(o.F_) {
+        : layout_(o.layout_), u_(o.u_), y_(o.y_), y_vec_(o.y_vec_), F_(o.F_), sparse_(o.sparse_),
+          row_ptr_(o.row_ptr_), col_idx_(o.col_idx_) {
         krpg_segtree_t t = nullptr;
         detail::segtree_check(krpg_segtree_clone(o.h_.get(), &t));
         h_.reset(t);
@@ -74,15 +79,50 @@ public:
     SegmentTreeSampler(SegmentTreeSampler&&) noexcept = default;
     SegmentTreeSampler& operator=(SegmentTreeSampler&&) noexcept = default;
 
-    // Sparse construction (segment_tree_sampler.cpp:67-109) is outside this port's
-    // scope: the device tree has a fixed leaf capacity.
-    static SegmentTreeSampler from_sparse(const SparseMatrixCoo&, Layout = Layout::Compact) {
-        throw std::invalid_argument("SegmentTreeSampler::from_sparse: not supported by the device tree");
+    // Sparse construction (segment_tree_sampler.cpp:67-109) with Y fixed to all-ones:
+    // leaves by the greedy rule "at most R^2 stored nonzeros per leaf".
+    static SegmentTreeSampler from_sparse(const SparseMatrixCoo& U, Layout layout = Layout::Compact) {
+        if (U.rows < 1 || U.cols < 1) throw std::invalid_argument("build_sampler_sparse: empty matrix");
+        if (U.entries.empty()) throw std::invalid_argument("build_sampler_sparse: matrix has no nonzeros");
+        if (!U.sorted_row_major()) throw std::invalid_argument("build_sampler_sparse: entries must be sorted row-major");
+        SegmentTreeSampler s(layout);
+        s.sparse_ = true;
+        s.u_ = Matrix(U.rows, U.cols);
+        s.y_vec_.assign(U.cols, 1.0);
+        s.row_ptr_.assign(U.rows + 1, 0);
+        s.col_idx_.reserve(U.nnz());
+        for (const auto& e : U.entries) {
+            if (e.row >= U.rows || e.col >= U.cols) throw std::invalid_argument("build_sampler_sparse: entry out of range");
+            if (!std::isfinite(e.value)) throw std::invalid_argument("build_sampler_sparse: non-finite entry");
+            s.row_ptr_[e.row + 1]++;
+            s.col_idx_.push_back(e.col);
+            s.u_(e.row, e.col) = e.value;
+        }
+        for (std::size_t i = 0; i < U.rows; ++i) s.row_ptr_[i + 1] += s.row_ptr_[i];
+        const std::size_t cap = U.cols * U.cols;
+        std::vector<std::uint64_t> offs{0};
+        std::size_t cur = 0;
+        for (std::size_t i = 0; i < U.rows; ++i) {
+            const std::size_t rn = s.row_ptr_[i + 1] - s.row_ptr_[i];
+            if (cur + rn > cap && cur > 0) {
+                offs.push_back(i);
+                cur = 0;
+            }
+            cur += rn;
+        }
+        offs.push_back(U.rows);
+        s.F_ = U.cols;  // nominal, as the reference
+        krpg_segtree_t t = nullptr;
+        detail::segtree_check(krpg_segtree_create_segments(s.u_.data.data(), s.u_.rows,
+                                                           static_cast<std::uint32_t>(s.u_.cols), offs.data(),
+                                                           offs.size() - 1, nullptr, s.y_vec_.data(), 0, &t));
+        s.h_.reset(t);
+        return s;
     }
 
     std::size_t rows() const { return u_.rows; }
     std::size_t cols() const { return u_.cols; }
-    bool sparse() const { return false; }
+    bool sparse() const { return sparse_; }
 
     // Draws one row index in [0, I); consumes exactly one uniform variate.
     std::size_t row_sample(std::span<const double> h, CounterRng& rng) const {
@@ -116,6 +156,10 @@ public:
     }
 
     void update_entry(std::size_t r, std::size_t c, double value) {
+        if (sparse_ && r < rows() && c < cols() &&
+            !std::binary_search(col_idx_.begin() + row_ptr_[r], col_idx_.begin() + row_ptr_[r + 1],
+                                static_cast<std::uint32_t>(c)))
+            throw std::invalid_argument("update_entry: entry outside the stored sparsity pattern");
         detail::segtree_check(krpg_segtree_update_entry(h_.get(), r, static_cast<std::uint32_t>(c), value));
         u_(r, c) = value;
     }
@@ -124,13 +168,15 @@ public:
     std::size_t leaf_count() const { return shape().first; }
     std::size_t node_count() const { return shape().second; }
     std::pair<std::size_t, std::size_t> leaf_segment(std::size_t leaf) const {
-        if (leaf >= leaf_count()) throw std::invalid_argument("leaf_segment: leaf out of range");
-        const std::size_t first = leaf * F_;
-        return {first, std::min(first + F_, rows())};
+        const std::size_t L = leaf_count();
+        if (leaf >= L) throw std::invalid_argument("leaf_segment: leaf out of range");
+        std::vector<std::uint64_t> offs(L + 1);
+        detail::segtree_check(krpg_segtree_leaf_offsets(h_.get(), offs.data()));
+        return {static_cast<std::size_t>(offs[leaf]), static_cast<std::size_t>(offs[leaf + 1])};
     }
     std::pair<std::size_t, std::size_t> node_segment(std::size_t node) const {
-        std::uint64_t f = 0, l = 0, L = 0, n = 0;
-        detail::segtree_check(krpg_topology_node_rows(rows(), F_, node, &f, &l, &L, &n));
+        std::uint64_t f = 0, l = 0;
+        detail::segtree_check(krpg_segtree_node_rows(h_.get(), node, &f, &l));
         return {static_cast<std::size_t>(f), static_cast<std::size_t>(l)};
     }
     bool gram_stored(std::size_t node) const { return layout_ == Layout::Full || node == 0 || (node & 1); }
@@ -166,12 +212,17 @@ public:
         detail::segtree_check(krpg_segtree_probabilities(h_.get(), h.data(), q.data()));
         return q;
     }
-    const Matrix& dense_matrix() const { return u_; }
+    const Matrix& dense_matrix() const {
+        if (sparse_) throw std::logic_error("dense_matrix: sampler was built from sparse input");
+        return u_;
+    }
 
 private:
     struct Del {
         void operator()(krpg_segtree* t) const { krpg_segtree_destroy(t); }
     };
+
+    explicit SegmentTreeSampler(Layout layout) : layout_(layout) {}
 
     void create(std::size_t F, const double* Y, const double* y) {
         if (u_.empty()) throw std::invalid_argument("SegmentTreeSampler: empty matrix");
@@ -206,6 +257,9 @@ private:
     Matrix u_, y_;
     std::vector<double> y_vec_;
     std::size_t F_ = 0;
+    bool sparse_ = false;
+    std::vector<std::size_t> row_ptr_;  // sparse-built: stored pattern (CSR)
+    std::vector<std::uint32_t> col_idx_;
     std::unique_ptr<krpg_segtree, Del> h_;
 };
 

@@ -269,6 +269,43 @@ class OracleTree:
         for n in ("tree_node_count", "tree_leaf_count"):
             self.b.fn(n).restype = _u64
 
+    @classmethod
+    def from_sparse(cls, rows, cols, er, ec, ev, backend="port", full=True):
+        """SegmentTreeSampler::from_sparse (segment_tree_sampler.cpp:67-109). The port
+        restates the greedy R^2-nonzero leaf partition (:88-101) over the densified rows
+        (ko_tree_create_segments); the reference backend calls from_sparse itself."""
+        self = cls.__new__(cls)
+        self.b = _Backend(backend)
+        er = np.ascontiguousarray(er, dtype=np.uint32)
+        ec = np.ascontiguousarray(ec, dtype=np.uint32)
+        ev = _c64(ev)
+        U = np.zeros((rows, cols))
+        U[er.astype(np.int64), ec.astype(np.int64)] = ev
+        self.U, self.R, self._Y = U, cols, None
+        h = _vp()
+        if backend == "ref":
+            p32 = C.POINTER(C.c_uint32)
+            self.b.check(self.b.fn("tree_create_sparse")(_u64(rows), _u64(cols), er.ctypes.data_as(p32),
+                                                         ec.ctypes.data_as(p32), _dptr(ev), _u64(len(ev)),
+                                                         C.c_int(1 if full else 0), C.byref(h)))
+        else:
+            counts = np.bincount(er.astype(np.int64), minlength=rows)
+            offs, cur = [0], 0
+            for i in range(rows):
+                if cur + counts[i] > cols * cols and cur > 0:
+                    offs.append(i)
+                    cur = 0
+                cur += int(counts[i])
+            offs.append(rows)
+            self.offsets = np.asarray(offs, dtype=np.uint64)
+            self.b.check(self.b.fn("tree_create_segments")(_dptr(U), _u64(rows), _u32(cols),
+                                                           self.offsets.ctypes.data_as(C.POINTER(_u64)),
+                                                           _u64(len(offs) - 1), None, C.byref(h)))
+        self.h = h
+        for n in ("tree_node_count", "tree_leaf_count"):
+            self.b.fn(n).restype = _u64
+        return self
+
     def __del__(self):
         h = getattr(self, "h", None)
         if h:

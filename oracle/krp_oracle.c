@@ -238,6 +238,7 @@ struct ko_tree {
     int own_u;
     double* Y;  /* general Y (R x R) or NULL */
     double* y1; /* rank-1 factor or NULL */
+    const uint64_t* offs; /* explicit leaf offsets (L + 1) during tree_topology, or NULL */
 };
 
 static uint64_t ceil_log2(uint64_t n) { /* :18-22 */
@@ -258,8 +259,13 @@ static void tree_topology(ko_tree* t) { /* init_tree :111-149 */
     for (uint64_t l = 0; l < L; ++l) {
         const uint64_t node = (l < bottom) ? (((uint64_t)1 << d) - 1 + l) : (L - 1 + (l - bottom));
         t->leaf_node[l] = node;
-        t->seg0[node] = l * t->F;
-        t->seg1[node] = (l * t->F + t->F < t->I) ? l * t->F + t->F : t->I;
+        if (t->offs) { /* explicit leaf_segments (from_sparse's partition, :88-101) */
+            t->seg0[node] = t->offs[l];
+            t->seg1[node] = t->offs[l + 1];
+        } else {
+            t->seg0[node] = l * t->F;
+            t->seg1[node] = (l * t->F + t->F < t->I) ? l * t->F + t->F : t->I;
+        }
     }
     for (uint64_t v = n; v-- > 0;)
         if (!is_leaf(t, v)) {
@@ -338,6 +344,48 @@ int ko_tree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, const do
         free(t);
         return rc;
     }
+    *out = t;
+    return 0;
+}
+/* init_tree over explicit leaf segments [offs[l], offs[l+1]) (:111-149); F becomes
+ * the longest leaf (scan work size). Y == NULL -> rank-1 all-ones (from_sparse). */
+int ko_tree_create_segments(const double* U, uint64_t I, uint32_t R, const uint64_t* offs, uint64_t L,
+                            const double* Y, ko_tree** out) {
+    if (L < 1 || offs[0] != 0 || offs[L] != I) return fail(1, "build_sampler: leaf segments must cover [0, I)");
+    uint64_t fmax = 0;
+    for (uint64_t l = 0; l < L; ++l) {
+        if (offs[l + 1] <= offs[l]) return fail(1, "build_sampler: leaf segments must be non-empty and ascending");
+        if (offs[l + 1] - offs[l] > fmax) fmax = offs[l + 1] - offs[l];
+    }
+    ko_tree* t = malloc(sizeof *t);
+    double* u = malloc(sizeof(double) * (I * R ? I * R : 1));
+    memcpy(u, U, sizeof(double) * I * R);
+    memset(t, 0, sizeof *t);
+    for (uint64_t k = 0; k < I * R; ++k)
+        if (!isfinite(u[k])) {
+            free(u);
+            free(t);
+            return fail(1, "build_sampler: non-finite entries");
+        }
+    t->I = I;
+    t->R = R;
+    t->F = fmax;
+    t->P = (uint64_t)R * (R + 1) / 2;
+    t->U = u;
+    t->own_u = 1;
+    if (Y) {
+        t->Y = malloc(sizeof(double) * R * R);
+        memcpy(t->Y, Y, sizeof(double) * R * R);
+    } else {
+        t->y1 = malloc(sizeof(double) * R);
+        for (uint32_t c = 0; c < R; ++c) t->y1[c] = 1.0;
+    }
+    t->L = L;
+    t->offs = offs;
+    tree_topology(t);
+    t->offs = NULL;
+    t->grams = malloc(sizeof(double) * t->n * t->P);
+    tree_build(t);
     *out = t;
     return 0;
 }

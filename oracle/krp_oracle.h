@@ -36,6 +36,8 @@ int ko_pinv(const double* G, uint32_t n, double* out, uint64_t* rank);
 typedef struct ko_tree ko_tree;
 int ko_tree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, const double* Y,
                    ko_tree** out);
+int ko_tree_create_segments(const double* U, uint64_t I, uint32_t R, const uint64_t* offs, uint64_t L,
+                            const double* Y, ko_tree** out);
 void ko_tree_destroy(ko_tree* t);
 uint64_t ko_tree_node_count(const ko_tree* t);
 uint64_t ko_tree_leaf_count(const ko_tree* t);

@@ -237,6 +237,18 @@ int kref_tree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, const 
             *out = new SegmentTreeSampler(to_matrix(U, I, R), F, std::vector<double>(R, 1.0), lay);
     });
 }
+// SegmentTreeSampler::from_sparse (segment_tree_sampler.cpp:67-109) over COO entries
+int kref_tree_create_sparse(uint64_t rows, uint64_t cols, const uint32_t* er, const uint32_t* ec, const double* ev,
+                            uint64_t nnz, int full, void** out) {
+    return guard([&] {
+        SparseMatrixCoo c;
+        c.rows = rows;
+        c.cols = cols;
+        for (uint64_t k = 0; k < nnz; ++k) c.entries.push_back({er[k], ec[k], ev[k]});
+        const auto lay = full ? SegmentTreeSampler::Layout::Full : SegmentTreeSampler::Layout::Compact;
+        *out = new SegmentTreeSampler(SegmentTreeSampler::from_sparse(c, lay));
+    });
+}
 void kref_tree_destroy(void* t) { delete static_cast<SegmentTreeSampler*>(t); }
 uint64_t kref_tree_node_count(void* t) { return static_cast<SegmentTreeSampler*>(t)->node_count(); }
 uint64_t kref_tree_leaf_count(void* t) { return static_cast<SegmentTreeSampler*>(t)->leaf_count(); }

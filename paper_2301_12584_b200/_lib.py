@@ -93,6 +93,9 @@ _SIGS = {
     "krpg_sts_solve": ([_vp, _vp, _u32, _u64, _u64, _dp], _int),
     "krpg_sts_last_stats": ([_vp, C.POINTER(_u64)], _int),
     "krpg_segtree_create": ([_dp, _u64, _u32, _u64, _dp, _dp, _int, C.POINTER(_vp)], _int),
+    "krpg_segtree_create_segments": ([_dp, _u64, _u32, C.POINTER(_u64), _u64, _dp, _dp, _int, C.POINTER(_vp)], _int),
+    "krpg_segtree_leaf_offsets": ([_vp, C.POINTER(_u64)], _int),
+    "krpg_segtree_node_rows": ([_vp, _u64, C.POINTER(_u64), C.POINTER(_u64)], _int),
     "krpg_segtree_destroy": ([_vp], _int),
     "krpg_segtree_clone": ([_vp, C.POINTER(_vp)], _int),
     "krpg_segtree_shape": ([_vp, C.POINTER(_u64), C.POINTER(_u64)], _int),

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
         hr[s] = b < R ? ((a.pos == 0 && !STANDALONE) ? 1.0 : a.H[d * R + b]) : 0.0;
     }
     double margin = (a.pos == 0 || STANDALONE || !a.margin) ? HUGE_VAL : a.margin[d];
-    const Topo tz = make_topo(a.I, a.F ? a.F : R);
+    const Topo tz = a.segs ? make_topo_segments(a.I, a.nleaves, a.segs) : make_topo(a.I, a.F ? a.F : R);
 
     double zr[S];
     double inv_c, low, u;
@@ -191,9 +191,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_draws(DrawArgs a) {
     // ---- leaf scan (:281-292): first row whose running mass reaches u ----
     uint64_t first, last;
     {
-        const uint64_t l = leaf_index(tz, node);
-        first = l * tz.F;
-        last = first + tz.F < tz.I ? first + tz.F : tz.I;
+        leaf_rows(tz, leaf_index(tz, node), &first, &last);
     }
     double cum = low;
     uint64_t pick = ~uint64_t{0}, last_nz = ~uint64_t{0};

@@ -706,18 +706,24 @@ void krpg_sampler::sts_solve(krpg_tensor& T, uint32_t j, uint64_t J, uint64_t se
 struct krpg_segtree {
     int device = 0;
     uint64_t I = 0, F = 0;
+    uint64_t L = 0;  // leaves when built over explicit segments (from_sparse), else 0
     uint32_t R = 0;
     bool rank1 = true;
-    DevBuf U, tree, tbuf, yv, Yp, err, scratch;
+    DevBuf U, tree, tbuf, yv, Yp, err, scratch, segs;
     std::vector<double> y_host, Y_host;  // as given (validation / introspection)
+    std::vector<uint64_t> segs_host;     // L + 1 leaf offsets (segmented trees)
     cudaStream_t stream = nullptr;
     std::mutex mu;
     uint64_t P() const { return uint64_t(R) * (R + 1) / 2; }
+    const uint64_t* segs_d() const { return L ? segs.as<uint64_t>() : nullptr; }
+    krpg::Topo topo() const {  // host-side topology (segment table in host memory)
+        return L ? krpg::make_topo_segments(I, L, segs_host.data()) : krpg::make_topo(I, F);
+    }
     void build() {
-        const krpg::Topo t = krpg::make_topo(I, F);
+        const krpg::Topo t = topo();
         tree.ensure(sizeof(double) * t.L * P());
         uint64_t na, nb;
-        krpg::tree_transient_doubles(I, R, &na, &nb, F);
+        krpg::tree_transient_doubles(I, R, &na, &nb, F, L);
         double* base = static_cast<double*>(tbuf.ensure(sizeof(double) * (na + nb) + 16));
         krpg::TreeBuildArgs a{};
         a.U = U.p;
@@ -725,6 +731,9 @@ struct krpg_segtree {
         a.I = I;
         a.R = R;
         a.F = F;
+        a.segs = segs_d();
+        a.segs_h = L ? segs_host.data() : nullptr;
+        a.nleaves = L;
         a.compact = tree.as<double>();
         a.tbuf_a = base;
         a.tbuf_b = base + na;
@@ -735,7 +744,7 @@ struct krpg_segtree {
         CK(cudaStreamSynchronize(stream));
     }
     ~krpg_segtree() {
-        for (DevBuf* b : {&U, &tree, &tbuf, &yv, &Yp, &err, &scratch}) b->release();
+        for (DevBuf* b : {&U, &tree, &tbuf, &yv, &Yp, &err, &scratch, &segs}) b->release();
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -744,14 +753,21 @@ extern "C" {
 
 const char* krpg_last_error(void) { return g_err.c_str(); }
 
-int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, const double* Y, const double* y,
-                        int device, krpg_segtree_t* out) {
-    return guard([&] {
+static void segtree_create_impl(const double* U, uint64_t I, uint32_t R, uint64_t F, const uint64_t* leaf_offsets,
+                                uint64_t L, const double* Y, const double* y, int device, krpg_segtree_t* out) {
+    {
         *out = nullptr;
         // validation and messages as segment_tree_sampler.cpp:26-45 / :47-65
         require(I >= 1 && R >= 1, "build_sampler: empty matrix");
         for (uint64_t e = 0; e < I * R; ++e) require(std::isfinite(U[e]), "build_sampler: non-finite entries");
-        require(F >= 1, "build_sampler: leaf capacity must be positive");
+        if (leaf_offsets) {  // explicit partition (init_tree's leaf_segments, :111-149)
+            require(L >= 1, "build_sampler: no leaf segments");
+            require(leaf_offsets[0] == 0 && leaf_offsets[L] == I, "build_sampler: leaf segments must cover [0, I)");
+            for (uint64_t l = 0; l < L; ++l)
+                require(leaf_offsets[l] < leaf_offsets[l + 1], "build_sampler: leaf segments must be non-empty and ascending");
+        } else {
+            require(F >= 1, "build_sampler: leaf capacity must be positive");
+        }
         require(R <= 256, "krpg: rank above 256 is not supported on device");
         require((Y != nullptr) != (y != nullptr), "SegmentTreeSampler: give exactly one of Y (R x R) or y (R)");
         if (Y) {
@@ -765,11 +781,17 @@ int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, con
         t->device = device;
         t->I = I;
         t->R = R;
-        t->F = F;
+        t->F = leaf_offsets ? R : F;
         t->rank1 = y != nullptr;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
         CK(cudaMemcpyAsync(t->U.ensure(8 * I * R), U, 8 * I * R, cudaMemcpyHostToDevice, t->stream));
+        if (leaf_offsets) {
+            t->L = L;
+            t->segs_host.assign(leaf_offsets, leaf_offsets + L + 1);
+            CK(cudaMemcpyAsync(t->segs.ensure(8 * (L + 1)), t->segs_host.data(), 8 * (L + 1),
+                               cudaMemcpyHostToDevice, t->stream));
+        }
         if (y) {
             t->y_host.assign(y, y + R);
             for (double v : t->y_host) require(std::isfinite(v), "build_sampler: non-finite y");
@@ -784,6 +806,44 @@ int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, con
         }
         t->build();
         *out = t.release();
+    }
+}
+
+int krpg_segtree_create(const double* U, uint64_t I, uint32_t R, uint64_t F, const double* Y, const double* y,
+                        int device, krpg_segtree_t* out) {
+    return guard([&] { segtree_create_impl(U, I, R, F, nullptr, 0, Y, y, device, out); });
+}
+
+int krpg_segtree_create_segments(const double* U, uint64_t I, uint32_t R, const uint64_t* leaf_offsets, uint64_t L,
+                                 const double* Y, const double* y, int device, krpg_segtree_t* out) {
+    return guard([&] {
+        require(leaf_offsets != nullptr, "build_sampler: null leaf offsets");
+        segtree_create_impl(U, I, R, 0, leaf_offsets, L, Y, y, device, out);
+    });
+}
+
+int krpg_segtree_leaf_offsets(krpg_segtree_t t, uint64_t* offsets) {
+    return guard([&] {
+        require(t, "krpg: null tree");
+        const krpg::Topo tp = t->topo();
+        for (uint64_t l = 0; l <= tp.L; ++l) {
+            uint64_t f = 0, e = 0;
+            if (l < tp.L) {
+                krpg::leaf_rows(tp, l, &f, &e);
+                offsets[l] = f;
+            } else {
+                offsets[l] = t->I;
+            }
+        }
+    });
+}
+
+int krpg_segtree_node_rows(krpg_segtree_t t, uint64_t v, uint64_t* first, uint64_t* last) {
+    return guard([&] {
+        require(t, "krpg: null tree");
+        const krpg::Topo tp = t->topo();
+        require(v < tp.n, "node_segment: node out of range");
+        krpg::node_rows(tp, v, first, last);
     });
 }
 
@@ -798,6 +858,8 @@ int krpg_segtree_clone(krpg_segtree_t t, krpg_segtree_t* out) {
         c->I = t->I;
         c->R = t->R;
         c->F = t->F;
+        c->L = t->L;
+        c->segs_host = t->segs_host;
         c->rank1 = t->rank1;
         c->y_host = t->y_host;
         c->Y_host = t->Y_host;
@@ -810,6 +872,7 @@ int krpg_segtree_clone(krpg_segtree_t t, krpg_segtree_t* out) {
         dup(c->tree, t->tree);
         dup(c->yv, t->yv);
         dup(c->Yp, t->Yp);
+        dup(c->segs, t->segs);
         CK(cudaStreamSynchronize(t->stream));
         *out = c.release();
     });
@@ -826,7 +889,7 @@ int krpg_segtree_destroy(krpg_segtree_t t) {
 int krpg_segtree_shape(krpg_segtree_t t, uint64_t* leaf_count, uint64_t* node_count) {
     return guard([&] {
         require(t, "krpg: null tree");
-        const krpg::Topo tp = krpg::make_topo(t->I, t->F);
+        const krpg::Topo tp = t->topo();
         *leaf_count = tp.L;
         *node_count = tp.n;
     });
@@ -835,7 +898,7 @@ int krpg_segtree_shape(krpg_segtree_t t, uint64_t* leaf_count, uint64_t* node_co
 int krpg_segtree_node_gram(krpg_segtree_t t, uint64_t node, double* out) {
     return guard([&] {
         require(t, "krpg: null tree");
-        const krpg::Topo tp = krpg::make_topo(t->I, t->F);
+        const krpg::Topo tp = t->topo();
         require(node < tp.n, "node_gram: node out of range");
         require(node == 0 || (node & 1), "node_gram: Gram of this node is not stored (compact layout)");
         std::lock_guard<std::mutex> lk(t->mu);
@@ -902,6 +965,8 @@ static void segtree_sample_impl(krpg_segtree_t t, const double* H, uint64_t J, u
         a.storage = KRPG_STORE_F64;
         a.I = t->I;
         a.F = t->F;
+        a.segs = t->segs_d();
+        a.nleaves = t->L;
         a.counter = counter;
         a.keys = keys ? dkeys : nullptr;
         a.counters = keys ? dctr : nullptr;
@@ -958,7 +1023,7 @@ int krpg_segtree_update_entry(krpg_segtree_t t, uint64_t r, uint32_t c, double v
         CK(cudaMemcpyAsync(d_old, oldr.data(), 8 * R, cudaMemcpyHostToDevice, t->stream));
         CK(cudaMemcpyAsync(d_new, newr.data(), 8 * R, cudaMemcpyHostToDevice, t->stream));
         CK(cudaMemcpyAsync(d_row, &r, 8, cudaMemcpyHostToDevice, t->stream));
-        krpg::launch_row_deltas(t->tree.as<double>(), t->I, R, t->F, 1, d_row, d_old, d_new, t->stream);
+        krpg::launch_row_deltas(t->tree.as<double>(), t->I, R, t->F, t->segs_d(), t->L, 1, d_row, d_old, d_new, t->stream);
         CK(cudaMemcpyAsync(t->U.as<double>() + r * R + c, &value, 8, cudaMemcpyHostToDevice, t->stream));
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(t->stream));
@@ -1444,7 +1509,7 @@ int krpg_update_entries(krpg_t h, uint32_t j, const uint64_t* r, const uint32_t*
         }
         CK(cudaMemcpyAsync(dnew, newh.data(), rb, cudaMemcpyHostToDevice, h->stream));
         cudaEvent_t t0 = h->pbegin();
-        krpg::launch_row_deltas(h->f[j].tree.as<double>(), h->f[j].I, R, 0, nr, drows, dold, dnew, h->stream);
+        krpg::launch_row_deltas(h->f[j].tree.as<double>(), h->f[j].I, R, 0, nullptr, 0, nr, drows, dold, dnew, h->stream);
         krpg::launch_scatter_rows(h->f[j].U.p, h->storage, R, nr, drows, dnew, h->stream);
         h->pend(KRPG_PROF_UPDATE, t0, 2);
         h->prof_launches[KRPG_PROF_OTHER] += 1;  // gather of the old rows

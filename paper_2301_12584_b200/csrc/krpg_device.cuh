@@ -40,6 +40,7 @@ struct Topo {
     uint64_t n;       // nodes
     uint32_t d;       // depth
     uint64_t bottom;  // leaves on the deepest level
+    const uint64_t* seg = nullptr;  // variable leaf segments: leaf l = rows [seg[l], seg[l+1])
 };
 
 __host__ __device__ __forceinline__ uint32_t ceil_log2_u64(uint64_t n) {
@@ -56,6 +57,20 @@ __host__ __device__ inline Topo make_topo(uint64_t I, uint64_t F) {
     t.n = 2 * t.L - 1;
     t.d = ceil_log2_u64(t.L);
     t.bottom = 2 * t.L - (uint64_t{1} << t.d);
+    return t;
+}
+
+// complete tree over L leaves with explicit row segments (init_tree with arbitrary
+// leaf_segments, segment_tree_sampler.cpp:111-149; from_sparse's partition)
+__host__ __device__ inline Topo make_topo_segments(uint64_t I, uint64_t L, const uint64_t* seg) {
+    Topo t;
+    t.I = I;
+    t.F = 0;
+    t.L = L;
+    t.n = 2 * t.L - 1;
+    t.d = ceil_log2_u64(t.L);
+    t.bottom = 2 * t.L - (uint64_t{1} << t.d);
+    t.seg = seg;
     return t;
 }
 
@@ -91,9 +106,25 @@ __host__ __device__ inline void node_rows(const Topo& t, uint64_t v, uint64_t* f
         if (vr < t.n) llast = vr - ((uint64_t{1} << t.d) - 1);
         else llast = leaf_index(t, ((v + 2) << (s - 1)) - 2);
     }
+    if (t.seg) {
+        *first = t.seg[lfirst];
+        *last = t.seg[llast + 1];
+        return;
+    }
     *first = lfirst * t.F;
     const uint64_t e = (llast + 1) * t.F;
     *last = e < t.I ? e : t.I;
+}
+
+// rows [first, last) of the in-order leaf l
+__host__ __device__ __forceinline__ void leaf_rows(const Topo& t, uint64_t l, uint64_t* first, uint64_t* last) {
+    if (t.seg) {
+        *first = t.seg[l];
+        *last = t.seg[l + 1];
+        return;
+    }
+    *first = l * t.F;
+    *last = *first + t.F < t.I ? *first + t.F : t.I;
 }
 
 // packed upper-triangle index, segment_tree_sampler.hpp:111-115 (a <= b)

@@ -20,12 +20,15 @@ struct TreeBuildArgs {
     cudaStream_t stream;
     int force_generic;   // test hook: use the scalar kernel
     uint64_t F = 0;      // leaf capacity (0: F = R, the KrpSampler trees)
+    const uint64_t* segs = nullptr;  // variable leaf segments (L + 1 device offsets; host copy in segs_h)
+    const uint64_t* segs_h = nullptr;
+    uint64_t nleaves = 0;
     uint32_t parts = 1;  // > 1: build only subtree `part` of `parts` (a power of two)
     uint32_t part = 0;
     double* subroot = nullptr;  // partitioned build: receives the subtree root Gram (P)
 };
 // doubles needed for (tbuf_a, tbuf_b)
-void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b, uint64_t F = 0);
+void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b, uint64_t F = 0, uint64_t nleaves = 0);
 // leaf / first-pair level (DMMA) then the remaining levels; returns #launches (< 0: CUDA error)
 int launch_tree_leaves(const TreeBuildArgs& a);
 int launch_tree_levels(const TreeBuildArgs& a);
@@ -63,6 +66,8 @@ struct DrawArgs {
     uint64_t counter = 1;
     const double* yv = nullptr;
     uint64_t* idx64 = nullptr;
+    const uint64_t* segs = nullptr;      // variable leaf segments (L + 1 offsets, device), nullable
+    uint64_t nleaves = 0;
     const uint64_t* keys = nullptr;      // per-draw CounterRng keys (nullable: derive from seed)
     const uint64_t* counters = nullptr;  // per-draw counters (nullable: `counter`)
 };
@@ -119,7 +124,8 @@ void launch_conditional_probs(const void* U, uint32_t storage, uint64_t I, uint3
 
 // ---- updates (segment_tree_sampler.cpp:358-409) ----
 // for each touched row: patch u'u'^T - uu^T into every stored node on its path
-void launch_row_deltas(double* compact, uint64_t I, uint32_t R, uint64_t F, uint64_t nrows,
+void launch_row_deltas(double* compact, uint64_t I, uint32_t R, uint64_t F, const uint64_t* segs, uint64_t nleaves,
+                       uint64_t nrows,
                        const uint64_t* rows, const double* old_rows, const double* new_rows,
                        cudaStream_t s);
 void launch_scatter_rows(void* U, uint32_t storage, uint32_t R, uint64_t nrows,

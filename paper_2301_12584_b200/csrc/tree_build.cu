@@ -30,10 +30,23 @@ struct PosGeom {
     uint64_t I, F, npos, hb, pos_node0, left_slot0;
     uint64_t p0, p1;  // positions processed by this launch: [p0, p1) (a partition's subtree)
     uint32_t R, P;
+    const uint64_t* seg;  // variable leaf segments (device, L + 1 offsets) or null
 };
 
 __host__ __device__ __forceinline__ void pos_rows(const PosGeom& g, uint64_t j, uint64_t& r0,
                                                   uint64_t& rs, uint64_t& r1) {
+    if (g.seg) {  // in-order leaves: bottom pairs first, then the singles one level up
+        if (j < g.hb) {
+            r0 = g.seg[2 * j];
+            rs = g.seg[2 * j + 1];
+            r1 = g.seg[2 * j + 2];
+        } else {
+            r0 = g.seg[j + g.hb];
+            rs = ~uint64_t{0};
+            r1 = g.seg[j + g.hb + 1];
+        }
+        return;
+    }
     if (j < g.hb) {  // pair of bottom-level leaves 2j, 2j+1
         r0 = 2 * j * g.F;
         rs = r0 + g.F;
@@ -45,10 +58,11 @@ __host__ __device__ __forceinline__ void pos_rows(const PosGeom& g, uint64_t j, 
     }
 }
 
-PosGeom make_geom(uint64_t I, uint32_t R, uint64_t F = 0) {
+PosGeom make_geom(uint64_t I, uint32_t R, uint64_t F = 0, uint64_t nleaves = 0, const uint64_t* seg = nullptr) {
     if (!F) F = R;
-    const Topo t = make_topo(I, F);
+    const Topo t = nleaves ? make_topo_segments(I, nleaves, seg) : make_topo(I, F);
     PosGeom g;
+    g.seg = nleaves ? seg : nullptr;
     g.I = I;
     g.F = F;
     g.R = R;
@@ -493,7 +507,7 @@ void launch_big(const T* U, const PosGeom& g, double* compact, double* tout, cud
 template <typename T>
 void launch_leaf(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s,
                  bool generic) {
-    if (g.F % 8 != 0) generic = true;  // the DMMA kernels stream leaves in 8-row chunks
+    if (g.F % 8 != 0 || g.seg) generic = true;  // the DMMA kernels stream uniform leaves in 8-row chunks
     if (!generic) {
         switch (g.R) {
             case 96: return launch_big<96, T>(U, g, compact, tout, s);
@@ -531,14 +545,14 @@ void tree_partition_rows(uint64_t I, uint32_t R, uint32_t parts, uint32_t part, 
     *last = r1;
 }
 
-void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b, uint64_t F) {
-    const PosGeom g = make_geom(I, R, F);
+void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b, uint64_t F, uint64_t nleaves) {
+    const PosGeom g = make_geom(I, R, F, nleaves);
     *a = g.npos > 1 ? g.npos * g.P : 0;
     *b = g.npos > 2 ? (g.npos / 2) * g.P : 0;
 }
 
 int launch_tree_leaves(const TreeBuildArgs& a) {
-    PosGeom g = make_geom(a.I, a.R, a.F);
+    PosGeom g = make_geom(a.I, a.R, a.F, a.nleaves, a.segs);
     if (a.parts > 1) {  // one partition's subtree: positions [part, part+1) * npos / parts
         const uint64_t span = g.npos / a.parts;
         g.p0 = uint64_t(a.part) * span;
@@ -556,7 +570,7 @@ int launch_tree_leaves(const TreeBuildArgs& a) {
 // root. One partition (parts = 2^gl > 1): only the partition's own nodes on
 // levels D-1 .. gl, and its subtree root Gram (level gl) is copied to a.subroot.
 int launch_tree_levels(const TreeBuildArgs& a) {
-    const PosGeom g = make_geom(a.I, a.R, a.F);
+    const PosGeom g = make_geom(a.I, a.R, a.F, a.nleaves, a.segs);
     uint32_t D = 0;
     while ((uint64_t{1} << D) < g.npos) ++D;
     uint32_t gl = 0;
@@ -586,7 +600,7 @@ int launch_tree_levels(const TreeBuildArgs& a) {
 // Top of a partitioned build: the parts = 2^gl subtree roots (parts x P, in
 // subtree order) are level gl; stores the stored ones and reduces to the root.
 int launch_tree_top(const TreeBuildArgs& a, const double* subroots) {
-    const PosGeom g = make_geom(a.I, a.R, a.F);
+    const PosGeom g = make_geom(a.I, a.R, a.F, a.nleaves, a.segs);
     uint32_t gl = 0;
     while ((1u << gl) < a.parts) ++gl;
     int launches = 0;

@@ -99,10 +99,11 @@ __global__ void k_full_gram(const T* __restrict__ U, uint64_t I, uint32_t R, uin
 
 }  // namespace
 
-void launch_row_deltas(double* compact, uint64_t I, uint32_t R, uint64_t F, uint64_t nrows, const uint64_t* rows,
-                       const double* old_rows, const double* new_rows, cudaStream_t s) {
+void launch_row_deltas(double* compact, uint64_t I, uint32_t R, uint64_t F, const uint64_t* segs, uint64_t nleaves,
+                       uint64_t nrows, const uint64_t* rows, const double* old_rows, const double* new_rows,
+                       cudaStream_t s) {
     if (!nrows) return;
-    const Topo t = make_topo(I, F ? F : R);
+    const Topo t = segs ? make_topo_segments(I, nleaves, segs) : make_topo(I, F ? F : R);
     const uint64_t threads = nrows * 32;
     k_row_deltas<<<unsigned((threads + 255) / 256), 256, 0, s>>>(compact, t, R, nrows, rows, old_rows, new_rows);
 }

@@ -150,6 +150,33 @@ def test_port_tree_matches_reference_full_layout():
             assert np.array_equal(a.row_sample(h, 5, 2, 300), b.row_sample(h, 5, 2, 300))
 
 
+def sparse_coo(I, R, density, seed):
+    rng = np.random.default_rng(seed)
+    U = np.where(rng.random((I, R)) < density, rng.standard_normal((I, R)), 0.0)
+    U[0, 0] = 1.5
+    r, c = np.nonzero(U)  # row-major order
+    return U, r, c, U[r, c]
+
+
+@ref_only
+@pytest.mark.parametrize("I,R,density", [(64, 4, 0.1), (200, 3, 0.3), (500, 5, 0.6), (40, 6, 1.0), (6, 3, 0.0)])
+def test_port_sparse_tree_matches_reference(I, R, density):
+    """from_sparse (segment_tree_sampler.cpp:67-109): the port's greedy partition over
+    densified rows gives the reference's leaves, Grams (bitwise) and draws."""
+    U, r, c, v = sparse_coo(I, R, density, I + R)
+    a = oracle.OracleTree.from_sparse(I, R, r, c, v, "port")
+    b = oracle.OracleTree.from_sparse(I, R, r, c, v, "ref", full=True)
+    assert a.node_count == b.node_count and a.leaf_count == b.leaf_count
+    for node in range(a.node_count):
+        assert a.node_segment(node) == b.node_segment(node)
+        assert np.array_equal(a.node_gram(node), b.node_gram(node))
+    for lf in range(a.leaf_count):
+        f, l = int(a.offsets[lf]), int(a.offsets[lf + 1])
+        assert (np.count_nonzero(U[f:l]) <= R * R) or (l - f == 1)
+    h = oracle.random_matrix(1, R, 8)[0]
+    assert np.array_equal(a.row_sample(h, 5, 2, 300), b.row_sample(h, 5, 2, 300))
+
+
 @ref_only
 def test_port_eigh_matches_reference():
     port, ref = oracle.backend("port"), oracle.backend("ref")

@@ -1,9 +1,8 @@
 """The reference's OWN unit tests (test_krp_sampler.cpp, test_segment_tree.cpp,
 test_rng.cpp, test_sketch.cpp), compiled unmodified against the B200 drop-in headers and libkrpg.so
 (oracle/Makefile target `_ref/refsuite`, built where /root/reference exists), run
-on the device. The five sparse-construction cases exercise
-SegmentTreeSampler::from_sparse, which is out of this port's scope (SURVEY 8(f)
-rank 4) and are skipped by name."""
+on the device -- all cases, the five sparse-construction ones (from_sparse over
+variable leaf segments) included."""
 import os
 import subprocess
 
@@ -11,7 +10,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "oracle", "_ref", "refsuite")
-SKIP = "sparse"
+SKIP = ""
 
 
 @pytest.mark.gpu
