@@ -196,6 +196,24 @@ int krpg_sts_solve(krpg_t h, krpg_tensor_t T, uint32_t j, uint64_t J, uint64_t s
  * distinct sampled fibers, tensor entries visited by the scatter */
 int krpg_sts_last_stats(krpg_t h, uint64_t* stats);
 
+/* ---- CP-ARLS-LEV product-of-leverage sampler (sketch.cpp:86-149, §8(f) rank 3) ----
+ * Each included factor drawn independently from its own normalised leverage scores
+ * p_i = u_i^T pinv(G_k) u_i (cumulative-table inversion, draw_from_cumulative
+ * :19-26, CounterRng(seed, draw_offset + d), one uniform per included factor in
+ * order); probability = product of the p; rows = Hadamard of the drawn rows.
+ * idx: J x N (excluded column 0xFFFFFFFF); prob J; rows J x R; margin (nullable) J:
+ * smallest |cum - target| (normalised) over every pick. The handle form uses the
+ * resident factors and their cached Grams; the _factors form takes host factors
+ * (fp64, row-major) and forms gram(U) on the device, as the reference's free
+ * function does. */
+int krpg_product_lev_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t draw_offset,
+                            uint32_t* idx, double* prob, double* rows, double* margin);
+int krpg_product_lev_sample_factors(const double* const* factors, const uint64_t* I, uint32_t N, uint32_t R,
+                                    int64_t excluded, uint64_t J, uint64_t seed, int device, uint32_t* idx,
+                                    double* prob, double* rows, double* margin);
+/* unnormalised leverage scores u_i^T pinv(G_j) u_i of every row of factor j (out: I_j) */
+int krpg_leverage_scores(krpg_t h, uint32_t j, double* out);
+
 /* ---- standalone segment tree (SegmentTreeSampler, segment_tree_sampler.hpp:26-139) ----
  * The tree over U (I x R, host, row-major) with leaf capacity F and a fixed PSD Y,
  * rank-1 (y, R) or general (Y, R x R): give exactly one. Device build identical to

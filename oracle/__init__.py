@@ -138,6 +138,21 @@ class _Backend:
         self.check(self.fn("leverage")(ptrs, I, _u32(len(fs)), _u32(R), _dptr(out)))
         return out
 
+    def product_lev_sample(self, factors, excluded, J, seed):
+        """CP-ARLS-LEV product_lev_sample (sketch.cpp:86-149): indices (J x N,
+        excluded column 0xFFFFFFFF), probabilities, rows, margins (port only)."""
+        fs = [_c64(f) for f in factors]
+        N, R = len(fs), fs[0].shape[1]
+        I = (_u64 * N)(*[f.shape[0] for f in fs])
+        ptrs = (_dp * N)(*[_dptr(f) for f in fs])
+        idx = np.empty((J, N), dtype=np.uint32)
+        prob, rows, mg = np.empty(J), np.empty((J, R)), np.empty(J)
+        e = -1 if excluded is None else int(excluded)
+        self.check(self.fn("product_lev_sample")(ptrs, I, _u32(N), _u32(R), _i64(e), _u64(J), _u64(seed),
+                                                  idx.ctypes.data_as(C.POINTER(_u32)), _dptr(prob), _dptr(rows),
+                                                  _dptr(mg)))
+        return idx, prob, rows, mg
+
     def sampling_weights(self, prob, J):
         prob = _c64(prob)
         w = np.empty_like(prob)

@@ -928,3 +928,89 @@ int ko_sampling_weights(const double* prob, uint64_t n, uint64_t J, double* w) {
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* CP-ARLS-LEV product sampler — sketch.cpp:86-149                           */
+/* ------------------------------------------------------------------------ */
+/* Per included factor: p_i = u_i^T pinv(gram(U)) u_i (quadratic_form order),
+ * normalised by their sequential sum, cumulative table by a sequential running
+ * sum (:104-122). Draw d: CounterRng(seed, d), per included factor in order one
+ * uniform, t = min(lower_bound(cum, u * cum.back()), I - 1) (:19-26); prob = prod
+ * p[t], rows = Hadamard of the drawn rows (:133-145). margin (nullable, J): per
+ * draw the smallest |cum[x] - target| over the two bin edges of every pick. */
+int ko_product_lev_sample(const double* const* U, const uint64_t* I, uint32_t N, uint32_t R, int64_t excluded,
+                          uint64_t J, uint64_t seed, uint32_t* idx, double* prob, double* rows, double* margin) {
+    if (N == 0) return fail(1, "product_lev_sample: factor list is empty");
+    if (J < 1) return fail(1, "product_lev_sample: J must be positive");
+    if (excluded >= 0 && (uint64_t)excluded >= N) return fail(1, "product_lev_sample: excluded index out of range");
+    if (N == 1 && excluded == 0) return fail(1, "product_lev_sample: no factors left after exclusion");
+    double** p = calloc(N, sizeof(double*));
+    double** c = calloc(N, sizeof(double*));
+    double* G = malloc(sizeof(double) * R * R);
+    double* Gp = malloc(sizeof(double) * R * R);
+    int rc = 0;
+    for (uint32_t k = 0; k < N && !rc; ++k) {
+        if ((int64_t)k == excluded) continue;
+        ko_gram(U[k], I[k], R, G);
+        uint64_t rk = 0;
+        rc = ko_pinv(G, R, Gp, &rk);
+        if (rc) break;
+        p[k] = malloc(sizeof(double) * I[k]);
+        c[k] = malloc(sizeof(double) * I[k]);
+        double total = 0.0;
+        for (uint64_t i = 0; i < I[k]; ++i) {
+            p[k][i] = quadratic_form(U[k] + i * R, Gp, R, U[k] + i * R);
+            total += p[k][i];
+        }
+        if (!(total > 0.0)) {
+            rc = fail(2, "product_lev_sample: zero factor");
+            break;
+        }
+        double run = 0.0;
+        for (uint64_t i = 0; i < I[k]; ++i) {
+            p[k][i] /= total;
+            run += p[k][i];
+            c[k][i] = run;
+        }
+    }
+    if (!rc) {
+#pragma omp parallel for schedule(static)
+        for (int64_t d = 0; d < (int64_t)J; ++d) {
+            rng_t rng;
+            rng_init(&rng, seed, (uint64_t)d);
+            double* h = rows + (uint64_t)d * R;
+            for (uint32_t a = 0; a < R; ++a) h[a] = 1.0;
+            double pr = 1.0, mg = INFINITY;
+            for (uint32_t k = 0; k < N; ++k) {
+                idx[(uint64_t)d * N + k] = 0xFFFFFFFFu;
+                if ((int64_t)k == excluded) continue;
+                const uint64_t n = I[k];
+                const double target = rng_uniform(&rng) * c[k][n - 1];
+                uint64_t lo = 0, hi = n; /* first x with c[x] >= target */
+                while (lo < hi) {
+                    const uint64_t mid = lo + (hi - lo) / 2;
+                    if (c[k][mid] < target) lo = mid + 1;
+                    else hi = mid;
+                }
+                const uint64_t t = lo < n - 1 ? lo : n - 1;
+                mg = fmin(mg, fabs(c[k][t] - target));
+                if (t > 0) mg = fmin(mg, fabs(c[k][t - 1] - target));
+                idx[(uint64_t)d * N + k] = (uint32_t)t;
+                pr *= p[k][t];
+                const double* r = U[k] + t * R;
+                for (uint32_t a = 0; a < R; ++a) h[a] *= r[a];
+            }
+            prob[d] = pr;
+            if (margin) margin[d] = mg;
+        }
+    }
+    for (uint32_t k = 0; k < N; ++k) {
+        free(p[k]);
+        free(c[k]);
+    }
+    free(p);
+    free(c);
+    free(G);
+    free(Gp);
+    return rc;
+}

@@ -48,6 +48,10 @@ int ko_tree_row_sample(const ko_tree* t, const double* h, uint64_t seed, uint64_
                        uint64_t n, uint64_t* out);
 int ko_tree_update_entry(ko_tree* t, uint64_t r, uint64_t c, double v);
 
+/* CP-ARLS-LEV product_lev_sample (sketch.cpp:86-149); excluded < 0: none */
+int ko_product_lev_sample(const double* const* U, const uint64_t* I, uint32_t N, uint32_t R, int64_t excluded,
+                          uint64_t J, uint64_t seed, uint32_t* idx, double* prob, double* rows, double* margin);
+
 /* KrpSampler */
 typedef struct ko_krp ko_krp;
 int ko_krp_create(const double* const* U, const uint64_t* I, uint32_t N, uint32_t R,

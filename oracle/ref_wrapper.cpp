@@ -305,6 +305,23 @@ int kref_leverage(const double* const* U, const uint64_t* I, uint32_t N, uint32_
     });
 }
 
+// ---------------- CP-ARLS-LEV product sampler (sketch.cpp:86-149) ----------------
+int kref_product_lev_sample(const double* const* U, const uint64_t* I, uint32_t N, uint32_t R, int64_t excluded,
+                            uint64_t J, uint64_t seed, uint32_t* idx, double* prob, double* rows, double* margin) {
+    return guard([&] {
+        std::vector<Matrix> fs;
+        for (uint32_t k = 0; k < N; ++k) fs.push_back(to_matrix(U[k], I[k], R));
+        std::optional<std::size_t> ex;
+        if (excluded >= 0) ex = static_cast<std::size_t>(excluded);
+        const SampleBatch b = product_lev_sample(fs, ex, J, seed);
+        std::memcpy(idx, b.indices.data(), sizeof(uint32_t) * b.indices.size());
+        std::memcpy(prob, b.probabilities.data(), sizeof(double) * J);
+        std::memcpy(rows, b.rows.data.data(), sizeof(double) * J * R);
+        if (margin)
+            for (uint64_t d = 0; d < J; ++d) margin[d] = HUGE_VAL;
+    });
+}
+
 // ---------------- STS-CP gather weights (sketch.cpp:36-52) ----------------
 int kref_sampling_weights(const double* prob, uint64_t n, uint64_t J, double* w) {
     return guard([&] {

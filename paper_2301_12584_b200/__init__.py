@@ -6,12 +6,12 @@ hand-written sm_100a CUDA behind the C ABI in include/krpg.h, with a Python
 mirror of the reference's KrpSampler API for tests and benchmarks.
 """
 from ._lib import (EXCLUDED, KrpgCudaError, KrpgError, KrpgInvalidArgument, build, lib)
-from .sampler import ConditionalDistribution, KrpSampler, RowOrder, SampleBatch, device_count
+from .sampler import ConditionalDistribution, KrpSampler, RowOrder, SampleBatch, device_count, product_lev_sample
 from .segtree import SegmentTreeSampler
 from .tensor import SparseTensor
 
 __all__ = [
     "EXCLUDED", "KrpgCudaError", "KrpgError", "KrpgInvalidArgument", "build", "lib",
     "ConditionalDistribution", "KrpSampler", "RowOrder", "SampleBatch", "device_count",
-    "SparseTensor", "SegmentTreeSampler",
+    "SparseTensor", "SegmentTreeSampler", "product_lev_sample",
 ]

@@ -92,6 +92,10 @@ _SIGS = {
     "krpg_tensor_entries": ([_vp, C.POINTER(_u32), _dp], _int),
     "krpg_sts_solve": ([_vp, _vp, _u32, _u64, _u64, _dp], _int),
     "krpg_sts_last_stats": ([_vp, C.POINTER(_u64)], _int),
+    "krpg_product_lev_sample": ([_vp, C.c_int64, _u64, _u64, _u64, C.POINTER(_u32), _dp, _dp, _dp], _int),
+    "krpg_product_lev_sample_factors": ([C.POINTER(_dp), C.POINTER(_u64), _u32, _u32, C.c_int64, _u64, _u64, _int,
+                                         C.POINTER(_u32), _dp, _dp, _dp], _int),
+    "krpg_leverage_scores": ([_vp, _u32, _dp], _int),
     "krpg_segtree_create": ([_dp, _u64, _u32, _u64, _dp, _dp, _int, C.POINTER(_vp)], _int),
     "krpg_segtree_create_segments": ([_dp, _u64, _u32, C.POINTER(_u64), _u64, _dp, _dp, _int, C.POINTER(_vp)], _int),
     "krpg_segtree_leaf_offsets": ([_vp, C.POINTER(_u64)], _int),

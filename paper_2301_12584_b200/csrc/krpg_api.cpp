@@ -154,6 +154,7 @@ struct krpg_sampler {
     float last_build_ms = 0.f;
     std::mutex mu;
     DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf, gstate, zbuf, stswork;
+    DevBuf levtab, levwork, levg;  // product_lev_sample: per-factor tables, scan work, pseudo-inverses
     uint64_t sts_stats[4] = {0, 0, 0, 0};  // last STS step: draws hitting a nonzero fiber, fibers, entries
     PinBuf up[2], errh;       // operand staging is double-buffered (async calls)
     cudaEvent_t up_ev[2] = {nullptr, nullptr};
@@ -749,6 +750,82 @@ struct krpg_segtree {
     }
 };
 
+// ---- CP-ARLS-LEV product sampler (sketch.cpp:86-149) ----
+// Factors U[k] on the device (storage dtype), G[k] = their Grams on the host
+// (R x R; only included factors are read). Outputs are device pointers.
+namespace {
+struct LevBufs {
+    DevBuf *tab, *work, *g;
+};
+void product_lev_device(cudaStream_t s, LevBufs b, uint32_t N, uint32_t R, uint32_t storage,
+                        const std::vector<const void*>& U, const std::vector<uint64_t>& I,
+                        const std::vector<const double*>& G, int64_t excluded, uint64_t J, uint64_t seed,
+                        uint64_t draw_offset, uint32_t* d_idx, double* d_prob, double* d_rows, double* d_margin) {
+    std::vector<uint32_t> inc;
+    for (uint32_t k = 0; k < N; ++k)
+        if (excluded < 0 || uint32_t(excluded) != k) inc.push_back(k);
+    require(!inc.empty(), "product_lev_sample: no factors left after exclusion");
+    require(inc.size() <= krpg::LEV_MAX_FACTORS, "product_lev_sample: at most 16 included factors on device");
+    const uint64_t P = uint64_t(R) * (R + 1) / 2, RR = uint64_t(R) * R;
+    uint64_t tab = 0;
+    size_t work = 0;
+    for (uint32_t k : inc) {
+        if (I[k] == 0) throw std::runtime_error("product_lev_sample: zero factor");
+        tab += 2 * I[k];
+        work = std::max(work, krpg::lev_scan_work_bytes(I[k]));
+    }
+    // host: G+ = pinv_psd(G_k) (dense_kernels.cpp:207), packed and dense
+    const size_t gstride = P + RR;
+    std::vector<double> gh(inc.size() * gstride);
+    for (size_t q = 0; q < inc.size(); ++q) {
+        const std::vector<double> gp = krpg::pinv_from_eigen(krpg::eigh_psd(G[inc[q]], R));
+        const std::vector<double> pk = krpg::pack_upper(gp.data(), R);
+        std::copy(pk.begin(), pk.end(), gh.begin() + q * gstride);
+        std::copy(gp.begin(), gp.end(), gh.begin() + q * gstride + P);
+    }
+    double* dg = static_cast<double*>(b.g->ensure(8 * gh.size()));
+    CK(cudaMemcpyAsync(dg, gh.data(), 8 * gh.size(), cudaMemcpyHostToDevice, s));
+    double* dt = static_cast<double*>(b.tab->ensure(8 * tab));
+    void* dw = b.work->ensure(work + 16);
+    krpg::LevDrawArgs a;
+    a.N = N;
+    a.ninc = uint32_t(inc.size());
+    a.R = R;
+    a.storage = storage;
+    a.J = J;
+    a.seed = seed;
+    a.draw_offset = draw_offset;
+    uint64_t off = 0;
+    for (size_t q = 0; q < inc.size(); ++q) {
+        const uint32_t k = inc[q];
+        double* p = dt + off;
+        double* cum = p + I[k];
+        off += 2 * I[k];
+        krpg::launch_row_leverage(U[k], storage, I[k], R, dg + q * gstride, dg + q * gstride + P, p, s);
+        if (krpg::launch_lev_scan(p, cum, I[k], dw, work + 16, s) < 0) throw CudaError("product_lev_sample: scan failed");
+        a.inc[q] = k;
+        a.p[q] = p;
+        a.cum[q] = cum;
+        a.U[q] = U[k];
+        a.I[q] = I[k];
+    }
+    CK(cudaGetLastError());
+    // totals (the reference's "zero factor" check, :113) before any draw
+    std::vector<double> tot(inc.size());
+    for (size_t q = 0; q < inc.size(); ++q)
+        CK(cudaMemcpyAsync(&tot[q], a.cum[q] + a.I[q] - 1, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (double t : tot)
+        if (!(t > 0.0)) throw std::runtime_error("product_lev_sample: zero factor");
+    a.idx = d_idx;
+    a.prob = d_prob;
+    a.rows = d_rows;
+    a.margin = d_margin;
+    krpg::launch_lev_draws(a, s);
+    CK(cudaGetLastError());
+}
+}  // namespace
+
 extern "C" {
 
 const char* krpg_last_error(void) { return g_err.c_str(); }
@@ -1214,7 +1291,7 @@ int krpg_destroy(krpg_t h) {
         F.tree.release();
     }
     for (DevBuf* b : {&h->tbuf, &h->small, &h->Q, &h->err, &h->sH, &h->sIdx, &h->sProb, &h->sMargin, &h->rowbuf, &h->stswork,
-                      &h->gstate, &h->zbuf})
+                      &h->gstate, &h->zbuf, &h->levtab, &h->levwork, &h->levg})
         b->release();
     for (int i = 0; i < 2; ++i) {
         h->up[i].release();
@@ -1328,6 +1405,121 @@ int krpg_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t 
         if (rows) CK(cudaMemcpyAsync(rows, dr, 8 * J * h->R, cudaMemcpyDeviceToHost, h->stream));
         if (margin) CK(cudaMemcpyAsync(margin, dm, 8 * J, cudaMemcpyDeviceToHost, h->stream));
         h->sync_check();
+    });
+}
+
+int krpg_product_lev_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t draw_offset,
+                            uint32_t* idx, double* prob, double* rows, double* margin) {
+    return guard([&] {
+        require(h, "krpg: null handle");
+        require(J >= 1, "product_lev_sample: J must be positive");
+        if (excluded >= 0) require(uint64_t(excluded) < h->N, "product_lev_sample: excluded index out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->sync_check();  // drain async calls before the synchronous path
+        std::vector<const void*> U(h->N);
+        std::vector<uint64_t> I(h->N);
+        std::vector<const double*> G(h->N);
+        for (uint32_t k = 0; k < h->N; ++k) {
+            U[k] = h->f[k].U.p;
+            I[k] = h->f[k].I;
+            G[k] = h->f[k].G.data();
+        }
+        uint32_t* di = static_cast<uint32_t*>(h->sIdx.ensure(4 * J * h->N));
+        double* dp = prob ? static_cast<double*>(h->sProb.ensure(8 * J)) : nullptr;
+        double* dr = rows ? static_cast<double*>(h->sH.ensure(8 * J * h->R)) : nullptr;
+        double* dm = margin ? static_cast<double*>(h->sMargin.ensure(8 * J)) : nullptr;
+        cudaEvent_t t0 = h->pbegin();
+        product_lev_device(h->stream, {&h->levtab, &h->levwork, &h->levg}, h->N, h->R, h->storage, U, I, G, excluded,
+                           J, seed, draw_offset, di, dp, dr, dm);
+        h->pend(KRPG_PROF_OTHER, t0, 0);
+        if (idx) CK(cudaMemcpyAsync(idx, di, 4 * J * h->N, cudaMemcpyDeviceToHost, h->stream));
+        if (prob) CK(cudaMemcpyAsync(prob, dp, 8 * J, cudaMemcpyDeviceToHost, h->stream));
+        if (rows) CK(cudaMemcpyAsync(rows, dr, 8 * J * h->R, cudaMemcpyDeviceToHost, h->stream));
+        if (margin) CK(cudaMemcpyAsync(margin, dm, 8 * J, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->prof_on) h->presolve();
+    });
+}
+
+int krpg_product_lev_sample_factors(const double* const* factors, const uint64_t* I, uint32_t N, uint32_t R,
+                                    int64_t excluded, uint64_t J, uint64_t seed, int device, uint32_t* idx,
+                                    double* prob, double* rows, double* margin) {
+    return guard([&] {
+        // validation and messages as sketch.cpp:89-100
+        require(N >= 1, "product_lev_sample: factor list is empty");
+        require(J >= 1, "product_lev_sample: J must be positive");
+        if (excluded >= 0) require(uint64_t(excluded) < N, "product_lev_sample: excluded index out of range");
+        require(R >= 1 && R <= 256, "krpg: rank must be in [1, 256] on device");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, "krpg: no such CUDA device");
+        CK(cudaSetDevice(device));
+        cudaStream_t s = nullptr;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        std::vector<DevBuf> dU(N);
+        DevBuf tab, work, g, gram, o_idx, o_prob, o_rows, o_m;
+        auto cleanup = [&] {
+            cudaStreamSynchronize(s);
+            for (DevBuf& b : dU) b.release();
+            for (DevBuf* b : {&tab, &work, &g, &gram, &o_idx, &o_prob, &o_rows, &o_m}) b->release();
+            cudaStreamDestroy(s);
+        };
+        try {
+            std::vector<const void*> U(N, nullptr);
+            std::vector<std::vector<double>> Gh(N);
+            std::vector<const double*> G(N, nullptr);
+            double* dgram = static_cast<double*>(gram.ensure(8 * size_t(R) * R));
+            for (uint32_t k = 0; k < N; ++k) {
+                if (excluded >= 0 && uint32_t(excluded) == k) continue;
+                if (I[k] == 0) throw std::runtime_error("product_lev_sample: zero factor");
+                U[k] = dU[k].ensure(8 * I[k] * R);
+                CK(cudaMemcpyAsync(dU[k].p, factors[k], 8 * I[k] * R, cudaMemcpyHostToDevice, s));
+                // gram(U) (dense_kernels.cpp:19-42) on the device
+                krpg::launch_full_gram(U[k], KRPG_STORE_F64, I[k], R, dgram, s);
+                Gh[k].resize(size_t(R) * R);
+                CK(cudaMemcpyAsync(Gh[k].data(), dgram, 8 * size_t(R) * R, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                G[k] = Gh[k].data();
+            }
+            std::vector<uint64_t> Iv(I, I + N);
+            uint32_t* di = static_cast<uint32_t*>(o_idx.ensure(4 * J * N));
+            double* dp = static_cast<double*>(o_prob.ensure(8 * J));
+            double* dr = static_cast<double*>(o_rows.ensure(8 * J * R));
+            double* dm = margin ? static_cast<double*>(o_m.ensure(8 * J)) : nullptr;
+            product_lev_device(s, {&tab, &work, &g}, N, R, KRPG_STORE_F64, U, Iv, G, excluded, J, seed, 0, di, dp, dr,
+                               dm);
+            if (idx) CK(cudaMemcpyAsync(idx, di, 4 * J * N, cudaMemcpyDeviceToHost, s));
+            if (prob) CK(cudaMemcpyAsync(prob, dp, 8 * J, cudaMemcpyDeviceToHost, s));
+            if (rows) CK(cudaMemcpyAsync(rows, dr, 8 * J * R, cudaMemcpyDeviceToHost, s));
+            if (margin) CK(cudaMemcpyAsync(margin, dm, 8 * J, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
+}
+
+int krpg_leverage_scores(krpg_t h, uint32_t j, double* out) {
+    return guard([&] {
+        require(h && j < h->N, "leverage_scores: index out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->sync_check();
+        const uint32_t R = h->R;
+        const uint64_t P = uint64_t(R) * (R + 1) / 2, I = h->f[j].I;
+        const std::vector<double> gp = krpg::pinv_from_eigen(krpg::eigh_psd(h->f[j].G.data(), R));
+        std::vector<double> gh = krpg::pack_upper(gp.data(), R);
+        gh.insert(gh.end(), gp.begin(), gp.end());
+        double* dg = static_cast<double*>(h->levg.ensure(8 * gh.size()));
+        CK(cudaMemcpyAsync(dg, gh.data(), 8 * gh.size(), cudaMemcpyHostToDevice, h->stream));
+        double* dp = static_cast<double*>(h->levtab.ensure(8 * I));
+        krpg::launch_row_leverage(h->f[j].U.p, h->storage, I, R, dg, dg + P, dp, h->stream);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, dp, 8 * I, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
     });
 }
 

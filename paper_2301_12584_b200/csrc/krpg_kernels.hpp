@@ -170,4 +170,27 @@ void launch_sts_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, con
 void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const double* pinv, double* Utmp, double* nrm,
                             void* Uout, uint32_t storage, cudaStream_t s);
 
+// ---- CP-ARLS-LEV product sampler (productlev.cu; sketch.cpp:86-149) ----
+// p_i = u_i^T G+ u_i for every row (DMMA for R % 8 == 0, R <= 160 from the packed
+// G+; otherwise the dense G_full, R <= 256)
+void launch_row_leverage(const void* U, uint32_t storage, uint64_t I, uint32_t R, const double* Gp_packed,
+                         const double* G_full, double* out, cudaStream_t s);
+size_t lev_scan_work_bytes(uint64_t I);
+int launch_lev_scan(const double* p, double* cum, uint64_t I, void* work, size_t work_bytes, cudaStream_t s);
+constexpr uint32_t LEV_MAX_FACTORS = 16;
+struct LevDrawArgs {
+    uint32_t N = 0, ninc = 0, R = 0, storage = 0;
+    uint64_t J = 0, seed = 0, draw_offset = 0;
+    uint32_t inc[LEV_MAX_FACTORS];        // included factor ids, in order
+    const double* p[LEV_MAX_FACTORS];     // unnormalised masses per included factor
+    const double* cum[LEV_MAX_FACTORS];   // their inclusive prefix sums
+    const void* U[LEV_MAX_FACTORS];       // factor rows (storage dtype)
+    uint64_t I[LEV_MAX_FACTORS];
+    uint32_t* idx = nullptr;  // J x N (excluded column 0xFFFFFFFF)
+    double* prob = nullptr;   // J (nullable)
+    double* rows = nullptr;   // J x R (nullable)
+    double* margin = nullptr; // J (nullable): min |cum - target| / cum_last over every pick
+};
+int launch_lev_draws(const LevDrawArgs& a, cudaStream_t s);
+
 }  // namespace krpg

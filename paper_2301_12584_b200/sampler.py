@@ -221,6 +221,33 @@ class KrpSampler:
                          for k in range(N)], dtype=np.uint64)
         return SampleBatch(excluded, J, N, dims, idx, prob, rows, mg)
 
+    def product_lev_sample(self, excluded: Optional[int], J: int, seed: int, *, draw_offset: int = 0,
+                           margin: bool = False) -> SampleBatch:
+        """CP-ARLS-LEV baseline (sketch.cpp:86-149) over the resident factors: each
+        included mode drawn from its own normalised leverage scores."""
+        if J < 1:
+            raise KrpgInvalidArgument("product_lev_sample: J must be positive")
+        e = -1 if excluded is None else int(excluded)
+        if e < -1:
+            raise KrpgInvalidArgument("product_lev_sample: excluded index out of range")
+        N, R = self._N, self._R
+        idx = _host_array((J, N), np.uint32)
+        prob = _host_array((J,), np.float64)
+        rows = _host_array((J, R), np.float64)
+        mg = _host_array((J,), np.float64) if margin else None
+        check(_lib.lib().krpg_product_lev_sample(self._h, e, J, seed, draw_offset,
+                                                 idx.ctypes.data_as(C.POINTER(C.c_uint32)), _ptr(prob),
+                                                 _ptr(rows), _ptr(mg) if mg is not None else None))
+        dims = np.array([0 if (excluded is not None and k == excluded) else self._dims[k]
+                         for k in range(N)], dtype=np.uint64)
+        return SampleBatch(excluded, J, N, dims, idx, prob, rows, mg)
+
+    def leverage_scores(self, j: int) -> np.ndarray:
+        """u_i^T pinv(G_j) u_i for every row of factor j (unnormalised; sums to rank)."""
+        out = np.empty(int(self._dims[j]))
+        check(_lib.lib().krpg_leverage_scores(self._h, j, _ptr(out)))
+        return out
+
     def sample_device(self, excluded: Optional[int], J: int, seed: int, idx=None, prob=None,
                       rows=None, margin=None, *, mode: str = "two_stage", draw_offset: int = 0) -> None:
         """Device-resident outputs (torch CUDA tensors or None)."""
@@ -358,6 +385,30 @@ class KrpSampler:
 
     def validate(self, tol: float = 1e-10) -> None:
         check(_lib.lib().krpg_validate(self._h, tol))
+
+
+def product_lev_sample(factors: Sequence, excluded: Optional[int], J: int, seed: int, *, device: int = 0,
+                       margin: bool = False) -> SampleBatch:
+    """Free-function CP-ARLS-LEV sampler (sketch.cpp:86-149) over host factors: the
+    factors are copied to the device, gram(U) is formed there, nothing persists."""
+    if len(factors) == 0:
+        raise KrpgInvalidArgument("product_lev_sample: factor list is empty")
+    fs = [_f64(f) for f in factors]
+    N, R = len(fs), fs[0].shape[1]
+    e = -1 if excluded is None else int(excluded)
+    for k, f in enumerate(fs):
+        if k != e and f.shape[1] != R:
+            raise KrpgInvalidArgument("product_lev_sample: inconsistent column counts")
+    I = (C.c_uint64 * N)(*[f.shape[0] for f in fs])
+    ptrs = (C.POINTER(C.c_double) * N)(*[_ptr(f) for f in fs])
+    idx = np.empty((J, N), dtype=np.uint32)
+    prob, rows = np.empty(J), np.empty((J, R))
+    mg = np.empty(J) if margin else None
+    check(_lib.lib().krpg_product_lev_sample_factors(ptrs, I, N, R, e, J, seed, device,
+                                                     idx.ctypes.data_as(C.POINTER(C.c_uint32)), _ptr(prob),
+                                                     _ptr(rows), _ptr(mg) if mg is not None else None))
+    dims = np.array([0 if k == e else f.shape[0] for k, f in enumerate(fs)], dtype=np.uint64)
+    return SampleBatch(excluded, J, N, dims, idx, prob, rows, mg)
 
 
 def device_count() -> int:

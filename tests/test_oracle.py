@@ -178,6 +178,19 @@ def test_port_sparse_tree_matches_reference(I, R, density):
 
 
 @ref_only
+@pytest.mark.parametrize("excluded", [None, 0, 2])
+def test_port_product_lev_matches_reference(excluded):
+    """CP-ARLS-LEV product_lev_sample (sketch.cpp:86-149): the port's restatement is
+    bitwise the reference's (indices, probabilities, rows)."""
+    fs = [oracle.random_matrix(n, 6, 700 + n) for n in (40, 90, 17)]
+    fs[1][::7] *= 10.0
+    a = oracle.backend("port").product_lev_sample(fs, excluded, 3000, 31)
+    b = oracle.backend("ref").product_lev_sample(fs, excluded, 3000, 31)
+    for x, y in zip(a[:3], b[:3]):
+        assert np.array_equal(x, y)
+
+
+@ref_only
 def test_port_eigh_matches_reference():
     port, ref = oracle.backend("port"), oracle.backend("ref")
     for n in (1, 2, 5, 16, 33):
