@@ -155,6 +155,8 @@ struct krpg_sampler {
     std::mutex mu;
     DevBuf tbuf, small, Q, err, sH, sIdx, sProb, sMargin, rowbuf, gstate, zbuf, stswork;
     DevBuf levtab, levwork, levg;  // product_lev_sample: per-factor tables, scan work, pseudo-inverses
+    DevBuf gramwork;               // launch_full_gram partials
+    double* gram_work() { return static_cast<double*>(gramwork.ensure(8 * krpg::full_gram_work_doubles(R))); }
     uint64_t sts_stats[4] = {0, 0, 0, 0};  // last STS step: draws hitting a nonzero fiber, fibers, entries
     PinBuf up[2], errh;       // operand staging is double-buffered (async calls)
     cudaEvent_t up_ev[2] = {nullptr, nullptr};
@@ -671,7 +673,7 @@ void krpg_sampler::sts_solve(krpg_tensor& T, uint32_t j, uint64_t J, uint64_t se
     cudaEvent_t t_sts = pbegin();
     krpg::launch_gather_sa(dp, dr, J, R, w, sa, derr, stream);
     CK(cudaMemsetAsync(gs, 0, 8 * size_t(R) * R, stream));
-    krpg::launch_full_gram(sa, KRPG_STORE_F64, J, R, gs, stream);
+    krpg::launch_full_gram(sa, KRPG_STORE_F64, J, R, gs, gram_work(), stream);
     pend(KRPG_PROF_STS, t_sts, 3);
     // 3) sampled_rhs_rows + gram_cross(sa, sb), sparse (overlaps the host pinv below)
     CK(cudaStreamSynchronize(T.stream));
@@ -1291,7 +1293,7 @@ int krpg_destroy(krpg_t h) {
         F.tree.release();
     }
     for (DevBuf* b : {&h->tbuf, &h->small, &h->Q, &h->err, &h->sH, &h->sIdx, &h->sProb, &h->sMargin, &h->rowbuf, &h->stswork,
-                      &h->gstate, &h->zbuf, &h->levtab, &h->levwork, &h->levg})
+                      &h->gstate, &h->zbuf, &h->levtab, &h->levwork, &h->levg, &h->gramwork})
         b->release();
     for (int i = 0; i < 2; ++i) {
         h->up[i].release();
@@ -1458,11 +1460,11 @@ int krpg_product_lev_sample_factors(const double* const* factors, const uint64_t
         cudaStream_t s = nullptr;
         CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         std::vector<DevBuf> dU(N);
-        DevBuf tab, work, g, gram, o_idx, o_prob, o_rows, o_m;
+        DevBuf tab, work, g, gram, gwork, o_idx, o_prob, o_rows, o_m;
         auto cleanup = [&] {
             cudaStreamSynchronize(s);
             for (DevBuf& b : dU) b.release();
-            for (DevBuf* b : {&tab, &work, &g, &gram, &o_idx, &o_prob, &o_rows, &o_m}) b->release();
+            for (DevBuf* b : {&tab, &work, &g, &gram, &gwork, &o_idx, &o_prob, &o_rows, &o_m}) b->release();
             cudaStreamDestroy(s);
         };
         try {
@@ -1470,13 +1472,14 @@ int krpg_product_lev_sample_factors(const double* const* factors, const uint64_t
             std::vector<std::vector<double>> Gh(N);
             std::vector<const double*> G(N, nullptr);
             double* dgram = static_cast<double*>(gram.ensure(8 * size_t(R) * R));
+            double* gw = static_cast<double*>(gwork.ensure(8 * krpg::full_gram_work_doubles(R)));
             for (uint32_t k = 0; k < N; ++k) {
                 if (excluded >= 0 && uint32_t(excluded) == k) continue;
                 if (I[k] == 0) throw std::runtime_error("product_lev_sample: zero factor");
                 U[k] = dU[k].ensure(8 * I[k] * R);
                 CK(cudaMemcpyAsync(dU[k].p, factors[k], 8 * I[k] * R, cudaMemcpyHostToDevice, s));
                 // gram(U) (dense_kernels.cpp:19-42) on the device
-                krpg::launch_full_gram(U[k], KRPG_STORE_F64, I[k], R, dgram, s);
+                krpg::launch_full_gram(U[k], KRPG_STORE_F64, I[k], R, dgram, gw, s);
                 Gh[k].resize(size_t(R) * R);
                 CK(cudaMemcpyAsync(Gh[k].data(), dgram, 8 * size_t(R) * R, cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
@@ -1723,7 +1726,7 @@ int krpg_validate(krpg_t h, double tol) {
         double* d = static_cast<double*>(h->small.ensure(8 * size_t(R) * R));
         std::vector<double> fresh(size_t(R) * R), root(h->P), G(size_t(R) * R);
         for (uint32_t j = 0; j < h->N; ++j) {
-            krpg::launch_full_gram(h->f[j].U.p, h->storage, h->f[j].I, R, d, h->stream);
+            krpg::launch_full_gram(h->f[j].U.p, h->storage, h->f[j].I, R, d, h->gram_work(), h->stream);
             CK(cudaMemcpyAsync(fresh.data(), d, 8 * size_t(R) * R, cudaMemcpyDeviceToHost, h->stream));
             CK(cudaMemcpyAsync(root.data(), h->f[j].tree.p, 8 * h->P, cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));

@@ -136,8 +136,11 @@ void launch_convert_f64_to_f32(const double* in, float* out, uint64_t n, cudaStr
 void launch_convert_f32_to_f64(const float* in, double* out, uint64_t n, cudaStream_t s);
 
 // fresh Gram of a whole factor (validate): out R x R
-void launch_full_gram(const void* U, uint32_t storage, uint64_t I, uint32_t R, double* out,
+// (DMMA for R = 8..64 step 8, else scalar; deterministic ordered reduction of
+// per-CTA partials held in work: full_gram_work_doubles(R) doubles)
+void launch_full_gram(const void* U, uint32_t storage, uint64_t I, uint32_t R, double* out, double* work,
                       cudaStream_t s);
+size_t full_gram_work_doubles(uint32_t R);
 
 // ---- STS-CP solve slice (sts.cu; cp_als.cpp:282-313) ----
 // dedup + lexicographic sort of COO entries (tensor.cpp:34-75); returns nnz after
