@@ -899,6 +899,7 @@ struct DeepArgs {
     const void* U;
     const double* tree;
     Topo topo;
+    uint32_t chunk;    // sorted draws per warp (<= 32)
 };
 
 // runs with fewer draws than this use the CUDA-core quadratic form (small_qf)
@@ -1002,9 +1003,9 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
     unsigned char* buf = wbase;
     double* xs = reinterpret_cast<double*>(wbase + C::BUF);
     uint32_t* perm_sm = reinterpret_cast<uint32_t*>(wbase + C::BUF + C::XS);
-    const uint64_t base = (uint64_t(blockIdx.x) * WPB + warp) * 32;
+    const uint64_t base = (uint64_t(blockIdx.x) * WPB + warp) * a.chunk;
     if (base >= a.J) return;
-    const int cnt = a.J - base < 32ull ? int(a.J - base) : 32;
+    const int cnt = a.J - base < uint64_t(a.chunk) ? int(a.J - base) : int(a.chunk);
     const bool live = lane < cnt;
     uint32_t d = live ? a.perm[base + lane] : 0u;
     uint32_t v = live ? a.node[d] : 0xFFFFFFFFu;
@@ -1365,8 +1366,27 @@ void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, bool
     }
 }
 
+// draws per warp in the fused deep kernel: fewer than 32 gives more, shorter warp
+// work units (the kernel holds ~12 warps per SM, so 32-draw units leave a ragged tail wave)
+inline uint32_t deep_chunk() {
+    static const uint32_t c = [] {
+        const char* e = std::getenv("KRPG_DEEP_CHUNK");
+        const int v = e ? std::atoi(e) : 8;
+        return uint32_t(v >= 1 && v <= 32 ? v : 8);
+    }();
+    return c;
+}
+
 // shallow levels (many draws per node) -> cooperative CTA kernel; deep -> per-warp
-inline bool deep_level(uint64_t J, uint32_t level) { return (J >> level) < 64; }
+inline uint64_t deep_threshold() {
+    static const uint64_t t = [] {
+        const char* e = std::getenv("KRPG_DEEP_THRESHOLD");
+        const long v = e ? std::atol(e) : 64;
+        return uint64_t(v >= 1 ? v : 64);
+    }();
+    return t;
+}
+inline bool deep_level(uint64_t J, uint32_t level) { return (J >> level) < deep_threshold(); }
 
 template <int NB, typename T>
 void launch_deep2(const DeepArgs& a, unsigned grid, cudaStream_t s) {
@@ -1551,7 +1571,8 @@ int launch_position_grouped(const GroupedArgs& g) {
         da.U = g.U;
         da.tree = g.Z;
         da.topo = tz;
-        const unsigned grid = unsigned((J + 32ull * WPB - 1) / (32ull * WPB));
+        da.chunk = deep_chunk();
+        const unsigned grid = unsigned((J + uint64_t(da.chunk) * WPB - 1) / (uint64_t(da.chunk) * WPB));
         if (g.storage == 1)
             dispatch_deep<float>(R, da, grid, g.stream);
         else

@@ -9,7 +9,10 @@
 #include "krpg.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <future>
 #include <memory>
@@ -390,6 +393,7 @@ struct krpg_sampler {
                        uint32_t* d_idx, double* d_prob, double* d_rows, double* d_margin) {
         require(J >= 1, "KrpSample: sample count must be positive");
         require(mode == KRPG_MODE_TWO_STAGE || mode == KRPG_MODE_ONE_STAGE, "krpg_sample: unknown mode");
+        const auto trace_t0 = std::chrono::steady_clock::now();
         const std::vector<uint32_t> inc = included(excluded);
         const size_t RR = size_t(R) * R;
 
@@ -451,6 +455,9 @@ struct krpg_sampler {
             CK(cudaMemcpyAsync(dsmall, up_h, sizeof(double) * P, cudaMemcpyHostToDevice, stream));
         }
         stage_pos(0);
+        if (std::getenv("KRPG_HOST_TRACE"))
+            std::fprintf(stderr, "krpg_sample host: position-0 operands staged after %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - trace_t0).count());
         struct JoinAll {  // never leave eigensolver threads behind on an exception
             std::vector<std::future<krpg::Eig>>& f;
             ~JoinAll() {
@@ -1401,12 +1408,21 @@ int krpg_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t 
         double* dp = prob ? static_cast<double*>(h->sProb.ensure(8 * J)) : nullptr;
         double* dr = static_cast<double*>(h->sH.ensure(8 * J * h->R));
         double* dm = margin ? static_cast<double*>(h->sMargin.ensure(8 * J)) : nullptr;
+        static const bool trace = std::getenv("KRPG_HOST_TRACE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         h->sample_device(excluded, J, seed, draw_offset, mode, di, dp, dr, dm);
+        const auto t1 = std::chrono::steady_clock::now();
         if (idx) CK(cudaMemcpyAsync(idx, di, 4 * J * h->N, cudaMemcpyDeviceToHost, h->stream));
         if (prob) CK(cudaMemcpyAsync(prob, dp, 8 * J, cudaMemcpyDeviceToHost, h->stream));
         if (rows) CK(cudaMemcpyAsync(rows, dr, 8 * J * h->R, cudaMemcpyDeviceToHost, h->stream));
         if (margin) CK(cudaMemcpyAsync(margin, dm, 8 * J, cudaMemcpyDeviceToHost, h->stream));
         h->sync_check();
+        if (trace) {
+            const auto t2 = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "krpg_sample host: setup+launch %.3f ms, wait %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                         std::chrono::duration<double, std::milli>(t2 - t1).count());
+        }
     });
 }
 
