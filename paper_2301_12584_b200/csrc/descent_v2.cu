@@ -69,7 +69,15 @@ struct EvalArgs {
     uint32_t* nsort_out;       // node of each position of perm_out
     uint32_t* GS;           // per node position range [GS, GE) at its level
     uint32_t* GE;
+    int fake;               // timing experiments only (KRPG_FAKE_QF): 1 skip the DMMA, 2 also the loads
+    unsigned long long* trace;  // timing experiments only: per-warp phase timestamps (nullable)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 using qf::FragAddr;
 using qf::block_qf_packed;
@@ -280,6 +288,844 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
                 if (a.nsort_out) a.nsort_out[pos] = 2 * v + (s_left[t] ? 1u : 2u);
             }
             __syncthreads();
+        }
+    }
+}
+
+// ---- register-resident Gram variant (R <= 64) -----------------------------
+// Same decisions, bit-identical masses (the DMMA chain and the epilogue run in
+// exactly block_qf_packed's order), different data movement. k_eval_cta
+// re-gathers every B fragment of the packed Gram from shared memory for every
+// 8-draw block (72 dependent LDS per 72 DMMA), which held the FP64 tensor pipe
+// near 45%. Here each warp owns a contiguous range of sorted positions (at most
+// 64, sized so that the whole level is one wave of 2 CTAs x 4 warps per SM) and
+// holds ALL B fragments of its current run's Gram in registers (NB(NB+1)
+// doubles per lane, 144 registers at R = 64), loaded once per run straight from
+// global memory / L2. The draws' rows (A fragments and the epilogue) stream
+// into a per-warp 3-slot shared-memory ring by cp.async two blocks ahead, row
+// stride R + 4 doubles so the A-fragment loads are bank-conflict free. Child
+// slots are claimed with one pair of atomics per (warp, run) at the run's end.
+constexpr int RW = 4;         // warps per CTA
+constexpr int RSLOTS = 3;     // x-row ring slots per warp (8 rows each)
+constexpr int RRANGE = 64;    // max sorted positions per warp
+constexpr int RMAXBLK = RRANGE / 8 + RRANGE;  // full blocks + one partial per run
+
+template <int NB>
+struct RegCfg {
+    static constexpr int R = 8 * NB;
+    static constexpr int XS = R + 4;               // doubles per staged row
+    static constexpr int SLOT = 8 * XS;            // doubles per ring slot
+    static constexpr int NFR = NB * (NB + 1);      // B-fragment doubles per lane
+    // per warp: row ring | decision inputs u, 1/C, low, margin, root mass (f64 x RRANGE each) |
+    // per-position info, per-run node / parent range / counts / claims (u32) | block list (u16)
+    static constexpr int WARP_D = RSLOTS * SLOT + 5 * RRANGE;
+    static constexpr int WARP_U32 = RRANGE + 9 * RRANGE;
+    static constexpr size_t WARP_BYTES = size_t(WARP_D) * 8 + WARP_U32 * 4 + RMAXBLK * 2;
+    static constexpr size_t WARP_STRIDE = (WARP_BYTES + 15) / 16 * 16;
+    static constexpr size_t SMEM = RW * WARP_STRIDE;
+};
+
+// fragment (p, s, q >= p) of the register-resident Gram
+template <int NB>
+__host__ __device__ constexpr int rfrag(int p, int s, int q) {
+    return 2 * (p * NB - (p * (p - 1)) / 2) + s * (NB - p) + (q - p);
+}
+
+template <int NB>
+__device__ __forceinline__ void load_gram_frags(double (&gf)[NB * (NB + 1)], const double* __restrict__ G, int lane) {
+    constexpr int R = 8 * NB;
+    const int r4 = lane & 3, cq = lane >> 2;
+#pragma unroll
+    for (int p = 0; p < NB; ++p)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int row = 8 * p + 4 * s + r4;
+            const int col = 8 * p + cq;
+            const int rowoff = row * R - (row * (row - 1)) / 2 - row;
+            const int diag = row <= col ? rowoff + col : col * R - (col * (col - 1)) / 2 - col + row;
+            gf[rfrag<NB>(p, s, p)] = __ldg(G + diag);
+#pragma unroll
+            for (int q = p + 1; q < NB; ++q) gf[rfrag<NB>(p, s, q)] = __ldg(G + rowoff + 8 * q + cq);
+        }
+}
+
+// block_qf_packed with the B fragments in registers and the rows in shared memory
+// (xs = the block's 8 staged rows, row m valid iff valid); same operation order
+template <int NB>
+__device__ __forceinline__ double block_qf_regs(const double (&gf)[NB * (NB + 1)], const double* xs, bool valid,
+                                                int lane) {
+    constexpr int XS = RegCfg<NB>::XS;
+    const int r4 = lane & 3, m = lane >> 2;
+    const double* xr = xs + m * XS;
+    double y[NB][2];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) y[q][0] = y[q][1] = 0.0;
+#pragma unroll
+    for (int p = 0; p < NB; ++p) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const double av = valid ? xr[8 * p + 4 * s + r4] : 0.0;
+            dmma_884(y[p][0], y[p][1], av, gf[rfrag<NB>(p, s, p)]);
+            const double a2 = av + av;
+#pragma unroll
+            for (int q = p + 1; q < NB; ++q) dmma_884(y[q][0], y[q][1], a2, gf[rfrag<NB>(p, s, q)]);
+        }
+    }
+    double part = 0.0;
+    if (valid) {
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const double2 xv = *reinterpret_cast<const double2*>(xr + 8 * q + 2 * r4);
+            part = fma(xv.x, y[q][0], part);
+            part = fma(xv.y, y[q][1], part);
+        }
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    return part;
+}
+
+// Everything a warp needs besides the quadratic forms is brought in with ONE
+// latency at the start (cp.async into the warp's shared memory: positions'
+// decision inputs, the parents' position ranges of its runs) and the child
+// slots of all its runs are claimed with ONE round of atomics at the end, so
+// the only per-block waits are the DMMA chain itself.
+template <int NB, int MODE, bool ROOT0>
+__global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t range) {
+    constexpr int R = 8 * NB;
+    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
+    using C = RegCfg<NB>;
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr bool LEVEL = MODE == EV_LEVEL;
+    extern __shared__ __align__(16) unsigned char smem_regb[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    griddep_launch_dependents();
+    griddep_wait();
+    const uint64_t p0 = (uint64_t(blockIdx.x) * RW + warp) * range;
+    if (p0 >= a.J) return;
+    const int cnt = int(a.J - p0 < uint64_t(range) ? a.J - p0 : uint64_t(range));
+    unsigned long long* tr = a.trace ? a.trace + ((uint64_t(blockIdx.x) * RW + warp) * 8) : nullptr;
+    if (tr && lane == 0) tr[0] = gtimer();
+    double* ring = reinterpret_cast<double*>(smem_regb + warp * C::WARP_STRIDE);
+    double* s_u = ring + RSLOTS * C::SLOT;
+    double* s_ic = s_u + RRANGE;
+    double* s_lo = s_ic + RRANGE;
+    double* s_mg = s_lo + RRANGE;
+    double* s_root = s_mg + RRANGE;
+    uint32_t* s_info = reinterpret_cast<uint32_t*>(s_root + RRANGE);
+    uint32_t* s_rv = s_info + RRANGE;   // per run: node
+    uint32_t* s_pgs = s_rv + RRANGE;    // parent's GS / cntL / GE
+    uint32_t* s_pcl = s_pgs + RRANGE;
+    uint32_t* s_pge = s_pcl + RRANGE;
+    uint32_t* s_cl = s_pge + RRANGE;    // per run: lefts / rights in this range
+    uint32_t* s_cr = s_cl + RRANGE;
+    uint32_t* s_bl = s_cr + RRANGE;     // claimed bases
+    uint32_t* s_br = s_bl + RRANGE;
+    uint16_t* s_blk = reinterpret_cast<uint16_t*>(s_br + RRANGE);
+
+    // the warp's sorted positions p0 + lane (A) and p0 + 32 + lane (B)
+    uint32_t dA = 0, dB = 0, vA = 0xFFFFFFFFu, vB = 0xFFFFFFFFu;
+    if (lane < cnt) {
+        dA = a.perm ? a.perm[p0 + lane] : uint32_t(p0 + lane);
+        vA = (LEVEL && !ROOT0) ? (a.nsort_in ? a.nsort_in[p0 + lane] : a.node[dA]) : 0u;
+    }
+    if (lane + 32 < cnt) {
+        dB = a.perm ? a.perm[p0 + 32 + lane] : uint32_t(p0 + 32 + lane);
+        vB = (LEVEL && !ROOT0) ? (a.nsort_in ? a.nsort_in[p0 + 32 + lane] : a.node[dB]) : 0u;
+    }
+    const uint32_t upA = __shfl_up_sync(FULL, vA, 1), lastA = __shfl_sync(FULL, vA, 31);
+    const uint32_t upB = __shfl_up_sync(FULL, vB, 1);
+    const bool stA = lane < cnt && (lane == 0 || vA != upA);
+    const bool stB = lane + 32 < cnt && vB != (lane == 0 ? lastA : upB);
+    const unsigned sA = __ballot_sync(FULL, stA);
+    const unsigned sB = __ballot_sync(FULL, stB);
+    const uint64_t starts = uint64_t(sA) | (uint64_t(sB) << 32);
+    const int nruns = __popcll(static_cast<long long>(starts));
+    if (tr && lane == 0) tr[1] = gtimer();
+    auto pos_d = [&](int t) {  // every lane participates; t may differ per lane
+        const uint32_t x = __shfl_sync(FULL, dA, t & 31), y = __shfl_sync(FULL, dB, t & 31);
+        return t < 32 ? x : y;
+    };
+    auto pos_v = [&](int t) {
+        const uint32_t x = __shfl_sync(FULL, vA, t & 31), y = __shfl_sync(FULL, vB, t & 31);
+        return t < 32 ? x : y;
+    };
+    auto run_of = [&](int t) { return __popcll(static_cast<long long>(starts & ((2ull << t) - 1ull))) - 1; };
+    auto run_end = [&](int b) {
+        const uint64_t mk = starts & ~((2ull << b) - 1ull);
+        return mk ? __ffsll(static_cast<long long>(mk)) - 1 : cnt;
+    };
+
+    // decision inputs of every position and the parents' ranges of every run: one group
+    if (LEVEL) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = lane + 32 * h;
+            const uint32_t d = h ? dB : dA;
+            if (t < cnt) {
+                cp_async8(s_u + t, a.ud + d);
+                if (!ROOT0) {
+                    cp_async8(s_ic + t, a.invc + d);
+                    cp_async8(s_lo + t, a.low + d);
+                }
+                if (a.margin) cp_async8(s_mg + t, a.margin + d);
+            }
+            if (h ? stB : stA) {
+                const uint32_t v = h ? vB : vA;
+                const int r = run_of(t);
+                s_rv[r] = v;
+                if (v != 0 && !(!ROOT0 && is_leaf(a.topo, v))) {
+                    const uint32_t pp = (v - 1) >> 1;
+                    cp_async4(s_pgs + r, a.GS + pp);
+                    cp_async4(s_pcl + r, a.cntL + pp);
+                    cp_async4(s_pge + r, a.GE + pp);
+                }
+            }
+        }
+    }
+    cp_async_commit();
+
+    // block list: (b0, n) of every 8-draw block of every non-leaf run; draws
+    // parked at a leaf one level up keep their positions
+    int nblk = 0;
+    {
+        uint64_t st = starts;
+        while (st) {
+            const int rs = __ffsll(static_cast<long long>(st)) - 1;
+            st &= st - 1;
+            const int re = st ? __ffsll(static_cast<long long>(st)) - 1 : cnt;
+            if (LEVEL && !ROOT0 && is_leaf(a.topo, pos_v(rs))) continue;
+            for (int b0 = rs; b0 < re; b0 += 8) {
+                if (lane == 0) s_blk[nblk] = uint16_t(b0 | (min(8, re - b0) << 8));
+                ++nblk;
+            }
+        }
+    }
+    __syncwarp();
+
+    auto stage = [&](int i) {  // rows of block i -> ring slot i % RSLOTS (one cp.async group)
+        if (i < nblk && a.fake < 2) {
+            const uint32_t e = s_blk[i];
+            const int b0 = e & 0xff, n = e >> 8;
+            double* dst = ring + (i % RSLOTS) * C::SLOT;
+            constexpr int PPR = R / 2;  // 16-byte pieces per row
+            const uint32_t drow = pos_d(b0 + (lane & 7) < cnt ? b0 + (lane & 7) : b0);
+#pragma unroll
+            for (int base = 0; base < 8 * PPR; base += 32) {
+                const int pc = base + lane;
+                const int row = pc / PPR, k = pc - row * PPR;
+                const uint32_t dr = __shfl_sync(FULL, drow, row & 7);
+                if (row < n) cp_async16(dst + row * C::XS + 2 * k, a.X + uint64_t(dr) * R + 2 * k);
+            }
+        }
+        cp_async_commit();
+    };
+
+    double gf[C::NFR];
+    const unsigned below = (1u << lane) - 1u;
+    // one sweep over the warp's blocks against node Grams (root_pass: the root
+    // Gram, masses kept as normalisers)
+    auto sweep = [&](bool root_pass) {
+        stage(0);
+        stage(1);
+        uint32_t gv = 0xFFFFFFFFu;
+        uint32_t cl = 0, cr = 0;
+        for (int i = 0; i < nblk; ++i) {
+            stage(i + 2);
+            cp_async_wait_n<2>();
+            __syncwarp();
+            const uint32_t e = s_blk[i];
+            const int b0 = e & 0xff, n = e >> 8;
+            const uint32_t v = pos_v(b0);
+            if (v != gv && a.fake < 2) {
+                const double* G = a.tree;
+                if (LEVEL && !root_pass) G = a.tree + slot_of(2ull * v + 1) * P;
+                load_gram_frags<NB>(gf, G, lane);
+                gv = v;
+            }
+            const int m = lane >> 2;
+            const bool valid = m < n;
+            const bool owner = valid && (lane & 3) == 0;
+            const int t = b0 + m;
+            const uint32_t dd = pos_d(t < cnt ? t : b0);
+            double mass;
+            if (a.fake) {  // timing experiment: pseudo-random branch, no quadratic form
+                const uint32_t hsh = (dd * 2654435761u) ^ (v * 40503u);
+                mass = ((hsh >> 13) & 1u) ? 1e300 : 0.0;
+                if (!(LEVEL && !root_pass)) mass = 1.0;
+            } else {
+                mass = block_qf_regs<NB>(gf, ring + (i % RSLOTS) * C::SLOT, valid, lane);
+            }
+            if (root_pass) {
+                if (owner) {
+                    if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
+                    s_root[t] = mass;
+                }
+            } else if (MODE == EV_ROOT) {
+                if (owner) {
+                    if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
+                    a.invc[dd] = 1.0 / mass;
+                }
+            } else if (MODE == EV_PROB) {
+                if (owner) a.prob[dd] = mass / a.rank_div;
+            } else {
+                bool left = false;
+                if (owner) {
+                    const double u = s_u[t];
+                    double ic, cutoff;
+                    if (ROOT0) {
+                        ic = 1.0 / s_root[t];
+                        a.invc[dd] = ic;
+                        cutoff = 0.0 + ic * mass;
+                    } else {
+                        ic = s_ic[t];
+                        cutoff = s_lo[t] + ic * mass;
+                    }
+                    left = cutoff >= u;
+                    if (a.margin) a.margin[dd] = fmin(s_mg[t], fabs(cutoff - u));
+                    if (left) {
+                        a.node[dd] = 2 * v + 1;
+                    } else {
+                        a.node[dd] = 2 * v + 2;
+                        a.low[dd] = cutoff;
+                    }
+                }
+                const unsigned lm = __ballot_sync(FULL, owner && left);
+                const unsigned rm = __ballot_sync(FULL, owner && !left);
+                if (owner)
+                    s_info[t] = left ? (cl + __popc(lm & below)) | 0x80000000u : cr + __popc(rm & below);
+                cl += __popc(lm);
+                cr += __popc(rm);
+                if (b0 + n == run_end(b0)) {  // the run's last block in this range
+                    if (lane == 0) {
+                        const int r = run_of(b0);
+                        s_cl[r] = cl;
+                        s_cr[r] = cr;
+                    }
+                    cl = cr = 0;
+                }
+            }
+            __syncwarp();
+        }
+        cp_async_wait_all();
+        __syncwarp();
+    };
+    if (tr && lane == 0) tr[2] = gtimer();
+    if (ROOT0) sweep(true);
+    sweep(false);
+    if (tr && lane == 0) tr[3] = gtimer();
+    if (!LEVEL) return;
+
+    // claim child slots for every run at once (one atomic round trip), then scatter
+    for (int r = lane; r < nruns; r += 32) {
+        const uint32_t v = s_rv[r];
+        if (!ROOT0 && is_leaf(a.topo, v)) continue;
+        uint32_t gs = 0, ge = uint32_t(a.J);
+        if (v != 0) {
+            const uint32_t gl = s_pgs[r] + s_pcl[r];
+            gs = (v & 1u) ? s_pgs[r] : gl;
+            ge = (v & 1u) ? gl : s_pge[r];
+        }
+        a.GS[v] = gs;
+        a.GE[v] = ge;
+        const uint32_t nl = s_cl[r], nr = s_cr[r];
+        const uint32_t bl = nl ? atomicAdd(a.cntL + v, nl) : 0u;
+        const uint32_t br = nr ? atomicAdd(a.cntR + v, nr) : 0u;
+        s_bl[r] = gs + bl;
+        s_br[r] = ge - 1u - br;
+    }
+    __syncwarp();
+    if (tr && lane == 0) tr[4] = gtimer();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int t = lane + 32 * h;
+        if (t < cnt) {
+            const uint32_t d = h ? dB : dA, v = h ? vB : vA;
+            if (!ROOT0 && is_leaf(a.topo, v)) {
+                a.perm_out[p0 + t] = d;
+                if (a.nsort_out) a.nsort_out[p0 + t] = v;
+            } else {
+                const int r = run_of(t);
+                const uint32_t info = s_info[t];
+                const bool lf = info >> 31;
+                const uint32_t rk = info & 0x7fffffffu;
+                const uint32_t pos = lf ? s_bl[r] + rk : s_br[r] - rk;
+                a.perm_out[pos] = d;
+                if (a.nsort_out) a.nsort_out[pos] = 2 * v + (lf ? 1u : 2u);
+            }
+        }
+    }
+    if (tr && lane == 0) tr[5] = gtimer();
+}
+
+// ---- first position (h = ones): per-draw quadratic forms become tables ----
+// Before the first included factor the history h is all ones (krp_sampler.cpp
+// two-stage loop), so (a) every draw's E-tree mass at node v is the same number
+// 1^T Q_v 1, and (b) a draw's factor-tree vector z = h o V[:, u] = V[:, u]
+// depends only on its eigen-component u (R possibilities). The masses of the
+// E-tree and of the top L0 factor-tree levels are therefore computed once per
+// (node, u) -- with block_qf_packed, i.e. exactly the arithmetic the per-draw
+// kernels apply to the identical row, so every decision is bit-identical -- and
+// each draw walks those levels with table lookups. The draws are then placed in
+// node order for level L0 (counting sort) and the level kernels take over.
+constexpr int kPos0Levels = 7;  // factor-tree levels served from the table (64 x 127 masses at R = 64)
+
+template <int NB>
+__global__ void __launch_bounds__(256) k_pos0_tables(const double* __restrict__ Q, Topo te, const double* __restrict__ Zt,
+                                                     uint32_t L0, const double* __restrict__ V, double* __restrict__ etab,
+                                                     double* __restrict__ ztab, int* err) {
+    constexpr int R = 8 * NB;
+    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
+    __shared__ __align__(16) double s_vt[R * R + R];  // V^T rows (z of component u) + a ones row
+    griddep_launch_dependents();
+    griddep_wait();
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i < R * R; i += blockDim.x) {
+        const int u = i / R, c = i - u * R;
+        s_vt[i] = 1.0 * V[uint64_t(c) * R + u];  // h o V[:, u] with h = 1 (k_make_z)
+    }
+    for (int i = tid; i < R; i += blockDim.x) s_vt[R * R + i] = 1.0;
+    __syncthreads();
+    const FragAddr<NB> fa(lane);
+    const uint32_t nz = (1u << L0);  // internal nodes of levels < L0, plus the root normaliser
+    const uint64_t ne = te.n + 1;     // E-tree: a mass per node (left child), plus the root
+    const uint64_t items = ne + uint64_t(nz) * NB;
+    const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + tid) >> 5, nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t it = gw; it < items; it += nw) {
+        const int m = lane >> 2;
+        if (it < ne) {  // E-tree node (x = h = ones for all 8 rows)
+            const uint64_t v = it;
+            const double* G;
+            if (v == te.n) G = Q;  // root
+            else if (!is_leaf(te, v)) G = Q + slot_of(2 * v + 1) * P;
+            else continue;
+            const double mass = block_qf_packed<NB>(G, fa, s_vt + R * R, lane);
+            if (lane == 0) etab[v] = mass;
+        } else {
+            const uint64_t j = it - ne;
+            const uint32_t vi = uint32_t(j / NB), ub = uint32_t(j % NB);
+            const double* G = vi == nz - 1 ? Zt : Zt + slot_of(2ull * vi + 1) * P;  // last row: root
+            const uint32_t u = ub * 8 + m;
+            const double mass = block_qf_packed<NB>(G, fa, s_vt + u * R, lane);
+            if ((lane & 3) == 0) {
+                ztab[uint64_t(vi) * R + u] = mass;
+                if (vi == nz - 1 && (!isfinite(mass) || mass <= 0.0)) atomicExch(err, 1);
+            }
+        }
+    }
+}
+
+// E-tree walk of every draw with the node masses of the table (F = 1 leaves)
+__global__ void k_pos0_ewalk(const double* __restrict__ etab, Topo te, uint64_t J, const double* __restrict__ ud,
+                             double* __restrict__ margin, uint32_t* __restrict__ node, uint32_t* __restrict__ comp,
+                             uint32_t* __restrict__ zero, uint32_t nzero, int* err) {
+    griddep_launch_dependents();
+    griddep_wait();
+    const uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (uint64_t i = i0; i < nzero; i += uint64_t(gridDim.x) * blockDim.x) zero[i] = 0;
+    const double croot = etab[te.n];
+    if (i0 == 0 && (!isfinite(croot) || croot <= 0.0)) atomicExch(err, 1);
+    const double ic = 1.0 / croot;
+    for (uint64_t d = i0; d < J; d += uint64_t(gridDim.x) * blockDim.x) {
+        const double u = ud[d];
+        double mg = margin ? margin[d] : 0.0;
+        uint64_t v = 0;
+        double low = 0.0;
+        bool first = true;
+        while (!is_leaf(te, v)) {
+            const double cutoff = first ? 0.0 + ic * etab[v] : low + ic * etab[v];
+            first = false;
+            const bool left = cutoff >= u;
+            mg = fmin(mg, fabs(cutoff - u));
+            if (left) {
+                v = 2 * v + 1;
+            } else {
+                v = 2 * v + 2;
+                low = cutoff;
+            }
+        }
+        node[d] = uint32_t(v);
+        comp[d] = uint32_t(leaf_index(te, v));
+        if (margin) margin[d] = mg;
+    }
+}
+
+// factor-tree levels [0, L0) of every draw from the table; counts per level-L0 node
+__global__ void k_pos0_zwalk(const double* __restrict__ ztab, uint32_t L0, const uint32_t* __restrict__ comp, uint32_t R,
+                             uint64_t J, const double* __restrict__ ud, double* __restrict__ margin,
+                             uint32_t* __restrict__ node, double* __restrict__ low_out, double* __restrict__ invc,
+                             uint32_t* __restrict__ hist) {
+    griddep_launch_dependents();
+    griddep_wait();
+    const uint32_t nz = 1u << L0;
+    for (uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; d < J; d += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t u = comp[d];
+        const double ic = 1.0 / ztab[uint64_t(nz - 1) * R + u];
+        const double uu = ud[d];
+        double mg = margin ? margin[d] : 0.0;
+        uint32_t v = 0;
+        double low = 0.0;
+        for (uint32_t l = 0; l < L0; ++l) {
+            const double m = ztab[uint64_t(v) * R + u];
+            const double cutoff = l == 0 ? 0.0 + ic * m : low + ic * m;
+            const bool left = cutoff >= uu;
+            mg = fmin(mg, fabs(cutoff - uu));
+            if (left) {
+                v = 2 * v + 1;
+            } else {
+                v = 2 * v + 2;
+                low = cutoff;
+            }
+        }
+        node[d] = v;
+        low_out[d] = low;
+        invc[d] = ic;
+        if (margin) margin[d] = mg;
+        atomicAdd(hist + (v - (nz - 1)), 1u);
+    }
+}
+
+// counting-sort placement into level-L0 node order; the level L0-1 nodes get the
+// position ranges the level kernels derive their children's ranges from
+__global__ void __launch_bounds__(256) k_pos0_place(uint32_t L0, uint64_t J, const uint32_t* __restrict__ node,
+                                                    const uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor,
+                                                    uint32_t* __restrict__ perm, uint32_t* __restrict__ nsort,
+                                                    uint32_t* __restrict__ GS, uint32_t* __restrict__ GE,
+                                                    uint32_t* __restrict__ cntL) {
+    __shared__ uint32_t s_off[1u << kPos0Levels];
+    griddep_launch_dependents();
+    griddep_wait();
+    const uint32_t nl = 1u << L0, first = nl - 1;
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t i = 0; i < nl; ++i) {
+            s_off[i] = acc;
+            acc += hist[i];
+        }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0)
+        for (uint32_t i = threadIdx.x; i < nl / 2; i += blockDim.x) {
+            const uint32_t p = (first - 1) / 2 + i;  // level L0-1 node; children 2p+1, 2p+2
+            const uint32_t c = 2 * p + 1 - first;
+            GS[p] = s_off[c];
+            cntL[p] = hist[c];
+            GE[p] = s_off[c + 1] + hist[c + 1];
+        }
+    for (uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; d < J; d += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t v = node[d], c = v - first;
+        const uint32_t pos = s_off[c] + atomicAdd(cursor + c, 1u);
+        perm[pos] = uint32_t(d);
+        nsort[pos] = v;
+    }
+}
+
+// ---- quad variant (R = 64): the Gram split over the 4 warps of a CTA -------
+// k_eval_reg holds the whole Gram per warp (240 registers): only 2 warps per SM
+// sub-partition, so every latency phase of a level (positions -> rows -> Gram ->
+// decisions -> slot claims) leaves the FP64 tensor pipe idle. Here the 4 warps
+// of a CTA share every 8-draw block: warp w owns the column blocks {w, 7 - w}
+// of the symmetric Gram (9 of the 36 upper-triangle tiles, 18 DMMA per block,
+// ~100 registers), so 4 CTAs (16 warps) fit an SM. Per block each warp's
+// partial x_d^T (G x_d)|_{its columns} goes to shared memory; a batch of 4
+// blocks is finalised by one warp each (partials summed in warp order, branch
+// decision). The CTA's positions, decision inputs and the parents' position
+// ranges are staged into shared memory up front; the rows of the next batch
+// stream in by cp.async while the current batch computes; the child slots of
+// all of the CTA's runs are claimed in one pass at the end.
+constexpr int QW = 4;     // warps per CTA
+constexpr int QCR = 128;  // max sorted positions per CTA
+constexpr int QBB = 4;    // blocks per batch (one finalising warp each)
+constexpr int QXS = 68;   // doubles per staged row (R = 64 + 4: conflict-free A fragments)
+constexpr uint32_t QPARKED = 0xFFFFFFFFu;
+
+struct QuadSmem {
+    static constexpr size_t XB = size_t(2) * QBB * 8 * QXS * 8;  // row batches, double-buffered
+    static constexpr size_t PART = size_t(2) * QBB * QW * 8 * 8;  // per-warp partial masses
+    static constexpr size_t DBL = size_t(5) * QCR * 8;            // root mass, u, 1/C, low, margin
+    static constexpr size_t U32 = size_t(4) * QCR * 4 + (QCR + 1) * 4 + size_t(6) * QCR * 4;
+    static constexpr size_t U16 = size_t(QCR) * 2 + (QCR / 8 + QCR) * 2;
+    static constexpr size_t U8 = QCR;
+    static constexpr size_t SMEM = XB + PART + DBL + U32 + U16 + U8;
+};
+
+template <int MODE, bool ROOT0>
+__global__ void __launch_bounds__(QW * 32, 4) k_eval_quad(EvalArgs a, uint32_t crange) {
+    constexpr int NB = 8, R = 64;
+    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
+    constexpr bool LEVEL = MODE == EV_LEVEL;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ __align__(16) double qsm[];
+    double* xb = qsm;
+    double* part = xb + 2 * QBB * 8 * QXS;
+    double* s_root = part + 2 * QBB * QW * 8;
+    double* s_u = s_root + QCR;
+    double* s_ic = s_u + QCR;
+    double* s_lo = s_ic + QCR;
+    double* s_mg = s_lo + QCR;
+    uint32_t* s_d = reinterpret_cast<uint32_t*>(s_mg + QCR);
+    uint32_t* s_v = s_d + QCR;
+    uint32_t* s_rank = s_v + QCR;
+    uint32_t* s_rs = s_rank + QCR;  // QCR + 1
+    uint32_t* s_nl = s_rs + QCR + 1;
+    uint32_t* s_nr = s_nl + QCR;
+    uint32_t* s_bl = s_nr + QCR;
+    uint32_t* s_br = s_bl + QCR;
+    uint32_t* s_gs = s_br + QCR;
+    uint32_t* s_ge = s_gs + QCR;
+    uint16_t* s_run = reinterpret_cast<uint16_t*>(s_ge + QCR);
+    uint16_t* s_blk = s_run + QCR;
+    uint8_t* s_left = reinterpret_cast<uint8_t*>(s_blk + QCR / 8 + QCR);
+    __shared__ int s_nruns, s_nblk;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    griddep_launch_dependents();
+    griddep_wait();
+    const uint64_t c0 = uint64_t(blockIdx.x) * crange;
+    if (c0 >= a.J) return;
+    const int cnt = int(a.J - c0 < uint64_t(crange) ? a.J - c0 : uint64_t(crange));
+
+    // 1. the CTA's positions and their decision inputs
+    for (int t = tid; t < cnt; t += QW * 32) {
+        const uint32_t d = a.perm ? a.perm[c0 + t] : uint32_t(c0 + t);
+        s_d[t] = d;
+        s_v[t] = (LEVEL && !ROOT0) ? (a.nsort_in ? a.nsort_in[c0 + t] : a.node[d]) : 0u;
+        if (LEVEL) {
+            s_u[t] = a.ud[d];
+            if (!ROOT0) {
+                s_ic[t] = a.invc[d];
+                s_lo[t] = a.low[d];
+            }
+            if (a.margin) s_mg[t] = a.margin[d];
+        }
+    }
+    __syncthreads();
+    // 2. runs and the block list (warp 0)
+    if (warp == 0) {
+        int nr = 0;
+        for (int tb = 0; tb < cnt; tb += 32) {
+            const int t = tb + lane;
+            const bool valid = t < cnt;
+            const bool start = valid && (t == 0 || s_v[t] != s_v[t - 1]);
+            const unsigned bal = __ballot_sync(FULL, start);
+            if (start) s_rs[nr + __popc(bal & ((1u << lane) - 1u))] = uint32_t(t);
+            if (valid) s_run[t] = uint16_t(nr + __popc(bal & ((2u << lane) - 1u)) - 1);
+            nr += __popc(bal);
+        }
+        if (lane == 0) {
+            s_rs[nr] = uint32_t(cnt);
+            int nb = 0;
+            for (int r = 0; r < nr; ++r) {
+                const int rs = int(s_rs[r]), re = int(s_rs[r + 1]);
+                if (LEVEL && !ROOT0 && is_leaf(a.topo, s_v[rs])) continue;
+                for (int b0 = rs; b0 < re; b0 += 8) s_blk[nb++] = uint16_t(b0 | (min(8, re - b0) << 8));
+            }
+            s_nruns = nr;
+            s_nblk = nb;
+        }
+    }
+    __syncthreads();
+    const int nruns = s_nruns, nblk = s_nblk;
+    // 3. each run's node range [GS, GE) from its parent's (final since the last level)
+    if (LEVEL)
+        for (int r = tid; r < nruns; r += QW * 32) {
+            const uint32_t v = s_v[s_rs[r]];
+            if (!ROOT0 && is_leaf(a.topo, v)) {
+                s_gs[r] = QPARKED;
+                continue;
+            }
+            uint32_t gs = 0, ge = uint32_t(a.J);
+            if (v != 0) {
+                const uint32_t pp = (v - 1) >> 1;
+                const uint32_t gl = a.GS[pp] + a.cntL[pp];
+                gs = (v & 1u) ? a.GS[pp] : gl;
+                ge = (v & 1u) ? gl : a.GE[pp];
+            }
+            s_gs[r] = gs;
+            s_ge[r] = ge;
+            a.GS[v] = gs;
+            a.GE[v] = ge;
+        }
+
+    // 4. sweeps over the blocks
+    const int q1 = warp, q2 = NB - 1 - warp;
+    const int r4 = lane & 3, cq = lane >> 2, m = lane >> 2;
+    double g1[4][2], g2[NB][2];
+    auto load_frags = [&](const double* __restrict__ G) {
+#pragma unroll
+        for (int p = 0; p < NB; ++p)
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const int row = 8 * p + 4 * s + r4;
+                const int rowoff = row * R - (row * (row - 1)) / 2 - row;
+                const int col = 8 * p + cq;
+                const int diag = row <= col ? rowoff + col : col * R - (col * (col - 1)) / 2 - col + row;
+                if (p < 4 && p <= q1) g1[p][s] = __ldg(G + (p == q1 ? diag : rowoff + 8 * q1 + cq));
+                if (p <= q2) g2[p][s] = __ldg(G + (p == q2 ? diag : rowoff + 8 * q2 + cq));
+            }
+    };
+    auto stage_batch = [&](int k) {
+        if (k * QBB < nblk) {
+            const int nj = min(QBB, nblk - k * QBB);
+            double* dst = xb + (k & 1) * QBB * 8 * QXS;
+            for (int i = tid; i < nj * 8 * 32; i += QW * 32) {
+                const int j = i >> 8, row = (i >> 5) & 7, pc = i & 31;
+                const uint32_t e = s_blk[k * QBB + j];
+                const int b0 = e & 0xff, n = e >> 8;
+                if (row < n)
+                    cp_async16(dst + (j * 8 + row) * QXS + 2 * pc, a.X + uint64_t(s_d[b0 + row]) * R + 2 * pc);
+            }
+        }
+        cp_async_commit();
+    };
+    auto sweep = [&](bool root_pass) {
+        stage_batch(0);
+        uint32_t gv = 0xFFFFFFFFu;
+        for (int k = 0; k * QBB < nblk; ++k) {
+            stage_batch(k + 1);
+            cp_async_wait_n<1>();
+            __syncthreads();
+            const int nj = min(QBB, nblk - k * QBB);
+            for (int j = 0; j < nj; ++j) {
+                const uint32_t e = s_blk[k * QBB + j];
+                const int b0 = e & 0xff, n = e >> 8;
+                const uint32_t v = s_v[b0];
+                if (v != gv) {
+                    load_frags((LEVEL && !root_pass) ? a.tree + slot_of(2ull * v + 1) * P : a.tree);
+                    gv = v;
+                }
+                const bool valid = m < n;
+                const double* xr = xb + ((k & 1) * QBB + j) * 8 * QXS + m * QXS;
+                double y1a = 0.0, y1b = 0.0, y2a = 0.0, y2b = 0.0;
+#pragma unroll
+                for (int p = 0; p < NB; ++p) {
+                    if (p > q2) break;
+#pragma unroll
+                    for (int s = 0; s < 2; ++s) {
+                        const double av = valid ? xr[8 * p + 4 * s + r4] : 0.0;
+                        const double a2 = av + av;
+                        if (p < 4 && p <= q1) dmma_884(y1a, y1b, p == q1 ? av : a2, g1[p][s]);
+                        dmma_884(y2a, y2b, p == q2 ? av : a2, g2[p][s]);
+                    }
+                }
+                double pt = 0.0;
+                if (valid) {
+                    const double2 x1 = *reinterpret_cast<const double2*>(xr + 8 * q1 + 2 * r4);
+                    const double2 x2 = *reinterpret_cast<const double2*>(xr + 8 * q2 + 2 * r4);
+                    pt = fma(x1.x, y1a, pt);
+                    pt = fma(x1.y, y1b, pt);
+                    pt = fma(x2.x, y2a, pt);
+                    pt = fma(x2.y, y2b, pt);
+                }
+                pt += __shfl_xor_sync(FULL, pt, 1);
+                pt += __shfl_xor_sync(FULL, pt, 2);
+                if (r4 == 0 && valid) part[(((k & 1) * QBB + j) * QW + warp) * 8 + m] = pt;
+            }
+            __syncthreads();
+            if (warp < nj) {  // finalise block k*QBB + warp
+                const uint32_t e = s_blk[k * QBB + warp];
+                const int b0 = e & 0xff, n = e >> 8;
+                if (lane < n) {
+                    const double* pp = part + ((k & 1) * QBB + warp) * QW * 8 + lane;
+                    const double mass = ((pp[0] + pp[8]) + pp[16]) + pp[24];
+                    const int t = b0 + lane;
+                    const uint32_t dd = s_d[t];
+                    if (root_pass) {
+                        if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
+                        s_root[t] = mass;
+                    } else if (MODE == EV_PROB) {
+                        a.prob[dd] = mass / a.rank_div;
+                    } else if (MODE == EV_ROOT) {
+                        if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
+                        a.invc[dd] = 1.0 / mass;
+                    } else {
+                        const uint32_t v = s_v[b0];
+                        const double u = s_u[t];
+                        double ic, cutoff;
+                        if (ROOT0) {
+                            ic = 1.0 / s_root[t];
+                            a.invc[dd] = ic;
+                            cutoff = 0.0 + ic * mass;
+                        } else {
+                            ic = s_ic[t];
+                            cutoff = s_lo[t] + ic * mass;
+                        }
+                        const bool left = cutoff >= u;
+                        if (a.margin) a.margin[dd] = fmin(s_mg[t], fabs(cutoff - u));
+                        if (left) {
+                            a.node[dd] = 2 * v + 1;
+                        } else {
+                            a.node[dd] = 2 * v + 2;
+                            a.low[dd] = cutoff;
+                        }
+                        s_left[t] = left ? 1 : 0;
+                    }
+                }
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+    };
+    if (ROOT0) sweep(true);
+    sweep(false);
+    if (!LEVEL) return;
+
+    // 5. ranks within each run's left / right part (warp 0, chunks of 32 in order)
+    if (warp == 0) {
+        uint32_t carryL = 0, carryR = 0;
+        const unsigned below = (1u << lane) - 1u;
+        for (int tb = 0; tb < cnt; tb += 32) {
+            const int t = tb + lane;
+            const bool valid = t < cnt;
+            const int r = valid ? s_run[t] : 0;
+            const bool moved = valid && s_gs[r] != QPARKED;
+            const bool lf = moved && s_left[t];
+            const unsigned lm = __ballot_sync(FULL, lf), rm = __ballot_sync(FULL, moved && !lf);
+            const int rs = valid ? int(s_rs[r]) : t, re = valid ? int(s_rs[r + 1]) : t + 1;
+            const int lo = rs > tb ? rs - tb : 0, hi = re - tb < 32 ? re - tb : 32;
+            const unsigned runm = (hi >= 32 ? FULL : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+            const bool cont = rs < tb;  // run began in an earlier chunk
+            const uint32_t nlc = __popc(lm & runm), nrc = __popc(rm & runm);
+            if (moved) {
+                s_rank[t] = lf ? __popc(lm & runm & below) + (cont ? carryL : 0u)
+                               : __popc(rm & runm & below) + (cont ? carryR : 0u);
+                if (t == re - 1) {
+                    s_nl[r] = nlc + (cont ? carryL : 0u);
+                    s_nr[r] = nrc + (cont ? carryR : 0u);
+                }
+            } else if (valid && t == re - 1) {
+                s_nl[r] = 0;
+                s_nr[r] = 0;
+            }
+            // the run crossing into the next chunk carries its counts
+            const uint32_t nL = __shfl_sync(FULL, nlc + (cont ? carryL : 0u), 31);
+            const uint32_t nR = __shfl_sync(FULL, nrc + (cont ? carryR : 0u), 31);
+            carryL = nL;
+            carryR = nR;
+        }
+    }
+    __syncthreads();
+    // 6. slot claims, one pair of atomics per run
+    for (int r = tid; r < nruns; r += QW * 32) {
+        if (s_gs[r] == QPARKED) continue;
+        const uint32_t v = s_v[s_rs[r]];
+        s_bl[r] = s_nl[r] ? atomicAdd(a.cntL + v, s_nl[r]) : 0u;
+        s_br[r] = s_nr[r] ? atomicAdd(a.cntR + v, s_nr[r]) : 0u;
+    }
+    __syncthreads();
+    // 7. next level's order
+    for (int t = tid; t < cnt; t += QW * 32) {
+        const int r = s_run[t];
+        const uint32_t d = s_d[t], v = s_v[t];
+        if (s_gs[r] == QPARKED) {
+            a.perm_out[c0 + t] = d;
+            if (a.nsort_out) a.nsort_out[c0 + t] = v;
+        } else {
+            const bool lf = s_left[t];
+            const uint32_t rk = s_rank[t];
+            const uint32_t pos = lf ? s_gs[r] + s_bl[r] + rk : s_ge[r] - 1u - (s_br[r] + rk);
+            a.perm_out[pos] = d;
+            if (a.nsort_out) a.nsort_out[pos] = 2 * v + (lf ? 1u : 2u);
         }
     }
 }
@@ -1322,9 +2168,76 @@ void launch_stream(int mode, const EvalArgs& a, cudaStream_t s) {
 }
 
 // mode EV_LEVEL with warp_variant selects the per-warp deep-level kernel (R <= 64).
+inline bool eval_reg_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KRPG_EVAL_REG");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <int NB, int MODE, bool ROOT0>
+void launch_reg(const EvalArgs& a, cudaStream_t s) {
+    using C = RegCfg<NB>;
+    static int slots = 0;
+    if (!slots) {
+        cudaFuncSetAttribute(k_eval_reg<NB, MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+        int dev = 0, sms = 0, bps = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_eval_reg<NB, MODE, ROOT0>, RW * 32, C::SMEM);
+        slots = std::max(1, sms * std::max(1, bps) * RW);
+    }
+    // one wave: the level's positions split evenly over the resident warps
+    uint64_t range = (a.J + uint64_t(slots) - 1) / uint64_t(slots);
+    range = std::min<uint64_t>(std::max<uint64_t>((range + 7) / 8 * 8, 8), RRANGE);
+    const unsigned grid = unsigned((a.J + range * RW - 1) / (range * RW));
+    launch_pdl(k_eval_reg<NB, MODE, ROOT0>, dim3(grid), dim3(RW * 32), C::SMEM, s, a, uint32_t(range));
+}
+
+inline int eval_quad_mode() {  // KRPG_EVAL_QUAD: 1 on, default off (measured slower)
+    static const int on = [] {
+        const char* e = std::getenv("KRPG_EVAL_QUAD");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return on;
+}
+
+template <int MODE, bool ROOT0>
+void launch_quad(const EvalArgs& a, cudaStream_t s) {
+    static int ctas = 0;
+    if (!ctas) {
+        cudaFuncSetAttribute(k_eval_quad<MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(QuadSmem::SMEM));
+        int dev = 0, sms = 0, bps = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_eval_quad<MODE, ROOT0>, QW * 32, QuadSmem::SMEM);
+        ctas = std::max(1, sms * std::max(1, bps));
+    }
+    uint64_t cr = (a.J + uint64_t(ctas) - 1) / uint64_t(ctas);
+    cr = std::min<uint64_t>(std::max<uint64_t>((cr + 7) / 8 * 8, 8), QCR);
+    const unsigned grid = unsigned((a.J + cr - 1) / cr);
+    launch_pdl(k_eval_quad<MODE, ROOT0>, dim3(grid), dim3(QW * 32), QuadSmem::SMEM, s, a, uint32_t(cr));
+}
+
 template <int NB>
 void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
     const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
+    if constexpr (NB == 8) {
+        if (eval_quad_mode() && !warp_variant) {
+            if (mode == EV_PROB) return launch_quad<EV_PROB, false>(a, s);
+            if (mode == EV_LEVEL0) return launch_quad<EV_LEVEL, true>(a, s);
+            if (mode == EV_LEVEL) return launch_quad<EV_LEVEL, false>(a, s);
+        }
+    }
+    if constexpr (NB <= 8) {
+        if (eval_reg_enabled() && !warp_variant) {
+            if (mode == EV_PROB) return launch_reg<NB, EV_PROB, false>(a, s);
+            if (mode == EV_LEVEL0) return launch_reg<NB, EV_LEVEL, true>(a, s);
+            if (mode == EV_LEVEL) return launch_reg<NB, EV_LEVEL, false>(a, s);
+        }
+    }
     if (mode == EV_ROOT)
         launch_cta<NB, EV_ROOT, false>(a, grid, s);
     else if (mode == EV_PROB)
@@ -1456,6 +2369,36 @@ void dispatch_leaf(uint32_t R, const LeafArgs& a, cudaStream_t s) {
 
 }  // namespace v2
 
+namespace v2 {
+inline bool pos0_tables_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KRPG_POS0_TABLES");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <int NB>
+void launch_pos0_tables(const double* Q, Topo te, const double* Z, uint32_t L0, const double* V, double* etab,
+                        double* ztab, int* err, cudaStream_t s) {
+    launch_pdl(k_pos0_tables<NB>, dim3(64), dim3(256), 0, s, Q, te, Z, L0, V, etab, ztab, err);
+}
+
+inline void dispatch_pos0_tables(uint32_t R, const double* Q, Topo te, const double* Z, uint32_t L0, const double* V,
+                                 double* etab, double* ztab, int* err, cudaStream_t s) {
+    switch (R / 8) {
+        case 1: return launch_pos0_tables<1>(Q, te, Z, L0, V, etab, ztab, err, s);
+        case 2: return launch_pos0_tables<2>(Q, te, Z, L0, V, etab, ztab, err, s);
+        case 3: return launch_pos0_tables<3>(Q, te, Z, L0, V, etab, ztab, err, s);
+        case 4: return launch_pos0_tables<4>(Q, te, Z, L0, V, etab, ztab, err, s);
+        case 5: return launch_pos0_tables<5>(Q, te, Z, L0, V, etab, ztab, err, s);
+        case 6: return launch_pos0_tables<6>(Q, te, Z, L0, V, etab, ztab, err, s);
+        case 7: return launch_pos0_tables<7>(Q, te, Z, L0, V, etab, ztab, err, s);
+        default: return launch_pos0_tables<8>(Q, te, Z, L0, V, etab, ztab, err, s);
+    }
+}
+}  // namespace v2
+
 // R <= 64: CTA levels + fused deep/leaf kernel; 64 < R <= 160: CTA kernel on every
 // level (both Gram buffers of a run fit in shared memory) + streaming leaf scan.
 // 160 < R <= 256 (R % 32 == 0): streamed-Gram level kernel + streaming leaf scan.
@@ -1476,6 +2419,10 @@ int launch_position_grouped(const GroupedArgs& g) {
     mark(-1);
     EvalArgs e{};
     e.J = J;
+    e.fake = [] {
+        const char* f = std::getenv("KRPG_FAKE_QF");
+        return f ? std::atoi(f) : 0;
+    }();
     e.node = g.node;
     e.rank = g.rank;
     e.low = g.low;
@@ -1496,9 +2443,11 @@ int launch_position_grouped(const GroupedArgs& g) {
     e.GE = g.gend;
     uint32_t* pin = g.perm_a;
     uint32_t* pout = g.perm_b;
-    // CTA-cooperative levels [0, lcta) with direct next-level scatter; level 0
-    // also computes the normaliser (a separate pass only when lcta == 0)
-    auto cta_levels = [&](uint32_t lcta) {
+    // CTA-cooperative levels [lstart, lcta) with direct next-level scatter; level 0
+    // also computes the normaliser (a separate pass only when lcta == 0); a
+    // nonzero lstart continues from draws already placed in node order in
+    // perm_a / nsort_a (first-position tables)
+    auto cta_levels = [&](uint32_t lcta, uint32_t lstart = 0) {
         pin = g.perm_a;
         pout = g.perm_b;
         if (lcta == 0) {
@@ -1516,7 +2465,7 @@ int launch_position_grouped(const GroupedArgs& g) {
         }
         uint32_t* nin = g.nsort_a;
         uint32_t* nout = g.nsort_b;
-        for (uint32_t l = 0; l < lcta; ++l) {
+        for (uint32_t l = lstart; l < lcta; ++l) {
             e.perm = l == 0 ? nullptr : pin;
             e.perm_out = pout;
             e.nsort_in = (l == 0 || !nin) ? nullptr : nin;
@@ -1530,17 +2479,34 @@ int launch_position_grouped(const GroupedArgs& g) {
         e.nsort_in = nullptr;
         e.nsort_out = nullptr;
     };
+    const Topo tz = make_topo(g.I, R);
+    // shallow levels: global regrouping; deep levels + leaf scan: one fused pass
+    uint32_t l0 = 0;
+    while (l0 < tz.d && (R > 64 || !deep_level(J, l0))) ++l0;
+    // first position: E-tree and the top factor-tree levels from (node, component) tables
+    const uint32_t L0 = tz.d >= 2 ? std::min<uint32_t>(kPos0Levels, std::min<uint32_t>(l0, tz.d - 1)) : 0;
+    const bool tab0 = g.h_ones && g.pos0_tab && R <= 64 && R % 8 == 0 && L0 >= 1 && pos0_tables_enabled();
+    double* etab = g.pos0_tab;
+    double* ztab = etab ? etab + 2 * R + 8 : nullptr;
+    uint32_t* hist = etab ? reinterpret_cast<uint32_t*>(ztab + (uint64_t(1) << kPos0Levels) * R) : nullptr;
     e.X = g.H;
     e.tree = g.Q;
     e.topo = te;
-    cta_levels(te.d);
+    if (tab0) {
+        dispatch_pos0_tables(R, g.Q, te, g.Z, L0, g.V, etab, ztab, g.err, g.stream);
+        launch_pdl(k_pos0_ewalk, dim3(grid_for(J, 256)), dim3(256), 0, g.stream, (const double*)etab, te, J,
+                   (const double*)g.ud, g.margin, g.node, g.rank, hist, uint32_t(2u << L0), g.err);
+        launches += 2;
+        mark(9);
+    } else {
+        cta_levels(te.d);
+    }
     launch_pdl(k_make_z, dim3(grid_for(J * R, 256)), dim3(256), 0, g.stream, (const double*)g.H, g.V,
                (const uint32_t*)g.node, te, R, J, g.Zb);
     ++launches;
     mark(13);
 
     // ---------------- stage 2: factor tree, rank-1 M = z z^T ----------------
-    const Topo tz = make_topo(g.I, R);
     launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
                g.draw_offset, 2ull * g.pos + 2, g.margin, 0, g.cntL, g.cntR, uint64_t(tz.n));
     ++launches;
@@ -1548,10 +2514,17 @@ int launch_position_grouped(const GroupedArgs& g) {
     e.X = g.Zb;
     e.tree = g.Z;
     e.topo = tz;
-    // shallow levels: global regrouping; deep levels + leaf scan: one fused pass
-    uint32_t l0 = 0;
-    while (l0 < tz.d && (R > 64 || !deep_level(J, l0))) ++l0;
-    cta_levels(l0);
+    if (tab0) {
+        launch_pdl(k_pos0_zwalk, dim3(grid_for(J, 256)), dim3(256), 0, g.stream, (const double*)ztab, L0,
+                   (const uint32_t*)g.rank, R, J, (const double*)g.ud, g.margin, g.node, g.low, g.invc, hist);
+        launch_pdl(k_pos0_place, dim3(grid_for(J, 256)), dim3(256), 0, g.stream, L0, J, (const uint32_t*)g.node,
+                   (const uint32_t*)hist, hist + (1u << L0), g.perm_a, g.nsort_a, g.gstart, g.gend, g.cntL);
+        launches += 2;
+        mark(9);
+        cta_levels(l0, L0);
+    } else {
+        cta_levels(l0);
+    }
     if (g.fused_deep && R <= 64) {
         DeepArgs da{};
         da.J = J;

@@ -486,7 +486,8 @@ struct krpg_sampler {
             // draw slices on concurrent streams: the level kernels of one slice are
             // latency bound, so a second independent slice fills the SMs' idle phases
             const int S = (prof_on && prof_detail) ? 1 : int(std::max<uint64_t>(1, std::min<uint64_t>(nslices, J / 8192)));
-            char* st = static_cast<char*>(gstate.ensure(Ju * (4 * 6 + 8 * 3) + S * nmax * 4 * 4 + 1024 * (S + 3)));
+            char* st = static_cast<char*>(gstate.ensure(Ju * (4 * 6 + 8 * 3) + S * nmax * 4 * 4 + 1024 * (S + 3) +
+                                                        S * (8 * krpg::pos0_tab_doubles(R) + 128)));
             auto carve = [&](size_t bytes) {
                 char* p = st;
                 st += (bytes + 127) / 128 * 128;
@@ -506,6 +507,7 @@ struct krpg_sampler {
             g.gend = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
             g.cntL = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
             g.cntR = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
+            double* pos0_tab = reinterpret_cast<double*>(carve(8 * krpg::pos0_tab_doubles(R) * S));
             g.Zb = static_cast<double*>(zbuf.ensure(sizeof(double) * J * R));
             g.R = R;
             g.N = N;
@@ -539,6 +541,7 @@ struct krpg_sampler {
                 g.V = blk;
                 g.Z = f[k].tree.as<double>();
                 g.U = f[k].U.p;
+                g.h_ones = p == 0 ? 1 : 0;  // H was just filled with ones
                 t0 = pbegin();
                 int nl = 0;
                 if (S > 1) CK(cudaEventRecord(fork_ev(), stream));
@@ -564,6 +567,7 @@ struct krpg_sampler {
                     gs.gend = g.gend + sl * nmax;
                     gs.cntL = g.cntL + sl * nmax;
                     gs.cntR = g.cntR + sl * nmax;
+                    gs.pos0_tab = pos0_tab + sl * krpg::pos0_tab_doubles(R);
                     gs.stream = sl == 0 ? stream : slice_stream(sl);
                     if (sl > 0) CK(cudaStreamWaitEvent(gs.stream, fork_ev(), 0));
                     nl += krpg::launch_position_grouped(gs);

@@ -96,7 +96,12 @@ struct GroupedArgs {
     void (*mark)(void* ctx, int cat);  // optional per-launch timing hook
     void* mark_ctx;
     int fused_deep;                    // deep levels + leaf in one warp-local pass
+    int h_ones;                        // H is all ones (first included position): table shortcut
+    double* pos0_tab;                  // scratch for the first-position tables (pos0_tab_doubles(R)), nullable
 };
+// doubles of scratch the first-position tables need at rank R (E-tree masses, factor-tree
+// masses per (node, component) for the top levels, per-node counters)
+inline uint64_t pos0_tab_doubles(uint32_t R) { return 2ull * R + 8 + 128ull * R + 256; }
 bool grouped_supported(uint32_t R, uint32_t mode);
 int launch_position_grouped(const GroupedArgs& g);
 void launch_probabilities_grouped(const double* H, const double* gp_packed, uint32_t R, uint64_t J,

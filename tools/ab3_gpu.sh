@@ -1,0 +1,16 @@
+#!/bin/bash
+# bench under several values of one env toggle: tools/ab3_gpu.sh VAR v1 v2 ... -- [bench args]
+VAR=$1; shift
+vals=()
+while [ $# -gt 0 ] && [ "$1" != "--" ]; do vals+=("$1"); shift; done
+[ "$1" == "--" ] && shift
+for val in "${vals[@]}"; do
+  env $VAR=$val python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 2 "$@" > gpurun_out/ab_$val.json 2> gpurun_out/ab_$val.err || tail -20 gpurun_out/ab_$val.err
+  python - "$VAR=$val" gpurun_out/ab_$val.json <<'PY'
+import json, sys
+d = json.load(open(sys.argv[2]))
+print("%s value %.4e samples/s  ms/step %.3f  e2e %.3e  frac %.3f  kernels %s" % (
+    sys.argv[1], d["value"], d["ms_per_step"], d["e2e"]["value"], d["roofline"]["frac"],
+    {k: round(v, 3) for k, v in d["kernel_ms_per_step"].items()}))
+PY
+done

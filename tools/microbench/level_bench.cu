@@ -1,0 +1,144 @@
+// One grouped-descent level in isolation (config-2 shape: J = 65536 draws, R = 64, all draws
+// in one node run as at the top of the tree), timed with events per launch:
+//   usage: level_bench [J] [nruns]   (nruns: the draws are spread over that many node runs)
+// Variants: KRPG_EVAL_QUAD / KRPG_EVAL_REG select the kernel as in the library;
+// KRPG_FAKE_QF=1 skips the DMMA, =2 also the row / Gram loads (k_eval_reg only).
+#include "../../paper_2301_12584_b200/csrc/descent_v2.cu"
+
+#include <cstdio>
+#include <random>
+#include <vector>
+
+using namespace krpg;
+using namespace krpg::v2;
+
+int main(int argc, char** argv) {
+    const uint64_t J = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 65536;
+    const uint32_t nruns = argc > 2 ? std::atoi(argv[2]) : 1;
+    const uint32_t R = 64, P = R * (R + 1) / 2;
+    const Topo tz = make_topo(1ull << 22, R);
+    // level l such that 2^l >= nruns: draws at nodes 2^l - 1 + (d * nruns / J)
+    uint32_t l = 0;
+    while ((1u << l) < nruns) ++l;
+    const uint32_t first = (1u << l) - 1;
+    std::mt19937_64 rng(7);
+    std::uniform_real_distribution<double> U(-1, 1), U01(0, 1);
+    std::vector<double> X(J * R), tree((size_t(tz.L)) * P), ud(J), invc(J), low(J, 0.0), mg(J, 1e300);
+    for (auto& x : X) x = U(rng);
+    for (auto& g : tree) g = U(rng) * 1e-3;
+    for (uint64_t s = 0; s < tz.L; ++s)
+        for (uint32_t a = 0; a < R; ++a) tree[s * P + pack_index(R, a, a)] = 10.0 + U01(rng);
+    for (uint64_t d = 0; d < J; ++d) {
+        ud[d] = U01(rng);
+        invc[d] = 1.0 / (2 * 640.0);
+    }
+    std::vector<uint32_t> node(J), perm(J), nsort(J);
+    for (uint64_t d = 0; d < J; ++d) {
+        perm[d] = uint32_t(d);
+        node[d] = first + uint32_t(d * nruns / J);
+        nsort[d] = node[d];
+    }
+    // node ranges of the parents: GS/GE for level l nodes must be derivable; set GS/GE/cntL of parents
+    const uint32_t nn = uint32_t(tz.n);
+    std::vector<uint32_t> GS(nn, 0), GE(nn, 0), cntL(nn, 0);
+    for (uint32_t r = 0; r < nruns; ++r) {
+        const uint32_t v = first + r;
+        const uint64_t s = uint64_t(r) * J / nruns, e = uint64_t(r + 1) * J / nruns;
+        if (v == 0) continue;
+        const uint32_t p = (v - 1) >> 1;
+        if (v & 1) {
+            GS[p] = uint32_t(s);
+            cntL[p] = uint32_t(e - s);
+        } else {
+            GE[p] = uint32_t(e);
+        }
+    }
+    auto up = [](const void* h, size_t bytes) {
+        void* d;
+        cudaMalloc(&d, bytes);
+        cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice);
+        return d;
+    };
+    EvalArgs a{};
+    a.J = J;
+    a.perm = static_cast<uint32_t*>(up(perm.data(), J * 4));
+    a.nsort_in = static_cast<uint32_t*>(up(nsort.data(), J * 4));
+    uint32_t* node_d = static_cast<uint32_t*>(up(node.data(), J * 4));
+    a.node = node_d;
+    cudaMalloc(&a.rank, J * 4);
+    a.low = static_cast<double*>(up(low.data(), J * 8));
+    a.invc = static_cast<double*>(up(invc.data(), J * 8));
+    a.ud = static_cast<double*>(up(ud.data(), J * 8));
+    a.margin = static_cast<double*>(up(mg.data(), J * 8));
+    uint32_t* cntL_d = static_cast<uint32_t*>(up(cntL.data(), nn * 4));
+    cudaMalloc(&a.cntR, size_t(nn) * 4);
+    a.cntL = cntL_d;
+    a.X = static_cast<double*>(up(X.data(), J * R * 8));
+    a.tree = static_cast<double*>(up(tree.data(), tree.size() * 8));
+    a.topo = tz;
+    cudaMalloc(&a.err, 4);
+    cudaMalloc(&a.perm_out, J * 4);
+    cudaMalloc(&a.nsort_out, J * 4);
+    a.GS = static_cast<uint32_t*>(up(GS.data(), nn * 4));
+    a.GE = static_cast<uint32_t*>(up(GE.data(), nn * 4));
+    const char* f = std::getenv("KRPG_FAKE_QF");
+    a.fake = f ? std::atoi(f) : 0;
+    const size_t ntr = (J / 8 + 64) * 8;
+    cudaMalloc(&a.trace, ntr * 8);
+    cudaMemset(a.trace, 0, ntr * 8);
+    // counters of this level's nodes are reset before every launch (memset not timed)
+    cudaStream_t s;
+    cudaStreamCreate(&s);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best = 1e30, sum = 0;
+    const int K = 20;
+    for (int it = 0; it < K + 3; ++it) {
+        cudaMemcpyAsync(node_d, node.data(), J * 4, cudaMemcpyHostToDevice, s);
+        cudaMemsetAsync(a.cntR, 0, size_t(nn) * 4, s);
+        cudaMemcpyAsync(cntL_d, cntL.data(), size_t(nn) * 4, cudaMemcpyHostToDevice, s);
+        // level-l counters must start at zero (cntL of the parents is preset above)
+        cudaMemsetAsync(cntL_d + first, 0, size_t(nruns) * 4, s);
+        cudaEventRecord(e0, s);
+        dispatch_eval(R, EV_LEVEL, a, s, false);
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (it >= 3) {
+            best = std::min(best, double(ms));
+            sum += ms;
+        }
+    }
+    const cudaError_t err = cudaGetLastError();
+    {
+        std::vector<unsigned long long> tr(ntr);
+        cudaMemcpy(tr.data(), a.trace, ntr * 8, cudaMemcpyDeviceToHost);
+        unsigned long long t0min = ~0ull, t0max = 0, t5max = 0;
+        double ph[5] = {0, 0, 0, 0, 0};
+        int nw = 0;
+        for (size_t w = 0; w * 8 < ntr; ++w) {
+            const unsigned long long* t = &tr[w * 8];
+            if (!t[0] || !t[5]) continue;
+            ++nw;
+            t0min = std::min(t0min, t[0]);
+            t0max = std::max(t0max, t[0]);
+            t5max = std::max(t5max, t[5]);
+            for (int k = 0; k < 5; ++k) ph[k] += double(t[k + 1] - t[k]);
+        }
+        if (nw)
+            std::printf("  last launch: %d warps, span %.1f us, start skew %.1f us; per warp: positions %.2f, list %.2f, "
+                        "sweep %.2f, claims %.2f, scatter %.2f us\n",
+                        nw, (t5max - t0min) * 1e-3, (t0max - t0min) * 1e-3, ph[0] / nw * 1e-3, ph[1] / nw * 1e-3,
+                        ph[2] / nw * 1e-3, ph[3] / nw * 1e-3, ph[4] / nw * 1e-3);
+    }
+    std::vector<uint32_t> po(J);
+    cudaMemcpy(po.data(), a.perm_out, J * 4, cudaMemcpyDeviceToHost);
+    std::vector<char> seen(J, 0);
+    uint64_t bad = 0;
+    for (auto p : po) bad += (p >= J || seen[p]++) ? 1 : 0;
+    std::printf("J %llu runs %u (level %u): best %.1f us  mean %.1f us  (DMMA floor at 37 TF/s: %.1f us)  perm %s  %s\n",
+                (unsigned long long)J, nruns, l, best * 1e3, sum / K * 1e3, double(J) / 8 * 72 * 512 / 37e12 * 1e6,
+                bad ? "BROKEN" : "ok", cudaGetErrorString(err));
+}
