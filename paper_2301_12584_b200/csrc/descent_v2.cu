@@ -318,8 +318,8 @@ struct RegCfg {
     static constexpr int NFR = NB * (NB + 1);      // B-fragment doubles per lane
     // per warp: row ring | decision inputs u, 1/C, low, margin, root mass (f64 x RRANGE each) |
     // per-position info, per-run node / parent range / counts / claims (u32) | block list (u16)
-    static constexpr int WARP_D = RSLOTS * SLOT + 5 * RRANGE;
-    static constexpr int WARP_U32 = RRANGE + 9 * RRANGE;
+    static constexpr int WARP_D = RSLOTS * SLOT + 6 * RRANGE;
+    static constexpr int WARP_U32 = 7 * RRANGE;
     static constexpr size_t WARP_BYTES = size_t(WARP_D) * 8 + WARP_U32 * 4 + RMAXBLK * 2;
     static constexpr size_t WARP_STRIDE = (WARP_BYTES + 15) / 16 * 16;
     static constexpr size_t SMEM = RW * WARP_STRIDE;
@@ -344,13 +344,19 @@ __device__ __forceinline__ void load_gram_frags(double (&gf)[NB * (NB + 1)], con
             const int rowoff = row * R - (row * (row - 1)) / 2 - row;
             const int diag = row <= col ? rowoff + col : col * R - (col * (col - 1)) / 2 - col + row;
             gf[rfrag<NB>(p, s, p)] = __ldg(G + diag);
+            // off-diagonal tiles count twice (folded weights); a (2g) == (2a) g exactly, so
+            // the doubling is applied once per run here instead of per block to the A fragment
 #pragma unroll
-            for (int q = p + 1; q < NB; ++q) gf[rfrag<NB>(p, s, q)] = __ldg(G + rowoff + 8 * q + cq);
+            for (int q = p + 1; q < NB; ++q) {
+                const double g = __ldg(G + rowoff + 8 * q + cq);
+                gf[rfrag<NB>(p, s, q)] = g + g;
+            }
         }
 }
 
-// block_qf_packed with the B fragments in registers and the rows in shared memory
-// (xs = the block's 8 staged rows, row m valid iff valid); same operation order
+// block_qf_packed with the B fragments in registers (off-diagonal ones doubled) and
+// the rows in shared memory (xs = the block's 8 staged rows, row m valid iff valid);
+// same operation order, bit-identical result
 template <int NB>
 __device__ __forceinline__ double block_qf_regs(const double (&gf)[NB * (NB + 1)], const double* xs, bool valid,
                                                 int lane) {
@@ -366,9 +372,8 @@ __device__ __forceinline__ double block_qf_regs(const double (&gf)[NB * (NB + 1)
         for (int s = 0; s < 2; ++s) {
             const double av = valid ? xr[8 * p + 4 * s + r4] : 0.0;
             dmma_884(y[p][0], y[p][1], av, gf[rfrag<NB>(p, s, p)]);
-            const double a2 = av + av;
 #pragma unroll
-            for (int q = p + 1; q < NB; ++q) dmma_884(y[q][0], y[q][1], a2, gf[rfrag<NB>(p, s, q)]);
+            for (int q = p + 1; q < NB; ++q) dmma_884(y[q][0], y[q][1], av, gf[rfrag<NB>(p, s, q)]);
         }
     }
     double part = 0.0;
@@ -387,9 +392,13 @@ __device__ __forceinline__ double block_qf_regs(const double (&gf)[NB * (NB + 1)
 
 // Everything a warp needs besides the quadratic forms is brought in with ONE
 // latency at the start (cp.async into the warp's shared memory: positions'
-// decision inputs, the parents' position ranges of its runs) and the child
-// slots of all its runs are claimed with ONE round of atomics at the end, so
-// the only per-block waits are the DMMA chain itself.
+// decision inputs, the parents' position ranges of its runs); the draws' rows
+// stream into a 3-slot ring by 1-D TMA (one bulk copy per row, lanes 0-7,
+// completing on the slot's mbarrier); the block loop does nothing but the DMMA
+// chain and a store of the 8 masses, so the two warps of an SM sub-partition
+// keep the FP64 tensor pipe busy; branch decisions, ranks, slot claims and the
+// next level's order are then computed for all of the warp's positions at once
+// (two per lane, run membership from ballot masks).
 template <int NB, int MODE, bool ROOT0>
 __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t range) {
     constexpr int R = 8 * NB;
@@ -398,6 +407,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     constexpr unsigned FULL = 0xffffffffu;
     constexpr bool LEVEL = MODE == EV_LEVEL;
     extern __shared__ __align__(16) unsigned char smem_regb[];
+    __shared__ __align__(8) uint64_t s_bar[RW][RSLOTS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     griddep_launch_dependents();
     griddep_wait();
@@ -412,16 +422,16 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     double* s_lo = s_ic + RRANGE;
     double* s_mg = s_lo + RRANGE;
     double* s_root = s_mg + RRANGE;
-    uint32_t* s_info = reinterpret_cast<uint32_t*>(s_root + RRANGE);
-    uint32_t* s_rv = s_info + RRANGE;   // per run: node
+    double* s_mass = s_root + RRANGE;
+    uint32_t* s_rs = reinterpret_cast<uint32_t*>(s_mass + RRANGE);  // per run: first position
+    uint32_t* s_rv = s_rs + RRANGE;     // per run: node
     uint32_t* s_pgs = s_rv + RRANGE;    // parent's GS / cntL / GE
     uint32_t* s_pcl = s_pgs + RRANGE;
     uint32_t* s_pge = s_pcl + RRANGE;
-    uint32_t* s_cl = s_pge + RRANGE;    // per run: lefts / rights in this range
-    uint32_t* s_cr = s_cl + RRANGE;
-    uint32_t* s_bl = s_cr + RRANGE;     // claimed bases
+    uint32_t* s_bl = s_pge + RRANGE;    // claimed bases of the run's left / right part
     uint32_t* s_br = s_bl + RRANGE;
     uint16_t* s_blk = reinterpret_cast<uint16_t*>(s_br + RRANGE);
+    uint64_t* bar = s_bar[warp];
 
     // the warp's sorted positions p0 + lane (A) and p0 + 32 + lane (B)
     uint32_t dA = 0, dB = 0, vA = 0xFFFFFFFFu, vB = 0xFFFFFFFFu;
@@ -437,9 +447,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     const uint32_t upB = __shfl_up_sync(FULL, vB, 1);
     const bool stA = lane < cnt && (lane == 0 || vA != upA);
     const bool stB = lane + 32 < cnt && vB != (lane == 0 ? lastA : upB);
-    const unsigned sA = __ballot_sync(FULL, stA);
-    const unsigned sB = __ballot_sync(FULL, stB);
-    const uint64_t starts = uint64_t(sA) | (uint64_t(sB) << 32);
+    const uint64_t starts = uint64_t(__ballot_sync(FULL, stA)) | (uint64_t(__ballot_sync(FULL, stB)) << 32);
     const int nruns = __popcll(static_cast<long long>(starts));
     if (tr && lane == 0) tr[1] = gtimer();
     auto pos_d = [&](int t) {  // every lane participates; t may differ per lane
@@ -451,42 +459,54 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
         return t < 32 ? x : y;
     };
     auto run_of = [&](int t) { return __popcll(static_cast<long long>(starts & ((2ull << t) - 1ull))) - 1; };
-    auto run_end = [&](int b) {
-        const uint64_t mk = starts & ~((2ull << b) - 1ull);
-        return mk ? __ffsll(static_cast<long long>(mk)) - 1 : cnt;
-    };
+    auto parked = [&](uint32_t v) { return LEVEL && !ROOT0 && is_leaf(a.topo, v); };
 
-    // decision inputs of every position and the parents' ranges of every run: one group
-    if (LEVEL) {
+    if (lane == 0) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int t = lane + 32 * h;
-            const uint32_t d = h ? dB : dA;
-            if (t < cnt) {
-                cp_async8(s_u + t, a.ud + d);
-                if (!ROOT0) {
-                    cp_async8(s_ic + t, a.invc + d);
-                    cp_async8(s_lo + t, a.low + d);
-                }
-                if (a.margin) cp_async8(s_mg + t, a.margin + d);
+        for (int sl = 0; sl < RSLOTS; ++sl) mbar_init(&bar[sl], 1);
+        fence_mbar_init();
+    }
+    // the first run's Gram (root Gram for the normaliser pass) is requested now, so
+    // its latency overlaps the input staging and the block list
+    double gf[C::NFR];
+    uint32_t gv_first = 0xFFFFFFFFu;
+    {
+        const uint32_t v0 = __shfl_sync(FULL, vA, 0);
+        if (a.fake < 2 && !parked(v0)) {
+            const double* G = (LEVEL && !ROOT0) ? a.tree + slot_of(2ull * v0 + 1) * P : a.tree;
+            load_gram_frags<NB>(gf, G, lane);
+            gv_first = v0;
+        }
+    }
+    // decision inputs of every position and the parents' ranges of every run: one group
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int t = lane + 32 * h;
+        const uint32_t d = h ? dB : dA;
+        if (LEVEL && t < cnt) {
+            cp_async8(s_u + t, a.ud + d);
+            if (!ROOT0) {
+                cp_async8(s_ic + t, a.invc + d);
+                cp_async8(s_lo + t, a.low + d);
             }
-            if (h ? stB : stA) {
-                const uint32_t v = h ? vB : vA;
-                const int r = run_of(t);
-                s_rv[r] = v;
-                if (v != 0 && !(!ROOT0 && is_leaf(a.topo, v))) {
-                    const uint32_t pp = (v - 1) >> 1;
-                    cp_async4(s_pgs + r, a.GS + pp);
-                    cp_async4(s_pcl + r, a.cntL + pp);
-                    cp_async4(s_pge + r, a.GE + pp);
-                }
+            if (a.margin) cp_async8(s_mg + t, a.margin + d);
+        }
+        if (h ? stB : stA) {
+            const uint32_t v = h ? vB : vA;
+            const int r = run_of(t);
+            s_rs[r] = uint32_t(t);
+            s_rv[r] = v;
+            if (LEVEL && v != 0 && !parked(v)) {
+                const uint32_t pp = (v - 1) >> 1;
+                cp_async4(s_pgs + r, a.GS + pp);
+                cp_async4(s_pcl + r, a.cntL + pp);
+                cp_async4(s_pge + r, a.GE + pp);
             }
         }
     }
     cp_async_commit();
 
-    // block list: (b0, n) of every 8-draw block of every non-leaf run; draws
-    // parked at a leaf one level up keep their positions
+    // block list: (b0, n) of every 8-draw block of every non-parked run
     int nblk = 0;
     {
         uint64_t st = starts;
@@ -494,7 +514,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
             const int rs = __ffsll(static_cast<long long>(st)) - 1;
             st &= st - 1;
             const int re = st ? __ffsll(static_cast<long long>(st)) - 1 : cnt;
-            if (LEVEL && !ROOT0 && is_leaf(a.topo, pos_v(rs))) continue;
+            if (parked(pos_v(rs))) continue;
             for (int b0 = rs; b0 < re; b0 += 8) {
                 if (lane == 0) s_blk[nblk] = uint16_t(b0 | (min(8, re - b0) << 8));
                 ++nblk;
@@ -502,38 +522,30 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
         }
     }
     __syncwarp();
+    if (tr && lane == 0) tr[2] = gtimer();
 
-    auto stage = [&](int i) {  // rows of block i -> ring slot i % RSLOTS (one cp.async group)
-        if (i < nblk && a.fake < 2) {
-            const uint32_t e = s_blk[i];
-            const int b0 = e & 0xff, n = e >> 8;
-            double* dst = ring + (i % RSLOTS) * C::SLOT;
-            constexpr int PPR = R / 2;  // 16-byte pieces per row
-            const uint32_t drow = pos_d(b0 + (lane & 7) < cnt ? b0 + (lane & 7) : b0);
-#pragma unroll
-            for (int base = 0; base < 8 * PPR; base += 32) {
-                const int pc = base + lane;
-                const int row = pc / PPR, k = pc - row * PPR;
-                const uint32_t dr = __shfl_sync(FULL, drow, row & 7);
-                if (row < n) cp_async16(dst + row * C::XS + 2 * k, a.X + uint64_t(dr) * R + 2 * k);
-            }
+    uint32_t phase = 0;  // bit sl: parity of slot sl's next completion
+    auto issue = [&](int i) {  // rows of block i -> ring slot i % RSLOTS (1-D TMA, one copy per row)
+        if (i >= nblk || a.fake >= 2) return;
+        const uint32_t e = s_blk[i];
+        const int b0 = e & 0xff, n = e >> 8;
+        const int sl = i % RSLOTS;
+        const uint32_t dr = pos_d(b0 + (lane & 7) < cnt ? b0 + (lane & 7) : b0);
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&bar[sl], uint32_t(n) * R * 8);
         }
-        cp_async_commit();
+        __syncwarp();
+        if (lane < n) tma_load_1d(ring + sl * C::SLOT + lane * C::XS, a.X + uint64_t(dr) * R, R * 8, &bar[sl]);
     };
 
-    double gf[C::NFR];
-    const unsigned below = (1u << lane) - 1u;
-    // one sweep over the warp's blocks against node Grams (root_pass: the root
-    // Gram, masses kept as normalisers)
-    auto sweep = [&](bool root_pass) {
-        stage(0);
-        stage(1);
-        uint32_t gv = 0xFFFFFFFFu;
-        uint32_t cl = 0, cr = 0;
+    // one sweep over the warp's blocks: masses into s_mass (root_pass: s_root)
+    auto sweep = [&](bool root_pass, uint32_t gv) {
+        double* out = root_pass ? s_root : s_mass;
+#pragma unroll
+        for (int i = 0; i < RSLOTS; ++i) issue(i);
         for (int i = 0; i < nblk; ++i) {
-            stage(i + 2);
-            cp_async_wait_n<2>();
-            __syncwarp();
+            const int sl = i % RSLOTS;
             const uint32_t e = s_blk[i];
             const int b0 = e & 0xff, n = e >> 8;
             const uint32_t v = pos_v(b0);
@@ -543,83 +555,91 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
                 load_gram_frags<NB>(gf, G, lane);
                 gv = v;
             }
+            if (a.fake < 2) {
+                mbar_wait(&bar[sl], (phase >> sl) & 1u);
+                phase ^= 1u << sl;
+            }
+            if (tr && lane == 0 && i == 0 && !root_pass) tr[6] = gtimer();
             const int m = lane >> 2;
             const bool valid = m < n;
-            const bool owner = valid && (lane & 3) == 0;
-            const int t = b0 + m;
-            const uint32_t dd = pos_d(t < cnt ? t : b0);
             double mass;
             if (a.fake) {  // timing experiment: pseudo-random branch, no quadratic form
-                const uint32_t hsh = (dd * 2654435761u) ^ (v * 40503u);
+                const uint32_t hsh = (pos_d(b0 + m < cnt ? b0 + m : b0) * 2654435761u) ^ (v * 40503u);
                 mass = ((hsh >> 13) & 1u) ? 1e300 : 0.0;
                 if (!(LEVEL && !root_pass)) mass = 1.0;
             } else {
-                mass = block_qf_regs<NB>(gf, ring + (i % RSLOTS) * C::SLOT, valid, lane);
+                mass = block_qf_regs<NB>(gf, ring + sl * C::SLOT, valid, lane);
             }
-            if (root_pass) {
-                if (owner) {
-                    if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
-                    s_root[t] = mass;
-                }
-            } else if (MODE == EV_ROOT) {
-                if (owner) {
-                    if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
-                    a.invc[dd] = 1.0 / mass;
-                }
-            } else if (MODE == EV_PROB) {
-                if (owner) a.prob[dd] = mass / a.rank_div;
-            } else {
-                bool left = false;
-                if (owner) {
-                    const double u = s_u[t];
-                    double ic, cutoff;
-                    if (ROOT0) {
-                        ic = 1.0 / s_root[t];
-                        a.invc[dd] = ic;
-                        cutoff = 0.0 + ic * mass;
-                    } else {
-                        ic = s_ic[t];
-                        cutoff = s_lo[t] + ic * mass;
-                    }
-                    left = cutoff >= u;
-                    if (a.margin) a.margin[dd] = fmin(s_mg[t], fabs(cutoff - u));
-                    if (left) {
-                        a.node[dd] = 2 * v + 1;
-                    } else {
-                        a.node[dd] = 2 * v + 2;
-                        a.low[dd] = cutoff;
-                    }
-                }
-                const unsigned lm = __ballot_sync(FULL, owner && left);
-                const unsigned rm = __ballot_sync(FULL, owner && !left);
-                if (owner)
-                    s_info[t] = left ? (cl + __popc(lm & below)) | 0x80000000u : cr + __popc(rm & below);
-                cl += __popc(lm);
-                cr += __popc(rm);
-                if (b0 + n == run_end(b0)) {  // the run's last block in this range
-                    if (lane == 0) {
-                        const int r = run_of(b0);
-                        s_cl[r] = cl;
-                        s_cr[r] = cr;
-                    }
-                    cl = cr = 0;
-                }
-            }
+            if (valid && (lane & 3) == 0) out[b0 + m] = mass;
+            if (tr && lane == 0 && i == 0 && !root_pass) tr[7] = gtimer();
             __syncwarp();
+            issue(i + RSLOTS);
         }
-        cp_async_wait_all();
         __syncwarp();
     };
-    if (tr && lane == 0) tr[2] = gtimer();
-    if (ROOT0) sweep(true);
-    sweep(false);
+    cp_async_wait_all();  // decision inputs (needed by the root pass only for the error check: none)
+    __syncwarp();
+    if (ROOT0) {
+        sweep(true, gv_first);
+        sweep(false, 0xFFFFFFFFu);
+    } else {
+        sweep(false, gv_first);
+    }
     if (tr && lane == 0) tr[3] = gtimer();
-    if (!LEVEL) return;
 
-    // claim child slots for every run at once (one atomic round trip), then scatter
+    // decisions for all positions (two per lane)
+    bool lf[2] = {false, false}, mv[2] = {false, false};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int t = lane + 32 * h;
+        if (t >= cnt) continue;
+        const uint32_t d = h ? dB : dA, v = h ? vB : vA;
+        if (parked(v)) continue;
+        const double mass = s_mass[t];
+        if (MODE == EV_ROOT) {
+            if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
+            a.invc[d] = 1.0 / mass;
+        } else if (MODE == EV_PROB) {
+            a.prob[d] = mass / a.rank_div;
+        } else {
+            const double u = s_u[t];
+            double ic, cutoff;
+            if (ROOT0) {
+                const double croot = s_root[t];
+                if (!isfinite(croot) || croot <= 0.0) atomicExch(a.err, 1);
+                ic = 1.0 / croot;
+                a.invc[d] = ic;
+                cutoff = 0.0 + ic * mass;
+            } else {
+                ic = s_ic[t];
+                cutoff = s_lo[t] + ic * mass;
+            }
+            const bool left = cutoff >= u;
+            if (a.margin) a.margin[d] = fmin(s_mg[t], fabs(cutoff - u));
+            if (left) {
+                a.node[d] = 2 * v + 1;
+            } else {
+                a.node[d] = 2 * v + 2;
+                a.low[d] = cutoff;
+            }
+            lf[h] = left;
+            mv[h] = true;
+        }
+    }
+    if (!LEVEL) return;
+    const uint64_t Lm = uint64_t(__ballot_sync(FULL, lf[0])) | (uint64_t(__ballot_sync(FULL, lf[1])) << 32);
+    const uint64_t Mm = uint64_t(__ballot_sync(FULL, mv[0])) | (uint64_t(__ballot_sync(FULL, mv[1])) << 32);
+    const uint64_t Rm = Mm & ~Lm;
+    auto bits = [](int lo, int hi) {  // [lo, hi) of a 64-bit mask
+        const uint64_t up = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
+        return up & ~((1ull << lo) - 1ull);
+    };
+    // claim child slots for every run at once (one atomic round trip)
     for (int r = lane; r < nruns; r += 32) {
         const uint32_t v = s_rv[r];
-        if (!ROOT0 && is_leaf(a.topo, v)) continue;
+        if (parked(v)) continue;
+        const int rs = int(s_rs[r]), re = r + 1 < nruns ? int(s_rs[r + 1]) : cnt;
+        const uint64_t rb = bits(rs, re);
         uint32_t gs = 0, ge = uint32_t(a.J);
         if (v != 0) {
             const uint32_t gl = s_pgs[r] + s_pcl[r];
@@ -628,7 +648,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
         }
         a.GS[v] = gs;
         a.GE[v] = ge;
-        const uint32_t nl = s_cl[r], nr = s_cr[r];
+        const uint32_t nl = __popcll(static_cast<long long>(Lm & rb)), nr = __popcll(static_cast<long long>(Rm & rb));
         const uint32_t bl = nl ? atomicAdd(a.cntL + v, nl) : 0u;
         const uint32_t br = nr ? atomicAdd(a.cntR + v, nr) : 0u;
         s_bl[r] = gs + bl;
@@ -641,17 +661,16 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
         const int t = lane + 32 * h;
         if (t < cnt) {
             const uint32_t d = h ? dB : dA, v = h ? vB : vA;
-            if (!ROOT0 && is_leaf(a.topo, v)) {
+            if (parked(v)) {
                 a.perm_out[p0 + t] = d;
                 if (a.nsort_out) a.nsort_out[p0 + t] = v;
             } else {
                 const int r = run_of(t);
-                const uint32_t info = s_info[t];
-                const bool lf = info >> 31;
-                const uint32_t rk = info & 0x7fffffffu;
-                const uint32_t pos = lf ? s_bl[r] + rk : s_br[r] - rk;
+                const uint64_t before = bits(int(s_rs[r]), t);
+                const uint32_t pos = lf[h] ? s_bl[r] + __popcll(static_cast<long long>(Lm & before))
+                                           : s_br[r] - __popcll(static_cast<long long>(Rm & before));
                 a.perm_out[pos] = d;
-                if (a.nsort_out) a.nsort_out[pos] = 2 * v + (lf ? 1u : 2u);
+                if (a.nsort_out) a.nsort_out[pos] = 2 * v + (lf[h] ? 1u : 2u);
             }
         }
     }
@@ -1765,7 +1784,7 @@ struct DeepCfg {
     static constexpr int LB = LROWS * RSP;
     static constexpr int BUF = ((GB > LB ? GB : LB) + 127) / 128 * 128;
     static constexpr int XS = 3 * R * 8;
-    static constexpr int WARP_BYTES = BUF + XS + 128;
+    static constexpr int WARP_BYTES = BUF + XS + 128 + 32;  // + perm scratch + 3 mbarriers
     static constexpr int SMEM = WPB * WARP_BYTES;
 };
 
@@ -1851,6 +1870,16 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
     uint32_t* perm_sm = reinterpret_cast<uint32_t*>(wbase + C::BUF + C::XS);
     const uint64_t base = (uint64_t(blockIdx.x) * WPB + warp) * a.chunk;
     if (base >= a.J) return;
+    // 1-D TMA completion barriers: [0] node Gram, [1], [2] leaf-row half buffers
+    uint64_t* wbar = reinterpret_cast<uint64_t*>(wbase + C::BUF + C::XS + 128);
+    if (lane == 0) {
+        mbar_init(&wbar[0], 1);
+        mbar_init(&wbar[1], 1);
+        mbar_init(&wbar[2], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t gph = 0, lph = 0, lpend = 0;
     const int cnt = a.J - base < uint64_t(a.chunk) ? int(a.J - base) : int(a.chunk);
     const bool live = lane < cnt;
     uint32_t d = live ? a.perm[base + lane] : 0u;
@@ -1878,9 +1907,12 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
             const uint32_t vr = __shfl_sync(0xffffffffu, v, rs);
             if (is_leaf(a.topo, vr)) continue;
             {  // stage this run's Gram, warm L2 with the next one
-                const char* g = reinterpret_cast<const char*>(a.tree + slot_of(2ull * vr + 1) * P);
-                for (int o = lane * 16; o < C::GB; o += 32 * 16) cp_async16(buf + o, g + o);
-                cp_async_commit();
+                const double* g = a.tree + slot_of(2ull * vr + 1) * P;
+                if (lane == 0) {  // one bulk copy (TMA) of the packed Gram
+                    fence_proxy_async();
+                    mbar_arrive_expect_tx(&wbar[0], uint32_t(P * 8));
+                    tma_load_1d(buf, g, uint32_t(P * 8), &wbar[0]);
+                }
                 if (st) {
                     const uint32_t vn = __shfl_sync(0xffffffffu, v, __ffs(st) - 1);
                     if (!is_leaf(a.topo, vn)) {
@@ -1892,7 +1924,8 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
             }
             const int n = re - rs;
             if (n >= kDeepDmmaMin) {
-                cp_async_wait_all();
+                mbar_wait(&wbar[0], gph);
+                gph ^= 1u;
                 __syncwarp();
                 for (int b0 = rs; b0 < re; b0 += 8) {
                     const int nb = min(8, re - b0);
@@ -1915,7 +1948,8 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
                         if (b < uint32_t(R)) xs[t * R + b] = x + x;
                     }
                 }
-                cp_async_wait_all();
+                mbar_wait(&wbar[0], gph);
+                gph ^= 1u;
                 __syncwarp();
                 double ms[3] = {0.0, 0.0, 0.0};
                 if (n == 1)
@@ -1991,15 +2025,22 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
         // rows stream through two half-buffers of PR rows: piece k+1 is in flight
         // while piece k is scanned
         constexpr int PR = C::LROWS / 2;
-        auto issue = [&](uint64_t c0, int slot) {
+        auto issue = [&](uint64_t c0, int slot) {  // one 1-D TMA copy per row (padded stride)
             const int nrow = last - c0 < uint64_t(PR) ? int(last - c0) : PR;
             const char* src = reinterpret_cast<const char*>(U + c0 * R);
             unsigned char* dst = buf + slot * PR * C::RSP;
-            for (int p = lane; p < nrow * PIECES; p += 32) {
-                const int row = p / PIECES, pc = p - row * PIECES;
-                cp_async16(dst + row * C::RSP + pc * 16, src + uint64_t(row) * C::ROWB + pc * 16);
+            if (lane == 0) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&wbar[1 + slot], uint32_t(nrow * C::ROWB));
             }
-            cp_async_commit();
+            __syncwarp();
+            if (lane < nrow) tma_load_1d(dst + lane * C::RSP, src + uint64_t(lane) * C::ROWB, C::ROWB, &wbar[1 + slot]);
+            lpend |= 1u << slot;
+        };
+        auto wait_piece = [&](int slot) {
+            mbar_wait(&wbar[1 + slot], (lph >> slot) & 1u);
+            lph ^= 1u << slot;
+            lpend &= ~(1u << slot);
         };
         issue(first, 0);
         if (st) {  // warm L2 with the first rows of the next run's leaf
@@ -2015,12 +2056,8 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
         for (uint64_t c0 = first; c0 < last; c0 += PR, slot ^= 1) {
             if (!__any_sync(0xffffffffu, in_run && pick == ~uint64_t{0})) break;  // every draw picked
             const int nrow = last - c0 < uint64_t(PR) ? int(last - c0) : PR;
-            if (c0 + PR < last) {
-                issue(c0 + PR, slot ^ 1);
-                cp_async_wait_one();
-            } else {
-                cp_async_wait_all();
-            }
+            if (c0 + PR < last) issue(c0 + PR, slot ^ 1);
+            wait_piece(slot);
             __syncwarp();
             const unsigned char* pbuf = buf + slot * PR * C::RSP;
             for (int b0 = rs; b0 < re; b0 += 8) {
@@ -2071,7 +2108,8 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
             }
             __syncwarp();
         }
-        cp_async_wait_all();  // drain a piece issued before an early exit
+        if (lpend & 1u) wait_piece(0);  // drain a piece issued before an early exit
+        if (lpend & 2u) wait_piece(1);
         __syncwarp();
         if (in_run) {
             if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : last - 1;

@@ -24,8 +24,9 @@ int main(int argc, char** argv) {
     std::mt19937_64 rng(7);
     std::uniform_real_distribution<double> U(-1, 1), U01(0, 1);
     std::vector<double> X(J * R), tree((size_t(tz.L)) * P), ud(J), invc(J), low(J, 0.0), mg(J, 1e300);
-    for (auto& x : X) x = U(rng);
-    for (auto& g : tree) g = U(rng) * 1e-3;
+    const bool simple = std::getenv("LB_SIMPLE") != nullptr;  // low-entropy operands (power / clock probe)
+    for (size_t i = 0; i < X.size(); ++i) X[i] = simple ? 1.0 + 0.125 * double(i % 7) : U(rng);
+    for (size_t i = 0; i < tree.size(); ++i) tree[i] = simple ? 1e-3 * double(1 + i % 5) : U(rng) * 1e-3;
     for (uint64_t s = 0; s < tz.L; ++s)
         for (uint32_t a = 0; a < R; ++a) tree[s * P + pack_index(R, a, a)] = 10.0 + U01(rng);
     for (uint64_t d = 0; d < J; ++d) {
@@ -116,7 +117,8 @@ int main(int argc, char** argv) {
         std::vector<unsigned long long> tr(ntr);
         cudaMemcpy(tr.data(), a.trace, ntr * 8, cudaMemcpyDeviceToHost);
         unsigned long long t0min = ~0ull, t0max = 0, t5max = 0;
-        double ph[5] = {0, 0, 0, 0, 0};
+        double ph[5] = {0, 0, 0, 0, 0}, f6 = 0, f7 = 0;
+        int n67 = 0;
         int nw = 0;
         for (size_t w = 0; w * 8 < ntr; ++w) {
             const unsigned long long* t = &tr[w * 8];
@@ -126,12 +128,18 @@ int main(int argc, char** argv) {
             t0max = std::max(t0max, t[0]);
             t5max = std::max(t5max, t[5]);
             for (int k = 0; k < 5; ++k) ph[k] += double(t[k + 1] - t[k]);
+            if (t[6] && t[7]) {
+                f6 += double(t[6] - t[2]);
+                f7 += double(t[7] - t[6]);
+                ++n67;
+            }
         }
         if (nw)
             std::printf("  last launch: %d warps, span %.1f us, start skew %.1f us; per warp: positions %.2f, list %.2f, "
                         "sweep %.2f, claims %.2f, scatter %.2f us\n",
                         nw, (t5max - t0min) * 1e-3, (t0max - t0min) * 1e-3, ph[0] / nw * 1e-3, ph[1] / nw * 1e-3,
                         ph[2] / nw * 1e-3, ph[3] / nw * 1e-3, ph[4] / nw * 1e-3);
+        if (n67) std::printf("  first block: gram + rows ready %.2f us after the list, its DMMA chain %.2f us\n", f6 / n67 * 1e-3, f7 / n67 * 1e-3);
     }
     std::vector<uint32_t> po(J);
     cudaMemcpy(po.data(), a.perm_out, J * 4, cudaMemcpyDeviceToHost);
