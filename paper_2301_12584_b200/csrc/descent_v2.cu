@@ -1548,12 +1548,13 @@ __global__ void k_make_z(const double* __restrict__ H, const double* __restrict_
                          Topo te, uint32_t R, uint64_t J, double* __restrict__ Z) {
     griddep_launch_dependents();
     griddep_wait();
-    const uint64_t total = J * R;
-    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t d = e / R;
-        const uint32_t c = uint32_t(e % R);
+    // a warp per draw row (no per-element 64-bit division): coalesced H / Z rows
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t d = w0; d < J; d += nw) {
         const uint64_t u = leaf_index(te, node[d]);
-        Z[e] = H[e] * V[uint64_t(c) * R + u];
+        for (uint32_t c = lane; c < R; c += 32) Z[d * R + c] = H[d * R + c] * V[uint64_t(c) * R + u];
     }
 }
 
@@ -2127,11 +2128,12 @@ __global__ void k_apply_pick(double* __restrict__ H, const T* __restrict__ U, co
                              uint64_t J, uint32_t R) {
     griddep_launch_dependents();
     griddep_wait();
-    const uint64_t total = J * R;
-    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t d = e / R;
-        const uint32_t c = uint32_t(e - d * R);
-        H[e] *= static_cast<double>(U[uint64_t(pick[d]) * R + c]);
+    const uint32_t lane = threadIdx.x & 31;  // a warp per draw row
+    const uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t d = w0; d < J; d += nw) {
+        const uint64_t row = uint64_t(pick[d]) * R;
+        for (uint32_t c = lane; c < R; c += 32) H[d * R + c] *= static_cast<double>(U[row + c]);
     }
 }
 
