@@ -2334,8 +2334,8 @@ inline uint32_t deep_chunk() {
 inline uint64_t deep_threshold() {
     static const uint64_t t = [] {
         const char* e = std::getenv("KRPG_DEEP_THRESHOLD");
-        const long v = e ? std::atol(e) : 64;
-        return uint64_t(v >= 1 ? v : 64);
+        const long v = e ? std::atol(e) : 32;
+        return uint64_t(v >= 1 ? v : 32);
     }();
     return t;
 }
