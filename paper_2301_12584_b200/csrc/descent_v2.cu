@@ -1773,6 +1773,11 @@ struct DeepArgs {
 #define KRPG_DEEP_DMMA_MIN 4
 #endif
 constexpr int kDeepDmmaMin = KRPG_DEEP_DMMA_MIN;
+// leaf runs with at most this many draws scan a piece warp-parallel (per draw)
+#ifndef KRPG_LEAF_SCAN_PAR
+#define KRPG_LEAF_SCAN_PAR 4
+#endif
+constexpr int kLeafScanPar = KRPG_LEAF_SCAN_PAR;
 
 template <int NB, typename T>
 struct DeepCfg {
@@ -2088,21 +2093,61 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
                     qa[tt][0] = acc0 * acc0;
                     qa[tt][1] = acc1 * acc1;
                 }
+                if (nb <= kLeafScanPar) {
+                    // few draws: each draw's scan over the piece's rows is spread over the
+                    // warp (lane i = row i): masses gathered from the tile, inclusive
+                    // prefix sum by shuffles, first crossing by ballot; the running sums
+                    // are the sequential ones up to rounding of the additions
+                    static_assert(NTL == 2, "leaf piece of 16 rows");
+                    for (int j = 0; j < nb; ++j) {
+                        const int own = b0 + j;
+                        if (!__shfl_sync(0xffffffffu, pick == ~uint64_t{0} ? 1 : 0, own)) continue;
+                        const double icj = __shfl_sync(0xffffffffu, ic, own);
+                        const double uj = __shfl_sync(0xffffffffu, uu, own);
+                        const double cj = __shfl_sync(0xffffffffu, cum, own);
+                        const int src = (lane & 7) * 4 + (j >> 1);
+                        const double v0 = __shfl_sync(0xffffffffu, (j & 1) ? qa[0][1] : qa[0][0], src);
+                        const double v1 = __shfl_sync(0xffffffffu, (j & 1) ? qa[1][1] : qa[1][0], src);
+                        const bool rowok = lane < nrow;
+                        const double mm = rowok ? icj * (lane < 8 ? v0 : v1) : 0.0;
+                        double sc = mm;
 #pragma unroll
-                for (int tt = 0; tt < NTL; ++tt) {
-                    if (8 * tt >= nrow) break;
-                    const double q0 = qa[tt][0], q1 = qa[tt][1];
-                    const uint64_t rb = c0 + 8 * tt;
+                        for (int o = 1; o < 16; o <<= 1) {
+                            const double t = __shfl_up_sync(0xffffffffu, sc, o);
+                            if (lane >= o) sc += t;
+                        }
+                        const double ci = cj + sc;
+                        const unsigned hit = __ballot_sync(0xffffffffu, rowok && ci >= uj);
+                        const int first = hit ? __ffs(hit) - 1 : nrow - 1;
+                        double dm = (rowok && lane <= first) ? fabs(ci - uj) : HUGE_VAL;
 #pragma unroll
-                    for (int rr = 0; rr < 8; ++rr) {
-                        const double w0 = __shfl_sync(0xffffffffu, q0, rr * 4 + (jj >> 1));
-                        const double w1 = __shfl_sync(0xffffffffu, q1, rr * 4 + (jj >> 1));
-                        if (mine_lane && pick == ~uint64_t{0} && rb + rr < last) {
-                            const double mm = ic * ((jj & 1) ? w1 : w0);
-                            if (mm > 0.0) last_nz = rb + rr;
-                            cum += mm;
-                            mg = fmin(mg, fabs(cum - uu));
-                            if (cum >= uu) pick = rb + rr;
+                        for (int o = 8; o > 0; o >>= 1) dm = fmin(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+                        const unsigned nz = __ballot_sync(0xffffffffu, rowok && lane <= first && mm > 0.0);
+                        const double cend = __shfl_sync(0xffffffffu, ci, first);
+                        if (lane == own) {
+                            mg = fmin(mg, dm);
+                            if (nz) last_nz = c0 + uint64_t(31 - __clz(nz));
+                            cum = cend;
+                            if (hit) pick = c0 + uint64_t(first);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int tt = 0; tt < NTL; ++tt) {
+                        if (8 * tt >= nrow) break;
+                        const double q0 = qa[tt][0], q1 = qa[tt][1];
+                        const uint64_t rb = c0 + 8 * tt;
+#pragma unroll
+                        for (int rr = 0; rr < 8; ++rr) {
+                            const double w0 = __shfl_sync(0xffffffffu, q0, rr * 4 + (jj >> 1));
+                            const double w1 = __shfl_sync(0xffffffffu, q1, rr * 4 + (jj >> 1));
+                            if (mine_lane && pick == ~uint64_t{0} && rb + rr < last) {
+                                const double mm = ic * ((jj & 1) ? w1 : w0);
+                                if (mm > 0.0) last_nz = rb + rr;
+                                cum += mm;
+                                mg = fmin(mg, fabs(cum - uu));
+                                if (cum >= uu) pick = rb + rr;
+                            }
                         }
                     }
                 }
