@@ -1766,6 +1766,7 @@ struct DeepArgs {
     const double* tree;
     Topo topo;
     uint32_t chunk;    // sorted draws per warp (<= 32)
+    int leaf_par;      // leaf runs with at most this many draws scan warp-parallel
 };
 
 // runs with fewer draws than this use the CUDA-core quadratic form (small_qf)
@@ -2093,7 +2094,7 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
                     qa[tt][0] = acc0 * acc0;
                     qa[tt][1] = acc1 * acc1;
                 }
-                if (nb <= kLeafScanPar) {
+                if (nb <= a.leaf_par) {
                     // few draws: each draw's scan over the piece's rows is spread over the
                     // warp (lane i = row i): masses gathered from the tile, inclusive
                     // prefix sum by shuffles, first crossing by ballot; the running sums
@@ -2630,6 +2631,10 @@ int launch_position_grouped(const GroupedArgs& g) {
         da.tree = g.Z;
         da.topo = tz;
         da.chunk = deep_chunk();
+        da.leaf_par = [] {
+            const char* e = std::getenv("KRPG_LEAF_PAR");
+            return e ? std::atoi(e) : kLeafScanPar;
+        }();
         const unsigned grid = unsigned((J + uint64_t(da.chunk) * WPB - 1) / (uint64_t(da.chunk) * WPB));
         if (g.storage == 1)
             dispatch_deep<float>(R, da, grid, g.stream);
