@@ -1767,6 +1767,7 @@ struct DeepArgs {
     Topo topo;
     uint32_t chunk;    // sorted draws per warp (<= 32)
     int leaf_par;      // leaf runs with at most this many draws scan warp-parallel
+    int dmma_min;      // internal-level runs with at least this many draws use DMMA
 };
 
 // runs with fewer draws than this use the CUDA-core quadratic form (small_qf)
@@ -1930,7 +1931,7 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
                 }
             }
             const int n = re - rs;
-            if (n >= kDeepDmmaMin) {
+            if (n >= a.dmma_min) {
                 mbar_wait(&wbar[0], gph);
                 gph ^= 1u;
                 __syncwarp();
@@ -2631,6 +2632,10 @@ int launch_position_grouped(const GroupedArgs& g) {
         da.tree = g.Z;
         da.topo = tz;
         da.chunk = deep_chunk();
+        da.dmma_min = [] {
+            const char* e = std::getenv("KRPG_DEEP_DMMA_MIN");
+            return e ? std::atoi(e) : kDeepDmmaMin;
+        }();
         da.leaf_par = [] {
             const char* e = std::getenv("KRPG_LEAF_PAR");
             return e ? std::atoi(e) : kLeafScanPar;
