@@ -49,7 +49,7 @@ def summarize(path):
         if len(r) <= vi:
             continue
         per.setdefault(r[ii], {"k": r[ki]})[r[mi]] = float(r[vi].replace(",", ""))
-    draws = [v for v in per.values() if any(t in v["k"] for t in ("k_eval", "k_deep", "k_apply_pick", "k_stage_init",
+    draws = [v for v in per.values() if any(t in v["k"] for t in ("k_eval", "k_deep", "k_apply_pick", "k_stage_init", "k_pos0",
                                                                   "k_make_z", "k_leaf2", "k_scatter"))]
     rd = sum(v.get("dram__bytes_read.sum", 0) for v in draws)
     wr = sum(v.get("dram__bytes_write.sum", 0) for v in draws)
