@@ -839,316 +839,6 @@ __global__ void __launch_bounds__(256) k_pos0_place(uint32_t L0, uint64_t J, con
     }
 }
 
-// ---- quad variant (R = 64): the Gram split over the 4 warps of a CTA -------
-// k_eval_reg holds the whole Gram per warp (240 registers): only 2 warps per SM
-// sub-partition, so every latency phase of a level (positions -> rows -> Gram ->
-// decisions -> slot claims) leaves the FP64 tensor pipe idle. Here the 4 warps
-// of a CTA share every 8-draw block: warp w owns the column blocks {w, 7 - w}
-// of the symmetric Gram (9 of the 36 upper-triangle tiles, 18 DMMA per block,
-// ~100 registers), so 4 CTAs (16 warps) fit an SM. Per block each warp's
-// partial x_d^T (G x_d)|_{its columns} goes to shared memory; a batch of 4
-// blocks is finalised by one warp each (partials summed in warp order, branch
-// decision). The CTA's positions, decision inputs and the parents' position
-// ranges are staged into shared memory up front; the rows of the next batch
-// stream in by cp.async while the current batch computes; the child slots of
-// all of the CTA's runs are claimed in one pass at the end.
-constexpr int QW = 4;     // warps per CTA
-constexpr int QCR = 128;  // max sorted positions per CTA
-constexpr int QBB = 4;    // blocks per batch (one finalising warp each)
-constexpr int QXS = 68;   // doubles per staged row (R = 64 + 4: conflict-free A fragments)
-constexpr uint32_t QPARKED = 0xFFFFFFFFu;
-
-struct QuadSmem {
-    static constexpr size_t XB = size_t(2) * QBB * 8 * QXS * 8;  // row batches, double-buffered
-    static constexpr size_t PART = size_t(2) * QBB * QW * 8 * 8;  // per-warp partial masses
-    static constexpr size_t DBL = size_t(5) * QCR * 8;            // root mass, u, 1/C, low, margin
-    static constexpr size_t U32 = size_t(4) * QCR * 4 + (QCR + 1) * 4 + size_t(6) * QCR * 4;
-    static constexpr size_t U16 = size_t(QCR) * 2 + (QCR / 8 + QCR) * 2;
-    static constexpr size_t U8 = QCR;
-    static constexpr size_t SMEM = XB + PART + DBL + U32 + U16 + U8;
-};
-
-template <int MODE, bool ROOT0>
-__global__ void __launch_bounds__(QW * 32, 4) k_eval_quad(EvalArgs a, uint32_t crange) {
-    constexpr int NB = 8, R = 64;
-    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
-    constexpr bool LEVEL = MODE == EV_LEVEL;
-    constexpr unsigned FULL = 0xffffffffu;
-    extern __shared__ __align__(16) double qsm[];
-    double* xb = qsm;
-    double* part = xb + 2 * QBB * 8 * QXS;
-    double* s_root = part + 2 * QBB * QW * 8;
-    double* s_u = s_root + QCR;
-    double* s_ic = s_u + QCR;
-    double* s_lo = s_ic + QCR;
-    double* s_mg = s_lo + QCR;
-    uint32_t* s_d = reinterpret_cast<uint32_t*>(s_mg + QCR);
-    uint32_t* s_v = s_d + QCR;
-    uint32_t* s_rank = s_v + QCR;
-    uint32_t* s_rs = s_rank + QCR;  // QCR + 1
-    uint32_t* s_nl = s_rs + QCR + 1;
-    uint32_t* s_nr = s_nl + QCR;
-    uint32_t* s_bl = s_nr + QCR;
-    uint32_t* s_br = s_bl + QCR;
-    uint32_t* s_gs = s_br + QCR;
-    uint32_t* s_ge = s_gs + QCR;
-    uint16_t* s_run = reinterpret_cast<uint16_t*>(s_ge + QCR);
-    uint16_t* s_blk = s_run + QCR;
-    uint8_t* s_left = reinterpret_cast<uint8_t*>(s_blk + QCR / 8 + QCR);
-    __shared__ int s_nruns, s_nblk;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    griddep_launch_dependents();
-    griddep_wait();
-    const uint64_t c0 = uint64_t(blockIdx.x) * crange;
-    if (c0 >= a.J) return;
-    const int cnt = int(a.J - c0 < uint64_t(crange) ? a.J - c0 : uint64_t(crange));
-
-    // 1. the CTA's positions and their decision inputs
-    for (int t = tid; t < cnt; t += QW * 32) {
-        const uint32_t d = a.perm ? a.perm[c0 + t] : uint32_t(c0 + t);
-        s_d[t] = d;
-        s_v[t] = (LEVEL && !ROOT0) ? (a.nsort_in ? a.nsort_in[c0 + t] : a.node[d]) : 0u;
-        if (LEVEL) {
-            s_u[t] = a.ud[d];
-            if (!ROOT0) {
-                s_ic[t] = a.invc[d];
-                s_lo[t] = a.low[d];
-            }
-            if (a.margin) s_mg[t] = a.margin[d];
-        }
-    }
-    __syncthreads();
-    // 2. runs and the block list (warp 0)
-    if (warp == 0) {
-        int nr = 0;
-        for (int tb = 0; tb < cnt; tb += 32) {
-            const int t = tb + lane;
-            const bool valid = t < cnt;
-            const bool start = valid && (t == 0 || s_v[t] != s_v[t - 1]);
-            const unsigned bal = __ballot_sync(FULL, start);
-            if (start) s_rs[nr + __popc(bal & ((1u << lane) - 1u))] = uint32_t(t);
-            if (valid) s_run[t] = uint16_t(nr + __popc(bal & ((2u << lane) - 1u)) - 1);
-            nr += __popc(bal);
-        }
-        if (lane == 0) {
-            s_rs[nr] = uint32_t(cnt);
-            int nb = 0;
-            for (int r = 0; r < nr; ++r) {
-                const int rs = int(s_rs[r]), re = int(s_rs[r + 1]);
-                if (LEVEL && !ROOT0 && is_leaf(a.topo, s_v[rs])) continue;
-                for (int b0 = rs; b0 < re; b0 += 8) s_blk[nb++] = uint16_t(b0 | (min(8, re - b0) << 8));
-            }
-            s_nruns = nr;
-            s_nblk = nb;
-        }
-    }
-    __syncthreads();
-    const int nruns = s_nruns, nblk = s_nblk;
-    // 3. each run's node range [GS, GE) from its parent's (final since the last level)
-    if (LEVEL)
-        for (int r = tid; r < nruns; r += QW * 32) {
-            const uint32_t v = s_v[s_rs[r]];
-            if (!ROOT0 && is_leaf(a.topo, v)) {
-                s_gs[r] = QPARKED;
-                continue;
-            }
-            uint32_t gs = 0, ge = uint32_t(a.J);
-            if (v != 0) {
-                const uint32_t pp = (v - 1) >> 1;
-                const uint32_t gl = a.GS[pp] + a.cntL[pp];
-                gs = (v & 1u) ? a.GS[pp] : gl;
-                ge = (v & 1u) ? gl : a.GE[pp];
-            }
-            s_gs[r] = gs;
-            s_ge[r] = ge;
-            a.GS[v] = gs;
-            a.GE[v] = ge;
-        }
-
-    // 4. sweeps over the blocks
-    const int q1 = warp, q2 = NB - 1 - warp;
-    const int r4 = lane & 3, cq = lane >> 2, m = lane >> 2;
-    double g1[4][2], g2[NB][2];
-    auto load_frags = [&](const double* __restrict__ G) {
-#pragma unroll
-        for (int p = 0; p < NB; ++p)
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                const int row = 8 * p + 4 * s + r4;
-                const int rowoff = row * R - (row * (row - 1)) / 2 - row;
-                const int col = 8 * p + cq;
-                const int diag = row <= col ? rowoff + col : col * R - (col * (col - 1)) / 2 - col + row;
-                if (p < 4 && p <= q1) g1[p][s] = __ldg(G + (p == q1 ? diag : rowoff + 8 * q1 + cq));
-                if (p <= q2) g2[p][s] = __ldg(G + (p == q2 ? diag : rowoff + 8 * q2 + cq));
-            }
-    };
-    auto stage_batch = [&](int k) {
-        if (k * QBB < nblk) {
-            const int nj = min(QBB, nblk - k * QBB);
-            double* dst = xb + (k & 1) * QBB * 8 * QXS;
-            for (int i = tid; i < nj * 8 * 32; i += QW * 32) {
-                const int j = i >> 8, row = (i >> 5) & 7, pc = i & 31;
-                const uint32_t e = s_blk[k * QBB + j];
-                const int b0 = e & 0xff, n = e >> 8;
-                if (row < n)
-                    cp_async16(dst + (j * 8 + row) * QXS + 2 * pc, a.X + uint64_t(s_d[b0 + row]) * R + 2 * pc);
-            }
-        }
-        cp_async_commit();
-    };
-    auto sweep = [&](bool root_pass) {
-        stage_batch(0);
-        uint32_t gv = 0xFFFFFFFFu;
-        for (int k = 0; k * QBB < nblk; ++k) {
-            stage_batch(k + 1);
-            cp_async_wait_n<1>();
-            __syncthreads();
-            const int nj = min(QBB, nblk - k * QBB);
-            for (int j = 0; j < nj; ++j) {
-                const uint32_t e = s_blk[k * QBB + j];
-                const int b0 = e & 0xff, n = e >> 8;
-                const uint32_t v = s_v[b0];
-                if (v != gv) {
-                    load_frags((LEVEL && !root_pass) ? a.tree + slot_of(2ull * v + 1) * P : a.tree);
-                    gv = v;
-                }
-                const bool valid = m < n;
-                const double* xr = xb + ((k & 1) * QBB + j) * 8 * QXS + m * QXS;
-                double y1a = 0.0, y1b = 0.0, y2a = 0.0, y2b = 0.0;
-#pragma unroll
-                for (int p = 0; p < NB; ++p) {
-                    if (p > q2) break;
-#pragma unroll
-                    for (int s = 0; s < 2; ++s) {
-                        const double av = valid ? xr[8 * p + 4 * s + r4] : 0.0;
-                        const double a2 = av + av;
-                        if (p < 4 && p <= q1) dmma_884(y1a, y1b, p == q1 ? av : a2, g1[p][s]);
-                        dmma_884(y2a, y2b, p == q2 ? av : a2, g2[p][s]);
-                    }
-                }
-                double pt = 0.0;
-                if (valid) {
-                    const double2 x1 = *reinterpret_cast<const double2*>(xr + 8 * q1 + 2 * r4);
-                    const double2 x2 = *reinterpret_cast<const double2*>(xr + 8 * q2 + 2 * r4);
-                    pt = fma(x1.x, y1a, pt);
-                    pt = fma(x1.y, y1b, pt);
-                    pt = fma(x2.x, y2a, pt);
-                    pt = fma(x2.y, y2b, pt);
-                }
-                pt += __shfl_xor_sync(FULL, pt, 1);
-                pt += __shfl_xor_sync(FULL, pt, 2);
-                if (r4 == 0 && valid) part[(((k & 1) * QBB + j) * QW + warp) * 8 + m] = pt;
-            }
-            __syncthreads();
-            if (warp < nj) {  // finalise block k*QBB + warp
-                const uint32_t e = s_blk[k * QBB + warp];
-                const int b0 = e & 0xff, n = e >> 8;
-                if (lane < n) {
-                    const double* pp = part + ((k & 1) * QBB + warp) * QW * 8 + lane;
-                    const double mass = ((pp[0] + pp[8]) + pp[16]) + pp[24];
-                    const int t = b0 + lane;
-                    const uint32_t dd = s_d[t];
-                    if (root_pass) {
-                        if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
-                        s_root[t] = mass;
-                    } else if (MODE == EV_PROB) {
-                        a.prob[dd] = mass / a.rank_div;
-                    } else if (MODE == EV_ROOT) {
-                        if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
-                        a.invc[dd] = 1.0 / mass;
-                    } else {
-                        const uint32_t v = s_v[b0];
-                        const double u = s_u[t];
-                        double ic, cutoff;
-                        if (ROOT0) {
-                            ic = 1.0 / s_root[t];
-                            a.invc[dd] = ic;
-                            cutoff = 0.0 + ic * mass;
-                        } else {
-                            ic = s_ic[t];
-                            cutoff = s_lo[t] + ic * mass;
-                        }
-                        const bool left = cutoff >= u;
-                        if (a.margin) a.margin[dd] = fmin(s_mg[t], fabs(cutoff - u));
-                        if (left) {
-                            a.node[dd] = 2 * v + 1;
-                        } else {
-                            a.node[dd] = 2 * v + 2;
-                            a.low[dd] = cutoff;
-                        }
-                        s_left[t] = left ? 1 : 0;
-                    }
-                }
-            }
-        }
-        cp_async_wait_all();
-        __syncthreads();
-    };
-    if (ROOT0) sweep(true);
-    sweep(false);
-    if (!LEVEL) return;
-
-    // 5. ranks within each run's left / right part (warp 0, chunks of 32 in order)
-    if (warp == 0) {
-        uint32_t carryL = 0, carryR = 0;
-        const unsigned below = (1u << lane) - 1u;
-        for (int tb = 0; tb < cnt; tb += 32) {
-            const int t = tb + lane;
-            const bool valid = t < cnt;
-            const int r = valid ? s_run[t] : 0;
-            const bool moved = valid && s_gs[r] != QPARKED;
-            const bool lf = moved && s_left[t];
-            const unsigned lm = __ballot_sync(FULL, lf), rm = __ballot_sync(FULL, moved && !lf);
-            const int rs = valid ? int(s_rs[r]) : t, re = valid ? int(s_rs[r + 1]) : t + 1;
-            const int lo = rs > tb ? rs - tb : 0, hi = re - tb < 32 ? re - tb : 32;
-            const unsigned runm = (hi >= 32 ? FULL : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
-            const bool cont = rs < tb;  // run began in an earlier chunk
-            const uint32_t nlc = __popc(lm & runm), nrc = __popc(rm & runm);
-            if (moved) {
-                s_rank[t] = lf ? __popc(lm & runm & below) + (cont ? carryL : 0u)
-                               : __popc(rm & runm & below) + (cont ? carryR : 0u);
-                if (t == re - 1) {
-                    s_nl[r] = nlc + (cont ? carryL : 0u);
-                    s_nr[r] = nrc + (cont ? carryR : 0u);
-                }
-            } else if (valid && t == re - 1) {
-                s_nl[r] = 0;
-                s_nr[r] = 0;
-            }
-            // the run crossing into the next chunk carries its counts
-            const uint32_t nL = __shfl_sync(FULL, nlc + (cont ? carryL : 0u), 31);
-            const uint32_t nR = __shfl_sync(FULL, nrc + (cont ? carryR : 0u), 31);
-            carryL = nL;
-            carryR = nR;
-        }
-    }
-    __syncthreads();
-    // 6. slot claims, one pair of atomics per run
-    for (int r = tid; r < nruns; r += QW * 32) {
-        if (s_gs[r] == QPARKED) continue;
-        const uint32_t v = s_v[s_rs[r]];
-        s_bl[r] = s_nl[r] ? atomicAdd(a.cntL + v, s_nl[r]) : 0u;
-        s_br[r] = s_nr[r] ? atomicAdd(a.cntR + v, s_nr[r]) : 0u;
-    }
-    __syncthreads();
-    // 7. next level's order
-    for (int t = tid; t < cnt; t += QW * 32) {
-        const int r = s_run[t];
-        const uint32_t d = s_d[t], v = s_v[t];
-        if (s_gs[r] == QPARKED) {
-            a.perm_out[c0 + t] = d;
-            if (a.nsort_out) a.nsort_out[c0 + t] = v;
-        } else {
-            const bool lf = s_left[t];
-            const uint32_t rk = s_rank[t];
-            const uint32_t pos = lf ? s_gs[r] + s_bl[r] + rk : s_ge[r] - 1u - (s_br[r] + rk);
-            a.perm_out[pos] = d;
-            if (a.nsort_out) a.nsort_out[pos] = 2 * v + (lf ? 1u : 2u);
-        }
-    }
-}
-
 // ---- ranks whose Gram does not fit shared memory (R > 160) ----------------
 // Same CTA / run / decision structure as k_eval_cta, but each run's packed
 // Gram is streamed HBM/L2 -> shared memory in chunks of whole 8-row tile-rows
@@ -1772,12 +1462,12 @@ struct DeepArgs {
 
 // runs with fewer draws than this use the CUDA-core quadratic form (small_qf)
 #ifndef KRPG_DEEP_DMMA_MIN
-#define KRPG_DEEP_DMMA_MIN 4
+#define KRPG_DEEP_DMMA_MIN 1
 #endif
 constexpr int kDeepDmmaMin = KRPG_DEEP_DMMA_MIN;
 // leaf runs with at most this many draws scan a piece warp-parallel (per draw)
 #ifndef KRPG_LEAF_SCAN_PAR
-#define KRPG_LEAF_SCAN_PAR 4
+#define KRPG_LEAF_SCAN_PAR 8
 #endif
 constexpr int kLeafScanPar = KRPG_LEAF_SCAN_PAR;
 
@@ -1902,6 +1592,7 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
     const FragAddr<NB> fa(lane);
     const unsigned below = (1u << lane) - 1u;
     const double* Gs = reinterpret_cast<const double*>(buf);
+    const int r4d = lane & 3;
 
     for (uint32_t lev = a.level0; lev < a.topo.d; ++lev) {
         const uint32_t prevv = __shfl_up_sync(0xffffffffu, v, 1);
@@ -1932,14 +1623,27 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
             }
             const int n = re - rs;
             if (n >= a.dmma_min) {
+                // the first block's A fragments are requested before waiting on the Gram
+                const int m = lane >> 2;
+                double av0[NB][2];
+                {
+                    const uint32_t dd = __shfl_sync(0xffffffffu, d, (rs + m) & 31);
+                    const double* xr = a.X + uint64_t(dd) * R;
+                    const bool valid = m < min(8, n);
+#pragma unroll
+                    for (int p = 0; p < NB; ++p)
+#pragma unroll
+                        for (int s = 0; s < 2; ++s) av0[p][s] = valid ? xr[8 * p + 4 * s + r4d] : 0.0;
+                }
                 mbar_wait(&wbar[0], gph);
                 gph ^= 1u;
                 __syncwarp();
                 for (int b0 = rs; b0 < re; b0 += 8) {
                     const int nb = min(8, re - b0);
-                    const int m = lane >> 2;
                     const uint32_t dd = __shfl_sync(0xffffffffu, d, (b0 + m) & 31);
-                    const double mass = block_qf_packed<NB>(Gs, fa, m < nb ? a.X + uint64_t(dd) * R : nullptr, lane);
+                    const double* xr = m < nb ? a.X + uint64_t(dd) * R : nullptr;
+                    const double mass = b0 == rs ? qf::block_qf_packed_pre<NB>(Gs, fa, av0, xr, lane)
+                                                 : block_qf_packed<NB>(Gs, fa, xr, lane);
                     const double mj = __shfl_sync(0xffffffffu, mass, (4 * (lane - b0)) & 31);
                     if (lane >= b0 && lane < b0 + nb) mine = mj;
                 }
@@ -2096,41 +1800,57 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
                     qa[tt][1] = acc1 * acc1;
                 }
                 if (nb <= a.leaf_par) {
-                    // few draws: each draw's scan over the piece's rows is spread over the
-                    // warp (lane i = row i): masses gathered from the tile, inclusive
-                    // prefix sum by shuffles, first crossing by ballot; the running sums
-                    // are the sequential ones up to rounding of the additions
+                    // each draw's scan over the piece's rows is spread over a half warp
+                    // (lane 16h + i = row i of draw j + h): masses gathered from the tile,
+                    // inclusive prefix sum by shuffles, first crossing by ballot; two draws
+                    // per step. A draw's result does not depend on the other draws of its run.
                     static_assert(NTL == 2, "leaf piece of 16 rows");
-                    for (int j = 0; j < nb; ++j) {
-                        const int own = b0 + j;
-                        if (!__shfl_sync(0xffffffffu, pick == ~uint64_t{0} ? 1 : 0, own)) continue;
+                    const int half = lane >> 4, i = lane & 15;
+                    for (int j = 0; j < nb; j += 2) {
+                        const int jj = j + half;
+                        const bool dv = jj < nb;
+                        const int own = b0 + (dv ? jj : j);
+                        const bool act = __shfl_sync(0xffffffffu, pick == ~uint64_t{0} ? 1 : 0, own) != 0;
                         const double icj = __shfl_sync(0xffffffffu, ic, own);
                         const double uj = __shfl_sync(0xffffffffu, uu, own);
                         const double cj = __shfl_sync(0xffffffffu, cum, own);
-                        const int src = (lane & 7) * 4 + (j >> 1);
-                        const double v0 = __shfl_sync(0xffffffffu, (j & 1) ? qa[0][1] : qa[0][0], src);
-                        const double v1 = __shfl_sync(0xffffffffu, (j & 1) ? qa[1][1] : qa[1][0], src);
-                        const bool rowok = lane < nrow;
-                        const double mm = rowok ? icj * (lane < 8 ? v0 : v1) : 0.0;
+                        const int src = (i & 7) * 4 + (jj >> 1);
+                        const double v00 = __shfl_sync(0xffffffffu, qa[0][0], src);
+                        const double v01 = __shfl_sync(0xffffffffu, qa[0][1], src);
+                        const double v10 = __shfl_sync(0xffffffffu, qa[1][0], src);
+                        const double v11 = __shfl_sync(0xffffffffu, qa[1][1], src);
+                        const double q = i < 8 ? ((jj & 1) ? v01 : v00) : ((jj & 1) ? v11 : v10);
+                        const bool rowok = dv && act && i < nrow;
+                        const double mm = rowok ? icj * q : 0.0;
                         double sc = mm;
 #pragma unroll
                         for (int o = 1; o < 16; o <<= 1) {
-                            const double t = __shfl_up_sync(0xffffffffu, sc, o);
-                            if (lane >= o) sc += t;
+                            const double t = __shfl_up_sync(0xffffffffu, sc, o, 16);
+                            if (i >= o) sc += t;
                         }
                         const double ci = cj + sc;
-                        const unsigned hit = __ballot_sync(0xffffffffu, rowok && ci >= uj);
+                        const unsigned hb = __ballot_sync(0xffffffffu, rowok && ci >= uj);
+                        const unsigned hit = (hb >> (16 * half)) & 0xffffu;
                         const int first = hit ? __ffs(hit) - 1 : nrow - 1;
-                        double dm = (rowok && lane <= first) ? fabs(ci - uj) : HUGE_VAL;
+                        double dm = (rowok && i <= first) ? fabs(ci - uj) : HUGE_VAL;
 #pragma unroll
                         for (int o = 8; o > 0; o >>= 1) dm = fmin(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-                        const unsigned nz = __ballot_sync(0xffffffffu, rowok && lane <= first && mm > 0.0);
-                        const double cend = __shfl_sync(0xffffffffu, ci, first);
-                        if (lane == own) {
-                            mg = fmin(mg, dm);
-                            if (nz) last_nz = c0 + uint64_t(31 - __clz(nz));
-                            cum = cend;
-                            if (hit) pick = c0 + uint64_t(first);
+                        const unsigned nzb = __ballot_sync(0xffffffffu, rowok && i <= first && mm > 0.0);
+                        const unsigned nz = (nzb >> (16 * half)) & 0xffffu;
+                        const double cend = __shfl_sync(0xffffffffu, ci, 16 * half + first);
+                        // results of half h live in its lanes; hand them to the draw's own lane
+                        const int h_of_me = lane - b0 - j;  // 0 or 1 if this lane owns draw j or j + 1
+                        const bool mine_here = h_of_me == 0 || (h_of_me == 1 && j + 1 < nb);
+                        const int from = 16 * (h_of_me == 1 ? 1 : 0);
+                        const double dm_r = __shfl_sync(0xffffffffu, dm, from);
+                        const double ce_r = __shfl_sync(0xffffffffu, cend, from);
+                        const unsigned hit_r = (hb >> from) & 0xffffu;
+                        const unsigned nz_r = (nzb >> from) & 0xffffu;
+                        if (mine_here && pick == ~uint64_t{0}) {
+                            mg = fmin(mg, dm_r);
+                            if (nz_r) last_nz = c0 + uint64_t(31 - __clz(nz_r));
+                            cum = ce_r;
+                            if (hit_r) pick = c0 + uint64_t(__ffs(hit_r) - 1);
                         }
                     }
                 } else {
@@ -2282,42 +2002,9 @@ void launch_reg(const EvalArgs& a, cudaStream_t s) {
     launch_pdl(k_eval_reg<NB, MODE, ROOT0>, dim3(grid), dim3(RW * 32), C::SMEM, s, a, uint32_t(range));
 }
 
-inline int eval_quad_mode() {  // KRPG_EVAL_QUAD: 1 on, default off (measured slower)
-    static const int on = [] {
-        const char* e = std::getenv("KRPG_EVAL_QUAD");
-        return (e && e[0] == '1') ? 1 : 0;
-    }();
-    return on;
-}
-
-template <int MODE, bool ROOT0>
-void launch_quad(const EvalArgs& a, cudaStream_t s) {
-    static int ctas = 0;
-    if (!ctas) {
-        cudaFuncSetAttribute(k_eval_quad<MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(QuadSmem::SMEM));
-        int dev = 0, sms = 0, bps = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_eval_quad<MODE, ROOT0>, QW * 32, QuadSmem::SMEM);
-        ctas = std::max(1, sms * std::max(1, bps));
-    }
-    uint64_t cr = (a.J + uint64_t(ctas) - 1) / uint64_t(ctas);
-    cr = std::min<uint64_t>(std::max<uint64_t>((cr + 7) / 8 * 8, 8), QCR);
-    const unsigned grid = unsigned((a.J + cr - 1) / cr);
-    launch_pdl(k_eval_quad<MODE, ROOT0>, dim3(grid), dim3(QW * 32), QuadSmem::SMEM, s, a, uint32_t(cr));
-}
-
 template <int NB>
 void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
     const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
-    if constexpr (NB == 8) {
-        if (eval_quad_mode() && !warp_variant) {
-            if (mode == EV_PROB) return launch_quad<EV_PROB, false>(a, s);
-            if (mode == EV_LEVEL0) return launch_quad<EV_LEVEL, true>(a, s);
-            if (mode == EV_LEVEL) return launch_quad<EV_LEVEL, false>(a, s);
-        }
-    }
     if constexpr (NB <= 8) {
         if (eval_reg_enabled() && !warp_variant) {
             if (mode == EV_PROB) return launch_reg<NB, EV_PROB, false>(a, s);

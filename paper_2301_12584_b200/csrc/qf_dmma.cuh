@@ -75,5 +75,43 @@ __device__ __forceinline__ double block_qf_packed(const double* G, const FragAdd
     return part;
 }
 
+// block_qf_packed with the A fragments already in registers (av[p][s] = x[8p+4s+(lane&3)]
+// of row lane>>2, zero for invalid rows); xr (the row, nullable) for the epilogue.
+// Same operation order, bit-identical result.
+template <int NB>
+__device__ __forceinline__ double block_qf_packed_pre(const double* G, const FragAddr<NB>& fa, const double (&av)[NB][2],
+                                                      const double* xr, int lane) {
+    const int r4 = lane & 3, cq = lane >> 2;
+    double y[NB][2];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) y[q][0] = y[q][1] = 0.0;
+#pragma unroll
+    for (int p = 0; p < NB; ++p) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const double gd = G[fa.diag[p][s]];
+            dmma_884(y[p][0], y[p][1], av[p][s], gd);
+            const double a2 = av[p][s] + av[p][s];
+#pragma unroll
+            for (int q = p + 1; q < NB; ++q) {
+                const double g = G[fa.rowoff[p][s] + 8 * q + cq];
+                dmma_884(y[q][0], y[q][1], a2, g);
+            }
+        }
+    }
+    double part = 0.0;
+    if (xr) {
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const double2 xv = *reinterpret_cast<const double2*>(xr + 8 * q + 2 * r4);
+            part = fma(xv.x, y[q][0], part);
+            part = fma(xv.y, y[q][1], part);
+        }
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    return part;
+}
+
 }  // namespace qf
 }  // namespace krpg
