@@ -1216,9 +1216,10 @@ __global__ void k_scatter(const uint32_t* __restrict__ perm_in, uint32_t* __rest
 // stage init: identity order, everyone at the root, this stage's uniform
 __global__ void k_stage_init(uint32_t* perm, uint32_t* node, double* low, double* ud, uint32_t* gstart,
                              uint64_t J, uint64_t seed, uint64_t off, uint64_t counter, double* margin,
-                             int reset_margin, uint32_t* cntL, uint32_t* cntR, uint64_t nnodes) {
+                             int reset_margin, uint32_t* cntL, uint32_t* cntR, uint64_t nnodes, uint32_t* zero1) {
     griddep_launch_dependents();
     griddep_wait();
+    if (zero1 && blockIdx.x == 0 && threadIdx.x == 0) *zero1 = 0;
     for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nnodes; v += uint64_t(gridDim.x) * blockDim.x) {
         cntL[v] = 0;
         cntR[v] = 0;
@@ -1458,6 +1459,7 @@ struct DeepArgs {
     uint32_t chunk;    // sorted draws per warp (<= 32)
     int leaf_par;      // leaf runs with at most this many draws scan warp-parallel
     int dmma_min;      // internal-level runs with at least this many draws use DMMA
+    uint32_t* work;    // chunk counter (zeroed before the launch) for persistent warps, nullable
 };
 
 // runs with fewer draws than this use the CUDA-core quadratic form (small_qf)
@@ -1566,8 +1568,6 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
     unsigned char* buf = wbase;
     double* xs = reinterpret_cast<double*>(wbase + C::BUF);
     uint32_t* perm_sm = reinterpret_cast<uint32_t*>(wbase + C::BUF + C::XS);
-    const uint64_t base = (uint64_t(blockIdx.x) * WPB + warp) * a.chunk;
-    if (base >= a.J) return;
     // 1-D TMA completion barriers: [0] node Gram, [1], [2] leaf-row half buffers
     uint64_t* wbar = reinterpret_cast<uint64_t*>(wbase + C::BUF + C::XS + 128);
     if (lane == 0) {
@@ -1578,6 +1578,20 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
     }
     __syncwarp();
     uint32_t gph = 0, lph = 0, lpend = 0;
+    // persistent warps take chunks of sorted positions from a counter (no ragged last
+    // wave); a chunk's result does not depend on which warp processes it
+    for (uint32_t it = 0;; ++it) {
+    uint64_t ci;
+    if (a.work) {
+        uint32_t c = 0;
+        if (lane == 0) c = atomicAdd(a.work, 1u);
+        ci = __shfl_sync(0xffffffffu, c, 0);
+    } else {
+        if (it > 0) break;
+        ci = uint64_t(blockIdx.x) * WPB + warp;
+    }
+    const uint64_t base = ci * a.chunk;
+    if (base >= a.J) break;
     const int cnt = a.J - base < uint64_t(a.chunk) ? int(a.J - base) : int(a.chunk);
     const bool live = lane < cnt;
     uint32_t d = live ? a.perm[base + lane] : 0u;
@@ -1886,6 +1900,7 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
             a.pick[d] = uint32_t(pick);
         }
     }
+    }  // chunk loop
 }
 
 // h_d *= U_k[pick_d] for every draw (krp_sampler.cpp:137-138): one thread per
@@ -2075,14 +2090,27 @@ inline uint64_t deep_threshold() {
 }
 inline bool deep_level(uint64_t J, uint32_t level) { return (J >> level) < deep_threshold(); }
 
+inline bool deep_persistent() {
+    static const bool on = [] {
+        const char* e = std::getenv("KRPG_DEEP_PERSISTENT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int NB, typename T>
 void launch_deep2(const DeepArgs& a, unsigned grid, cudaStream_t s) {
     using C = DeepCfg<NB, T>;
-    static bool configured = false;
-    if (!configured) {
+    static int resident = 0;
+    if (!resident) {
         cudaFuncSetAttribute(k_deep2<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        configured = true;
+        int dev = 0, sms = 0, bps = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_deep2<NB, T>, WPB * 32, C::SMEM);
+        resident = std::max(1, sms * std::max(1, bps));
     }
+    if (a.work) grid = std::min<unsigned>(grid, unsigned(resident));  // persistent: one wave
     launch_pdl(k_deep2<NB, T>, dim3(grid), dim3(WPB * 32), C::SMEM, s, a);
 }
 
@@ -2210,7 +2238,8 @@ int launch_position_grouped(const GroupedArgs& g) {
     // ---------------- stage 1: eigenvector tree (F = 1, Y = G_k) ----------------
     const Topo te = make_topo(R, 1);
     launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
-               g.draw_offset, 2ull * g.pos + 1, g.margin, int(g.pos == 0), g.cntL, g.cntR, uint64_t(te.n));
+               g.draw_offset, 2ull * g.pos + 1, g.margin, int(g.pos == 0), g.cntL, g.cntR, uint64_t(te.n),
+               (uint32_t*)nullptr);
     ++launches;
     mark(13);
     e.GS = g.gstart;
@@ -2263,6 +2292,8 @@ int launch_position_grouped(const GroupedArgs& g) {
     double* etab = g.pos0_tab;
     double* ztab = etab ? etab + 2 * R + 8 : nullptr;
     uint32_t* hist = etab ? reinterpret_cast<uint32_t*>(ztab + (uint64_t(1) << kPos0Levels) * R) : nullptr;
+    // chunk counter of the persistent deep pass (zeroed by the factor-tree stage init)
+    uint32_t* deep_work = (hist && g.fused_deep && R <= 64 && deep_persistent()) ? hist + 300 : nullptr;
     e.X = g.H;
     e.tree = g.Q;
     e.topo = te;
@@ -2282,7 +2313,7 @@ int launch_position_grouped(const GroupedArgs& g) {
 
     // ---------------- stage 2: factor tree, rank-1 M = z z^T ----------------
     launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
-               g.draw_offset, 2ull * g.pos + 2, g.margin, 0, g.cntL, g.cntR, uint64_t(tz.n));
+               g.draw_offset, 2ull * g.pos + 2, g.margin, 0, g.cntL, g.cntR, uint64_t(tz.n), deep_work);
     ++launches;
     mark(13);
     e.X = g.Zb;
@@ -2319,6 +2350,7 @@ int launch_position_grouped(const GroupedArgs& g) {
         da.tree = g.Z;
         da.topo = tz;
         da.chunk = deep_chunk();
+        da.work = deep_work;
         da.dmma_min = [] {
             const char* e = std::getenv("KRPG_DEEP_DMMA_MIN");
             return e ? std::atoi(e) : kDeepDmmaMin;
