@@ -677,6 +677,305 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     if (tr && lane == 0) tr[5] = gtimer();
 }
 
+// ---- R = 128: the Gram split over the 4 warps of a CTA (register-resident) ----
+// One register-resident Gram per warp does not fit at R = 128 (272 fragments per
+// lane), so the 4 warps of a CTA share every 8-draw block of the CTA's <= 64
+// positions: warp w holds the upper-triangle tiles of the column blocks
+// {w, 7-w, 8+w, 15-w} (34 tiles, 68 doubles per lane, off-diagonal ones pre-doubled)
+// and computes those columns' share of x_d^T G x_d for all blocks; the four
+// partial masses are summed in warp order after ONE CTA barrier per sweep. The
+// CTA's rows arrive by one 1-D TMA copy per row at the start; decisions, ranks,
+// slot claims and the next level's order follow k_eval_reg.
+constexpr int SPW = 4;        // warps per CTA
+constexpr int SPR = 64;       // max positions per CTA
+constexpr int SPXS = 128 + 4;  // doubles per staged row
+struct Split16Smem {
+    static constexpr size_t ROWS = size_t(SPR) * SPXS * 8;
+    static constexpr size_t PART = size_t(2) * SPW * SPR * 8;  // root and node partial masses
+    static constexpr size_t DBL = size_t(4) * SPR * 8;         // u, 1/C, low, margin
+    static constexpr size_t U32 = size_t(2) * SPR * 4 + size_t(7) * SPR * 4;
+    static constexpr size_t SMEM = ROWS + PART + DBL + U32 + SPR * 2 + 64;
+};
+
+// Warp w owns the column-block pairs {w, 15-w} and {7-w, 8+w}: every pair has 17
+// upper-triangle tiles (p <= q), listed as entries k = 0..16 of a fixed shape -
+// k <= a: tile (k, a), else tile (k-a-1, 15-a) - so the fragment registers are
+// indexed at compile time for any w; the entry's column selects its accumulator.
+__device__ __forceinline__ void split16_entry(int a, int k, int& p, int& col) {
+    p = k <= a ? k : k - a - 1;
+    col = k <= a ? a : 15 - a;
+}
+
+__device__ __forceinline__ void split16_load(double (&g)[2][17][2], const double* __restrict__ G, int w, int lane) {
+    constexpr int R = 128;
+    const int r4 = lane & 3, cq = lane >> 2;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int a = c == 0 ? w : 7 - w;
+#pragma unroll
+        for (int k = 0; k < 17; ++k) {
+            int p, q;  // tile (p, q) of column block q
+            split16_entry(a, k, p, q);
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const int row = 8 * p + 4 * s + r4;
+                const int rowoff = row * R - (row * (row - 1)) / 2 - row;
+                if (p == q) {
+                    const int cc = 8 * p + cq;
+                    const int diag = row <= cc ? rowoff + cc : cc * R - (cc * (cc - 1)) / 2 - cc + row;
+                    g[c][k][s] = __ldg(G + diag);
+                } else {
+                    const double x = __ldg(G + rowoff + 8 * q + cq);
+                    g[c][k][s] = x + x;
+                }
+            }
+        }
+    }
+}
+
+// this warp's columns' share of the masses of the block rows xs (row m valid iff valid)
+__device__ __forceinline__ double split16_block(const double (&g)[2][17][2], const double* xs, bool valid, int w,
+                                                int lane) {
+    const int r4 = lane & 3, m = lane >> 2;
+    const double* xr = xs + m * SPXS;
+    double y[2][2][2];  // [pair][first / second column][c0, c1]
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) y[c][h][0] = y[c][h][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int a = c == 0 ? w : 7 - w;
+#pragma unroll
+        for (int k = 0; k < 17; ++k) {
+            int p, col;
+            split16_entry(a, k, p, col);
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const double av = valid ? xr[8 * p + 4 * s + r4] : 0.0;
+                if (k <= a)
+                    dmma_884(y[c][0][0], y[c][0][1], av, g[c][k][s]);
+                else
+                    dmma_884(y[c][1][0], y[c][1][1], av, g[c][k][s]);
+            }
+        }
+    }
+    double part = 0.0;
+    if (valid) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int a = c == 0 ? w : 7 - w;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int q = h == 0 ? a : 15 - a;
+                const double2 xv = *reinterpret_cast<const double2*>(xr + 8 * q + 2 * r4);
+                part = fma(xv.x, y[c][h][0], part);
+                part = fma(xv.y, y[c][h][1], part);
+            }
+        }
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    return part;
+}
+
+template <int MODE, bool ROOT0>
+__global__ void __launch_bounds__(SPW * 32, 2) k_eval_split16(EvalArgs a) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr bool LEVEL = MODE == EV_LEVEL;
+    extern __shared__ __align__(16) unsigned char sp_smem[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ int s_nruns, s_nblk;
+    __shared__ uint64_t s_lm[2], s_mm[2];
+    double* rows = reinterpret_cast<double*>(sp_smem);
+    double* part = rows + SPR * SPXS;                 // [2][SPW][SPR]
+    double* s_u = part + 2 * SPW * SPR;
+    double* s_ic = s_u + SPR;
+    double* s_lo = s_ic + SPR;
+    double* s_mg = s_lo + SPR;
+    uint32_t* s_d = reinterpret_cast<uint32_t*>(s_mg + SPR);
+    uint32_t* s_v = s_d + SPR;
+    uint32_t* s_rs = s_v + SPR;  // per run (SPR + 1)
+    uint32_t* s_rv = s_rs + SPR + 1;
+    uint32_t* s_gs = s_rv + SPR;
+    uint32_t* s_ge = s_gs + SPR;
+    uint32_t* s_bl = s_ge + SPR;
+    uint32_t* s_br = s_bl + SPR;
+    uint16_t* s_blk = reinterpret_cast<uint16_t*>(s_br + SPR);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    griddep_launch_dependents();
+    griddep_wait();
+    const uint64_t c0 = uint64_t(blockIdx.x) * SPR;
+    if (c0 >= a.J) return;
+    const int cnt = int(a.J - c0 < uint64_t(SPR) ? a.J - c0 : uint64_t(SPR));
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+    }
+    if (tid < cnt) {
+        const uint32_t d = a.perm ? a.perm[c0 + tid] : uint32_t(c0 + tid);
+        s_d[tid] = d;
+        s_v[tid] = (LEVEL && !ROOT0) ? (a.nsort_in ? a.nsort_in[c0 + tid] : a.node[d]) : 0u;
+        if (LEVEL) {
+            s_u[tid] = a.ud[d];
+            if (!ROOT0) {
+                s_ic[tid] = a.invc[d];
+                s_lo[tid] = a.low[d];
+            }
+            if (a.margin) s_mg[tid] = a.margin[d];
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {  // rows (one bulk copy each), runs, block list
+        if (lane == 0) mbar_arrive_expect_tx(&s_bar, uint32_t(cnt) * 128 * 8);
+        __syncwarp();
+        for (int t = lane; t < cnt; t += 32)
+            tma_load_1d(rows + t * SPXS, a.X + uint64_t(s_d[t]) * 128, 128 * 8, &s_bar);
+        int nr = 0;
+        for (int tb = 0; tb < cnt; tb += 32) {
+            const int t = tb + lane;
+            const bool start = t < cnt && (t == 0 || s_v[t] != s_v[t - 1]);
+            const unsigned bal = __ballot_sync(FULL, start);
+            if (start) {
+                const int r = nr + __popc(bal & ((1u << lane) - 1u));
+                s_rs[r] = uint32_t(t);
+                s_rv[r] = s_v[t];
+            }
+            nr += __popc(bal);
+        }
+        if (lane == 0) {
+            s_rs[nr] = uint32_t(cnt);
+            int nb = 0;
+            for (int r = 0; r < nr; ++r) {
+                const int rs = int(s_rs[r]), re = int(s_rs[r + 1]);
+                if (LEVEL && !ROOT0 && is_leaf(a.topo, s_rv[r])) continue;
+                for (int b0 = rs; b0 < re; b0 += 8) s_blk[nb++] = uint16_t(b0 | (min(8, re - b0) << 8));
+            }
+            s_nruns = nr;
+            s_nblk = nb;
+        }
+    }
+    __syncthreads();
+    const int nruns = s_nruns, nblk = s_nblk;
+    if (LEVEL)  // the parents' ranges of every run
+        for (int r = tid; r < nruns; r += SPW * 32) {
+            const uint32_t v = s_rv[r];
+            if (!ROOT0 && is_leaf(a.topo, v)) continue;
+            uint32_t gs = 0, ge = uint32_t(a.J);
+            if (v != 0) {
+                const uint32_t pp = (v - 1) >> 1;
+                const uint32_t gl = a.GS[pp] + a.cntL[pp];
+                gs = (v & 1u) ? a.GS[pp] : gl;
+                ge = (v & 1u) ? gl : a.GE[pp];
+            }
+            s_gs[r] = gs;
+            s_ge[r] = ge;
+            a.GS[v] = gs;
+            a.GE[v] = ge;
+        }
+    mbar_wait(&s_bar, 0);
+    auto sweep = [&](bool node_gram, double* pbuf) {
+        double* pw = pbuf + warp * SPR;
+        constexpr uint64_t P = 128ull * 129 / 2;
+        double g[2][17][2];
+        uint32_t gv = 0xFFFFFFFFu;
+        for (int i = 0; i < nblk; ++i) {
+            const uint32_t e = s_blk[i];
+            const int b0 = e & 0xff, n = e >> 8;
+            const uint32_t v = s_v[b0];
+            if (v != gv) {
+                split16_load(g, node_gram ? a.tree + slot_of(2ull * v + 1) * P : a.tree, warp, lane);
+                gv = v;
+            }
+            const int m = lane >> 2;
+            const double pm = split16_block(g, rows + b0 * SPXS, m < n, warp, lane);
+            if ((lane & 3) == 0 && m < n) pw[b0 + m] = pm;
+        }
+    };
+    if (ROOT0) sweep(false, part + SPW * SPR);
+    sweep(LEVEL && true, part);
+    __syncthreads();
+    // decisions (positions t = tid < cnt: warps 0 and 1)
+    bool lf = false, mv = false;
+    if (tid < cnt) {
+        const int t = tid;
+        const uint32_t d = s_d[t], v = s_v[t];
+        const bool parked = LEVEL && !ROOT0 && is_leaf(a.topo, v);
+        if (!parked) {
+            const double mass = ((part[t] + part[SPR + t]) + part[2 * SPR + t]) + part[3 * SPR + t];
+            if (MODE == EV_PROB) {
+                a.prob[d] = mass / a.rank_div;
+            } else if (MODE == EV_ROOT) {
+                if (!isfinite(mass) || mass <= 0.0) atomicExch(a.err, 1);
+                a.invc[d] = 1.0 / mass;
+            } else {
+                const double u = s_u[t];
+                double ic, cutoff;
+                if (ROOT0) {
+                    const double* pr = part + SPW * SPR;
+                    const double croot = ((pr[t] + pr[SPR + t]) + pr[2 * SPR + t]) + pr[3 * SPR + t];
+                    if (!isfinite(croot) || croot <= 0.0) atomicExch(a.err, 1);
+                    ic = 1.0 / croot;
+                    a.invc[d] = ic;
+                    cutoff = 0.0 + ic * mass;
+                } else {
+                    ic = s_ic[t];
+                    cutoff = s_lo[t] + ic * mass;
+                }
+                const bool left = cutoff >= u;
+                if (a.margin) a.margin[d] = fmin(s_mg[t], fabs(cutoff - u));
+                if (left) {
+                    a.node[d] = 2 * v + 1;
+                } else {
+                    a.node[d] = 2 * v + 2;
+                    a.low[d] = cutoff;
+                }
+                lf = left;
+                mv = true;
+            }
+        }
+    }
+    if (!LEVEL) return;
+    if (warp < 2) {
+        const unsigned l = __ballot_sync(FULL, lf), mm = __ballot_sync(FULL, mv);
+        if (lane == 0) {
+            s_lm[warp] = l;
+            s_mm[warp] = mm;
+        }
+    }
+    __syncthreads();
+    const uint64_t Lm = s_lm[0] | (s_lm[1] << 32), Mm = s_mm[0] | (s_mm[1] << 32), Rm = Mm & ~Lm;
+    auto bits = [](int lo, int hi) {
+        const uint64_t up = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
+        return up & ~((1ull << lo) - 1ull);
+    };
+    for (int r = tid; r < nruns; r += SPW * 32) {
+        const uint32_t v = s_rv[r];
+        if (!ROOT0 && is_leaf(a.topo, v)) continue;
+        const uint64_t rb = bits(int(s_rs[r]), int(s_rs[r + 1]));
+        const uint32_t nl = __popcll(static_cast<long long>(Lm & rb)), nr = __popcll(static_cast<long long>(Rm & rb));
+        s_bl[r] = s_gs[r] + (nl ? atomicAdd(a.cntL + v, nl) : 0u);
+        s_br[r] = s_ge[r] - 1u - (nr ? atomicAdd(a.cntR + v, nr) : 0u);
+    }
+    __syncthreads();
+    if (tid < cnt) {
+        const int t = tid;
+        const uint32_t d = s_d[t], v = s_v[t];
+        if (!ROOT0 && is_leaf(a.topo, v)) {
+            a.perm_out[c0 + t] = d;
+            if (a.nsort_out) a.nsort_out[c0 + t] = v;
+        } else {
+            int r = 0;  // run of position t (runs are few: linear search from the run starts)
+            while (r + 1 < nruns && int(s_rs[r + 1]) <= t) ++r;
+            const uint64_t before = bits(int(s_rs[r]), t);
+            const uint32_t pos = lf ? s_bl[r] + __popcll(static_cast<long long>(Lm & before))
+                                    : s_br[r] - __popcll(static_cast<long long>(Rm & before));
+            a.perm_out[pos] = d;
+            if (a.nsort_out) a.nsort_out[pos] = 2 * v + (lf ? 1u : 2u);
+        }
+    }
+}
+
 // ---- first position (h = ones): per-draw quadratic forms become tables ----
 // Before the first included factor the history h is all ones (krp_sampler.cpp
 // two-stage loop), so (a) every draw's E-tree mass at node v is the same number
@@ -2017,6 +2316,26 @@ void launch_reg(const EvalArgs& a, cudaStream_t s) {
     launch_pdl(k_eval_reg<NB, MODE, ROOT0>, dim3(grid), dim3(RW * 32), C::SMEM, s, a, uint32_t(range));
 }
 
+inline bool eval_split16_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KRPG_EVAL_SPLIT16");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <int MODE, bool ROOT0>
+void launch_split16(const EvalArgs& a, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_eval_split16<MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(Split16Smem::SMEM));
+        configured = true;
+    }
+    const unsigned grid = unsigned((a.J + SPR - 1) / SPR);
+    launch_pdl(k_eval_split16<MODE, ROOT0>, dim3(grid), dim3(SPW * 32), Split16Smem::SMEM, s, a);
+}
+
 template <int NB>
 void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
     const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
@@ -2025,6 +2344,13 @@ void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant 
             if (mode == EV_PROB) return launch_reg<NB, EV_PROB, false>(a, s);
             if (mode == EV_LEVEL0) return launch_reg<NB, EV_LEVEL, true>(a, s);
             if (mode == EV_LEVEL) return launch_reg<NB, EV_LEVEL, false>(a, s);
+        }
+    }
+    if constexpr (NB == 16) {
+        if (eval_split16_enabled() && !warp_variant) {
+            if (mode == EV_PROB) return launch_split16<EV_PROB, false>(a, s);
+            if (mode == EV_LEVEL0) return launch_split16<EV_LEVEL, true>(a, s);
+            if (mode == EV_LEVEL) return launch_split16<EV_LEVEL, false>(a, s);
         }
     }
     if (mode == EV_ROOT)
