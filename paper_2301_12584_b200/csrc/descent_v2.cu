@@ -677,45 +677,51 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     if (tr && lane == 0) tr[5] = gtimer();
 }
 
-// ---- R = 128: the Gram split over the 4 warps of a CTA (register-resident) ----
-// One register-resident Gram per warp does not fit at R = 128 (272 fragments per
-// lane), so the 4 warps of a CTA share every 8-draw block of the CTA's <= 64
-// positions: warp w holds the upper-triangle tiles of the column blocks
-// {w, 7-w, 8+w, 15-w} (34 tiles, 68 doubles per lane, off-diagonal ones pre-doubled)
-// and computes those columns' share of x_d^T G x_d for all blocks; the four
-// partial masses are summed in warp order after ONE CTA barrier per sweep. The
-// CTA's rows arrive by one 1-D TMA copy per row at the start; decisions, ranks,
-// slot claims and the next level's order follow k_eval_reg.
-constexpr int SPW = 4;        // warps per CTA
-constexpr int SPR = 64;       // max positions per CTA
-constexpr int SPXS = 128 + 4;  // doubles per staged row
-struct Split16Smem {
-    static constexpr size_t ROWS = size_t(SPR) * SPXS * 8;
+// ---- R = 64 / 128: the Gram split over the 4 warps of a CTA (register-resident) ----
+// A CTA's 4 warps share every 8-draw block of the CTA's <= 64 positions: warp w
+// holds the upper-triangle tiles of the column-block pairs {q, NB-1-q} for
+// q = w + 4c (c < NB/8), NB+1 tiles per pair (9 at R = 64, 2 x 17 at R = 128), off-
+// diagonal ones pre-doubled, and computes those columns' share of x_d^T G x_d for
+// all blocks; the four partial masses are summed in warp order after ONE CTA
+// barrier per sweep. Every pair's tiles are listed as entries k = 0..NB of a fixed
+// shape (k <= q: tile (k, q), else tile (k-q-1, NB-1-q)) so the fragment registers
+// are indexed at compile time for any w. The CTA's rows arrive by one 1-D TMA copy
+// per row at the start; decisions, ranks, slot claims and the next level's order
+// follow k_eval_reg. qf_split_order computes the same sum in one warp (first-position
+// tables), so both give bit-identical masses.
+constexpr int SPW = 4;   // warps per CTA
+constexpr int SPR = 64;  // max positions per CTA
+template <int NB>
+struct SplitCfg {
+    static constexpr int R = 8 * NB;
+    static constexpr int PP = NB / 8;       // column-block pairs per warp
+    static constexpr int NE = NB + 1;       // tiles per pair
+    static constexpr int XS = R + 4;        // doubles per staged row
+    static constexpr size_t ROWS = size_t(SPR) * XS * 8;
     static constexpr size_t PART = size_t(2) * SPW * SPR * 8;  // root and node partial masses
     static constexpr size_t DBL = size_t(4) * SPR * 8;         // u, 1/C, low, margin
     static constexpr size_t U32 = size_t(2) * SPR * 4 + size_t(7) * SPR * 4;
     static constexpr size_t SMEM = ROWS + PART + DBL + U32 + SPR * 2 + 64;
 };
 
-// Warp w owns the column-block pairs {w, 15-w} and {7-w, 8+w}: every pair has 17
-// upper-triangle tiles (p <= q), listed as entries k = 0..16 of a fixed shape -
-// k <= a: tile (k, a), else tile (k-a-1, 15-a) - so the fragment registers are
-// indexed at compile time for any w; the entry's column selects its accumulator.
-__device__ __forceinline__ void split16_entry(int a, int k, int& p, int& col) {
-    p = k <= a ? k : k - a - 1;
-    col = k <= a ? a : 15 - a;
+template <int NB>
+__device__ __forceinline__ void split_entry(int q, int k, int& p, int& col) {
+    p = k <= q ? k : k - q - 1;
+    col = k <= q ? q : NB - 1 - q;
 }
 
-__device__ __forceinline__ void split16_load(double (&g)[2][17][2], const double* __restrict__ G, int w, int lane) {
-    constexpr int R = 128;
+template <int NB>
+__device__ __forceinline__ void split_load(double (&g)[NB / 8][NB + 1][2], const double* __restrict__ G, int w,
+                                           int lane) {
+    constexpr int R = 8 * NB;
     const int r4 = lane & 3, cq = lane >> 2;
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        const int a = c == 0 ? w : 7 - w;
+    for (int c = 0; c < NB / 8; ++c) {
+        const int qa = w + 4 * c;
 #pragma unroll
-        for (int k = 0; k < 17; ++k) {
+        for (int k = 0; k <= NB; ++k) {
             int p, q;  // tile (p, q) of column block q
-            split16_entry(a, k, p, q);
+            split_entry<NB>(qa, k, p, q);
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
                 const int row = 8 * p + 4 * s + r4;
@@ -733,27 +739,28 @@ __device__ __forceinline__ void split16_load(double (&g)[2][17][2], const double
     }
 }
 
-// this warp's columns' share of the masses of the block rows xs (row m valid iff valid)
-__device__ __forceinline__ double split16_block(const double (&g)[2][17][2], const double* xs, bool valid, int w,
-                                                int lane) {
+// warp w's columns' share of the masses of the 8 rows xs (row stride xs_stride; row m valid iff valid)
+template <int NB>
+__device__ __forceinline__ double split_block(const double (&g)[NB / 8][NB + 1][2], const double* xs, int xs_stride,
+                                              bool valid, int w, int lane) {
     const int r4 = lane & 3, m = lane >> 2;
-    const double* xr = xs + m * SPXS;
-    double y[2][2][2];  // [pair][first / second column][c0, c1]
+    const double* xr = xs + m * xs_stride;
+    double y[NB / 8][2][2];  // [pair][first / second column][c0, c1]
 #pragma unroll
-    for (int c = 0; c < 2; ++c)
+    for (int c = 0; c < NB / 8; ++c)
 #pragma unroll
         for (int h = 0; h < 2; ++h) y[c][h][0] = y[c][h][1] = 0.0;
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        const int a = c == 0 ? w : 7 - w;
+    for (int c = 0; c < NB / 8; ++c) {
+        const int qa = w + 4 * c;
 #pragma unroll
-        for (int k = 0; k < 17; ++k) {
+        for (int k = 0; k <= NB; ++k) {
             int p, col;
-            split16_entry(a, k, p, col);
+            split_entry<NB>(qa, k, p, col);
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
                 const double av = valid ? xr[8 * p + 4 * s + r4] : 0.0;
-                if (k <= a)
+                if (k <= qa)
                     dmma_884(y[c][0][0], y[c][0][1], av, g[c][k][s]);
                 else
                     dmma_884(y[c][1][0], y[c][1][1], av, g[c][k][s]);
@@ -763,11 +770,11 @@ __device__ __forceinline__ double split16_block(const double (&g)[2][17][2], con
     double part = 0.0;
     if (valid) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int a = c == 0 ? w : 7 - w;
+        for (int c = 0; c < NB / 8; ++c) {
+            const int qa = w + 4 * c;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int q = h == 0 ? a : 15 - a;
+                const int q = h == 0 ? qa : NB - 1 - qa;
                 const double2 xv = *reinterpret_cast<const double2*>(xr + 8 * q + 2 * r4);
                 part = fma(xv.x, y[c][h][0], part);
                 part = fma(xv.y, y[c][h][1], part);
@@ -779,8 +786,26 @@ __device__ __forceinline__ double split16_block(const double (&g)[2][17][2], con
     return part;
 }
 
-template <int MODE, bool ROOT0>
-__global__ void __launch_bounds__(SPW * 32, 2) k_eval_split16(EvalArgs a) {
+// the split-order mass of 8 rows in ONE warp: the four warps' partials in turn,
+// summed in warp order (bit-identical to k_eval_split; row stride xs_stride)
+template <int NB>
+__device__ __forceinline__ double qf_split_order(const double* __restrict__ G, const double* xs, int xs_stride,
+                                                 bool valid, int lane) {
+    double part[SPW];
+#pragma unroll 1
+    for (int w = 0; w < SPW; ++w) {
+        double g[NB / 8][NB + 1][2];
+        split_load<NB>(g, G, w, lane);
+        part[w] = split_block<NB>(g, xs, xs_stride, valid, w, lane);
+    }
+    return ((part[0] + part[1]) + part[2]) + part[3];
+}
+
+template <int NB, int MODE, bool ROOT0>
+__global__ void __launch_bounds__(SPW * 32, NB <= 8 ? 4 : 2) k_eval_split(EvalArgs a) {
+    using SC = SplitCfg<NB>;
+    constexpr int R = 8 * NB;
+    constexpr int SPXS = SC::XS;
     constexpr unsigned FULL = 0xffffffffu;
     constexpr bool LEVEL = MODE == EV_LEVEL;
     extern __shared__ __align__(16) unsigned char sp_smem[];
@@ -827,10 +852,10 @@ __global__ void __launch_bounds__(SPW * 32, 2) k_eval_split16(EvalArgs a) {
     }
     __syncthreads();
     if (warp == 0) {  // rows (one bulk copy each), runs, block list
-        if (lane == 0) mbar_arrive_expect_tx(&s_bar, uint32_t(cnt) * 128 * 8);
+        if (lane == 0) mbar_arrive_expect_tx(&s_bar, uint32_t(cnt) * R * 8);
         __syncwarp();
         for (int t = lane; t < cnt; t += 32)
-            tma_load_1d(rows + t * SPXS, a.X + uint64_t(s_d[t]) * 128, 128 * 8, &s_bar);
+            tma_load_1d(rows + t * SPXS, a.X + uint64_t(s_d[t]) * R, R * 8, &s_bar);
         int nr = 0;
         for (int tb = 0; tb < cnt; tb += 32) {
             const int t = tb + lane;
@@ -876,19 +901,19 @@ __global__ void __launch_bounds__(SPW * 32, 2) k_eval_split16(EvalArgs a) {
     mbar_wait(&s_bar, 0);
     auto sweep = [&](bool node_gram, double* pbuf) {
         double* pw = pbuf + warp * SPR;
-        constexpr uint64_t P = 128ull * 129 / 2;
-        double g[2][17][2];
+        constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
+        double g[NB / 8][NB + 1][2];
         uint32_t gv = 0xFFFFFFFFu;
         for (int i = 0; i < nblk; ++i) {
             const uint32_t e = s_blk[i];
             const int b0 = e & 0xff, n = e >> 8;
             const uint32_t v = s_v[b0];
             if (v != gv) {
-                split16_load(g, node_gram ? a.tree + slot_of(2ull * v + 1) * P : a.tree, warp, lane);
+                split_load<NB>(g, node_gram ? a.tree + slot_of(2ull * v + 1) * P : a.tree, warp, lane);
                 gv = v;
             }
             const int m = lane >> 2;
-            const double pm = split16_block(g, rows + b0 * SPXS, m < n, warp, lane);
+            const double pm = split_block<NB>(g, rows + b0 * SPXS, SPXS, m < n, warp, lane);
             if ((lane & 3) == 0 && m < n) pw[b0 + m] = pm;
         }
     };
@@ -991,7 +1016,7 @@ constexpr int kPos0Levels = 7;  // factor-tree levels served from the table (64 
 template <int NB>
 __global__ void __launch_bounds__(256) k_pos0_tables(const double* __restrict__ Q, Topo te, const double* __restrict__ Zt,
                                                      uint32_t L0, const double* __restrict__ V, double* __restrict__ etab,
-                                                     double* __restrict__ ztab, int* err) {
+                                                     double* __restrict__ ztab, int* err, int split) {
     constexpr int R = 8 * NB;
     constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
     __shared__ __align__(16) double s_vt[R * R + R];  // V^T rows (z of component u) + a ones row
@@ -1017,14 +1042,24 @@ __global__ void __launch_bounds__(256) k_pos0_tables(const double* __restrict__ 
             if (v == te.n) G = Q;  // root
             else if (!is_leaf(te, v)) G = Q + slot_of(2 * v + 1) * P;
             else continue;
-            const double mass = block_qf_packed<NB>(G, fa, s_vt + R * R, lane);
+            double mass;
+            if constexpr (NB == 8) {  // the level kernel's arithmetic: split order when it is the split kernel
+                mass = split ? qf_split_order<NB>(G, s_vt + R * R, 0, true, lane) : block_qf_packed<NB>(G, fa, s_vt + R * R, lane);
+            } else {
+                mass = block_qf_packed<NB>(G, fa, s_vt + R * R, lane);
+            }
             if (lane == 0) etab[v] = mass;
         } else {
             const uint64_t j = it - ne;
             const uint32_t vi = uint32_t(j / NB), ub = uint32_t(j % NB);
             const double* G = vi == nz - 1 ? Zt : Zt + slot_of(2ull * vi + 1) * P;  // last row: root
             const uint32_t u = ub * 8 + m;
-            const double mass = block_qf_packed<NB>(G, fa, s_vt + u * R, lane);
+            double mass;
+            if constexpr (NB == 8) {
+                mass = split ? qf_split_order<NB>(G, s_vt + ub * 8 * R, R, true, lane) : block_qf_packed<NB>(G, fa, s_vt + u * R, lane);
+            } else {
+                mass = block_qf_packed<NB>(G, fa, s_vt + u * R, lane);
+            }
             if ((lane & 3) == 0) {
                 ztab[uint64_t(vi) * R + u] = mass;
                 if (vi == nz - 1 && (!isfinite(mass) || mass <= 0.0)) atomicExch(err, 1);
@@ -2316,41 +2351,43 @@ void launch_reg(const EvalArgs& a, cudaStream_t s) {
     launch_pdl(k_eval_reg<NB, MODE, ROOT0>, dim3(grid), dim3(RW * 32), C::SMEM, s, a, uint32_t(range));
 }
 
-inline bool eval_split16_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("KRPG_EVAL_SPLIT16");
-        return !(e && e[0] == '0');
+// KRPG_EVAL_SPLIT: 0 off, 1 R = 64 and 128, 16 (default) R = 128 only -- at R = 64 the
+// register-resident single-warp kernel measured faster (2.41 vs 2.83 ms per config-2 step)
+inline bool eval_split_enabled(int NB) {
+    static const int v = [] {
+        const char* e = std::getenv("KRPG_EVAL_SPLIT");
+        return e ? std::atoi(e) : 16;
     }();
-    return on;
+    return v == 1 || v == NB;
 }
 
-template <int MODE, bool ROOT0>
-void launch_split16(const EvalArgs& a, cudaStream_t s) {
+template <int NB, int MODE, bool ROOT0>
+void launch_split(const EvalArgs& a, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_eval_split16<MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(Split16Smem::SMEM));
+        cudaFuncSetAttribute(k_eval_split<NB, MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(SplitCfg<NB>::SMEM));
         configured = true;
     }
     const unsigned grid = unsigned((a.J + SPR - 1) / SPR);
-    launch_pdl(k_eval_split16<MODE, ROOT0>, dim3(grid), dim3(SPW * 32), Split16Smem::SMEM, s, a);
+    launch_pdl(k_eval_split<NB, MODE, ROOT0>, dim3(grid), dim3(SPW * 32), SplitCfg<NB>::SMEM, s, a);
 }
 
 template <int NB>
 void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
     const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
+    if constexpr (NB == 8 || NB == 16) {
+        if (eval_split_enabled(NB) && !warp_variant) {
+            if (mode == EV_PROB) return launch_split<NB, EV_PROB, false>(a, s);
+            if (mode == EV_LEVEL0) return launch_split<NB, EV_LEVEL, true>(a, s);
+            if (mode == EV_LEVEL) return launch_split<NB, EV_LEVEL, false>(a, s);
+        }
+    }
     if constexpr (NB <= 8) {
         if (eval_reg_enabled() && !warp_variant) {
             if (mode == EV_PROB) return launch_reg<NB, EV_PROB, false>(a, s);
             if (mode == EV_LEVEL0) return launch_reg<NB, EV_LEVEL, true>(a, s);
             if (mode == EV_LEVEL) return launch_reg<NB, EV_LEVEL, false>(a, s);
-        }
-    }
-    if constexpr (NB == 16) {
-        if (eval_split16_enabled() && !warp_variant) {
-            if (mode == EV_PROB) return launch_split16<EV_PROB, false>(a, s);
-            if (mode == EV_LEVEL0) return launch_split16<EV_LEVEL, true>(a, s);
-            if (mode == EV_LEVEL) return launch_split16<EV_LEVEL, false>(a, s);
         }
     }
     if (mode == EV_ROOT)
@@ -2509,7 +2546,8 @@ inline bool pos0_tables_enabled() {
 template <int NB>
 void launch_pos0_tables(const double* Q, Topo te, const double* Z, uint32_t L0, const double* V, double* etab,
                         double* ztab, int* err, cudaStream_t s) {
-    launch_pdl(k_pos0_tables<NB>, dim3(64), dim3(256), 0, s, Q, te, Z, L0, V, etab, ztab, err);
+    launch_pdl(k_pos0_tables<NB>, dim3(64), dim3(256), 0, s, Q, te, Z, L0, V, etab, ztab, err,
+               int(NB == 8 && eval_split_enabled(NB)));
 }
 
 inline void dispatch_pos0_tables(uint32_t R, const double* Q, Topo te, const double* Z, uint32_t L0, const double* V,

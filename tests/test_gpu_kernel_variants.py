@@ -62,10 +62,17 @@ def run_variant(env_extra, shapes, seed, J):
     ([(5000, 24), (3000, 24)], 4096),                     # non-power-of-two E-tree (parked leaves)
 ])
 def test_level_kernel_and_tables_bit_identical(shapes, J):
-    base = run_variant({"KRPG_EVAL_REG": "0", "KRPG_POS0_TABLES": "0"}, shapes, 11, J)
-    for extra in ({"KRPG_EVAL_REG": "1", "KRPG_POS0_TABLES": "0"},
-                  {"KRPG_EVAL_REG": "0", "KRPG_POS0_TABLES": "1"},
-                  {}):
+    # block_qf_packed order: the CTA kernel, the register-resident kernel, the tables
+    base = run_variant({"KRPG_EVAL_SPLIT": "0", "KRPG_EVAL_REG": "0", "KRPG_POS0_TABLES": "0"}, shapes, 11, J)
+    for extra in ({"KRPG_EVAL_SPLIT": "0", "KRPG_EVAL_REG": "1", "KRPG_POS0_TABLES": "0"},
+                  {"KRPG_EVAL_SPLIT": "0", "KRPG_EVAL_REG": "0", "KRPG_POS0_TABLES": "1"},
+                  {"KRPG_EVAL_SPLIT": "0"}):
         got = run_variant(extra, shapes, 11, J)
         for k, v in base.items():
             assert np.array_equal(got[k], v), f"{extra}: {k} differs"
+    # split order (R = 64: the Gram split over a CTA's warps): the split kernel on every
+    # level vs the first-position tables computed in the same order
+    base = run_variant({"KRPG_EVAL_SPLIT": "1", "KRPG_POS0_TABLES": "0"}, shapes, 11, J)
+    got = run_variant({"KRPG_EVAL_SPLIT": "1"}, shapes, 11, J)
+    for k, v in base.items():
+        assert np.array_equal(got[k], v), f"split order with tables: {k} differs"
