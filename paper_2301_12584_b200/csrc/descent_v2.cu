@@ -69,7 +69,7 @@ struct EvalArgs {
     uint32_t* nsort_out;       // node of each position of perm_out
     uint32_t* GS;           // per node position range [GS, GE) at its level
     uint32_t* GE;
-    int fake;               // timing experiments only (KRPG_FAKE_QF): 1 skip the DMMA, 2 also the loads
+    int fake;               // microbenchmark only (level_bench): 1 skip the DMMA, 2 also the loads; 0 in the library
     unsigned long long* trace;  // timing experiments only: per-warp phase timestamps (nullable)
 };
 
@@ -2585,10 +2585,7 @@ int launch_position_grouped(const GroupedArgs& g) {
     mark(-1);
     EvalArgs e{};
     e.J = J;
-    e.fake = [] {
-        const char* f = std::getenv("KRPG_FAKE_QF");
-        return f ? std::atoi(f) : 0;
-    }();
+    e.fake = 0;  // timing experiments set it only in tools/microbench/level_bench.cu
     e.node = g.node;
     e.rank = g.rank;
     e.low = g.low;
