@@ -159,6 +159,23 @@ def test_draw_offset_sharding_matches_one_call():
     assert np.array_equal(np.concatenate([p.probabilities for p in parts]), full.probabilities)
 
 
+@pytest.mark.parametrize("R", [64, 128])
+def test_draw_sharding_bit_identical_at_large_rank(R):
+    """Draws sharded into draw_offset ranges (one per GPU in the multi-GPU bench) give the
+    same bits as one call -- indices, probabilities, rows and margins -- for the level
+    kernels of R = 64 (register-resident Gram) and R = 128 (Gram split over a CTA), the
+    first-position tables and the persistent deep pass: a draw's arithmetic never depends
+    on which other draws share its warp, CTA or call (krp_sampler.hpp:72-73)."""
+    fs = pareto_factors([(20000, R), (9000, R), (12000, R)], 5)
+    s = K()(fs)
+    J = 9000
+    full = s.sample(1, J, 77, margin=True)
+    cuts = [0, 1234, 5000, J]
+    parts = [s.sample(1, b - a, 77, draw_offset=a, margin=True) for a, b in zip(cuts[:-1], cuts[1:])]
+    for attr in ("indices", "probabilities", "rows", "margin"):
+        assert np.array_equal(np.concatenate([getattr(p, attr) for p in parts]), getattr(full, attr)), attr
+
+
 def test_async_calls_match_synchronous_calls():
     """KRPG_OPT_ASYNC: back-to-back calls without host synchronisation (staging
     buffers reused across in-flight calls) give the same bits as synchronous calls."""
