@@ -1573,13 +1573,27 @@ __global__ void k_make_z(const double* __restrict__ H, const double* __restrict_
                          Topo te, uint32_t R, uint64_t J, double* __restrict__ Z) {
     griddep_launch_dependents();
     griddep_wait();
-    // a warp per draw row (no per-element 64-bit division): coalesced H / Z rows
+    // a warp per draw row (no per-element 64-bit division): coalesced H / Z rows; for
+    // R <= 64 the CTA first transposes V into shared memory (column u contiguous)
+    extern __shared__ double s_vt[];
     const uint32_t lane = threadIdx.x & 31;
+    const bool tr = R <= 64;
+    if (tr) {
+        for (uint32_t i = threadIdx.x; i < R * R; i += blockDim.x) {
+            const uint32_t c = i / R, u = i - c * R;
+            s_vt[u * (R + 1) + c] = V[i];
+        }
+        __syncthreads();
+    }
     const uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     for (uint64_t d = w0; d < J; d += nw) {
         const uint64_t u = leaf_index(te, node[d]);
-        for (uint32_t c = lane; c < R; c += 32) Z[d * R + c] = H[d * R + c] * V[uint64_t(c) * R + u];
+        if (tr) {
+            for (uint32_t c = lane; c < R; c += 32) Z[d * R + c] = H[d * R + c] * s_vt[u * (R + 1) + c];
+        } else {
+            for (uint32_t c = lane; c < R; c += 32) Z[d * R + c] = H[d * R + c] * V[uint64_t(c) * R + u];
+        }
     }
 }
 
@@ -2667,8 +2681,12 @@ int launch_position_grouped(const GroupedArgs& g) {
     } else {
         cta_levels(te.d);
     }
-    launch_pdl(k_make_z, dim3(grid_for(J * R, 256)), dim3(256), 0, g.stream, (const double*)g.H, g.V,
-               (const uint32_t*)g.node, te, R, J, g.Zb);
+    {  // a few CTAs per SM, each transposing V once (R <= 64)
+        const size_t zsm = R <= 64 ? size_t(R) * (R + 1) * sizeof(double) : 0;
+        const unsigned zg = unsigned(std::min<uint64_t>((J + 7) / 8, 148ull * 4));
+        launch_pdl(k_make_z, dim3(zg), dim3(256), zsm, g.stream, (const double*)g.H, g.V, (const uint32_t*)g.node, te, R,
+                   J, g.Zb);
+    }
     ++launches;
     mark(13);
 
