@@ -2261,11 +2261,41 @@ __global__ void k_apply_pick(double* __restrict__ H, const T* __restrict__ U, co
     const uint32_t lane = threadIdx.x & 31;  // a warp per draw row
     const uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    if (R == 64) {  // four rows per step, every load of the four issued before any use
+        uint64_t d = w0;
+        for (; d + 3 * nw < J; d += 4 * nw) {
+            double u[4][2], h[4][2];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t dk = d + k * nw;
+                const uint64_t row = uint64_t(pick[dk]) * 64;
+                u[k][0] = static_cast<double>(U[row + lane]);
+                u[k][1] = static_cast<double>(U[row + 32 + lane]);
+                h[k][0] = H[dk * 64 + lane];
+                h[k][1] = H[dk * 64 + 32 + lane];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t dk = d + k * nw;
+                H[dk * 64 + lane] = h[k][0] * u[k][0];
+                H[dk * 64 + 32 + lane] = h[k][1] * u[k][1];
+            }
+        }
+        for (; d < J; d += nw) {
+            const uint64_t row = uint64_t(pick[d]) * 64;
+            H[d * 64 + lane] *= static_cast<double>(U[row + lane]);
+            H[d * 64 + 32 + lane] *= static_cast<double>(U[row + 32 + lane]);
+        }
+        return;
+    }
     for (uint64_t d = w0; d < J; d += nw) {
         const uint64_t row = uint64_t(pick[d]) * R;
         for (uint32_t c = lane; c < R; c += 32) H[d * R + c] *= static_cast<double>(U[row + c]);
     }
 }
+
+// h-update grid: 8 warps per CTA, ~4 rows per warp
+inline unsigned apply_grid(uint64_t J) { return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((J + 31) / 32, 148ull * 16))); }
 
 unsigned grid_for(uint64_t n, unsigned block) {
     return unsigned(std::min<uint64_t>((n + block - 1) / block, 148ull * 64));
@@ -2745,10 +2775,10 @@ int launch_position_grouped(const GroupedArgs& g) {
             dispatch_deep<double>(R, da, grid, g.stream);
         mark(12);
         if (g.storage == 1)
-            launch_pdl(k_apply_pick<float>, dim3(grid_for(J * R, 256)), dim3(256), 0, g.stream, g.H,
+            launch_pdl(k_apply_pick<float>, dim3(apply_grid(J)), dim3(256), 0, g.stream, g.H,
                        static_cast<const float*>(g.U), (const uint32_t*)g.rank, J, R);
         else
-            launch_pdl(k_apply_pick<double>, dim3(grid_for(J * R, 256)), dim3(256), 0, g.stream, g.H,
+            launch_pdl(k_apply_pick<double>, dim3(apply_grid(J)), dim3(256), 0, g.stream, g.H,
                        static_cast<const double*>(g.U), (const uint32_t*)g.rank, J, R);
         launches += 2;
         mark(13);
