@@ -159,8 +159,8 @@ def test_draw_offset_sharding_matches_one_call():
     assert np.array_equal(np.concatenate([p.probabilities for p in parts]), full.probabilities)
 
 
-@pytest.mark.parametrize("R", [64, 128])
-def test_draw_sharding_bit_identical_at_large_rank(R):
+@pytest.mark.parametrize("R,J", [(64, 9000), (128, 9000), (64, 200000)])
+def test_draw_sharding_bit_identical_at_large_rank(R, J):
     """Draws sharded into draw_offset ranges (one per GPU in the multi-GPU bench) give the
     same bits as one call -- indices, probabilities, rows and margins -- for the level
     kernels of R = 64 (register-resident Gram) and R = 128 (Gram split over a CTA), the
@@ -168,9 +168,8 @@ def test_draw_sharding_bit_identical_at_large_rank(R):
     on which other draws share its warp, CTA or call (krp_sampler.hpp:72-73)."""
     fs = pareto_factors([(20000, R), (9000, R), (12000, R)], 5)
     s = K()(fs)
-    J = 9000
-    full = s.sample(1, J, 77, margin=True)
-    cuts = [0, 1234, 5000, J]
+    full = s.sample(1, J, 77, margin=True)  # J = 200000: several waves of the level kernel
+    cuts = [0, 1234, J // 2, J]
     parts = [s.sample(1, b - a, 77, draw_offset=a, margin=True) for a, b in zip(cuts[:-1], cuts[1:])]
     for attr in ("indices", "probabilities", "rows", "margin"):
         assert np.array_equal(np.concatenate([getattr(p, attr) for p in parts]), getattr(full, attr)), attr
