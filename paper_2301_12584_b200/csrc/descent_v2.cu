@@ -357,7 +357,7 @@ __device__ __forceinline__ void load_gram_frags(double (&gf)[NB * (NB + 1)], con
 // block_qf_packed with the B fragments in registers (off-diagonal ones doubled) and
 // the rows in shared memory (xs = the block's 8 staged rows, row m valid iff valid);
 // same operation order, bit-identical result
-template <int NB>
+template <int NB, bool PRED = true>
 __device__ __forceinline__ double block_qf_regs(const double (&gf)[NB * (NB + 1)], const double* xs, bool valid,
                                                 int lane) {
     constexpr int XS = RegCfg<NB>::XS;
@@ -370,14 +370,14 @@ __device__ __forceinline__ double block_qf_regs(const double (&gf)[NB * (NB + 1)
     for (int p = 0; p < NB; ++p) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-            const double av = valid ? xr[8 * p + 4 * s + r4] : 0.0;
+            const double av = (!PRED || valid) ? xr[8 * p + 4 * s + r4] : 0.0;
             dmma_884(y[p][0], y[p][1], av, gf[rfrag<NB>(p, s, p)]);
 #pragma unroll
             for (int q = p + 1; q < NB; ++q) dmma_884(y[q][0], y[q][1], av, gf[rfrag<NB>(p, s, q)]);
         }
     }
     double part = 0.0;
-    if (valid) {
+    if (!PRED || valid) {
 #pragma unroll
         for (int q = 0; q < NB; ++q) {
             const double2 xv = *reinterpret_cast<const double2*>(xr + 8 * q + 2 * r4);
@@ -558,6 +558,12 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
             if (a.fake < 2) {
                 mbar_wait(&bar[sl], (phase >> sl) & 1u);
                 phase ^= 1u << sl;
+                if (n < 8) {  // partial block: zero the unused rows, so the chain needs no predicates
+                    double* zr = ring + sl * C::SLOT + n * C::XS;
+                    for (int e = lane; e < (8 - n) * C::XS; e += 32) zr[e] = 0.0;
+                    fence_proxy_async();
+                    __syncwarp();
+                }
             }
             if (tr && lane == 0 && i == 0 && !root_pass) tr[6] = gtimer();
             const int m = lane >> 2;
@@ -568,7 +574,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
                 mass = ((hsh >> 13) & 1u) ? 1e300 : 0.0;
                 if (!(LEVEL && !root_pass)) mass = 1.0;
             } else {
-                mass = block_qf_regs<NB>(gf, ring + sl * C::SLOT, valid, lane);
+                mass = block_qf_regs<NB, false>(gf, ring + sl * C::SLOT, valid, lane);
             }
             if (valid && (lane & 3) == 0) out[b0 + m] = mass;
             if (tr && lane == 0 && i == 0 && !root_pass) tr[7] = gtimer();
