@@ -478,6 +478,21 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
             gv_first = v0;
         }
     }
+    // block 0's rows (positions [0, min(8, first run end))) requested right away as well
+    bool pre0 = false;
+    {
+        const uint32_t v0 = __shfl_sync(FULL, vA, 0);
+        if (a.fake < 2 && !parked(v0)) {
+            const uint64_t mk = starts & ~1ull;
+            const int re0 = mk ? __ffsll(static_cast<long long>(mk)) - 1 : cnt;
+            const int n0 = re0 < 8 ? re0 : 8;
+            const uint32_t dr = __shfl_sync(FULL, dA, lane & 7);
+            if (lane == 0) mbar_arrive_expect_tx(&bar[0], uint32_t(n0) * R * 8);
+            __syncwarp();
+            if (lane < n0) tma_load_1d(ring + lane * C::XS, a.X + uint64_t(dr) * R, R * 8, &bar[0]);
+            pre0 = true;
+        }
+    }
     // decision inputs of every position and the parents' ranges of every run: one group
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -543,7 +558,8 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     auto sweep = [&](bool root_pass, uint32_t gv) {
         double* out = root_pass ? s_root : s_mass;
 #pragma unroll
-        for (int i = 0; i < RSLOTS; ++i) issue(i);
+        for (int i = (pre0 ? 1 : 0); i < RSLOTS; ++i) issue(i);
+        pre0 = false;
         for (int i = 0; i < nblk; ++i) {
             const int sl = i % RSLOTS;
             const uint32_t e = s_blk[i];
