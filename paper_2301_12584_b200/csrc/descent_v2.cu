@@ -1569,6 +1569,17 @@ __global__ void k_scatter(const uint32_t* __restrict__ perm_in, uint32_t* __rest
     }
 }
 
+// position ranges of the nodes of level l (first .. first+count) from their parents'
+// (unfused deep path: the per-warp level kernel + k_scatter read gstart of the current
+// level's nodes, while the level kernels record the range of their own runs' nodes)
+__global__ void k_child_ranges(uint32_t* __restrict__ gstart, const uint32_t* __restrict__ cntL, uint64_t first,
+                               uint64_t count) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t c = first + i, pp = (c - 1) / 2;
+        gstart[c] = (c & 1) ? gstart[pp] : gstart[pp] + cntL[pp];
+    }
+}
+
 // stage init: identity order, everyone at the root, this stage's uniform
 __global__ void k_stage_init(uint32_t* perm, uint32_t* node, double* low, double* ud, uint32_t* gstart,
                              uint64_t J, uint64_t seed, uint64_t off, uint64_t counter, double* margin,
@@ -2805,6 +2816,12 @@ int launch_position_grouped(const GroupedArgs& g) {
         launches += 2;
         mark(13);
         return launches;
+    }
+    if (l0 > 0 && l0 < tz.d) {
+        const uint64_t first = (uint64_t(1) << l0) - 1;
+        const uint64_t count = std::min<uint64_t>(uint64_t(1) << l0, tz.n - first);
+        k_child_ranges<<<grid_for(count, 256), 256, 0, g.stream>>>(g.gstart, g.cntL, first, count);
+        ++launches;
     }
     for (uint32_t l = l0; l < tz.d; ++l) {
         e.perm = pin;

@@ -105,6 +105,8 @@ CASES = [
     ([(2000, 72), (1000, 72)], 11),
     ([(3000, 256), (1100, 256)], 12),
     ([(2500, 192), (700, 192)], 13),
+    ([(20000, 128), (3000, 128)], 14),   # R = 128 split-Gram level kernel over 8 levels
+    ([(70000, 64), (9000, 64)], 15),     # R = 64: level kernel + deep pass over 11 levels
 ]
 
 
