@@ -10,9 +10,20 @@ epilogue. Factors and trees are resident in HBM before timing starts.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun, one rank per GPU): the tree structure is replicated and
-each rank draws its own J with draw ids offset by rank*J (weak scaling, no
-collective on the data path); time = max over ranks.
+Multi-GPU (one process per GPU over NCCL; `--gpus N` without torchrun's
+WORLD_SIZE re-executes itself under torch.distributed.run): the tree structure is
+replicated and each rank draws its own J with draw ids offset by rank*J (weak
+scaling, no collective on the data path); time = max over ranks. At N > 1 the
+row-partitioned construction (per-rank subtrees + NCCL all-gather of
+level slices and subtree roots) is timed next to "all-gather U + redundant
+rebuild" and reported under "construction".
+
+Parity of the benchmarked call itself: rank 0 at N = 1 runs the unmodified
+reference (oracle/_ref, the cpu_baseline leg) on the same factors and seeds as
+the last timed step and the three exclude-one calls, and reports the comparison
+under "parity" (indices bit-exact except counted boundary draws, whose margin
+|cutoff - u| <= 1e-10 comes from a deterministic re-run of the same call with
+margins; probabilities / rows relative error).
 """
 from __future__ import annotations
 
@@ -47,6 +58,18 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
     return p.parse_args()
+
+
+REF_FLAGS = ("g++ -std=c++20 -O3 -march=x86-64-v3 -ffp-contract=off -fopenmp (oracle/Makefile; the "
+             "reference's own CMake Release build uses -O3 without -march)")
+
+
+def bench_config(args, world):
+    """The workload dict, identical in both arms (the driver compares them)."""
+    return {"workload": WORKLOAD, "N": args.N, "I": args.I, "R": args.R, "J": args.J, "mode": args.mode,
+            "l2": "flushed (256 MiB write) before every step inside the timed region; resident inputs "
+                  "9.7 GB >> L2",
+            "parallelism": f"draws sharded across {world} GPU(s) (weak), trees replicated"}
 
 
 def load_peaks():
@@ -165,8 +188,9 @@ def descent_bytes(idx, dims, R, excluded=None, elt=8):
 
 
 # ---------------------------------------------------------------- reference arm
-def cpu_reference_run(host_factors, J, seed, steps, warmup):
-    """The reference's own CPU sampler (oracle/_ref: unmodified sources), all host cores."""
+def cpu_reference_run(host_factors, J, seed, steps, warmup, keep=None):
+    """The reference's own CPU sampler (oracle/_ref: unmodified sources), all host cores.
+    Returns (construction s, per-step seconds, reference handle if keep, last outputs)."""
     import oracle
     if not oracle.ref_available():
         raise RuntimeError("oracle/_ref not built")
@@ -176,11 +200,43 @@ def cpu_reference_run(host_factors, J, seed, steps, warmup):
     for i in range(warmup):
         s.sample(None, J, seed + 100 + i)
     times = []
+    out = None
     for i in range(steps):
         t0 = time.perf_counter()
-        s.sample(None, J, seed + i)
+        out = s.sample(None, J, seed + i)
         times.append(time.perf_counter() - t0)
-    return build_s, times
+    return build_s, times, (s if keep else None), out
+
+
+def parity_against_reference(ref, ours, last_seed, J, N):
+    """Compare the timed call (and the exclude-one calls) with the reference's own
+    KrpSampler::sample on the same factors and seeds (krp_sampler.cpp:82-151).
+    `ours[e]` = (idx, prob, rows, margin, seed) host arrays of our call for exclusion e."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from parity_util import BOUNDARY_TOL, compare_draws, rel_err_vec, rows_rel_err
+    tot = {"against": "reference KrpSampler::sample (oracle/_ref), same factors and seeds, every draw",
+           "calls": [], "checked": 0, "mismatches": 0, "boundary_draws": 0, "unexplained": 0,
+           "max_prob_rel_err": 0.0, "max_rows_rel_err": 0.0, "boundary_tol": BOUNDARY_TOL}
+    for e, (gi, gp, gr, gm, sd, first) in ours.items():
+        if first is not None:
+            ri, rp, rr = first
+        else:
+            ri, rp, rr = ref.sample(None if e == "none" else int(e), J, sd)
+        n, nb, nu = compare_draws(gi, gm, ri)
+        same = ~np.any(gi != ri, axis=1)
+        pe = rel_err_vec(gp[same], rp[same])
+        re_ = rows_rel_err(gr[same], rr[same])
+        tot["calls"].append({"excluded": e, "seed": sd, "draws": int(J), "mismatches": n, "boundary": nb,
+                             "unexplained": nu, "prob_rel_err": pe, "rows_rel_err": re_})
+        tot["checked"] += int(J)
+        tot["mismatches"] += n
+        tot["boundary_draws"] += nb
+        tot["unexplained"] += nu
+        tot["max_prob_rel_err"] = max(tot["max_prob_rel_err"], pe)
+        tot["max_rows_rel_err"] = max(tot["max_rows_rel_err"], re_)
+    tot["ok"] = tot["unexplained"] == 0 and tot["max_prob_rel_err"] <= 1e-10
+    return tot
 
 
 def run_reference(args):
@@ -192,20 +248,21 @@ def run_reference(args):
     fs = [f.cpu().numpy() for f in make_factors(args, dev)]
     torch.cuda.empty_cache() if torch.cuda.is_available() else None
     cores = os.cpu_count()
-    build_s, times = cpu_reference_run(fs, args.J, args.seed, args.steps, args.warmup)
+    build_s, times, _, _ = cpu_reference_run(fs, args.J, args.seed, args.steps, args.warmup)
     tot = sum(times)
     value = args.J * len(times) / tot
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     line = {
-        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": WORKLOAD, "N": args.N, "I": args.I, "R": args.R, "J": args.J,
-                   "mode": "two_stage"},
+        "config": bench_config(args, world),
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "reference",
                          "sample": f"full step: KrpSampler::sample(nullopt, J={args.J}) on config 2 "
                                    f"(OMP threads={os.environ.get('OMP_NUM_THREADS', cores)}); "
-                                   f"construction {build_s:.1f} s untimed"},
+                                   f"construction {build_s:.1f} s untimed",
+                         "compile": REF_FLAGS},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "build_s": build_s,
     }
@@ -312,6 +369,22 @@ def run_ours(args):
     # the rest measures the API as a user calls it
     s.profile_enable(False)
 
+    # ---- the timed call's outputs (last step), and a deterministic re-run with margins ----
+    last_seed = args.seed + args.steps - 1
+    ours = {}
+
+    def keep(e, seed_, excluded):
+        mg = torch.empty(J, dtype=torch.float64, device=dev)
+        i2, p2, r2 = torch.empty_like(idx), torch.empty_like(prob), torch.empty_like(rows)
+        s.sample_device(excluded, J, seed_, i2, p2, r2, mg, mode=args.mode, draw_offset=rank * J)
+        s.sync()
+        det = bool(torch.equal(i2, idx) and torch.equal(p2, prob) and torch.equal(r2, rows))
+        ours[e] = (idx.cpu().numpy().view(np.uint32), prob.cpu().numpy(), rows.cpu().numpy(),
+                   mg.cpu().numpy(), seed_, None)
+        return det
+
+    deterministic = keep("none", last_seed, None)
+
     # ---- exclude-one rates (device-timed, not part of the headline) ----
     excl = {}
     for k in range(N):
@@ -322,6 +395,7 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         excl[str(k)] = J / (e0.elapsed_time(e1) / 1e3)
+        deterministic &= keep(str(k), args.seed + 500 + k, k)
 
     # ---- e2e: the public host API (host outputs, copies inside the region) ----
     e2e_t = []
@@ -340,36 +414,47 @@ def run_ours(args):
     h2d = 8 * (P + N * (R * R + R))  # per-call operand upload (G+, eigenvectors, eigenvalues)
     d2h = J * (N * 4 + 8 + R * 8)   # indices, probabilities, rows
 
+    # ---- multi-GPU construction, N > 1 only ----
+    construction = None
+    if world > 1:
+        try:
+            construction = time_construction(s, fs, args, dist, torch, dev)
+        except Exception as ex:  # reported, never hides the headline
+            construction = {"error": f"{type(ex).__name__}: {ex}"}
+
+    # ---- cpu_baseline leg: the reference on the same factors; parity of the timed call ----
     cpu_base = None
+    parity = {"deterministic_rerun": deterministic}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             host = [f.cpu().numpy() for f in fs]
-            build_s, times = cpu_reference_run(host, J, args.seed, steps=1, warmup=0)
+            build_s, times, ref, out = cpu_reference_run(host, J, last_seed, steps=1, warmup=0, keep=True)
             cpu_base = {"value": J / times[0], "unit": "samples/s", "cores": os.cpu_count(),
-                        "kind": "reference",
+                        "kind": "reference", "compile": REF_FLAGS,
                         "sample": f"one KrpSampler::sample(nullopt, J={J}) of the reference on the same "
                                   f"config-2 factors, all host cores (construction {build_s:.1f} s untimed)"}
+            gi, gp, gr, gm, sd, _ = ours["none"]
+            ours["none"] = (gi, gp, gr, gm, sd, out)
+            parity.update(parity_against_reference(ref, ours, last_seed, J, N))
+            del ref
         except Exception as ex:  # reported, never silently substituted
             cpu_base = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "reference",
-                        "sample": f"unavailable: {ex}"}
+                        "sample": f"unavailable: {type(ex).__name__}: {ex}"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "N": N, "I": args.I, "R": R, "J": J, "mode": args.mode,
-                       "l2": "flushed (256 MiB write on the sampler stream) before every step, inside the timed "
-                             "region; resident inputs 9.7 GB >> L2",
-                       "issue": "asynchronous calls (KRPG_OPT_ASYNC): host setup overlaps the previous "
-                                "step's kernels",
-                       "parallelism": f"draws sharded across {world} GPU(s) (weak), trees replicated"},
+            "config": bench_config(args, world),
+            "issue": "asynchronous calls (KRPG_OPT_ASYNC): host setup overlaps the previous step's kernels",
             "roofline": {"bound": "hbm", "kernel": "k_draws (batched root-to-leaf descent)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_kind": peak_kind,
                          "alg_bytes_per_step": bytes_step, "kernel_ms_per_step": draws_ms,
                          "kernel_share_of_step": share},
             "cpu_baseline": cpu_base,
+            "parity": parity,
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
@@ -381,13 +466,77 @@ def run_ours(args):
             "exclude_one_samples_per_s": excl,
             "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items() if v["launches"]},
         }
+        if construction is not None:
+            line["construction"] = construction
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def time_construction(s, fs, args, dist, torch, dev):
+    """N > 1: rebuild factor 0 three ways, device-timed, max over ranks.
+    (a) row-partitioned: each rank builds the subtree of its rows, the level slices
+        and subtree roots are all-gathered over NCCL, the top levels reduced locally;
+    (b) (a) plus the all-gather of the factor's row slices (what a row-partitioned
+        producer, e.g. the STS-CP solve, has to add so every rank can scan leaves);
+    (c) all-gather U's row slices + redundant full rebuild on every rank.
+    (a) is checked bit-identical to the single-GPU build."""
+    from paper_2301_12584_b200.sharding import build_partitioned
+    world, rank = dist.get_world_size(), dist.get_rank()
+    I, R = args.I, args.R
+    U = fs[0]
+    ref_tree = s.tree_device(0).clone()
+    rows = (I + world - 1) // world
+    mine = torch.zeros(rows * args.R, dtype=U.dtype, device=dev)
+    lo, hi = rank * rows, min(I, (rank + 1) * rows)
+    mine[:(hi - lo) * R] = U[lo:hi].reshape(-1)
+    gathered = torch.empty(world * rows * R, dtype=U.dtype, device=dev)
+
+    def timed(fn, reps=3):
+        best = None
+        for _ in range(reps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            best = float(dt.item()) if best is None else min(best, float(dt.item()))
+        return best * 1e3
+
+    def ag_u():
+        dist.all_gather_into_tensor(gathered, mine)
+
+    ms_a = timed(lambda: build_partitioned(s, 0))
+    same = bool(torch.equal(s.tree_device(0), ref_tree))
+    ms_b = timed(lambda: (ag_u(), build_partitioned(s, 0)))
+    ms_c = timed(lambda: (ag_u(), s.rebuild(0)))
+    ms_u = timed(ag_u)
+    return {"factor": 0, "ranks": world, "partitioned_ms": ms_a, "partitioned_plus_allgather_U_ms": ms_b,
+            "allgather_U_plus_rebuild_ms": ms_c, "allgather_U_ms": ms_u,
+            "partitioned_bit_identical_to_single_build": same,
+            "timing": "host wall clock around device-synchronised calls, best of 3, max over ranks"}
+
+
+def respawn_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) without torchrun: re-execute under
+    torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execvpe(sys.executable, cmd, env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        respawn_under_torchrun(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -565,3 +565,78 @@ def test_config2_full_size_draws_match_lazy_reference():
         b = s.sample(e, n, 42, draw_offset=d0, margin=True)
         li, lp, lr, lm = lz.sample(e, np.arange(d0, d0 + n), 42)
         assert_draws_match(b, li, lp, lr, lm)
+
+
+def _stride_check(s, lz, excluded, J, seed, stride, fp32=False):
+    """Run ONE device call of J draws exactly as the bench does (sample_device into
+    resident buffers, margins on), then check every `stride`-th draw against the
+    lazy reference restatement. Returns (checked, mismatches, boundary)."""
+    import torch
+    N, R = s.factor_count(), s.rank()
+    idx = torch.empty(J, N, dtype=torch.int32, device="cuda")
+    prob = torch.empty(J, dtype=torch.float64, device="cuda")
+    rows = torch.empty(J, R, dtype=torch.float64, device="cuda")
+    mg = torch.empty(J, dtype=torch.float64, device="cuda")
+    s.sample_device(excluded, J, seed, idx, prob, rows, mg)
+    s.sync()
+    sel = np.arange(0, J, stride)
+    gi = idx.cpu().numpy().view(np.uint32)[sel]
+    gp, gr, gm = prob.cpu().numpy()[sel], rows.cpu().numpy()[sel], mg.cpu().numpy()[sel]
+    li, lp, lr, lm = lz.sample(excluded, sel, seed)
+    n, nb, nu = compare_draws(gi, gm, li, lm)
+    assert nu == 0, f"excluded={excluded}: {nu} index mismatches outside the boundary margin"
+    same = ~np.any(gi != li, axis=1)
+    assert rel_err_vec(gp[same], lp[same]) <= TOL
+    assert rows_rel_err(gr[same], lr[same]) <= TOL
+    return sel.size, n, nb
+
+
+def test_config2_bench_call_matches_lazy_reference():
+    """The benchmarked call itself (bench.py: config-2 factors from make_factors,
+    sample(nullopt, J = 65536, seed) — first-position tables on levels 0-6, the
+    level kernel on 7-11, the fused deep pass from level 12) and the three
+    exclude-one calls: every 32nd (resp. 128th) draw of the J = 65536 call checked
+    against the lazy restatement of the reference (krp_sampler.cpp:82-151)."""
+    import sys
+
+    import torch
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import make_factors
+    from oracle.lazy import LazyKrp
+
+    class A:
+        N, I, R, seed = 3, 1 << 22, 64, 2301
+
+    fs = make_factors(A(), "cuda")
+    s = K().from_device(fs)
+    host = [f.cpu().numpy() for f in fs]
+    del fs
+    torch.cuda.empty_cache()
+    lz = LazyKrp(host)
+    tot = [0, 0, 0]
+    for e, stride in ((None, 32), (0, 128), (1, 128), (2, 128)):
+        c, n, nb = _stride_check(s, lz, e, 65536, 2310 + (0 if e is None else 1 + e), stride)
+        tot = [tot[0] + c, tot[1] + n, tot[2] + nb]
+    print(f"config-2 bench call: checked {tot[0]} draws, {tot[1]} mismatches, {tot[2]} boundary")
+    s.close()
+
+
+def test_config3_shape_call_matches_lazy_reference():
+    """Config-3 shape: N = 4 factors 1.5e7 x 32, uniform[-1,1], fp32-stored (non-perfect
+    depth-19 tree: 413,212 leaves at depth 19, 55,538 at depth 18), one call of
+    J = 2^20 draws; every 512th draw against the lazy restatement on the exact fp64
+    up-cast of the stored values."""
+    import torch
+    from oracle.lazy import LazyKrp
+
+    N, I, R, J = 4, 15_000_000, 32, 1 << 20
+    g = torch.Generator(device="cuda").manual_seed(3)
+    fs = [torch.rand(I, R, dtype=torch.float32, device="cuda", generator=g) * 2 - 1 for _ in range(N)]
+    s = K().from_device(fs, storage="f32")
+    host = [f.cpu().numpy().astype(np.float64) for f in fs]
+    del fs
+    torch.cuda.empty_cache()
+    lz = LazyKrp(host)
+    c, n, nb = _stride_check(s, lz, None, J, 33, 512)
+    print(f"config-3 shape call: checked {c} draws, {n} mismatches, {nb} boundary")
+    s.close()
