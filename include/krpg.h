@@ -171,6 +171,18 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
  * many slices run on concurrent streams (results are identical for any value; on
  * config 2 one slice measured fastest). */
 #define KRPG_OPT_SLICES 5
+#define KRPG_OPT_HOST_TRACE 6 /* host-side phase times of krpg_sample on stderr */
+/* Kernel-variant / tuning options of the grouped descent (defaults = measured best).
+ * EVAL_REG (1), POS0_TABLES (1), DEEP_THRESHOLD (32), DEEP_CHUNK (8) give bit-identical
+ * samples; EVAL_SPLIT (16: R = 128 only; 1: also R = 64; 0: off), DEEP_DMMA_MIN (1) and
+ * LEAF_PAR (8) change last-bit rounding when moved off their defaults. */
+#define KRPG_OPT_EVAL_REG 16
+#define KRPG_OPT_POS0_TABLES 17
+#define KRPG_OPT_DEEP_THRESHOLD 18
+#define KRPG_OPT_DEEP_CHUNK 19
+#define KRPG_OPT_EVAL_SPLIT 20
+#define KRPG_OPT_DEEP_DMMA_MIN 21
+#define KRPG_OPT_LEAF_PAR 22
 int krpg_set_option(krpg_t h, int option, int64_t value);
 
 /* ---- STS-CP solve slice ----

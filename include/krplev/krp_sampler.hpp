@@ -108,7 +108,10 @@ public:
     std::size_t factor_count() const { return factors_.size(); }
     std::size_t rank() const { return rank_; }
     const Matrix& factor(std::size_t j) const { return factors_.at(j); }
-    const Matrix& factor_gram(std::size_t j) const { return grams_.at(j); }
+    const Matrix& factor_gram(std::size_t j) const {
+        if (gram_dirty_.at(j)) refresh_gram(j);  // single-entry updates since the last read
+        return grams_.at(j);
+    }
 
     SampleBatch sample(std::optional<std::size_t> excluded, std::size_t J, std::uint64_t seed) const {
         return sample(excluded, J, seed, Mode::TwoStage, 0, false);
@@ -172,7 +175,7 @@ public:
                                                v.data(), v.size()));
         for (std::size_t i = 0; i < v.size(); ++i)  // mirror exactly what the device stores
             factors_[j](r[i], c[i]) = fp32_ ? static_cast<double>(static_cast<float>(v[i])) : v[i];
-        refresh_gram(j);
+        gram_dirty_[j] = 1;  // the device queues the entries; G is re-read on the next factor_gram(j)
     }
 
     void validate(double tol = 1e-10) const { detail::krpg_check(krpg_validate(h_.get(), tol)); }
@@ -198,11 +201,14 @@ private:
 
     void refresh_grams() {
         grams_.assign(factors_.size(), Matrix(rank_, rank_));
+        gram_dirty_.assign(factors_.size(), 0);
         for (std::size_t j = 0; j < factors_.size(); ++j) refresh_gram(j);
     }
-    void refresh_gram(std::size_t j) {
+    void refresh_gram(std::size_t j) const {
         if (grams_.size() != factors_.size()) grams_.assign(factors_.size(), Matrix(rank_, rank_));
+        if (gram_dirty_.size() != factors_.size()) gram_dirty_.assign(factors_.size(), 0);
         detail::krpg_check(krpg_factor_gram(h_.get(), static_cast<std::uint32_t>(j), grams_[j].data.data()));
+        gram_dirty_[j] = 0;
     }
     void refresh_factor(std::size_t j) {
         detail::krpg_check(krpg_factor(h_.get(), static_cast<std::uint32_t>(j), factors_[j].data.data()));
@@ -210,7 +216,8 @@ private:
     std::size_t rank_ = 0;
     bool fp32_ = false;
     std::vector<Matrix> factors_;
-    std::vector<Matrix> grams_;
+    mutable std::vector<Matrix> grams_;       // host mirror of the device Grams, refreshed lazily
+    mutable std::vector<char> gram_dirty_;
     std::unique_ptr<krpg_sampler, Closer> h_;
 };
 

@@ -29,6 +29,7 @@
 
 #include "krpg_device.cuh"
 #include "krpg_kernels.hpp"
+#include "launch_util.hpp"
 #include "ptx.cuh"
 #include "qf_dmma.cuh"
 
@@ -69,9 +70,19 @@ struct EvalArgs {
     uint32_t* nsort_out;       // node of each position of perm_out
     uint32_t* GS;           // per node position range [GS, GE) at its level
     uint32_t* GE;
-    int fake;               // microbenchmark only (level_bench): 1 skip the DMMA, 2 also the loads; 0 in the library
+#ifdef KRPG_LEVEL_BENCH
+    int fake;               // microbenchmark only (tools/microbench/level_bench.cu): 1 skip the DMMA, 2 also the loads
+#endif
     unsigned long long* trace;  // timing experiments only: per-warp phase timestamps (nullable)
 };
+
+// timing-experiment switch of the level microbenchmark; always 0 in the library
+#ifdef KRPG_LEVEL_BENCH
+#define EV_FAKE(a) ((a).fake)
+#else
+#define EV_FAKE(a) 0
+#endif
+
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -472,7 +483,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     uint32_t gv_first = 0xFFFFFFFFu;
     {
         const uint32_t v0 = __shfl_sync(FULL, vA, 0);
-        if (a.fake < 2 && !parked(v0)) {
+        if (EV_FAKE(a) < 2 && !parked(v0)) {
             const double* G = (LEVEL && !ROOT0) ? a.tree + slot_of(2ull * v0 + 1) * P : a.tree;
             load_gram_frags<NB>(gf, G, lane);
             gv_first = v0;
@@ -482,7 +493,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     bool pre0 = false;
     {
         const uint32_t v0 = __shfl_sync(FULL, vA, 0);
-        if (a.fake < 2 && !parked(v0)) {
+        if (EV_FAKE(a) < 2 && !parked(v0)) {
             const uint64_t mk = starts & ~1ull;
             const int re0 = mk ? __ffsll(static_cast<long long>(mk)) - 1 : cnt;
             const int n0 = re0 < 8 ? re0 : 8;
@@ -541,7 +552,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
 
     uint32_t phase = 0;  // bit sl: parity of slot sl's next completion
     auto issue = [&](int i) {  // rows of block i -> ring slot i % RSLOTS (1-D TMA, one copy per row)
-        if (i >= nblk || a.fake >= 2) return;
+        if (i >= nblk || EV_FAKE(a) >= 2) return;
         const uint32_t e = s_blk[i];
         const int b0 = e & 0xff, n = e >> 8;
         const int sl = i % RSLOTS;
@@ -565,13 +576,13 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
             const uint32_t e = s_blk[i];
             const int b0 = e & 0xff, n = e >> 8;
             const uint32_t v = pos_v(b0);
-            if (v != gv && a.fake < 2) {
+            if (v != gv && EV_FAKE(a) < 2) {
                 const double* G = a.tree;
                 if (LEVEL && !root_pass) G = a.tree + slot_of(2ull * v + 1) * P;
                 load_gram_frags<NB>(gf, G, lane);
                 gv = v;
             }
-            if (a.fake < 2) {
+            if (EV_FAKE(a) < 2) {
                 mbar_wait(&bar[sl], (phase >> sl) & 1u);
                 phase ^= 1u << sl;
                 if (n < 8) {  // partial block: zero the unused rows, so the chain needs no predicates
@@ -585,7 +596,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
             const int m = lane >> 2;
             const bool valid = m < n;
             double mass;
-            if (a.fake) {  // timing experiment: pseudo-random branch, no quadratic form
+            if (EV_FAKE(a)) {  // timing experiment: pseudo-random branch, no quadratic form
                 const uint32_t hsh = (pos_d(b0 + m < cnt ? b0 + m : b0) * 2654435761u) ^ (v * 40503u);
                 mass = ((hsh >> 13) & 1u) ? 1e300 : 0.0;
                 if (!(LEVEL && !root_pass)) mass = 1.0;
@@ -1843,16 +1854,6 @@ struct DeepArgs {
     uint32_t* work;    // chunk counter (zeroed before the launch) for persistent warps, nullable
 };
 
-// runs with fewer draws than this use the CUDA-core quadratic form (small_qf)
-#ifndef KRPG_DEEP_DMMA_MIN
-#define KRPG_DEEP_DMMA_MIN 1
-#endif
-constexpr int kDeepDmmaMin = KRPG_DEEP_DMMA_MIN;
-// leaf runs with at most this many draws scan a piece warp-parallel (per draw)
-#ifndef KRPG_LEAF_SCAN_PAR
-#define KRPG_LEAF_SCAN_PAR 8
-#endif
-constexpr int kLeafScanPar = KRPG_LEAF_SCAN_PAR;
 
 template <int NB, typename T>
 struct DeepCfg {
@@ -2355,13 +2356,7 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
 template <int NB, int MODE, bool ROOT0>
 void launch_cta(const EvalArgs& a, unsigned grid, cudaStream_t s) {
     constexpr size_t smem = cta_nbuf<NB, ROOT0>() * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
-    if constexpr (smem > 48 * 1024) {
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(k_eval_cta<NB, MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            configured = true;
-        }
-    }
+    smem_optin(k_eval_cta<NB, MODE, ROOT0>, smem);
     // launched with programmatic stream serialization: overlaps the previous
     // kernel's tail (k_eval_cta waits on griddepcontrol before reading its inputs)
     cudaLaunchConfig_t cfg{};
@@ -2380,11 +2375,7 @@ void launch_cta(const EvalArgs& a, unsigned grid, cudaStream_t s) {
 template <int NB, int MODE>
 void launch_stream_mode(const EvalArgs& a, unsigned grid, cudaStream_t s) {
     constexpr size_t smem = size_t(SB_STAGES) * SB_CHD * sizeof(double);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_eval_stream<NB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured = true;
-    }
+    smem_optin(k_eval_stream<NB, MODE>, smem);
     k_eval_stream<NB, MODE><<<grid, CB, smem, s>>>(a);
 }
 
@@ -2400,27 +2391,10 @@ void launch_stream(int mode, const EvalArgs& a, cudaStream_t s) {
         launch_stream_mode<NB, EV_LEVEL>(a, grid, s);
 }
 
-// mode EV_LEVEL with warp_variant selects the per-warp deep-level kernel (R <= 64).
-inline bool eval_reg_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("KRPG_EVAL_REG");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 template <int NB, int MODE, bool ROOT0>
 void launch_reg(const EvalArgs& a, cudaStream_t s) {
     using C = RegCfg<NB>;
-    static int slots = 0;
-    if (!slots) {
-        cudaFuncSetAttribute(k_eval_reg<NB, MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-        int dev = 0, sms = 0, bps = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_eval_reg<NB, MODE, ROOT0>, RW * 32, C::SMEM);
-        slots = std::max(1, sms * std::max(1, bps) * RW);
-    }
+    const int slots = sm_count_current() * occupancy(k_eval_reg<NB, MODE, ROOT0>, RW * 32, C::SMEM) * RW;
     // one wave: the level's positions split evenly over the resident warps
     uint64_t range = (a.J + uint64_t(slots) - 1) / uint64_t(slots);
     range = std::min<uint64_t>(std::max<uint64_t>((range + 7) / 8 * 8, 8), RRANGE);
@@ -2428,40 +2402,29 @@ void launch_reg(const EvalArgs& a, cudaStream_t s) {
     launch_pdl(k_eval_reg<NB, MODE, ROOT0>, dim3(grid), dim3(RW * 32), C::SMEM, s, a, uint32_t(range));
 }
 
-// KRPG_EVAL_SPLIT: 0 off, 1 R = 64 and 128, 16 (default) R = 128 only -- at R = 64 the
+// Tuning::eval_split: 0 off, 1 R = 64 and 128, 16 (default) R = 128 only -- at R = 64 the
 // register-resident single-warp kernel measured faster (2.41 vs 2.83 ms per config-2 step)
-inline bool eval_split_enabled(int NB) {
-    static const int v = [] {
-        const char* e = std::getenv("KRPG_EVAL_SPLIT");
-        return e ? std::atoi(e) : 16;
-    }();
-    return v == 1 || v == NB;
-}
+inline bool eval_split_on(const Tuning& t, int NB) { return t.eval_split == 1 || t.eval_split == NB; }
 
 template <int NB, int MODE, bool ROOT0>
 void launch_split(const EvalArgs& a, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_eval_split<NB, MODE, ROOT0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(SplitCfg<NB>::SMEM));
-        configured = true;
-    }
+    smem_optin(k_eval_split<NB, MODE, ROOT0>, SplitCfg<NB>::SMEM);
     const unsigned grid = unsigned((a.J + SPR - 1) / SPR);
     launch_pdl(k_eval_split<NB, MODE, ROOT0>, dim3(grid), dim3(SPW * 32), SplitCfg<NB>::SMEM, s, a);
 }
 
 template <int NB>
-void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
+void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t, bool warp_variant) {
     const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
     if constexpr (NB == 8 || NB == 16) {
-        if (eval_split_enabled(NB) && !warp_variant) {
+        if (eval_split_on(t, NB) && !warp_variant) {
             if (mode == EV_PROB) return launch_split<NB, EV_PROB, false>(a, s);
             if (mode == EV_LEVEL0) return launch_split<NB, EV_LEVEL, true>(a, s);
             if (mode == EV_LEVEL) return launch_split<NB, EV_LEVEL, false>(a, s);
         }
     }
     if constexpr (NB <= 8) {
-        if (eval_reg_enabled() && !warp_variant) {
+        if (t.eval_reg && !warp_variant) {
             if (mode == EV_PROB) return launch_reg<NB, EV_PROB, false>(a, s);
             if (mode == EV_LEVEL0) return launch_reg<NB, EV_LEVEL, true>(a, s);
             if (mode == EV_LEVEL) return launch_reg<NB, EV_LEVEL, false>(a, s);
@@ -2480,76 +2443,49 @@ void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant 
         launch_cta<NB, EV_LEVEL, false>(a, grid, s);
 }
 
-void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, bool warp_variant = false) {
+void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t,
+                   bool warp_variant = false) {
     switch (R / 8) {
-        case 1: return launch_eval<1>(mode, a, s, warp_variant);
-        case 2: return launch_eval<2>(mode, a, s, warp_variant);
-        case 3: return launch_eval<3>(mode, a, s, warp_variant);
-        case 4: return launch_eval<4>(mode, a, s, warp_variant);
-        case 5: return launch_eval<5>(mode, a, s, warp_variant);
-        case 6: return launch_eval<6>(mode, a, s, warp_variant);
-        case 7: return launch_eval<7>(mode, a, s, warp_variant);
-        case 8: return launch_eval<8>(mode, a, s, warp_variant);
-        case 9: return launch_eval<9>(mode, a, s);
-        case 10: return launch_eval<10>(mode, a, s);
-        case 11: return launch_eval<11>(mode, a, s);
-        case 12: return launch_eval<12>(mode, a, s);
-        case 13: return launch_eval<13>(mode, a, s);
-        case 14: return launch_eval<14>(mode, a, s);
-        case 15: return launch_eval<15>(mode, a, s);
-        case 16: return launch_eval<16>(mode, a, s);
-        case 17: return launch_eval<17>(mode, a, s);
-        case 18: return launch_eval<18>(mode, a, s);
-        case 19: return launch_eval<19>(mode, a, s);
-        case 20: return launch_eval<20>(mode, a, s);
+        case 1: return launch_eval<1>(mode, a, s, t, warp_variant);
+        case 2: return launch_eval<2>(mode, a, s, t, warp_variant);
+        case 3: return launch_eval<3>(mode, a, s, t, warp_variant);
+        case 4: return launch_eval<4>(mode, a, s, t, warp_variant);
+        case 5: return launch_eval<5>(mode, a, s, t, warp_variant);
+        case 6: return launch_eval<6>(mode, a, s, t, warp_variant);
+        case 7: return launch_eval<7>(mode, a, s, t, warp_variant);
+        case 8: return launch_eval<8>(mode, a, s, t, warp_variant);
+        case 9: return launch_eval<9>(mode, a, s, t, false);
+        case 10: return launch_eval<10>(mode, a, s, t, false);
+        case 11: return launch_eval<11>(mode, a, s, t, false);
+        case 12: return launch_eval<12>(mode, a, s, t, false);
+        case 13: return launch_eval<13>(mode, a, s, t, false);
+        case 14: return launch_eval<14>(mode, a, s, t, false);
+        case 15: return launch_eval<15>(mode, a, s, t, false);
+        case 16: return launch_eval<16>(mode, a, s, t, false);
+        case 17: return launch_eval<17>(mode, a, s, t, false);
+        case 18: return launch_eval<18>(mode, a, s, t, false);
+        case 19: return launch_eval<19>(mode, a, s, t, false);
+        case 20: return launch_eval<20>(mode, a, s, t, false);
         case 24: return launch_stream<24>(mode, a, s);
         case 28: return launch_stream<28>(mode, a, s);
         default: return launch_stream<32>(mode, a, s);
     }
 }
 
-// draws per warp in the fused deep kernel: fewer than 32 gives more, shorter warp
-// work units (the kernel holds ~12 warps per SM, so 32-draw units leave a ragged tail wave)
-inline uint32_t deep_chunk() {
-    static const uint32_t c = [] {
-        const char* e = std::getenv("KRPG_DEEP_CHUNK");
-        const int v = e ? std::atoi(e) : 8;
-        return uint32_t(v >= 1 && v <= 32 ? v : 8);
-    }();
-    return c;
-}
+// draws per warp in the fused deep kernel (Tuning::deep_chunk): fewer than 32 gives more,
+// shorter warp work units (the kernel holds ~12 warps per SM, so 32-draw units leave a
+// ragged tail wave)
+inline uint32_t deep_chunk(const Tuning& t) { return uint32_t(t.deep_chunk >= 1 && t.deep_chunk <= 32 ? t.deep_chunk : 8); }
 
-// shallow levels (many draws per node) -> cooperative CTA kernel; deep -> per-warp
-inline uint64_t deep_threshold() {
-    static const uint64_t t = [] {
-        const char* e = std::getenv("KRPG_DEEP_THRESHOLD");
-        const long v = e ? std::atol(e) : 32;
-        return uint64_t(v >= 1 ? v : 32);
-    }();
-    return t;
-}
-inline bool deep_level(uint64_t J, uint32_t level) { return (J >> level) < deep_threshold(); }
-
-inline bool deep_persistent() {
-    static const bool on = [] {
-        const char* e = std::getenv("KRPG_DEEP_PERSISTENT");
-        return !(e && e[0] == '0');
-    }();
-    return on;
+// shallow levels (many draws per node) -> level kernels with global regrouping; deep -> fused pass
+inline bool deep_level(const Tuning& t, uint64_t J, uint32_t level) {
+    return (J >> level) < uint64_t(t.deep_threshold >= 1 ? t.deep_threshold : 32);
 }
 
 template <int NB, typename T>
 void launch_deep2(const DeepArgs& a, unsigned grid, cudaStream_t s) {
     using C = DeepCfg<NB, T>;
-    static int resident = 0;
-    if (!resident) {
-        cudaFuncSetAttribute(k_deep2<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        int dev = 0, sms = 0, bps = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_deep2<NB, T>, WPB * 32, C::SMEM);
-        resident = std::max(1, sms * std::max(1, bps));
-    }
+    const int resident = sm_count_current() * occupancy(k_deep2<NB, T>, WPB * 32, C::SMEM);
     if (a.work) grid = std::min<unsigned>(grid, unsigned(resident));  // persistent: one wave
     launch_pdl(k_deep2<NB, T>, dim3(grid), dim3(WPB * 32), C::SMEM, s, a);
 }
@@ -2571,11 +2507,7 @@ void dispatch_deep(uint32_t R, const DeepArgs& a, unsigned grid, cudaStream_t s)
 template <int NB, typename T>
 void launch_leaf2(const LeafArgs& a, cudaStream_t s) {
     using C = LeafCfg2<NB, T>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_leaf2<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        configured = true;
-    }
+    smem_optin(k_leaf2<NB, T>, C::SMEM);
     const unsigned grid = unsigned((a.J + uint64_t(CHUNK) * WPB - 1) / (uint64_t(CHUNK) * WPB));
     k_leaf2<NB, T><<<grid, WPB * 32, C::SMEM, s>>>(a);
 }
@@ -2612,32 +2544,25 @@ void dispatch_leaf(uint32_t R, const LeafArgs& a, cudaStream_t s) {
 }  // namespace v2
 
 namespace v2 {
-inline bool pos0_tables_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("KRPG_POS0_TABLES");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 template <int NB>
 void launch_pos0_tables(const double* Q, Topo te, const double* Z, uint32_t L0, const double* V, double* etab,
-                        double* ztab, int* err, cudaStream_t s) {
+                        double* ztab, int* err, cudaStream_t s, int split_order) {
     launch_pdl(k_pos0_tables<NB>, dim3(64), dim3(256), 0, s, Q, te, Z, L0, V, etab, ztab, err,
-               int(NB == 8 && eval_split_enabled(NB)));
+               int(NB == 8 && split_order));
 }
 
 inline void dispatch_pos0_tables(uint32_t R, const double* Q, Topo te, const double* Z, uint32_t L0, const double* V,
-                                 double* etab, double* ztab, int* err, cudaStream_t s) {
+                                 double* etab, double* ztab, int* err, cudaStream_t s, const Tuning& t) {
+    const int so = eval_split_on(t, 8) ? 1 : 0;
     switch (R / 8) {
-        case 1: return launch_pos0_tables<1>(Q, te, Z, L0, V, etab, ztab, err, s);
-        case 2: return launch_pos0_tables<2>(Q, te, Z, L0, V, etab, ztab, err, s);
-        case 3: return launch_pos0_tables<3>(Q, te, Z, L0, V, etab, ztab, err, s);
-        case 4: return launch_pos0_tables<4>(Q, te, Z, L0, V, etab, ztab, err, s);
-        case 5: return launch_pos0_tables<5>(Q, te, Z, L0, V, etab, ztab, err, s);
-        case 6: return launch_pos0_tables<6>(Q, te, Z, L0, V, etab, ztab, err, s);
-        case 7: return launch_pos0_tables<7>(Q, te, Z, L0, V, etab, ztab, err, s);
-        default: return launch_pos0_tables<8>(Q, te, Z, L0, V, etab, ztab, err, s);
+        case 1: return launch_pos0_tables<1>(Q, te, Z, L0, V, etab, ztab, err, s, so);
+        case 2: return launch_pos0_tables<2>(Q, te, Z, L0, V, etab, ztab, err, s, so);
+        case 3: return launch_pos0_tables<3>(Q, te, Z, L0, V, etab, ztab, err, s, so);
+        case 4: return launch_pos0_tables<4>(Q, te, Z, L0, V, etab, ztab, err, s, so);
+        case 5: return launch_pos0_tables<5>(Q, te, Z, L0, V, etab, ztab, err, s, so);
+        case 6: return launch_pos0_tables<6>(Q, te, Z, L0, V, etab, ztab, err, s, so);
+        case 7: return launch_pos0_tables<7>(Q, te, Z, L0, V, etab, ztab, err, s, so);
+        default: return launch_pos0_tables<8>(Q, te, Z, L0, V, etab, ztab, err, s, so);
     }
 }
 }  // namespace v2
@@ -2662,7 +2587,6 @@ int launch_position_grouped(const GroupedArgs& g) {
     mark(-1);
     EvalArgs e{};
     e.J = J;
-    e.fake = 0;  // timing experiments set it only in tools/microbench/level_bench.cu
     e.node = g.node;
     e.rank = g.rank;
     e.low = g.low;
@@ -2693,14 +2617,14 @@ int launch_position_grouped(const GroupedArgs& g) {
         pout = g.perm_b;
         if (lcta == 0) {
             e.perm = nullptr;
-            dispatch_eval(R, EV_ROOT, e, g.stream);
+            dispatch_eval(R, EV_ROOT, e, g.stream, g.tune);
             ++launches;
             mark(8);
             return;
         }
         if (R > 160) {  // streamed kernel: separate normaliser pass
             e.perm = nullptr;
-            dispatch_eval(R, EV_ROOT, e, g.stream);
+            dispatch_eval(R, EV_ROOT, e, g.stream, g.tune);
             ++launches;
             mark(8);
         }
@@ -2711,7 +2635,7 @@ int launch_position_grouped(const GroupedArgs& g) {
             e.perm_out = pout;
             e.nsort_in = (l == 0 || !nin) ? nullptr : nin;
             e.nsort_out = nout;
-            dispatch_eval(R, (l == 0 && R <= 160) ? EV_LEVEL0 : EV_LEVEL, e, g.stream, false);
+            dispatch_eval(R, (l == 0 && R <= 160) ? EV_LEVEL0 : EV_LEVEL, e, g.stream, g.tune, false);
             ++launches;
             mark(9);
             std::swap(pin, pout);
@@ -2723,20 +2647,20 @@ int launch_position_grouped(const GroupedArgs& g) {
     const Topo tz = make_topo(g.I, R);
     // shallow levels: global regrouping; deep levels + leaf scan: one fused pass
     uint32_t l0 = 0;
-    while (l0 < tz.d && (R > 64 || !deep_level(J, l0))) ++l0;
+    while (l0 < tz.d && (R > 64 || !deep_level(g.tune, J, l0))) ++l0;
     // first position: E-tree and the top factor-tree levels from (node, component) tables
     const uint32_t L0 = tz.d >= 2 ? std::min<uint32_t>(kPos0Levels, std::min<uint32_t>(l0, tz.d - 1)) : 0;
-    const bool tab0 = g.h_ones && g.pos0_tab && R <= 64 && R % 8 == 0 && L0 >= 1 && pos0_tables_enabled();
+    const bool tab0 = g.h_ones && g.pos0_tab && R <= 64 && R % 8 == 0 && L0 >= 1 && g.tune.pos0_tables;
     double* etab = g.pos0_tab;
     double* ztab = etab ? etab + 2 * R + 8 : nullptr;
     uint32_t* hist = etab ? reinterpret_cast<uint32_t*>(ztab + (uint64_t(1) << kPos0Levels) * R) : nullptr;
     // chunk counter of the persistent deep pass (zeroed by the factor-tree stage init)
-    uint32_t* deep_work = (hist && g.fused_deep && R <= 64 && deep_persistent()) ? hist + 300 : nullptr;
+    uint32_t* deep_work = (hist && g.fused_deep && R <= 64) ? hist + 300 : nullptr;
     e.X = g.H;
     e.tree = g.Q;
     e.topo = te;
     if (tab0) {
-        dispatch_pos0_tables(R, g.Q, te, g.Z, L0, g.V, etab, ztab, g.err, g.stream);
+        dispatch_pos0_tables(R, g.Q, te, g.Z, L0, g.V, etab, ztab, g.err, g.stream, g.tune);
         launch_pdl(k_pos0_ewalk, dim3(grid_for(J, 256)), dim3(256), 0, g.stream, (const double*)etab, te, J,
                    (const double*)g.ud, g.margin, g.node, g.rank, hist, uint32_t(2u << L0), g.err);
         launches += 2;
@@ -2791,16 +2715,10 @@ int launch_position_grouped(const GroupedArgs& g) {
         da.U = g.U;
         da.tree = g.Z;
         da.topo = tz;
-        da.chunk = deep_chunk();
+        da.chunk = deep_chunk(g.tune);
         da.work = deep_work;
-        da.dmma_min = [] {
-            const char* e = std::getenv("KRPG_DEEP_DMMA_MIN");
-            return e ? std::atoi(e) : kDeepDmmaMin;
-        }();
-        da.leaf_par = [] {
-            const char* e = std::getenv("KRPG_LEAF_PAR");
-            return e ? std::atoi(e) : kLeafScanPar;
-        }();
+        da.dmma_min = g.tune.deep_dmma_min;
+        da.leaf_par = g.tune.leaf_par;
         const unsigned grid = unsigned((J + uint64_t(da.chunk) * WPB - 1) / (uint64_t(da.chunk) * WPB));
         if (g.storage == 1)
             dispatch_deep<float>(R, da, grid, g.stream);
@@ -2825,7 +2743,7 @@ int launch_position_grouped(const GroupedArgs& g) {
     }
     for (uint32_t l = l0; l < tz.d; ++l) {
         e.perm = pin;
-        dispatch_eval(R, EV_LEVEL, e, g.stream, true);
+        dispatch_eval(R, EV_LEVEL, e, g.stream, g.tune, true);
         mark(10);
         k_scatter<<<gs, 256, 0, g.stream>>>(pin, pout, g.node, g.rank, g.gstart, g.cntL, J, (2u << l) - 1);
         mark(11);
@@ -2865,7 +2783,7 @@ void launch_probabilities_grouped(const double* H, const double* gp_packed, uint
     e.tree = gp_packed;
     e.prob = prob;
     e.rank_div = rank;
-    dispatch_eval(R, EV_PROB, e, s);
+    dispatch_eval(R, EV_PROB, e, s, Tuning{});
 }
 
 }  // namespace krpg

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <future>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -170,6 +171,38 @@ struct krpg_sampler {
     bool prof_detail = false;  // per-kernel-type timing marks inside the descent
     bool fused_deep = true;    // deep levels + leaf scan fused (descent_v2.cu k_deep)
     uint32_t nslices = 1;      // KRPG_OPT_SLICES: concurrent draw slices of the grouped descent
+    bool host_trace = false;   // KRPG_OPT_HOST_TRACE: host-side phase times on stderr
+    krpg::Tuning tune;         // kernel-variant / tuning options (KRPG_OPT_EVAL_REG ...)
+    // single-entry updates queued by krpg_update_entries (update_factor_entry), per factor,
+    // in call order; flushed as one deterministic device patch per factor
+    struct PendingEntry {
+        uint64_t r;
+        uint32_t c;
+        double v;
+    };
+    std::vector<std::vector<PendingEntry>> pending;
+    // per-call R x R setup (G+, rank, G_{>k} and its eigenpairs) keyed by (excluded, mode),
+    // valid while the included factors' Grams are unchanged (compared bitwise)
+    struct SetupEntry {
+        bool valid = false;
+        std::vector<std::vector<double>> grams;
+        krpg::Eig ge;
+        size_t rank = 0;
+        std::vector<double> gp;
+        std::vector<std::vector<double>> Y;
+        std::vector<krpg::Eig> ye;
+    };
+    std::map<std::pair<int64_t, uint32_t>, SetupEntry> setup_cache;
+    DevBuf patchbuf;
+    void flush_updates() {
+        for (uint32_t j = 0; j < pending.size(); ++j)
+            if (!pending[j].empty()) {
+                std::vector<PendingEntry> e;
+                e.swap(pending[j]);
+                apply_entries(j, e);
+            }
+    }
+    void apply_entries(uint32_t j, const std::vector<PendingEntry>& E);
     std::vector<cudaStream_t> sstreams;
     std::vector<cudaEvent_t> sevents;  // [0] fork, [s] join of slice s
     cudaStream_t slice_stream(int sl) {
@@ -398,26 +431,41 @@ struct krpg_sampler {
         const size_t RR = size_t(R) * R;
 
         // ---- R x R setup (krp_sampler.cpp:89-96, 115-122) ----
-        const std::vector<double> G = hadamard_of(inc);
-        const krpg::Eig ge = krpg::eigh_psd(G.data(), R);
-        const size_t rank = krpg::numerical_rank(ge);
-        if (rank == 0) throw std::runtime_error("KRPSample: Khatri-Rao product of included factors is zero");
-        const std::vector<double> gp = krpg::pinv_from_eigen(ge);
-
+        // A pure function of the included factors' Grams: cached per (excluded, mode)
+        // and reused while those Grams are bitwise unchanged (repeated calls, the
+        // per-mode loop of an ALS sweep), so only the first call pays the eigensolves.
         const size_t npos = inc.size();
-        std::vector<std::vector<double>> Y(npos);
-        for (size_t p = 0; p < npos; ++p) {  // downstream_gram :74-80
-            Y[p].assign(RR, 1.0);
-            krpg::hadamard_into(Y[p], gp.data());
-            for (size_t q = p + 1; q < npos; ++q) krpg::hadamard_into(Y[p], f[inc[q]].G.data());
+        SetupEntry& se = setup_cache[{excluded, mode}];
+        bool hit = se.valid && se.grams.size() == npos;
+        for (size_t p = 0; hit && p < npos; ++p) hit = se.grams[p] == f[inc[p]].G;
+        std::vector<std::future<krpg::Eig>> fut(npos);
+        if (!hit) {
+            se.valid = false;
+            se.grams.clear();
+            for (uint32_t k : inc) se.grams.push_back(f[k].G);
+            const std::vector<double> G = hadamard_of(inc);
+            se.ge = krpg::eigh_psd(G.data(), R);
+            se.rank = krpg::numerical_rank(se.ge);
+            if (se.rank == 0) throw std::runtime_error("KRPSample: Khatri-Rao product of included factors is zero");
+            se.gp = krpg::pinv_from_eigen(se.ge);
+            se.Y.assign(npos, {});
+            for (size_t p = 0; p < npos; ++p) {  // downstream_gram :74-80
+                se.Y[p].assign(RR, 1.0);
+                krpg::hadamard_into(se.Y[p], se.gp.data());
+                for (size_t q = p + 1; q < npos; ++q) krpg::hadamard_into(se.Y[p], f[inc[q]].G.data());
+            }
+            se.ye.assign(npos, {});
         }
+        const krpg::Eig& ge = se.ge;
+        const size_t rank = se.rank;
+        const std::vector<double>& gp = se.gp;
+        const std::vector<std::vector<double>>& Y = se.Y;
+        std::vector<krpg::Eig>& ye = se.ye;
         // Eigendecompositions of G_{>k} (two-stage): position 0 on this thread,
         // the others concurrently; each position's operands are uploaded just
         // before its kernels, so the device starts on position 0 while later
         // eigensolves are still running on the host.
-        std::vector<krpg::Eig> ye(npos);
-        std::vector<std::future<krpg::Eig>> fut(npos);
-        if (mode == KRPG_MODE_TWO_STAGE) {
+        if (mode == KRPG_MODE_TWO_STAGE && !hit) {
             // the last position's Y is G+ itself (no later factor): its eigenpairs are
             // those of G, inverted and reordered, no eigensolve needed
             const size_t last = npos - 1;
@@ -439,7 +487,7 @@ struct krpg_sampler {
         auto stage_pos = [&](size_t p) {  // fill + upload position p's operands
             double* dst = up_h + P + p * per_pos;
             if (mode == KRPG_MODE_TWO_STAGE) {
-                if (p > 0) ye[p] = fut[p].get();
+                if (p > 0 && fut[p].valid()) ye[p] = fut[p].get();
                 std::memcpy(dst, ye[p].vectors.data(), sizeof(double) * RR);
                 std::memcpy(dst + RR, ye[p].values.data(), sizeof(double) * R);
             } else {
@@ -455,7 +503,7 @@ struct krpg_sampler {
             CK(cudaMemcpyAsync(dsmall, up_h, sizeof(double) * P, cudaMemcpyHostToDevice, stream));
         }
         stage_pos(0);
-        if (std::getenv("KRPG_HOST_TRACE"))
+        if (host_trace)
             std::fprintf(stderr, "krpg_sample host: position-0 operands staged after %.3f ms\n",
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - trace_t0).count());
         struct JoinAll {  // never leave eigensolver threads behind on an exception
@@ -521,6 +569,7 @@ struct krpg_sampler {
             g.err = derr;
             g.stream = stream;
             g.fused_deep = fused_deep ? 1 : 0;
+            g.tune = tune;
             if (prof_on && prof_detail) {
                 g.mark = &krpg_sampler::mark_cb;
                 g.mark_ctx = this;
@@ -579,6 +628,7 @@ struct krpg_sampler {
                 pend(KRPG_PROF_DRAWS, t0, nl);
             }
             CK(cudaEventRecord(up_ev[slot], stream));
+            se.valid = true;  // every position's operands are complete
             if (d_prob) {
                 cudaEvent_t t0 = pbegin();
                 krpg::launch_probabilities_grouped(H, dsmall, R, J, double(rank), d_prob, stream);
@@ -624,6 +674,7 @@ struct krpg_sampler {
             pend(KRPG_PROF_DRAWS, t0, 1);
         }
         CK(cudaEventRecord(up_ev[slot], stream));
+        se.valid = true;
         if (d_prob) {
             cudaEvent_t t0 = pbegin();
             krpg::launch_probabilities(H, dsmall, R, J, double(rank), d_prob, stream);
@@ -704,15 +755,112 @@ void krpg_sampler::sts_solve(krpg_tensor& T, uint32_t j, uint64_t J, uint64_t se
     const std::vector<double> ph = krpg::pinv_from_eigen(krpg::eigh_psd(gh.data(), R));
     CK(cudaMemcpyAsync(pinv, ph.data(), 8 * ph.size(), cudaMemcpyHostToDevice, stream));
     // 5) unew = transpose(matmul(pinv, gram_cross)) (:295), normalize_columns (:309)
-    // stored straight into U_j (sampler->update_factor(j, unew), :312-313), rebuild
+    // stored into U_j (sampler->update_factor(j, unew), :312-313) only once the column
+    // norms are finite (update_factor validates before it mutates), then rebuild
     Factor& Fj = f[j];
     t_sts = pbegin();
-    krpg::launch_solve_normalize(M, Ij, R, pinv, Unew, nrm, Fj.U.p, storage, stream);
-    pend(KRPG_PROF_STS, t_sts, 4);
+    krpg::launch_solve_normalize(M, Ij, R, pinv, Unew, nrm, nullptr, storage, stream);
     std::vector<double> sg(R);
     CK(cudaMemcpyAsync(sg.data(), nrm, 8 * R, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    for (double x : sg) require(std::isfinite(x), "update_factor: invalid factor");
+    krpg::launch_normalize_store(Unew, Ij, R, nrm, Fj.U.p, storage, stream);
+    pend(KRPG_PROF_STS, t_sts, 4);
     build_tree(j);
     if (sigma_out) std::copy(sg.begin(), sg.end(), sigma_out);
+}
+
+// A sequence of update_factor_entry calls on factor j (krp_sampler.cpp:207-228 ->
+// segment_tree_sampler.cpp:358-409), applied at once: the touched rows are read back,
+// the entries applied to them on the host in call order (the sequential semantics),
+// and every node on a touched row's path patched by the net u'u'^T - u u^T of its rows,
+// reduced bottom-up in a fixed order (update.cu k_patch_level, no atomics).
+void krpg_sampler::apply_entries(uint32_t j, const std::vector<PendingEntry>& E) {
+    Factor& F = f[j];
+    std::vector<uint64_t> rows;
+    rows.reserve(E.size());
+    for (const auto& e : E) rows.push_back(e.r);
+    std::sort(rows.begin(), rows.end());
+    rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
+    const uint64_t nr = rows.size();
+    // tree items, deepest level first
+    const krpg::Topo t = krpg::make_topo(F.I, R);
+    std::vector<std::vector<krpg::PatchItem>> lv(t.d + 1);
+    for (uint64_t i = 0; i < nr;) {
+        const uint64_t leaf = rows[i] / R;
+        uint64_t e = i;
+        while (e < nr && rows[e] / R == leaf) ++e;
+        const uint64_t node = krpg::leaf_node(t, leaf);
+        lv[krpg::depth_of(node)].push_back({node, -1, -1, uint32_t(i), uint32_t(e)});
+        i = e;
+    }
+    for (uint32_t dd = t.d; dd >= 1; --dd) {
+        auto& cur = lv[dd];
+        std::sort(cur.begin(), cur.end(), [](const krpg::PatchItem& a, const krpg::PatchItem& b) { return a.node < b.node; });
+        std::vector<krpg::PatchItem> par;
+        for (uint64_t i = 0; i < cur.size(); ++i) {
+            const uint64_t p = (cur[i].node - 1) / 2;
+            if (par.empty() || par.back().node != p) par.push_back({p, -1, -1, 0, 0});
+            if (cur[i].node & 1) par.back().lc = int64_t(i);
+            else par.back().rc = int64_t(i);
+        }
+        auto& up = lv[dd - 1];  // may already hold leaves of a ragged tree (distinct nodes)
+        up.insert(up.end(), par.begin(), par.end());
+    }
+    std::sort(lv[0].begin(), lv[0].end(), [](const krpg::PatchItem& a, const krpg::PatchItem& b) { return a.node < b.node; });
+    uint64_t nitems = 0, maxl = 0;
+    for (auto& l : lv) {
+        nitems += l.size();
+        maxl = std::max<uint64_t>(maxl, l.size());
+    }
+    // device scratch: rows, old, new, items, two delta buffers
+    const size_t rb = 8 * nr * R;
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t o_old = al(8 * nr), o_new = o_old + al(rb), o_it = o_new + al(rb),
+                 o_d0 = o_it + al(sizeof(krpg::PatchItem) * nitems), o_d1 = o_d0 + al(8 * maxl * P),
+                 total = o_d1 + al(8 * maxl * P);
+    char* d = static_cast<char*>(patchbuf.ensure(total));
+    uint64_t* drows = reinterpret_cast<uint64_t*>(d);
+    double* dold = reinterpret_cast<double*>(d + o_old);
+    double* dnew = reinterpret_cast<double*>(d + o_new);
+    krpg::PatchItem* dit = reinterpret_cast<krpg::PatchItem*>(d + o_it);
+    double* dl[2] = {reinterpret_cast<double*>(d + o_d0), reinterpret_cast<double*>(d + o_d1)};
+    CK(cudaMemcpyAsync(drows, rows.data(), 8 * nr, cudaMemcpyHostToDevice, stream));
+    krpg::launch_gather_rows(F.U.p, storage, R, nr, drows, dold, stream);
+    std::vector<double> oldh(nr * R);
+    CK(cudaMemcpyAsync(oldh.data(), dold, rb, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    std::vector<double> newh = oldh;
+    for (const auto& e : E) {  // sequential semantics of update_factor_entry
+        const double val = storage == KRPG_STORE_F32 ? double(float(e.v)) : e.v;
+        const uint64_t i = uint64_t(std::lower_bound(rows.begin(), rows.end(), e.r) - rows.begin());
+        newh[i * R + e.c] = val;
+    }
+    std::vector<krpg::PatchItem> flat;
+    flat.reserve(nitems);
+    for (int dd = int(t.d); dd >= 0; --dd) flat.insert(flat.end(), lv[dd].begin(), lv[dd].end());
+    // pinned staging would help only huge batches; these copies are stream-ordered
+    CK(cudaMemcpyAsync(dnew, newh.data(), rb, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(dit, flat.data(), sizeof(krpg::PatchItem) * nitems, cudaMemcpyHostToDevice, stream));
+    cudaEvent_t t0 = pbegin();
+    uint64_t off = 0;
+    int cur = 0, launches = 0;
+    for (int dd = int(t.d); dd >= 0; --dd) {
+        const uint64_t m = lv[dd].size();
+        krpg::launch_tree_patch_level(F.tree.as<double>(), R, dit + off, m, dl[cur ^ 1], dl[cur], dold, dnew, stream);
+        off += m;
+        cur ^= 1;
+        launches += m ? 1 : 0;
+    }
+    krpg::launch_scatter_rows(F.U.p, storage, R, nr, drows, dnew, stream);
+    pend(KRPG_PROF_UPDATE, t0, launches + 1);
+    prof_launches[KRPG_PROF_OTHER] += 1;  // gather of the old rows
+    CK(cudaGetLastError());
+    std::vector<double> root(P);
+    CK(cudaMemcpyAsync(root.data(), F.tree.p, 8 * P, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));  // also keeps newh / flat alive until the copies ran
+    presolve();
+    krpg::unpack_upper(root.data(), R, F.G.data());
 }
 
 // Device SegmentTreeSampler (segment_tree_sampler.hpp:26-139): a standalone tree over
@@ -1206,6 +1354,7 @@ int krpg_sts_solve(krpg_t h, krpg_tensor_t T, uint32_t j, uint64_t J, uint64_t s
         std::lock_guard<std::mutex> lk(h->mu);
         std::lock_guard<std::mutex> lt(T->mu);
         h->set_device();
+        h->flush_updates();
         h->sts_solve(*T, j, J, seed, sigma);
     });
 }
@@ -1247,6 +1396,7 @@ int krpg_create(const double* const* factors, const uint64_t* I, uint32_t N, uin
             CK(cudaEventCreate(&h->ev0));
             CK(cudaEventCreate(&h->ev1));
             h->f.resize(N);
+            h->pending.resize(N);
             for (uint32_t k = 0; k < N; ++k) {
                 h->upload_factor(k, factors[k], I[k]);
                 h->build_tree(k);
@@ -1277,6 +1427,7 @@ int krpg_create_device(const void* const* dev_factors, const uint64_t* I, uint32
             CK(cudaEventCreate(&h->ev0));
             CK(cudaEventCreate(&h->ev1));
             h->f.resize(N);
+            h->pending.resize(N);
             for (uint32_t k = 0; k < N; ++k) {
                 Factor& F = h->f[k];
                 F.I = I[k];
@@ -1334,6 +1485,9 @@ int krpg_info(krpg_t h, uint32_t* N, uint32_t* R, uint64_t* I) {
 int krpg_factor_gram(krpg_t h, uint32_t j, double* out) {
     return guard([&] {
         require(h && j < h->N, "factor_gram: index out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->flush_updates();
         std::memcpy(out, h->f[j].G.data(), sizeof(double) * h->R * h->R);
     });
 }
@@ -1343,6 +1497,7 @@ int krpg_factor(krpg_t h, uint32_t j, double* out) {
         require(h && j < h->N, "factor: index out of range");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         const uint64_t n = h->f[j].I * h->R;
         if (h->storage == KRPG_STORE_F32) {
             double* tmp = static_cast<double*>(h->rowbuf.ensure(8 * n));
@@ -1372,6 +1527,7 @@ int krpg_node_gram(krpg_t h, uint32_t j, uint64_t node, double* out) {
         require(krpg::stored(node), "node_gram: partial Gram not stored at this node");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         std::vector<double> p(h->P);
         CK(cudaMemcpyAsync(p.data(), h->f[j].tree.as<double>() + krpg::slot_of(node) * h->P, 8 * h->P,
                            cudaMemcpyDeviceToHost, h->stream));
@@ -1386,6 +1542,7 @@ int krpg_tree_grams(krpg_t h, uint32_t j, double* out) {
         const krpg::Topo t = krpg::make_topo(h->f[j].I, h->R);
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         CK(cudaMemcpyAsync(out, h->f[j].tree.p, 8 * t.L * h->P, cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     });
@@ -1397,6 +1554,7 @@ int krpg_sample_device(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, ui
         require(h, "krpg: null handle");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         h->sample_device(excluded, J, seed, draw_offset, mode, d_idx, d_prob, d_rows, d_margin);
     });
 }
@@ -1408,11 +1566,12 @@ int krpg_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t 
         require(J >= 1, "KrpSample: sample count must be positive");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         uint32_t* di = idx ? static_cast<uint32_t*>(h->sIdx.ensure(4 * J * h->N)) : nullptr;
         double* dp = prob ? static_cast<double*>(h->sProb.ensure(8 * J)) : nullptr;
         double* dr = static_cast<double*>(h->sH.ensure(8 * J * h->R));
         double* dm = margin ? static_cast<double*>(h->sMargin.ensure(8 * J)) : nullptr;
-        static const bool trace = std::getenv("KRPG_HOST_TRACE") != nullptr;
+        const bool trace = h->host_trace;
         const auto t0 = std::chrono::steady_clock::now();
         h->sample_device(excluded, J, seed, draw_offset, mode, di, dp, dr, dm);
         const auto t1 = std::chrono::steady_clock::now();
@@ -1438,6 +1597,7 @@ int krpg_product_lev_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t see
         if (excluded >= 0) require(uint64_t(excluded) < h->N, "product_lev_sample: excluded index out of range");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         h->sync_check();  // drain async calls before the synchronous path
         std::vector<const void*> U(h->N);
         std::vector<uint64_t> I(h->N);
@@ -1530,6 +1690,7 @@ int krpg_leverage_scores(krpg_t h, uint32_t j, double* out) {
         require(h && j < h->N, "leverage_scores: index out of range");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         h->sync_check();
         const uint32_t R = h->R;
         const uint64_t P = uint64_t(R) * (R + 1) / 2, I = h->f[j].I;
@@ -1551,6 +1712,7 @@ int krpg_sync(krpg_t h) {
         require(h, "krpg: null handle");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         h->sync_check();
     });
 }
@@ -1563,6 +1725,7 @@ int krpg_conditional(krpg_t h, int64_t excluded, uint32_t k, const double* hist,
         require(h, "krpg: null handle");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         const uint32_t R = h->R;
         const size_t RR = size_t(R) * R;
         const std::vector<uint32_t> inc = h->included(excluded);
@@ -1616,6 +1779,7 @@ int krpg_update_factor(krpg_t h, uint32_t j, const double* U, uint64_t I) {
         for (uint64_t e = 0; e < I * h->R; ++e) require(std::isfinite(U[e]), "update_factor: invalid factor");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         h->upload_factor(j, U, I);
         h->build_tree(j);
     });
@@ -1627,12 +1791,27 @@ int krpg_update_factor_device(krpg_t h, uint32_t j, const void* dU, uint64_t I) 
         require(I >= 1 && dU, "update_factor: invalid factor");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
-        Factor& F = h->f[j];
-        F.I = I;
-        F.U.ensure(h->elt() * I * h->R);
-        CK(cudaMemcpyAsync(F.U.p, dU, h->elt() * I * h->R, cudaMemcpyDeviceToDevice, h->stream));
-        h->build_tree(j);
-        for (double x : F.G) require(std::isfinite(x), "update_factor: invalid factor");
+        h->flush_updates();
+        // validate before mutating (krp_sampler.cpp:198-205): the new factor and its tree
+        // are built aside and swapped in only when the root Gram is finite (a non-finite
+        // entry makes its row's diagonal, hence the root, non-finite)
+        Factor nf;
+        nf.I = I;
+        nf.U.ensure(h->elt() * I * h->R);
+        CK(cudaMemcpyAsync(nf.U.p, dU, h->elt() * I * h->R, cudaMemcpyDeviceToDevice, h->stream));
+        std::swap(h->f[j], nf);
+        try {
+            h->build_tree(j);
+            for (double x : h->f[j].G) require(std::isfinite(x), "update_factor: invalid factor");
+        } catch (...) {
+            std::swap(h->f[j], nf);
+            CK(cudaStreamSynchronize(h->stream));
+            nf.U.release();
+            nf.tree.release();
+            throw;
+        }
+        nf.U.release();
+        nf.tree.release();
     });
 }
 
@@ -1641,6 +1820,7 @@ int krpg_rebuild(krpg_t h, uint32_t j) {
         require(h && j < h->N, "rebuild: index out of range");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         h->build_tree(j);
     });
 }
@@ -1648,6 +1828,9 @@ int krpg_rebuild(krpg_t h, uint32_t j) {
 int krpg_tree_device(krpg_t h, uint32_t j, double** d_tree, uint64_t* slots) {
     return guard([&] {
         require(h && j < h->N, "krpg_tree_device: index out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->flush_updates();
         *d_tree = h->f[j].tree.as<double>();
         *slots = krpg::make_topo(h->f[j].I, h->R).L;
     });
@@ -1656,6 +1839,9 @@ int krpg_tree_device(krpg_t h, uint32_t j, double** d_tree, uint64_t* slots) {
 int krpg_factor_device(krpg_t h, uint32_t j, void** d_U) {
     return guard([&] {
         require(h && j < h->N, "krpg_factor_device: index out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        h->set_device();
+        h->flush_updates();
         *d_U = h->f[j].U.p;
     });
 }
@@ -1666,6 +1852,7 @@ int krpg_build_partition(krpg_t h, uint32_t j, uint32_t parts, uint32_t part, do
         require(d_subroot, "krpg_build_partition: null subroot buffer");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         h->build_partition(j, parts, part, d_subroot);
     });
 }
@@ -1676,6 +1863,7 @@ int krpg_finish_partitions(krpg_t h, uint32_t j, uint32_t parts, const double* d
         require(d_subroots, "krpg_finish_partitions: null subroot buffer");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         h->finish_partitions(j, parts, d_subroots);
     });
 }
@@ -1699,41 +1887,10 @@ int krpg_update_entries(krpg_t h, uint32_t j, const uint64_t* r, const uint32_t*
         }
         if (n == 0) return;
         std::lock_guard<std::mutex> lk(h->mu);
-        h->set_device();
-        // distinct rows in first-touch order
-        std::unordered_map<uint64_t, uint64_t> slot;
-        std::vector<uint64_t> rows;
-        for (uint64_t e = 0; e < n; ++e)
-            if (slot.emplace(r[e], rows.size()).second) rows.push_back(r[e]);
-        const uint64_t nr = rows.size();
-        const size_t rb = 8 * nr * R;
-        char* d = static_cast<char*>(h->rowbuf.ensure(8 * nr + 2 * rb + 64));
-        uint64_t* drows = reinterpret_cast<uint64_t*>(d);
-        double* dold = reinterpret_cast<double*>(d + ((8 * nr + 15) / 16) * 16);
-        double* dnew = dold + nr * R;
-        CK(cudaMemcpyAsync(drows, rows.data(), 8 * nr, cudaMemcpyHostToDevice, h->stream));
-        krpg::launch_gather_rows(h->f[j].U.p, h->storage, R, nr, drows, dold, h->stream);
-        std::vector<double> oldh(nr * R);
-        CK(cudaMemcpyAsync(oldh.data(), dold, rb, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
-        std::vector<double> newh = oldh;
-        for (uint64_t e = 0; e < n; ++e) {  // sequential semantics of update_factor_entry
-            double val = v[e];
-            if (h->storage == KRPG_STORE_F32) val = static_cast<double>(static_cast<float>(val));
-            newh[slot[r[e]] * R + c[e]] = val;
-        }
-        CK(cudaMemcpyAsync(dnew, newh.data(), rb, cudaMemcpyHostToDevice, h->stream));
-        cudaEvent_t t0 = h->pbegin();
-        krpg::launch_row_deltas(h->f[j].tree.as<double>(), h->f[j].I, R, 0, nullptr, 0, nr, drows, dold, dnew, h->stream);
-        krpg::launch_scatter_rows(h->f[j].U.p, h->storage, R, nr, drows, dnew, h->stream);
-        h->pend(KRPG_PROF_UPDATE, t0, 2);
-        h->prof_launches[KRPG_PROF_OTHER] += 1;  // gather of the old rows
-        CK(cudaGetLastError());
-        std::vector<double> root(h->P);
-        CK(cudaMemcpyAsync(root.data(), h->f[j].tree.p, 8 * h->P, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
-        h->presolve();
-        krpg::unpack_upper(root.data(), R, h->f[j].G.data());
+        // queued: applied as one device patch before the next call that reads this
+        // handle's factors, trees or Grams (krpg_sampler::flush_updates)
+        auto& q = h->pending[j];  // amortised growth: per-entry calls append one at a time
+        for (uint64_t e = 0; e < n; ++e) q.push_back({r[e], c[e], v[e]});
     });
 }
 
@@ -1742,6 +1899,7 @@ int krpg_validate(krpg_t h, double tol) {
         require(h, "krpg: null handle");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         const uint32_t R = h->R;
         double* d = static_cast<double*>(h->small.ensure(8 * size_t(R) * R));
         std::vector<double> fresh(size_t(R) * R), root(h->P), G(size_t(R) * R);
@@ -1771,6 +1929,7 @@ int krpg_gather_sa_device(krpg_t h, uint64_t J, const double* d_prob, const doub
         require(J >= 1, "make_sampling_weights: J must be positive");
         std::lock_guard<std::mutex> lk(h->mu);
         h->set_device();
+        h->flush_updates();
         int* derr = static_cast<int*>(h->err.ensure(sizeof(int)));
         CK(cudaMemsetAsync(derr, 0, sizeof(int), h->stream));
         krpg::launch_gather_sa(d_prob, d_rows, J, h->R, d_weights, d_sa, derr, h->stream);
@@ -1831,6 +1990,27 @@ int krpg_set_option(krpg_t h, int option, int64_t value) {
         } else if (option == KRPG_OPT_ASYNC) {
             if (!value && h->async_mode) h->sync_check();
             h->async_mode = value != 0;
+        } else if (option == KRPG_OPT_HOST_TRACE)
+            h->host_trace = value != 0;
+        else if (option == KRPG_OPT_EVAL_REG)
+            h->tune.eval_reg = value != 0;
+        else if (option == KRPG_OPT_POS0_TABLES)
+            h->tune.pos0_tables = value != 0;
+        else if (option == KRPG_OPT_DEEP_THRESHOLD) {
+            require(value >= 1 && value <= (int64_t(1) << 30), "krpg_set_option: deep threshold out of range");
+            h->tune.deep_threshold = int(value);
+        } else if (option == KRPG_OPT_DEEP_CHUNK) {
+            require(value >= 1 && value <= 32, "krpg_set_option: deep chunk must be in [1, 32]");
+            h->tune.deep_chunk = int(value);
+        } else if (option == KRPG_OPT_EVAL_SPLIT) {
+            require(value == 0 || value == 1 || value == 16, "krpg_set_option: eval split must be 0, 1 or 16");
+            h->tune.eval_split = int(value);
+        } else if (option == KRPG_OPT_DEEP_DMMA_MIN) {
+            require(value >= 1 && value <= 64, "krpg_set_option: deep DMMA minimum must be in [1, 64]");
+            h->tune.deep_dmma_min = int(value);
+        } else if (option == KRPG_OPT_LEAF_PAR) {
+            require(value >= 0 && value <= 64, "krpg_set_option: leaf scan parallel bound must be in [0, 64]");
+            h->tune.leaf_par = int(value);
         }
         else
             throw std::invalid_argument("krpg_set_option: unknown option");

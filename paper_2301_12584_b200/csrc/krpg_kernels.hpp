@@ -77,6 +77,21 @@ void launch_segtree_masses(const double* U, uint64_t I, uint32_t R, const double
                            const double* Y, const double* root, double* out, cudaStream_t s);
 
 // ---- grouped (level-synchronous, DMMA) two-stage descent, descent_v2.cu ----
+// Kernel-variant / tuning choices of the grouped descent (set per handle through
+// krpg_set_option; the defaults are the measured best). The first four give
+// bit-identical samples (same arithmetic, tests/test_gpu_kernel_variants.py);
+// eval_split == 1 (split summation order at R = 64), deep_dmma_min > 1 (CUDA-core
+// forms for small runs) and leaf_par < 8 change last-bit rounding.
+struct Tuning {
+    int eval_reg = 1;          // R <= 64 shallow levels: register-resident kernel (0: CTA kernel)
+    int pos0_tables = 1;       // first included position from (node, component) tables
+    int deep_threshold = 32;   // a level is "deep" below this many draws per node on average
+    int deep_chunk = 8;        // sorted draws per warp work unit of the fused deep pass (1..32)
+    int eval_split = 16;       // split-Gram level kernel: 16 = R 128 only, 1 = R 64 and 128, 0 = off
+    int deep_dmma_min = 1;     // deep-pass runs with fewer draws use CUDA-core forms
+    int leaf_par = 8;          // leaf runs with at most this many draws scan warp-parallel
+};
+
 struct GroupedArgs {
     uint32_t R, N, k, pos, storage;
     uint64_t J, seed, draw_offset, I;
@@ -98,6 +113,7 @@ struct GroupedArgs {
     int fused_deep;                    // deep levels + leaf in one warp-local pass
     int h_ones;                        // H is all ones (first included position): table shortcut
     double* pos0_tab;                  // scratch for the first-position tables (pos0_tab_doubles(R)), nullable
+    Tuning tune;
 };
 // doubles of scratch the first-position tables need at rank R (E-tree masses, factor-tree
 // masses per (node, component) for the top levels, per-node counters)
@@ -129,6 +145,22 @@ void launch_conditional_probs(const void* U, uint32_t storage, uint64_t I, uint3
 
 // ---- updates (segment_tree_sampler.cpp:358-409) ----
 // for each touched row: patch u'u'^T - uu^T into every stored node on its path
+// Deterministic batched tree patch (update_entry, segment_tree_sampler.cpp:358-409, for a
+// batch of distinct rows): every touched node v gets G_v += Delta_v with
+// Delta_v = sum over its touched rows of u'u'^T - u u^T, reduced bottom-up in a fixed
+// order (a leaf sums its rows in ascending order, a parent adds left + right), one warp
+// per node and no atomics, so the patched tree is bit-reproducible run to run.
+// Items of one tree depth: leaf items carry the row range [rb, re) of their rows in
+// the (ascending) row arrays; internal items the indices of their touched children in
+// the previous (deeper) depth's item list (-1 = untouched).
+struct PatchItem {
+    uint64_t node;
+    int64_t lc, rc;
+    uint32_t rb, re;
+};
+void launch_tree_patch_level(double* compact, uint32_t R, const PatchItem* items, uint64_t nitems,
+                             const double* delta_prev, double* delta_cur, const double* old_rows,
+                             const double* new_rows, cudaStream_t s);
 void launch_row_deltas(double* compact, uint64_t I, uint32_t R, uint64_t F, const uint64_t* segs, uint64_t nleaves,
                        uint64_t nrows,
                        const uint64_t* rows, const double* old_rows, const double* new_rows,
@@ -177,6 +209,9 @@ void launch_sts_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, con
 // normalised columns (cp_als.cpp:39-52) stored into Uout (storage 0 f64, 1 f32)
 void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const double* pinv, double* Utmp, double* nrm,
                             void* Uout, uint32_t storage, cudaStream_t s);
+// U_out = Utmp / nrm column-wise in the storage dtype (normalize_columns' store)
+void launch_normalize_store(const double* Utmp, uint64_t I, uint32_t R, const double* nrm, void* Uout,
+                            uint32_t storage, cudaStream_t s);
 
 // ---- CP-ARLS-LEV product sampler (productlev.cu; sketch.cpp:86-149) ----
 // p_i = u_i^T G+ u_i for every row (DMMA for R % 8 == 0, R <= 160 from the packed

@@ -27,6 +27,7 @@
 
 #include "krpg_device.cuh"
 #include "krpg_kernels.hpp"
+#include "launch_util.hpp"
 #include "qf_dmma.cuh"
 
 namespace krpg {
@@ -121,28 +122,14 @@ __global__ void k_row_leverage_generic(const T* __restrict__ U, uint64_t I, uint
     }
 }
 
-int sm_count_lev() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return n;
-}
+int sm_count_lev() { return sm_count_current(); }
 
 template <int NB, typename T>
 void launch_lev(const T* U, uint64_t I, const double* Gp, double* out, cudaStream_t s) {
     using C = LevCfg<NB>;
     auto kern = k_row_leverage<NB, T>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        configured = true;
-    }
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::WARPS * 32, C::SMEM);
-    if (occ < 1) occ = 1;
+    smem_optin(kern, C::SMEM);
+    const int occ = occupancy(kern, C::WARPS * 32, C::SMEM);
     const uint64_t nblk = (I + 7) / 8;
     const uint64_t need = (nblk + C::WARPS - 1) / C::WARPS;
     const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(need, uint64_t(sm_count_lev()) * occ));

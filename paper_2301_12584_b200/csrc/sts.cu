@@ -28,6 +28,7 @@
 
 #include "krpg_device.cuh"
 #include "krpg_kernels.hpp"
+#include "launch_util.hpp"
 #include "ptx.cuh"
 
 namespace krpg {
@@ -523,21 +524,13 @@ void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const doubl
     const size_t need = sizeof(double) * R * R;
     const bool staged = need <= 160 * 1024;  // R <= 144; larger pinv is read through L1/L2
     const size_t smem = staged ? need : 0;
-    static size_t configured_for = 0;
-    if (smem > 48 * 1024 && configured_for < smem) {
-        cudaFuncSetAttribute(k_solve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured_for = smem;
-    }
+    smem_optin(k_solve_rows, smem);
     cudaMemsetAsync(nrm, 0, sizeof(double) * R, s);
     if (R % 8 == 0 && R <= 128) {  // FP64 tensor-core path (padded pinv fits shared memory)
         const size_t dsm = sizeof(double) * R * (R + 4);
         const unsigned grid = unsigned(std::min<uint64_t>((I + 63) / 64, 148ull * 8));
         auto launch = [&](auto kern) {
-            static size_t conf = 0;
-            if (dsm > 48 * 1024 && conf < dsm) {
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));
-                conf = dsm;
-            }
+            smem_optin(kern, dsm);
             kern<<<grid, 256, dsm, s>>>(M, I, pinv, Utmp, nrm);
         };
         switch (R / 8) {
@@ -561,6 +554,11 @@ void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const doubl
         k_solve_rows<<<grid, 256, smem, s>>>(M, I, R, pinv, Utmp, nrm, staged ? 1 : 0);
     }
     k_sqrt_inplace<<<1, 256, 0, s>>>(nrm, R);
+    if (Uout) launch_normalize_store(Utmp, I, R, nrm, Uout, storage, s);
+}
+
+void launch_normalize_store(const double* Utmp, uint64_t I, uint32_t R, const double* nrm, void* Uout,
+                            uint32_t storage, cudaStream_t s) {
     if (storage == 1)
         k_normalize_store<float><<<grid_of(I * R), 256, 0, s>>>(Utmp, I, R, nrm, static_cast<float*>(Uout));
     else

@@ -20,6 +20,7 @@
 
 #include "krpg_device.cuh"
 #include "krpg_kernels.hpp"
+#include "launch_util.hpp"
 #include "ptx.cuh"
 
 namespace krpg {
@@ -461,28 +462,14 @@ __global__ void k_level_reduce(const double* __restrict__ child, double* __restr
     }
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return n;
-}
+int sm_count() { return sm_count_current(); }
 
 template <int NB, typename T>
 void launch_dmma(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s) {
     using C = LeafCfg<NB, T>;
     auto kern = k_leaf_dmma<NB, T>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        configured = true;
-    }
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::WPC * 32, C::SMEM);
-    if (occ < 1) occ = 1;
+    smem_optin(kern, C::SMEM);
+    const int occ = occupancy(kern, C::WPC * 32, C::SMEM);
     const uint64_t need = (g.p1 - g.p0 + C::WPC - 1) / C::WPC;
     const uint64_t grid = std::min<uint64_t>(need, uint64_t(sm_count()) * occ);
     kern<<<unsigned(grid), C::WPC * 32, C::SMEM, s>>>(U, g, compact, tout);
@@ -492,14 +479,8 @@ template <int R_, typename T>
 void launch_big(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s) {
     using C = BigCfg<R_, T>;
     auto kern = k_leaf_cta<R_, T>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        configured = true;
-    }
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NW * 32, C::SMEM);
-    if (occ < 1) occ = 1;
+    smem_optin(kern, C::SMEM);
+    const int occ = occupancy(kern, C::NW * 32, C::SMEM);
     const uint64_t grid = std::min<uint64_t>(g.p1 - g.p0, std::max<uint64_t>(1, uint64_t(sm_count()) * occ / C::SPLIT));
     kern<<<dim3(unsigned(grid), C::SPLIT), C::NW * 32, C::SMEM, s>>>(U, g, compact, tout);
 }

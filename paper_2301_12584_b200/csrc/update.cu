@@ -12,6 +12,7 @@
 
 #include "krpg_device.cuh"
 #include "krpg_kernels.hpp"
+#include "launch_util.hpp"
 #include "ptx.cuh"
 
 namespace krpg {
@@ -193,15 +194,7 @@ __global__ void k_full_gram_finish(const double* __restrict__ partial, int npart
     out[uint64_t(b) * R + a] = acc;
 }
 
-int sm_count_upd() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return n;
-}
+int sm_count_upd() { return sm_count_current(); }
 
 template <int NB, typename T>
 void launch_gram_dmma(const T* U, uint64_t I, double* out, double* partial, cudaStream_t s) {
@@ -233,7 +226,54 @@ void launch_gram_any(const T* U, uint64_t I, uint32_t R, double* out, double* pa
     k_full_gram_finish<<<(P + 255) / 256, 256, 0, s>>>(partial, grid, R, out);
 }
 
+__global__ void __launch_bounds__(256) k_patch_level(double* __restrict__ compact, uint32_t R,
+                                                     const PatchItem* __restrict__ items, uint64_t nitems,
+                                                     const double* __restrict__ dprev, double* __restrict__ dcur,
+                                                     const double* __restrict__ oldr, const double* __restrict__ newr) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= nitems) return;
+    const PatchItem it = items[w];
+    const uint64_t P = uint64_t(R) * (R + 1) / 2;
+    double* out = dcur + w * P;
+    double* g = stored(it.node) ? compact + slot_of(it.node) * P : nullptr;
+    if (it.re > it.rb) {  // leaf: its touched rows in ascending order
+        for (uint32_t a = 0; a < R; ++a) {
+            const uint32_t k0 = pack_index(R, a, a);
+            for (uint32_t b = a + lane; b < R; b += 32) {
+                double acc = 0.0;
+                for (uint32_t r = it.rb; r < it.re; ++r) {
+                    const double* u0 = oldr + uint64_t(r) * R;
+                    const double* u1 = newr + uint64_t(r) * R;
+                    // u'_a u'_b - u_a u_b  ==  u_a (u'_b - u_b) + (u'_a - u_a) u'_b
+                    acc += fma(u0[a], u1[b] - u0[b], (u1[a] - u0[a]) * u1[b]);
+                }
+                const uint32_t k = k0 + (b - a);
+                out[k] = acc;
+                if (g) g[k] += acc;
+            }
+        }
+        return;
+    }
+    const double* l = it.lc >= 0 ? dprev + uint64_t(it.lc) * P : nullptr;
+    const double* r = it.rc >= 0 ? dprev + uint64_t(it.rc) * P : nullptr;
+    for (uint64_t k = lane; k < P; k += 32) {
+        const double d = l && r ? l[k] + r[k] : (l ? l[k] : r[k]);
+        out[k] = d;
+        if (g) g[k] += d;
+    }
+}
+
 }  // namespace
+
+void launch_tree_patch_level(double* compact, uint32_t R, const PatchItem* items, uint64_t nitems,
+                             const double* delta_prev, double* delta_cur, const double* old_rows,
+                             const double* new_rows, cudaStream_t s) {
+    if (!nitems) return;
+    k_patch_level<<<unsigned((nitems * 32 + 255) / 256), 256, 0, s>>>(compact, R, items, nitems, delta_prev,
+                                                                    delta_cur, old_rows, new_rows);
+}
+
 
 size_t full_gram_work_doubles(uint32_t R) {
     const size_t P = size_t(R) * (R + 1) / 2;

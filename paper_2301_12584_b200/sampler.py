@@ -46,6 +46,24 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(_dp)
 
 
+def _dev_tensor(t, name: str, dtype, device: int, shape=None):
+    """Validate a torch CUDA tensor handed to the C ABI as a raw pointer: dtype,
+    contiguity, device and shape must match exactly, since the library reads and
+    writes through data_ptr() with no further checks."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise KrpgInvalidArgument(f"{name}: expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise KrpgInvalidArgument(f"{name}: expected dtype {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise KrpgInvalidArgument(f"{name}: tensor must be contiguous (row-major)")
+    if t.device.index != device:
+        raise KrpgInvalidArgument(f"{name}: tensor is on cuda:{t.device.index}, sampler on cuda:{device}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise KrpgInvalidArgument(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    return C.c_void_p(t.data_ptr())
+
+
 class RowOrder(enum.Enum):
     """krp_sampler.hpp:17-25."""
     Ascending = 0  # first factor varies slowest
@@ -122,6 +140,7 @@ class KrpSampler:
         h = C.c_void_p()
         st = STORE_F32 if storage == "f32" else STORE_F64
         check(L.krpg_create(ptrs, I, N, R, st, device, C.byref(h)))
+        self._device = device
         self._h = h
         self._N, self._R = N, R
         self._dims = [f.shape[0] for f in fs]
@@ -129,21 +148,48 @@ class KrpSampler:
 
     @classmethod
     def from_device(cls, factors, storage: str = "f64", device: int = 0) -> "KrpSampler":
-        """Build from torch CUDA tensors (row-major, float64 or float32)."""
+        """Build from torch CUDA tensors (row-major, float64 for storage "f64",
+        float32 for "f32", all on cuda:`device`). The library reads them on its own
+        stream after the producer (torch's current stream) has finished."""
+        import torch
         L = _lib.lib()
         N = len(factors)
-        R = int(factors[0].shape[1])
-        I = (C.c_uint64 * N)(*[int(f.shape[0]) for f in factors])
-        ptrs = (C.c_void_p * N)(*[C.c_void_p(f.data_ptr()) for f in factors])
-        h = C.c_void_p()
+        if N == 0:
+            raise KrpgInvalidArgument("KrpSampler: factor list is empty")
         st = STORE_F32 if storage == "f32" else STORE_F64
+        dt = torch.float32 if st == STORE_F32 else torch.float64
+        if any(f.dim() != 2 for f in factors):
+            raise KrpgInvalidArgument("KrpSampler: factors must be 2-D")
+        R = int(factors[0].shape[1])
+        if any(int(f.shape[1]) != R for f in factors):
+            raise KrpgInvalidArgument("KrpSampler: inconsistent column counts")
+        ptrs = (C.c_void_p * N)(*[_dev_tensor(f, f"factor {k}", dt, device) for k, f in enumerate(factors)])
+        I = (C.c_uint64 * N)(*[int(f.shape[0]) for f in factors])
+        torch.cuda.current_stream(device).synchronize()  # producer -> library (no handle/stream yet)
+        h = C.c_void_p()
         check(L.krpg_create_device(ptrs, I, N, R, st, device, C.byref(h)))
         self = cls.__new__(cls)
         self._h = h
         self._N, self._R = N, R
         self._dims = [int(f.shape[0]) for f in factors]
         self._storage = st
+        self._device = device
         return self
+
+    # ---- stream ordering between torch and the library's own stream ----
+    def _lib_stream(self):
+        import torch
+        return torch.cuda.ExternalStream(self.stream(), device=torch.device("cuda", self._device))
+
+    def _after_torch(self):
+        """Library work issued next waits for what torch's current stream has queued."""
+        import torch
+        self._lib_stream().wait_stream(torch.cuda.current_stream(self._device))
+
+    def _before_torch(self):
+        """torch's current stream waits for the library's queued work (device outputs)."""
+        import torch
+        torch.cuda.current_stream(self._device).wait_stream(self._lib_stream())
 
     def close(self) -> None:
         h = getattr(self, "_h", None)
@@ -251,24 +297,44 @@ class KrpSampler:
     def sample_device(self, excluded: Optional[int], J: int, seed: int, idx=None, prob=None,
                       rows=None, margin=None, *, mode: str = "two_stage", draw_offset: int = 0) -> None:
         """Device-resident outputs (torch CUDA tensors or None)."""
+        import torch
         e = -1 if excluded is None else int(excluded)
         m = MODE_ONE_STAGE if mode == "one_stage" else MODE_TWO_STAGE
+        d = self._device
 
-        def p(t):
-            return C.c_void_p(t.data_ptr()) if t is not None else None
+        def p(t, name, dtype, shape):
+            return _dev_tensor(t, name, dtype, d, shape) if t is not None else None
 
-        check(_lib.lib().krpg_sample_device(self._h, e, J, seed, draw_offset, m, p(idx), p(prob),
-                                            p(rows), p(margin)))
+        pi = p(idx, "idx", torch.int32, (J, self._N))
+        pp = p(prob, "prob", torch.float64, (J,))
+        pr = p(rows, "rows", torch.float64, (J, self._R))
+        pm = p(margin, "margin", torch.float64, (J,))
+        self._after_torch()
+        check(_lib.lib().krpg_sample_device(self._h, e, J, seed, draw_offset, m, pi, pp, pr, pm))
+        self._before_torch()
 
     def gather_sa_device(self, J: int, prob, rows, weights, sa) -> None:
-        check(_lib.lib().krpg_gather_sa_device(self._h, J, C.c_void_p(prob.data_ptr()),
-                                               C.c_void_p(rows.data_ptr()),
-                                               C.c_void_p(weights.data_ptr()) if weights is not None else None,
-                                               C.c_void_p(sa.data_ptr())))
+        import torch
+        d, R, f64 = self._device, self._R, torch.float64
+        pp = _dev_tensor(prob, "prob", f64, d, (J,))
+        pr = _dev_tensor(rows, "rows", f64, d, (J, R))
+        pw = _dev_tensor(weights, "weights", f64, d, (J,)) if weights is not None else None
+        ps = _dev_tensor(sa, "sa", f64, d, (J, R))
+        self._after_torch()
+        check(_lib.lib().krpg_gather_sa_device(self._h, J, pp, pr, pw, ps))
+        self._before_torch()
 
     def update_factor_device(self, j: int, U) -> None:
         """New factor j from a torch CUDA tensor (storage dtype), full device rebuild."""
-        check(_lib.lib().krpg_update_factor_device(self._h, j, C.c_void_p(U.data_ptr()), int(U.shape[0])))
+        import torch
+        if not 0 <= j < self._N:
+            raise KrpgInvalidArgument("update_factor: index out of range")
+        dt = torch.float32 if self._storage == STORE_F32 else torch.float64
+        if U.dim() != 2 or int(U.shape[1]) != self._R:
+            raise KrpgInvalidArgument("update_factor: column count mismatch")
+        pu = _dev_tensor(U, "U", dt, self._device)
+        self._after_torch()
+        check(_lib.lib().krpg_update_factor_device(self._h, j, pu, int(U.shape[0])))
         self._dims[j] = int(U.shape[0])
 
     def set_grouped_descent(self, on: bool) -> None:
@@ -282,6 +348,15 @@ class KrpSampler:
     def set_slices(self, n: int) -> None:
         """Concurrent draw slices of the grouped descent (KRPG_OPT_SLICES, default 1)."""
         check(_lib.lib().krpg_set_option(self._h, _lib.OPT_SLICES, int(n)))
+
+    def set_tuning(self, **opts) -> None:
+        """Kernel-variant / tuning options of the grouped descent (include/krpg.h
+        KRPG_OPT_EVAL_REG ...): eval_reg, pos0_tables, deep_threshold, deep_chunk,
+        eval_split, deep_dmma_min, leaf_par."""
+        for k, v in opts.items():
+            if k not in _lib.TUNING:
+                raise KrpgInvalidArgument(f"set_tuning: unknown option {k}")
+            check(_lib.lib().krpg_set_option(self._h, _lib.TUNING[k], int(v)))
 
     def set_async(self, on: bool) -> None:
         """KRPG_OPT_ASYNC: sample_device returns once enqueued (no host sync), so
@@ -319,15 +394,25 @@ class KrpSampler:
         ptr, slots = C.c_void_p(), C.c_uint64()
         check(_lib.lib().krpg_tree_device(self._h, j, C.byref(ptr), C.byref(slots)))
         P = self._R * (self._R + 1) // 2
-        return torch.as_tensor(_DeviceArray(ptr.value, slots.value * P), device="cuda")
+        return torch.as_tensor(_DeviceArray(ptr.value, slots.value * P), device=f"cuda:{self._device}")
 
     def build_partition(self, j: int, parts: int, part: int, subroot) -> None:
         """Stored nodes of subtree `part` of `parts`; subtree root Gram -> `subroot` (P doubles, CUDA)."""
-        check(_lib.lib().krpg_build_partition(self._h, j, parts, part, C.c_void_p(subroot.data_ptr())))
+        import torch
+        P = self._R * (self._R + 1) // 2
+        ps = _dev_tensor(subroot, "subroot", torch.float64, self._device, (P,))
+        self._after_torch()
+        check(_lib.lib().krpg_build_partition(self._h, j, parts, part, ps))
+        self._before_torch()
 
     def finish_partitions(self, j: int, parts: int, subroots) -> None:
         """Top levels from all subtree roots (parts x P doubles, CUDA, subtree order)."""
-        check(_lib.lib().krpg_finish_partitions(self._h, j, parts, C.c_void_p(subroots.data_ptr())))
+        import torch
+        P = self._R * (self._R + 1) // 2
+        ps = _dev_tensor(subroots, "subroots", torch.float64, self._device, (parts * P,))
+        self._after_torch()
+        check(_lib.lib().krpg_finish_partitions(self._h, j, parts, ps))
+        self._before_torch()
 
     def profile_enable(self, on: bool = True, detail: bool = False) -> None:
         check(_lib.lib().krpg_profile_enable(self._h, 1 if on else 0))

@@ -5,55 +5,33 @@ fragments) and the first-position tables (E-tree and top factor-tree levels
 computed once per (node, eigen-component) when h = ones) are claimed to apply
 exactly the arithmetic of the per-draw DMMA quadratic form (block_qf_packed) to
 exactly the same operands, so every branch decision, probability, row and
-margin must equal the k_eval_cta path bit for bit. The variants are selected by
-environment switches that are read once per process, so each runs in its own
-subprocess on the same factors and seeds.
+margin must equal the k_eval_cta path bit for bit -- and so must other deep /
+shallow splits and deep-pass work-unit sizes. The variants are per-handle
+options (krpg_set_option, KRPG_OPT_EVAL_REG ...), switched on one sampler.
 """
-import os
-import subprocess
-import sys
-import tempfile
-
 import numpy as np
 import pytest
 
+from parity_util import pareto_factors
+
 pytestmark = pytest.mark.gpu
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-CHILD = r"""
-import sys
-import numpy as np
-sys.path.insert(0, sys.argv[1])
-sys.path.insert(0, sys.argv[1] + "/tests")
-from parity_util import pareto_factors
-from paper_2301_12584_b200 import KrpSampler
-shapes = [(int(a), int(b)) for a, b in (x.split("x") for x in sys.argv[3].split(","))]
-fs = pareto_factors(shapes, seed=int(sys.argv[4]), frac=0.01)
-s = KrpSampler(fs)
-out = {}
-for ex in (None, 0, len(shapes) - 1):
-    b = s.sample(ex, int(sys.argv[5]), seed=777, margin=True)
-    key = "none" if ex is None else str(ex)
-    out["idx_" + key] = b.indices
-    out["prob_" + key] = b.probabilities
-    out["rows_" + key] = b.rows
-    out["margin_" + key] = b.margin
-np.savez(sys.argv[2], **out)
-"""
+def draws(s, n_factors, J):
+    out = {}
+    for ex in (None, 0, n_factors - 1):
+        b = s.sample(ex, J, seed=777, margin=True)
+        key = "none" if ex is None else str(ex)
+        out["idx_" + key] = b.indices.copy()
+        out["prob_" + key] = b.probabilities.copy()
+        out["rows_" + key] = b.rows.copy()
+        out["margin_" + key] = b.margin.copy()
+    return out
 
 
-def run_variant(env_extra, shapes, seed, J):
-    fd, path = tempfile.mkstemp(suffix=".npz")
-    os.close(fd)
-    env = dict(os.environ)
-    env.update(env_extra)
-    spec = ",".join(f"{i}x{r}" for i, r in shapes)
-    subprocess.run([sys.executable, "-c", CHILD, ROOT, path, spec, str(seed), str(J)], env=env, check=True,
-                   timeout=600)
-    d = dict(np.load(path))
-    os.unlink(path)
-    return d
+def same(a, b, what):
+    for k, v in a.items():
+        assert np.array_equal(b[k], v), f"{what}: {k} differs"
 
 
 @pytest.mark.parametrize("shapes,J", [
@@ -62,17 +40,33 @@ def run_variant(env_extra, shapes, seed, J):
     ([(5000, 24), (3000, 24)], 4096),                     # non-power-of-two E-tree (parked leaves)
 ])
 def test_level_kernel_and_tables_bit_identical(shapes, J):
+    from paper_2301_12584_b200 import KrpSampler
+    s = KrpSampler(pareto_factors(shapes, seed=11, frac=0.01))
     # block_qf_packed order: the CTA kernel, the register-resident kernel, the tables
-    base = run_variant({"KRPG_EVAL_SPLIT": "0", "KRPG_EVAL_REG": "0", "KRPG_POS0_TABLES": "0"}, shapes, 11, J)
-    for extra in ({"KRPG_EVAL_SPLIT": "0", "KRPG_EVAL_REG": "1", "KRPG_POS0_TABLES": "0"},
-                  {"KRPG_EVAL_SPLIT": "0", "KRPG_EVAL_REG": "0", "KRPG_POS0_TABLES": "1"},
-                  {"KRPG_EVAL_SPLIT": "0"}):
-        got = run_variant(extra, shapes, 11, J)
-        for k, v in base.items():
-            assert np.array_equal(got[k], v), f"{extra}: {k} differs"
+    s.set_tuning(eval_split=0, eval_reg=0, pos0_tables=0)
+    base = draws(s, len(shapes), J)
+    for opts in ({"eval_reg": 1, "pos0_tables": 0}, {"eval_reg": 0, "pos0_tables": 1},
+                 {"eval_reg": 1, "pos0_tables": 1}, {"deep_threshold": 64}, {"deep_threshold": 16},
+                 {"deep_chunk": 32}, {"deep_chunk": 3}):
+        s.set_tuning(**opts)
+        same(base, draws(s, len(shapes), J), opts)
     # split order (R = 64: the Gram split over a CTA's warps): the split kernel on every
     # level vs the first-position tables computed in the same order
-    base = run_variant({"KRPG_EVAL_SPLIT": "1", "KRPG_POS0_TABLES": "0"}, shapes, 11, J)
-    got = run_variant({"KRPG_EVAL_SPLIT": "1"}, shapes, 11, J)
-    for k, v in base.items():
-        assert np.array_equal(got[k], v), f"split order with tables: {k} differs"
+    s.set_tuning(eval_reg=1, pos0_tables=0, deep_threshold=32, deep_chunk=8, eval_split=1)
+    base = draws(s, len(shapes), J)
+    s.set_tuning(pos0_tables=1)
+    same(base, draws(s, len(shapes), J), "split order with tables")
+    s.set_tuning(eval_split=16)
+    s.close()
+
+
+def test_tuning_option_errors():
+    from paper_2301_12584_b200 import KrpgInvalidArgument, KrpSampler
+    s = KrpSampler(pareto_factors([(300, 8), (200, 8)], seed=1))
+    with pytest.raises(KrpgInvalidArgument):
+        s.set_tuning(deep_chunk=0)
+    with pytest.raises(KrpgInvalidArgument):
+        s.set_tuning(eval_split=2)
+    with pytest.raises(KrpgInvalidArgument):
+        s.set_tuning(nonsense=1)
+    s.close()

@@ -352,6 +352,70 @@ def test_update_entries_match_sequential_reference_updates(I, R, n):
     assert_draws_match(b, ri, rp, rr, rm)
 
 
+@pytest.mark.parametrize("I,R,n", [(4096, 16, 3000), (70001, 64, 20000), (3001, 32, 1)])
+def test_per_entry_calls_queue_and_match_one_batch(I, R, n):
+    """update_factor_entry one call at a time (queued on the handle, applied before the next
+    read) gives the same bits as one update_factor_entries batch, run after run: the patch
+    is reduced bottom-up in a fixed order (no atomics), so trees, G and later draws are
+    reproducible; interleaved reads flush the queue in between."""
+    fs = pareto_factors([(I, R), (max(I // 3, 3), R)], seed=n)
+    rng = np.random.default_rng(n)
+    r = rng.integers(0, I, n).astype(np.uint64)
+    c = rng.integers(0, R, n).astype(np.uint32)
+    v = rng.standard_normal(n)
+    a, b, d = K()(fs), K()(fs), K()(fs)
+    for i in range(n):
+        a.update_factor_entry(0, int(r[i]), int(c[i]), float(v[i]))
+    b.update_factor_entries(0, r, c, v)
+    half = n // 2
+    d.update_factor_entries(0, r[:half], c[:half], v[:half])
+    _ = d.factor_gram(0)  # flush in between: two patches in sequence
+    d.update_factor_entries(0, r[half:], c[half:], v[half:])
+    ta, tb = a.tree_grams(0), b.tree_grams(0)
+    assert np.array_equal(ta, tb), "per-entry calls vs one batch: trees differ"
+    assert np.array_equal(a.factor_gram(0), b.factor_gram(0))
+    assert np.array_equal(a.factor(0), b.factor(0)) and np.array_equal(a.factor(0), d.factor(0))
+    o = oracle.OracleKrp(fs, "port")
+    o.update_entries(0, r, c, v)
+    L, nn = d.tree_shape(0)
+    for node in [0] + list(range(1, nn, 2))[:400]:
+        assert rel_err_matrix(d.node_gram(0, node), o.node_gram(0, node)) <= TOL
+    x, y = a.sample(None, 3000, 9, margin=True), b.sample(None, 3000, 9, margin=True)
+    assert np.array_equal(x.indices, y.indices) and np.array_equal(x.probabilities, y.probabilities)
+    ri, rp, rr, rm = o.sample(None, 3000, 9, want_margin=True)
+    assert_draws_match(x, ri, rp, rr, rm)
+
+
+def test_update_then_whole_factor_replacement_discards_nothing_wrongly():
+    """Queued entries followed by update_factor: the new factor wins (sequential semantics)."""
+    fs = pareto_factors([(2000, 16), (900, 16)], seed=4)
+    s = K()(fs)
+    s.update_factor_entry(0, 5, 3, 7.0)
+    unew = pareto_factors([(2100, 16)], seed=5)[0]
+    s.update_factor(0, unew)
+    assert np.array_equal(s.factor(0), unew)
+    assert rel_err_matrix(s.factor_gram(0), unew.T @ unew) <= TOL
+
+
+def test_invalid_update_factor_leaves_the_handle_untouched():
+    """update_factor validates before it mutates (krp_sampler.cpp:198-205): a non-finite
+    device factor is rejected and the old factor, tree and G stay in place."""
+    import torch
+    fs = pareto_factors([(3000, 16), (900, 16)], seed=6)
+    s = K()(fs)
+    g0, t0 = s.factor_gram(0), s.tree_grams(0)
+    bad = torch.tensor(pareto_factors([(3100, 16)], seed=7)[0], device="cuda")
+    bad[17, 3] = float("nan")
+    with pytest.raises(ValueError):
+        s.update_factor_device(0, bad)
+    assert np.array_equal(s.factor_gram(0), g0) and np.array_equal(s.tree_grams(0), t0)
+    assert np.array_equal(s.factor(0), fs[0])
+    with pytest.raises(ValueError):
+        s.update_factor_device(0, bad.float())  # wrong dtype for f64 storage
+    with pytest.raises(ValueError):
+        s.update_factor_device(0, torch.tensor(fs[0], device="cuda").t())  # not row-major
+
+
 def test_update_golden_sequence():
     g = golden()
     fu = [oracle.random_matrix(10, 3, 760 + j) for j in range(2)]

@@ -3,6 +3,7 @@
 //   usage: level_bench [J] [nruns]   (nruns: the draws are spread over that many node runs)
 // Variants: KRPG_EVAL_QUAD / KRPG_EVAL_REG select the kernel as in the library;
 // KRPG_FAKE_QF=1 skips the DMMA, =2 also the row / Gram loads (k_eval_reg only).
+#define KRPG_LEVEL_BENCH 1
 #include "../../paper_2301_12584_b200/csrc/descent_v2.cu"
 
 #include <cstdio>
@@ -102,7 +103,7 @@ int main(int argc, char** argv) {
         // level-l counters must start at zero (cntL of the parents is preset above)
         cudaMemsetAsync(cntL_d + first, 0, size_t(nruns) * 4, s);
         cudaEventRecord(e0, s);
-        dispatch_eval(R, EV_LEVEL, a, s, false);
+        dispatch_eval(R, EV_LEVEL, a, s, Tuning{}, false);
         cudaEventRecord(e1, s);
         cudaEventSynchronize(e1);
         float ms;
