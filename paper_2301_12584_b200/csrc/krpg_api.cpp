@@ -422,8 +422,40 @@ struct krpg_sampler {
         require(tr > 0.0, "KrpSampler: Khatri-Rao product is identically zero");
     }
 
+    // host destinations of krpg_sample: the grouped path copies the last position's
+    // draw slices out while the next slice computes (copy stream, stream-ordered events)
+    struct HostOut {
+        uint32_t* idx;
+        double *prob, *rows, *margin;
+        bool done;  // set by sample_device when it issued the copies itself
+    };
+    static bool pinned(const void* p) {
+        if (!p) return true;
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    }
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t out_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    void copy_out_slice(const HostOut& ho, uint64_t s0, uint64_t s1, const uint32_t* d_idx, const double* d_prob,
+                        const double* d_rows, const double* d_margin, int sl) {
+        if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+        if (!out_ev[sl]) CK(cudaEventCreateWithFlags(&out_ev[sl], cudaEventDisableTiming));
+        CK(cudaEventRecord(out_ev[sl], stream));
+        CK(cudaStreamWaitEvent(copy_stream, out_ev[sl], 0));
+        const uint64_t n = s1 - s0;
+        if (ho.idx) CK(cudaMemcpyAsync(ho.idx + s0 * N, d_idx + s0 * N, 4 * n * N, cudaMemcpyDeviceToHost, copy_stream));
+        if (ho.prob) CK(cudaMemcpyAsync(ho.prob + s0, d_prob + s0, 8 * n, cudaMemcpyDeviceToHost, copy_stream));
+        if (ho.rows) CK(cudaMemcpyAsync(ho.rows + s0 * R, d_rows + s0 * R, 8 * n * R, cudaMemcpyDeviceToHost, copy_stream));
+        if (ho.margin) CK(cudaMemcpyAsync(ho.margin + s0, d_margin + s0, 8 * n, cudaMemcpyDeviceToHost, copy_stream));
+    }
+
     void sample_device(int64_t excluded, uint64_t J, uint64_t seed, uint64_t off, uint32_t mode,
-                       uint32_t* d_idx, double* d_prob, double* d_rows, double* d_margin) {
+                       uint32_t* d_idx, double* d_prob, double* d_rows, double* d_margin,
+                       const HostOut* hout = nullptr) {
         require(J >= 1, "KrpSample: sample count must be positive");
         require(mode == KRPG_MODE_TWO_STAGE || mode == KRPG_MODE_ONE_STAGE, "krpg_sample: unknown mode");
         const auto trace_t0 = std::chrono::steady_clock::now();
@@ -576,6 +608,11 @@ struct krpg_sampler {
             }
             krpg::launch_fill(H, 1.0, J * R, stream);
             prof_launches[KRPG_PROF_OTHER] += 1;
+            // host outputs: the last position runs as SO draw slices one after the other,
+            // each slice's probabilities and D2H copies issued as soon as it is done, so
+            // all but the last slice's copies overlap the remaining compute
+            const int SO = (hout && S == 1 && J >= 16384) ? 2 : 1;
+            bool copied = false;
             for (size_t p = 0; p < npos; ++p) {
                 const uint32_t k = inc[p];
                 const double* blk = dsmall + P + p * per_pos;
@@ -593,6 +630,37 @@ struct krpg_sampler {
                 g.h_ones = p == 0 ? 1 : 0;  // H was just filled with ones
                 t0 = pbegin();
                 int nl = 0;
+                if (SO > 1 && p + 1 == npos) {
+                    for (int sl = 0; sl < SO; ++sl) {
+                        const uint64_t s0 = J * uint64_t(sl) / SO, s1 = J * uint64_t(sl + 1) / SO;
+                        krpg::GroupedArgs gs = g;
+                        gs.J = s1 - s0;
+                        gs.draw_offset = off + s0;
+                        gs.H = H + s0 * R;
+                        gs.Zb = g.Zb + s0 * R;
+                        gs.idx = d_idx ? d_idx + s0 * N : nullptr;
+                        gs.margin = d_margin ? d_margin + s0 : nullptr;
+                        gs.perm_a = g.perm_a + s0;
+                        gs.perm_b = g.perm_b + s0;
+                        gs.node = g.node + s0;
+                        gs.rank = g.rank + s0;
+                        gs.nsort_a = g.nsort_a + s0;
+                        gs.nsort_b = g.nsort_b + s0;
+                        gs.low = g.low + s0;
+                        gs.invc = g.invc + s0;
+                        gs.ud = g.ud + s0;
+                        nl += krpg::launch_position_grouped(gs);
+                        if (d_prob) {
+                            krpg::launch_probabilities_grouped(H + s0 * R, dsmall, R, s1 - s0, double(rank),
+                                                               d_prob + s0, stream);
+                            ++nl;
+                        }
+                        copy_out_slice(*hout, s0, s1, d_idx, d_prob, H, d_margin, sl);
+                    }
+                    copied = true;
+                    pend(KRPG_PROF_DRAWS, t0, nl);
+                    continue;
+                }
                 if (S > 1) CK(cudaEventRecord(fork_ev(), stream));
                 for (int sl = 0; sl < S; ++sl) {
                     const uint64_t s0 = J * uint64_t(sl) / S, s1 = J * uint64_t(sl + 1) / S;
@@ -629,10 +697,17 @@ struct krpg_sampler {
             }
             CK(cudaEventRecord(up_ev[slot], stream));
             se.valid = true;  // every position's operands are complete
-            if (d_prob) {
+            if (d_prob && !copied) {
                 cudaEvent_t t0 = pbegin();
                 krpg::launch_probabilities_grouped(H, dsmall, R, J, double(rank), d_prob, stream);
                 pend(KRPG_PROF_PROB, t0, 1);
+            }
+            if (hout && !copied) copy_out_slice(*hout, 0, J, d_idx, d_prob, H, d_margin, 0);
+            if (hout) {  // the call's stream joins the copies (sync mode waits for them below)
+                const_cast<HostOut*>(hout)->done = true;
+                if (!out_ev[3]) CK(cudaEventCreateWithFlags(&out_ev[3], cudaEventDisableTiming));
+                CK(cudaEventRecord(out_ev[3], copy_stream));
+                CK(cudaStreamWaitEvent(stream, out_ev[3], 0));
             }
             finish_call(derr);
             return;
@@ -1573,12 +1648,19 @@ int krpg_sample(krpg_t h, int64_t excluded, uint64_t J, uint64_t seed, uint64_t 
         double* dm = margin ? static_cast<double*>(h->sMargin.ensure(8 * J)) : nullptr;
         const bool trace = h->host_trace;
         const auto t0 = std::chrono::steady_clock::now();
-        h->sample_device(excluded, J, seed, draw_offset, mode, di, dp, dr, dm);
+        // page-locked destinations: the copies are pipelined with the last position's
+        // compute inside sample_device; pageable ones are copied after it
+        krpg_sampler::HostOut ho{idx, prob, rows, margin, false};
+        const bool pipe = krpg_sampler::pinned(idx) && krpg_sampler::pinned(prob) &&
+                          krpg_sampler::pinned(rows) && krpg_sampler::pinned(margin);
+        h->sample_device(excluded, J, seed, draw_offset, mode, di, dp, dr, dm, pipe ? &ho : nullptr);
         const auto t1 = std::chrono::steady_clock::now();
-        if (idx) CK(cudaMemcpyAsync(idx, di, 4 * J * h->N, cudaMemcpyDeviceToHost, h->stream));
-        if (prob) CK(cudaMemcpyAsync(prob, dp, 8 * J, cudaMemcpyDeviceToHost, h->stream));
-        if (rows) CK(cudaMemcpyAsync(rows, dr, 8 * J * h->R, cudaMemcpyDeviceToHost, h->stream));
-        if (margin) CK(cudaMemcpyAsync(margin, dm, 8 * J, cudaMemcpyDeviceToHost, h->stream));
+        if (!ho.done) {
+            if (idx) CK(cudaMemcpyAsync(idx, di, 4 * J * h->N, cudaMemcpyDeviceToHost, h->stream));
+            if (prob) CK(cudaMemcpyAsync(prob, dp, 8 * J, cudaMemcpyDeviceToHost, h->stream));
+            if (rows) CK(cudaMemcpyAsync(rows, dr, 8 * J * h->R, cudaMemcpyDeviceToHost, h->stream));
+            if (margin) CK(cudaMemcpyAsync(margin, dm, 8 * J, cudaMemcpyDeviceToHost, h->stream));
+        }
         h->sync_check();
         if (trace) {
             const auto t2 = std::chrono::steady_clock::now();

@@ -704,3 +704,39 @@ def test_config3_shape_call_matches_lazy_reference():
     c, n, nb = _stride_check(s, lz, None, J, 33, 512)
     print(f"config-3 shape call: checked {c} draws, {n} mismatches, {nb} boundary")
     s.close()
+
+
+@pytest.mark.parametrize("shapes,excluded", [([(1 << 16, 64), (40000, 64), (50000, 64)], None),
+                                             ([(30000, 32), (20000, 32)], 0),
+                                             ([(5000, 128), (7000, 128), (3000, 128)], 1)])
+def test_host_outputs_pipelined_match_device_outputs(shapes, excluded):
+    """krpg_sample into page-locked host buffers runs the last position as draw slices
+    whose copies overlap the remaining compute; the bits equal the device-output call
+    (no slicing) and a pageable-buffer call."""
+    import ctypes as C
+
+    import torch
+    from paper_2301_12584_b200 import _lib
+    fs = pareto_factors(shapes, seed=31, frac=0.01)
+    s = K()(fs)
+    J, N, R = 40000, len(shapes), shapes[0][1]
+    b = s.sample(excluded, J, 99, margin=True)  # pinned (torch caching host allocator)
+    idx = torch.empty(J, N, dtype=torch.int32, device="cuda")
+    prob = torch.empty(J, dtype=torch.float64, device="cuda")
+    rows = torch.empty(J, R, dtype=torch.float64, device="cuda")
+    mg = torch.empty(J, dtype=torch.float64, device="cuda")
+    s.sample_device(excluded, J, 99, idx, prob, rows, mg)
+    s.sync()
+    gi = idx.cpu().numpy().view(np.uint32)
+    if excluded is not None:
+        gi[:, excluded] = 0xFFFFFFFF
+    assert np.array_equal(b.indices, gi)
+    assert np.array_equal(b.probabilities, prob.cpu().numpy())
+    assert np.array_equal(b.rows, rows.cpu().numpy())
+    assert np.array_equal(b.margin, mg.cpu().numpy())
+    pi, pp, pr = np.empty((J, N), dtype=np.uint32), np.empty(J), np.empty((J, R))  # pageable
+    e = -1 if excluded is None else excluded
+    _lib.check(_lib.lib().krpg_sample(s.handle, e, J, 99, 0, 0, pi.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                      pp.ctypes.data_as(C.POINTER(C.c_double)),
+                                      pr.ctypes.data_as(C.POINTER(C.c_double)), None))
+    assert np.array_equal(pi, b.indices) and np.array_equal(pp, b.probabilities) and np.array_equal(pr, b.rows)
