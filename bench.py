@@ -187,8 +187,33 @@ def descent_bytes(idx, dims, R, excluded=None, elt=8):
     return total, per_pos
 
 
+DMMA_PEAK_TFLOPS = 37.0  # measured FP64 tensor (DMMA) peak on this pool's B200 (profiles/r01_fp64_peak_probe.txt)
+
+
+def one_stage_flops(idx, dims, R, excluded=None):
+    """Algorithmic FP64 flops of one one-stage step (north_star M = G+ o hh^T o G_{>k}):
+    per draw and included factor, one packed quadratic form R(R+1) per internal node on
+    its root-to-leaf path plus the normaliser, and per leaf row scanned up to the pick
+    (the reference's early exit, segment_tree_sampler.cpp:284-291) R (r o h) + R(R+1)."""
+    import numpy as np
+    total = 0
+    inc = [k for k in range(len(dims)) if excluded is None or k != excluded]
+    qf = R * (R + 1)
+    for k in inc:
+        I = dims[k]
+        L = (I + R - 1) // R
+        d = int(np.ceil(np.log2(L))) if L > 1 else 0
+        bottom = 2 * L - (1 << d)
+        t = idx[:, k].astype(np.int64)
+        leaf = t // R
+        depth = np.where(leaf < bottom, d, d - 1)
+        scanned = t - leaf * R + 1
+        total += int(((depth + 1) * qf).sum()) + int((scanned * (qf + R)).sum())
+    return total
+
+
 # ---------------------------------------------------------------- reference arm
-def cpu_reference_run(host_factors, J, seed, steps, warmup, keep=None):
+def cpu_reference_run(host_factors, J, seed, steps, warmup, keep=None, one_stage=False):
     """The reference's own CPU sampler (oracle/_ref: unmodified sources), all host cores.
     Returns (construction s, per-step seconds, reference handle if keep, last outputs)."""
     import oracle
@@ -198,17 +223,17 @@ def cpu_reference_run(host_factors, J, seed, steps, warmup, keep=None):
     s = oracle.OracleKrp(host_factors, "ref")
     build_s = time.perf_counter() - t0
     for i in range(warmup):
-        s.sample(None, J, seed + 100 + i)
+        s.sample(None, J, seed + 100 + i, one_stage=one_stage)
     times = []
     out = None
     for i in range(steps):
         t0 = time.perf_counter()
-        out = s.sample(None, J, seed + i)
+        out = s.sample(None, J, seed + i, one_stage=one_stage)
         times.append(time.perf_counter() - t0)
     return build_s, times, (s if keep else None), out
 
 
-def parity_against_reference(ref, ours, last_seed, J, N):
+def parity_against_reference(ref, ours, last_seed, J, N, one_stage=False):
     """Compare the timed call (and the exclude-one calls) with the reference's own
     KrpSampler::sample on the same factors and seeds (krp_sampler.cpp:82-151).
     `ours[e]` = (idx, prob, rows, margin, seed) host arrays of our call for exclusion e."""
@@ -222,7 +247,7 @@ def parity_against_reference(ref, ours, last_seed, J, N):
         if first is not None:
             ri, rp, rr = first
         else:
-            ri, rp, rr = ref.sample(None if e == "none" else int(e), J, sd)
+            ri, rp, rr = ref.sample(None if e == "none" else int(e), J, sd, one_stage=one_stage)
         n, nb, nu = compare_draws(gi, gm, ri)
         same = ~np.any(gi != ri, axis=1)
         pe = rel_err_vec(gp[same], rp[same])
@@ -248,7 +273,8 @@ def run_reference(args):
     fs = [f.cpu().numpy() for f in make_factors(args, dev)]
     torch.cuda.empty_cache() if torch.cuda.is_available() else None
     cores = os.cpu_count()
-    build_s, times, _, _ = cpu_reference_run(fs, args.J, args.seed, args.steps, args.warmup)
+    build_s, times, _, _ = cpu_reference_run(fs, args.J, args.seed, args.steps, args.warmup,
+                                             one_stage=args.mode == "one_stage")
     tot = sum(times)
     value = args.J * len(times) / tot
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
@@ -354,6 +380,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (draws) from this run's own paths ----
     idx_h = idx.cpu().numpy().view(np.uint32)
     bytes_step, _ = descent_bytes(idx_h, dims, R)
+    flops_step = one_stage_flops(idx_h, dims, R) if args.mode == "one_stage" else None
     draws_ms = prof["draws"]["ms"] / args.steps
     achieved = bytes_step / (draws_ms / 1e3) / 1e9
     share = prof["draws"]["ms"] / max(elapsed_ms, 1e-9)
@@ -428,14 +455,15 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             host = [f.cpu().numpy() for f in fs]
-            build_s, times, ref, out = cpu_reference_run(host, J, last_seed, steps=1, warmup=0, keep=True)
+            build_s, times, ref, out = cpu_reference_run(host, J, last_seed, steps=1, warmup=0, keep=True,
+                                                         one_stage=args.mode == "one_stage")
             cpu_base = {"value": J / times[0], "unit": "samples/s", "cores": os.cpu_count(),
                         "kind": "reference", "compile": REF_FLAGS,
                         "sample": f"one KrpSampler::sample(nullopt, J={J}) of the reference on the same "
                                   f"config-2 factors, all host cores (construction {build_s:.1f} s untimed)"}
             gi, gp, gr, gm, sd, _ = ours["none"]
             ours["none"] = (gi, gp, gr, gm, sd, out)
-            parity.update(parity_against_reference(ref, ours, last_seed, J, N))
+            parity.update(parity_against_reference(ref, ours, last_seed, J, N, one_stage=args.mode == "one_stage"))
             del ref
         except Exception as ex:  # reported, never silently substituted
             cpu_base = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "reference",
@@ -448,11 +476,17 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": bench_config(args, world),
             "issue": "asynchronous calls (KRPG_OPT_ASYNC): host setup overlaps the previous step's kernels",
-            "roofline": {"bound": "hbm", "kernel": "k_draws (batched root-to-leaf descent)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_kind": peak_kind,
-                         "alg_bytes_per_step": bytes_step, "kernel_ms_per_step": draws_ms,
-                         "kernel_share_of_step": share},
+            "roofline": ({"bound": "hbm", "kernel": "k_draws (batched root-to-leaf descent)",
+                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                          "traffic": traffic, "peak_kind": peak_kind,
+                          "alg_bytes_per_step": bytes_step, "kernel_ms_per_step": draws_ms,
+                          "kernel_share_of_step": share} if args.mode == "two_stage" else
+                         {"bound": "tensor", "kernel": "one-stage descent (k_eval_reg with B = G_v o Y, k_leaf_os)",
+                          "achieved": flops_step / (draws_ms / 1e3) / 1e12, "peak": DMMA_PEAK_TFLOPS,
+                          "unit": "TFLOP/s", "frac": flops_step / (draws_ms / 1e3) / 1e12 / DMMA_PEAK_TFLOPS,
+                          "traffic": None, "peak_kind": "measured FP64 DMMA (profiles/r01_fp64_peak_probe.txt)",
+                          "alg_flops_per_step": flops_step, "kernel_ms_per_step": draws_ms,
+                          "kernel_share_of_step": share, "hbm_alg_bytes_per_step": bytes_step}),
             "cpu_baseline": cpu_base,
             "parity": parity,
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,

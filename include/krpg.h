@@ -193,6 +193,12 @@ int krpg_set_option(krpg_t h, int option, int64_t value);
 typedef struct krpg_tensor* krpg_tensor_t;
 int krpg_tensor_create(const uint64_t* dims, uint32_t N, const uint32_t* coords, const double* values,
                        uint64_t nnz, int device, krpg_tensor_t* out);
+/* Same as krpg_tensor_create from device-resident COO arrays (nnz x N uint32 coordinates,
+ * nnz doubles, on `device`; read only, the caller keeps ownership). Coordinates are
+ * range-checked on the device; norm_sq is summed in a fixed blocked order (the host
+ * entry sums sequentially). For tensors too large to stage through host memory. */
+int krpg_tensor_create_device(const uint64_t* dims, uint32_t N, const uint32_t* d_coords, const double* d_values,
+                              uint64_t nnz, int device, krpg_tensor_t* out);
 int krpg_tensor_destroy(krpg_tensor_t t);
 int krpg_tensor_info(krpg_tensor_t t, uint64_t* nnz, double* norm_sq);
 /* deduplicated, sorted entries (host): coords nnz x N, values nnz (each nullable) */

@@ -87,6 +87,7 @@ _SIGS = {
     "krpg_finish_partitions": ([_vp, _u32, _u32, _vp], _int),
     "krpg_partition_rows": ([_u64, _u32, _u32, _u32, C.POINTER(_u64), C.POINTER(_u64)], _int),
     "krpg_tensor_create": ([C.POINTER(_u64), _u32, C.POINTER(_u32), _dp, _u64, _int, C.POINTER(_vp)], _int),
+    "krpg_tensor_create_device": ([C.POINTER(_u64), _u32, _vp, _vp, _u64, _int, C.POINTER(_vp)], _int),
     "krpg_tensor_destroy": ([_vp], _int),
     "krpg_tensor_info": ([_vp, C.POINTER(_u64), C.POINTER(C.c_double)], _int),
     "krpg_tensor_entries": ([_vp, C.POINTER(_u32), _dp], _int),

@@ -70,6 +70,7 @@ struct EvalArgs {
     uint32_t* nsort_out;       // node of each position of perm_out
     uint32_t* GS;           // per node position range [GS, GE) at its level
     uint32_t* GE;
+    const double* W;        // one-stage mode: packed Y = G_{>k}; node masses use G_v o Y (nullable)
 #ifdef KRPG_LEVEL_BENCH
     int fake;               // microbenchmark only (tools/microbench/level_bench.cu): 1 skip the DMMA, 2 also the loads
 #endif
@@ -342,8 +343,12 @@ __host__ __device__ constexpr int rfrag(int p, int s, int q) {
     return 2 * (p * NB - (p * (p - 1)) / 2) + s * (NB - p) + (q - p);
 }
 
-template <int NB>
-__device__ __forceinline__ void load_gram_frags(double (&gf)[NB * (NB + 1)], const double* __restrict__ G, int lane) {
+// WGT (one-stage mode, north_star's M = G+ o hh^T o G_{>k}): the B operand is the
+// elementwise product G_v o Y, so <G_v, hh^T o Y> = h^T (G_v o Y) h is the same
+// GEMM-shaped quadratic form over the draws' h rows (segment_tree_sampler.cpp:193-218)
+template <int NB, bool WGT = false>
+__device__ __forceinline__ void load_gram_frags(double (&gf)[NB * (NB + 1)], const double* __restrict__ G,
+                                                const double* __restrict__ W, int lane) {
     constexpr int R = 8 * NB;
     const int r4 = lane & 3, cq = lane >> 2;
 #pragma unroll
@@ -354,12 +359,13 @@ __device__ __forceinline__ void load_gram_frags(double (&gf)[NB * (NB + 1)], con
             const int col = 8 * p + cq;
             const int rowoff = row * R - (row * (row - 1)) / 2 - row;
             const int diag = row <= col ? rowoff + col : col * R - (col * (col - 1)) / 2 - col + row;
-            gf[rfrag<NB>(p, s, p)] = __ldg(G + diag);
+            gf[rfrag<NB>(p, s, p)] = WGT ? __ldg(G + diag) * __ldg(W + diag) : __ldg(G + diag);
             // off-diagonal tiles count twice (folded weights); a (2g) == (2a) g exactly, so
             // the doubling is applied once per run here instead of per block to the A fragment
 #pragma unroll
             for (int q = p + 1; q < NB; ++q) {
-                const double g = __ldg(G + rowoff + 8 * q + cq);
+                const double g = WGT ? __ldg(G + rowoff + 8 * q + cq) * __ldg(W + rowoff + 8 * q + cq)
+                                     : __ldg(G + rowoff + 8 * q + cq);
                 gf[rfrag<NB>(p, s, q)] = g + g;
             }
         }
@@ -410,7 +416,7 @@ __device__ __forceinline__ double block_qf_regs(const double (&gf)[NB * (NB + 1)
 // keep the FP64 tensor pipe busy; branch decisions, ranks, slot claims and the
 // next level's order are then computed for all of the warp's positions at once
 // (two per lane, run membership from ballot masks).
-template <int NB, int MODE, bool ROOT0>
+template <int NB, int MODE, bool ROOT0, bool WGT = false>
 __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t range) {
     constexpr int R = 8 * NB;
     constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
         const uint32_t v0 = __shfl_sync(FULL, vA, 0);
         if (EV_FAKE(a) < 2 && !parked(v0)) {
             const double* G = (LEVEL && !ROOT0) ? a.tree + slot_of(2ull * v0 + 1) * P : a.tree;
-            load_gram_frags<NB>(gf, G, lane);
+            load_gram_frags<NB, WGT>(gf, G, a.W, lane);
             gv_first = v0;
         }
     }
@@ -579,7 +585,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
             if (v != gv && EV_FAKE(a) < 2) {
                 const double* G = a.tree;
                 if (LEVEL && !root_pass) G = a.tree + slot_of(2ull * v + 1) * P;
-                load_gram_frags<NB>(gf, G, lane);
+                load_gram_frags<NB, WGT>(gf, G, a.W, lane);
                 gv = v;
             }
             if (EV_FAKE(a) < 2) {
@@ -2329,6 +2335,135 @@ __global__ void k_apply_pick(double* __restrict__ H, const T* __restrict__ U, co
 }
 
 // h-update grid: 8 warps per CTA, ~4 rows per warp
+// ---- one-stage leaf (general Y = G_{>k}), R <= 64 --------------------------
+// segment_masses' general branch (segment_tree_sampler.cpp:240-251) + the leaf scan
+// (:281-292): mass_i = (r_i o h)^T Y (r_i o h) for the rows of the draw's leaf, 8 rows
+// at a time as one DMMA quadratic-form block (block_qf_regs) with Y's B fragments
+// (off-diagonal doubled) held in registers for the whole kernel -- Y is the same for
+// every draw of the position -- and the rows (times h) staged in shared memory, the
+// next block's rows loaded into registers while the current block computes. The scan
+// runs the reference's sequential cum += inv_c * mass, first cum >= u wins, early exit.
+// Persistent warps take sorted positions (draws grouped by leaf) from a counter.
+struct LeafOsArgs {
+    uint64_t J;
+    uint32_t N, k;
+    const uint32_t* perm;
+    const uint32_t* node;
+    const double* low;
+    const double* invc;
+    const double* ud;
+    double* margin;
+    const double* H;
+    uint32_t* idx;
+    uint32_t* pick;
+    const void* U;
+    const double* W;
+    Topo topo;
+    uint32_t* work;
+};
+
+template <int NB>
+struct LeafOsCfg {
+    static constexpr int R = 8 * NB;
+    static constexpr int XS = RegCfg<NB>::XS;
+    static constexpr int PER = 8 * R / 32;  // staged elements per lane per block
+    static constexpr size_t WARP_DBL = size_t(8) * XS + R;
+    static constexpr size_t SMEM = RW * WARP_DBL * 8;
+};
+
+template <int NB, typename T>
+__global__ void __launch_bounds__(RW * 32, 2) k_leaf_os(LeafOsArgs a) {
+    constexpr int R = 8 * NB;
+    using C = LeafOsCfg<NB>;
+    extern __shared__ __align__(16) double smem_los[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    griddep_launch_dependents();
+    griddep_wait();
+    double* xs = smem_los + warp * C::WARP_DBL;
+    double* hs = xs + 8 * C::XS;
+    const T* U = static_cast<const T*>(a.U);
+    double gf[NB * (NB + 1)];
+    load_gram_frags<NB>(gf, a.W, nullptr, lane);
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(a.work, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= a.J) break;
+        const uint32_t d = a.perm[t];
+        const uint64_t v = a.node[d];
+        uint64_t f, l;
+        leaf_rows(a.topo, leaf_index(a.topo, v), &f, &l);
+        const double ic = a.invc[d], u = a.ud[d];
+        double cum = a.low[d];
+        double mg = a.margin ? a.margin[d] : HUGE_VAL;
+        for (int c = lane; c < R; c += 32) hs[c] = a.H[uint64_t(d) * R + c];
+        double cur[C::PER];
+        auto fetch = [&](uint64_t b0, double (&buf)[C::PER]) {
+#pragma unroll
+            for (int i = 0; i < C::PER; ++i) {
+                const int e = lane + 32 * i, m = e / R, c = e % R;
+                buf[i] = b0 + m < l ? static_cast<double>(U[(b0 + m) * R + c]) : 0.0;
+            }
+        };
+        fetch(f, cur);
+        __syncwarp();
+        uint64_t pick = ~uint64_t{0}, last_nz = ~uint64_t{0};
+        for (uint64_t b0 = f; b0 < l; b0 += 8) {
+#pragma unroll
+            for (int i = 0; i < C::PER; ++i) {
+                const int e = lane + 32 * i, m = e / R, c = e % R;
+                xs[m * C::XS + c] = cur[i] * hs[c];
+            }
+            if (b0 + 8 < l) fetch(b0 + 8, cur);
+            __syncwarp();
+            const double mass = block_qf_regs<NB, false>(gf, xs, true, lane);
+            const int n = int(l - b0 < 8 ? l - b0 : 8);
+            for (int j = 0; j < n; ++j) {
+                const double mj = __shfl_sync(0xffffffffu, mass, 4 * j);
+                const double m = ic * mj;
+                if (m > 0.0) last_nz = b0 + j;
+                cum += m;
+                mg = fmin(mg, fabs(cum - u));
+                if (cum >= u) {
+                    pick = b0 + j;
+                    break;
+                }
+            }
+            __syncwarp();
+            if (pick != ~uint64_t{0}) break;
+        }
+        if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : l - 1;
+        if (lane == 0) {
+            if (a.idx) a.idx[uint64_t(d) * a.N + a.k] = uint32_t(pick);
+            a.pick[d] = uint32_t(pick);
+            if (a.margin) a.margin[d] = mg;
+        }
+        __syncwarp();
+    }
+}
+
+template <int NB, typename T>
+void launch_leaf_os(const LeafOsArgs& a, cudaStream_t s) {
+    using C = LeafOsCfg<NB>;
+    const int occ = occupancy(k_leaf_os<NB, T>, RW * 32, C::SMEM);
+    const unsigned grid = unsigned(std::min<uint64_t>(uint64_t(sm_count_current()) * occ, (a.J + RW - 1) / RW));
+    launch_pdl(k_leaf_os<NB, T>, dim3(std::max(1u, grid)), dim3(RW * 32), C::SMEM, s, a);
+}
+
+template <typename T>
+void dispatch_leaf_os(uint32_t R, const LeafOsArgs& a, cudaStream_t s) {
+    switch (R / 8) {
+        case 1: return launch_leaf_os<1, T>(a, s);
+        case 2: return launch_leaf_os<2, T>(a, s);
+        case 3: return launch_leaf_os<3, T>(a, s);
+        case 4: return launch_leaf_os<4, T>(a, s);
+        case 5: return launch_leaf_os<5, T>(a, s);
+        case 6: return launch_leaf_os<6, T>(a, s);
+        case 7: return launch_leaf_os<7, T>(a, s);
+        default: return launch_leaf_os<8, T>(a, s);
+    }
+}
+
 inline unsigned apply_grid(uint64_t J) { return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((J + 31) / 32, 148ull * 16))); }
 
 unsigned grid_for(uint64_t n, unsigned block) {
@@ -2391,15 +2526,15 @@ void launch_stream(int mode, const EvalArgs& a, cudaStream_t s) {
         launch_stream_mode<NB, EV_LEVEL>(a, grid, s);
 }
 
-template <int NB, int MODE, bool ROOT0>
+template <int NB, int MODE, bool ROOT0, bool WGT = false>
 void launch_reg(const EvalArgs& a, cudaStream_t s) {
     using C = RegCfg<NB>;
-    const int slots = sm_count_current() * occupancy(k_eval_reg<NB, MODE, ROOT0>, RW * 32, C::SMEM) * RW;
+    const int slots = sm_count_current() * occupancy(k_eval_reg<NB, MODE, ROOT0, WGT>, RW * 32, C::SMEM) * RW;
     // one wave: the level's positions split evenly over the resident warps
     uint64_t range = (a.J + uint64_t(slots) - 1) / uint64_t(slots);
     range = std::min<uint64_t>(std::max<uint64_t>((range + 7) / 8 * 8, 8), RRANGE);
     const unsigned grid = unsigned((a.J + range * RW - 1) / (range * RW));
-    launch_pdl(k_eval_reg<NB, MODE, ROOT0>, dim3(grid), dim3(RW * 32), C::SMEM, s, a, uint32_t(range));
+    launch_pdl(k_eval_reg<NB, MODE, ROOT0, WGT>, dim3(grid), dim3(RW * 32), C::SMEM, s, a, uint32_t(range));
 }
 
 // Tuning::eval_split: 0 off, 1 R = 64 and 128, 16 (default) R = 128 only -- at R = 64 the
@@ -2416,6 +2551,12 @@ void launch_split(const EvalArgs& a, cudaStream_t s) {
 template <int NB>
 void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t, bool warp_variant) {
     const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
+    if constexpr (NB <= 8) {
+        if (a.W) {  // one-stage mode: every level on the register-resident kernel
+            if (mode == EV_LEVEL0) return launch_reg<NB, EV_LEVEL, true, true>(a, s);
+            if (mode == EV_LEVEL) return launch_reg<NB, EV_LEVEL, false, true>(a, s);
+        }
+    }
     if constexpr (NB == 8 || NB == 16) {
         if (eval_split_on(t, NB) && !warp_variant) {
             if (mode == EV_PROB) return launch_split<NB, EV_PROB, false>(a, s);
@@ -2571,12 +2712,85 @@ inline void dispatch_pos0_tables(uint32_t R, const double* Q, Topo te, const dou
 // level (both Gram buffers of a run fit in shared memory) + streaming leaf scan.
 // 160 < R <= 256 (R % 32 == 0): streamed-Gram level kernel + streaming leaf scan.
 bool grouped_supported(uint32_t R, uint32_t mode) {
+    if (mode == 1) return R % 8 == 0 && R >= 8 && R <= 64;  // one-stage: register-resident kernels
     return mode == 0 && R % 8 == 0 && R >= 8 && (R <= 160 || (R <= 256 && R % 32 == 0));
+}
+
+// One factor position of the one-stage draw (north_star (2)/(3): M = G+ o hh^T o G_{>k}
+// per draw, SURVEY 8(c) chain: counter p+1, general-Y tree walk + leaf). Every internal
+// level runs the node-grouped register-resident DMMA kernel with B = G_v o Y, then the
+// one-stage leaf kernel, then h o= U_k[pick]. Requires a tree of depth >= 1.
+static int launch_position_one_stage(const GroupedArgs& g) {
+    using namespace v2;
+    const uint32_t R = g.R;
+    const uint64_t J = g.J;
+    const unsigned gs = grid_for(J, 256);
+    const Topo tz = make_topo(g.I, R);
+    uint32_t* work = reinterpret_cast<uint32_t*>(g.pos0_tab);  // leaf-kernel counter (tables unused here)
+    launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
+               g.draw_offset, uint64_t(g.pos) + 1, g.margin, int(g.pos == 0), g.cntL, g.cntR, uint64_t(tz.n), work);
+    int launches = 1;
+    EvalArgs e{};
+    e.J = J;
+    e.node = g.node;
+    e.rank = g.rank;
+    e.low = g.low;
+    e.invc = g.invc;
+    e.ud = g.ud;
+    e.margin = g.margin;
+    e.cntL = g.cntL;
+    e.cntR = g.cntR;
+    e.err = g.err;
+    e.GS = g.gstart;
+    e.GE = g.gend;
+    e.X = g.H;
+    e.tree = g.Z;
+    e.topo = tz;
+    e.W = g.W;
+    uint32_t *pin = g.perm_a, *pout = g.perm_b, *nin = g.nsort_a, *nout = g.nsort_b;
+    for (uint32_t l = 0; l < tz.d; ++l) {
+        e.perm = l == 0 ? nullptr : pin;
+        e.perm_out = pout;
+        e.nsort_in = l == 0 ? nullptr : nin;
+        e.nsort_out = nout;
+        dispatch_eval(R, l == 0 ? EV_LEVEL0 : EV_LEVEL, e, g.stream, g.tune, false);
+        ++launches;
+        std::swap(pin, pout);
+        std::swap(nin, nout);
+    }
+    LeafOsArgs la{};
+    la.J = J;
+    la.N = g.N;
+    la.k = g.k;
+    la.perm = pin;
+    la.node = g.node;
+    la.low = g.low;
+    la.invc = g.invc;
+    la.ud = g.ud;
+    la.margin = g.margin;
+    la.H = g.H;
+    la.idx = g.idx;
+    la.pick = g.rank;  // rank[] is free after the last level
+    la.U = g.U;
+    la.W = g.W;
+    la.topo = tz;
+    la.work = work;
+    if (g.storage == 1) {
+        dispatch_leaf_os<float>(R, la, g.stream);
+        launch_pdl(k_apply_pick<float>, dim3(apply_grid(J)), dim3(256), 0, g.stream, g.H,
+                   static_cast<const float*>(g.U), (const uint32_t*)g.rank, J, R);
+    } else {
+        dispatch_leaf_os<double>(R, la, g.stream);
+        launch_pdl(k_apply_pick<double>, dim3(apply_grid(J)), dim3(256), 0, g.stream, g.H,
+                   static_cast<const double*>(g.U), (const uint32_t*)g.rank, J, R);
+    }
+    return launches + 2;
 }
 
 // One factor position of the two-stage draw, grouped version. Returns #launches.
 int launch_position_grouped(const GroupedArgs& g) {
     using namespace v2;
+    if (g.one_stage) return launch_position_one_stage(g);
     const uint32_t R = g.R;
     const uint64_t J = g.J;
     int launches = 0;

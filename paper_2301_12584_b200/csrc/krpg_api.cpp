@@ -558,7 +558,10 @@ struct krpg_sampler {
         }
         double* dQ = mode == KRPG_MODE_TWO_STAGE ? static_cast<double*>(Q.ensure(sizeof(double) * R * P)) : nullptr;
 
-        if (use_grouped && krpg::grouped_supported(R, mode)) {
+        bool grouped = use_grouped && krpg::grouped_supported(R, mode);
+        if (mode == KRPG_MODE_ONE_STAGE)  // the grouped one-stage path needs trees of depth >= 1
+            for (uint32_t k : inc) grouped = grouped && f[k].I > R;
+        if (grouped) {
             // ---- level-synchronous grouped descent (descent_v2.cu) ----
             uint64_t nmax = 2ull * R;
             for (uint32_t k : inc) nmax = std::max<uint64_t>(nmax, krpg::make_topo(f[k].I, R).n);
@@ -588,6 +591,7 @@ struct krpg_sampler {
             g.cntL = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
             g.cntR = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
             double* pos0_tab = reinterpret_cast<double*>(carve(8 * krpg::pos0_tab_doubles(R) * S));
+            g.pos0_tab = pos0_tab;
             g.Zb = static_cast<double*>(zbuf.ensure(sizeof(double) * J * R));
             g.R = R;
             g.N = N;
@@ -618,8 +622,12 @@ struct krpg_sampler {
                 const double* blk = dsmall + P + p * per_pos;
                 if (p > 0) stage_pos(p);
                 cudaEvent_t t0 = pbegin();
-                krpg::launch_etree_build(blk, blk + RR, f[k].tree.as<double>(), R, dQ, stream);
-                pend(KRPG_PROF_ETREE, t0, 1);
+                if (mode == KRPG_MODE_TWO_STAGE) {
+                    krpg::launch_etree_build(blk, blk + RR, f[k].tree.as<double>(), R, dQ, stream);
+                    pend(KRPG_PROF_ETREE, t0, 1);
+                }
+                g.one_stage = mode == KRPG_MODE_ONE_STAGE ? 1 : 0;
+                g.W = mode == KRPG_MODE_ONE_STAGE ? blk : nullptr;
                 g.k = k;
                 g.pos = uint32_t(p);
                 g.I = f[k].I;
@@ -1384,6 +1392,45 @@ int krpg_tensor_create(const uint64_t* dims, uint32_t N, const uint32_t* coords,
             double sq = 0.0;
             for (double x : vh) sq += x * x;
             t->norm_sq = sq;
+        }
+        *out = t.release();
+    });
+}
+
+int krpg_tensor_create_device(const uint64_t* dims, uint32_t N, const uint32_t* d_coords, const double* d_values,
+                              uint64_t nnz, int device, krpg_tensor_t* out) {
+    return guard([&] {
+        *out = nullptr;
+        require(N >= 1, "SparseTensorCoo: no dimensions");
+        require(N <= 8, "krpg_tensor_create: at most 8 modes on device");
+        for (uint32_t k = 0; k < N; ++k) require(dims[k] >= 1, "SparseTensorCoo: empty mode");
+        unsigned __int128 prod = 1;
+        for (uint32_t k = 0; k < N; ++k) prod *= dims[k];
+        require(prod <= (unsigned __int128)(~uint64_t{0}), "krpg_tensor_create: tensor index space exceeds 2^64");
+        require(nnz < (uint64_t{1} << 32), "krpg_tensor_create: more than 2^32 entries");
+        require(nnz == 0 || (d_coords && d_values), "krpg_tensor_create_device: null input");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, "krpg: no such CUDA device");
+        auto t = std::make_unique<krpg_tensor>();
+        t->device = device;
+        t->N = N;
+        t->dims.assign(dims, dims + N);
+        t->fib.resize(N);
+        t->fib_built.assign(N, false);
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+        if (nnz) {
+            // the caller's producer work is complete (legacy default stream semantics do
+            // not apply to our non-blocking stream)
+            CK(cudaDeviceSynchronize());
+            require(krpg::coords_in_range(d_coords, nnz, N, dims, t->stream), "SparseTensorCoo: coordinate out of range");
+            uint32_t* co = nullptr;
+            double* vo = nullptr;
+            t->nnz = krpg::tensor_ingest(d_coords, d_values, nnz, N, dims, &co, &vo, t->stream);
+            t->coords.p = co;
+            t->values.p = vo;
+            t->norm_sq = krpg::sum_of_squares(vo, t->nnz, t->stream);
         }
         *out = t.release();
     });

@@ -114,6 +114,8 @@ struct GroupedArgs {
     int h_ones;                        // H is all ones (first included position): table shortcut
     double* pos0_tab;                  // scratch for the first-position tables (pos0_tab_doubles(R)), nullable
     Tuning tune;
+    int one_stage;                     // mode 1: M = hh^T o Y on the factor tree directly
+    const double* W;                   // one-stage: packed Y = G_{>k} of this position (device)
 };
 // doubles of scratch the first-position tables need at rank R (E-tree masses, factor-tree
 // masses per (node, component) for the top levels, per-node counters)
@@ -182,6 +184,10 @@ size_t full_gram_work_doubles(uint32_t R);
 // ---- STS-CP solve slice (sts.cu; cp_als.cpp:282-313) ----
 // dedup + lexicographic sort of COO entries (tensor.cpp:34-75); returns nnz after
 // dedup, *_out allocated with cudaMalloc (caller frees)
+// device-resident COO input (krpg_tensor_create_device): every coordinate < its mode's
+// size; sum of squared values in a fixed, reproducible order
+bool coords_in_range(const uint32_t* d_coords, uint64_t nnz, uint32_t N, const uint64_t* dims, cudaStream_t s);
+double sum_of_squares(const double* d_v, uint64_t n, cudaStream_t s);
 uint64_t tensor_ingest(const uint32_t* d_coords, const double* d_vals, uint64_t nnz, uint32_t N, const uint64_t* dims,
                        uint32_t** d_coords_out, double** d_vals_out, cudaStream_t s);
 // fiber index of mode j (tensor.cpp:104-129): distinct keys, CSR offsets, and the

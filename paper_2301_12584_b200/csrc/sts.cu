@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <vector>
 #include <cmath>
 #include <stdexcept>
 #include <string>
@@ -385,14 +386,15 @@ uint64_t tensor_ingest(const uint32_t* d_coords, const double* d_vals, uint64_t 
         rx.stride[m] = st;
         st *= dims[m];
     }
-    uint64_t *key = nullptr, *key2 = nullptr, *ukey = nullptr, *nrun = nullptr;
+    // the unsorted keys' buffer is reused for the distinct keys (4 x 8 B per entry of scratch)
+    uint64_t *key = nullptr, *key2 = nullptr, *nrun = nullptr;
     double *val2 = nullptr, *uval = nullptr;
     STS_CK(cudaMallocAsync(&key, 8 * nnz, s));
     STS_CK(cudaMallocAsync(&key2, 8 * nnz, s));
     STS_CK(cudaMallocAsync(&val2, 8 * nnz, s));
-    STS_CK(cudaMallocAsync(&ukey, 8 * nnz, s));
     STS_CK(cudaMallocAsync(&uval, 8 * nnz, s));
     STS_CK(cudaMallocAsync(&nrun, 8, s));
+    uint64_t* ukey = key;
     k_linear_keys<<<grid_of(nnz), 256, 0, s>>>(d_coords, nnz, rx, key, nullptr);
     Scratch tmp;
     size_t need = 0;
@@ -410,10 +412,66 @@ uint64_t tensor_ingest(const uint32_t* d_coords, const double* d_vals, uint64_t 
     k_decode<<<grid_of(n), 256, 0, s>>>(ukey, n, rx, *d_coords_out);
     STS_CK(cudaMemcpyAsync(*d_vals_out, uval, 8 * n, cudaMemcpyDeviceToDevice, s));
     for (void* p : {static_cast<void*>(key), static_cast<void*>(key2), static_cast<void*>(val2),
-                    static_cast<void*>(ukey), static_cast<void*>(uval), static_cast<void*>(nrun)})
+                    static_cast<void*>(uval), static_cast<void*>(nrun)})
         STS_CK(cudaFreeAsync(p, s));
     STS_CK(cudaStreamSynchronize(s));
     return n;
+}
+
+// ---- device-resident input: coordinate range check, sum of squares ----
+__global__ void k_check_coords(const uint32_t* __restrict__ coords, uint64_t nnz, uint32_t N, Radix lim,
+                               int* __restrict__ bad) {
+    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < nnz * N;
+         e += uint64_t(gridDim.x) * blockDim.x)
+        if (coords[e] >= lim.stride[e % N]) atomicExch(bad, 1);
+}
+
+constexpr int kNormBlocks = 1184;
+// per-block partial sums over a fixed contiguous split (block b sums [b*chunk, ...) in
+// thread-strided order + a fixed tree), so the total is run-to-run reproducible
+__global__ void __launch_bounds__(256) k_sumsq_partials(const double* __restrict__ v, uint64_t n,
+                                                        double* __restrict__ part) {
+    const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t b0 = blockIdx.x * chunk, b1 = b0 + chunk < n ? b0 + chunk : n;
+    double acc = 0.0;
+    for (uint64_t e = b0 + threadIdx.x; e < b1; e += blockDim.x) acc = fma(v[e], v[e], acc);
+    __shared__ double red[256];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (int(threadIdx.x) < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+bool coords_in_range(const uint32_t* d_coords, uint64_t nnz, uint32_t N, const uint64_t* dims, cudaStream_t s) {
+    Radix lim{};
+    lim.N = N;
+    for (uint32_t m = 0; m < N; ++m) lim.stride[m] = dims[m];
+    int* bad = nullptr;
+    STS_CK(cudaMallocAsync(&bad, sizeof(int), s));
+    STS_CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    if (nnz) k_check_coords<<<grid_of(nnz * N), 256, 0, s>>>(d_coords, nnz, N, lim, bad);
+    int h = 0;
+    STS_CK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    STS_CK(cudaFreeAsync(bad, s));
+    STS_CK(cudaStreamSynchronize(s));
+    return h == 0;
+}
+
+double sum_of_squares(const double* d_v, uint64_t n, cudaStream_t s) {
+    if (!n) return 0.0;
+    double* part = nullptr;
+    STS_CK(cudaMallocAsync(&part, 8 * kNormBlocks, s));
+    k_sumsq_partials<<<kNormBlocks, 256, 0, s>>>(d_v, n, part);
+    std::vector<double> h(kNormBlocks);
+    STS_CK(cudaMemcpyAsync(h.data(), part, 8 * kNormBlocks, cudaMemcpyDeviceToHost, s));
+    STS_CK(cudaFreeAsync(part, s));
+    STS_CK(cudaStreamSynchronize(s));
+    double t = 0.0;
+    for (double x : h) t += x;
+    return t;
 }
 
 // ---- fiber index of mode j ----

@@ -35,6 +35,26 @@ class SparseTensor:
     def from_entries(cls, dims, coords, values, device: int = 0) -> "SparseTensor":
         return cls(dims, coords, values, device)
 
+    @classmethod
+    def from_device(cls, dims, coords, values, device: int = 0) -> "SparseTensor":
+        """From torch CUDA tensors (coords nnz x N int32/uint32, values nnz float64) without
+        staging through host memory (krpg_tensor_create_device); inputs are only read."""
+        import torch
+        from ._lib import KrpgInvalidArgument
+        from .sampler import _dev_tensor
+        self = cls.__new__(cls)
+        self.dims = [int(d) for d in dims]
+        N = len(self.dims)
+        nnz = int(values.shape[0])
+        if coords.dim() != 2 or int(coords.shape[1]) != N or int(coords.shape[0]) != nnz:
+            raise KrpgInvalidArgument("SparseTensorCoo: coords/values mismatch")
+        pc = _dev_tensor(coords, "coords", coords.dtype if coords.dtype in (torch.int32,) else torch.int32, device)
+        pv = _dev_tensor(values, "values", torch.float64, device)
+        self._h = C.c_void_p()
+        dims_c = (C.c_uint64 * N)(*self.dims)
+        check(_lib.lib().krpg_tensor_create_device(dims_c, N, pc, pv, nnz, device, C.byref(self._h)))
+        return self
+
     def ndim(self) -> int:
         return len(self.dims)
 

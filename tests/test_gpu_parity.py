@@ -112,7 +112,8 @@ CASES = [
 
 @pytest.mark.parametrize("shapes,seed", CASES)
 @pytest.mark.parametrize("mode,descent", [("two_stage", "grouped"), ("two_stage", "grouped_unfused"),
-                                          ("two_stage", "per_draw"), ("one_stage", "per_draw")])
+                                          ("two_stage", "per_draw"), ("one_stage", "per_draw"),
+                                          ("one_stage", "grouped")])
 def test_sample_bit_exact_against_oracle(shapes, seed, mode, descent):
     """KrpSampler::sample (two-stage, krp_sampler.cpp:82-151) and the one-stage
     M = G+ o hh^T o G_{>k} chain, every exclusion setting, through both descent
@@ -740,3 +741,28 @@ def test_host_outputs_pipelined_match_device_outputs(shapes, excluded):
                                       pp.ctypes.data_as(C.POINTER(C.c_double)),
                                       pr.ctypes.data_as(C.POINTER(C.c_double)), None))
     assert np.array_equal(pi, b.indices) and np.array_equal(pp, b.probabilities) and np.array_equal(pr, b.rows)
+
+
+def test_device_tensor_ingestion_matches_host_ingestion():
+    """krpg_tensor_create_device (inputs already in HBM) == krpg_tensor_create
+    (SparseTensorCoo::from_entries semantics): same deduplicated sorted entries, norm
+    within rounding; out-of-range coordinates rejected on the device."""
+    import torch
+    from paper_2301_12584_b200 import KrpgInvalidArgument, SparseTensor
+    rng = np.random.default_rng(12)
+    dims = [700, 300, 90]
+    nnz = 200_000
+    coords = np.stack([rng.integers(0, d, nnz) for d in dims], axis=1).astype(np.uint32)
+    coords[: nnz // 3] = coords[nnz // 3: 2 * (nnz // 3)]  # duplicates
+    vals = rng.standard_normal(nnz)
+    Th = SparseTensor(dims, coords, vals)
+    Td = SparseTensor.from_device(dims, torch.tensor(coords.astype(np.int32), device="cuda"),
+                                  torch.tensor(vals, device="cuda"))
+    ch, vh = Th.entries()
+    cd, vd = Td.entries()
+    assert np.array_equal(ch, cd) and np.array_equal(vh, vd)
+    assert abs(Th.norm_squared() - Td.norm_squared()) <= 1e-12 * Th.norm_squared()
+    bad = coords.astype(np.int32).copy()
+    bad[5, 2] = 90
+    with pytest.raises(KrpgInvalidArgument):
+        SparseTensor.from_device(dims, torch.tensor(bad, device="cuda"), torch.tensor(vals, device="cuda"))
