@@ -183,6 +183,9 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
 #define KRPG_OPT_EVAL_SPLIT 20
 #define KRPG_OPT_DEEP_DMMA_MIN 21
 #define KRPG_OPT_LEAF_PAR 22
+/* krpg_sample into page-locked host buffers: the last position runs as this many draw
+ * slices, each copied out while the next computes (default 2, 1..4; same bits) */
+#define KRPG_OPT_OUT_SLICES 23
 int krpg_set_option(krpg_t h, int option, int64_t value);
 
 /* ---- STS-CP solve slice ----

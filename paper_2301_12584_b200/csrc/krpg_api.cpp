@@ -439,7 +439,7 @@ struct krpg_sampler {
         return a.type == cudaMemoryTypeHost;
     }
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t out_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t out_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // [0..3] slices, [4] join
     void copy_out_slice(const HostOut& ho, uint64_t s0, uint64_t s1, const uint32_t* d_idx, const double* d_prob,
                         const double* d_rows, const double* d_margin, int sl) {
         if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
@@ -615,7 +615,7 @@ struct krpg_sampler {
             // host outputs: the last position runs as SO draw slices one after the other,
             // each slice's probabilities and D2H copies issued as soon as it is done, so
             // all but the last slice's copies overlap the remaining compute
-            const int SO = (hout && S == 1 && J >= 16384) ? 2 : 1;
+            const int SO = (hout && S == 1 && J >= 16384) ? std::max(1, std::min(4, tune.out_slices)) : 1;
             bool copied = false;
             for (size_t p = 0; p < npos; ++p) {
                 const uint32_t k = inc[p];
@@ -713,9 +713,9 @@ struct krpg_sampler {
             if (hout && !copied) copy_out_slice(*hout, 0, J, d_idx, d_prob, H, d_margin, 0);
             if (hout) {  // the call's stream joins the copies (sync mode waits for them below)
                 const_cast<HostOut*>(hout)->done = true;
-                if (!out_ev[3]) CK(cudaEventCreateWithFlags(&out_ev[3], cudaEventDisableTiming));
-                CK(cudaEventRecord(out_ev[3], copy_stream));
-                CK(cudaStreamWaitEvent(stream, out_ev[3], 0));
+                if (!out_ev[4]) CK(cudaEventCreateWithFlags(&out_ev[4], cudaEventDisableTiming));
+                CK(cudaEventRecord(out_ev[4], copy_stream));
+                CK(cudaStreamWaitEvent(stream, out_ev[4], 0));
             }
             finish_call(derr);
             return;
@@ -2137,6 +2137,9 @@ int krpg_set_option(krpg_t h, int option, int64_t value) {
         } else if (option == KRPG_OPT_DEEP_DMMA_MIN) {
             require(value >= 1 && value <= 64, "krpg_set_option: deep DMMA minimum must be in [1, 64]");
             h->tune.deep_dmma_min = int(value);
+        } else if (option == KRPG_OPT_OUT_SLICES) {
+            require(value >= 1 && value <= 4, "krpg_set_option: output slices must be in [1, 4]");
+            h->tune.out_slices = int(value);
         } else if (option == KRPG_OPT_LEAF_PAR) {
             require(value >= 0 && value <= 64, "krpg_set_option: leaf scan parallel bound must be in [0, 64]");
             h->tune.leaf_par = int(value);

@@ -26,6 +26,7 @@ struct TreeBuildArgs {
     uint32_t parts = 1;  // > 1: build only subtree `part` of `parts` (a power of two)
     uint32_t part = 0;
     double* subroot = nullptr;  // partitioned build: receives the subtree root Gram (P)
+    int leaf_variant = 0;       // reserved (leaf-kernel variants were measured and removed)
 };
 // doubles needed for (tbuf_a, tbuf_b)
 void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b, uint64_t F = 0, uint64_t nleaves = 0);
@@ -90,6 +91,8 @@ struct Tuning {
     int eval_split = 16;       // split-Gram level kernel: 16 = R 128 only, 1 = R 64 and 128, 0 = off
     int deep_dmma_min = 1;     // deep-pass runs with fewer draws use CUDA-core forms
     int leaf_par = 8;          // leaf runs with at most this many draws scan warp-parallel
+    int out_slices = 2;        // krpg_sample into page-locked host memory: draw slices of the
+                               // last position whose copies overlap the following slices (1..4)
 };
 
 struct GroupedArgs {

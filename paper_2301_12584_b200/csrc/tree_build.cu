@@ -10,9 +10,10 @@
 //    tile set in registers: after the left leaf's rows the accumulators are the
 //    left leaf's Gram (stored: it is a left child), after the right leaf's rows
 //    they are the parent's Gram. So the first reduction level costs nothing.
-//  * k_level_reduce: the remaining levels, coalesced packed sums level by level
-//    (parent = left + right, :180-186), writing only the stored nodes (root and
-//    left children, :142) into the compact array.
+//  * k_subtree_reduce: the remaining levels, up to 5 per pass: a block owns a
+//    subtree, each thread one packed entry of all its nodes (parent = left + right,
+//    :180-186), writing only the stored nodes (root and left children, :142) into
+//    the compact array; the transient position level is read once.
 //  * k_leaf_generic: scalar fallback for ranks the DMMA path does not cover.
 #include <algorithm>
 #include <cstdio>
@@ -78,12 +79,14 @@ PosGeom make_geom(uint64_t I, uint32_t R, uint64_t F = 0, uint64_t nleaves = 0, 
     return g;
 }
 
-template <int NB, typename T>
+// MINB resident CTAs of WPC warps per SM (register budget 64K / (MINB * WPC * 32)),
+// STAGES-deep TMA ring per warp
+template <int NB, typename T, int MINB = 2, int STAGES_ = 4>
 struct LeafCfg {
     static constexpr int R = 8 * NB;
     static constexpr int NT = NB * (NB + 1) / 2;  // upper-triangle 8x8 tiles
     static constexpr int CH = 8;                  // rows per TMA chunk (2 k-steps)
-    static constexpr int STAGES = 4;
+    static constexpr int STAGES = STAGES_;
     static constexpr int ROWB = R * int(sizeof(T));
     static constexpr int RS = ROWB + 16;  // padded row stride: conflict-free fragment reads
     static constexpr int CHB = CH * RS;
@@ -144,11 +147,11 @@ __device__ __forceinline__ void store_tiles(const double (&acc)[NB * (NB + 1) / 
     }
 }
 
-template <int NB, typename T>
-__global__ void __launch_bounds__(LeafCfg<NB, T>::WPC * 32)
+template <int NB, typename T, int MINB = 2, int STAGES = 4>
+__global__ void __launch_bounds__(LeafCfg<NB, T, MINB, STAGES>::WPC * 32, MINB)
     k_leaf_dmma(const T* __restrict__ U, PosGeom g, double* __restrict__ compact,
                 double* __restrict__ tout) {
-    using C = LeafCfg<NB, T>;
+    using C = LeafCfg<NB, T, MINB, STAGES>;
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* ring = smem + warp * (C::STAGES * C::CHB);
@@ -462,17 +465,63 @@ __global__ void k_level_reduce(const double* __restrict__ child, double* __restr
     }
 }
 
+// K levels at once (:180-186, parent = left + right in the same order as k_level_reduce,
+// so the tree is bit-identical): block b owns the subtree of 2^K consecutive child-level
+// nodes under parent-level-(c-K) node j0 + b; thread e reads packed entry e of all 2^K
+// children (2^K independent loads in flight, coalesced across the warp), sums pairs K
+// times in registers, writes every stored node's entry, and the subtree root's entry to
+// `top` (next pass's child level; null at the root). One pass replaces K launches and
+// reads the transient level once.
+template <int K>
+__global__ void __launch_bounds__(256) k_subtree_reduce(const double* __restrict__ child, double* __restrict__ top,
+                                                        double* __restrict__ compact, uint32_t c, uint64_t j0,
+                                                        uint64_t nj, uint64_t P) {
+    constexpr int W = 1 << K;
+    const uint64_t j = j0 + blockIdx.x;  // parent-level (c - K) relative index
+    if (j >= nj) return;
+    for (uint64_t e = threadIdx.x; e < P; e += blockDim.x) {
+        double v[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) v[i] = child[(j * W + i) * P + e];
+#pragma unroll
+        for (int l = 1; l <= K; ++l) {
+            const uint32_t lev = c - l;  // level of the nodes formed now
+#pragma unroll
+            for (int i = 0; i < (W >> l); ++i) {
+                v[i] = v[2 * i] + v[2 * i + 1];
+                const uint64_t node = ((uint64_t{1} << lev) - 1) + (j << (K - l)) + i;
+                if (stored(node)) compact[slot_of(node) * P + e] = v[i];
+            }
+        }
+        if (top) top[j * P + e] = v[0];
+    }
+}
+
+template <int K>
+void launch_subtree(const double* child, double* top, double* compact, uint32_t c, uint64_t j0, uint64_t nj,
+                    uint64_t P, cudaStream_t s) {
+    k_subtree_reduce<K><<<unsigned(nj - j0), 256, 0, s>>>(child, top, compact, c, j0, nj, P);
+}
+
 int sm_count() { return sm_count_current(); }
 
-template <int NB, typename T>
-void launch_dmma(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s) {
-    using C = LeafCfg<NB, T>;
-    auto kern = k_leaf_dmma<NB, T>;
+template <int NB, typename T, int MINB, int STAGES>
+void launch_dmma_v(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s) {
+    using C = LeafCfg<NB, T, MINB, STAGES>;
+    auto kern = k_leaf_dmma<NB, T, MINB, STAGES>;
     smem_optin(kern, C::SMEM);
     const int occ = occupancy(kern, C::WPC * 32, C::SMEM);
     const uint64_t need = (g.p1 - g.p0 + C::WPC - 1) / C::WPC;
     const uint64_t grid = std::min<uint64_t>(need, uint64_t(sm_count()) * occ);
     kern<<<unsigned(grid), C::WPC * 32, C::SMEM, s>>>(U, g, compact, tout);
+}
+
+// 2 CTAs x 4 warps per SM with 4-stage rings: forcing 3 CTAs (168 registers, 3 stages) or
+// 4 CTAs (128 registers, 2 stages) spills accumulators and measured 1.59 / 2.71 ms per
+// config-2 leaf build against 1.19 ms (profiles/r02_tree_variants.jsonl)
+template <int NB, typename T>
+void launch_dmma(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s, int) {
+    launch_dmma_v<NB, T, 2, 4>(U, g, compact, tout, s);
 }
 
 template <int R_, typename T>
@@ -487,7 +536,7 @@ void launch_big(const T* U, const PosGeom& g, double* compact, double* tout, cud
 
 template <typename T>
 void launch_leaf(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s,
-                 bool generic) {
+                 bool generic, int variant) {
     if (g.F % 8 != 0 || g.seg) generic = true;  // the DMMA kernels stream uniform leaves in 8-row chunks
     if (!generic) {
         switch (g.R) {
@@ -497,14 +546,14 @@ void launch_leaf(const T* U, const PosGeom& g, double* compact, double* tout, cu
             case 192: return launch_big<192, T>(U, g, compact, tout, s);
             case 224: return launch_big<224, T>(U, g, compact, tout, s);
             case 256: return launch_big<256, T>(U, g, compact, tout, s);
-            case 8: return launch_dmma<1, T>(U, g, compact, tout, s);
-            case 16: return launch_dmma<2, T>(U, g, compact, tout, s);
-            case 24: return launch_dmma<3, T>(U, g, compact, tout, s);
-            case 32: return launch_dmma<4, T>(U, g, compact, tout, s);
-            case 40: return launch_dmma<5, T>(U, g, compact, tout, s);
-            case 48: return launch_dmma<6, T>(U, g, compact, tout, s);
-            case 56: return launch_dmma<7, T>(U, g, compact, tout, s);
-            case 64: return launch_dmma<8, T>(U, g, compact, tout, s);
+            case 8: return launch_dmma<1, T>(U, g, compact, tout, s, variant);
+            case 16: return launch_dmma<2, T>(U, g, compact, tout, s, variant);
+            case 24: return launch_dmma<3, T>(U, g, compact, tout, s, variant);
+            case 32: return launch_dmma<4, T>(U, g, compact, tout, s, variant);
+            case 40: return launch_dmma<5, T>(U, g, compact, tout, s, variant);
+            case 48: return launch_dmma<6, T>(U, g, compact, tout, s, variant);
+            case 56: return launch_dmma<7, T>(U, g, compact, tout, s, variant);
+            case 64: return launch_dmma<8, T>(U, g, compact, tout, s, variant);
             default: break;
         }
     }
@@ -541,9 +590,11 @@ int launch_tree_leaves(const TreeBuildArgs& a) {
     }
     double* tout = g.npos > 1 ? a.tbuf_a : nullptr;
     if (a.storage == 1)
-        launch_leaf<float>(static_cast<const float*>(a.U), g, a.compact, tout, a.stream, a.force_generic);
+        launch_leaf<float>(static_cast<const float*>(a.U), g, a.compact, tout, a.stream, a.force_generic,
+                           a.leaf_variant);
     else
-        launch_leaf<double>(static_cast<const double*>(a.U), g, a.compact, tout, a.stream, a.force_generic);
+        launch_leaf<double>(static_cast<const double*>(a.U), g, a.compact, tout, a.stream, a.force_generic,
+                            a.leaf_variant);
     return 1;
 }
 
@@ -559,16 +610,25 @@ int launch_tree_levels(const TreeBuildArgs& a) {
     double* cur = a.tbuf_a;
     double* nxt = a.tbuf_b;
     int launches = 0;
-    for (int l = int(D) - 1; l >= int(gl); --l) {
+    // passes of up to 5 levels each (k_subtree_reduce): level c -> c - k
+    for (int c = int(D); c > int(gl);) {
+        const int k = std::min(5, c - int(gl));
+        const int l = c - k;  // parent level of this pass
         const uint64_t nj = uint64_t{1} << l;
-        const uint64_t span = nj >> gl;  // nodes of this level per partition
+        const uint64_t span = nj >> gl;
         const uint64_t j0 = a.parts > 1 ? uint64_t(a.part) * span : 0;
         const uint64_t j1 = a.parts > 1 ? j0 + span : nj;
-        double* parent = (l > 0) ? nxt : nullptr;
-        const unsigned grid = unsigned(std::min<uint64_t>(j1 - j0, uint64_t(sm_count()) * 8));
-        k_level_reduce<<<grid, 256, 0, a.stream>>>(cur, parent, a.compact, j0, j1, g.P, nj - 1);
+        double* parent = (l > 0 || a.parts > 1) ? nxt : nullptr;
+        switch (k) {
+            case 1: launch_subtree<1>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
+            case 2: launch_subtree<2>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
+            case 3: launch_subtree<3>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
+            case 4: launch_subtree<4>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
+            default: launch_subtree<5>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
+        }
         ++launches;
         std::swap(cur, nxt);
+        c = l;
     }
     if (a.parts > 1 && a.subroot) {  // cur holds level gl
         if (cudaMemcpyAsync(a.subroot, cur + uint64_t(a.part) * g.P, sizeof(double) * g.P,
