@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     const uint64_t p0 = (uint64_t(blockIdx.x) * RW + warp) * range;
     if (p0 >= a.J) return;
     const int cnt = int(a.J - p0 < uint64_t(range) ? a.J - p0 : uint64_t(range));
-    unsigned long long* tr = a.trace ? a.trace + ((uint64_t(blockIdx.x) * RW + warp) * 8) : nullptr;
+    unsigned long long* tr = a.trace ? a.trace + ((uint64_t(blockIdx.x) * RW + warp) * 16) : nullptr;
     if (tr && lane == 0) tr[0] = gtimer();
     double* ring = reinterpret_cast<double*>(smem_regb + warp * C::WARP_STRIDE);
     double* s_u = ring + RSLOTS * C::SLOT;
@@ -495,6 +495,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
             gv_first = v0;
         }
     }
+    if (tr && lane == 0) tr[8] = gtimer();
     // block 0's rows (positions [0, min(8, first run end))) requested right away as well
     bool pre0 = false;
     {
@@ -510,6 +511,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
             pre0 = true;
         }
     }
+    if (tr && lane == 0) tr[9] = gtimer();
     // decision inputs of every position and the parents' ranges of every run: one group
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -537,6 +539,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
         }
     }
     cp_async_commit();
+    if (tr && lane == 0) tr[10] = gtimer();
 
     // block list: (b0, n) of every 8-draw block of every non-parked run
     int nblk = 0;
@@ -618,6 +621,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     };
     cp_async_wait_all();  // decision inputs (needed by the root pass only for the error check: none)
     __syncwarp();
+    if (tr && lane == 0) tr[11] = gtimer();
     if (ROOT0) {
         sweep(true, gv_first);
         sweep(false, 0xFFFFFFFFu);
@@ -1858,6 +1862,8 @@ struct DeepArgs {
     int leaf_par;      // leaf runs with at most this many draws scan warp-parallel
     int dmma_min;      // internal-level runs with at least this many draws use DMMA
     uint32_t* work;    // chunk counter (zeroed before the launch) for persistent warps, nullable
+    int final_rows;    // apply h o= U_k[pick] here (last position of a host-output call)
+    double* host_rows; // with final_rows: the call's page-locked host rows (device-mapped), nullable
 };
 
 
@@ -2286,6 +2292,51 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
             if (a.margin) a.margin[d] = mg;
             if (a.idx) a.idx[uint64_t(d) * a.N + a.k] = uint32_t(pick);
             a.pick[d] = uint32_t(pick);
+        }
+    }
+    if (a.final_rows) {
+        // last position of a host-output call (krp_sampler.cpp:137-138): the chunk's final
+        // rows h o= U_k[pick] are formed here and stored to HBM and, over PCIe, straight into
+        // the caller's page-locked rows, so the 33.5 MB output copy overlaps the deep pass
+        // instead of following it
+        __syncwarp();
+        const unsigned own = __ballot_sync(0xffffffffu, live);
+        constexpr int CPL = (R + 31) / 32;
+        for (unsigned mm = own; mm;) {
+            uint32_t dd[8];
+            uint64_t pk[8];
+            int nd = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int src = mm ? __ffs(mm) - 1 : 0;
+                dd[q] = __shfl_sync(0xffffffffu, d, src);
+                pk[q] = __shfl_sync(0xffffffffu, pick, src);
+                if (mm) {
+                    mm &= mm - 1;
+                    nd = q + 1;
+                }
+            }
+            double hv[8][CPL], uv[8][CPL];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int cc = 0; cc < CPL; ++cc) {
+                    const int c = lane + 32 * cc;
+                    const bool ok = q < nd && c < R;
+                    hv[q][cc] = ok ? a.H[uint64_t(dd[q]) * R + c] : 0.0;
+                    uv[q][cc] = ok ? static_cast<double>(U[pk[q] * R + c]) : 0.0;
+                }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int cc = 0; cc < CPL; ++cc) {
+                    const int c = lane + 32 * cc;
+                    if (q < nd && c < R) {
+                        const double x = hv[q][cc] * uv[q][cc];
+                        a.H[uint64_t(dd[q]) * R + c] = x;
+                        if (a.host_rows) a.host_rows[uint64_t(dd[q]) * R + c] = x;
+                    }
+                }
         }
     }
     }  // chunk loop
@@ -2933,12 +2984,15 @@ int launch_position_grouped(const GroupedArgs& g) {
         da.work = deep_work;
         da.dmma_min = g.tune.deep_dmma_min;
         da.leaf_par = g.tune.leaf_par;
+        da.final_rows = g.final_rows;
+        da.host_rows = g.host_rows;
         const unsigned grid = unsigned((J + uint64_t(da.chunk) * WPB - 1) / (uint64_t(da.chunk) * WPB));
         if (g.storage == 1)
             dispatch_deep<float>(R, da, grid, g.stream);
         else
             dispatch_deep<double>(R, da, grid, g.stream);
         mark(12);
+        if (g.final_rows) return launches + 1;  // h o= U_k[pick] done in the deep pass
         if (g.storage == 1)
             launch_pdl(k_apply_pick<float>, dim3(apply_grid(J)), dim3(256), 0, g.stream, g.H,
                        static_cast<const float*>(g.U), (const uint32_t*)g.rank, J, R);

@@ -441,7 +441,7 @@ struct krpg_sampler {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t out_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // [0..3] slices, [4] join
     void copy_out_slice(const HostOut& ho, uint64_t s0, uint64_t s1, const uint32_t* d_idx, const double* d_prob,
-                        const double* d_rows, const double* d_margin, int sl) {
+                        const double* d_rows, const double* d_margin, int sl, bool rows_done = false) {
         if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
         if (!out_ev[sl]) CK(cudaEventCreateWithFlags(&out_ev[sl], cudaEventDisableTiming));
         CK(cudaEventRecord(out_ev[sl], stream));
@@ -449,7 +449,8 @@ struct krpg_sampler {
         const uint64_t n = s1 - s0;
         if (ho.idx) CK(cudaMemcpyAsync(ho.idx + s0 * N, d_idx + s0 * N, 4 * n * N, cudaMemcpyDeviceToHost, copy_stream));
         if (ho.prob) CK(cudaMemcpyAsync(ho.prob + s0, d_prob + s0, 8 * n, cudaMemcpyDeviceToHost, copy_stream));
-        if (ho.rows) CK(cudaMemcpyAsync(ho.rows + s0 * R, d_rows + s0 * R, 8 * n * R, cudaMemcpyDeviceToHost, copy_stream));
+        if (ho.rows && !rows_done)
+            CK(cudaMemcpyAsync(ho.rows + s0 * R, d_rows + s0 * R, 8 * n * R, cudaMemcpyDeviceToHost, copy_stream));
         if (ho.margin) CK(cudaMemcpyAsync(ho.margin + s0, d_margin + s0, 8 * n, cudaMemcpyDeviceToHost, copy_stream));
     }
 
@@ -615,7 +616,16 @@ struct krpg_sampler {
             // host outputs: the last position runs as SO draw slices one after the other,
             // each slice's probabilities and D2H copies issued as soon as it is done, so
             // all but the last slice's copies overlap the remaining compute
-            const int SO = (hout && S == 1 && J >= 16384) ? std::max(1, std::min(4, tune.out_slices)) : 1;
+            // host rows written by the last deep pass itself (fused path), else output slices
+            double* mapped_rows = nullptr;
+            if (hout && hout->rows && S == 1 && mode == KRPG_MODE_TWO_STAGE && R <= 64 && fused_deep &&
+                !(prof_on && prof_detail)) {
+                if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped_rows), hout->rows, 0) != cudaSuccess) {
+                    cudaGetLastError();
+                    mapped_rows = nullptr;
+                }
+            }
+            const int SO = (hout && S == 1 && J >= 16384 && !mapped_rows) ? std::max(1, std::min(4, tune.out_slices)) : 1;
             bool copied = false;
             for (size_t p = 0; p < npos; ++p) {
                 const uint32_t k = inc[p];
@@ -636,6 +646,8 @@ struct krpg_sampler {
                 g.Z = f[k].tree.as<double>();
                 g.U = f[k].U.p;
                 g.h_ones = p == 0 ? 1 : 0;  // H was just filled with ones
+                g.final_rows = (mapped_rows && p + 1 == npos) ? 1 : 0;
+                g.host_rows = g.final_rows ? mapped_rows : nullptr;
                 t0 = pbegin();
                 int nl = 0;
                 if (SO > 1 && p + 1 == npos) {
@@ -710,7 +722,7 @@ struct krpg_sampler {
                 krpg::launch_probabilities_grouped(H, dsmall, R, J, double(rank), d_prob, stream);
                 pend(KRPG_PROF_PROB, t0, 1);
             }
-            if (hout && !copied) copy_out_slice(*hout, 0, J, d_idx, d_prob, H, d_margin, 0);
+            if (hout && !copied) copy_out_slice(*hout, 0, J, d_idx, d_prob, H, d_margin, 0, mapped_rows != nullptr);
             if (hout) {  // the call's stream joins the copies (sync mode waits for them below)
                 const_cast<HostOut*>(hout)->done = true;
                 if (!out_ev[4]) CK(cudaEventCreateWithFlags(&out_ev[4], cudaEventDisableTiming));

@@ -117,6 +117,8 @@ struct GroupedArgs {
     int h_ones;                        // H is all ones (first included position): table shortcut
     double* pos0_tab;                  // scratch for the first-position tables (pos0_tab_doubles(R)), nullable
     Tuning tune;
+    int final_rows;                    // fused deep pass forms h o= U_k[pick] itself (no k_apply_pick)
+    double* host_rows;                 // with final_rows: device-mapped page-locked output rows, nullable
     int one_stage;                     // mode 1: M = hh^T o Y on the factor tree directly
     const double* W;                   // one-stage: packed Y = G_{>k} of this position (device)
 };

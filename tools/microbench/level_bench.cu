@@ -85,7 +85,7 @@ int main(int argc, char** argv) {
     a.GE = static_cast<uint32_t*>(up(GE.data(), nn * 4));
     const char* f = std::getenv("KRPG_FAKE_QF");
     a.fake = f ? std::atoi(f) : 0;
-    const size_t ntr = (J / 8 + 64) * 8;
+    const size_t ntr = (J / 8 + 64) * 16;
     cudaMalloc(&a.trace, ntr * 8);
     cudaMemset(a.trace, 0, ntr * 8);
     // counters of this level's nodes are reset before every launch (memset not timed)
@@ -118,17 +118,26 @@ int main(int argc, char** argv) {
         std::vector<unsigned long long> tr(ntr);
         cudaMemcpy(tr.data(), a.trace, ntr * 8, cudaMemcpyDeviceToHost);
         unsigned long long t0min = ~0ull, t0max = 0, t5max = 0;
-        double ph[5] = {0, 0, 0, 0, 0}, f6 = 0, f7 = 0;
+        double ph[5] = {0, 0, 0, 0, 0}, f6 = 0, f7 = 0, g8 = 0, g9 = 0, g10 = 0, g2 = 0, g11 = 0;
+        int ng = 0;
         int n67 = 0;
         int nw = 0;
-        for (size_t w = 0; w * 8 < ntr; ++w) {
-            const unsigned long long* t = &tr[w * 8];
+        for (size_t w = 0; w * 16 < ntr; ++w) {
+            const unsigned long long* t = &tr[w * 16];
             if (!t[0] || !t[5]) continue;
             ++nw;
             t0min = std::min(t0min, t[0]);
             t0max = std::max(t0max, t[0]);
             t5max = std::max(t5max, t[5]);
             for (int k = 0; k < 5; ++k) ph[k] += double(t[k + 1] - t[k]);
+            if (t[8] && t[9] && t[10] && t[11]) {
+                g8 += double(t[8] - t[1]);
+                g9 += double(t[9] - t[8]);
+                g10 += double(t[10] - t[9]);
+                g2 += double(t[2] - t[10]);
+                g11 += double(t[11] - t[2]);
+                ++ng;
+            }
             if (t[6] && t[7]) {
                 f6 += double(t[6] - t[2]);
                 f7 += double(t[7] - t[6]);
@@ -140,6 +149,9 @@ int main(int argc, char** argv) {
                         "sweep %.2f, claims %.2f, scatter %.2f us\n",
                         nw, (t5max - t0min) * 1e-3, (t0max - t0min) * 1e-3, ph[0] / nw * 1e-3, ph[1] / nw * 1e-3,
                         ph[2] / nw * 1e-3, ph[3] / nw * 1e-3, ph[4] / nw * 1e-3);
+        if (ng) std::printf("  list phase: gram issue %.2f, block-0 rows %.2f, cp.async inputs %.2f, block list %.2f, "
+                            "inputs wait %.2f us\n", g8 / ng * 1e-3, g9 / ng * 1e-3, g10 / ng * 1e-3, g2 / ng * 1e-3,
+                            g11 / ng * 1e-3);
         if (n67) std::printf("  first block: gram + rows ready %.2f us after the list, its DMMA chain %.2f us\n", f6 / n67 * 1e-3, f7 / n67 * 1e-3);
     }
     std::vector<uint32_t> po(J);
