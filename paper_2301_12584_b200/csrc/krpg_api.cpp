@@ -191,6 +191,8 @@ struct krpg_sampler {
         std::vector<double> gp;
         std::vector<std::vector<double>> Y;
         std::vector<krpg::Eig> ye;
+        DevBuf etrees;         // two-stage: the E-tree of every position (npos x R x P), same validity
+        bool etrees_ok = false;
     };
     std::map<std::pair<int64_t, uint32_t>, SetupEntry> setup_cache;
     DevBuf patchbuf;
@@ -474,6 +476,7 @@ struct krpg_sampler {
         std::vector<std::future<krpg::Eig>> fut(npos);
         if (!hit) {
             se.valid = false;
+            se.etrees_ok = false;
             se.grams.clear();
             for (uint32_t k : inc) se.grams.push_back(f[k].G);
             const std::vector<double> G = hadamard_of(inc);
@@ -632,9 +635,12 @@ struct krpg_sampler {
                 const double* blk = dsmall + P + p * per_pos;
                 if (p > 0) stage_pos(p);
                 cudaEvent_t t0 = pbegin();
-                if (mode == KRPG_MODE_TWO_STAGE) {
-                    krpg::launch_etree_build(blk, blk + RR, f[k].tree.as<double>(), R, dQ, stream);
-                    pend(KRPG_PROF_ETREE, t0, 1);
+                if (mode == KRPG_MODE_TWO_STAGE) {  // E-trees are cached with the setup
+                    dQ = static_cast<double*>(se.etrees.ensure(sizeof(double) * npos * R * P)) + p * size_t(R) * P;
+                    if (!se.etrees_ok) {
+                        krpg::launch_etree_build(blk, blk + RR, f[k].tree.as<double>(), R, dQ, stream);
+                        pend(KRPG_PROF_ETREE, t0, 1);
+                    }
                 }
                 g.one_stage = mode == KRPG_MODE_ONE_STAGE ? 1 : 0;
                 g.W = mode == KRPG_MODE_ONE_STAGE ? blk : nullptr;
@@ -717,6 +723,7 @@ struct krpg_sampler {
             }
             CK(cudaEventRecord(up_ev[slot], stream));
             se.valid = true;  // every position's operands are complete
+            if (mode == KRPG_MODE_TWO_STAGE) se.etrees_ok = true;
             if (d_prob && !copied) {
                 cudaEvent_t t0 = pbegin();
                 krpg::launch_probabilities_grouped(H, dsmall, R, J, double(rank), d_prob, stream);
@@ -1596,6 +1603,11 @@ int krpg_destroy(krpg_t h) {
         if (h->up_ev[i]) cudaEventDestroy(h->up_ev[i]);
     }
     h->errh.release();
+    h->patchbuf.release();
+    for (auto& kv : h->setup_cache) kv.second.etrees.release();
+    for (cudaEvent_t e : h->out_ev)
+        if (e) cudaEventDestroy(e);
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
