@@ -187,6 +187,8 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
  * slices, each copied out while the next computes (default 2, 1..4; same bits) */
 #define KRPG_OPT_OUT_SLICES 23
 int krpg_set_option(krpg_t h, int option, int64_t value);
+/* 1 for the bounds-checked library (make CHECKED=1, device asserts), 0 for production */
+int krpg_is_checked_build(void);
 
 /* ---- STS-CP solve slice ----
  * A device-resident sparse tensor: SparseTensorCoo::from_entries (tensor.cpp:34-75)

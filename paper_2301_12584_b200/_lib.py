@@ -12,7 +12,9 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "lib", "libkrpg.so")
+# KRPG_LIB_VARIANT=checked selects the bounds-checked build (make CHECKED=1, tests only)
+LIB_PATH = os.path.join(PKG, "lib", "libkrpg_checked.so" if os.environ.get("KRPG_LIB_VARIANT") == "checked"
+                        else "libkrpg.so")
 HEADER = os.path.join(ROOT, "include", "krpg.h")
 
 KRPG_OK = 0
@@ -80,6 +82,7 @@ _SIGS = {
     "krpg_topology_node_rows": ([_u64, _u64, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64),
                                  C.POINTER(_u64)], _int),
     "krpg_host_eigh": ([_dp, _u32, _dp, _dp], _int),
+    "krpg_is_checked_build": ([], _int),
     "krpg_set_option": ([_vp, _int, _i64], _int),
     "krpg_tree_device": ([_vp, _u32, C.POINTER(_vp), C.POINTER(_u64)], _int),
     "krpg_factor_device": ([_vp, _u32, C.POINTER(_vp)], _int),

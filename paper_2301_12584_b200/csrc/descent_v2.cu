@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     {
         const uint32_t v0 = __shfl_sync(FULL, vA, 0);
         if (EV_FAKE(a) < 2 && !parked(v0)) {
+            KRPG_DCHECK(!(LEVEL && !ROOT0) || (v0 < a.topo.n && slot_of(2ull * v0 + 1) < a.topo.L));
             const double* G = (LEVEL && !ROOT0) ? a.tree + slot_of(2ull * v0 + 1) * P : a.tree;
             load_gram_frags<NB, WGT>(gf, G, a.W, lane);
             gv_first = v0;
@@ -557,6 +558,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
         }
     }
     __syncwarp();
+    KRPG_DCHECK(nblk <= RMAXBLK && nruns <= RRANGE && cnt <= RRANGE);
     if (tr && lane == 0) tr[2] = gtimer();
 
     uint32_t phase = 0;  // bit sl: parity of slot sl's next completion
@@ -565,7 +567,9 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
         const uint32_t e = s_blk[i];
         const int b0 = e & 0xff, n = e >> 8;
         const int sl = i % RSLOTS;
+        KRPG_DCHECK(n >= 1 && n <= 8 && b0 + n <= cnt);
         const uint32_t dr = pos_d(b0 + (lane & 7) < cnt ? b0 + (lane & 7) : b0);
+        KRPG_DCHECK(dr < a.J || a.perm == nullptr);
         if (lane == 0) {
             fence_proxy_async();
             mbar_arrive_expect_tx(&bar[sl], uint32_t(n) * R * 8);
@@ -588,6 +592,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
             if (v != gv && EV_FAKE(a) < 2) {
                 const double* G = a.tree;
                 if (LEVEL && !root_pass) G = a.tree + slot_of(2ull * v + 1) * P;
+                KRPG_DCHECK(!(LEVEL && !root_pass) || (v < a.topo.n && slot_of(2ull * v + 1) < a.topo.L));
                 load_gram_frags<NB, WGT>(gf, G, a.W, lane);
                 gv = v;
             }
@@ -712,6 +717,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
                 const uint64_t before = bits(int(s_rs[r]), t);
                 const uint32_t pos = lf[h] ? s_bl[r] + __popcll(static_cast<long long>(Lm & before))
                                            : s_br[r] - __popcll(static_cast<long long>(Rm & before));
+                KRPG_DCHECK(pos < a.J && 2ull * v + 2 < a.topo.n);
                 a.perm_out[pos] = d;
                 if (a.nsort_out) a.nsort_out[pos] = 2 * v + (lf[h] ? 1u : 2u);
             }
@@ -2014,6 +2020,7 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
             const uint32_t vr = __shfl_sync(0xffffffffu, v, rs);
             if (is_leaf(a.topo, vr)) continue;
             {  // stage this run's Gram, warm L2 with the next one
+                KRPG_DCHECK(vr < a.topo.n && slot_of(2ull * vr + 1) < a.topo.L);
                 const double* g = a.tree + slot_of(2ull * vr + 1) * P;
                 if (lane == 0) {  // one bulk copy (TMA) of the packed Gram
                     fence_proxy_async();
@@ -2130,9 +2137,11 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
         st &= st - 1;
         const int re = st ? __ffs(st) - 1 : cnt;
         const uint32_t vr = __shfl_sync(0xffffffffu, v, rs);
+        KRPG_DCHECK(vr < a.topo.n && is_leaf(a.topo, vr));
         const uint64_t l = leaf_index(a.topo, vr);
         const uint64_t first = l * a.topo.F;
         const uint64_t last = first + a.topo.F < a.topo.I ? first + a.topo.F : a.topo.I;
+        KRPG_DCHECK(l < a.topo.L && first < last && last <= a.topo.I);
         const bool in_run = lane >= rs && lane < re;
         // z fragments of the run's first 8-draw block, loaded once for all its chunks
         double zfirst[2 * NB];
@@ -2290,6 +2299,7 @@ __global__ void __launch_bounds__(WPB * 32) k_deep2(DeepArgs a) {
         if (in_run) {
             if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : last - 1;
             if (a.margin) a.margin[d] = mg;
+            KRPG_DCHECK(pick >= first && pick < last && d < a.J);
             if (a.idx) a.idx[uint64_t(d) * a.N + a.k] = uint32_t(pick);
             a.pick[d] = uint32_t(pick);
         }
@@ -2441,9 +2451,12 @@ __global__ void __launch_bounds__(RW * 32, 2) k_leaf_os(LeafOsArgs a) {
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= a.J) break;
         const uint32_t d = a.perm[t];
+        KRPG_DCHECK(d < a.J);
         const uint64_t v = a.node[d];
+        KRPG_DCHECK(v < a.topo.n && is_leaf(a.topo, v));
         uint64_t f, l;
         leaf_rows(a.topo, leaf_index(a.topo, v), &f, &l);
+        KRPG_DCHECK(f < l && l <= a.topo.I);
         const double ic = a.invc[d], u = a.ud[d];
         double cum = a.low[d];
         double mg = a.margin ? a.margin[d] : HUGE_VAL;
@@ -2484,6 +2497,7 @@ __global__ void __launch_bounds__(RW * 32, 2) k_leaf_os(LeafOsArgs a) {
             if (pick != ~uint64_t{0}) break;
         }
         if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : l - 1;
+        KRPG_DCHECK(pick >= f && pick < l);
         if (lane == 0) {
             if (a.idx) a.idx[uint64_t(d) * a.N + a.k] = uint32_t(pick);
             a.pick[d] = uint32_t(pick);

@@ -2185,6 +2185,14 @@ int krpg_topology_node_rows(uint64_t I, uint64_t F, uint64_t v, uint64_t* first,
     });
 }
 
+int krpg_is_checked_build(void) {
+#ifdef KRPG_CHECKED
+    return 1;
+#else
+    return 0;
+#endif
+}
+
 int krpg_host_eigh(const double* G, uint32_t n, double* vectors, double* values) {
     return guard([&] {
         const krpg::Eig e = krpg::eigh_psd(G, n);

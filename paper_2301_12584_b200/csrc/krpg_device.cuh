@@ -6,6 +6,20 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Checked build (make CHECKED=1 -> lib/libkrpg_checked.so): bounds / invariant checks on
+// the kernels' index arithmetic (node ids, stored slots, row ranges, sorted positions,
+// ring and block-list capacity). A failed check traps the kernel through a device-side
+// assert, so the call returns a CUDA error; the production build compiles them away.
+// This stands in for compute-sanitizer's memcheck, which is closed on the GPU pool.
+#ifdef KRPG_CHECKED
+#include <cassert>
+#define KRPG_DCHECK(cond) assert(cond)
+#else
+#define KRPG_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 namespace krpg {
 
 // ---------------------------------------------------------------------------

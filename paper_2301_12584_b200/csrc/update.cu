@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(256) k_patch_level(double* __restrict__ compac
     if (w >= nitems) return;
     const PatchItem it = items[w];
     const uint64_t P = uint64_t(R) * (R + 1) / 2;
+    KRPG_DCHECK(it.re >= it.rb && (it.re > it.rb || it.lc >= 0 || it.rc >= 0));
     double* out = dcur + w * P;
     double* g = stored(it.node) ? compact + slot_of(it.node) * P : nullptr;
     if (it.re > it.rb) {  // leaf: its touched rows in ascending order
