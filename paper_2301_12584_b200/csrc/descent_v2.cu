@@ -1494,119 +1494,6 @@ __global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a) {
     }
 }
 
-// Per-warp variant for deep levels (runs of a few draws, Grams read once from
-// HBM): B fragments gathered straight from global memory per block, the next
-// run's Gram prefetched into L2 while this run computes, and all runs' child
-// slots claimed with one warp-wide round of atomics at the end.
-template <int NB>
-__global__ void __launch_bounds__(WPB * 32) k_eval_warp(EvalArgs a) {
-    constexpr int R = 8 * NB;
-    constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
-    const int lane = threadIdx.x & 31;
-    const uint64_t base = (uint64_t(blockIdx.x) * WPB + (threadIdx.x >> 5)) * CHUNK;
-    if (base >= a.J) return;
-    const int cnt = a.J - base < uint64_t(CHUNK) ? int(a.J - base) : CHUNK;
-    const bool live = lane < cnt;
-    const uint32_t dl = live ? a.perm[base + lane] : 0u;
-    const uint32_t vl = live ? a.node[dl] : 0xFFFFFFFFu;
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, vl, 1);
-    const uint32_t starts0 = __ballot_sync(0xffffffffu, live && (lane == 0 || vl != prev));
-    const FragAddr<NB> fa(lane);
-    uint32_t leftm = 0, movedm = 0;
-    uint32_t starts = starts0;
-    while (starts) {
-        const int rs = __ffs(starts) - 1;
-        starts &= starts - 1;
-        const int re = starts ? __ffs(starts) - 1 : cnt;
-        const uint32_t v = __shfl_sync(0xffffffffu, vl, rs);
-        if (is_leaf(a.topo, v)) continue;
-        if (starts) {  // warm L2 with the next run's Gram (prefetch.global.L2)
-            const uint32_t vn = __shfl_sync(0xffffffffu, vl, __ffs(starts) - 1);
-            if (!is_leaf(a.topo, vn)) {
-                const char* gn = reinterpret_cast<const char*>(a.tree + slot_of(2ull * vn + 1) * P);
-                for (uint32_t o = lane * 128; o < P * 8; o += 32 * 128)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(gn + o));
-            }
-        }
-        const double* G = a.tree + slot_of(2ull * v + 1) * P;
-        for (int b0 = rs; b0 < re; b0 += 8) {
-            const int n = min(8, re - b0);
-            const int m = lane >> 2;
-            const bool valid = m < n;
-            const uint32_t dd = __shfl_sync(0xffffffffu, dl, (b0 + m) & 31);
-            const double mass = block_qf_packed<NB>(G, fa, valid ? a.X + uint64_t(dd) * R : nullptr, lane);
-            const bool owner = valid && (lane & 3) == 0;
-            bool left = false;
-            if (owner) {
-                const double u = a.ud[dd];
-                const double cutoff = a.low[dd] + a.invc[dd] * mass;
-                left = cutoff >= u;
-                if (a.margin) a.margin[dd] = fmin(a.margin[dd], fabs(cutoff - u));
-                a.node[dd] = left ? 2 * v + 1 : 2 * v + 2;
-                if (!left) a.low[dd] = cutoff;
-            }
-            const unsigned lm = __ballot_sync(0xffffffffu, owner && left);
-#pragma unroll
-            for (int mm = 0; mm < 8; ++mm)
-                if (mm < n) leftm |= ((lm >> (4 * mm)) & 1u) << (b0 + mm);
-            movedm |= (n == 32 ? 0xffffffffu : ((1u << n) - 1u)) << b0;
-        }
-    }
-    // one round of atomics for every run of the warp, then slots
-    if (live && ((movedm >> lane) & 1u)) {
-        const uint32_t le = starts0 & ((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
-        const int rs = 31 - __clz(le);
-        const uint32_t gt = starts0 & ~((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
-        const int re = gt ? __ffs(gt) - 1 : cnt;
-        const uint32_t runm = (re == 32 ? 0xffffffffu : ((1u << re) - 1u)) & ~((1u << rs) - 1u);
-        const bool left = (leftm >> lane) & 1u;
-        const uint32_t side = (left ? leftm : (movedm & ~leftm)) & runm;
-        uint32_t bl = 0, br = 0;
-        if (lane == rs) {
-            const uint32_t nl = __popc(leftm & runm), nr = __popc(movedm & ~leftm & runm);
-            if (nl) bl = atomicAdd(a.cntL + vl, nl);
-            if (nr) br = atomicAdd(a.cntR + vl, nr);
-        }
-        const unsigned mv = __activemask();
-        bl = __shfl_sync(mv, bl, rs);
-        br = __shfl_sync(mv, br, rs);
-        a.rank[dl] = (left ? bl : br) + __popc(side & ((1u << lane) - 1u));
-    }
-}
-
-// perm_out for the next level (draws that moved to depth l+1 take their slot in
-// the child run; draws parked at a leaf one level up keep their position).
-__global__ void k_scatter(const uint32_t* __restrict__ perm_in, uint32_t* __restrict__ perm_out,
-                          const uint32_t* __restrict__ node, const uint32_t* __restrict__ rank,
-                          uint32_t* __restrict__ gstart, const uint32_t* __restrict__ cntL, uint64_t J,
-                          uint32_t first_next) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < J; i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t d = perm_in[i];
-        const uint32_t c = node[d];
-        if (c >= first_next) {
-            const uint32_t par = (c - 1) >> 1;
-            const bool left = c & 1;
-            const uint32_t b = left ? gstart[par] : gstart[par] + cntL[par];
-            const uint32_t r = rank[d];
-            perm_out[b + r] = d;
-            if (r == 0) gstart[c] = b;
-        } else {
-            perm_out[i] = d;
-        }
-    }
-}
-
-// position ranges of the nodes of level l (first .. first+count) from their parents'
-// (unfused deep path: the per-warp level kernel + k_scatter read gstart of the current
-// level's nodes, while the level kernels record the range of their own runs' nodes)
-__global__ void k_child_ranges(uint32_t* __restrict__ gstart, const uint32_t* __restrict__ cntL, uint64_t first,
-                               uint64_t count) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count; i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t c = first + i, pp = (c - 1) / 2;
-        gstart[c] = (c & 1) ? gstart[pp] : gstart[pp] + cntL[pp];
-    }
-}
-
 // stage init: identity order, everyone at the root, this stage's uniform
 __global__ void k_stage_init(uint32_t* perm, uint32_t* node, double* low, double* ud, uint32_t* gstart,
                              uint64_t J, uint64_t seed, uint64_t off, uint64_t counter, double* margin,
@@ -2614,7 +2501,7 @@ void launch_split(const EvalArgs& a, cudaStream_t s) {
 }
 
 template <int NB>
-void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t, bool warp_variant) {
+void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t) {
     const unsigned grid = unsigned((a.J + uint64_t(CB) - 1) / uint64_t(CB));
     if constexpr (NB <= 8) {
         if (a.W) {  // one-stage mode: every level on the register-resident kernel
@@ -2623,14 +2510,14 @@ void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t, b
         }
     }
     if constexpr (NB == 8 || NB == 16) {
-        if (eval_split_on(t, NB) && !warp_variant) {
+        if (eval_split_on(t, NB)) {
             if (mode == EV_PROB) return launch_split<NB, EV_PROB, false>(a, s);
             if (mode == EV_LEVEL0) return launch_split<NB, EV_LEVEL, true>(a, s);
             if (mode == EV_LEVEL) return launch_split<NB, EV_LEVEL, false>(a, s);
         }
     }
     if constexpr (NB <= 8) {
-        if (t.eval_reg && !warp_variant) {
+        if (t.eval_reg) {
             if (mode == EV_PROB) return launch_reg<NB, EV_PROB, false>(a, s);
             if (mode == EV_LEVEL0) return launch_reg<NB, EV_LEVEL, true>(a, s);
             if (mode == EV_LEVEL) return launch_reg<NB, EV_LEVEL, false>(a, s);
@@ -2642,36 +2529,32 @@ void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t, b
         launch_cta<NB, EV_PROB, false>(a, grid, s);
     else if (mode == EV_LEVEL0)
         launch_cta<NB, EV_LEVEL, true>(a, grid, s);
-    else if (warp_variant) {
-        if constexpr (NB <= 8)
-            k_eval_warp<NB><<<unsigned((a.J + uint64_t(CHUNK) * WPB - 1) / (uint64_t(CHUNK) * WPB)), WPB * 32, 0, s>>>(a);
-    } else
+    else
         launch_cta<NB, EV_LEVEL, false>(a, grid, s);
 }
 
-void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t,
-                   bool warp_variant = false) {
+void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t) {
     switch (R / 8) {
-        case 1: return launch_eval<1>(mode, a, s, t, warp_variant);
-        case 2: return launch_eval<2>(mode, a, s, t, warp_variant);
-        case 3: return launch_eval<3>(mode, a, s, t, warp_variant);
-        case 4: return launch_eval<4>(mode, a, s, t, warp_variant);
-        case 5: return launch_eval<5>(mode, a, s, t, warp_variant);
-        case 6: return launch_eval<6>(mode, a, s, t, warp_variant);
-        case 7: return launch_eval<7>(mode, a, s, t, warp_variant);
-        case 8: return launch_eval<8>(mode, a, s, t, warp_variant);
-        case 9: return launch_eval<9>(mode, a, s, t, false);
-        case 10: return launch_eval<10>(mode, a, s, t, false);
-        case 11: return launch_eval<11>(mode, a, s, t, false);
-        case 12: return launch_eval<12>(mode, a, s, t, false);
-        case 13: return launch_eval<13>(mode, a, s, t, false);
-        case 14: return launch_eval<14>(mode, a, s, t, false);
-        case 15: return launch_eval<15>(mode, a, s, t, false);
-        case 16: return launch_eval<16>(mode, a, s, t, false);
-        case 17: return launch_eval<17>(mode, a, s, t, false);
-        case 18: return launch_eval<18>(mode, a, s, t, false);
-        case 19: return launch_eval<19>(mode, a, s, t, false);
-        case 20: return launch_eval<20>(mode, a, s, t, false);
+        case 1: return launch_eval<1>(mode, a, s, t);
+        case 2: return launch_eval<2>(mode, a, s, t);
+        case 3: return launch_eval<3>(mode, a, s, t);
+        case 4: return launch_eval<4>(mode, a, s, t);
+        case 5: return launch_eval<5>(mode, a, s, t);
+        case 6: return launch_eval<6>(mode, a, s, t);
+        case 7: return launch_eval<7>(mode, a, s, t);
+        case 8: return launch_eval<8>(mode, a, s, t);
+        case 9: return launch_eval<9>(mode, a, s, t);
+        case 10: return launch_eval<10>(mode, a, s, t);
+        case 11: return launch_eval<11>(mode, a, s, t);
+        case 12: return launch_eval<12>(mode, a, s, t);
+        case 13: return launch_eval<13>(mode, a, s, t);
+        case 14: return launch_eval<14>(mode, a, s, t);
+        case 15: return launch_eval<15>(mode, a, s, t);
+        case 16: return launch_eval<16>(mode, a, s, t);
+        case 17: return launch_eval<17>(mode, a, s, t);
+        case 18: return launch_eval<18>(mode, a, s, t);
+        case 19: return launch_eval<19>(mode, a, s, t);
+        case 20: return launch_eval<20>(mode, a, s, t);
         case 24: return launch_stream<24>(mode, a, s);
         case 28: return launch_stream<28>(mode, a, s);
         default: return launch_stream<32>(mode, a, s);
@@ -2818,7 +2701,7 @@ static int launch_position_one_stage(const GroupedArgs& g) {
         e.perm_out = pout;
         e.nsort_in = l == 0 ? nullptr : nin;
         e.nsort_out = nout;
-        dispatch_eval(R, l == 0 ? EV_LEVEL0 : EV_LEVEL, e, g.stream, g.tune, false);
+        dispatch_eval(R, l == 0 ? EV_LEVEL0 : EV_LEVEL, e, g.stream, g.tune);
         ++launches;
         std::swap(pin, pout);
         std::swap(nin, nout);
@@ -2914,7 +2797,7 @@ int launch_position_grouped(const GroupedArgs& g) {
             e.perm_out = pout;
             e.nsort_in = (l == 0 || !nin) ? nullptr : nin;
             e.nsort_out = nout;
-            dispatch_eval(R, (l == 0 && R <= 160) ? EV_LEVEL0 : EV_LEVEL, e, g.stream, g.tune, false);
+            dispatch_eval(R, (l == 0 && R <= 160) ? EV_LEVEL0 : EV_LEVEL, e, g.stream, g.tune);
             ++launches;
             mark(9);
             std::swap(pin, pout);
@@ -2924,9 +2807,10 @@ int launch_position_grouped(const GroupedArgs& g) {
         e.nsort_out = nullptr;
     };
     const Topo tz = make_topo(g.I, R);
-    // shallow levels: global regrouping; deep levels + leaf scan: one fused pass
+    // shallow levels: global regrouping; deep levels + leaf scan: one fused pass (R <= 64).
+    // Without the fused pass (R > 64, or fused_deep off) every level runs on the level kernels.
     uint32_t l0 = 0;
-    while (l0 < tz.d && (R > 64 || !deep_level(g.tune, J, l0))) ++l0;
+    while (l0 < tz.d && (R > 64 || !g.fused_deep || !deep_level(g.tune, J, l0))) ++l0;
     // first position: E-tree and the top factor-tree levels from (node, component) tables
     const uint32_t L0 = tz.d >= 2 ? std::min<uint32_t>(kPos0Levels, std::min<uint32_t>(l0, tz.d - 1)) : 0;
     const bool tab0 = g.h_ones && g.pos0_tab && R <= 64 && R % 8 == 0 && L0 >= 1 && g.tune.pos0_tables;
@@ -3016,21 +2900,6 @@ int launch_position_grouped(const GroupedArgs& g) {
         launches += 2;
         mark(13);
         return launches;
-    }
-    if (l0 > 0 && l0 < tz.d) {
-        const uint64_t first = (uint64_t(1) << l0) - 1;
-        const uint64_t count = std::min<uint64_t>(uint64_t(1) << l0, tz.n - first);
-        k_child_ranges<<<grid_for(count, 256), 256, 0, g.stream>>>(g.gstart, g.cntL, first, count);
-        ++launches;
-    }
-    for (uint32_t l = l0; l < tz.d; ++l) {
-        e.perm = pin;
-        dispatch_eval(R, EV_LEVEL, e, g.stream, g.tune, true);
-        mark(10);
-        k_scatter<<<gs, 256, 0, g.stream>>>(pin, pout, g.node, g.rank, g.gstart, g.cntL, J, (2u << l) - 1);
-        mark(11);
-        launches += 2;
-        std::swap(pin, pout);
     }
     LeafArgs la{};
     la.J = J;

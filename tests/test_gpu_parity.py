@@ -106,16 +106,17 @@ CASES = [
     ([(3000, 256), (1100, 256)], 12),
     ([(2500, 192), (700, 192)], 13),
     ([(20000, 128), (3000, 128)], 14),   # R = 128 split-Gram level kernel over 8 levels (no deep pass at R > 64)
-    ([(70000, 64), (9000, 64)], 15),     # R = 64: level kernel + deep pass over 11 levels; unfused: k_child_ranges
+    ([(70000, 64), (9000, 64)], 15),     # R = 64: level kernel + deep pass over 11 levels
 ]
 
 
 @pytest.mark.parametrize("J", [2000, 3000])
 def test_unfused_deep_levels_after_first_position_tables(J):
-    """R = 64, unfused deep path, J small enough that the first deep level l0 equals the
-    number of table levels L0 (J >> l0 < 32 with l0 <= 7): the first position's draws are
-    placed by k_pos0_place and the per-warp level kernel needs their level-l0 node ranges
-    from k_child_ranges -- that hand-off is covered here."""
+    """R = 64 with the fused deep pass off and a small J: the first position's draws are
+    placed by the tables (k_pos0_place, which records the level-L0 node ranges) and every
+    further level runs on the level kernel, which derives its nodes' ranges from those --
+    that hand-off is covered here (round 2 dropped the separate per-warp
+    deep-level kernel, so the unfused path is the level kernel down to the leaves)."""
     fs = pareto_factors([(70000, 64), (9000, 64), (20000, 64)], 16)
     s = K()(fs)
     s.set_fused_deep(False)

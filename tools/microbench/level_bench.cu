@@ -103,7 +103,7 @@ int main(int argc, char** argv) {
         // level-l counters must start at zero (cntL of the parents is preset above)
         cudaMemsetAsync(cntL_d + first, 0, size_t(nruns) * 4, s);
         cudaEventRecord(e0, s);
-        dispatch_eval(R, EV_LEVEL, a, s, Tuning{}, false);
+        dispatch_eval(R, EV_LEVEL, a, s, Tuning{});
         cudaEventRecord(e1, s);
         cudaEventSynchronize(e1);
         float ms;
