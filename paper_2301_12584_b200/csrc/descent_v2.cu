@@ -1664,6 +1664,16 @@ __global__ void __launch_bounds__(WPB * 32) k_leaf2(LeafArgs a) {
         const int re = cstarts ? __ffs(cstarts) - 1 : cnt;
         uint64_t first, last;
         run_rows(__shfl_sync(0xffffffffu, vl, rs), first, last);
+        // z fragments of the run's first 8-draw block, loaded once for all of the leaf's
+        // chunks (re-reading them per chunk put one global-latency load in front of every
+        // DMMA: 75 % long-scoreboard stalls at R = 128)
+        double zfirst[2 * NB];
+        {
+            const int n0 = min(8, re - rs);
+            const uint32_t dd0 = __shfl_sync(0xffffffffu, dl, (rs + m8) & 31);
+#pragma unroll
+            for (int s = 0; s < 2 * NB; ++s) zfirst[s] = m8 < n0 ? a.Z[uint64_t(dd0) * R + 4 * s + r4] : 0.0;
+        }
         for (uint64_t r0 = first; r0 < last; r0 += C::CH, ++chunk_i) {
             produce();
             const int st = int(chunk_i % C::STAGES);
@@ -1676,7 +1686,8 @@ __global__ void __launch_bounds__(WPB * 32) k_leaf2(LeafArgs a) {
                 const uint32_t dd = __shfl_sync(0xffffffffu, dl, (b0 + m8) & 31);
                 double zb[2 * NB];
 #pragma unroll
-                for (int s = 0; s < 2 * NB; ++s) zb[s] = valid ? a.Z[uint64_t(dd) * R + 4 * s + r4] : 0.0;
+                for (int s = 0; s < 2 * NB; ++s)
+                    zb[s] = b0 == rs ? zfirst[s] : (valid ? a.Z[uint64_t(dd) * R + 4 * s + r4] : 0.0);
 #pragma unroll
                 for (int mt = 0; mt < C::CH / 8; ++mt) {
                     const int row = 8 * mt + m8;
@@ -1726,11 +1737,30 @@ __global__ void __launch_bounds__(WPB * 32) k_leaf2(LeafArgs a) {
             if (a.margin) a.margin[dl] = mg;
             if (a.idx) a.idx[uint64_t(dl) * a.N + a.k] = uint32_t(pick);
         }
-        // h *= U[pick]  (krp_sampler.cpp:137-138)
-        for (int t = rs; t < re; ++t) {
-            const uint32_t dt = __shfl_sync(0xffffffffu, dl, t);
-            const uint64_t pt = __shfl_sync(0xffffffffu, pick, t);
-            for (int c = lane; c < R; c += 32) a.H[uint64_t(dt) * R + c] *= static_cast<double>(U[pt * R + c]);
+        // h *= U[pick]  (krp_sampler.cpp:137-138): every load of a group of 4 draws issued first
+        constexpr int CPL = (R + 31) / 32;
+        for (int t0 = rs; t0 < re; t0 += 4) {
+            double hv[4][CPL], uv[4][CPL];
+            uint32_t dt[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int t = t0 + q < re ? t0 + q : rs;
+                dt[q] = __shfl_sync(0xffffffffu, dl, t);
+                const uint64_t pt = __shfl_sync(0xffffffffu, pick, t);
+#pragma unroll
+                for (int cc = 0; cc < CPL; ++cc) {
+                    const int c = lane + 32 * cc;
+                    hv[q][cc] = c < R ? a.H[uint64_t(dt[q]) * R + c] : 0.0;
+                    uv[q][cc] = c < R ? static_cast<double>(U[pt * R + c]) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int cc = 0; cc < CPL; ++cc) {
+                    const int c = lane + 32 * cc;
+                    if (t0 + q < re && c < R) a.H[uint64_t(dt[q]) * R + c] = hv[q][cc] * uv[q][cc];
+                }
         }
     }
 }
