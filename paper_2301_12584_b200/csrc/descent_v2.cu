@@ -1573,7 +1573,9 @@ struct LeafCfg2 {
     static constexpr int CH = NB <= 8 ? 16 : 8;  // rows per stage (smem: 4 warps x 3 stages)
     static constexpr int STAGES = 3;
     static constexpr int ROWB = R * int(sizeof(T));
-    static constexpr int RS = ROWB;  // unpadded: one bulk copy per chunk
+    // rows padded by 16 bytes (one bulk copy per row): unpadded 1 KB rows put the 8 rows of
+    // a DMMA A fragment on the same banks (8-way conflicts, 22 % short-scoreboard at R = 128)
+    static constexpr int RS = ROWB + 16;
     static constexpr int CHB = CH * RS;
     static constexpr int WARP_BYTES = (STAGES * CHB + CH * 8 * 8 + STAGES * 8 + 127) / 128 * 128;
     static constexpr int SMEM = WPB * WARP_BYTES;
