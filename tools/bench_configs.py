@@ -1,7 +1,9 @@
 """Secondary BASELINE.json configurations (the headline config 2 is bench.py):
 
   --config 3 : N=4 factors 1.5e7 x 32, uniform[-1,1], fp32-stored / fp64-accumulated;
-               tree build, 2^20 two-stage draws, 10^5 random single-entry updates.
+               tree build, 2^20 two-stage draws, 10^5 random single-entry updates; under
+               torchrun (WORLD_SIZE > 1) the 2^20 draws are sharded over the ranks (strong
+               scaling, NCCL, max over ranks).
   --config 4 : rank sweep, N=3 factors 2^20 x R (R in 16..256), N(0,1); J = 65536.
   --config 5 : STS-CP factor updates (krpg_sts_solve) on a synthetic COO tensor with the
                Amazon-Reviews shape 4.8e6 x 1.8e6 x 1.8e6, Zipf(1.1) coordinates per mode,
@@ -89,7 +91,55 @@ def measure(s, N, I, R, J, storage, label, reps=5, extra=None):
     print(json.dumps(line), flush=True)
 
 
+def config3_sharded(args):
+    """Config 3's draws sharded over the ranks of one node (strong scaling: the 2^20 draws of
+    one call split into contiguous ranges, draw_offset = range start, trees replicated --
+    bit-identical to one call, sharding.shard_range); launch with torchrun (one process per
+    GPU, NCCL). Device time of the call per rank, max over ranks."""
+    import torch.distributed as dist
+
+    from paper_2301_12584_b200.sharding import shard_range
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    N, I, R, J = 4, 15_000_000, 32, 1 << 20
+    g = torch.Generator(device="cuda").manual_seed(3)
+    fs = [torch.rand(I, R, dtype=torch.float32, device="cuda", generator=g) * 2 - 1 for _ in range(N)]
+    s = KrpSampler.from_device(fs, storage="f32", device=local)
+    del fs
+    torch.cuda.empty_cache()
+    start, count = shard_range(J, rank, world)
+    idx = torch.empty(count, N, dtype=torch.int32, device="cuda")
+    prob = torch.empty(count, dtype=torch.float64, device="cuda")
+    rows = torch.empty(count, R, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.ExternalStream(s.stream(), device=torch.device("cuda", local))
+    for i in range(2):
+        s.sample_device(None, count, 7 + i, idx, prob, rows, draw_offset=start)
+    s.sync()
+    reps = 3
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(reps):
+        s.sample_device(None, count, 100 + i, idx, prob, rows, draw_offset=start)
+    e1.record(stream)
+    s.sync()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        ms = float(t.item())
+        print(json.dumps({"config": "config3_sharded", "N": N, "I": I, "R": R, "J": J, "ranks": world,
+                          "scaling": "strong (J split over the ranks)", "ms_per_call_max_over_ranks": ms,
+                          "samples_per_s": J / (ms / 1e3)}), flush=True)
+    dist.destroy_process_group()
+
+
 def config3(args):
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.sharded:
+        return config3_sharded(args)
     N, I, R, J = 4, 15_000_000, 32, 1 << 20
     g = torch.Generator(device="cuda").manual_seed(3)
     fs = [torch.rand(I, R, dtype=torch.float32, device="cuda", generator=g) * 2 - 1 for _ in range(N)]
@@ -204,6 +254,7 @@ def main():
     p.add_argument("--nnz", type=float, default=1.7e9)
     p.add_argument("--rounds", type=int, default=3)
     p.add_argument("--ranks", type=int, nargs="+", default=[16, 32, 64, 128, 256])
+    p.add_argument("--sharded", action="store_true", help="config 3: the sharded (torchrun) path even at one rank")
     args = p.parse_args()
     torch.cuda.init()
     {3: config3, 4: config4, 5: config5}[args.config](args)
