@@ -759,9 +759,9 @@ __device__ __forceinline__ void split_entry(int q, int k, int& p, int& col) {
     col = k <= q ? q : NB - 1 - q;
 }
 
-template <int NB>
+template <int NB, bool WGT = false>
 __device__ __forceinline__ void split_load(double (&g)[NB / 8][NB + 1][2], const double* __restrict__ G, int w,
-                                           int lane) {
+                                           int lane, const double* __restrict__ W = nullptr) {
     constexpr int R = 8 * NB;
     const int r4 = lane & 3, cq = lane >> 2;
 #pragma unroll
@@ -778,9 +778,10 @@ __device__ __forceinline__ void split_load(double (&g)[NB / 8][NB + 1][2], const
                 if (p == q) {
                     const int cc = 8 * p + cq;
                     const int diag = row <= cc ? rowoff + cc : cc * R - (cc * (cc - 1)) / 2 - cc + row;
-                    g[c][k][s] = __ldg(G + diag);
+                    g[c][k][s] = WGT ? __ldg(G + diag) * __ldg(W + diag) : __ldg(G + diag);
                 } else {
-                    const double x = __ldg(G + rowoff + 8 * q + cq);
+                    const double x = WGT ? __ldg(G + rowoff + 8 * q + cq) * __ldg(W + rowoff + 8 * q + cq)
+                                         : __ldg(G + rowoff + 8 * q + cq);
                     g[c][k][s] = x + x;
                 }
             }
@@ -850,7 +851,7 @@ __device__ __forceinline__ double qf_split_order(const double* __restrict__ G, c
     return ((part[0] + part[1]) + part[2]) + part[3];
 }
 
-template <int NB, int MODE, bool ROOT0>
+template <int NB, int MODE, bool ROOT0, bool WGT = false>
 __global__ void __launch_bounds__(SPW * 32, NB <= 8 ? 4 : 2) k_eval_split(EvalArgs a) {
     using SC = SplitCfg<NB>;
     constexpr int R = 8 * NB;
@@ -958,7 +959,7 @@ __global__ void __launch_bounds__(SPW * 32, NB <= 8 ? 4 : 2) k_eval_split(EvalAr
             const int b0 = e & 0xff, n = e >> 8;
             const uint32_t v = s_v[b0];
             if (v != gv) {
-                split_load<NB>(g, node_gram ? a.tree + slot_of(2ull * v + 1) * P : a.tree, warp, lane);
+                split_load<NB, WGT>(g, node_gram ? a.tree + slot_of(2ull * v + 1) * P : a.tree, warp, lane, a.W);
                 gv = v;
             }
             const int m = lane >> 2;
@@ -2434,8 +2435,98 @@ void launch_leaf_os(const LeafOsArgs& a, cudaStream_t s) {
     launch_pdl(k_leaf_os<NB, T>, dim3(std::max(1u, grid)), dim3(RW * 32), C::SMEM, s, a);
 }
 
+// ---- one-stage leaf at R = 128: Y's fragments split over the 4 warps of a CTA ----
+// (272 B-fragment doubles per lane would not fit one warp): the CTA takes one draw at a
+// time, stages 8 rows (times h) in shared memory, every warp computes its column pairs'
+// share of the 8 masses (split_block, k_eval_split's order) and the partials are summed
+// in warp order after a barrier; warp 0 runs the sequential scan and early exit.
+template <int NB>
+struct LeafOsSplitCfg {
+    static constexpr int R = 8 * NB;
+    static constexpr int XS = R + 4;
+    static constexpr size_t SMEM = (size_t(8) * XS + R + SPW * 8 + 8) * 8;
+};
+
+template <int NB, typename T>
+__global__ void __launch_bounds__(SPW * 32, 2) k_leaf_os_split(LeafOsArgs a) {
+    constexpr int R = 8 * NB;
+    using C = LeafOsSplitCfg<NB>;
+    extern __shared__ __align__(16) double smem_lss[];
+    double* xs = smem_lss;             // 8 x XS staged rows o h
+    double* hs = xs + 8 * C::XS;       // h of the current draw
+    double* part = hs + R;             // [SPW][8] partial masses
+    double* ctl = part + SPW * 8;      // [0] = picked flag (as double)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+    griddep_launch_dependents();
+    griddep_wait();
+    const T* U = static_cast<const T*>(a.U);
+    double g[NB / 8][NB + 1][2];
+    split_load<NB>(g, a.W, warp, lane);
+    __shared__ uint32_t s_t;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_t = atomicAdd(a.work, 1u);
+        __syncthreads();
+        const uint32_t t = s_t;
+        if (t >= a.J) break;
+        const uint32_t d = a.perm[t];
+        KRPG_DCHECK(d < a.J);
+        const uint64_t v = a.node[d];
+        KRPG_DCHECK(v < a.topo.n && is_leaf(a.topo, v));
+        uint64_t f, l;
+        leaf_rows(a.topo, leaf_index(a.topo, v), &f, &l);
+        for (int c = tid; c < R; c += SPW * 32) hs[c] = a.H[uint64_t(d) * R + c];
+        const double ic = a.invc[d], u = a.ud[d];
+        double cum = a.low[d], mg = a.margin ? a.margin[d] : HUGE_VAL;
+        uint64_t pick = ~uint64_t{0}, last_nz = ~uint64_t{0};
+        __syncthreads();
+        for (uint64_t b0 = f; b0 < l; b0 += 8) {
+            for (int e = tid; e < 8 * R; e += SPW * 32) {
+                const int m = e / R, c = e - m * R;
+                xs[m * C::XS + c] = b0 + m < l ? static_cast<double>(U[(b0 + m) * R + c]) * hs[c] : 0.0;
+            }
+            __syncthreads();
+            const double pm = split_block<NB>(g, xs, C::XS, true, warp, lane);
+            if ((lane & 3) == 0) part[warp * 8 + (lane >> 2)] = pm;
+            __syncthreads();
+            if (warp == 0) {  // sequential scan (segment_tree_sampler.cpp:284-291), uniform in the warp
+                const int n = int(l - b0 < 8 ? l - b0 : 8);
+                for (int j = 0; j < n; ++j) {
+                    const double mass = ((part[j] + part[8 + j]) + part[16 + j]) + part[24 + j];
+                    const double mm = ic * mass;
+                    if (mm > 0.0) last_nz = b0 + j;
+                    cum += mm;
+                    mg = fmin(mg, fabs(cum - u));
+                    if (cum >= u) {
+                        pick = b0 + j;
+                        break;
+                    }
+                }
+                if (lane == 0) ctl[0] = pick != ~uint64_t{0} ? 1.0 : 0.0;
+            }
+            __syncthreads();
+            if (ctl[0] != 0.0) break;
+        }
+        if (tid == 0) {
+            if (pick == ~uint64_t{0}) pick = last_nz != ~uint64_t{0} ? last_nz : l - 1;
+            KRPG_DCHECK(pick >= f && pick < l);
+            if (a.idx) a.idx[uint64_t(d) * a.N + a.k] = uint32_t(pick);
+            a.pick[d] = uint32_t(pick);
+            if (a.margin) a.margin[d] = mg;
+        }
+        if (tid == 0) ctl[0] = 0.0;
+    }
+}
+
 template <typename T>
 void dispatch_leaf_os(uint32_t R, const LeafOsArgs& a, cudaStream_t s) {
+    if (R == 128) {
+        using C = LeafOsSplitCfg<16>;
+        const int occ = occupancy(k_leaf_os_split<16, T>, SPW * 32, C::SMEM);
+        const unsigned grid = unsigned(std::min<uint64_t>(uint64_t(sm_count_current()) * occ, a.J));
+        launch_pdl(k_leaf_os_split<16, T>, dim3(std::max(1u, grid)), dim3(SPW * 32), C::SMEM, s, a);
+        return;
+    }
     switch (R / 8) {
         case 1: return launch_leaf_os<1, T>(a, s);
         case 2: return launch_leaf_os<2, T>(a, s);
@@ -2525,11 +2616,11 @@ void launch_reg(const EvalArgs& a, cudaStream_t s) {
 // register-resident single-warp kernel measured faster (2.41 vs 2.83 ms per config-2 step)
 inline bool eval_split_on(const Tuning& t, int NB) { return t.eval_split == 1 || t.eval_split == NB; }
 
-template <int NB, int MODE, bool ROOT0>
+template <int NB, int MODE, bool ROOT0, bool WGT = false>
 void launch_split(const EvalArgs& a, cudaStream_t s) {
-    smem_optin(k_eval_split<NB, MODE, ROOT0>, SplitCfg<NB>::SMEM);
+    smem_optin(k_eval_split<NB, MODE, ROOT0, WGT>, SplitCfg<NB>::SMEM);
     const unsigned grid = unsigned((a.J + SPR - 1) / SPR);
-    launch_pdl(k_eval_split<NB, MODE, ROOT0>, dim3(grid), dim3(SPW * 32), SplitCfg<NB>::SMEM, s, a);
+    launch_pdl(k_eval_split<NB, MODE, ROOT0, WGT>, dim3(grid), dim3(SPW * 32), SplitCfg<NB>::SMEM, s, a);
 }
 
 template <int NB>
@@ -2539,6 +2630,12 @@ void launch_eval(int mode, const EvalArgs& a, cudaStream_t s, const Tuning& t) {
         if (a.W) {  // one-stage mode: every level on the register-resident kernel
             if (mode == EV_LEVEL0) return launch_reg<NB, EV_LEVEL, true, true>(a, s);
             if (mode == EV_LEVEL) return launch_reg<NB, EV_LEVEL, false, true>(a, s);
+        }
+    }
+    if constexpr (NB == 16) {
+        if (a.W) {  // one-stage mode at R = 128: the split-Gram kernel with B = G_v o Y
+            if (mode == EV_LEVEL0) return launch_split<NB, EV_LEVEL, true, true>(a, s);
+            if (mode == EV_LEVEL) return launch_split<NB, EV_LEVEL, false, true>(a, s);
         }
     }
     if constexpr (NB == 8 || NB == 16) {
@@ -2692,7 +2789,7 @@ inline void dispatch_pos0_tables(uint32_t R, const double* Q, Topo te, const dou
 // level (both Gram buffers of a run fit in shared memory) + streaming leaf scan.
 // 160 < R <= 256 (R % 32 == 0): streamed-Gram level kernel + streaming leaf scan.
 bool grouped_supported(uint32_t R, uint32_t mode) {
-    if (mode == 1) return R % 8 == 0 && R >= 8 && R <= 64;  // one-stage: register-resident kernels
+    if (mode == 1) return (R % 8 == 0 && R >= 8 && R <= 64) || R == 128;  // one-stage grouped kernels
     return mode == 0 && R % 8 == 0 && R >= 8 && (R <= 160 || (R <= 256 && R % 32 == 0));
 }
 

@@ -62,6 +62,14 @@ def case_onestage():
     cd = s.conditional(None, 1, np.ones(16))
     assert abs(cd.probabilities.sum() - 1.0) < 1e-9
     s.close()
+    fs = factors([(40000, 64), (30000, 64)], 12)  # grouped one-stage, several levels
+    s = pkg.KrpSampler(fs)
+    assert np.all(s.sample(0, 8192, 3, mode="one_stage").probabilities > 0)
+    s.close()
+    fs = factors([(20000, 128), (3000, 128)], 13)  # R = 128: split level kernel + split leaf
+    s = pkg.KrpSampler(fs)
+    assert np.all(s.sample(None, 4096, 4, mode="one_stage").probabilities > 0)
+    s.close()
 
 
 def case_rank():
