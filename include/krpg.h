@@ -186,6 +186,10 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
 /* krpg_sample into page-locked host buffers: the last position runs as this many draw
  * slices, each copied out while the next computes (default 2, 1..4; same bits) */
 #define KRPG_OPT_OUT_SLICES 23
+/* krpg_sts_solve: 1 (default) the row-ordered, atomic-free scatter and block-ordered column
+ * norms (bit-reproducible factor updates); 0 the fp64-atomic fiber scatter (faster on
+ * large tensors, sums in run-dependent order) */
+#define KRPG_OPT_STS_DETERMINISTIC 25
 int krpg_set_option(krpg_t h, int option, int64_t value);
 /* 1 for the bounds-checked library (make CHECKED=1, device asserts), 0 for production */
 int krpg_is_checked_build(void);

@@ -843,7 +843,7 @@ void krpg_sampler::sts_solve(krpg_tensor& T, uint32_t j, uint64_t J, uint64_t se
     CK(cudaStreamSynchronize(T.stream));
     const krpg::FiberIndexDev& F = T.fiber(j);
     t_sts = pbegin();
-    krpg::launch_sts_rhs(di, J, N, j, T.dims.data(), dp, dr, R, F, work, M, derr, stream);
+    krpg::launch_sts_rhs(di, J, N, j, T.dims.data(), dp, dr, R, F, work, M, derr, stream, tune.sts_deterministic != 0);
     pend(KRPG_PROF_STS_SCATTER, t_sts, 9);
     // 4) pinv_psd(gram(sa)) on the host (dense_kernels.cpp:207)
     std::vector<double> gh(size_t(R) * R);
@@ -2161,7 +2161,9 @@ int krpg_set_option(krpg_t h, int option, int64_t value) {
         } else if (option == KRPG_OPT_DEEP_DMMA_MIN) {
             require(value >= 1 && value <= 64, "krpg_set_option: deep DMMA minimum must be in [1, 64]");
             h->tune.deep_dmma_min = int(value);
-        } else if (option == KRPG_OPT_OUT_SLICES) {
+        } else if (option == KRPG_OPT_STS_DETERMINISTIC)
+            h->tune.sts_deterministic = value != 0;
+        else if (option == KRPG_OPT_OUT_SLICES) {
             require(value >= 1 && value <= 4, "krpg_set_option: output slices must be in [1, 4]");
             h->tune.out_slices = int(value);
         } else if (option == KRPG_OPT_LEAF_PAR) {

@@ -91,6 +91,7 @@ struct Tuning {
     int eval_split = 16;       // split-Gram level kernel: 16 = R 128 only, 1 = R 64 and 128, 0 = off
     int deep_dmma_min = 1;     // deep-pass runs with fewer draws use CUDA-core forms
     int leaf_par = 8;          // leaf runs with at most this many draws scan warp-parallel
+    int sts_deterministic = 1; // STS-CP scatter: 1 row-ordered (bit-reproducible), 0 fp64 atomics (faster)
     int out_slices = 2;        // krpg_sample into page-locked host memory: draw slices of the
                                // last position whose copies overlap the following slices (1..4)
 };
@@ -215,7 +216,7 @@ const void* sts_stats_ptr(void* work, uint64_t J, uint32_t R);
 // S = sum w^2 rows, entries scattered v S (M zeroed here)
 void launch_sts_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, const uint64_t* dims, const double* prob,
                     const double* rows, uint32_t R, const FiberIndexDev& F, void* work, double* M, int* err,
-                    cudaStream_t s);
+                    cudaStream_t s, bool deterministic = true);
 // U = (pinv M^T)^T row by row into Utmp, column norms -> nrm (R), then the
 // normalised columns (cp_als.cpp:39-52) stored into Uout (storage 0 f64, 1 f32)
 void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const double* pinv, double* Utmp, double* nrm,

@@ -214,6 +214,145 @@ __global__ void k_fiber_scatter(const uint32_t* __restrict__ ug, const uint32_t*
     }
 }
 
+// ---- deterministic row-ordered scatter (replaces the atomic fiber scatter) ----
+// M[i] = sum over the sampled fibers' entries with coordinate i of v_e S[sg_e], in the
+// fixed order (fiber slot sg ascending, entry ascending): every visited entry gets its
+// position e in that order, a stable radix sort by row groups them, and each row is summed
+// by one warp in pieces of at most RPIECE entries (partial rows of multi-piece rows summed
+// in piece order), so M -- and the solved factor -- are bit-reproducible run to run.
+constexpr uint32_t RPIECE = 1024;
+
+__global__ void k_seg_len(const uint32_t* __restrict__ ug, const uint32_t* __restrict__ nseg,
+                          const uint64_t* __restrict__ fptr, uint64_t J, uint32_t* __restrict__ len) {
+    const uint32_t n = *nseg;
+    for (uint64_t sg = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; sg <= J; sg += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t L = 0;
+        if (sg < n && ug[sg] != NONE) L = uint32_t(fptr[ug[sg] + 1] - fptr[ug[sg]]);
+        len[sg] = L;
+    }
+}
+
+// one warp per work item (SCHUNK entries of one sampled fiber): row key, order position
+__global__ void k_visit(const uint32_t* __restrict__ ug, const uint32_t* __restrict__ wstart,
+                        const uint32_t* __restrict__ nseg, uint64_t J, const uint64_t* __restrict__ fptr,
+                        const uint32_t* __restrict__ fcoord, const double* __restrict__ fval,
+                        const uint32_t* __restrict__ eoff, uint32_t* __restrict__ key, uint32_t* __restrict__ ord,
+                        double* __restrict__ pv, uint32_t* __restrict__ psg) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t n = *nseg;
+    if (n == 0) return;
+    const uint64_t total = wstart[J];
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t it = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); it < total; it += warps) {
+        uint32_t lo = 0, hi = n;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (wstart[mid] <= it)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const uint32_t sg = lo, g = ug[sg];
+        const uint64_t f0 = fptr[g];
+        const uint64_t p0 = f0 + (it - wstart[sg]) * SCHUNK;
+        const uint64_t p1 = p0 + SCHUNK < fptr[g + 1] ? p0 + SCHUNK : fptr[g + 1];
+        for (uint64_t p = p0 + lane; p < p1; p += 32) {
+            const uint32_t e = eoff[sg] + uint32_t(p - f0);
+            key[e] = fcoord[p];
+            ord[e] = e;
+            pv[e] = fval[p];
+            psg[e] = sg;
+        }
+    }
+}
+
+__global__ void k_row_pieces(const uint32_t* __restrict__ rcnt, const uint32_t* __restrict__ nrows, uint64_t cap,
+                             uint32_t* __restrict__ np, uint32_t* __restrict__ mp) {
+    const uint32_t n = *nrows;
+    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r <= cap; r += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t k = 0;
+        if (r < n) k = (rcnt[r] + RPIECE - 1) / RPIECE;
+        np[r] = k;
+        mp[r] = k > 1 ? k : 0;  // partial-row slots only for multi-piece rows
+    }
+}
+
+// (value, fiber slot) of every visited entry in row-sorted order (coalesced for the sums)
+__global__ void k_gather_sorted(const uint32_t* __restrict__ ord, const double* __restrict__ pv,
+                                const uint32_t* __restrict__ psg, uint64_t E, double* __restrict__ vs,
+                                uint32_t* __restrict__ ss) {
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < E; t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t e = ord[t];
+        vs[t] = pv[e];
+        ss[t] = psg[e];
+    }
+}
+
+// one warp per piece: lane owns columns lane + 32 c (R <= 256); the piece's (v, slot) pairs
+// are read 32 at a time by the lanes and broadcast, so every S-row load is independent
+__global__ void k_piece_sums(const uint32_t* __restrict__ urow, const uint32_t* __restrict__ rcnt,
+                             const uint32_t* __restrict__ roff, const uint32_t* __restrict__ poff,
+                             const uint32_t* __restrict__ moff, const uint32_t* __restrict__ nrows,
+                             const double* __restrict__ vs, const uint32_t* __restrict__ ss,
+                             const double* __restrict__ S, uint32_t R, double* __restrict__ M,
+                             double* __restrict__ pbuf) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nr = *nrows;
+    if (nr == 0) return;
+    const uint64_t npieces = poff[nr];
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t q = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); q < npieces; q += warps) {
+        uint32_t lo = 0, hi = nr;  // last row with poff <= q
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (poff[mid] <= q)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const uint32_t r = lo, k = uint32_t(q - poff[r]);
+        const uint32_t b = roff[r] + k * RPIECE;
+        const uint32_t e1 = min(roff[r] + rcnt[r], b + RPIECE);
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint32_t t0 = b; t0 < e1; t0 += 32) {
+            const uint32_t nt = min(32u, e1 - t0);
+            const double myv = lane < int(nt) ? vs[t0 + lane] : 0.0;
+            const uint32_t mys = lane < int(nt) ? ss[t0 + lane] : 0u;
+#pragma unroll 8
+            for (uint32_t j = 0; j < nt; ++j) {  // entries in order: the sum is order-fixed
+                const double v = __shfl_sync(0xffffffffu, myv, int(j));
+                const double* Sg = S + uint64_t(__shfl_sync(0xffffffffu, mys, int(j))) * R;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (lane + 32 * c < int(R)) acc[c] = fma(v, Sg[lane + 32 * c], acc[c]);
+            }
+        }
+        const bool multi = poff[r + 1] - poff[r] > 1;
+        double* dst = multi ? pbuf + (uint64_t(moff[r]) + k) * R : M + uint64_t(urow[r]) * R;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (lane + 32 * c < int(R)) dst[lane + 32 * c] = acc[c];
+    }
+}
+
+// rows split into several pieces: their partial rows summed in piece order
+__global__ void k_piece_merge(const uint32_t* __restrict__ urow, const uint32_t* __restrict__ poff,
+                              const uint32_t* __restrict__ moff, const uint32_t* __restrict__ nrows,
+                              const double* __restrict__ pbuf, uint32_t R, double* __restrict__ M) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nr = *nrows;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x >> 5) + (threadIdx.x >> 5); r < nr; r += warps) {
+        const uint32_t k = poff[r + 1] - poff[r];
+        if (k <= 1) continue;
+        for (uint32_t c = lane; c < R; c += 32) {
+            double acc = 0.0;
+            for (uint32_t t = 0; t < k; ++t) acc += pbuf[(uint64_t(moff[r]) + t) * R + c];
+            M[uint64_t(urow[r]) * R + c] = acc;
+        }
+    }
+}
+
 // U[i, a] = sum_k pinv[a, k] M[i, k] (matmul(pinv, gram_cross) transposed,
 // dense_kernels.cpp:209-223), one warp per row; pinv staged transposed in shared
 // memory so lanes (= output columns) read consecutive words. The column sums of
@@ -255,13 +394,19 @@ __global__ void k_solve_rows(const double* __restrict__ M, uint64_t I, uint32_t 
             }
         }
     }
+    // column sums of squares, reproducibly: warps in order within the block, blocks in
+    // order in k_colsq_finish (colsq = this block's partial row of the grid x R buffer)
+    const int warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int w = 0; w < nwarp; ++w) {
+        if (warp == w)
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        const uint32_t a = lane + 32 * t;
-        if (a < R) atomicAdd(&s_sq[a], sq[t]);
+            for (int t = 0; t < 8; ++t) {
+                const uint32_t a = lane + 32 * t;
+                if (a < R) s_sq[a] += sq[t];
+            }
+        __syncthreads();
     }
-    __syncthreads();
-    for (uint32_t e = threadIdx.x; e < R; e += blockDim.x) atomicAdd(colsq + e, s_sq[e]);
+    for (uint32_t e = threadIdx.x; e < R; e += blockDim.x) colsq[uint64_t(blockIdx.x) * R + e] = s_sq[e];
 }
 
 // Same solve on the FP64 tensor cores: a warp takes 8 rows, D (8 rows x 8 cols of
@@ -321,10 +466,27 @@ __global__ void __launch_bounds__(256) k_solve_rows_dmma(const double* __restric
             v += __shfl_xor_sync(0xffffffffu, v, 4);
             v += __shfl_xor_sync(0xffffffffu, v, 8);
             v += __shfl_xor_sync(0xffffffffu, v, 16);
-            if (m == 0) atomicAdd(&s_sq[8 * q + 2 * kq + e], v);
+            sq[q][e] = v;
         }
-    __syncthreads();
-    for (int e = threadIdx.x; e < R; e += blockDim.x) atomicAdd(colsq + e, s_sq[e]);
+    // warps in order within the block, blocks in order in k_colsq_finish
+    const int warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int w = 0; w < nwarp; ++w) {
+        if (warp == w && m == 0)
+#pragma unroll
+            for (int q = 0; q < NB; ++q)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) s_sq[8 * q + 2 * kq + e] += sq[q][e];
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < R; e += blockDim.x) colsq[uint64_t(blockIdx.x) * R + e] = s_sq[e];
+}
+
+__global__ void k_colsq_finish(const double* __restrict__ part, int nblocks, uint32_t R, double* __restrict__ nrm) {
+    for (uint32_t a = threadIdx.x; a < R; a += blockDim.x) {
+        double t = 0.0;
+        for (int b = 0; b < nblocks; ++b) t += part[uint64_t(b) * R + a];
+        nrm[a] = sqrt(t);
+    }
 }
 
 __global__ void k_sqrt_inplace(double* x, uint32_t n) {
@@ -539,7 +701,7 @@ const void* sts_stats_ptr(void* work, uint64_t J, uint32_t R) { return StsWork(w
 
 void launch_sts_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, const uint64_t* dims, const double* prob,
                     const double* rows, uint32_t R, const FiberIndexDev& F, void* work, double* M, int* err,
-                    cudaStream_t s) {
+                    cudaStream_t s, bool deterministic) {
     Radix colrx{};
     colrx.N = N;
     uint64_t st = 1;
@@ -574,7 +736,82 @@ void launch_sts_rhs(const uint32_t* idx, uint64_t J, uint32_t N, uint32_t j, con
     STS_CK(cudaMemsetAsync(W.stats, 0, 32, s));
     k_sts_stats<<<64, 256, 0, s>>>(W.ug, W.cnt, W.nseg, F.fptr, W.stats);
     STS_CK(cudaMemsetAsync(M, 0, 8 * F.I * R, s));
-    k_fiber_scatter<<<148 * 16, 256, 0, s>>>(W.ug, W.wstart, W.nseg, J, F.fptr, F.fcoord, F.fval, W.S, R, M);
+    if (!deterministic) {  // fp64 atomics: faster, sums in run-dependent order
+        k_fiber_scatter<<<148 * 16, 256, 0, s>>>(W.ug, W.wstart, W.nseg, J, F.fptr, F.fcoord, F.fval, W.S, R, M);
+        return;
+    }
+    // deterministic row-ordered scatter (k_visit -> stable sort by row -> per-row pieces);
+    // its E-sized buffers come from the stream-ordered pool, kept cached between steps
+    // (the default release threshold 0 would hand them back to the driver at every sync)
+    {
+        static bool pool_set[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64 && !pool_set[dev]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = ~uint64_t{0};
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            pool_set[dev] = true;
+        }
+    }
+    uint32_t* len = nullptr;
+    uint32_t* eoff = nullptr;
+    STS_CK(cudaMallocAsync(&len, 4 * (J + 1), s));
+    STS_CK(cudaMallocAsync(&eoff, 4 * (J + 1), s));
+    k_seg_len<<<grid_of(J + 1), 256, 0, s>>>(W.ug, W.nseg, F.fptr, J, len);
+    Scratch tmp;
+    need = 0;
+    STS_CK(cub::DeviceScan::ExclusiveSum(nullptr, need, len, eoff, J + 1, s));
+    STS_CK(cub::DeviceScan::ExclusiveSum(tmp.get(need), need, len, eoff, J + 1, s));
+    uint32_t E = 0;
+    STS_CK(cudaMemcpyAsync(&E, eoff + J, 4, cudaMemcpyDeviceToHost, s));
+    STS_CK(cudaStreamSynchronize(s));
+    if (E > 0) {
+        const uint64_t E1 = E;
+        uint32_t *key, *key2, *ord, *ord2, *psg, *ss, *urow, *rcnt, *roff, *nrows, *np, *poff, *mp, *moff;
+        double *pv, *vs;
+        for (uint32_t** b : {&key, &key2, &ord, &ord2, &psg, &ss}) STS_CK(cudaMallocAsync(b, 4 * E1, s));
+        for (double** b : {&pv, &vs}) STS_CK(cudaMallocAsync(b, 8 * E1, s));
+        for (uint32_t** b : {&urow, &rcnt, &roff, &np, &poff, &mp, &moff}) STS_CK(cudaMallocAsync(b, 4 * (E1 + 1), s));
+        STS_CK(cudaMallocAsync(&nrows, 4, s));
+        k_visit<<<148 * 16, 256, 0, s>>>(W.ug, W.wstart, W.nseg, J, F.fptr, F.fcoord, F.fval, eoff, key, ord, pv, psg);
+        const int bits = bits_for(F.I > 1 ? F.I - 1 : 1);
+        need = 0;
+        STS_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, ord, ord2, E1, 0, bits, s));
+        STS_CK(cub::DeviceRadixSort::SortPairs(tmp.get(need), need, key, key2, ord, ord2, E1, 0, bits, s));
+        k_gather_sorted<<<grid_of(E1), 256, 0, s>>>(ord2, pv, psg, E1, vs, ss);
+        need = 0;
+        STS_CK(cub::DeviceRunLengthEncode::Encode(nullptr, need, key2, urow, rcnt, nrows, E1, s));
+        STS_CK(cub::DeviceRunLengthEncode::Encode(tmp.get(need), need, key2, urow, rcnt, nrows, E1, s));
+        need = 0;
+        STS_CK(cub::DeviceScan::ExclusiveSum(nullptr, need, rcnt, roff, E1, s));
+        STS_CK(cub::DeviceScan::ExclusiveSum(tmp.get(need), need, rcnt, roff, E1, s));
+        k_row_pieces<<<grid_of(E1 + 1), 256, 0, s>>>(rcnt, nrows, E1, np, mp);
+        need = 0;
+        STS_CK(cub::DeviceScan::ExclusiveSum(nullptr, need, np, poff, E1 + 1, s));
+        STS_CK(cub::DeviceScan::ExclusiveSum(tmp.get(need), need, np, poff, E1 + 1, s));
+        need = 0;
+        STS_CK(cub::DeviceScan::ExclusiveSum(nullptr, need, mp, moff, E1 + 1, s));
+        STS_CK(cub::DeviceScan::ExclusiveSum(tmp.get(need), need, mp, moff, E1 + 1, s));
+        // partial rows: at most E / RPIECE + (rows with > RPIECE entries) pieces in multi-piece rows
+        const uint64_t pmax = 2 * (E1 / RPIECE) + 2;
+        double* pbuf = nullptr;
+        STS_CK(cudaMallocAsync(&pbuf, 8 * pmax * R, s));
+        k_piece_sums<<<148 * 16, 256, 0, s>>>(urow, rcnt, roff, poff, moff, nrows, vs, ss, W.S, R, M, pbuf);
+        k_piece_merge<<<148 * 8, 256, 0, s>>>(urow, poff, moff, nrows, pbuf, R, M);
+        for (void* b : {static_cast<void*>(key), static_cast<void*>(key2), static_cast<void*>(ord),
+                        static_cast<void*>(ord2), static_cast<void*>(pv), static_cast<void*>(psg),
+                        static_cast<void*>(vs), static_cast<void*>(ss),
+                        static_cast<void*>(urow), static_cast<void*>(rcnt), static_cast<void*>(roff),
+                        static_cast<void*>(np), static_cast<void*>(poff), static_cast<void*>(mp),
+                        static_cast<void*>(moff), static_cast<void*>(nrows), static_cast<void*>(pbuf)})
+            STS_CK(cudaFreeAsync(b, s));
+    }
+    STS_CK(cudaFreeAsync(len, s));
+    STS_CK(cudaFreeAsync(eoff, s));
+    STS_CK(cudaStreamSynchronize(s));  // the CUB scratch (tmp) is freed on return
 }
 
 void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const double* pinv, double* Utmp, double* nrm,
@@ -583,13 +820,17 @@ void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const doubl
     const bool staged = need <= 160 * 1024;  // R <= 144; larger pinv is read through L1/L2
     const size_t smem = staged ? need : 0;
     smem_optin(k_solve_rows, smem);
-    cudaMemsetAsync(nrm, 0, sizeof(double) * R, s);
+    // per-block column partials (grid x R), summed in block order by k_colsq_finish
+    double* part = nullptr;
+    STS_CK(cudaMallocAsync(&part, sizeof(double) * 148ull * 8 * R, s));
+    int nblocks = 0;
     if (R % 8 == 0 && R <= 128) {  // FP64 tensor-core path (padded pinv fits shared memory)
         const size_t dsm = sizeof(double) * R * (R + 4);
         const unsigned grid = unsigned(std::min<uint64_t>((I + 63) / 64, 148ull * 8));
+        nblocks = int(grid);
         auto launch = [&](auto kern) {
             smem_optin(kern, dsm);
-            kern<<<grid, 256, dsm, s>>>(M, I, pinv, Utmp, nrm);
+            kern<<<grid, 256, dsm, s>>>(M, I, pinv, Utmp, part);
         };
         switch (R / 8) {
             case 1: launch(k_solve_rows_dmma<1>); break;
@@ -604,14 +845,17 @@ void launch_solve_normalize(const double* M, uint64_t I, uint32_t R, const doubl
             case 16: launch(k_solve_rows_dmma<16>); break;
             default: {
                 const unsigned g2 = unsigned(std::min<uint64_t>((I + 7) / 8, 148ull * 8));
-                k_solve_rows<<<g2, 256, smem, s>>>(M, I, R, pinv, Utmp, nrm, staged ? 1 : 0);
+                nblocks = int(g2);
+                k_solve_rows<<<g2, 256, smem, s>>>(M, I, R, pinv, Utmp, part, staged ? 1 : 0);
             }
         }
     } else {
         const unsigned grid = unsigned(std::min<uint64_t>((I + 7) / 8, 148ull * 8));
-        k_solve_rows<<<grid, 256, smem, s>>>(M, I, R, pinv, Utmp, nrm, staged ? 1 : 0);
+        nblocks = int(grid);
+        k_solve_rows<<<grid, 256, smem, s>>>(M, I, R, pinv, Utmp, part, staged ? 1 : 0);
     }
-    k_sqrt_inplace<<<1, 256, 0, s>>>(nrm, R);
+    k_colsq_finish<<<1, 256, 0, s>>>(part, nblocks, R, nrm);
+    STS_CK(cudaFreeAsync(part, s));
     if (Uout) launch_normalize_store(Utmp, I, R, nrm, Uout, storage, s);
 }
 

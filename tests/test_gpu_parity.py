@@ -602,6 +602,23 @@ def test_sts_solve_matches_restatement(dims, R, storage):
     assert_draws_match(bb, ri, rp, rr, rm)
 
 
+def test_sts_solve_is_bit_reproducible():
+    """The STS-CP update is atomic-free (row-ordered scatter, block-ordered column norms):
+    the same step on two samplers built from the same factors gives identical bits."""
+    from paper_2301_12584_b200 import SparseTensor
+    from parity_util import sparse_tensor
+    dims, R = (900, 700, 500), 32
+    coords, values = sparse_tensor(dims, 200000, seed=77)
+    fs = pareto_factors([(d, R) for d in dims], seed=78)
+    T = SparseTensor(dims, coords, values)
+    a, b = K()(fs), K()(fs)
+    for j in range(3):
+        sa, sb = a.sts_solve(T, j, 8192, 40 + j), b.sts_solve(T, j, 8192, 40 + j)
+        assert np.array_equal(sa, sb)
+        assert np.array_equal(a.factor(j), b.factor(j))
+        assert np.array_equal(a.tree_grams(j), b.tree_grams(j))
+
+
 def test_descent_slices_give_identical_draws():
     """KRPG_OPT_SLICES: the J draws split into slices on concurrent streams give the
     same bits as one slice (the per-draw RNG stream is the global draw index)."""

@@ -222,27 +222,33 @@ def config5(args):
     warm_s = time.perf_counter() - t0
     s.profile_enable(True)
     res = []
-    for rnd in range(args.rounds):
-        for j in range(3):
-            s.profile_read(reset=True)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            s.sts_solve(T, j, J, 1000 * rnd + j)
-            torch.cuda.synchronize()
-            wall = time.perf_counter() - t0
-            pr = s.profile_read(reset=True)
-            res.append({"mode": j, "I_j": dims[j], "wall_ms": wall * 1e3, "stats": s.sts_last_stats(),
-                        "device_ms": {k: round(v["ms"], 4) for k, v in pr.items() if v["launches"]}})
+    for det in (1, 0):  # row-ordered bit-reproducible scatter (default), then fp64 atomics
+        s.set_tuning(sts_deterministic=det)
+        for rnd in range(args.rounds):
+            for j in range(3):
+                s.profile_read(reset=True)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                s.sts_solve(T, j, J, 1000 * rnd + j)
+                torch.cuda.synchronize()
+                wall = time.perf_counter() - t0
+                pr = s.profile_read(reset=True)
+                res.append({"mode": j, "I_j": dims[j], "wall_ms": wall * 1e3, "stats": s.sts_last_stats(),
+                            "deterministic": det,
+                            "device_ms": {k: round(v["ms"], 4) for k, v in pr.items() if v["launches"]}})
+    s.set_tuning(sts_deterministic=1)
     free, total = torch.cuda.mem_get_info()
     for j in range(3):
-        walls = [r["wall_ms"] for r in res if r["mode"] == j]
-        last = [r for r in res if r["mode"] == j][-1]
+        walls = [r["wall_ms"] for r in res if r["mode"] == j and r["deterministic"]]
+        walls_at = [r["wall_ms"] for r in res if r["mode"] == j and not r["deterministic"]]
+        last = [r for r in res if r["mode"] == j and r["deterministic"]][-1]
         print(json.dumps({"config": "config5", "workload": "STS-CP factor update (krpg_sts_solve)",
                           "dims": dims, "R": R, "J": J, "raw_nnz": nnz, "nnz": T.nnz(),
                           "scaled": ("full raw nonzero count 1.7e9" if nnz >= 1_700_000_000 else
                                      f"raw nonzeros {nnz:.3g} instead of 1.7e9") +
                                     " (synthetic Zipf(1.1) tensor, lognormal values; one GPU)",
                           "mode": j, "ms_per_update_median": float(np.median(walls)),
+                          "ms_per_update_median_atomic_scatter": float(np.median(walls_at)),
                           "device_ms_breakdown_last": last["device_ms"], "step_stats_last": last["stats"],
                           "ingest_s": ingest_s, "first_solves_incl_fiber_indexes_s": warm_s,
                           "device_mem_used_gb": (total - free) / 1e9}), flush=True)
