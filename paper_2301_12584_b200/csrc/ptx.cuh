@@ -69,7 +69,9 @@ __device__ __forceinline__ void cp_async_wait_n() {  // all but the N newest gro
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// D(8x8) += A(8x4) * B(4x8), fp64 tensor core (DMMA.8x8x4)
+// D(8x8) += A(8x4) * B(4x8), fp64 tensor core (DMMA.8x8x4). `volatile` is required:
+// mma.sync.aligned is warp-collective, and a non-volatile asm may be moved into divergent
+// control flow (measured: no speed-up, and a kernel hung when it was dropped)
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
