@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--seed", type=int, default=2301)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--tune", nargs="*", default=[], metavar="KEY=VALUE",
+                   help="kernel-variant / tuning options for A/B runs (KrpSampler.set_tuning keys)")
     return p.parse_args()
 
 
@@ -314,6 +316,8 @@ def run_ours(args):
     fs = make_factors(args, dev)
     torch.cuda.synchronize()
     s = KrpSampler.from_device(fs, device=local)
+    if args.tune:
+        s.set_tuning(**{k: int(v) for k, v in (t.split("=", 1) for t in args.tune)})
     R, N, J = args.R, args.N, args.J
     dims = [args.I] * N
 
@@ -476,6 +480,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": bench_config(args, world),
             "issue": "asynchronous calls (KRPG_OPT_ASYNC): host setup overlaps the previous step's kernels",
+            "tuning": dict(t.split("=", 1) for t in args.tune) or "defaults",
             "roofline": ({"bound": "hbm", "kernel": "k_draws (batched root-to-leaf descent)",
                           "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                           "traffic": traffic, "peak_kind": peak_kind,

@@ -1,7 +1,7 @@
 // One grouped-descent level in isolation (config-2 shape: J = 65536 draws, R = 64, all draws
 // in one node run as at the top of the tree), timed with events per launch:
 //   usage: level_bench [J] [nruns]   (nruns: the draws are spread over that many node runs)
-// Variants: KRPG_EVAL_QUAD / KRPG_EVAL_REG select the kernel as in the library;
+// The level kernel as the library launches it (default tuning);
 // KRPG_FAKE_QF=1 skips the DMMA, =2 also the row / Gram loads (k_eval_reg only).
 #define KRPG_LEVEL_BENCH 1
 #include "../../paper_2301_12584_b200/csrc/descent_v2.cu"
