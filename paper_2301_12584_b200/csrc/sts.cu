@@ -215,6 +215,7 @@ __global__ void k_fiber_scatter(const uint32_t* __restrict__ ug, const uint32_t*
 }
 
 // ---- deterministic row-ordered scatter (replaces the atomic fiber scatter) ----
+// gram_cross(SA, SB) of cp_als.cpp:290-294 without the dense J x I_j SB block (:128):
 // M[i] = sum over the sampled fibers' entries with coordinate i of v_e S[sg_e], in the
 // fixed order (fiber slot sg ascending, entry ascending): every visited entry gets its
 // position e in that order, a stable radix sort by row groups them, and each row is summed
