@@ -28,6 +28,15 @@ namespace krpg {
 
 namespace {
 
+// timing-experiment switch of the leaf microbenchmark (tools/microbench/leaf_bench.cu);
+// always false in the library
+#ifdef KRPG_LEAF_BENCH
+__device__ int g_leaf_exp = 0;
+#define LEAF_EXP(x) (g_leaf_exp == (x))
+#else
+#define LEAF_EXP(x) false
+#endif
+
 struct PosGeom {
     uint64_t I, F, npos, hb, pos_node0, left_slot0;
     uint64_t p0, p1;  // positions processed by this launch: [p0, p1) (a partition's subtree)
@@ -224,7 +233,7 @@ __global__ void __launch_bounds__(LeafCfg<NB, T, MINB, STAGES>::WPC * 32, MINB)
         fence_proxy_async();
         __syncwarp();
         crow += C::CH;
-        if (crow == crs) {  // left leaf of a pair complete: it is a left child -> stored
+        if (crow == crs && !LEAF_EXP(1)) {  // left leaf of a pair complete: it is a left child -> stored
             store_tiles<NB>(acc, lane, compact + (g.left_slot0 + cj) * P, nullptr);
         }
         if (crow >= cr1) {
@@ -235,13 +244,172 @@ __global__ void __launch_bounds__(LeafCfg<NB, T, MINB, STAGES>::WPC * 32, MINB)
                 d0 = d1;
                 d1 = nullptr;
             }
-            if (d0) store_tiles<NB>(acc, lane, d0, d1);
+            if (d0 && !LEAF_EXP(1)) store_tiles<NB>(acc, lane, d0, d1);
 #pragma unroll
             for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
             cj += nw;
             if (cj < g.p1) pos_rows(g, cj, crow, crs, cr1);
         }
     }
+}
+
+// ---- staged-store variant -------------------------------------------------
+// k_leaf_dmma's accumulator layout (strided column blocks) scatters every Gram as
+// 8-byte stores over the whole packed triangle: each one occupies a 32-byte L2 sector
+// slot, and the 1.6 GB of Grams per config-2 factor cost as much L2 write bandwidth as
+// 6.5 GB would (measured: 1.17 ms with the stores, 0.65 ms without). Here a finished
+// Gram is first laid out packed in a shared-memory staging buffer (NSTG per CTA, taken
+// with a shared-memory lock for the ~0.5 us a store lasts) and leaves as ONE bulk
+// shared -> global copy per destination (TMA store: full lines, one instruction). The
+// rows come in by one elected lane (no divergent per-lane issue loop).
+template <int NB, typename T, int CH_, int STAGES_, int NSTG_>
+struct LeafCfgS {
+    static constexpr int R = 8 * NB;
+    static constexpr int NT = NB * (NB + 1) / 2;
+    static constexpr int P = R * (R + 1) / 2;
+    static constexpr int CH = CH_;
+    static constexpr int STAGES = STAGES_;
+    static constexpr int NSTG = NSTG_;
+    static constexpr int ROWB = R * int(sizeof(T));
+    static constexpr int RS = ROWB + 16;
+    static constexpr int CHB = CH * RS;
+    static constexpr int WPC = 4;
+    static constexpr int STGB = (P * 8 + 127) / 128 * 128;  // staging buffer bytes
+    static constexpr int OFF_BARS = WPC * STAGES * CHB;
+    static constexpr int OFF_STG = (OFF_BARS + WPC * STAGES * 8 + 127) / 128 * 128;
+    static constexpr int OFF_LOCK = OFF_STG + NSTG * STGB;
+    static constexpr int SMEM = OFF_LOCK + 16 * ((NSTG + 3) / 4);
+    static_assert((P * 8) % 16 == 0, "bulk copies move multiples of 16 bytes");
+};
+
+template <int NB, typename T, int CH, int STAGES, int NSTG>
+__global__ void __launch_bounds__(128, 2)
+    k_leaf_dmma_s(const T* __restrict__ U, PosGeom g, double* __restrict__ compact, double* __restrict__ tout) {
+    using C = LeafCfgS<NB, T, CH, STAGES, NSTG>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* ring = smem + warp * (C::STAGES * C::CHB);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BARS) + warp * C::STAGES;
+    int* lock = reinterpret_cast<int*>(smem + C::OFF_LOCK);
+    if (threadIdx.x < C::NSTG) lock[threadIdx.x] = 0;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const uint64_t nw = uint64_t(gridDim.x) * C::WPC;
+    const uint64_t gw = g.p0 + uint64_t(blockIdx.x) * C::WPC + warp;
+    if (gw >= g.p1) return;
+    constexpr uint64_t P = C::P;
+
+    // producer cursor (runs STAGES-1 chunks ahead): one elected lane issues the chunk's rows
+    uint64_t pj = gw, prow, prs, pr1;
+    pos_rows(g, pj, prow, prs, pr1);
+    uint32_t issued = 0;
+    auto produce = [&]() {
+        if (pj >= g.p1) return;
+        const uint64_t left = pr1 - prow;
+        const uint32_t nrows = left < uint64_t(C::CH) ? uint32_t(left) : uint32_t(C::CH);
+        if (lane == 0) {
+            const int st = int(issued % C::STAGES);
+            mbar_arrive_expect_tx(&bars[st], nrows * C::ROWB);
+            unsigned char* dst = ring + st * C::CHB;
+            const T* src = U + prow * C::R;
+#pragma unroll
+            for (int r = 0; r < C::CH; ++r)
+                if (uint32_t(r) < nrows) tma_load_1d(dst + r * C::RS, src + r * C::R, C::ROWB, &bars[st]);
+        }
+        ++issued;
+        prow += C::CH;
+        if (prow >= pr1) {
+            pj += nw;
+            if (pj < g.p1) pos_rows(g, pj, prow, prs, pr1);
+        }
+    };
+    for (int s = 0; s < C::STAGES - 1; ++s) produce();
+
+    uint64_t cj = gw, crow, crs, cr1;
+    pos_rows(g, cj, crow, crs, cr1);
+    double acc[C::NT][2];
+#pragma unroll
+    for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+
+    // the finished Gram in `acc` -> d0 (and d1): staged packed in shared memory, bulk-stored
+    auto emit = [&](double* d0, double* d1) {
+        int b = -1;
+        if (lane == 0) {
+            for (;;) {
+#pragma unroll
+                for (int k = 0; k < C::NSTG; ++k)
+                    if (b < 0 && atomicCAS(&lock[k], 0, 1) == 0) b = k;
+                if (b >= 0) break;
+                __nanosleep(100);
+            }
+        }
+        b = __shfl_sync(0xffffffffu, b, 0);
+        double* stg = reinterpret_cast<double*>(smem + C::OFF_STG + b * C::STGB);
+        store_tiles<NB>(acc, lane, stg, nullptr);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_1d(d0, stg, uint32_t(P * 8));
+            if (d1) tma_store_1d(d1, stg, uint32_t(P * 8));
+            tma_store_commit();
+            tma_store_wait_read();  // the buffer has been read: hand it back
+            __threadfence_block();
+            atomicExch(&lock[b], 0);
+        }
+        __syncwarp();
+    };
+
+    const int frow = lane & 3;
+    const int fcol = (lane >> 2) * NB * int(sizeof(T));
+    for (uint32_t i = 0; cj < g.p1; ++i) {
+        produce();
+        const int st = int(i % C::STAGES);
+        mbar_wait(&bars[st], (i / C::STAGES) & 1u);
+        const uint64_t left = cr1 - crow;
+        const int nvalid = left < uint64_t(C::CH) ? int(left) : C::CH;
+        const unsigned char* buf = ring + st * C::CHB;
+#pragma unroll
+        for (int ks = 0; ks < C::CH / 4; ++ks) {
+            const int row = ks * 4 + frow;
+            double x[NB];
+            if (row < nvalid) {
+                load_frag<NB, T>(buf + row * C::RS + fcol, x);
+            } else {
+#pragma unroll
+                for (int p = 0; p < NB; ++p) x[p] = 0.0;
+            }
+            int t = 0;
+#pragma unroll
+            for (int p = 0; p < NB; ++p)
+#pragma unroll
+                for (int q = p; q < NB; ++q, ++t) dmma_884(acc[t][0], acc[t][1], x[p], x[q]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        crow += C::CH;
+        // left leaf of a pair complete: it is a left child -> stored
+        if (crow == crs && !LEAF_EXP(1)) emit(compact + (g.left_slot0 + cj) * P, nullptr);
+        if (crow >= cr1) {
+            const uint64_t v = g.pos_node0 + cj;
+            double* d0 = tout ? tout + cj * P : nullptr;
+            double* d1 = stored(v) ? compact + slot_of(v) * P : nullptr;
+            if (!d0) {
+                d0 = d1;
+                d1 = nullptr;
+            }
+            if (d0 && !LEAF_EXP(1)) emit(d0, d1);
+#pragma unroll
+            for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+            cj += nw;
+            if (cj < g.p1) pos_rows(g, cj, crow, crs, cr1);
+        }
+    }
+    if (lane == 0) tma_store_wait_all();
 }
 
 // ---- large ranks (R = 96 .. 256, R % 32 == 0): one CTA per position ------
@@ -505,6 +673,7 @@ void launch_subtree(const double* child, double* top, double* compact, uint32_t 
 
 int sm_count() { return sm_count_current(); }
 
+
 template <int NB, typename T, int MINB, int STAGES>
 void launch_dmma_v(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s) {
     using C = LeafCfg<NB, T, MINB, STAGES>;
@@ -516,12 +685,39 @@ void launch_dmma_v(const T* U, const PosGeom& g, double* compact, double* tout, 
     kern<<<unsigned(grid), C::WPC * 32, C::SMEM, s>>>(U, g, compact, tout);
 }
 
+// ring depth of the staged-store kernel: as deep as lets two CTAs share an SM (2..4 stages)
+template <int NB, typename T, int CH>
+constexpr int staged_stages() {
+    constexpr int R = 8 * NB;
+    constexpr int stage = 4 * CH * (R * int(sizeof(T)) + 16);
+    constexpr int stg = 2 * ((R * (R + 1) / 2 * 8 + 127) / 128 * 128);
+    constexpr int fit = (110 * 1024 - stg) / stage;
+    return fit < 2 ? 2 : (fit > 4 ? 4 : fit);
+}
+
+template <int NB, typename T, int CH, int STAGES, int NSTG>
+void launch_dmma_s(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s) {
+    using C = LeafCfgS<NB, T, CH, STAGES, NSTG>;
+    auto kern = k_leaf_dmma_s<NB, T, CH, STAGES, NSTG>;
+    smem_optin(kern, C::SMEM);
+    const int occ = occupancy(kern, C::WPC * 32, C::SMEM);
+    const uint64_t need = (g.p1 - g.p0 + C::WPC - 1) / C::WPC;
+    const uint64_t grid = std::min<uint64_t>(need, uint64_t(sm_count()) * occ);
+    kern<<<unsigned(grid), C::WPC * 32, C::SMEM, s>>>(U, g, compact, tout);
+}
+
 // 2 CTAs x 4 warps per SM with 4-stage rings: forcing 3 CTAs (168 registers, 3 stages) or
 // 4 CTAs (128 registers, 2 stages) spills accumulators and measured 1.59 / 2.71 ms per
 // config-2 leaf build against 1.19 ms (profiles/r02_tree_variants.jsonl)
 template <int NB, typename T>
-void launch_dmma(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s, int) {
-    launch_dmma_v<NB, T, 2, 4>(U, g, compact, tout, s);
+void launch_dmma(const T* U, const PosGeom& g, double* compact, double* tout, cudaStream_t s, int variant) {
+    // small Grams (R <= 16: at most 1 KB) are cheaper to scatter straight from the registers
+    // than to stage (measured per 2^22-row factor, staged / direct: R = 8 0.245 / 0.168 ms,
+    // 16 0.204 / 0.189, 24 0.247 / 0.351, 32 0.400 / 0.426, 48 0.53 / 0.88, 64 0.79 / 1.17)
+    if (variant == 1 || NB <= 2) return launch_dmma_v<NB, T, 2, 4>(U, g, compact, tout, s);
+    // 16-row chunks when the leaf boundary (a multiple of F) falls on a chunk boundary
+    if (g.F % 16 == 0) return launch_dmma_s<NB, T, 16, staged_stages<NB, T, 16>(), 2>(U, g, compact, tout, s);
+    launch_dmma_s<NB, T, 8, staged_stages<NB, T, 8>(), 2>(U, g, compact, tout, s);
 }
 
 template <int R_, typename T>
