@@ -190,6 +190,9 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
  * norms (bit-reproducible factor updates); 0 the fp64-atomic fiber scatter (faster on
  * large tensors, sums in run-dependent order) */
 #define KRPG_OPT_STS_DETERMINISTIC 25
+/* R <= 64: the levels >= 1 of a sampling stage run in ONE cooperatively launched kernel with
+ * grid barriers between the levels (default 1; 0: one launch per level; same bits) */
+#define KRPG_OPT_EVAL_ML 26
 int krpg_set_option(krpg_t h, int option, int64_t value);
 /* 1 for the bounds-checked library (make CHECKED=1, device asserts), 0 for production */
 int krpg_is_checked_build(void);

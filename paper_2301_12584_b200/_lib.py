@@ -124,7 +124,7 @@ OPT_SLICES = 5
 OPT_HOST_TRACE = 6
 # kernel-variant / tuning options (include/krpg.h)
 TUNING = {"eval_reg": 16, "pos0_tables": 17, "deep_threshold": 18, "deep_chunk": 19, "eval_split": 20,
-          "deep_dmma_min": 21, "leaf_par": 22, "out_slices": 23, "sts_deterministic": 25}
+          "deep_dmma_min": 21, "leaf_par": 22, "out_slices": 23, "sts_deterministic": 25, "eval_ml": 26}
 
 _lib: C.CDLL | None = None
 

@@ -79,6 +79,7 @@ struct EvalArgs {
 
 // timing-experiment switch of the level microbenchmark; always 0 in the library
 #ifdef KRPG_LEVEL_BENCH
+__device__ int g_ml_dbg = 0;  // multi-level kernel: 1 skip the tiles of levels >= 1, 2 skip the grid barrier
 #define EV_FAKE(a) ((a).fake)
 #else
 #define EV_FAKE(a) 0
@@ -416,24 +417,22 @@ __device__ __forceinline__ double block_qf_regs(const double (&gf)[NB * (NB + 1)
 // keep the FP64 tensor pipe busy; branch decisions, ranks, slot claims and the
 // next level's order are then computed for all of the warp's positions at once
 // (two per lane, run membership from ballot masks).
-template <int NB, int MODE, bool ROOT0, bool WGT = false>
-__global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t range) {
+// One warp's tile of a level: the sorted positions [p0, p0 + cnt), cnt <= RRANGE. `wsmem` is
+// the warp's shared-memory area (RegCfg::WARP_STRIDE bytes), `bar` its RSLOTS mbarriers
+// (initialised by the kernel, count 1) and `phase` their parities (bit sl: parity of slot
+// sl's next completion; 0 after the initialisation, carried from tile to tile).
+template <int NB, int MODE, bool ROOT0, bool WGT>
+__device__ __forceinline__ void eval_reg_tile(const EvalArgs& a, const uint64_t p0, const int cnt,
+                                              unsigned char* wsmem, uint64_t* bar, uint32_t& phase,
+                                              unsigned long long* tr) {
     constexpr int R = 8 * NB;
     constexpr uint64_t P = uint64_t(R) * (R + 1) / 2;
     using C = RegCfg<NB>;
     constexpr unsigned FULL = 0xffffffffu;
     constexpr bool LEVEL = MODE == EV_LEVEL;
-    extern __shared__ __align__(16) unsigned char smem_regb[];
-    __shared__ __align__(8) uint64_t s_bar[RW][RSLOTS];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    griddep_launch_dependents();
-    griddep_wait();
-    const uint64_t p0 = (uint64_t(blockIdx.x) * RW + warp) * range;
-    if (p0 >= a.J) return;
-    const int cnt = int(a.J - p0 < uint64_t(range) ? a.J - p0 : uint64_t(range));
-    unsigned long long* tr = a.trace ? a.trace + ((uint64_t(blockIdx.x) * RW + warp) * 16) : nullptr;
+    const int lane = threadIdx.x & 31;
     if (tr && lane == 0) tr[0] = gtimer();
-    double* ring = reinterpret_cast<double*>(smem_regb + warp * C::WARP_STRIDE);
+    double* ring = reinterpret_cast<double*>(wsmem);
     double* s_u = ring + RSLOTS * C::SLOT;
     double* s_ic = s_u + RRANGE;
     double* s_lo = s_ic + RRANGE;
@@ -448,7 +447,6 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     uint32_t* s_bl = s_pge + RRANGE;    // claimed bases of the run's left / right part
     uint32_t* s_br = s_bl + RRANGE;
     uint16_t* s_blk = reinterpret_cast<uint16_t*>(s_br + RRANGE);
-    uint64_t* bar = s_bar[warp];
 
     // the warp's sorted positions p0 + lane (A) and p0 + 32 + lane (B)
     uint32_t dA = 0, dB = 0, vA = 0xFFFFFFFFu, vB = 0xFFFFFFFFu;
@@ -478,11 +476,6 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     auto run_of = [&](int t) { return __popcll(static_cast<long long>(starts & ((2ull << t) - 1ull))) - 1; };
     auto parked = [&](uint32_t v) { return LEVEL && !ROOT0 && is_leaf(a.topo, v); };
 
-    if (lane == 0) {
-#pragma unroll
-        for (int sl = 0; sl < RSLOTS; ++sl) mbar_init(&bar[sl], 1);
-        fence_mbar_init();
-    }
     // the first run's Gram (root Gram for the normaliser pass) is requested now, so
     // its latency overlaps the input staging and the block list
     double gf[C::NFR];
@@ -561,7 +554,6 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
     KRPG_DCHECK(nblk <= RMAXBLK && nruns <= RRANGE && cnt <= RRANGE);
     if (tr && lane == 0) tr[2] = gtimer();
 
-    uint32_t phase = 0;  // bit sl: parity of slot sl's next completion
     auto issue = [&](int i) {  // rows of block i -> ring slot i % RSLOTS (1-D TMA, one copy per row)
         if (i >= nblk || EV_FAKE(a) >= 2) return;
         const uint32_t e = s_blk[i];
@@ -724,6 +716,93 @@ __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t ra
         }
     }
     if (tr && lane == 0) tr[5] = gtimer();
+}
+
+template <int NB, int MODE, bool ROOT0, bool WGT = false>
+__global__ void __launch_bounds__(RW * 32, 2) k_eval_reg(EvalArgs a, uint32_t range) {
+    using C = RegCfg<NB>;
+    extern __shared__ __align__(16) unsigned char smem_regb[];
+    __shared__ __align__(8) uint64_t s_bar[RW][RSLOTS];
+    const int warp = threadIdx.x >> 5;
+    griddep_launch_dependents();
+    griddep_wait();
+    const uint64_t p0 = (uint64_t(blockIdx.x) * RW + warp) * range;
+    if (p0 >= a.J) return;
+    const int cnt = int(a.J - p0 < uint64_t(range) ? a.J - p0 : uint64_t(range));
+    unsigned long long* tr = a.trace ? a.trace + ((uint64_t(blockIdx.x) * RW + warp) * 16) : nullptr;
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int sl = 0; sl < RSLOTS; ++sl) mbar_init(&s_bar[warp][sl], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t phase = 0;
+    eval_reg_tile<NB, MODE, ROOT0, WGT>(a, p0, cnt, smem_regb + warp * C::WARP_STRIDE, s_bar[warp], phase, tr);
+}
+
+// Grid-wide barrier of a cooperatively launched (fully resident) grid: the pattern of
+// cooperative groups' grid.sync() on a caller-provided counter that starts at zero
+// (the n-th barrier waits for n * gridDim.x arrivals): release arrival after the CTA barrier,
+// acquire polling (which invalidates the SM's L1) before it, so plain loads see the other CTAs' data.
+__device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t seen;
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(seen) : "l"(ctr) : "memory");
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+        } while (seen < target);
+    }
+    __syncthreads();
+}
+
+// Several consecutive levels in ONE cooperative launch (levels >= 1 of a stage): the same
+// per-warp tile routine, a grid barrier where the kernel boundary was, the sorted-order
+// buffers swapped in place. Same arithmetic, bit-identical draws; saves the launch, drain
+// and ramp of a kernel boundary per level (the level kernels are latency bound, DESIGN 3).
+// Persistent: warp w takes tiles w, w + #warps, ... so any J runs in one resident wave.
+template <int NB, bool WGT>
+__global__ void __launch_bounds__(RW * 32, 2) k_eval_reg_ml(EvalArgs a, uint32_t range, uint32_t nlev, uint32_t* gbar) {
+    using C = RegCfg<NB>;
+    extern __shared__ __align__(16) unsigned char smem_regb[];
+    __shared__ __align__(8) uint64_t s_bar[RW][RSLOTS];
+    const int warp = threadIdx.x >> 5;
+    griddep_launch_dependents();
+    griddep_wait();
+    const uint64_t nwarps = uint64_t(gridDim.x) * RW, gw = uint64_t(blockIdx.x) * RW + warp;
+    const uint64_t ntiles = (a.J + range - 1) / range;
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int sl = 0; sl < RSLOTS; ++sl) mbar_init(&s_bar[warp][sl], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t phase = 0;
+    for (uint32_t li = 0;; ++li) {
+        for (uint64_t t = gw; t < ntiles; t += nwarps) {
+            const uint64_t p0 = t * range;
+            const int cnt = int(a.J - p0 < uint64_t(range) ? a.J - p0 : uint64_t(range));
+#ifdef KRPG_LEVEL_BENCH
+            if (g_ml_dbg == 1 && li > 0) continue;
+#endif
+            eval_reg_tile<NB, EV_LEVEL, false, WGT>(a, p0, cnt, smem_regb + warp * C::WARP_STRIDE, s_bar[warp], phase,
+                                                    nullptr);
+            __syncwarp();
+        }
+        if (li + 1 == nlev) break;
+#ifdef KRPG_LEVEL_BENCH
+        if (g_ml_dbg != 2)
+#endif
+        grid_barrier(gbar, (li + 1) * gridDim.x);
+        const uint32_t* pn = a.perm_out;
+        a.perm_out = const_cast<uint32_t*>(a.perm);
+        a.perm = pn;
+        if (a.nsort_in) {
+            const uint32_t* nn = a.nsort_out;
+            a.nsort_out = const_cast<uint32_t*>(a.nsort_in);
+            a.nsort_in = nn;
+        }
+    }
 }
 
 // ---- R = 64 / 128: the Gram split over the 4 warps of a CTA (register-resident) ----
@@ -1498,10 +1577,12 @@ __global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a) {
 // stage init: identity order, everyone at the root, this stage's uniform
 __global__ void k_stage_init(uint32_t* perm, uint32_t* node, double* low, double* ud, uint32_t* gstart,
                              uint64_t J, uint64_t seed, uint64_t off, uint64_t counter, double* margin,
-                             int reset_margin, uint32_t* cntL, uint32_t* cntR, uint64_t nnodes, uint32_t* zero1) {
+                             int reset_margin, uint32_t* cntL, uint32_t* cntR, uint64_t nnodes, uint32_t* zero1,
+                             uint32_t* zero2) {
     griddep_launch_dependents();
     griddep_wait();
     if (zero1 && blockIdx.x == 0 && threadIdx.x == 0) *zero1 = 0;
+    if (zero2 && blockIdx.x == 0 && threadIdx.x == 0) *zero2 = 0;
     for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nnodes; v += uint64_t(gridDim.x) * blockDim.x) {
         cntL[v] = 0;
         cntR[v] = 0;
@@ -2616,6 +2697,51 @@ void launch_reg(const EvalArgs& a, cudaStream_t s) {
 // register-resident single-warp kernel measured faster (2.41 vs 2.83 ms per config-2 step)
 inline bool eval_split_on(const Tuning& t, int NB) { return t.eval_split == 1 || t.eval_split == NB; }
 
+// levels [l, l + nlev) of a stage in one cooperative launch (a.perm / a.perm_out etc. are
+// level l's; the kernel swaps them per level). Returns false if the device refuses the launch
+// (the caller then launches level by level).
+template <int NB, bool WGT>
+bool launch_reg_ml(const EvalArgs& a, uint32_t nlev, uint32_t* gbar, cudaStream_t s) {
+    using C = RegCfg<NB>;
+    auto kern = k_eval_reg_ml<NB, WGT>;
+    const int ctas = sm_count_current() * occupancy(kern, RW * 32, C::SMEM);
+    const uint64_t slots = uint64_t(ctas) * RW;
+    uint64_t range = (a.J + slots - 1) / slots;
+    range = std::min<uint64_t>(std::max<uint64_t>((range + 7) / 8 * 8, 8), RRANGE);
+    const uint64_t ntiles = (a.J + range - 1) / range;
+    const unsigned grid = unsigned(std::min<uint64_t>((ntiles + RW - 1) / RW, uint64_t(ctas)));
+    EvalArgs arg = a;
+    uint32_t r32 = uint32_t(range);
+    void* params[] = {&arg, &r32, &nlev, &gbar};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(RW * 32), params, C::SMEM,
+                                       s) == cudaSuccess;
+}
+
+template <int NB>
+bool launch_eval_ml(const EvalArgs& a, uint32_t nlev, uint32_t* gbar, cudaStream_t s, const Tuning& t) {
+    if constexpr (NB <= 8) {
+        if (!t.eval_reg || !t.eval_ml || !gbar || nlev < 2) return false;
+        if (NB == 8 && eval_split_on(t, NB)) return false;
+        if (a.W) return launch_reg_ml<NB, true>(a, nlev, gbar, s);
+        return launch_reg_ml<NB, false>(a, nlev, gbar, s);
+    }
+    return false;
+}
+
+bool dispatch_eval_ml(uint32_t R, const EvalArgs& a, uint32_t nlev, uint32_t* gbar, cudaStream_t s, const Tuning& t) {
+    if (R % 8 != 0 || R > 64) return false;
+    switch (R / 8) {
+        case 1: return launch_eval_ml<1>(a, nlev, gbar, s, t);
+        case 2: return launch_eval_ml<2>(a, nlev, gbar, s, t);
+        case 3: return launch_eval_ml<3>(a, nlev, gbar, s, t);
+        case 4: return launch_eval_ml<4>(a, nlev, gbar, s, t);
+        case 5: return launch_eval_ml<5>(a, nlev, gbar, s, t);
+        case 6: return launch_eval_ml<6>(a, nlev, gbar, s, t);
+        case 7: return launch_eval_ml<7>(a, nlev, gbar, s, t);
+        default: return launch_eval_ml<8>(a, nlev, gbar, s, t);
+    }
+}
+
 template <int NB, int MODE, bool ROOT0, bool WGT = false>
 void launch_split(const EvalArgs& a, cudaStream_t s) {
     smem_optin(k_eval_split<NB, MODE, ROOT0, WGT>, SplitCfg<NB>::SMEM);
@@ -2805,7 +2931,8 @@ static int launch_position_one_stage(const GroupedArgs& g) {
     const Topo tz = make_topo(g.I, R);
     uint32_t* work = reinterpret_cast<uint32_t*>(g.pos0_tab);  // leaf-kernel counter (tables unused here)
     launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
-               g.draw_offset, uint64_t(g.pos) + 1, g.margin, int(g.pos == 0), g.cntL, g.cntR, uint64_t(tz.n), work);
+               g.draw_offset, uint64_t(g.pos) + 1, g.margin, int(g.pos == 0), g.cntL, g.cntR, uint64_t(tz.n), work,
+               (uint32_t*)nullptr);
     int launches = 1;
     EvalArgs e{};
     e.J = J;
@@ -2892,7 +3019,7 @@ int launch_position_grouped(const GroupedArgs& g) {
     const Topo te = make_topo(R, 1);
     launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
                g.draw_offset, 2ull * g.pos + 1, g.margin, int(g.pos == 0), g.cntL, g.cntR, uint64_t(te.n),
-               (uint32_t*)nullptr);
+               (uint32_t*)nullptr, g.gbar);
     ++launches;
     mark(13);
     e.GS = g.gstart;
@@ -2926,6 +3053,16 @@ int launch_position_grouped(const GroupedArgs& g) {
             e.perm_out = pout;
             e.nsort_in = (l == 0 || !nin) ? nullptr : nin;
             e.nsort_out = nout;
+            // levels l .. lcta - 1 in one cooperative launch with grid barriers (R <= 64)
+            if (l >= 1 && lcta - l >= 2 && dispatch_eval_ml(R, e, lcta - l, g.gbar, g.stream, g.tune)) {
+                ++launches;
+                mark(9);
+                if ((lcta - l) & 1u) {
+                    std::swap(pin, pout);
+                    std::swap(nin, nout);
+                }
+                break;
+            }
             dispatch_eval(R, (l == 0 && R <= 160) ? EV_LEVEL0 : EV_LEVEL, e, g.stream, g.tune);
             ++launches;
             mark(9);
@@ -2971,7 +3108,7 @@ int launch_position_grouped(const GroupedArgs& g) {
 
     // ---------------- stage 2: factor tree, rank-1 M = z z^T ----------------
     launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
-               g.draw_offset, 2ull * g.pos + 2, g.margin, 0, g.cntL, g.cntR, uint64_t(tz.n), deep_work);
+               g.draw_offset, 2ull * g.pos + 2, g.margin, 0, g.cntL, g.cntR, uint64_t(tz.n), deep_work, g.gbar);
     ++launches;
     mark(13);
     e.X = g.Zb;

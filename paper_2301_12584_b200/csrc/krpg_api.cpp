@@ -573,7 +573,7 @@ struct krpg_sampler {
             // draw slices on concurrent streams: the level kernels of one slice are
             // latency bound, so a second independent slice fills the SMs' idle phases
             const int S = (prof_on && prof_detail) ? 1 : int(std::max<uint64_t>(1, std::min<uint64_t>(nslices, J / 8192)));
-            char* st = static_cast<char*>(gstate.ensure(Ju * (4 * 6 + 8 * 3) + S * nmax * 4 * 4 + 1024 * (S + 3) +
+            char* st = static_cast<char*>(gstate.ensure(Ju * (4 * 6 + 8 * 3) + S * nmax * 4 * 4 + 1024 * (S + 3) + 128 * S +
                                                         S * (8 * krpg::pos0_tab_doubles(R) + 128)));
             auto carve = [&](size_t bytes) {
                 char* p = st;
@@ -596,6 +596,7 @@ struct krpg_sampler {
             g.cntR = reinterpret_cast<uint32_t*>(carve(4 * nmax * S));
             double* pos0_tab = reinterpret_cast<double*>(carve(8 * krpg::pos0_tab_doubles(R) * S));
             g.pos0_tab = pos0_tab;
+            g.gbar = reinterpret_cast<uint32_t*>(carve(128 * S));
             g.Zb = static_cast<double*>(zbuf.ensure(sizeof(double) * J * R));
             g.R = R;
             g.N = N;
@@ -710,6 +711,7 @@ struct krpg_sampler {
                     gs.gend = g.gend + sl * nmax;
                     gs.cntL = g.cntL + sl * nmax;
                     gs.cntR = g.cntR + sl * nmax;
+                    gs.gbar = g.gbar + sl * 32;
                     gs.pos0_tab = pos0_tab + sl * krpg::pos0_tab_doubles(R);
                     gs.stream = sl == 0 ? stream : slice_stream(sl);
                     if (sl > 0) CK(cudaStreamWaitEvent(gs.stream, fork_ev(), 0));
@@ -2166,6 +2168,8 @@ int krpg_set_option(krpg_t h, int option, int64_t value) {
         else if (option == KRPG_OPT_OUT_SLICES) {
             require(value >= 1 && value <= 4, "krpg_set_option: output slices must be in [1, 4]");
             h->tune.out_slices = int(value);
+        } else if (option == KRPG_OPT_EVAL_ML) {
+            h->tune.eval_ml = value != 0;
         } else if (option == KRPG_OPT_LEAF_PAR) {
             require(value >= 0 && value <= 64, "krpg_set_option: leaf scan parallel bound must be in [0, 64]");
             h->tune.leaf_par = int(value);

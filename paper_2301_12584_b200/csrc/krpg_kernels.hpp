@@ -92,6 +92,7 @@ struct Tuning {
     int deep_dmma_min = 1;     // deep-pass runs with fewer draws use CUDA-core forms
     int leaf_par = 8;          // leaf runs with at most this many draws scan warp-parallel
     int sts_deterministic = 1; // STS-CP scatter: 1 row-ordered (bit-reproducible), 0 fp64 atomics (faster)
+    int eval_ml = 1;           // R <= 64: a stage's levels >= 1 in one cooperative launch with grid barriers
     int out_slices = 2;        // krpg_sample into page-locked host memory: draw slices of the
                                // last position whose copies overlap the following slices (1..4)
 };
@@ -117,6 +118,7 @@ struct GroupedArgs {
     int fused_deep;                    // deep levels + leaf in one warp-local pass
     int h_ones;                        // H is all ones (first included position): table shortcut
     double* pos0_tab;                  // scratch for the first-position tables (pos0_tab_doubles(R)), nullable
+    uint32_t* gbar;                    // grid-barrier counter of the multi-level level kernel (zeroed per stage), nullable
     Tuning tune;
     int final_rows;                    // fused deep pass forms h o= U_k[pick] itself (no k_apply_pick)
     double* host_rows;                 // with final_rows: device-mapped page-locked output rows, nullable

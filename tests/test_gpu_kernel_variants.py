@@ -6,7 +6,8 @@ computed once per (node, eigen-component) when h = ones) are claimed to apply
 exactly the arithmetic of the per-draw DMMA quadratic form (block_qf_packed) to
 exactly the same operands, so every branch decision, probability, row and
 margin must equal the k_eval_cta path bit for bit -- and so must other deep /
-shallow splits and deep-pass work-unit sizes. The variants are per-handle
+shallow splits and deep-pass work-unit sizes, and the multi-level cooperative launch
+(k_eval_reg_ml: grid barriers instead of kernel boundaries). The variants are per-handle
 options (krpg_set_option, KRPG_OPT_EVAL_REG ...), switched on one sampler.
 """
 import numpy as np
@@ -38,6 +39,7 @@ def same(a, b, what):
     ([(1 << 16, 64), (40000, 64), (50000, 64)], 32768),   # level kernel + deep pass + first-position tables
     ([(20000, 32), (30000, 32), (9000, 32)], 20000),      # R = 32, J not a multiple of the warp ranges
     ([(5000, 24), (3000, 24)], 4096),                     # non-power-of-two E-tree (parked leaves)
+    ([(70000, 64), (3000, 64)], 200000),                  # several tiles per warp in the multi-level kernel
 ])
 def test_level_kernel_and_tables_bit_identical(shapes, J):
     from paper_2301_12584_b200 import KrpSampler
@@ -47,7 +49,9 @@ def test_level_kernel_and_tables_bit_identical(shapes, J):
     base = draws(s, len(shapes), J)
     for opts in ({"eval_reg": 1, "pos0_tables": 0}, {"eval_reg": 0, "pos0_tables": 1},
                  {"eval_reg": 1, "pos0_tables": 1}, {"deep_threshold": 64}, {"deep_threshold": 16},
-                 {"deep_chunk": 32}, {"deep_chunk": 3}):
+                 {"deep_chunk": 32}, {"deep_chunk": 3},
+                 # one launch per level instead of the multi-level cooperative launch, and back
+                 {"eval_ml": 0}, {"eval_ml": 0, "pos0_tables": 0}, {"eval_ml": 1}, {"pos0_tables": 1}):
         s.set_tuning(**opts)
         same(base, draws(s, len(shapes), J), opts)
     # split order (R = 64: the Gram split over a CTA's warps): the split kernel on every

@@ -96,14 +96,49 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e1);
     double best = 1e30, sum = 0;
     const int K = 20;
+    const char* mlv = std::getenv("LB_ML");
+    const int ml = mlv ? std::atoi(mlv) : 0;
+    uint32_t* gbar;
+    cudaMalloc(&gbar, 128);
+    if (const char* dbg = std::getenv("LB_ML_DBG")) {
+        const int v = std::atoi(dbg);
+        cudaMemcpyToSymbol(g_ml_dbg, &v, sizeof(int));
+    }
+    // the multi-level runs rewrite the order buffers: restore them before every launch
+    uint32_t* perm0 = const_cast<uint32_t*>(a.perm);
+    uint32_t* nsort0 = const_cast<uint32_t*>(a.nsort_in);
     for (int it = 0; it < K + 3; ++it) {
         cudaMemcpyAsync(node_d, node.data(), J * 4, cudaMemcpyHostToDevice, s);
+        if (ml) {
+            cudaMemcpyAsync(perm0, perm.data(), J * 4, cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync(nsort0, nsort.data(), J * 4, cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync(a.low, low.data(), J * 8, cudaMemcpyHostToDevice, s);
+        }
         cudaMemsetAsync(a.cntR, 0, size_t(nn) * 4, s);
         cudaMemcpyAsync(cntL_d, cntL.data(), size_t(nn) * 4, cudaMemcpyHostToDevice, s);
         // level-l counters must start at zero (cntL of the parents is preset above)
         cudaMemsetAsync(cntL_d + first, 0, size_t(nruns) * 4, s);
         cudaEventRecord(e0, s);
-        dispatch_eval(R, EV_LEVEL, a, s, Tuning{});
+        if (ml >= 2) {  // LB_ML=n: n consecutive levels in one cooperative launch (k_eval_reg_ml)
+            cudaMemsetAsync(gbar, 0, 4, s);
+            cudaEventRecord(e0, s);
+            const bool ok = dispatch_eval_ml(R, a, uint32_t(ml), gbar, s, Tuning{});
+            if (!ok) std::printf("cooperative launch refused: %s\n", cudaGetErrorString(cudaGetLastError()));
+        } else if (ml == 1) {  // LB_ML=1 with LB_SEQ=n: n levels as n launches
+            const char* sq = std::getenv("LB_SEQ");
+            EvalArgs b = a;
+            for (int q = 0; q < (sq ? std::atoi(sq) : 1); ++q) {
+                dispatch_eval(R, EV_LEVEL, b, s, Tuning{});
+                const uint32_t* t = b.perm_out;
+                b.perm_out = const_cast<uint32_t*>(b.perm);
+                b.perm = t;
+                t = b.nsort_out;
+                b.nsort_out = const_cast<uint32_t*>(b.nsort_in);
+                b.nsort_in = t;
+            }
+        } else {
+            dispatch_eval(R, EV_LEVEL, a, s, Tuning{});
+        }
         cudaEventRecord(e1, s);
         cudaEventSynchronize(e1);
         float ms;
