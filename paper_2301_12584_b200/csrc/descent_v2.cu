@@ -2932,7 +2932,7 @@ static int launch_position_one_stage(const GroupedArgs& g) {
     uint32_t* work = reinterpret_cast<uint32_t*>(g.pos0_tab);  // leaf-kernel counter (tables unused here)
     launch_pdl(k_stage_init, dim3(gs), dim3(256), 0, g.stream, g.perm_a, g.node, g.low, g.ud, g.gstart, J, g.seed,
                g.draw_offset, uint64_t(g.pos) + 1, g.margin, int(g.pos == 0), g.cntL, g.cntR, uint64_t(tz.n), work,
-               (uint32_t*)nullptr);
+               g.gbar);
     int launches = 1;
     EvalArgs e{};
     e.J = J;
@@ -2957,6 +2957,15 @@ static int launch_position_one_stage(const GroupedArgs& g) {
         e.perm_out = pout;
         e.nsort_in = l == 0 ? nullptr : nin;
         e.nsort_out = nout;
+        // levels l .. d - 1 in one cooperative launch with grid barriers (R <= 64)
+        if (l >= 1 && tz.d - l >= 2 && dispatch_eval_ml(R, e, tz.d - l, g.gbar, g.stream, g.tune)) {
+            ++launches;
+            if ((tz.d - l) & 1u) {
+                std::swap(pin, pout);
+                std::swap(nin, nout);
+            }
+            break;
+        }
         dispatch_eval(R, l == 0 ? EV_LEVEL0 : EV_LEVEL, e, g.stream, g.tune);
         ++launches;
         std::swap(pin, pout);

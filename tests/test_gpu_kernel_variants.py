@@ -64,6 +64,20 @@ def test_level_kernel_and_tables_bit_identical(shapes, J):
     s.close()
 
 
+def test_one_stage_multi_level_launch_bit_identical():
+    """One-stage mode (B = G_v o Y): the multi-level cooperative launch against one launch per level."""
+    from paper_2301_12584_b200 import KrpSampler
+    s = KrpSampler(pareto_factors([(30000, 32), (9000, 32), (20000, 32)], seed=5, frac=0.01))
+    out = []
+    for ml in (0, 1):
+        s.set_tuning(eval_ml=ml)
+        b = s.sample(1, 20000, seed=99, mode="one_stage", margin=True)
+        out.append((b.indices.copy(), b.probabilities.copy(), b.rows.copy(), b.margin.copy()))
+    for x, y in zip(*out):
+        assert np.array_equal(x, y)
+    s.close()
+
+
 def test_tuning_option_errors():
     from paper_2301_12584_b200 import KrpgInvalidArgument, KrpSampler
     s = KrpSampler(pareto_factors([(300, 8), (200, 8)], seed=1))
