@@ -760,7 +760,8 @@ __device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t target) {
 // per-warp tile routine, a grid barrier where the kernel boundary was, the sorted-order
 // buffers swapped in place. Same arithmetic, bit-identical draws; saves the launch, drain
 // and ramp of a kernel boundary per level (the level kernels are latency bound, DESIGN 3).
-// Persistent: warp w takes tiles w, w + #warps, ... so any J runs in one resident wave.
+// Warp w takes tiles w, w + #warps, ...; the launcher only uses it while the level is one
+// resident wave (one tile per warp).
 template <int NB, bool WGT>
 __global__ void __launch_bounds__(RW * 32, 2) k_eval_reg_ml(EvalArgs a, uint32_t range, uint32_t nlev, uint32_t* gbar) {
     using C = RegCfg<NB>;
@@ -2709,6 +2710,10 @@ bool launch_reg_ml(const EvalArgs& a, uint32_t nlev, uint32_t* gbar, cudaStream_
     uint64_t range = (a.J + slots - 1) / slots;
     range = std::min<uint64_t>(std::max<uint64_t>((range + 7) / 8 * 8, 8), RRANGE);
     const uint64_t ntiles = (a.J + range - 1) / range;
+    // several tiles per warp (J beyond one resident wave): the static tile order of the
+    // persistent kernel balances worse than the hardware's CTA scheduling and the launch
+    // overhead is amortised anyway (config 3, J = 2^20: 34.2 ms fused against 24.1 ms)
+    if (ntiles > slots) return false;
     const unsigned grid = unsigned(std::min<uint64_t>((ntiles + RW - 1) / RW, uint64_t(ctas)));
     EvalArgs arg = a;
     uint32_t r32 = uint32_t(range);

@@ -39,7 +39,7 @@ def same(a, b, what):
     ([(1 << 16, 64), (40000, 64), (50000, 64)], 32768),   # level kernel + deep pass + first-position tables
     ([(20000, 32), (30000, 32), (9000, 32)], 20000),      # R = 32, J not a multiple of the warp ranges
     ([(5000, 24), (3000, 24)], 4096),                     # non-power-of-two E-tree (parked leaves)
-    ([(70000, 64), (3000, 64)], 200000),                  # several tiles per warp in the multi-level kernel
+    ([(70000, 64), (3000, 64)], 200000),                  # J beyond one resident wave: the multi-level launch falls back to one launch per level
 ])
 def test_level_kernel_and_tables_bit_identical(shapes, J):
     from paper_2301_12584_b200 import KrpSampler
