@@ -2718,8 +2718,11 @@ bool launch_reg_ml(const EvalArgs& a, uint32_t nlev, uint32_t* gbar, cudaStream_
     EvalArgs arg = a;
     uint32_t r32 = uint32_t(range);
     void* params[] = {&arg, &r32, &nlev, &gbar};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(RW * 32), params, C::SMEM,
-                                       s) == cudaSuccess;
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(RW * 32), params, C::SMEM,
+                                    s) == cudaSuccess)
+        return true;
+    cudaGetLastError();  // refused (e.g. fewer SMs available than the grid needs): not an error of the call
+    return false;
 }
 
 template <int NB>
