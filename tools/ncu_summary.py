@@ -28,13 +28,16 @@ def main(path):
         for k in KEYS:
             if k in d:
                 print(f"  {k:65s} {d[k]:>16s} {units[hdr.index(k)]}")
-        stalls = [(k, float(d[k].replace(',', '') or 0)) for k in hdr
-                  if k.startswith("smsp__average_warp_latency_issue_stalled") or
-                  (k.startswith("smsp__warp_issue_stalled_") and k.endswith("_per_warp_active.pct"))]
+        # warp-state samples (pc sampling), as a share of all samples
+        stalls = [(k[len("smsp__pcsamp_warps_issue_stalled_"):], float(d[k].replace(',', '') or 0)) for k in hdr
+                  if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued")]
+        tot = sum(v for _, v in stalls) or 1.0
         stalls.sort(key=lambda x: -x[1])
-        print("  top stalls:")
-        for k, v in stalls[:10]:
-            print(f"    {k:75s} {v:10.2f}")
+        print("  warp stall samples: " + ", ".join(f"{k} {100 * v / tot:.1f}%" for k, v in stalls[:8]))
+        for k in ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+                  "smsp__issue_active.avg.pct_of_peak_sustained_active"):
+            if k in d:
+                print(f"  {k:65s} {d[k]:>16s} {units[hdr.index(k)]}")
 
 
 if __name__ == "__main__":
