@@ -645,8 +645,10 @@ __global__ void __launch_bounds__(256) k_subtree_reduce(const double* __restrict
                                                         double* __restrict__ compact, uint32_t c, uint64_t j0,
                                                         uint64_t nj, uint64_t P) {
     constexpr int W = 1 << K;
-    const uint64_t j = j0 + blockIdx.x;  // parent-level (c - K) relative index
-    if (j >= nj) return;
+    // last subtrees first: the child level was just written in ascending order, so its tail
+    // is what the L2 still holds
+    const uint64_t j = nj - 1 - blockIdx.x;  // parent-level (c - K) index in [j0, nj)
+    if (j < j0 || j >= nj) return;
     for (uint64_t e = threadIdx.x; e < P; e += blockDim.x) {
         double v[W];
 #pragma unroll
