@@ -26,7 +26,7 @@ struct TreeBuildArgs {
     uint32_t parts = 1;  // > 1: build only subtree `part` of `parts` (a power of two)
     uint32_t part = 0;
     double* subroot = nullptr;  // partitioned build: receives the subtree root Gram (P)
-    int leaf_variant = 0;       // reserved (leaf-kernel variants were measured and removed)
+    int leaf_variant = 0;       // 1: the direct-store leaf kernel at every rank (A/B in tools/microbench/leaf_bench.cu)
 };
 // doubles needed for (tbuf_a, tbuf_b)
 void tree_transient_doubles(uint64_t I, uint32_t R, uint64_t* a, uint64_t* b, uint64_t F = 0, uint64_t nleaves = 0);
