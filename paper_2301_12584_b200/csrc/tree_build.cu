@@ -260,8 +260,7 @@ __global__ void __launch_bounds__(LeafCfg<NB, T, MINB, STAGES>::WPC * 32, MINB)
 // 6.5 GB would (measured: 1.17 ms with the stores, 0.65 ms without). Here a finished
 // Gram is first laid out packed in a shared-memory staging buffer (NSTG per CTA, taken
 // with a shared-memory lock for the ~0.5 us a store lasts) and leaves as ONE bulk
-// shared -> global copy per destination (TMA store: full lines, one instruction). The
-// rows come in by one elected lane (no divergent per-lane issue loop).
+// shared -> global copy per destination (TMA store: full lines, one instruction).
 template <int NB, typename T, int CH_, int STAGES_, int NSTG_>
 struct LeafCfgS {
     static constexpr int R = 8 * NB;
@@ -304,7 +303,7 @@ __global__ void __launch_bounds__(128, 2)
     if (gw >= g.p1) return;
     constexpr uint64_t P = C::P;
 
-    // producer cursor (runs STAGES-1 chunks ahead): one elected lane issues the chunk's rows
+    // producer cursor (runs STAGES-1 chunks ahead)
     uint64_t pj = gw, prow, prs, pr1;
     pos_rows(g, pj, prow, prs, pr1);
     uint32_t issued = 0;
@@ -312,15 +311,12 @@ __global__ void __launch_bounds__(128, 2)
         if (pj >= g.p1) return;
         const uint64_t left = pr1 - prow;
         const uint32_t nrows = left < uint64_t(C::CH) ? uint32_t(left) : uint32_t(C::CH);
-        if (lane == 0) {
-            const int st = int(issued % C::STAGES);
-            mbar_arrive_expect_tx(&bars[st], nrows * C::ROWB);
-            unsigned char* dst = ring + st * C::CHB;
-            const T* src = U + prow * C::R;
-#pragma unroll
-            for (int r = 0; r < C::CH; ++r)
-                if (uint32_t(r) < nrows) tma_load_1d(dst + r * C::RS, src + r * C::R, C::ROWB, &bars[st]);
-        }
+        // one lane per row (measured faster than one elected lane issuing all rows: 0.77 vs 0.79 ms)
+        const int st = int(issued % C::STAGES);
+        if (lane == 0) mbar_arrive_expect_tx(&bars[st], nrows * C::ROWB);
+        __syncwarp();
+        if (uint32_t(lane) < nrows)
+            tma_load_1d(ring + st * C::CHB + lane * C::RS, U + (prow + lane) * C::R, C::ROWB, &bars[st]);
         ++issued;
         prow += C::CH;
         if (prow >= pr1) {
