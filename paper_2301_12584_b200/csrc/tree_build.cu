@@ -41,8 +41,29 @@ struct PosGeom {
     uint64_t I, F, npos, hb, pos_node0, left_slot0;
     uint64_t p0, p1;  // positions processed by this launch: [p0, p1) (a partition's subtree)
     uint32_t R, P;
+    // 1: the transient position level holds only the right children (odd positions, at index
+    // j >> 1); a left child is read back from its compact slot by the first level pass, so it
+    // is written once instead of twice
+    uint32_t tr_half;
     const uint64_t* seg;  // variable leaf segments (device, L + 1 offsets) or null
 };
+
+// where a finished position Gram goes: d0 (and d1, nullable)
+__device__ __forceinline__ void pos_dest(const PosGeom& g, uint64_t j, double* compact, double* tout, double*& d0,
+                                         double*& d1) {
+    const uint64_t v = g.pos_node0 + j;
+    if (g.tr_half) {
+        d0 = stored(v) ? compact + slot_of(v) * g.P : tout + (j >> 1) * g.P;
+        d1 = nullptr;
+        return;
+    }
+    d0 = tout ? tout + j * g.P : nullptr;
+    d1 = stored(v) ? compact + slot_of(v) * g.P : nullptr;
+    if (!d0) {
+        d0 = d1;
+        d1 = nullptr;
+    }
+}
 
 __host__ __device__ __forceinline__ void pos_rows(const PosGeom& g, uint64_t j, uint64_t& r0,
                                                   uint64_t& rs, uint64_t& r1) {
@@ -85,6 +106,7 @@ PosGeom make_geom(uint64_t I, uint32_t R, uint64_t F = 0, uint64_t nleaves = 0, 
     g.left_slot0 = t.d ? (uint64_t{1} << (t.d - 1)) : 0;  // slot of node 2^d-1+2j is 2^(d-1)+j
     g.p0 = 0;
     g.p1 = g.npos;
+    g.tr_half = 0;
     return g;
 }
 
@@ -237,13 +259,8 @@ __global__ void __launch_bounds__(LeafCfg<NB, T, MINB, STAGES>::WPC * 32, MINB)
             store_tiles<NB>(acc, lane, compact + (g.left_slot0 + cj) * P, nullptr);
         }
         if (crow >= cr1) {
-            const uint64_t v = g.pos_node0 + cj;
-            double* d0 = tout ? tout + cj * P : nullptr;
-            double* d1 = stored(v) ? compact + slot_of(v) * P : nullptr;
-            if (!d0) {
-                d0 = d1;
-                d1 = nullptr;
-            }
+            double *d0, *d1;
+            pos_dest(g, cj, compact, tout, d0, d1);
             if (d0 && !LEAF_EXP(1)) store_tiles<NB>(acc, lane, d0, d1);
 #pragma unroll
             for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
@@ -391,13 +408,8 @@ __global__ void __launch_bounds__(128, 2)
         // left leaf of a pair complete: it is a left child -> stored
         if (crow == crs && !LEAF_EXP(1)) emit(compact + (g.left_slot0 + cj) * P, nullptr);
         if (crow >= cr1) {
-            const uint64_t v = g.pos_node0 + cj;
-            double* d0 = tout ? tout + cj * P : nullptr;
-            double* d1 = stored(v) ? compact + slot_of(v) * P : nullptr;
-            if (!d0) {
-                d0 = d1;
-                d1 = nullptr;
-            }
+            double *d0, *d1;
+            pos_dest(g, cj, compact, tout, d0, d1);
             if (d0 && !LEAF_EXP(1)) emit(d0, d1);
 #pragma unroll
             for (int t = 0; t < C::NT; ++t) acc[t][0] = acc[t][1] = 0.0;
@@ -571,13 +583,8 @@ __global__ void __launch_bounds__(BigCfg<R_, T>::NW * 32, 1)
                 if (has[k]) store_superblock<C::R>(acc[k], sp[k], sq[k], lane, dst, nullptr);
         }
         if (crow >= cr1) {
-            const uint64_t v = g.pos_node0 + cj;
-            double* d0 = tout ? tout + cj * P : nullptr;
-            double* d1 = stored(v) ? compact + slot_of(v) * P : nullptr;
-            if (!d0) {
-                d0 = d1;
-                d1 = nullptr;
-            }
+            double *d0, *d1;
+            pos_dest(g, cj, compact, tout, d0, d1);
 #pragma unroll
             for (int k = 0; k < C::SBW; ++k) {
                 if (has[k] && d0) store_superblock<C::R>(acc[k], sp[k], sq[k], lane, d0, d1);
@@ -598,7 +605,6 @@ __global__ void k_leaf_generic(const T* __restrict__ U, PosGeom g, double* __res
     for (uint64_t j = g.p0 + blockIdx.x; j < g.p1; j += gridDim.x) {
         uint64_t r0, rs, r1;
         pos_rows(g, j, r0, rs, r1);
-        const uint64_t v = g.pos_node0 + j;
         for (uint32_t k = threadIdx.x; k < P; k += blockDim.x) {
             uint32_t a, b;
             unpack_pair(R, k, a, b);
@@ -607,8 +613,10 @@ __global__ void k_leaf_generic(const T* __restrict__ U, PosGeom g, double* __res
                 acc += static_cast<double>(U[i * R + a]) * static_cast<double>(U[i * R + b]);
                 if (i + 1 == rs) compact[(g.left_slot0 + j) * P + k] = acc;
             }
-            if (tout) tout[j * P + k] = acc;
-            if (stored(v)) compact[slot_of(v) * P + k] = acc;
+            double *d0, *d1;
+            pos_dest(g, j, compact, tout, d0, d1);
+            if (d0) d0[k] = acc;
+            if (d1) d1[k] = acc;
         }
     }
 }
@@ -636,9 +644,11 @@ __global__ void k_level_reduce(const double* __restrict__ child, double* __restr
 // times in registers, writes every stored node's entry, and the subtree root's entry to
 // `top` (next pass's child level; null at the root). One pass replaces K launches and
 // reads the transient level once.
-template <int K>
+// HALF (first pass after a tr_half leaf pass): the child level holds the right children only
+// (index >> 1); the left children are read from their compact slots.
+template <int K, bool HALF>
 __global__ void __launch_bounds__(256) k_subtree_reduce(const double* __restrict__ child, double* __restrict__ top,
-                                                        double* __restrict__ compact, uint32_t c, uint64_t j0,
+                                                        double* compact, uint32_t c, uint64_t j0,
                                                         uint64_t nj, uint64_t P) {
     constexpr int W = 1 << K;
     // last subtrees first: the child level was just written in ascending order, so its tail
@@ -648,7 +658,13 @@ __global__ void __launch_bounds__(256) k_subtree_reduce(const double* __restrict
     for (uint64_t e = threadIdx.x; e < P; e += blockDim.x) {
         double v[W];
 #pragma unroll
-        for (int i = 0; i < W; ++i) v[i] = child[(j * W + i) * P + e];
+        for (int i = 0; i < W; ++i) {
+            const uint64_t ci = j * W + i;
+            if (HALF)
+                v[i] = (i & 1) ? child[(ci >> 1) * P + e] : compact[slot_of(((uint64_t{1} << c) - 1) + ci) * P + e];
+            else
+                v[i] = child[ci * P + e];
+        }
 #pragma unroll
         for (int l = 1; l <= K; ++l) {
             const uint32_t lev = c - l;  // level of the nodes formed now
@@ -665,9 +681,15 @@ __global__ void __launch_bounds__(256) k_subtree_reduce(const double* __restrict
 
 template <int K>
 void launch_subtree(const double* child, double* top, double* compact, uint32_t c, uint64_t j0, uint64_t nj,
-                    uint64_t P, cudaStream_t s) {
-    k_subtree_reduce<K><<<unsigned(nj - j0), 256, 0, s>>>(child, top, compact, c, j0, nj, P);
+                    uint64_t P, bool half, cudaStream_t s) {
+    if (half)
+        k_subtree_reduce<K, true><<<unsigned(nj - j0), 256, 0, s>>>(child, top, compact, c, j0, nj, P);
+    else
+        k_subtree_reduce<K, false><<<unsigned(nj - j0), 256, 0, s>>>(child, top, compact, c, j0, nj, P);
 }
+
+// the leaf pass of this launch writes the halved transient level (at least one level pass follows)
+bool transient_half(const PosGeom& g) { return g.p1 - g.p0 >= 2; }
 
 int sm_count() { return sm_count_current(); }
 
@@ -783,6 +805,7 @@ int launch_tree_leaves(const TreeBuildArgs& a) {
         g.p1 = g.p0 + span;
     }
     double* tout = g.npos > 1 ? a.tbuf_a : nullptr;
+    g.tr_half = transient_half(g) ? 1 : 0;
     if (a.storage == 1)
         launch_leaf<float>(static_cast<const float*>(a.U), g, a.compact, tout, a.stream, a.force_generic,
                            a.leaf_variant);
@@ -804,6 +827,16 @@ int launch_tree_levels(const TreeBuildArgs& a) {
     double* cur = a.tbuf_a;
     double* nxt = a.tbuf_b;
     int launches = 0;
+    bool half = false;  // the position level as the leaf pass left it (launch_tree_leaves)
+    {
+        PosGeom gp = g;
+        if (a.parts > 1) {
+            const uint64_t span = g.npos / a.parts;
+            gp.p0 = uint64_t(a.part) * span;
+            gp.p1 = gp.p0 + span;
+        }
+        half = transient_half(gp);
+    }
     // passes of up to 5 levels each (k_subtree_reduce): level c -> c - k
     for (int c = int(D); c > int(gl);) {
         const int k = std::min(5, c - int(gl));
@@ -814,13 +847,14 @@ int launch_tree_levels(const TreeBuildArgs& a) {
         const uint64_t j1 = a.parts > 1 ? j0 + span : nj;
         double* parent = (l > 0 || a.parts > 1) ? nxt : nullptr;
         switch (k) {
-            case 1: launch_subtree<1>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
-            case 2: launch_subtree<2>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
-            case 3: launch_subtree<3>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
-            case 4: launch_subtree<4>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
-            default: launch_subtree<5>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, a.stream); break;
+            case 1: launch_subtree<1>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, half, a.stream); break;
+            case 2: launch_subtree<2>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, half, a.stream); break;
+            case 3: launch_subtree<3>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, half, a.stream); break;
+            case 4: launch_subtree<4>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, half, a.stream); break;
+            default: launch_subtree<5>(cur, parent, a.compact, uint32_t(c), j0, j1, g.P, half, a.stream); break;
         }
         ++launches;
+        half = false;
         std::swap(cur, nxt);
         c = l;
     }
