@@ -439,7 +439,9 @@ struct BigCfg {
     // (gridDim.y) that read the same rows (the repeat reads are L2 hits when
     // the group runs concurrently; these ranks are FP64-pipe bound anyway).
     static constexpr int SPLIT = R >= 256 ? 3 : (R >= 192 ? 2 : 1);
-    static constexpr int SBW = R >= 192 ? 1 : 2;      // super-blocks per warp
+    // super-blocks per warp: one from R = 192 (registers) and at R = 128 (10 warps per CTA keep the
+    // DMMA pipe busier than 5: 1.41 -> 1.06 ms per 2^20-row factor; at R = 96 / 160 two measured better)
+    static constexpr int SBW = (R >= 192 || R == 128) ? 1 : 2;
     static constexpr int SS = (S + SPLIT - 1) / SPLIT;  // super-blocks per CTA
     static constexpr int NW = (SS + SBW - 1) / SBW;     // warps per CTA
     static constexpr int CH = 8;                      // rows per chunk (2 k-steps)
