@@ -932,7 +932,7 @@ __device__ __forceinline__ double qf_split_order(const double* __restrict__ G, c
 }
 
 template <int NB, int MODE, bool ROOT0, bool WGT = false>
-__global__ void __launch_bounds__(SPW * 32, NB <= 8 ? 4 : 2) k_eval_split(EvalArgs a) {
+__global__ void __launch_bounds__(SPW * 32, NB <= 8 ? 4 : 2) k_eval_split(EvalArgs a, uint32_t range) {
     using SC = SplitCfg<NB>;
     constexpr int R = 8 * NB;
     constexpr int SPXS = SC::XS;
@@ -960,9 +960,9 @@ __global__ void __launch_bounds__(SPW * 32, NB <= 8 ? 4 : 2) k_eval_split(EvalAr
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     griddep_launch_dependents();
     griddep_wait();
-    const uint64_t c0 = uint64_t(blockIdx.x) * SPR;
+    const uint64_t c0 = uint64_t(blockIdx.x) * range;  // range <= SPR positions per CTA
     if (c0 >= a.J) return;
-    const int cnt = int(a.J - c0 < uint64_t(SPR) ? a.J - c0 : uint64_t(SPR));
+    const int cnt = int(a.J - c0 < uint64_t(range) ? a.J - c0 : uint64_t(range));
     if (tid == 0) {
         mbar_init(&s_bar, 1);
         fence_mbar_init();
@@ -2752,9 +2752,17 @@ bool dispatch_eval_ml(uint32_t R, const EvalArgs& a, uint32_t nlev, uint32_t* gb
 
 template <int NB, int MODE, bool ROOT0, bool WGT = false>
 void launch_split(const EvalArgs& a, cudaStream_t s) {
-    smem_optin(k_eval_split<NB, MODE, ROOT0, WGT>, SplitCfg<NB>::SMEM);
-    const unsigned grid = unsigned((a.J + SPR - 1) / SPR);
-    launch_pdl(k_eval_split<NB, MODE, ROOT0, WGT>, dim3(grid), dim3(SPW * 32), SplitCfg<NB>::SMEM, s, a);
+    // whole waves: the positions per CTA are sized so that the level fills the last wave too
+    // (J = 65536 at R = 128: 1171 CTAs of 56 positions = 3.96 waves of 296 instead of 1024
+    // CTAs of 64 = 3.46 waves, the last one half empty)
+    const uint64_t ctas = uint64_t(sm_count_current()) *
+                          occupancy(k_eval_split<NB, MODE, ROOT0, WGT>, SPW * 32, SplitCfg<NB>::SMEM);
+    const uint64_t waves = (a.J + ctas * SPR - 1) / (ctas * SPR);
+    uint64_t range = (a.J + ctas * waves - 1) / (ctas * waves);
+    range = std::min<uint64_t>(std::max<uint64_t>((range + 7) / 8 * 8, 8), SPR);
+    const unsigned grid = unsigned((a.J + range - 1) / range);
+    launch_pdl(k_eval_split<NB, MODE, ROOT0, WGT>, dim3(grid), dim3(SPW * 32), SplitCfg<NB>::SMEM, s, a,
+               uint32_t(range));
 }
 
 template <int NB>
