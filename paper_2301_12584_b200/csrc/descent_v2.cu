@@ -104,7 +104,7 @@ template <int NB, bool ROOT0>
 __host__ __device__ constexpr int cta_nbuf() { return (ROOT0 || NB <= 8) ? 2 : 1; }
 
 template <int NB, int MODE, bool ROOT0 = false>
-__global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
+__global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a, uint32_t range) {
     constexpr int R = 8 * NB;
     constexpr uint32_t P = uint32_t(R) * (R + 1) / 2;
     constexpr int NBUF = cta_nbuf<NB, ROOT0>();
@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(CB) k_eval_cta(EvalArgs a) {
     // one (its perm / node / counters) before touching global state
     griddep_launch_dependents();
     griddep_wait();
-    const uint64_t base = uint64_t(blockIdx.x) * CB;
-    const int cnt = a.J - base < uint64_t(CB) ? int(a.J - base) : CB;
+    const uint64_t base = uint64_t(blockIdx.x) * range;  // range <= CB positions per CTA
+    const int cnt = a.J - base < uint64_t(range) ? int(a.J - base) : int(range);
     if (tid < cnt) {
         const uint32_t d = a.perm ? a.perm[base + tid] : uint32_t(base + tid);
         s_d[tid] = d;
@@ -1325,7 +1325,7 @@ __device__ __forceinline__ int tile_row_off(int p) {  // pack_index(8p, 8p)
 }
 
 template <int NB, int MODE>
-__global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a) {
+__global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a, uint32_t range) {
     constexpr int R = 8 * NB;
     constexpr uint32_t P = uint32_t(R) * (R + 1) / 2;
     static_assert(8 * R <= SB_CHD, "tile-row larger than a ring stage");
@@ -1340,8 +1340,8 @@ __global__ void __launch_bounds__(CB) k_eval_stream(EvalArgs a) {
     __shared__ uint32_t s_cnt[2], s_base[2], s_gs, s_ge;
     __shared__ __align__(8) uint64_t bar[SB_STAGES];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t base = uint64_t(blockIdx.x) * CB;
-    const int cnt = a.J - base < uint64_t(CB) ? int(a.J - base) : CB;
+    const uint64_t base = uint64_t(blockIdx.x) * range;  // range <= CB positions per CTA
+    const int cnt = a.J - base < uint64_t(range) ? int(a.J - base) : int(range);
     if (tid < cnt) {
         const uint32_t d = a.perm ? a.perm[base + tid] : uint32_t(base + tid);
         s_d[tid] = d;
@@ -2645,10 +2645,22 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// positions per CTA (a multiple of 8, at most maxpos) such that the level's CTAs fill whole
+// waves of `ctas` resident CTAs: the last wave of a fixed-size tiling is otherwise part empty
+// (J = 65536 in 128-position CTAs on 296 slots: 1.73 waves)
+inline uint64_t wave_range(uint64_t J, uint64_t ctas, uint64_t maxpos) {
+    const uint64_t waves = (J + ctas * maxpos - 1) / (ctas * maxpos);
+    const uint64_t range = (J + ctas * waves - 1) / (ctas * waves);
+    return std::min<uint64_t>(std::max<uint64_t>((range + 7) / 8 * 8, 8), maxpos);
+}
+
 template <int NB, int MODE, bool ROOT0>
-void launch_cta(const EvalArgs& a, unsigned grid, cudaStream_t s) {
+void launch_cta(const EvalArgs& a, unsigned, cudaStream_t s) {
     constexpr size_t smem = cta_nbuf<NB, ROOT0>() * sizeof(double) * (8 * NB) * (8 * NB + 1) / 2;
     smem_optin(k_eval_cta<NB, MODE, ROOT0>, smem);
+    const uint32_t range = uint32_t(wave_range(
+        a.J, uint64_t(sm_count_current()) * occupancy(k_eval_cta<NB, MODE, ROOT0>, CB, smem), CB));
+    const unsigned grid = unsigned((a.J + range - 1) / range);
     // launched with programmatic stream serialization: overlaps the previous
     // kernel's tail (k_eval_cta waits on griddepcontrol before reading its inputs)
     cudaLaunchConfig_t cfg{};
@@ -2661,14 +2673,17 @@ void launch_cta(const EvalArgs& a, unsigned grid, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_eval_cta<NB, MODE, ROOT0>, a);
+    cudaLaunchKernelEx(&cfg, k_eval_cta<NB, MODE, ROOT0>, a, range);
 }
 
 template <int NB, int MODE>
-void launch_stream_mode(const EvalArgs& a, unsigned grid, cudaStream_t s) {
+void launch_stream_mode(const EvalArgs& a, unsigned, cudaStream_t s) {
     constexpr size_t smem = size_t(SB_STAGES) * SB_CHD * sizeof(double);
     smem_optin(k_eval_stream<NB, MODE>, smem);
-    k_eval_stream<NB, MODE><<<grid, CB, smem, s>>>(a);
+    const uint32_t range =
+        uint32_t(wave_range(a.J, uint64_t(sm_count_current()) * occupancy(k_eval_stream<NB, MODE>, CB, smem), CB));
+    const unsigned grid = unsigned((a.J + range - 1) / range);
+    k_eval_stream<NB, MODE><<<grid, CB, smem, s>>>(a, range);
 }
 
 // R > 160: streamed-Gram kernel; no root-fused level 0 (the host runs EV_ROOT first)
@@ -2757,9 +2772,7 @@ void launch_split(const EvalArgs& a, cudaStream_t s) {
     // CTAs of 64 = 3.46 waves, the last one half empty)
     const uint64_t ctas = uint64_t(sm_count_current()) *
                           occupancy(k_eval_split<NB, MODE, ROOT0, WGT>, SPW * 32, SplitCfg<NB>::SMEM);
-    const uint64_t waves = (a.J + ctas * SPR - 1) / (ctas * SPR);
-    uint64_t range = (a.J + ctas * waves - 1) / (ctas * waves);
-    range = std::min<uint64_t>(std::max<uint64_t>((range + 7) / 8 * 8, 8), SPR);
+    const uint64_t range = wave_range(a.J, ctas, SPR);
     const unsigned grid = unsigned((a.J + range - 1) / range);
     launch_pdl(k_eval_split<NB, MODE, ROOT0, WGT>, dim3(grid), dim3(SPW * 32), SplitCfg<NB>::SMEM, s, a,
                uint32_t(range));
