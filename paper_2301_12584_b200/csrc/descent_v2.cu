@@ -2845,10 +2845,16 @@ void dispatch_eval(uint32_t R, int mode, const EvalArgs& a, cudaStream_t s, cons
     }
 }
 
-// draws per warp in the fused deep kernel (Tuning::deep_chunk): fewer than 32 gives more,
-// shorter warp work units (the kernel holds ~12 warps per SM, so 32-draw units leave a
-// ragged tail wave)
-inline uint32_t deep_chunk(const Tuning& t) { return uint32_t(t.deep_chunk >= 1 && t.deep_chunk <= 32 ? t.deep_chunk : 8); }
+// draws per warp work unit of the fused deep kernel (Tuning::deep_chunk; 0 = by J): larger
+// units share a node's Gram among more draws and fill the 8-draw DMMA blocks better, but the
+// kernel holds ~12 warps per SM, so the units must stay numerous enough to balance: about four
+// per resident warp (J = 65536: 8 draws, measured best against 4 / 6 / 12 / 16; J = 2^20 at
+// R = 32: 32 draws, 21.2 ms per config-3 call against 23.9 ms with 8)
+inline uint32_t deep_chunk(const Tuning& t, uint64_t J) {
+    if (t.deep_chunk >= 1 && t.deep_chunk <= 32) return uint32_t(t.deep_chunk);
+    const uint64_t per = J / (4ull * 12ull * uint64_t(sm_count_current()));
+    return uint32_t(std::min<uint64_t>(std::max<uint64_t>(per / 8 * 8, 8), 32));
+}
 
 // shallow levels (many draws per node) -> level kernels with global regrouping; deep -> fused pass
 inline bool deep_level(const Tuning& t, uint64_t J, uint32_t level) {
@@ -3182,7 +3188,7 @@ int launch_position_grouped(const GroupedArgs& g) {
         da.U = g.U;
         da.tree = g.Z;
         da.topo = tz;
-        da.chunk = deep_chunk(g.tune);
+        da.chunk = deep_chunk(g.tune, J);
         da.work = deep_work;
         da.dmma_min = g.tune.deep_dmma_min;
         da.leaf_par = g.tune.leaf_par;

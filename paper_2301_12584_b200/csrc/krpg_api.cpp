@@ -2155,7 +2155,7 @@ int krpg_set_option(krpg_t h, int option, int64_t value) {
             require(value >= 1 && value <= (int64_t(1) << 30), "krpg_set_option: deep threshold out of range");
             h->tune.deep_threshold = int(value);
         } else if (option == KRPG_OPT_DEEP_CHUNK) {
-            require(value >= 1 && value <= 32, "krpg_set_option: deep chunk must be in [1, 32]");
+            require(value >= 0 && value <= 32, "krpg_set_option: deep chunk must be in [0, 32]");
             h->tune.deep_chunk = int(value);
         } else if (option == KRPG_OPT_EVAL_SPLIT) {
             require(value == 0 || value == 1 || value == 16, "krpg_set_option: eval split must be 0, 1 or 16");

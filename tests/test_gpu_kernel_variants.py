@@ -49,7 +49,7 @@ def test_level_kernel_and_tables_bit_identical(shapes, J):
     base = draws(s, len(shapes), J)
     for opts in ({"eval_reg": 1, "pos0_tables": 0}, {"eval_reg": 0, "pos0_tables": 1},
                  {"eval_reg": 1, "pos0_tables": 1}, {"deep_threshold": 64}, {"deep_threshold": 16},
-                 {"deep_chunk": 32}, {"deep_chunk": 3},
+                 {"deep_chunk": 32}, {"deep_chunk": 3}, {"deep_chunk": 0},
                  # one launch per level instead of the multi-level cooperative launch, and back
                  {"eval_ml": 0}, {"eval_ml": 0, "pos0_tables": 0}, {"eval_ml": 1}, {"pos0_tables": 1}):
         s.set_tuning(**opts)
@@ -82,7 +82,7 @@ def test_tuning_option_errors():
     from paper_2301_12584_b200 import KrpgInvalidArgument, KrpSampler
     s = KrpSampler(pareto_factors([(300, 8), (200, 8)], seed=1))
     with pytest.raises(KrpgInvalidArgument):
-        s.set_tuning(deep_chunk=0)
+        s.set_tuning(deep_chunk=33)
     with pytest.raises(KrpgInvalidArgument):
         s.set_tuning(eval_split=2)
     with pytest.raises(KrpgInvalidArgument):
