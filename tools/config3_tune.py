@@ -18,8 +18,8 @@ prob = torch.empty(J, dtype=torch.float64, device="cuda")
 rows = torch.empty(J, R, dtype=torch.float64, device="cuda")
 stream = torch.cuda.ExternalStream(s.stream(), device="cuda")
 base = None
-for opts in ({}, {"deep_chunk": 8}, {"deep_chunk": 16}, {"deep_chunk": 32}, {"deep_chunk": 0, "deep_threshold": 16},
-             {"deep_threshold": 8}, {"deep_threshold": 64}, {"deep_threshold": 32}):
+for opts in ({}, {"deep_chunk": 0},
+             {"deep_threshold": 16}, {"deep_threshold": 32}):
     s.set_tuning(**opts)
     ts = []
     for i in range(4):
