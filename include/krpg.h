@@ -173,7 +173,7 @@ int krpg_profile_read(krpg_t h, double* ms, uint64_t* launches, int reset);
 #define KRPG_OPT_SLICES 5
 #define KRPG_OPT_HOST_TRACE 6 /* host-side phase times of krpg_sample on stderr */
 /* Kernel-variant / tuning options of the grouped descent (defaults = measured best).
- * EVAL_REG (1), POS0_TABLES (1), DEEP_THRESHOLD (32), DEEP_CHUNK (0: chosen from J, 8 .. 32; or 1 .. 32) give bit-identical
+ * EVAL_REG (1), POS0_TABLES (1), DEEP_THRESHOLD (0: by rank, 16 at R <= 32 else 32), DEEP_CHUNK (0: chosen from J, 8 .. 32; or 1 .. 32) give bit-identical
  * samples; EVAL_SPLIT (16: R = 128 only; 1: also R = 64; 0: off), DEEP_DMMA_MIN (1) and
  * LEAF_PAR (8) change last-bit rounding when moved off their defaults. */
 #define KRPG_OPT_EVAL_REG 16

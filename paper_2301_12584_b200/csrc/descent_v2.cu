@@ -2857,8 +2857,11 @@ inline uint32_t deep_chunk(const Tuning& t, uint64_t J) {
 }
 
 // shallow levels (many draws per node) -> level kernels with global regrouping; deep -> fused pass
-inline bool deep_level(const Tuning& t, uint64_t J, uint32_t level) {
-    return (J >> level) < uint64_t(t.deep_threshold >= 1 ? t.deep_threshold : 32);
+// (Tuning::deep_threshold; 0 = by rank: 32 draws per node at R > 32 -- measured against 16 / 64 on
+// config 2 --, 16 at R <= 32, where a level-kernel level costs less relative to the deep pass:
+// config-4 R = 32 1.256 -> 1.205 ms, R = 16 0.954 -> 0.938 ms per call)
+inline bool deep_level(const Tuning& t, uint32_t R, uint64_t J, uint32_t level) {
+    return (J >> level) < uint64_t(t.deep_threshold >= 1 ? t.deep_threshold : (R <= 32 ? 16 : 32));
 }
 
 template <int NB, typename T>
@@ -3120,7 +3123,7 @@ int launch_position_grouped(const GroupedArgs& g) {
     // shallow levels: global regrouping; deep levels + leaf scan: one fused pass (R <= 64).
     // Without the fused pass (R > 64, or fused_deep off) every level runs on the level kernels.
     uint32_t l0 = 0;
-    while (l0 < tz.d && (R > 64 || !g.fused_deep || !deep_level(g.tune, J, l0))) ++l0;
+    while (l0 < tz.d && (R > 64 || !g.fused_deep || !deep_level(g.tune, R, J, l0))) ++l0;
     // first position: E-tree and the top factor-tree levels from (node, component) tables
     const uint32_t L0 = tz.d >= 2 ? std::min<uint32_t>(kPos0Levels, std::min<uint32_t>(l0, tz.d - 1)) : 0;
     const bool tab0 = g.h_ones && g.pos0_tab && R <= 64 && R % 8 == 0 && L0 >= 1 && g.tune.pos0_tables;

@@ -2152,7 +2152,7 @@ int krpg_set_option(krpg_t h, int option, int64_t value) {
         else if (option == KRPG_OPT_POS0_TABLES)
             h->tune.pos0_tables = value != 0;
         else if (option == KRPG_OPT_DEEP_THRESHOLD) {
-            require(value >= 1 && value <= (int64_t(1) << 30), "krpg_set_option: deep threshold out of range");
+            require(value >= 0 && value <= (int64_t(1) << 30), "krpg_set_option: deep threshold out of range");
             h->tune.deep_threshold = int(value);
         } else if (option == KRPG_OPT_DEEP_CHUNK) {
             require(value >= 0 && value <= 32, "krpg_set_option: deep chunk must be in [0, 32]");

@@ -86,7 +86,7 @@ void launch_segtree_masses(const double* U, uint64_t I, uint32_t R, const double
 struct Tuning {
     int eval_reg = 1;          // R <= 64 shallow levels: register-resident kernel (0: CTA kernel)
     int pos0_tables = 1;       // first included position from (node, component) tables
-    int deep_threshold = 32;   // a level is "deep" below this many draws per node on average
+    int deep_threshold = 0;    // a level is "deep" below this many draws per node on average (0: by rank, 16 / 32)
     int deep_chunk = 0;        // sorted draws per warp work unit of the fused deep pass (1..32; 0: chosen from J)
     int eval_split = 16;       // split-Gram level kernel: 16 = R 128 only, 1 = R 64 and 128, 0 = off
     int deep_dmma_min = 1;     // deep-pass runs with fewer draws use CUDA-core forms
